@@ -1,0 +1,281 @@
+"""Generate the golden fixtures under tests/golden/ FROM THE REFERENCE ITSELF.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the reference ``linkatlas`` package from
+``/root/reference/pkg/src`` (read-only) and records its outputs on seeded
+inputs.  The GPU box never runs this script; it only reads the committed
+``.npz`` files.  Library versions are stored inside every fixture.
+"""
+
+from __future__ import annotations
+
+import platform
+import sys
+from pathlib import Path
+
+import numpy as np
+import scipy
+
+REF_SRC = "/root/reference/pkg/src"
+sys.path.insert(0, REF_SRC)
+
+from linkatlas import atlas as ref_atlas  # noqa: E402
+from linkatlas import curves as ref_curves  # noqa: E402
+from linkatlas import generator as ref_gen  # noqa: E402
+from linkatlas import solver as ref_solver  # noqa: E402
+from linkatlas.mechanism import JointType, Mechanism  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+NMAX = 20
+SMAX = 18
+
+
+def versions():
+    return np.array(
+        f"python={platform.python_version()} numpy={np.__version__} scipy={scipy.__version__}"
+    )
+
+
+def four_bar(ground=(0.7, 0.5), coupler=(0.6, 0.62)) -> Mechanism:
+    # same topology as the reference's tests/conftest.py:7-18 fixture
+    adj = np.zeros((4, 4), dtype=np.uint8)
+    for i, j in [(0, 1), (1, 3), (2, 3)]:
+        adj[i, j] = adj[j, i] = 1
+    types = np.array([0, 2, 0, 1], dtype=np.int8)
+    pos = np.array([(0.5, 0.5), (0.55, 0.5), ground, coupler])
+    return Mechanism(adj, types, pos)
+
+
+def outcome_arrays(outs, T):
+    ft = np.array([o.step if isinstance(o, ref_solver.Locking) else T for o in outs], dtype=np.int64)
+    fj = np.array([o.joint if isinstance(o, ref_solver.Locking) else -1 for o in outs], dtype=np.int64)
+    return ft, fj
+
+
+def pack_topology(mech, plan):
+    adj = np.zeros((NMAX, NMAX), dtype=np.uint8)
+    adj[: mech.n, : mech.n] = mech.adjacency
+    types = np.full(NMAX, -1, dtype=np.int8)
+    types[: mech.n] = mech.types
+    steps = np.full((SMAX, 3), -1, dtype=np.int16)
+    for s, st in enumerate(plan.steps):
+        steps[s] = (st.target, st.a, st.b)
+    return adj, types, steps
+
+
+def solver_fixture():
+    d = {"versions": versions()}
+    # --- C1-style four-bars
+    mech = four_bar()
+    plan = ref_solver.compile_plan(mech)
+    rng = np.random.default_rng(0)
+    pos = rng.uniform(size=(256, 4, 2))
+    pos[:, 0] = (0.5, 0.5)
+    pos[:, 1] = (0.55, 0.5)
+    outs = ref_solver.simulate_batch(pos, plan, 200)
+    ft, fj = outcome_arrays(outs, 200)
+    d["fb_pos0"] = pos
+    d["fb_first_t"] = ft
+    d["fb_first_joint"] = fj
+    valid = np.flatnonzero(ft == 200)[:12]
+    d["fb_traj_idx"] = valid
+    d["fb_traj"] = np.stack([outs[i].positions for i in valid])
+    outs50 = ref_solver.simulate_batch(pos, plan, 50)
+    d["fb_first_t50"], d["fb_first_joint50"] = outcome_arrays(outs50, 50)
+    # --- known answers of the reference tests (test_solver.py:78-126)
+    lock_mech = four_bar(ground=(0.9, 0.5), coupler=(0.72, 0.51))
+    lp = ref_solver.compile_plan(lock_mech)
+    o200 = ref_solver.simulate(lock_mech, lp, 200)
+    o50 = ref_solver.simulate(lock_mech, lp, 50)
+    d["ka_lock_pos0"] = lock_mech.positions0
+    d["ka_lock"] = np.array([o200.step, o200.joint, o50.step, o50.joint])
+    okm = four_bar()
+    ok = ref_solver.simulate(okm, ref_solver.compile_plan(okm), 200)
+    d["ka_valid_traj"] = ok.positions
+    d["ka_dyad"] = np.array(ref_solver.dyad_solve((0.0, 0.0), (1.0, 0.0), 1.0, 1.0, 1.0))
+
+    # --- mixed topologies from the reference generator (generator.py:200-238)
+    adjs, typs, stps, ns, nsteps = [], [], [], [], []
+    c_pos, c_topo, c_ft, c_fj, c_ft50, c_fj50 = [], [], [], [], [], []
+    tr_idx, tr = [], []
+    g = 0
+    for n in [5, 6, 7, 8, 10, 12, 14, 16, 18, 20]:
+        for rep in range(3):
+            trng = np.random.default_rng([7, n, rep, 0])
+            prng = np.random.default_rng([7, n, rep, 1])
+            mech, plan = ref_gen.sample_topology(trng, n)
+            a, t, s = pack_topology(mech, plan)
+            adjs.append(a); typs.append(t); stps.append(s); ns.append(n); nsteps.append(len(plan.steps))
+            cand = ref_gen._sample_positions_batch(n, 64, prng)
+            outs = ref_solver.simulate_batch(cand, plan, 200)
+            ft, fj = outcome_arrays(outs, 200)
+            outs50 = ref_solver.simulate_batch(cand, plan, 50)
+            ft50, fj50 = outcome_arrays(outs50, 50)
+            padded = np.full((64, NMAX, 2), np.nan)
+            padded[:, :n] = cand
+            base = len(c_topo) * 1
+            c_pos.append(padded); c_topo.append(np.full(64, g, dtype=np.int32))
+            c_ft.append(ft); c_fj.append(fj); c_ft50.append(ft50); c_fj50.append(fj50)
+            for i in np.flatnonzero(ft == 200)[:2]:
+                tp = np.full((NMAX, 200, 2), np.nan)
+                tp[:n] = outs[i].positions
+                tr_idx.append(g * 64 + i)
+                tr.append(tp)
+            g += 1
+    d["mx_adj"] = np.stack(adjs)
+    d["mx_types"] = np.stack(typs)
+    d["mx_steps"] = np.stack(stps)
+    d["mx_n"] = np.array(ns, dtype=np.int32)
+    d["mx_nsteps"] = np.array(nsteps, dtype=np.int32)
+    d["mx_pos0"] = np.concatenate(c_pos)
+    d["mx_topo"] = np.concatenate(c_topo)
+    d["mx_first_t"] = np.concatenate(c_ft)
+    d["mx_first_joint"] = np.concatenate(c_fj)
+    d["mx_first_t50"] = np.concatenate(c_ft50)
+    d["mx_first_joint50"] = np.concatenate(c_fj50)
+    d["mx_traj_idx"] = np.array(tr_idx, dtype=np.int64)
+    d["mx_traj"] = np.stack(tr)
+
+    # --- find_valid_variant (generator.py:241-283): attempts + accepted pose
+    fv_topo, fv_att, fv_pos, fv_seed = [], [], [], []
+    for n, seed in [(6, 11), (8, 12), (8, 13), (10, 14), (12, 15)]:
+        mech, plan = ref_gen.sample_topology(np.random.default_rng([seed, 0]), n)
+        res = ref_gen.find_valid_variant(mech, plan, np.random.default_rng([seed, 1]))
+        a, t, s = pack_topology(mech, plan)
+        fv_topo.append((a, t, s, n))
+        fv_att.append(res.attempts)
+        p = np.full((NMAX, 2), np.nan)
+        p[:n] = res.mechanism.positions0
+        fv_pos.append(p)
+        fv_seed.append(seed)
+    d["fv_adj"] = np.stack([x[0] for x in fv_topo])
+    d["fv_types"] = np.stack([x[1] for x in fv_topo])
+    d["fv_steps"] = np.stack([x[2] for x in fv_topo])
+    d["fv_n"] = np.array([x[3] for x in fv_topo], dtype=np.int32)
+    d["fv_seed"] = np.array(fv_seed, dtype=np.int64)
+    d["fv_attempts"] = np.array(fv_att, dtype=np.int64)
+    d["fv_pos"] = np.stack(fv_pos)
+    np.savez_compressed(OUT / "solver_golden.npz", **d)
+    return d
+
+
+def fourier_curves(seed: int, count: int, P: int) -> np.ndarray:
+    """Random closed Fourier curves, 5 harmonics, coefficients N(0, 1/k^2)
+    (BASELINE.json configs[3])."""
+    rng = np.random.default_rng(seed)
+    t = 2.0 * np.pi * np.arange(P) / P
+    k = np.arange(1, 6)
+    coef = rng.normal(size=(count, 4, 5)) / k
+    cos_kt = np.cos(np.outer(t, k))  # (P, 5)
+    sin_kt = np.sin(np.outer(t, k))
+    x = coef[:, 0] @ cos_kt.T + coef[:, 1] @ sin_kt.T
+    y = coef[:, 2] @ cos_kt.T + coef[:, 3] @ sin_kt.T
+    return np.stack([x, y], axis=-1)
+
+
+def curves_fixture(sol):
+    d = {"versions": versions()}
+    paths = []
+    kinds = []
+    # moving-joint curves of valid mixed mechanisms (cli.py:131-134 pattern)
+    for tp, gi in zip(sol["mx_traj"], sol["mx_traj_idx"]):
+        topo = sol["mx_topo"][gi]
+        n = int(sol["mx_n"][topo])
+        types = sol["mx_types"][topo]
+        for j in range(n):
+            if types[j] == 0:
+                continue
+            paths.append(tp[j]); kinds.append(0)
+            if len(paths) >= 48:
+                break
+        if len(paths) >= 48:
+            break
+    for p in fourier_curves(5, 24, 200):
+        paths.append(p); kinds.append(1)
+    # reference-test style noisy lemniscates (test_curves.py:12-16)
+    rng = np.random.default_rng(9)
+    t = np.linspace(0, 2 * np.pi, 200, endpoint=False)
+    for _ in range(8):
+        p = np.stack([np.cos(t), np.sin(2 * t) * 0.4], axis=1) + rng.normal(scale=0.05, size=(200, 2))
+        paths.append(p); kinds.append(2)
+    # circle (is_circle true), and a scaled/shifted circle
+    paths.append(np.stack([np.cos(t), np.sin(t)], axis=1) * 3.0 + 7.0); kinds.append(3)
+    paths = np.stack(paths)
+    outs, pairs, circ, circv, normd = [], [], [], [], []
+    for p in paths:
+        o = ref_curves.normalize(p)
+        i, j, dd = ref_curves._farthest_pair(p)
+        outs.append(o); pairs.append((i, j)); circ.append(ref_curves.is_circle(o))
+        circv.append(float(np.var(np.hypot(o[:, 0] - 0.5, o[:, 1] - 0.5))))
+        normd.append(ref_curves.is_normalized(o))
+    d["paths"] = paths
+    d["kinds"] = np.array(kinds, dtype=np.int8)
+    d["normalized"] = np.stack(outs)
+    d["pairs"] = np.array(pairs, dtype=np.int64)
+    d["is_circle"] = np.array(circ)
+    d["circle_var"] = np.array(circv)
+    d["is_normalized"] = np.array(normd)
+    d["is_normalized_raw"] = np.array([ref_curves.is_normalized(p) for p in paths])
+    # the order-preservation example of SURVEY.md §8a a-7
+    d["two_point"] = ref_curves.normalize(np.array([[2.0, 2.0], [4.0, 2.0]]))
+    # chamfer pairs (curves.py:123-129) incl. known answer {(0,0)} vs {(1,0)}
+    A = d["normalized"][:16]
+    Bm = d["normalized"][16:32]
+    d["chamfer_AB"] = np.array([[ref_curves.chamfer(a, b) for b in Bm] for a in A])
+    d["chamfer_ka"] = np.array(ref_curves.chamfer(np.array([[0.0, 0.0]]), np.array([[1.0, 0.0]])))
+    d["resample_64"] = np.stack([ref_curves.resample(p, 64) for p in paths[:4]])
+    np.savez_compressed(OUT / "curves_golden.npz", **d)
+
+
+def atlas_fixture():
+    d = {"versions": versions()}
+    N, P = 400, 64
+    raw = fourier_curves(21, N, P)
+    pts = np.stack([ref_curves.normalize(p) for p in raw])
+    mech = four_bar()
+    from linkatlas.records import CurveRecord
+
+    recs = [CurveRecord(mech_id=i, joint_id=3, is_arc=False, is_circle=False, points=p.tolist())
+            for i, p in enumerate(pts)]
+    mechs = {i: mech for i in range(N)}
+    atlas = ref_atlas.Atlas.build(recs, mechs, seed=3)
+    assert np.array_equal(atlas.points, pts)
+    d["points"] = pts
+    d["order"] = atlas.order
+    d["seed"] = np.array(3)
+    queries = [
+        pts[17].copy(),                                   # exact member -> self hit
+        ref_curves.normalize(fourier_curves(99, 1, P)[0]),  # fresh curve
+        ref_curves.normalize(fourier_curves(98, 1, P)[0]),
+        ref_curves.normalize(np.array([[0.0, 0.0], [1.0, 1.0], [2.0, 0.0]])),  # far shape, Q=3
+    ]
+    cases = [(3, 0.03), (10, 1e-6), (5, 0.2), (3, np.inf)]
+    rows = []
+    for qi, q in enumerate(queries):
+        for ci, (k, thr) in enumerate(cases):
+            hits = atlas.retrieve(q, k=k, threshold=thr)
+            for r, h in enumerate(hits):
+                rows.append((qi, ci, r, h.mech_id, h.distance, float(h.above_threshold)))
+    d["cases_k"] = np.array([c[0] for c in cases])
+    d["cases_thr"] = np.array([c[1] for c in cases])
+    d["hits"] = np.array(rows)
+    for qi, q in enumerate(queries):
+        d[f"query{qi}"] = q
+        d[f"chamfer_cdist{qi}"] = np.array([ref_curves.chamfer(q, p) for p in pts])
+        d[f"chamfer_block{qi}"] = ref_atlas._chamfer_block(pts, q)
+    # brute-force ordering (test_atlas.py:106-118) for the fresh query
+    full = atlas.retrieve(queries[1], k=N, threshold=np.inf)
+    d["brute_ids"] = np.array([h.mech_id for h in full])
+    d["brute_d"] = np.array([h.distance for h in full])
+    np.savez_compressed(OUT / "atlas_golden.npz", **d)
+
+
+if __name__ == "__main__":
+    sol = solver_fixture()
+    curves_fixture(sol)
+    atlas_fixture()
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)
