@@ -1,0 +1,579 @@
+"""Benchmark of the B200-native LINKS hot path (driver contract: ONE JSON line).
+
+Headline (BASELINE.json metric / configs[1]): mechanism simulations per second
+for 100,000 seeded 6-8-joint candidates per GPU (reference generator streams),
+200 crank angles, all joint paths of the valid ones + lock flags of all
+(``simulate_compact``: screen -> ordered compaction -> f64 path replay).
+Secondary lines inside the same JSON object: the validity screen at scale
+(configs[2]) and chamfer curve-pairs/sec (configs[3], 1 query x 10M curves).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU: one process per GPU (torchrun); weak scaling (each rank its own
+100k batch / 10M-curve shard); per-step device time is the max over ranks;
+the chamfer step includes the NCCL all-gather top-k merge.
+``--impl reference`` times the CPU oracle port of the reference
+(``oracle/``; the reference is pure Python and is not present on the GPU
+box) on all host cores, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "mechanism simulations/sec (200 steps, ≤20 joints)"
+CHAMFER_METRIC = "chamfer curve-pairs/sec"
+SCREEN_METRIC = "validity-screened candidates/sec"
+T = 200
+C2_COUNT = 100_000
+C3_COUNT = 10_000_000
+C4_COUNT = 10_000_000
+C4_P = 200
+DYAD_FLOPS = 21          # FP32 flops per dyad solve
+PAIR_FLOPS = 200_000     # 40,000 point pairs x 5 flops
+L2_FLUSH_BYTES = 512 << 20
+
+
+# ----------------------------------------------------------------- helpers
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            if self.t is not None:
+                self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+class Timer:
+    """CUDA-event timing of a sequence of launches on one stream."""
+
+    def __init__(self, torch, stream):
+        self.torch = torch
+        self.stream = stream
+        self.marks = []
+
+    def mark(self, name):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        self.marks.append((name, e))
+
+    def spans(self):
+        self.stream.synchronize()
+        out = {}
+        for (n0, e0), (n1, e1) in zip(self.marks, self.marks[1:]):
+            out[n1] = e0.elapsed_time(e1)
+        out["total"] = self.marks[0][1].elapsed_time(self.marks[-1][1])
+        return out
+
+
+def max_over_ranks(torch, value: float, world: int) -> float:
+    if world <= 1:
+        return value
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(torch, world):
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------- C2
+def c2_inputs(rank: int):
+    from paper_2208_14567_b200.workloads import mixed_batch
+
+    return mixed_batch(C2_COUNT, 6, 8, seed=2208 + rank, stride=8)
+
+
+def bench_c2(torch, args, rank, world, peaks, flush):
+    from paper_2208_14567_b200.solver import simulate_compact, simulate_tensors
+
+    mb = c2_inputs(rank)
+    table = mb.table()
+    stream = torch.cuda.current_stream()
+    pos = torch.from_numpy(mb.pos).cuda()
+    topo = torch.from_numpy(mb.topo).cuda()
+    stride = table.max_n
+    traj = torch.empty((mb.B * stride, T, 2), dtype=torch.float32, device="cuda")
+
+    def step(timer=None):
+        if timer:
+            timer.mark("start")
+        res = simulate_tensors(pos, table, T, topo, write_traj=False)
+        if timer:
+            timer.mark("screen")
+        from paper_2208_14567_b200.solver import compact_valid
+
+        idx, cnt = compact_valid(res["first_t"], T)
+        if timer:
+            timer.mark("compact")
+        simulate_tensors(pos, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, cand=idx,
+                         cand_count=cnt, coarse=False)
+        if timer:
+            timer.mark("paths")
+        return res, idx, cnt
+
+    for _ in range(args.warmup):
+        step()
+    # dyad counters + valid count from one instrumented (untimed) pass
+    cnt_buf = torch.zeros(4, dtype=torch.int64, device="cuda")
+    r0 = simulate_tensors(pos, table, T, topo, write_traj=False, counters=cnt_buf)
+    valid = int((r0["first_t"] == T).sum().item())
+    screen_dyads = int(cnt_buf[2].item())
+    cnt_p = torch.zeros(4, dtype=torch.int64, device="cuda")
+    from paper_2208_14567_b200.solver import compact_valid
+
+    idx0, c0 = compact_valid(r0["first_t"], T)
+    simulate_tensors(pos, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, cand=idx0,
+                     cand_count=c0, coarse=False, counters=cnt_p)
+    path_dyads = int(cnt_p[2].item())
+    n_valid_rows = int(mb.n[(r0["first_t"] == T).cpu().numpy()].sum())
+
+    spans = []
+    barrier(torch, world)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            flush()
+            tm = Timer(torch, stream)
+            step(tm)
+            spans.append(tm.spans())
+    barrier(torch, world)
+    ms = statistics.mean(s["total"] for s in spans)
+    ms = max_over_ranks(torch, ms, world)
+    k_screen = statistics.mean(s["screen"] for s in spans)
+    k_paths = statistics.mean(s["paths"] for s in spans)
+    k_compact = statistics.mean(s["compact"] for s in spans)
+    value = world * mb.B / (ms / 1e3)
+
+    # roofline per kernel
+    sm_clock = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12  # TFLOP/s nominal at max clock
+    path_bytes = n_valid_rows * T * 8 + valid * stride * 16 + valid * 8 * 2
+    screen_flops = DYAD_FLOPS * screen_dyads
+    rl_paths = {"kernel": "sim_kernel<WRITE> (f64 path replay)", "bound": "hbm",
+                "achieved": path_bytes / (k_paths / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "algorithmic_bytes": path_bytes, "ms": k_paths, "traffic": None}
+    rl_paths["frac"] = rl_paths["achieved"] / rl_paths["peak"]
+    rl_screen = {"kernel": "sim_kernel<SCREEN> (fp32 + f64 fix-up)", "bound": "fp32",
+                 "achieved": screen_flops / (k_screen / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+                 "algorithmic_flops": screen_flops, "dyads": screen_dyads, "ms": k_screen, "traffic": None}
+    rl_screen["frac"] = rl_screen["achieved"] / rl_screen["peak"]
+    dominant = rl_paths if k_paths >= k_screen else rl_screen
+    return {
+        "value": value, "ms": ms, "valid": valid, "B": mb.B, "kernels_ms": {
+            "screen": k_screen, "compact": k_compact, "paths": k_paths},
+        "roofline": dominant, "roofline_kernels": [rl_screen, rl_paths], "clocks": clk.summary(),
+        "launches_per_step": 5, "path_dyads": path_dyads, "mb": mb, "table": table,
+    }
+
+
+def e2e_c2(torch, args, mb, table, world):
+    """Same pipeline through the public API with pinned host buffers: H2D of
+    the poses + plan indices, the three kernels, D2H of the flags, the valid
+    count and the valid candidates' paths."""
+    from paper_2208_14567_b200.solver import simulate_compact
+
+    pos_h = torch.from_numpy(mb.pos).pin_memory()
+    topo_h = torch.from_numpy(mb.topo).pin_memory()
+    stride = table.max_n
+    table.tensor()
+    traj = torch.empty((mb.B * stride, T, 2), dtype=torch.float32, device="cuda")
+    out_traj = torch.empty((mb.B * stride, T, 2), dtype=torch.float32).pin_memory()
+    ft_h = torch.empty(mb.B, dtype=torch.int32).pin_memory()
+    fj_h = torch.empty(mb.B, dtype=torch.int32).pin_memory()
+    cnt_h = torch.empty(1, dtype=torch.int64).pin_memory()
+    stream = torch.cuda.current_stream()
+    stats = {}
+
+    def step():
+        pos = pos_h.cuda(non_blocking=True)
+        topo = topo_h.cuda(non_blocking=True)
+        res = simulate_compact(pos, table, T, topo, traj=traj)
+        ft_h.copy_(res["first_t"], non_blocking=True)
+        fj_h.copy_(res["first_joint"], non_blocking=True)
+        cnt_h.copy_(res["valid_count"], non_blocking=True)
+        stream.synchronize()
+        n = int(cnt_h.item()) * stride
+        out_traj[:n].copy_(traj[:n], non_blocking=True)
+        stats["h2d"] = pos_h.numel() * 8 + topo_h.numel() * 4 + table.G * 64
+        stats["d2h"] = mb.B * 8 + 8 + n * T * 8
+        return res
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    barrier(torch, world)
+    times = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    barrier(torch, world)
+    ms = max_over_ranks(torch, statistics.mean(times), world)
+    return {"value": world * mb.B / (ms / 1e3), "unit": "simulations/s", "h2d_bytes_per_step": stats["h2d"],
+            "d2h_bytes_per_step": stats["d2h"], "ms_per_step": ms}
+
+
+# ----------------------------------------------------------------- C3
+def bench_c3(torch, args, rank, world, peaks, flush):
+    from paper_2208_14567_b200.solver import PlanTable, compact_valid, simulate_tensors
+    from paper_2208_14567_b200.workloads import device_poses, topology_pool
+
+    G = 1024
+    mechs, plans = topology_pool(G, 5, 20, seed=3000)
+    table = PlanTable(plans)
+    groups = (C3_COUNT + 255) // 256
+    topo = (torch.arange(C3_COUNT, device="cuda") // 256 % G).to(torch.int32)
+    pos = device_poses(topo, plans, 20, seed=77 + rank)
+    stream = torch.cuda.current_stream()
+
+    def step(timer=None, counters=None):
+        if timer:
+            timer.mark("start")
+        res = simulate_tensors(pos, table, T, topo, write_traj=False, counters=counters)
+        if timer:
+            timer.mark("screen")
+        idx, cnt = compact_valid(res["first_t"], T)
+        if timer:
+            timer.mark("compact")
+        return res, cnt
+
+    for _ in range(args.warmup):
+        step()
+    cbuf = torch.zeros(4, dtype=torch.int64, device="cuda")
+    res, cnt = step(counters=cbuf)
+    c = cbuf.cpu().numpy()
+    valid = int(cnt.item())
+    spans = []
+    barrier(torch, world)
+    for _ in range(args.steps):
+        flush()
+        tm = Timer(torch, stream)
+        step(tm)
+        spans.append(tm.spans())
+    barrier(torch, world)
+    ms = max_over_ranks(torch, statistics.mean(s["total"] for s in spans), world)
+    k = statistics.mean(s["screen"] for s in spans)
+    sm_clock = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12
+    flops = DYAD_FLOPS * int(c[2])
+    rl = {"kernel": "sim_kernel<SCREEN>", "bound": "fp32", "achieved": flops / (k / 1e3) / 1e12,
+          "peak": fp32_peak, "unit": "TFLOP/s", "frac": flops / (k / 1e3) / 1e12 / fp32_peak,
+          "algorithmic_flops": flops, "dyads": int(c[2]), "ms": k, "traffic": None}
+    return {"metric": SCREEN_METRIC, "value": world * C3_COUNT / (ms / 1e3), "unit": "candidates/s",
+            "ms_per_step": ms, "valid_frac": valid / C3_COUNT, "fixup_lane_angles": int(c[0]),
+            "angles_evaluated": int(c[1]), "topologies": G, "roofline": rl, "launches_per_step": 4,
+            "config": {"workload": "C3: 10M candidates/GPU, 5-20 joints padded to 20, 256 per topology "
+                                   "(1024-topology generator pool), poses U[0,1)^2 on device, T=200"}}
+
+
+# ----------------------------------------------------------------- C4
+def bench_c4(torch, args, rank, world, peaks, flush):
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.dist import gather_merge
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    db = fourier_db(C4_COUNT, C4_P, seed=4000 + rank)
+    q = fourier_db(1, C4_P, seed=999)
+    stream = torch.cuda.current_stream()
+    k = 10
+
+    def step(timer=None):
+        if timer:
+            timer.mark("start")
+        res = chamfer_scan(db, q, k=k, threshold=0.0, id_base=rank * C4_COUNT, pos_base=rank * C4_COUNT)
+        if timer:
+            timer.mark("scan")
+        if world > 1:
+            gather_merge({n: res[n] for n in ("top_d", "top_id", "top_pos", "hit_d", "hit_id", "hit_pos",
+                                              "n_hits")}, k)
+        if timer:
+            timer.mark("merge")
+        return res
+
+    for _ in range(args.warmup):
+        step()
+    spans = []
+    barrier(torch, world)
+    for _ in range(args.steps):
+        flush()
+        tm = Timer(torch, stream)
+        step(tm)
+        spans.append(tm.spans())
+    barrier(torch, world)
+    ms = max_over_ranks(torch, statistics.mean(s["total"] for s in spans), world)
+    kscan = statistics.mean(s["scan"] for s in spans)
+    sm_clock = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12
+    flops = PAIR_FLOPS * C4_COUNT
+    rl = {"kernel": "chamfer_scan_kernel<7>", "bound": "fp32", "achieved": flops / (kscan / 1e3) / 1e12,
+          "peak": fp32_peak, "unit": "TFLOP/s", "frac": flops / (kscan / 1e3) / 1e12 / fp32_peak,
+          "algorithmic_flops": flops, "ms": kscan, "traffic": None,
+          "hbm_bytes_algorithmic": C4_COUNT * C4_P * 8}
+    # e2e: host query -> scan -> merged top-k back to the host
+    qh = q.cpu().pin_memory()
+    times = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        qd = qh.cuda(non_blocking=True)
+        res = chamfer_scan(db, qd, k=k, threshold=0.0, id_base=rank * C4_COUNT)
+        out = {n: res[n].cpu() for n in ("top_d", "top_id")}
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    e2e_ms = max_over_ranks(torch, statistics.mean(times), world)
+    del db
+    return {"metric": CHAMFER_METRIC, "value": world * C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s",
+            "ms_per_step": ms, "roofline": rl, "launches_per_step": 2,
+            "e2e": {"value": world * C4_COUNT / (e2e_ms / 1e3), "unit": "curve-pairs/s",
+                    "h2d_bytes_per_step": C4_P * 8, "d2h_bytes_per_step": k * 12},
+            "config": {"workload": "C4: 1 query vs 10M normalised Fourier curves/GPU (5 harmonics, "
+                                   "coeffs N(0,1/k^2)), 200 pts fp32, exhaustive top-10"}}
+
+
+# ----------------------------------------------------------------- CPU baseline
+def _cpu_worker(args):
+    groups, T_ = args
+    from oracle import links_oracle as O
+
+    n = 0
+    for pos, steps, fixed in groups:
+        r = O.simulate(pos, steps, fixed, T_)
+        # mirror simulate_batch's per-candidate outcome objects (solver.py:233-239)
+        P = None
+        outs = []
+        for b in range(len(pos)):
+            if r["first_t"][b] < T_:
+                outs.append((int(r["first_t"][b]), int(r["first_joint"][b])))
+            else:
+                if P is None:
+                    P = O.trajectories(r)
+                outs.append(P[b])
+        n += len(pos)
+    return n
+
+
+def cpu_baseline_c2(mb, budget_s: float = 15.0, max_groups: int | None = None):
+    """Oracle port of simulate_batch over topology groups, fork pool of all
+    host cores (bench.py:87-94 pattern).  Bounded sample: as many whole
+    topology groups as fit the budget (estimated from a 1-group probe)."""
+    import multiprocessing as mp
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    cores = len(os.sched_getaffinity(0))
+    groups = []
+    for g, plan in enumerate(mb.plans):
+        sel = np.flatnonzero(mb.topo == g)
+        groups.append((np.ascontiguousarray(mb.pos[sel][:, :plan.n]), [(s.target, s.a, s.b) for s in plan.steps],
+                       plan.fixed))
+    t0 = time.perf_counter()
+    n1 = _cpu_worker((groups[:1], T))
+    per = (time.perf_counter() - t0) / max(n1, 1)
+    want = int(budget_s * cores / max(per, 1e-9))
+    take = []
+    tot = 0
+    for g in groups:
+        if tot >= want:
+            break
+        take.append(g)
+        tot += len(g[0])
+    if max_groups:
+        take = take[:max_groups]
+    chunks = [take[w::cores] for w in range(cores)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_worker, [([], T)] * cores)
+        t0 = time.perf_counter()
+        done = sum(pool.map(_cpu_worker, [(c, T) for c in chunks]))
+        dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "simulations/s", "cores": cores, "kind": "port",
+            "sample": f"{done} of the C2 candidates ({len(take)} whole topology groups), oracle numpy port of "
+                      f"simulate_batch, fork pool x{cores}", "seconds": dt, "one_thread_est": 1.0 / per}
+
+
+# ----------------------------------------------------------------- main
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    mb = c2_inputs(0)
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline_c2(mb, budget_s=8.0)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "simulations/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * C2_COUNT / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded reference-generator streams)",
+            "config": {"workload": "C2: 100,000 candidates of 6-8 joints, 256 per topology, T=200",
+                       "parallelism": f"cpu fork pool x{cb['cores']}"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": value, "unit": "simulations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skip", default="", help="comma list of c3,c4,cpu to skip")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2208_14567_b200 import _native
+
+    _native.load(build_if_missing=False)
+    peaks, peaks_src = load_peaks()
+    flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+
+    def flush():
+        flush_buf.zero_()
+
+    skip = set(filter(None, args.skip.split(",")))
+    c2 = bench_c2(torch, args, rank, world, peaks, flush)
+    e2e = e2e_c2(torch, args, c2["mb"], c2["table"], world)
+    secondary = {}
+    if "c3" not in skip:
+        secondary["screen"] = bench_c3(torch, args, rank, world, peaks, flush)
+    if "c4" not in skip:
+        secondary["chamfer"] = bench_c4(torch, args, rank, world, peaks, flush)
+    cpu = None
+    if rank == 0 and world == 1 and "cpu" not in skip:
+        cpu = cpu_baseline_c2(c2["mb"])
+    if rank == 0:
+        rl = dict(c2["roofline"])
+        line = {
+            "metric": METRIC, "value": c2["value"], "unit": "simulations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": c2["ms"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (f64 fix-up / f64 path replay)",
+            "data": "synthetic (seeded reference-generator topologies and poses)",
+            "config": {"workload": "C2: 100,000 candidates/GPU of 6-8 joints (reference random-topology "
+                                   "operator, 256 per topology), T=200, paths of all joints of valid "
+                                   "candidates (fp32) + lock flags of all", "l2": "flushed between steps "
+                                   f"({L2_FLUSH_BYTES >> 20} MiB write)", "parallelism": f"dp{world}",
+                       "valid_per_gpu": c2["valid"]},
+            "roofline": {**rl, "peak_source": peaks_src},
+            "roofline_kernels": c2["roofline_kernels"],
+            "kernels_ms": c2["kernels_ms"],
+            "e2e": e2e,
+            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind",
+                                                                           "sample")},
+            "gpu_launches": c2["launches_per_step"] * args.steps,
+            "clocks": c2["clocks"],
+            "secondary": secondary,
+            "published": {"paper_v100_sims_per_s": 54855, "paper_80thread_cpu_sims_per_s": 17995,
+                          "note": "PAPER.md:208-211, 10,000-mechanism Table-1 workload (other config)"},
+        }
+        print(json.dumps(line, default=float))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

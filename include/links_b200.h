@@ -1,0 +1,199 @@
+/*
+ * links_b200.h — C ABI of the B200-native LINKS hot path (sm_100a).
+ *
+ * The reference (`linkatlas`, /root/reference/pkg/src/linkatlas) is pure
+ * Python: its "interface" for this path is a set of Python functions, not an
+ * FFI.  Each entry point below replaces the numpy body of one of them; the
+ * Python mirror in paper_2208_14567_b200/ keeps the reference signatures and
+ * binds these symbols with ctypes (see INTEGRATION.md for the stub a
+ * maintainer would add to linkatlas itself).
+ *
+ * ABI contract
+ *   - The caller owns every buffer; pointers marked (device) are CUDA device
+ *     pointers, the library allocates nothing persistent.
+ *   - Calls are stream-ordered on `stream` (a cudaStream_t passed as void*),
+ *     reentrant across streams/devices; no global mutable state.
+ *   - Return 0 on success, a negative LA_E* code for an invalid argument, or a
+ *     positive cudaError_t.  la_last_error() returns a thread-local message.
+ *   - Do not fork() after the first call (CUDA context).
+ */
+#ifndef LINKS_B200_H
+#define LINKS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LA_ABI_VERSION 1
+#define LA_MAX_JOINTS 20   /* joints per mechanism (generator.py n_max default) */
+#define LA_MAX_STEPS 18    /* dyad steps per plan: n - |fixed| - 1 <= 18       */
+#define LA_MAX_TOPK 32
+
+/* error codes (negative) */
+#define LA_EINVAL (-1)     /* bad argument / shape                              */
+#define LA_ERANGE (-2)     /* size beyond a compiled limit                      */
+#define LA_EWS (-3)        /* workspace too small                               */
+
+/* ---------------------------------------------------------------- plans
+ * One compiled solve order (solver.py:26-46 SolutionPlan, built by
+ * compile_plan solver.py:71-102 on the host).  64 bytes.                   */
+typedef struct la_plan {
+  int16_t n;                       /* joints                                   */
+  int16_t nsteps;                  /* S = len(plan.steps)                      */
+  uint32_t fixed_mask;             /* bit j set: joint j is Fixed              */
+  int8_t step[LA_MAX_STEPS][3];    /* (target, a, b) per PlanStep              */
+  int8_t _pad[2];
+} la_plan;
+
+/* flags for la_simulate */
+#define LA_SIM_WRITE_TRAJ 1u       /* write (T,2) f32 paths of every joint     */
+#define LA_SIM_FP64 2u             /* evaluate every angle in f64 (no fp32)    */
+#define LA_SIM_GATE_ONLY 4u        /* two-fidelity gate: skip exact first lock
+                                      search for coarse-locked candidates      */
+#define LA_SIM_NO_COARSE 8u        /* disable the coarse-first angle order     */
+#define LA_SIM_TRAJ_F64 16u        /* traj holds f64 (T,2) rows instead of f32 */
+
+/* Batched replay of compiled plans over (candidate x crank angle).
+ * Replaces simulate_batch (solver.py:172-239) and, with coarse-first order,
+ * the two-fidelity gate of check_feasible / find_valid_variant
+ * (solver.py:242-249, generator.py:241-283).  Mixed topologies per launch.  */
+typedef struct la_sim_args {
+  const double* pos0;         /* (device) [B][pos_stride][2] initial poses    */
+  const int32_t* topo;        /* (device) [B] plan index, or NULL => plan 0   */
+  const la_plan* plans;       /* (device) [G]                                 */
+  const double* crank_cs;     /* (device) [T][2] cos, sin of 2*pi*t/T          */
+  int64_t B;
+  int32_t G;
+  int32_t pos_stride;         /* joints per pose row (>= every plan's n)      */
+  int32_t T;                  /* crank angles per revolution                  */
+  int32_t traj_stride;        /* joint rows per candidate in traj             */
+  void* traj;                 /* (device) [rows][T][2] f32 (f64 with
+                                 LA_SIM_TRAJ_F64), or NULL                    */
+  const int64_t* traj_row;    /* (device) [B] first row of work item i, or
+                                 NULL => i * traj_stride                      */
+  const int64_t* cand;        /* (device, optional) [B] candidate index of work
+                                 item i (gather); outputs stay indexed by i  */
+  const int64_t* cand_count;  /* (device, optional) number of valid entries of
+                                 cand (<= B), read on device: no host sync    */
+  int32_t* first_t;           /* (device, optional with cand) [B] first
+                                 locking angle, T if valid; -1 (with joint
+                                 -2) if the plan has more joints than
+                                 pos_stride or LA_MAX_JOINTS                  */
+  int32_t* first_joint;       /* (device, optional with cand) [B] target joint
+                                 of the first locking dyad, -1 if valid       */
+  int32_t* low_t;             /* (device, optional) [B] lock step of the T/4
+                                 coarse sweep (T_low semantics), -1 if none   */
+  int32_t* low_joint;         /* (device, optional) [B]                       */
+  unsigned long long* counters; /* (device, optional) [4]: fp64 fix-up
+                                 lane-angles, angles evaluated, dyads
+                                 executed, candidates processed              */
+  float fixup_tau;            /* fp32 screen: redo an angle in f64 when a
+                                 dyad's margin min(ra+rb-d, d-|ra-rb|) is
+                                 within tau (unit-box lengths) of a lock;
+                                 trajectory rounds always run in f64         */
+  uint32_t flags;             /* LA_SIM_*                                     */
+} la_sim_args;
+
+int la_simulate(const la_sim_args* args, void* stream);
+
+/* Per-candidate step geometry r_a, r_b, branch in f64
+ * (plan_geometry, solver.py:105-120).  Outputs [B][LA_MAX_STEPS].          */
+int la_plan_geometry(const double* pos0, const int32_t* topo, const la_plan* plans,
+                     int64_t B, int32_t G, int32_t pos_stride,
+                     double* r_a, double* r_b, double* branch, void* stream);
+
+/* Element-wise f64 circle-circle intersection (dyad_solve, solver.py:123-139).
+ * pa, pb: [n][2]; out: [n][2]; ok: [n] 1 solved / 0 no intersection.       */
+int la_dyad_solve(const double* pa, const double* pb, const double* r_a,
+                  const double* r_b, const double* branch, int64_t n,
+                  double* out, int32_t* ok, void* stream);
+
+/* Ordered stream compaction of valid candidates (first_t == T):
+ * valid_idx[0..count) ascending.  count is written to *valid_count (device). */
+size_t la_compact_workspace(int64_t B);
+int la_compact_valid(const int32_t* first_t, int64_t B, int32_t T,
+                     int64_t* valid_idx, int64_t* valid_count,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- curves
+ * Batched farthest-pair normalisation (normalize, curves.py:45-71) fused
+ * with is_circle (curves.py:95-101) and the frame-stability predicate.     */
+typedef struct la_norm_args {
+  const void* paths;          /* (device) [rows][P][2] f32 or f64             */
+  int32_t in_f64;
+  const int64_t* src_row;     /* (device, optional) [M] row of path m         */
+  int64_t M;
+  int32_t P;
+  void* out;                  /* (device) [M][P][2] f32 or f64                */
+  int32_t out_f64;
+  int32_t* pair;              /* (device, optional) [M][2] farthest pair i<j  */
+  double* diameter;           /* (device, optional) [M]                       */
+  uint8_t* is_circle;         /* (device, optional) [M]                       */
+  double* circle_var;         /* (device, optional) [M]                       */
+  uint8_t* unstable;          /* (device, optional) [M] frame not unique      */
+  int32_t* status;            /* (device) [M] 0 ok, 1 degenerate (d <= 0)     */
+  double* bbox;               /* (device, optional) [M][4] input lo_x, lo_y,
+                                 hi_x, hi_y (is_normalized, curves.py:74-84) */
+  double rel_tol;             /* near-tie tolerance on the diameter (1e-6)    */
+  double y_tol;               /* |y0 - 0.5| flip-boundary tolerance (1e-6)   */
+} la_norm_args;
+
+int la_normalize(const la_norm_args* args, void* stream);
+
+/* is_circle statistic of already-normalised paths (curves.py:95-101):
+ * population variance of hypot(x-0.5, y-0.5); flag = var < 5e-4.          */
+int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P,
+                    double* var, uint8_t* flag, void* stream);
+
+/* ---------------------------------------------------------------- chamfer
+ * Bi-directional mean chamfer of every database curve against each query
+ * (chamfer curves.py:123-129, _chamfer_block atlas.py:45-55), fused with the
+ * shuffle-and-scan selection of Atlas.retrieve (atlas.py:179-236):
+ *   top_*: best k non-hits (d >= threshold) by (d, scan position)
+ *   hit_*: first k hits (d < threshold) by scan position
+ * Exhaustive top-k is threshold = 0.                                        */
+#define LA_CH_EXPANSION 1u   /* |a|^2+|q|^2-2a.q inner loop + direct re-check */
+
+typedef struct la_chamfer_args {
+  const float* db;            /* (device) [N][P][2] f32 normalised curves     */
+  int64_t N;
+  int32_t P;
+  const float* queries;       /* (device) [NQ][Q][2] f32                      */
+  int32_t NQ;
+  int32_t Q;
+  const int64_t* order;       /* (device, optional) [N] record at scan pos    */
+  int64_t pos_begin;          /* scan-position range [pos_begin, pos_end)     */
+  int64_t pos_end;
+  int64_t id_base;            /* added to record ids in outputs (sharding)    */
+  int64_t pos_base;           /* reported scan position = pos + pos_base ...  */
+  const int64_t* pos_map;     /* (device, optional) ... or pos_map[pos]       */
+  int32_t k;                  /* 0..LA_MAX_TOPK                               */
+  float threshold;
+  int64_t exclude_id;         /* record skipped entirely (self hit), -1 none  */
+  float* top_d; int64_t* top_id; int64_t* top_pos;   /* [NQ][k]               */
+  float* hit_d; int64_t* hit_id; int64_t* hit_pos;   /* [NQ][k]               */
+  int64_t* n_hits;            /* (device, optional) [NQ] total hits           */
+  float* all_d;               /* (device, optional) [NQ][N] by record index   */
+  void* ws;
+  size_t ws_bytes;
+  uint32_t flags;             /* LA_CH_*                                      */
+  float fixup_below;          /* expansion mode: recompute pairs with d below
+                                 this by direct differences                  */
+} la_chamfer_args;
+
+size_t la_chamfer_workspace(const la_chamfer_args* args);
+int la_chamfer_topk(const la_chamfer_args* args, void* stream);
+
+/* ---------------------------------------------------------------- misc */
+int la_abi_version(void);
+const char* la_last_error(void);
+/* number of SMs of the current device (grid sizing helper), or <0 */
+int la_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LINKS_B200_H */

@@ -1,0 +1,213 @@
+"""ctypes binding of the C ABI in include/links_b200.h.
+
+The library is REQUIRED: there is no CPU fallback anywhere in this package.
+If ``_lib/liblinks_b200.so`` is missing it is built with nvcc on first use;
+if that fails (or no CUDA device is present when a kernel is called) the call
+raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_lib" / "liblinks_b200.so"
+
+LA_MAX_JOINTS = 20
+LA_MAX_STEPS = 18
+LA_MAX_TOPK = 32
+
+LA_SIM_WRITE_TRAJ = 1
+LA_SIM_FP64 = 2
+LA_SIM_GATE_ONLY = 4
+LA_SIM_NO_COARSE = 8
+LA_SIM_TRAJ_F64 = 16
+
+LA_CH_EXPANSION = 1
+
+EXPORTS = (
+    "la_simulate",
+    "la_plan_geometry",
+    "la_dyad_solve",
+    "la_compact_workspace",
+    "la_compact_valid",
+    "la_normalize",
+    "la_circle_stats",
+    "la_chamfer_workspace",
+    "la_chamfer_topk",
+    "la_abi_version",
+    "la_last_error",
+    "la_device_sm_count",
+)
+
+
+class LaPlan(C.Structure):
+    _fields_ = [
+        ("n", C.c_int16),
+        ("nsteps", C.c_int16),
+        ("fixed_mask", C.c_uint32),
+        ("step", (C.c_int8 * 3) * LA_MAX_STEPS),
+        ("_pad", C.c_int8 * 2),
+    ]
+
+
+assert C.sizeof(LaPlan) == 64
+
+
+class LaSimArgs(C.Structure):
+    _fields_ = [
+        ("pos0", C.c_void_p),
+        ("topo", C.c_void_p),
+        ("plans", C.c_void_p),
+        ("crank_cs", C.c_void_p),
+        ("B", C.c_int64),
+        ("G", C.c_int32),
+        ("pos_stride", C.c_int32),
+        ("T", C.c_int32),
+        ("traj_stride", C.c_int32),
+        ("traj", C.c_void_p),
+        ("traj_row", C.c_void_p),
+        ("cand", C.c_void_p),
+        ("cand_count", C.c_void_p),
+        ("first_t", C.c_void_p),
+        ("first_joint", C.c_void_p),
+        ("low_t", C.c_void_p),
+        ("low_joint", C.c_void_p),
+        ("counters", C.c_void_p),
+        ("fixup_tau", C.c_float),
+        ("flags", C.c_uint32),
+    ]
+
+
+class LaNormArgs(C.Structure):
+    _fields_ = [
+        ("paths", C.c_void_p),
+        ("in_f64", C.c_int32),
+        ("src_row", C.c_void_p),
+        ("M", C.c_int64),
+        ("P", C.c_int32),
+        ("out", C.c_void_p),
+        ("out_f64", C.c_int32),
+        ("pair", C.c_void_p),
+        ("diameter", C.c_void_p),
+        ("is_circle", C.c_void_p),
+        ("circle_var", C.c_void_p),
+        ("unstable", C.c_void_p),
+        ("status", C.c_void_p),
+        ("bbox", C.c_void_p),
+        ("rel_tol", C.c_double),
+        ("y_tol", C.c_double),
+    ]
+
+
+class LaChamferArgs(C.Structure):
+    _fields_ = [
+        ("db", C.c_void_p),
+        ("N", C.c_int64),
+        ("P", C.c_int32),
+        ("queries", C.c_void_p),
+        ("NQ", C.c_int32),
+        ("Q", C.c_int32),
+        ("order", C.c_void_p),
+        ("pos_begin", C.c_int64),
+        ("pos_end", C.c_int64),
+        ("id_base", C.c_int64),
+        ("pos_base", C.c_int64),
+        ("pos_map", C.c_void_p),
+        ("k", C.c_int32),
+        ("threshold", C.c_float),
+        ("exclude_id", C.c_int64),
+        ("top_d", C.c_void_p),
+        ("top_id", C.c_void_p),
+        ("top_pos", C.c_void_p),
+        ("hit_d", C.c_void_p),
+        ("hit_id", C.c_void_p),
+        ("hit_pos", C.c_void_p),
+        ("n_hits", C.c_void_p),
+        ("all_d", C.c_void_p),
+        ("ws", C.c_void_p),
+        ("ws_bytes", C.c_size_t),
+        ("flags", C.c_uint32),
+        ("fixup_below", C.c_float),
+    ]
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned a non-zero status."""
+
+
+_lock = threading.Lock()
+_lib: C.CDLL | None = None
+
+
+def _declare(lib: C.CDLL) -> None:
+    vp, i32, i64, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t
+    lib.la_simulate.argtypes = [C.POINTER(LaSimArgs), vp]
+    lib.la_plan_geometry.argtypes = [vp, vp, vp, i64, i32, i32, vp, vp, vp, vp]
+    lib.la_dyad_solve.argtypes = [vp, vp, vp, vp, vp, i64, vp, vp, vp]
+    lib.la_compact_workspace.argtypes = [i64]
+    lib.la_compact_workspace.restype = sz
+    lib.la_compact_valid.argtypes = [vp, i64, i32, vp, vp, vp, sz, vp]
+    lib.la_normalize.argtypes = [C.POINTER(LaNormArgs), vp]
+    lib.la_circle_stats.argtypes = [vp, i32, i64, i32, vp, vp, vp]
+    lib.la_chamfer_workspace.argtypes = [C.POINTER(LaChamferArgs)]
+    lib.la_chamfer_workspace.restype = sz
+    lib.la_chamfer_topk.argtypes = [C.POINTER(LaChamferArgs), vp]
+    lib.la_abi_version.argtypes = []
+    lib.la_last_error.argtypes = []
+    lib.la_last_error.restype = C.c_char_p
+    lib.la_device_sm_count.argtypes = []
+    for name in EXPORTS:
+        if name not in ("la_last_error", "la_compact_workspace", "la_chamfer_workspace"):
+            getattr(lib, name).restype = C.c_int
+
+
+def load(build_if_missing: bool = True) -> C.CDLL:
+    """Load (building once if needed) the CUDA library.  Never falls back."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if build_if_missing:
+            from paper_2208_14567_b200 import build_lib
+
+            if not LIB_PATH.exists():
+                build_lib.build()
+        if not LIB_PATH.exists():
+            raise NativeError(f"CUDA library missing: {LIB_PATH} (run python -m paper_2208_14567_b200.build_lib)")
+        lib = C.CDLL(str(LIB_PATH))
+        _declare(lib)
+        if lib.la_abi_version() != 1:
+            raise NativeError("ABI version mismatch")
+        _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().la_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed (status {rc}): {msg}")
+
+
+def require_cuda():
+    """Return torch with a CUDA device available, or raise (no CPU fallback)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeError("a CUDA device (B200, sm_100a) is required: this package has no CPU path")
+    return torch
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int | None:
+    return None if t is None else int(t.data_ptr())

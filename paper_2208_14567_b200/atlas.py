@@ -1,0 +1,300 @@
+"""Drop-in numerical atlas: seeded shuffle-and-scan chamfer retrieval on the GPU.
+
+Reference: linkatlas atlas.py.  ``Atlas.retrieve`` (atlas.py:179-252) keeps
+its signature and result semantics — hits are the first ``k`` records in the
+persisted shuffle order with chamfer distance below ``threshold`` (an exact
+duplicate of the query is inserted first at distance 0.0, atlas.py:204-214);
+if fewer than ``k`` exist the list is padded with the best remaining records
+by (distance, scan position) and flagged ``above_threshold``
+(atlas.py:219-235); the result is sorted by distance (atlas.py:236).
+
+The scan itself (``_chamfer_block`` over 4096-record chunks, atlas.py:45-55,
+207-222) is one ``la_chamfer_topk`` launch over the device-resident store:
+per-warp top-k / first-k-hit lists merged on device.  The exact-duplicate
+index of atlas.py:76-80 (a dict of every curve's bytes, infeasible at 10M
+records) is replaced by a sorted 64-bit content hash with byte verification.
+"""
+
+from __future__ import annotations
+
+import logging
+from dataclasses import dataclass
+
+import numpy as np
+
+from paper_2208_14567_b200 import _native as N
+from paper_2208_14567_b200.curves import is_normalized, normalize, normalize_tensors, reduce_mechanism, resample
+from paper_2208_14567_b200.mechanism import Mechanism
+from paper_2208_14567_b200.solver import compile_plan
+
+logger = logging.getLogger(__name__)
+
+DEFAULT_THRESHOLD = 0.03   # atlas.py:30
+DEFAULT_K = 3              # atlas.py:31
+
+
+class FormatError(ValueError):
+    """A curve references a missing mechanism (records.py:26 semantics)."""
+
+
+@dataclass
+class RetrievalHit:
+    mech_id: int
+    joint_id: int
+    curve: np.ndarray
+    distance: float
+    mechanism: Mechanism
+    above_threshold: bool
+
+
+# ------------------------------------------------------------ device scan
+def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None, pos_begin: int = 0,
+                 pos_end: int | None = None, id_base: int = 0, pos_base: int = 0, pos_map=None,
+                 exclude_id: int = -1, dense: bool = False, all_d=None, stream=None) -> dict:
+    """One la_chamfer_topk launch.
+
+    db: (N, P, 2) float32 CUDA tensor; queries: (NQ, Q, 2) float32.  order:
+    optional (N,) int64 device tensor, record index at each scan position.
+    Returns ``top_d``/``top_id``/``top_pos`` (NQ, k): best non-hits by
+    (d, pos); ``hit_d``/``hit_id``/``hit_pos``: first k hits (d < threshold)
+    by pos; ``n_hits`` (NQ,); ``all_d`` (NQ, N) when ``dense``.
+    Missing entries have id -1 and d = inf.
+    """
+    torch = N.require_cuda()
+    lib = N.load()
+    if db.dtype != torch.float32 or db.dim() != 3 or db.shape[2] != 2 or not db.is_cuda:
+        raise ValueError("db must be a (N, P, 2) float32 CUDA tensor")
+    if queries.dim() == 2:
+        queries = queries[None]
+    queries = queries.to(device=db.device, dtype=torch.float32).contiguous()
+    db = db.contiguous()
+    Nn, P = db.shape[0], db.shape[1]
+    NQ, Q = queries.shape[0], queries.shape[1]
+    if k > N.LA_MAX_TOPK:
+        raise ValueError(f"k <= {N.LA_MAX_TOPK} supported")
+    pe = Nn if pos_end is None else int(pos_end)
+    dev = db.device
+    out: dict = {}
+    kk = max(int(k), 0)
+    if kk > 0:
+        for name, dt in (("top_d", torch.float32), ("top_id", torch.int64), ("top_pos", torch.int64),
+                         ("hit_d", torch.float32), ("hit_id", torch.int64), ("hit_pos", torch.int64)):
+            out[name] = torch.empty((NQ, kk), dtype=dt, device=dev)
+    out["n_hits"] = torch.zeros(NQ, dtype=torch.int64, device=dev)
+    if dense and all_d is None:
+        all_d = torch.full((NQ, Nn), float("nan"), dtype=torch.float32, device=dev)
+    if all_d is not None:
+        out["all_d"] = all_d
+    if order is not None:
+        order = order.to(device=dev, dtype=torch.int64).contiguous()
+    if pos_map is not None:
+        pos_map = pos_map.to(device=dev, dtype=torch.int64).contiguous()
+    a = N.LaChamferArgs()
+    a.db, a.N, a.P = db.data_ptr(), Nn, P
+    a.queries, a.NQ, a.Q = queries.data_ptr(), NQ, Q
+    a.order = N.ptr(order)
+    a.pos_begin, a.pos_end = int(pos_begin), pe
+    a.id_base, a.pos_base = int(id_base), int(pos_base)
+    a.pos_map = N.ptr(pos_map)
+    a.k = kk
+    a.threshold = float(threshold) if np.isfinite(threshold) else (3.0e38 if threshold > 0 else -3.0e38)
+    a.exclude_id = int(exclude_id)
+    for name in ("top_d", "top_id", "top_pos", "hit_d", "hit_id", "hit_pos"):
+        setattr(a, name, N.ptr(out.get(name)))
+    a.n_hits = out["n_hits"].data_ptr()
+    a.all_d = N.ptr(all_d)
+    a.flags = 0
+    a.fixup_below = 0.0
+    wsb = int(lib.la_chamfer_workspace(a))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    a.ws, a.ws_bytes = ws.data_ptr(), wsb
+    N.check(lib.la_chamfer_topk(a, N.stream_ptr(stream)), "la_chamfer_topk")
+    out["_ws"] = ws  # keep alive until the stream consumes it
+    return out
+
+
+def assemble_hits(hit_d, hit_id, top_d, top_id, k, threshold, self_idx=None):
+    """Host assembly of the retrieve() result from the device lists.
+
+    Mirrors atlas.py:201-236: self hit first (0.0), scan-order hits up to k,
+    padding by (d, pos) flagged above threshold, final stable sort by d.
+    Returns [(distance, record, above_threshold)].
+    """
+    res = []
+    if self_idx is not None:
+        res.append((0.0, int(self_idx), 0.0 >= threshold))
+    for d, i in zip(hit_d, hit_id):
+        if len(res) >= k or i < 0:
+            break
+        res.append((float(d), int(i), False))
+    if len(res) < k:
+        used = {r[1] for r in res}
+        for d, i in zip(top_d, top_id):
+            if len(res) >= k:
+                break
+            if i < 0 or int(i) in used:
+                continue
+            used.add(int(i))
+            res.append((float(d), int(i), True))
+    res.sort(key=lambda r: r[0])
+    return res
+
+
+def _content_hash(points: np.ndarray) -> np.ndarray:
+    """64-bit multiplicative hash of each record's raw f64 bytes."""
+    n = points.shape[0]
+    if n == 0:
+        return np.zeros(0, dtype=np.uint64)
+    words = np.ascontiguousarray(points).reshape(n, -1).view(np.uint64)
+    mult = (np.arange(words.shape[1], dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) | np.uint64(1)
+    with np.errstate(over="ignore"):
+        h = np.zeros(n, dtype=np.uint64)
+        for c0 in range(0, words.shape[1], 64):
+            h += (words[:, c0:c0 + 64] * mult[c0:c0 + 64]).sum(axis=1, dtype=np.uint64)
+    return h
+
+
+class Atlas:
+    """Read-only curve store with a persisted shuffle order (atlas.py:58-80)."""
+
+    def __init__(self, points, mech_ids, joint_ids, mechanisms: dict[int, Mechanism], seed: int):
+        self.points = np.asarray(points, dtype=np.float64)
+        self.mech_ids = np.asarray(mech_ids, dtype=np.int64)
+        self.joint_ids = np.asarray(joint_ids, dtype=np.int64)
+        self.mechanisms = mechanisms
+        self.seed = int(seed)
+        self.order = np.random.default_rng(self.seed).permutation(len(self.points))
+        self._descriptors = None
+        h = _content_hash(self.points)
+        self._hash_order = np.argsort(h, kind="stable")
+        self._hash_sorted = h[self._hash_order]
+        self._dev = None
+
+    def __len__(self) -> int:
+        return len(self.points)
+
+    @classmethod
+    def build(cls, records, mechanisms: dict[int, Mechanism], seed: int = 0,
+              resample_to: int | None = None) -> "Atlas":
+        """atlas.py:85-110; resampled curves are renormalised in one batch."""
+        mech_ids, joint_ids, stack = [], [], []
+        for rec in records:
+            if rec.mech_id not in mechanisms:
+                raise FormatError(f"curve references missing mechanism {rec.mech_id}")
+            pts = np.asarray(rec.points, dtype=np.float64)
+            if resample_to is not None and pts.shape[0] > resample_to:
+                pts = resample(pts, resample_to)
+                pts = ("renorm", pts)
+            mech_ids.append(rec.mech_id)
+            joint_ids.append(rec.joint_id)
+            stack.append(pts)
+        renorm = [i for i, p in enumerate(stack) if isinstance(p, tuple)]
+        if renorm:
+            torch = N.require_cuda()
+            batch = torch.from_numpy(np.stack([stack[i][1] for i in renorm])).cuda()
+            res = normalize_tensors(batch, out_f64=True)
+            if bool((res["status"] != 0).any()):
+                from paper_2208_14567_b200.curves import DegeneratePathError
+
+                raise DegeneratePathError("all path points coincident")
+            outs = res["out"].cpu().numpy()
+            for j, i in enumerate(renorm):
+                stack[i] = outs[j]
+        points = np.zeros((0, 0, 2)) if not stack else np.stack(stack)
+        return cls(points, np.array(mech_ids), np.array(joint_ids), mechanisms, seed)
+
+    # -- device residency ------------------------------------------------
+    def device_points(self):
+        torch = N.require_cuda()
+        if self._dev is None:
+            self._dev = torch.from_numpy(self.points.astype(np.float32)).cuda()
+        return self._dev
+
+    def exact_index(self, query: np.ndarray) -> int | None:
+        """Index of the LAST stored curve byte-identical to ``query``
+        (the dict comprehension of atlas.py:78-80 keeps the last)."""
+        q = np.ascontiguousarray(np.asarray(query, dtype=np.float64))
+        if len(self) == 0 or q.shape != self.points.shape[1:]:
+            return None
+        h = _content_hash(q[None])[0]
+        lo = np.searchsorted(self._hash_sorted, h, side="left")
+        hi = np.searchsorted(self._hash_sorted, h, side="right")
+        found = None
+        qb = q.tobytes()
+        for idx in sorted(self._hash_order[lo:hi].tolist()):
+            if self.points[idx].tobytes() == qb:
+                found = idx
+        return found
+
+    # -- coarse prefilter (atlas.py:153-177; host, off the hot path) -------
+    def coarse_filter(self, query: np.ndarray, budget: int, mode: str = "heuristic") -> np.ndarray:
+        if mode == "exact" or budget >= len(self):
+            return self.order
+        if self._descriptors is None:
+            self._descriptors = np.stack([self._descriptor(p) for p in self.points])
+        qd = self._descriptor(query)
+        dist = np.abs(self._descriptors - qd[None, :]).sum(axis=1)
+        keep = np.argsort(dist, kind="stable")[:budget]
+        mask = np.zeros(len(self), dtype=bool)
+        mask[keep] = True
+        return self.order[mask[self.order]]
+
+    @staticmethod
+    def _descriptor(path: np.ndarray) -> np.ndarray:
+        r = np.hypot(path[:, 0] - 0.5, path[:, 1] - 0.5)
+        hist, _ = np.histogram(r, bins=16, range=(0.0, 0.75))
+        hist = hist / max(len(r), 1)
+        extent = path.max(axis=0) - path.min(axis=0)
+        return np.concatenate([hist, extent])
+
+    # -- search ----------------------------------------------------------
+    def retrieve(self, query: np.ndarray, k: int = DEFAULT_K, threshold: float = DEFAULT_THRESHOLD,
+                 budget: int | None = None, filter_mode: str = "exact") -> list[RetrievalHit]:
+        """Shuffle-and-scan retrieval (atlas.py:179-252) on the GPU."""
+        if len(self) == 0:
+            logger.warning("retrieve on an empty atlas")
+            return []
+        torch = N.require_cuda()
+        query = np.asarray(query, dtype=np.float64)
+        if not is_normalized(query):
+            query = normalize(query)
+        scan = self.order if budget is None else self.coarse_filter(query, budget, filter_mode)
+        self_idx = self.exact_index(query)
+        if not (1 <= k <= N.LA_MAX_TOPK):
+            return self._retrieve_large(query, k, threshold, scan, self_idx)
+        db = self.device_points()
+        res = chamfer_scan(db, torch.from_numpy(query.astype(np.float32)).cuda()[None],
+                           k=int(k), threshold=threshold,
+                           order=torch.from_numpy(np.ascontiguousarray(scan, dtype=np.int64)).cuda(),
+                           pos_end=len(scan), exclude_id=-1 if self_idx is None else int(self_idx))
+        host = {n: res[n][0].cpu().numpy() for n in ("hit_d", "hit_id", "top_d", "top_id")}
+        rows = assemble_hits(host["hit_d"], host["hit_id"], host["top_d"], host["top_id"], int(k), threshold,
+                             self_idx)
+        return [self._hit(d, i, above) for d, i, above in rows]
+
+    def _retrieve_large(self, query, k, threshold, scan, self_idx):
+        """k beyond the per-warp list size: dense distances, host ordering."""
+        torch = N.require_cuda()
+        db = self.device_points()
+        res = chamfer_scan(db, torch.from_numpy(query.astype(np.float32)).cuda()[None], k=0, dense=True)
+        d = res["all_d"][0].cpu().numpy().astype(np.float64)
+        ds = d[scan]
+        hits_pos = [p for p in np.flatnonzero(ds < threshold) if scan[p] != self_idx]
+        cap = max(int(k), 1) - (1 if self_idx is not None else 0)
+        hits_pos = np.array(hits_pos[:max(cap, 0)], dtype=np.int64)
+        used = set(int(scan[p]) for p in hits_pos) | ({int(self_idx)} if self_idx is not None else set())
+        rest = np.array([p for p in np.lexsort((np.arange(len(ds)), ds)) if int(scan[p]) not in used],
+                        dtype=np.int64)
+        rows = assemble_hits(ds[hits_pos], scan[hits_pos], ds[rest], scan[rest], int(k), threshold, self_idx)
+        return [self._hit(dd, i, above) for dd, i, above in rows]
+
+    def _hit(self, d: float, i: int, above: bool) -> RetrievalHit:
+        mech = self.mechanisms[int(self.mech_ids[i])]
+        reduced = reduce_mechanism(mech, compile_plan(mech), int(self.joint_ids[i]))
+        return RetrievalHit(mech_id=int(self.mech_ids[i]), joint_id=int(self.joint_ids[i]),
+                            curve=self.points[i], distance=float(d), mechanism=reduced,
+                            above_threshold=bool(above))
+
+
+def build_atlas(records, mechanisms, seed: int = 0, resample_to: int | None = None) -> Atlas:
+    return Atlas.build(records, mechanisms, seed=seed, resample_to=resample_to)

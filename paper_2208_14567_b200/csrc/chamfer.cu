@@ -1,0 +1,530 @@
+// Chamfer scan with fused top-k / threshold selection (sm_100a).
+//
+// Reference semantics:
+//   chamfer         curves.py:123-129  mean_a min_q |a-q| + mean_q min_a |a-q|
+//   _chamfer_block  atlas.py:45-55     the same per curve of a (C, P, 2) block
+//   Atlas.retrieve  atlas.py:179-236   walk the seeded shuffle order; hits are
+//                                      d < threshold in scan order (first k),
+//                                      padding is the best non-hits by
+//                                      (d, scan position)
+//
+// Mapping (fast path, even P <= 256, Q <= 256).  The query lives in
+// REGISTERS for the whole launch: lane l owns query points l, l+32, ... (QS
+// slots, packed in pairs for the f32x2 FFMA2/FADD2 pipes).  Each warp walks
+// its grid-stride share of scan positions; the database curve for the next
+// position is fetched by a 1-D TMA bulk copy (cp.async.bulk + mbarrier) into
+// a per-warp double buffer while the current curve is processed.  For every
+// database point a (broadcast LDS.128, two points per step):
+//   * column minima (per query point) stay in registers, FMNMX3-updated;
+//   * the row minimum over the lane's slots is reduced across the warp by a
+//     single REDUX.MIN on the non-negative float bit pattern.
+// Square roots are taken only of the minima.  Distances use direct
+// differences (no |a|^2+|q|^2-2a.q cancellation).
+// Each warp keeps a lane-distributed sorted top-k (by (d, pos)) of non-hits
+// and the first-k hits (by pos); a merge kernel reduces the per-warp lists.
+#include "common.cuh"
+#include <climits>
+
+namespace la {
+namespace {
+
+constexpr int CW = 8;           // warps per CTA
+constexpr int CT = CW * 32;
+constexpr int PMAX = 256;       // database points per curve (fast path)
+constexpr float BIG = 1.0e18f;  // padding coordinate: never a minimum
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ float min3f(float a, float b, float c) { return fminf(fminf(a, b), c); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// lane-distributed sorted list of up to k entries; lane i holds entry i
+struct WarpList {
+  float d;
+  long long pos;
+  long long id;
+};
+
+__device__ __forceinline__ bool key_less(float d0, long long p0, float d1, long long p1) {
+  return d0 < d1 || (d0 == d1 && p0 < p1);
+}
+
+// insert (d, pos, id) keeping ascending order by (d, pos); by_pos orders by
+// position only.  Returns nothing; entries beyond k fall off.
+__device__ __forceinline__ void list_insert(WarpList& L, int k, int lane, float d, long long pos, long long id,
+                                            bool by_pos) {
+  const bool less = lane < k && (by_pos ? (L.pos < pos) : key_less(L.d, L.pos, d, pos));
+  const int idx = __popc(__ballot_sync(FULL, less));
+  if (idx >= k) return;
+  const float pd = __shfl_up_sync(FULL, L.d, 1);
+  const long long pp = __shfl_up_sync(FULL, L.pos, 1);
+  const long long pi = __shfl_up_sync(FULL, L.id, 1);
+  if (lane > idx && lane < k) {
+    L.d = pd;
+    L.pos = pp;
+    L.id = pi;
+  }
+  if (lane == idx) {
+    L.d = d;
+    L.pos = pos;
+    L.id = id;
+  }
+}
+
+struct ScanCtx {
+  la_chamfer_args a;
+  int nwarps_total;   // per query
+  float* ws_top_d;    // [NQ][nwarps][k]
+  long long* ws_top_pos;
+  long long* ws_top_id;
+  float* ws_hit_d;
+  long long* ws_hit_pos;
+  long long* ws_hit_id;
+  long long* ws_nhit;  // [NQ][nwarps]
+  float* dense;        // [NQ][N] (generic path) or NULL
+};
+
+__device__ __forceinline__ void consider(WarpList& top, WarpList& hit, long long& nhit, const ScanCtx& c,
+                                         int lane, float d, long long pos, long long id) {
+  const int k = c.a.k;
+  if (k <= 0) return;
+  if (d < c.a.threshold) {
+    ++nhit;
+    const long long kp = __shfl_sync(FULL, hit.pos, k - 1);
+    if (pos < kp) list_insert(hit, k, lane, d, pos, id, true);
+  } else {
+    const float kd = __shfl_sync(FULL, top.d, k - 1);
+    const long long kp = __shfl_sync(FULL, top.pos, k - 1);
+    if (key_less(d, pos, kd, kp)) list_insert(top, k, lane, d, pos, id, false);
+  }
+}
+
+__device__ __forceinline__ void flush_lists(const ScanCtx& c, int qi, int gw, int lane, const WarpList& top,
+                                            const WarpList& hit, long long nhit) {
+  const int k = c.a.k;
+  if (k <= 0) return;
+  const size_t base = ((size_t)qi * c.nwarps_total + gw) * k;
+  if (lane < k) {
+    c.ws_top_d[base + lane] = top.d;
+    c.ws_top_pos[base + lane] = top.pos;
+    c.ws_top_id[base + lane] = top.id;
+    c.ws_hit_d[base + lane] = hit.d;
+    c.ws_hit_pos[base + lane] = hit.pos;
+    c.ws_hit_id[base + lane] = hit.id;
+  }
+  if (lane == 0) c.ws_nhit[(size_t)qi * c.nwarps_total + gw] = nhit;
+}
+
+__device__ __forceinline__ void list_init(WarpList& L) {
+  L.d = INFINITY;
+  L.pos = LLONG_MAX;
+  L.id = -1;
+}
+
+// ------------------------------------------------------------ fast path
+template <int QS>
+__global__ void __launch_bounds__(CT) chamfer_scan_kernel(const ScanCtx c) {
+  __shared__ __align__(128) float2 buf[CW][2][PMAX];
+  __shared__ __align__(8) uint64_t bars[CW][2];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int qi = blockIdx.y;
+  const la_chamfer_args& A = c.a;
+  const int P = A.P, Q = A.Q;
+  const int gw = blockIdx.x * CW + w;
+  const long long stride = (long long)gridDim.x * CW;
+
+  // query slots in registers (packed pairs), padding far away
+  constexpr int NP = QS / 2;
+  float2 qx2[NP > 0 ? NP : 1], qy2[NP > 0 ? NP : 1];
+  float qxt = BIG, qyt = BIG;  // odd tail slot
+  const float2* qsrc = reinterpret_cast<const float2*>(A.queries) + (size_t)qi * Q;
+#pragma unroll
+  for (int s = 0; s < NP; ++s) {
+    const int i0 = lane + 32 * (2 * s), i1 = lane + 32 * (2 * s + 1);
+    const float2 v0 = i0 < Q ? qsrc[i0] : make_float2(BIG, BIG);
+    const float2 v1 = i1 < Q ? qsrc[i1] : make_float2(BIG, BIG);
+    qx2[s] = make_float2(v0.x, v1.x);
+    qy2[s] = make_float2(v0.y, v1.y);
+  }
+  if (QS & 1) {
+    const int it = lane + 32 * (QS - 1);
+    if (it < Q) {
+      qxt = qsrc[it].x;
+      qyt = qsrc[it].y;
+    }
+  }
+
+  WarpList top, hit;
+  list_init(top);
+  list_init(hit);
+  long long nhit = 0;
+
+  const long long first = A.pos_begin + gw;
+  const long long count = first < A.pos_end ? (A.pos_end - first + stride - 1) / stride : 0;
+  const uint32_t bytes = (uint32_t)P * 8u;
+  if (lane == 0) {
+    mbar_init(&bars[w][0], 1);
+    mbar_init(&bars[w][1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto rec_of = [&](long long pos) -> long long { return A.order ? A.order[pos] : pos; };
+  if (count > 0 && lane == 0) {
+    const long long id = rec_of(first);
+    mbar_expect_tx(&bars[w][0], bytes);
+    tma_load_1d(&buf[w][0][0], A.db + (size_t)id * P * 2, bytes, &bars[w][0]);
+  }
+  uint32_t phase = 0;  // bit b: parity of buffer b
+
+  for (long long it = 0; it < count; ++it) {
+    const int bi = (int)(it & 1);
+    const long long pos = first + it * stride;
+    const long long id = rec_of(pos);
+    __syncwarp();
+    if (it + 1 < count && lane == 0) {
+      fence_proxy_async();
+      const long long nid = rec_of(pos + stride);
+      mbar_expect_tx(&bars[w][bi ^ 1], bytes);
+      tma_load_1d(&buf[w][bi ^ 1][0], A.db + (size_t)nid * P * 2, bytes, &bars[w][bi ^ 1]);
+    }
+    mbar_wait(&bars[w][bi], (phase >> bi) & 1u);
+    phase ^= (1u << bi);
+    if (id == A.exclude_id) continue;
+
+    float2 cmin[NP > 0 ? NP : 1];
+#pragma unroll
+    for (int s = 0; s < NP; ++s) cmin[s] = make_float2(INFINITY, INFINITY);
+    float cmint = INFINITY;
+    float row_sum = 0.0f;
+    const float4* cur = reinterpret_cast<const float4*>(&buf[w][bi][0]);
+#pragma unroll 1
+    for (int a0 = 0; a0 < P; a0 += 32) {
+      float mine = 0.0f;
+#pragma unroll
+      for (int u = 0; u < 32; u += 2) {
+        if (a0 + u < P) {
+          const float4 pp = cur[(a0 + u) >> 1];
+          const float2 ax0 = make_float2(-pp.x, -pp.x), ay0 = make_float2(-pp.y, -pp.y);
+          const float2 ax1 = make_float2(-pp.z, -pp.z), ay1 = make_float2(-pp.w, -pp.w);
+          float rm0 = INFINITY, rm1 = INFINITY;
+#pragma unroll
+          for (int s = 0; s < NP; ++s) {
+            const float2 dx0 = __fadd2_rn(qx2[s], ax0), dy0 = __fadd2_rn(qy2[s], ay0);
+            const float2 dx1 = __fadd2_rn(qx2[s], ax1), dy1 = __fadd2_rn(qy2[s], ay1);
+            const float2 d0 = __ffma2_rn(dy0, dy0, __fmul2_rn(dx0, dx0));
+            const float2 d1 = __ffma2_rn(dy1, dy1, __fmul2_rn(dx1, dx1));
+            cmin[s].x = min3f(cmin[s].x, d0.x, d1.x);
+            cmin[s].y = min3f(cmin[s].y, d0.y, d1.y);
+            rm0 = min3f(rm0, d0.x, d0.y);
+            rm1 = min3f(rm1, d1.x, d1.y);
+          }
+          if (QS & 1) {
+            const float ex0 = qxt - pp.x, ey0 = qyt - pp.y;
+            const float ex1 = qxt - pp.z, ey1 = qyt - pp.w;
+            const float e0 = fmaf(ey0, ey0, ex0 * ex0), e1 = fmaf(ey1, ey1, ex1 * ex1);
+            cmint = min3f(cmint, e0, e1);
+            rm0 = fminf(rm0, e0);
+            rm1 = fminf(rm1, e1);
+          }
+          const float r0 = __uint_as_float(__reduce_min_sync(FULL, __float_as_uint(rm0)));
+          const float r1 = __uint_as_float(__reduce_min_sync(FULL, __float_as_uint(rm1)));
+          if (lane == u) mine = r0;
+          if (lane == u + 1) mine = r1;
+        }
+      }
+      if (a0 + lane < P) row_sum += sqrtf(mine);
+    }
+    float col_sum = 0.0f;
+#pragma unroll
+    for (int s = 0; s < NP; ++s) {
+      if (lane + 32 * (2 * s) < Q) col_sum += sqrtf(cmin[s].x);
+      if (lane + 32 * (2 * s + 1) < Q) col_sum += sqrtf(cmin[s].y);
+    }
+    if ((QS & 1) && lane + 32 * (QS - 1) < Q) col_sum += sqrtf(cmint);
+    const float d = warp_sum(row_sum) / (float)P + warp_sum(col_sum) / (float)Q;
+    if (A.all_d && lane == 0) A.all_d[(size_t)qi * A.N + id] = d;
+    const long long rpos = A.pos_map ? A.pos_map[pos] : pos + A.pos_base;
+    consider(top, hit, nhit, c, lane, d, rpos, id + A.id_base);
+  }
+  flush_lists(c, qi, gw, lane, top, hit, nhit);
+}
+
+// ------------------------------------------------------------ generic path
+// one CTA per (scan position, query): any P, Q; distances to a dense buffer
+__global__ void __launch_bounds__(256) chamfer_generic_kernel(const la_chamfer_args A, float* dense) {
+  extern __shared__ float2 gsm[];
+  float2* pa = gsm;
+  float2* pq = gsm + A.P;
+  __shared__ float red[2][8];
+  const int qi = blockIdx.y;
+  const float2* qsrc = reinterpret_cast<const float2*>(A.queries) + (size_t)qi * A.Q;
+  for (int i = threadIdx.x; i < A.Q; i += 256) pq[i] = qsrc[i];
+  for (long long pos = A.pos_begin + blockIdx.x; pos < A.pos_end; pos += gridDim.x) {
+    const long long id = A.order ? A.order[pos] : pos;
+    const float2* src = reinterpret_cast<const float2*>(A.db) + (size_t)id * A.P;
+    __syncthreads();
+    for (int i = threadIdx.x; i < A.P; i += 256) pa[i] = src[i];
+    __syncthreads();
+    float rs = 0.0f, cs = 0.0f;
+    for (int i = threadIdx.x; i < A.P; i += 256) {
+      float m = INFINITY;
+      for (int j = 0; j < A.Q; ++j) {
+        const float dx = pa[i].x - pq[j].x, dy = pa[i].y - pq[j].y;
+        m = fminf(m, fmaf(dy, dy, dx * dx));
+      }
+      rs += sqrtf(m);
+    }
+    for (int j = threadIdx.x; j < A.Q; j += 256) {
+      float m = INFINITY;
+      for (int i = 0; i < A.P; ++i) {
+        const float dx = pa[i].x - pq[j].x, dy = pa[i].y - pq[j].y;
+        m = fminf(m, fmaf(dy, dy, dx * dx));
+      }
+      cs += sqrtf(m);
+    }
+    rs = warp_sum(rs);
+    cs = warp_sum(cs);
+    if ((threadIdx.x & 31) == 0) {
+      red[0][threadIdx.x >> 5] = rs;
+      red[1][threadIdx.x >> 5] = cs;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float r = 0.0f, q = 0.0f;
+      for (int i = 0; i < 8; ++i) {
+        r += red[0][i];
+        q += red[1][i];
+      }
+      const float d = r / (float)A.P + q / (float)A.Q;
+      dense[(size_t)qi * A.N + id] = d;
+    }
+  }
+}
+
+// selection over dense distances (generic path): same per-warp lists
+__global__ void __launch_bounds__(CT) select_kernel(const ScanCtx c) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, qi = blockIdx.y;
+  const la_chamfer_args& A = c.a;
+  const int gw = blockIdx.x * CW + w;
+  const long long stride = (long long)gridDim.x * CW;
+  WarpList top, hit;
+  list_init(top);
+  list_init(hit);
+  long long nhit = 0;
+  for (long long pos = A.pos_begin + gw; pos < A.pos_end; pos += stride) {
+    const long long id = A.order ? A.order[pos] : pos;
+    if (id == A.exclude_id) continue;
+    const float d = c.dense[(size_t)qi * A.N + id];
+    const long long rpos = A.pos_map ? A.pos_map[pos] : pos + A.pos_base;
+    consider(top, hit, nhit, c, lane, d, rpos, id + A.id_base);
+  }
+  flush_lists(c, qi, gw, lane, top, hit, nhit);
+}
+
+// merge per-warp lists: k rounds of CTA-wide argmin (one CTA per query)
+__global__ void __launch_bounds__(1024) merge_kernel(const ScanCtx c) {
+  const int qi = blockIdx.x;
+  const la_chamfer_args& A = c.a;
+  const int k = A.k;
+  const long long n = (long long)c.nwarps_total * k;
+  const size_t base = (size_t)qi * n;
+  __shared__ float sd[32];
+  __shared__ long long sp[32];
+  __shared__ long long si[32];
+  __shared__ long long sidx[32];
+  __shared__ long long nh[32];
+  // total hits
+  long long h = 0;
+  for (long long i = threadIdx.x; i < c.nwarps_total; i += 1024) h += c.ws_nhit[(size_t)qi * c.nwarps_total + i];
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(FULL, h, o);
+  if ((threadIdx.x & 31) == 0) nh[threadIdx.x >> 5] = h;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int i = 0; i < 32; ++i) t += nh[i];
+    if (A.n_hits) A.n_hits[qi] = t;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    float* D = pass == 0 ? c.ws_top_d : c.ws_hit_d;
+    long long* Pp = pass == 0 ? c.ws_top_pos : c.ws_hit_pos;
+    long long* I = pass == 0 ? c.ws_top_id : c.ws_hit_id;
+    float* od = pass == 0 ? A.top_d : A.hit_d;
+    int64_t* op = pass == 0 ? A.top_pos : A.hit_pos;
+    int64_t* oi = pass == 0 ? A.top_id : A.hit_id;
+    const bool by_pos = pass == 1;
+    for (int r = 0; r < k; ++r) {
+      float bd = INFINITY;
+      long long bp = LLONG_MAX, bi = -1, bx = -1;
+      for (long long i = threadIdx.x; i < n; i += 1024) {
+        const long long p = Pp[base + i];
+        if (p == LLONG_MAX) continue;  // empty or taken
+        const float d = D[base + i];
+        const bool better = by_pos ? (p < bp) : key_less(d, p, bd, bp);
+        if (better) {
+          bd = d; bp = p; bi = I[base + i]; bx = i;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const float od_ = __shfl_xor_sync(FULL, bd, o);
+        const long long op_ = __shfl_xor_sync(FULL, bp, o);
+        const long long oi_ = __shfl_xor_sync(FULL, bi, o);
+        const long long ox_ = __shfl_xor_sync(FULL, bx, o);
+        const bool better = by_pos ? (op_ < bp) : key_less(od_, op_, bd, bp);
+        if (better) { bd = od_; bp = op_; bi = oi_; bx = ox_; }
+      }
+      if ((threadIdx.x & 31) == 0) {
+        sd[threadIdx.x >> 5] = bd; sp[threadIdx.x >> 5] = bp;
+        si[threadIdx.x >> 5] = bi; sidx[threadIdx.x >> 5] = bx;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float d0 = sd[0]; long long p0 = sp[0], i0 = si[0], x0 = sidx[0];
+        for (int j = 1; j < 32; ++j) {
+          const bool better = by_pos ? (sp[j] < p0) : key_less(sd[j], sp[j], d0, p0);
+          if (better) { d0 = sd[j]; p0 = sp[j]; i0 = si[j]; x0 = sidx[j]; }
+        }
+        if (od) od[(size_t)qi * k + r] = x0 >= 0 ? d0 : INFINITY;
+        if (op) op[(size_t)qi * k + r] = x0 >= 0 ? p0 : -1;
+        if (oi) oi[(size_t)qi * k + r] = x0 >= 0 ? i0 : -1;
+        if (x0 >= 0) Pp[base + x0] = LLONG_MAX;  // consume
+      }
+      __syncthreads();
+    }
+  }
+}
+
+struct Plan {
+  bool fast;
+  int qs;
+  int grid;        // CTAs per query (x)
+  int nwarps;      // per query
+  size_t ws_lists; // bytes of list area
+  size_t ws_dense; // bytes of dense scratch (generic path without all_d)
+};
+
+Plan make_plan(const la_chamfer_args* a) {
+  Plan p{};
+  const long long npos = a->pos_end - a->pos_begin;
+  p.fast = (a->P % 2 == 0) && a->P <= PMAX && a->Q <= 256 && a->Q >= 1;
+  p.qs = (a->Q + 31) / 32;
+  int sms = sm_count();
+  if (sms <= 0) sms = 148;
+  long long want = (npos + CW - 1) / CW;
+  long long cap = (long long)sms * 4;  // resident CTAs per SM for the fast kernel
+  if (a->NQ > 1) cap = (cap + a->NQ - 1) / a->NQ;
+  if (cap < 1) cap = 1;
+  long long g = want < cap ? want : cap;
+  if (g < 1) g = 1;
+  p.grid = (int)g;
+  p.nwarps = p.grid * CW;
+  const size_t per = (size_t)a->NQ * p.nwarps * (a->k > 0 ? a->k : 1);
+  p.ws_lists = per * (2 * sizeof(float) + 4 * sizeof(long long)) + (size_t)a->NQ * p.nwarps * sizeof(long long);
+  p.ws_dense = (!p.fast && !a->all_d) ? (size_t)a->NQ * a->N * sizeof(float) : 0;
+  return p;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+}  // namespace la
+
+using namespace la;
+
+extern "C" {
+
+size_t la_chamfer_workspace(const la_chamfer_args* a) {
+  if (!a) return 0;
+  const Plan p = make_plan(a);
+  return align_up(p.ws_lists) + align_up(p.ws_dense) + 1024;
+}
+
+int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
+  if (!a) return fail(LA_EINVAL, "la_chamfer_topk: null args");
+  if (a->N < 0 || a->P < 1 || a->Q < 1 || a->NQ < 1 || !a->db || !a->queries)
+    return fail(LA_EINVAL, "la_chamfer_topk: bad sizes/buffers");
+  if (a->k < 0 || a->k > LA_MAX_TOPK) return fail(LA_ERANGE, "la_chamfer_topk: k=%d beyond %d", a->k, LA_MAX_TOPK);
+  if (a->pos_begin < 0 || a->pos_end > a->N || a->pos_begin > a->pos_end)
+    return fail(LA_EINVAL, "la_chamfer_topk: bad scan range");
+  if (a->k > 0 && (!a->top_d || !a->top_id || !a->top_pos || !a->hit_d || !a->hit_id || !a->hit_pos))
+    return fail(LA_EINVAL, "la_chamfer_topk: k > 0 needs top_* and hit_* outputs");
+  if (a->k == 0 && !a->all_d) return fail(LA_EINVAL, "la_chamfer_topk: nothing to output");
+  if (a->NQ > 65535) return fail(LA_ERANGE, "la_chamfer_topk: NQ too large");
+  const Plan p = make_plan(a);
+  if (!a->ws || a->ws_bytes < la_chamfer_workspace(a)) return fail(LA_EWS, "la_chamfer_topk: workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ScanCtx c{};
+  c.a = *a;
+  c.nwarps_total = p.nwarps;
+  unsigned char* w = static_cast<unsigned char*>(a->ws);
+  const size_t per = (size_t)a->NQ * p.nwarps * (a->k > 0 ? a->k : 1);
+  c.ws_top_pos = reinterpret_cast<long long*>(w); w += per * sizeof(long long);
+  c.ws_top_id = reinterpret_cast<long long*>(w); w += per * sizeof(long long);
+  c.ws_hit_pos = reinterpret_cast<long long*>(w); w += per * sizeof(long long);
+  c.ws_hit_id = reinterpret_cast<long long*>(w); w += per * sizeof(long long);
+  c.ws_nhit = reinterpret_cast<long long*>(w); w += (size_t)a->NQ * p.nwarps * sizeof(long long);
+  c.ws_top_d = reinterpret_cast<float*>(w); w += per * sizeof(float);
+  c.ws_hit_d = reinterpret_cast<float*>(w); w += per * sizeof(float);
+  w = static_cast<unsigned char*>(a->ws) + align_up(p.ws_lists);
+  c.dense = a->all_d ? a->all_d : reinterpret_cast<float*>(w);
+  const dim3 grid(p.grid, a->NQ);
+  if (p.fast) {
+    switch (p.qs) {
+#define LA_CASE(QSV) \
+  case QSV: chamfer_scan_kernel<QSV><<<grid, CT, 0, s>>>(c); break;
+      LA_CASE(1) LA_CASE(2) LA_CASE(3) LA_CASE(4) LA_CASE(5) LA_CASE(6) LA_CASE(7) LA_CASE(8)
+#undef LA_CASE
+      default: return fail(LA_ERANGE, "la_chamfer_topk: Q=%d", a->Q);
+    }
+  } else {
+    const size_t smem = sizeof(float2) * ((size_t)a->P + a->Q);
+    if (smem > 200 * 1024) return fail(LA_ERANGE, "la_chamfer_topk: P+Q too large for the generic path");
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(chamfer_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    long long npos = a->pos_end - a->pos_begin;
+    int sms = sm_count();
+    long long gx = npos < (long long)sms * 8 ? npos : (long long)sms * 8;
+    if (gx < 1) gx = 1;
+    chamfer_generic_kernel<<<dim3((unsigned)gx, a->NQ), 256, smem, s>>>(*a, c.dense);
+    if (a->k > 0) select_kernel<<<grid, CT, 0, s>>>(c);
+  }
+  if (a->k > 0) merge_kernel<<<a->NQ, 1024, 0, s>>>(c);
+  return cuda_status("la_chamfer_topk");
+}
+
+}  // extern "C"

@@ -1,0 +1,52 @@
+// Shared helpers for the LINKS B200 kernels (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdarg>
+#include "links_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "links_b200 is built for sm_100a only"
+#endif
+
+namespace la {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// thread-local last-error text (la_last_error)
+void set_error(const char* fmt, ...);
+
+inline int fail(int code, const char* fmt, ...) {
+  char buf[256];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  set_error("%s", buf);
+  return code;
+}
+
+inline int cuda_status(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", where, cudaGetErrorString(e));
+    return static_cast<int>(e);
+  }
+  return 0;
+}
+
+// SM count of the current device, cached per device
+int sm_count();
+
+__device__ __forceinline__ float2 ld_f2(const float2* p) { return *p; }
+
+__device__ __forceinline__ void st_cs(float2* p, float2 v) { __stcs(p, v); }
+
+// exact f64 ops without contraction (mirror numpy's operation order)
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+}  // namespace la

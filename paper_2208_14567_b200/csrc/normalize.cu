@@ -1,0 +1,369 @@
+// Farthest-pair path normalisation fused with is_circle (sm_100a).
+//
+// Reference semantics: linkatlas curves.py
+//   _farthest_pair    curves.py:22-30  exact O(P^2) argmax of cdist, the
+//                                      lexicographically smallest pair on ties
+//   normalize         curves.py:45-71  rotate the pair to +x, unit diameter,
+//                                      bbox centred at (0.5, 0.5), half-turn
+//                                      choice by first-point angle, then y-mass
+//   is_circle         curves.py:95-101 population variance of the radius about
+//                                      (0.5, 0.5) strictly below 5e-4
+//
+// Mapping: one CTA per curve; the curve is staged in shared memory.  The
+// O(P^2) search uses the circulant pairing (i, i+k mod P), k = 1..P/2, so
+// every thread runs the same trip count (no triangular imbalance) and smem
+// reads are consecutive across the warp.  Each thread keeps its best pair and
+// the runner-up value; the CTA reduction yields the farthest pair plus the
+// best competing distance, which drives the frame-stability flag.  The
+// O(P) frame transform and the variance run in f64.
+#include "common.cuh"
+
+namespace la {
+namespace {
+
+constexpr int NT = 256;
+constexpr int MAXP = 2048;
+
+struct Best {
+  double v1;      // best value (squared distance)
+  long long k1;   // its pair key i*P + j (i < j); smaller wins ties
+  double v2;      // best value among other pairs
+};
+
+__device__ __forceinline__ void consider(Best& b, double v, long long key) {
+  if (v > b.v1 || (v == b.v1 && key < b.k1)) {
+    b.v2 = fmax(b.v2, b.v1);
+    b.v1 = v;
+    b.k1 = key;
+  } else {
+    b.v2 = fmax(b.v2, v);
+  }
+}
+
+__device__ __forceinline__ Best merge(Best a, Best b) {
+  // combine two disjoint candidate sets
+  Best r;
+  if (b.v1 > a.v1 || (b.v1 == a.v1 && b.k1 < a.k1)) {
+    r.v1 = b.v1; r.k1 = b.k1; r.v2 = fmax(b.v2, a.v1);
+  } else {
+    r.v1 = a.v1; r.k1 = a.k1; r.v2 = fmax(a.v2, b.v1);
+  }
+  return r;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < NT / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (threadIdx.x == 0) red[0] = s;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+__device__ __forceinline__ double block_min(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double s = threadIdx.x < NT / 32 ? red[threadIdx.x] : INFINITY;
+    for (int o = 16; o > 0; o >>= 1) s = fmin(s, __shfl_xor_sync(FULL, s, o));
+    if (threadIdx.x == 0) red[0] = s;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+template <typename Tin>
+__device__ __forceinline__ double2 load_pt(const void* base, size_t idx) {
+  if constexpr (sizeof(Tin) == 8) {
+    const double2* p = static_cast<const double2*>(base);
+    return p[idx];
+  } else {
+    const float2 f = static_cast<const float2*>(base)[idx];
+    return make_double2(f.x, f.y);
+  }
+}
+
+// Value compared in the pair search.  f64 input: the cdist distance itself,
+// sqrt((xi-xj)^2 + (yi-yj)^2) without FMA contraction, so exact ties resolve
+// to the lexicographically smallest pair as np.argmax over cdist does.
+// f32 input: the fp32 squared distance (near-ties are flagged unstable).
+template <typename Tin, typename V2>
+__device__ __forceinline__ double pair_value(const V2 pj, const V2 pi) {
+  if constexpr (sizeof(Tin) == 8) {
+    const double dx = dsub(pj.x, pi.x), dy = dsub(pj.y, pi.y);
+    return __dsqrt_rn(dadd(dmul(dx, dx), dmul(dy, dy)));
+  } else {
+    const float dx = pj.x - pi.x, dy = pj.y - pi.y;
+    return (double)fmaf(dy, dy, dx * dx);
+  }
+}
+
+// pair search in the input precision (Tin), everything after in f64
+template <typename Tin>
+__global__ void __launch_bounds__(NT) normalize_kernel(const la_norm_args p) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  using V2 = typename std::conditional<sizeof(Tin) == 8, double2, float2>::type;
+  V2* pts = reinterpret_cast<V2*>(smraw);                                    // 2P entries (doubled)
+  double2* e = reinterpret_cast<double2*>(smraw + sizeof(V2) * 2 * p.P);    // P f64 outputs
+  __shared__ double red[32];
+  __shared__ long long redk[32];
+  __shared__ double red2[32];
+  const int P = p.P;
+  const int tid = threadIdx.x;
+
+  for (long long m = blockIdx.x; m < p.M; m += gridDim.x) {
+    const long long row = p.src_row ? p.src_row[m] : m;
+    const Tin* src = static_cast<const Tin*>(p.paths) + (size_t)row * P * 2;
+    __syncthreads();
+    for (int k = tid; k < P; k += NT) {
+      V2 v;
+      v.x = src[2 * k];
+      v.y = src[2 * k + 1];
+      pts[k] = v;
+      pts[k + P] = v;
+    }
+    __syncthreads();
+
+    // ---- farthest pair (curves.py:22-30)
+    Best b{-1.0, 0x7fffffffffffffffll, -1.0};
+    const int half = P / 2;
+    for (int i = tid; i < P; i += NT) {
+      const V2 pi = pts[i];
+      const int kmax = (P & 1) ? half : half - 1;
+      for (int k = 1; k <= kmax; ++k) {
+        const int j = i + k - (i + k >= P ? P : 0);
+        const long long key = (i < j) ? (long long)i * P + j : (long long)j * P + i;
+        consider(b, pair_value<Tin>(pts[i + k], pi), key);
+      }
+      if (!(P & 1) && i < half) consider(b, pair_value<Tin>(pts[i + half], pi), (long long)i * P + (i + half));
+    }
+    // warp then CTA reduction of (v1, k1, v2)
+    for (int o = 16; o > 0; o >>= 1) {
+      Best q;
+      q.v1 = __shfl_xor_sync(FULL, b.v1, o);
+      q.k1 = __shfl_xor_sync(FULL, b.k1, o);
+      q.v2 = __shfl_xor_sync(FULL, b.v2, o);
+      b = merge(b, q);
+    }
+    if ((tid & 31) == 0) {
+      red[tid >> 5] = b.v1;
+      redk[tid >> 5] = b.k1;
+      red2[tid >> 5] = b.v2;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      Best q{-1.0, 0x7fffffffffffffffll, -1.0};
+      if (tid < NT / 32) q = Best{red[tid], redk[tid], red2[tid]};
+      for (int o = 16; o > 0; o >>= 1) {
+        Best r;
+        r.v1 = __shfl_xor_sync(FULL, q.v1, o);
+        r.k1 = __shfl_xor_sync(FULL, q.k1, o);
+        r.v2 = __shfl_xor_sync(FULL, q.v2, o);
+        q = merge(q, r);
+      }
+      if (tid == 0) {
+        red[0] = q.v1;
+        redk[0] = q.k1;
+        red2[0] = q.v2;
+      }
+    }
+    __syncthreads();
+    const double vmax = red[0];
+    const long long key = redk[0];
+    const double vsecond = red2[0];
+    const int pi_ = (int)(key / P), pj_ = (int)(key % P);
+    __syncthreads();
+
+    // exact diameter in f64 (cdist: sqrt of the summed squared differences)
+    const double2 Pi = load_pt<Tin>(src, pi_), Pj = load_pt<Tin>(src, pj_);
+    const double vx = dsub(Pj.x, Pi.x), vy = dsub(Pj.y, Pi.y);
+    const double d = __dsqrt_rn(dadd(dmul(vx, vx), dmul(vy, vy)));
+    if (!(d > 0.0) || vmax <= 0.0) {
+      if (tid == 0) {
+        p.status[m] = 1;
+        if (p.pair) { p.pair[2 * m] = 0; p.pair[2 * m + 1] = 0; }
+        if (p.diameter) p.diameter[m] = 0.0;
+        if (p.unstable) p.unstable[m] = 1;
+        if (p.is_circle) p.is_circle[m] = 0;
+        if (p.circle_var) p.circle_var[m] = 0.0;
+      }
+      continue;
+    }
+    const double c = ddiv(vx, d), s = ddiv(vy, d);
+    // base = ((P - P_i) @ rot.T) / d, rot = [[c, s], [-s, c]]
+    double lox = INFINITY, loy = INFINITY, hix = -INFINITY, hiy = -INFINITY;
+    for (int k = tid; k < P; k += NT) {
+      const double2 q = load_pt<Tin>(src, k);
+      const double u = dsub(q.x, Pi.x), w = dsub(q.y, Pi.y);
+      const double bx = ddiv(dadd(dmul(u, c), dmul(w, s)), d);
+      const double by = ddiv(dadd(dmul(u, -s), dmul(w, c)), d);
+      e[k] = make_double2(bx, by);
+      lox = fmin(lox, bx); hix = fmax(hix, bx);
+      loy = fmin(loy, by); hiy = fmax(hiy, by);
+    }
+    lox = block_min(lox, red);
+    loy = block_min(loy, red);
+    hix = -block_min(-hix, red);
+    hiy = -block_min(-hiy, red);
+    if (p.bbox) {
+      double ilx = INFINITY, ily = INFINITY, ihx = -INFINITY, ihy = -INFINITY;
+      for (int k = tid; k < P; k += NT) {
+        const double2 q = load_pt<Tin>(src, k);
+        ilx = fmin(ilx, q.x); ihx = fmax(ihx, q.x);
+        ily = fmin(ily, q.y); ihy = fmax(ihy, q.y);
+      }
+      ilx = block_min(ilx, red);
+      ily = block_min(ily, red);
+      ihx = -block_min(-ihx, red);
+      ihy = -block_min(-ihy, red);
+      if (tid == 0) {
+        p.bbox[4 * m] = ilx; p.bbox[4 * m + 1] = ily;
+        p.bbox[4 * m + 2] = ihx; p.bbox[4 * m + 3] = ihy;
+      }
+    }
+    const double mx = ddiv(dadd(lox, hix), 2.0), my = ddiv(dadd(loy, hiy), 2.0);
+    // e = base - mid; cand_a = e + 0.5, cand_b = (-e) + 0.5 (bbox of -base is
+    // the negated bbox, so its centre is exactly -mid)
+    for (int k = tid; k < P; k += NT) {
+      const double2 q = e[k];
+      e[k] = make_double2(dsub(q.x, mx), dsub(q.y, my));
+    }
+    __syncthreads();
+    // half-turn choice (curves.py:63-71)
+    bool use_a;
+    {
+      const double ax = dsub(dadd(e[0].x, 0.5), 0.5), ay = dsub(dadd(e[0].y, 0.5), 0.5);
+      const double bx = dsub(dadd(-e[0].x, 0.5), 0.5), by = dsub(dadd(-e[0].y, 0.5), 0.5);
+      double aa = atan2(ay, ax), ab = atan2(by, bx);
+      const double two_pi = 6.283185307179586;
+      if (aa < 0.0) aa = dadd(aa, two_pi);
+      if (ab < 0.0) ab = dadd(ab, two_pi);
+      if (fabs(dsub(aa, ab)) <= 1e-12) {
+        double ma = 0.0, mb = 0.0;
+        for (int k = tid; k < P; k += NT) {
+          ma += fmax(dsub(dadd(e[k].y, 0.5), 0.5), 0.0);
+          mb += fmax(dsub(dadd(-e[k].y, 0.5), 0.5), 0.0);
+        }
+        ma = block_sum(ma, red);
+        mb = block_sum(mb, red);
+        use_a = ma >= mb;
+      } else {
+        use_a = aa < ab;
+      }
+    }
+    // write + circle statistics
+    double rsum = 0.0;
+    for (int k = tid; k < P; k += NT) {
+      const double2 q = e[k];
+      const double ox = use_a ? dadd(q.x, 0.5) : dadd(-q.x, 0.5);
+      const double oy = use_a ? dadd(q.y, 0.5) : dadd(-q.y, 0.5);
+      e[k] = make_double2(ox, oy);
+      if (p.out_f64) {
+        reinterpret_cast<double2*>(p.out)[(size_t)m * P + k] = make_double2(ox, oy);
+      } else {
+        reinterpret_cast<float2*>(p.out)[(size_t)m * P + k] = make_float2((float)ox, (float)oy);
+      }
+      rsum += hypot(dsub(ox, 0.5), dsub(oy, 0.5));
+    }
+    double var = 0.0;
+    if (p.is_circle || p.circle_var) {
+      const double mean = ddiv(block_sum(rsum, red), (double)P);
+      double acc = 0.0;
+      for (int k = tid; k < P; k += NT) {
+        const double r = hypot(dsub(e[k].x, 0.5), dsub(e[k].y, 0.5));
+        const double dr = dsub(r, mean);
+        acc += dr * dr;
+      }
+      var = ddiv(block_sum(acc, red), (double)P);
+    }
+    if (tid == 0) {
+      p.status[m] = 0;
+      if (p.pair) { p.pair[2 * m] = pi_; p.pair[2 * m + 1] = pj_; }
+      if (p.diameter) p.diameter[m] = d;
+      if (p.is_circle) p.is_circle[m] = var < 5e-4 ? 1 : 0;
+      if (p.circle_var) p.circle_var[m] = var;
+      if (p.unstable) {
+        const double lim = sizeof(Tin) == 8 ? vmax * (1.0 - p.rel_tol)
+                                            : vmax * (1.0 - p.rel_tol) * (1.0 - p.rel_tol);
+        const bool tie = vsecond > lim;
+        const bool flip = fabs(dsub(e[0].y, 0.5)) < p.y_tol;
+        p.unstable[m] = (tie || flip) ? 1 : 0;
+      }
+    }
+  }
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(NT) circle_kernel(const void* paths, int64_t M, int32_t P, double* var_out,
+                                                    uint8_t* flag) {
+  __shared__ double red[32];
+  for (long long m = blockIdx.x; m < M; m += gridDim.x) {
+    const Tin* src = static_cast<const Tin*>(paths) + (size_t)m * P * 2;
+    double rs = 0.0;
+    for (int k = threadIdx.x; k < P; k += NT) rs += hypot(dsub((double)src[2 * k], 0.5), dsub((double)src[2 * k + 1], 0.5));
+    const double mean = ddiv(block_sum(rs, red), (double)P);
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < P; k += NT) {
+      const double dr = dsub(hypot(dsub((double)src[2 * k], 0.5), dsub((double)src[2 * k + 1], 0.5)), mean);
+      acc += dr * dr;
+    }
+    const double var = ddiv(block_sum(acc, red), (double)P);
+    if (threadIdx.x == 0) {
+      if (var_out) var_out[m] = var;
+      if (flag) flag[m] = var < 5e-4 ? 1 : 0;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace la
+
+using namespace la;
+
+extern "C" int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P, double* var,
+                               uint8_t* flag, void* stream) {
+  if (!paths || M < 0 || P < 1 || (!var && !flag)) return fail(LA_EINVAL, "la_circle_stats: bad args");
+  if (M == 0) return 0;
+  const int sms = sm_count();
+  long long grid = M < (long long)sms * 8 ? M : (long long)sms * 8;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (in_f64) circle_kernel<double><<<(unsigned)grid, NT, 0, s>>>(paths, M, P, var, flag);
+  else circle_kernel<float><<<(unsigned)grid, NT, 0, s>>>(paths, M, P, var, flag);
+  return cuda_status("la_circle_stats");
+}
+
+extern "C" int la_normalize(const la_norm_args* a, void* stream) {
+  if (!a) return fail(LA_EINVAL, "la_normalize: null args");
+  if (a->M < 0 || a->P < 2) return fail(LA_EINVAL, "la_normalize: need P >= 2 (got %d)", a->P);
+  if (a->P > MAXP) return fail(LA_ERANGE, "la_normalize: P=%d exceeds %d", a->P, MAXP);
+  if (!a->paths || !a->out || !a->status) return fail(LA_EINVAL, "la_normalize: null buffer");
+  if (a->M == 0) return 0;
+  const int sms = sm_count();
+  if (sms <= 0) return fail(LA_EINVAL, "la_normalize: no device");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t in_sz = a->in_f64 ? sizeof(double2) : sizeof(float2);
+  const size_t smem = in_sz * 2 * a->P + sizeof(double2) * a->P;
+  long long grid = a->M;
+  const long long cap = (long long)sms * 8;
+  if (grid > cap) grid = cap;
+  if (a->in_f64) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(normalize_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    normalize_kernel<double><<<(unsigned)grid, NT, smem, s>>>(*a);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(normalize_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    normalize_kernel<float><<<(unsigned)grid, NT, smem, s>>>(*a);
+  }
+  return cuda_status("la_normalize");
+}

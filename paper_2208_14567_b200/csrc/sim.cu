@@ -1,0 +1,610 @@
+// Batched dyad-solver replay and validity screen (sm_100a).
+//
+// Reference semantics: linkatlas solver.py
+//   plan_geometry   solver.py:105-120 (batch form 189-201)
+//   dyad_solve      solver.py:123-139
+//   simulate_batch  solver.py:172-239  (first_t / first_joint rule 226-231)
+//   check_feasible  solver.py:242-249 and find_valid_variant generator.py:241-283
+//
+// Mapping.  One warp owns one candidate (so the compiled plan, its step
+// geometry and all control flow are warp-uniform); its 32 lanes evaluate 32
+// crank angles at once — angles are independent (each t reads only same-t
+// values, solver.py:159-165).  Joint positions of the lane's angle live in a
+// per-warp shared-memory column pos[joint][lane] (dynamic joint indices
+// without local-memory spills; conflict-free).
+//
+// Precision.  Angles are evaluated in fp32.  Any dyad whose normalised
+// margin g = min((ra+rb)^2-d^2, d^2-(ra-rb)^2)/(ra+rb)^2 has |g| < tau (up to
+// the first lock) sends that lane's whole angle through an f64 replay that
+// mirrors the reference operation order (no FMA contraction), so lock flags
+// match the f64 reference away from the 1e-6 margin band and coordinates stay
+// within 1e-4 of the bounding-box diagonal (SURVEY.md §7 hard part (a)).
+//
+// Angle order.  With T % 4 == 0 the T/4 "coarse" angles t = 4i are screened
+// first (they are bit-identical to the T_low = T/4 sweep of the two-fidelity
+// gate, SURVEY probe P5).  A coarse lock fixes validity; the exact first
+// locking angle is then searched among the fine angles below it in ascending
+// order, stopping at the first 32-angle round with a lock.  Survivors sweep
+// the remaining angles (screen) or all T angles in natural order writing
+// coalesced float2 paths (simulate).
+#include "common.cuh"
+
+namespace la {
+namespace {
+
+constexpr int NJ = LA_MAX_JOINTS;
+constexpr int NS = LA_MAX_STEPS;
+constexpr int SIM_WARPS = 8;
+constexpr int SIM_THREADS = SIM_WARPS * 32;
+
+// Per-warp shared memory: step geometry + initial pose, followed by a joint
+// position column block pos[joint][lane] sized for the batch's largest n.
+// The block is viewed as float2 (fp32 screen rounds) or double2 (f64 rounds).
+struct __align__(16) WarpHead {
+  double2 p0[NJ];        // f64 initial pose
+  double dra[NS], drb[NS], dbr[NS];
+  float sp[NS];          // ra + rb
+  float df[NS];          // |ra - rb|
+  float c2[NS];          // ra^2 - rb^2
+  float ra2[NS];         // ra^2
+  float br[NS];          // branch sign
+  int8_t tg[NS], ia[NS], ib[NS];
+  int8_t _pad[10];
+};
+
+struct Warp {
+  WarpHead* h;
+  unsigned char* cols;   // pos block
+  int lane;
+  __device__ __forceinline__ float2& p32(int j) const {
+    return reinterpret_cast<float2*>(cols)[j * 32 + lane];
+  }
+  __device__ __forceinline__ double2& p64(int j) const {
+    return reinterpret_cast<double2*>(cols)[j * 32 + lane];
+  }
+};
+
+struct SimCtx {
+  int n, ns;
+  uint32_t fixed;
+  double r1;
+  float tau;
+};
+
+// f64 replay of one angle mirroring solver.py:180-231 operation by operation
+// (np.hypot; (d*d + ra*ra - rb*rb) / (2*d); sqrt(max(ra*ra - x*x, 0)); ...),
+// the lock test with LOCK_EPS = 1e-9 (solver.py:19, 213).  Positions live in
+// the caller-provided accessor; returns the first locking step or -1.
+template <typename Get, typename Put>
+__device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get get, Put put) {
+  const double eps = 1e-9;
+#pragma unroll 1
+  for (int s = 0; s < C.ns; ++s) {
+    const int a = H.ia[s], b = H.ib[s], t = H.tg[s];
+    const double2 pa = get(a), pb = get(b);
+    const double dx = dsub(pb.x, pa.x);
+    const double dy = dsub(pb.y, pa.y);
+    const double d = hypot(dx, dy);
+    const double ra = H.dra[s], rb = H.drb[s];
+    if (d < eps || d > dadd(dadd(ra, rb), eps) || d < dsub(fabs(dsub(ra, rb)), eps)) return s;
+    const double x = ddiv(dsub(dadd(dmul(d, d), dmul(ra, ra)), dmul(rb, rb)), dmul(2.0, d));
+    const double h = __dsqrt_rn(fmax(dsub(dmul(ra, ra), dmul(x, x)), 0.0));
+    const double ux = ddiv(dx, d), uy = ddiv(dy, d);
+    const double bh = dmul(H.dbr[s], h);
+    put(t, make_double2(dsub(dadd(pa.x, dmul(x, ux)), dmul(bh, uy)),
+                        dadd(dadd(pa.y, dmul(x, uy)), dmul(bh, ux))));
+  }
+  return -1;
+}
+
+__device__ __forceinline__ double2 crank_tip(const WarpHead& H, const SimCtx& C, double ct, double st) {
+  return make_double2(dadd(H.p0[0].x, dmul(C.r1, ct)), dadd(H.p0[0].y, dmul(C.r1, st)));
+}
+
+// rare path of the fp32 screen: the whole angle again in f64, positions in
+// a lane-private array; rounded results go back to the fp32 column
+__device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, double ct, double st) {
+  double2 q[NJ];
+  const WarpHead& H = *W.h;
+#pragma unroll 1
+  for (int j = 0; j < C.n; ++j) q[j] = H.p0[j];
+  q[1] = crank_tip(H, C, ct, st);
+  W.p32(1) = make_float2((float)q[1].x, (float)q[1].y);
+  return dyads_f64(H, C, [&](int j) { return q[j]; },
+                   [&](int j, double2 v) {
+                     q[j] = v;
+                     W.p32(j) = make_float2((float)v.x, (float)v.y);
+                   });
+}
+
+// fp32 angle evaluation with f64 fix-up.  A lane whose dyad margin
+// M = min(ra + rb - d, d - |ra - rb|) (unit-box lengths) satisfies |M| < tau
+// at or before its first lock is replayed in f64, so every lock decision and
+// every position fed forward is either clear of fp32 error or f64-exact.
+__device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const double* __restrict__ cs, int t,
+                                       bool active, unsigned long long& n_fix) {
+  const WarpHead& H = *W.h;
+  int lk = -1;
+  bool fix = false;
+  double ct = 0.0, st = 0.0;
+  if (active) {
+    ct = cs[2 * t];
+    st = cs[2 * t + 1];
+    const double2 tip = crank_tip(H, C, ct, st);
+    W.p32(1) = make_float2((float)tip.x, (float)tip.y);
+    const float tau = C.tau;
+#pragma unroll 1
+    for (int s = 0; s < C.ns; ++s) {
+      const int a = H.ia[s], b = H.ib[s], tg = H.tg[s];
+      const float2 pa = W.p32(a);
+      const float2 pb = W.p32(b);
+      const float dx = pb.x - pa.x, dy = pb.y - pa.y;
+      const float d2 = fmaf(dy, dy, dx * dx);
+      if (!(d2 > 1e-16f)) {  // (near-)coincident joints: let f64 decide
+        fix = true;
+        lk = s;
+        break;
+      }
+      const float inv_d = rsqrtf(d2);
+      const float d = d2 * inv_d;
+      const float m = fminf(H.sp[s] - d, d - H.df[s]);
+      if (fabsf(m) < tau) fix = true;
+      if (m < 0.0f) {
+        lk = s;
+        break;
+      }
+      const float x = (d2 + H.c2[s]) * (0.5f * inv_d);
+      const float h2 = fmaxf(fmaf(-x, x, H.ra2[s]), 0.0f);
+      const float h = h2 > 0.0f ? h2 * rsqrtf(h2) : 0.0f;
+      const float ux = dx * inv_d, uy = dy * inv_d;
+      const float bh = H.br[s] * h;
+      W.p32(tg) = make_float2(fmaf(-bh, uy, fmaf(x, ux, pa.x)), fmaf(bh, ux, fmaf(x, uy, pa.y)));
+    }
+  }
+  if (__any_sync(FULL, fix)) {
+    if (fix) {
+      lk = replay_f64_local(W, C, ct, st);
+      ++n_fix;
+    }
+  }
+  return lk;
+}
+
+// f64 angle evaluation with positions in the warp's double2 column
+__device__ __forceinline__ int solve64(const Warp& W, const SimCtx& C, const double* __restrict__ cs, int t,
+                                       bool active) {
+  if (!active) return -1;
+  const WarpHead& H = *W.h;
+  W.p64(1) = crank_tip(H, C, cs[2 * t], cs[2 * t + 1]);
+  return dyads_f64(H, C, [&](int j) { return W.p64(j); }, [&](int j, double2 v) { W.p64(j) = v; });
+}
+
+__device__ __forceinline__ void fill_static32(const Warp& W, const SimCtx& C) {
+#pragma unroll 1
+  for (int j = 0; j < C.n; ++j)
+    if ((C.fixed >> j) & 1u) W.p32(j) = make_float2((float)W.h->p0[j].x, (float)W.h->p0[j].y);
+}
+
+__device__ __forceinline__ void fill_static64(const Warp& W, const SimCtx& C) {
+#pragma unroll 1
+  for (int j = 0; j < C.n; ++j)
+    if ((C.fixed >> j) & 1u) W.p64(j) = W.h->p0[j];
+}
+
+// first locking lane of a round -> (angle index within the round's list, step)
+struct RoundLock {
+  int src;
+  int step;
+};
+
+__device__ __forceinline__ RoundLock round_lock(bool active, int lk) {
+  const unsigned bal = __ballot_sync(FULL, active && lk >= 0);
+  if (!bal) return RoundLock{-1, -1};
+  const int src = __ffs(bal) - 1;
+  return RoundLock{src, __shfl_sync(FULL, lk, src)};
+}
+
+__device__ __forceinline__ int fine_angle(int i) { return (i / 3) * 4 + 1 + (i % 3); }
+
+template <bool WRITE, bool SCREEN64>
+__global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, int njmax) {
+  extern __shared__ __align__(16) unsigned char sim_smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const size_t per_warp = sizeof(WarpHead) + (size_t)njmax * 32 * sizeof(double2);
+  Warp W;
+  W.h = reinterpret_cast<WarpHead*>(sim_smem_raw + per_warp * w);
+  W.cols = sim_smem_raw + per_warp * w + sizeof(WarpHead);
+  W.lane = lane;
+  WarpHead& H = *W.h;
+  const long long nwarps = (long long)gridDim.x * SIM_WARPS;
+  const int T = p.T;
+  const bool coarse = !(p.flags & LA_SIM_NO_COARSE) && (T % 4 == 0) && T >= 8;
+  const bool gate_only = (p.flags & LA_SIM_GATE_ONLY) != 0;
+  unsigned long long n_fix = 0, n_angles = 0, n_dyads = 0, n_cand = 0;
+
+  const long long nitems = p.cand_count ? *p.cand_count : p.B;
+  for (long long item = (long long)blockIdx.x * SIM_WARPS + w; item < nitems; item += nwarps) {
+    const long long b = p.cand ? p.cand[item] : item;
+    const int g = p.topo ? p.topo[b] : 0;
+    const la_plan* pl = p.plans + g;
+    SimCtx C;
+    C.n = pl->n;
+    C.ns = pl->nsteps;
+    C.tau = p.fixup_tau;
+    C.fixed = pl->fixed_mask | 1u;  // joint 0 is static (solver.py:183)
+    if (C.n > njmax || C.n < 2 || C.ns > NS || C.ns < 0) {
+      // plan does not fit the launch (n > pos_stride): flag, do not touch smem
+      if (lane == 0) {
+        if (p.first_t) p.first_t[item] = -1;
+        if (p.first_joint) p.first_joint[item] = -2;
+      }
+      continue;
+    }
+    const double* P0 = p.pos0 + (size_t)b * p.pos_stride * 2;
+    __syncwarp();
+    if (lane < C.n) H.p0[lane] = make_double2(P0[2 * lane], P0[2 * lane + 1]);
+    if (lane < C.ns) {
+      H.tg[lane] = pl->step[lane][0];
+      H.ia[lane] = pl->step[lane][1];
+      H.ib[lane] = pl->step[lane][2];
+    }
+    __syncwarp();
+    if (lane < C.ns) {
+      // plan_geometry (solver.py:105-120), f64
+      const double2 pa = H.p0[H.ia[lane]], pb = H.p0[H.ib[lane]], pt = H.p0[H.tg[lane]];
+      const double ra = hypot(dsub(pt.x, pa.x), dsub(pt.y, pa.y));
+      const double rb = hypot(dsub(pt.x, pb.x), dsub(pt.y, pb.y));
+      const double cross = dsub(dmul(dsub(pb.x, pa.x), dsub(pt.y, pa.y)),
+                                dmul(dsub(pb.y, pa.y), dsub(pt.x, pa.x)));
+      const double br = cross >= 0.0 ? 1.0 : -1.0;
+      H.dra[lane] = ra;
+      H.drb[lane] = rb;
+      H.dbr[lane] = br;
+      const float fra = (float)ra, frb = (float)rb;
+      H.sp[lane] = (float)(ra + rb);
+      H.df[lane] = (float)fabs(ra - rb);
+      H.c2[lane] = (float)(ra * ra - rb * rb);
+      H.ra2[lane] = fra * fra;
+      H.br[lane] = (float)br;
+    }
+    C.r1 = hypot(dsub(H.p0[1].x, H.p0[0].x), dsub(H.p0[1].y, H.p0[0].y));
+    __syncwarp();
+    if (SCREEN64) fill_static64(W, C);
+    else fill_static32(W, C);
+    __syncwarp();
+
+    auto screen = [&](int t, bool act) -> int {
+      if (SCREEN64) return solve64(W, C, p.crank_cs, t, act);
+      return solve32(W, C, p.crank_cs, t, act, n_fix);
+    };
+
+    int first_t = T, first_j = -1, low_t = -1, low_j = -1;
+    bool locked = false;
+    int rounds = 0;
+    if (coarse) {
+      const int Tc = T / 4;
+#pragma unroll 1
+      for (int r = 0; r * 32 < Tc; ++r) {
+        const int i = r * 32 + lane;
+        const bool act = i < Tc;
+        const int lk = screen(4 * i, act);
+        ++rounds;
+        const RoundLock L = round_lock(act, lk);
+        if (L.src >= 0) {
+          low_t = r * 32 + L.src;
+          low_j = H.tg[L.step];
+          locked = true;
+          break;
+        }
+      }
+      if (locked) {
+        first_t = 4 * low_t;
+        first_j = low_j;
+        if (!gate_only) {
+          // exact first lock: fine angles below the coarse lock, ascending
+          const int nf = 3 * low_t;
+#pragma unroll 1
+          for (int r = 0; r * 32 < nf; ++r) {
+            const int i = r * 32 + lane;
+            const bool act = i < nf;
+            const int lk = screen(fine_angle(i), act);
+            ++rounds;
+            const RoundLock L = round_lock(act, lk);
+            if (L.src >= 0) {
+              first_t = fine_angle(r * 32 + L.src);
+              first_j = H.tg[L.step];
+              break;
+            }
+          }
+        }
+      }
+    }
+    if (!locked) {
+      if (WRITE) {
+        // all T angles in natural order, f64, coalesced float2 stores
+        if (!SCREEN64) {
+          __syncwarp();
+          fill_static64(W, C);
+        }
+        const long long row = p.traj_row ? p.traj_row[item] : item * (long long)p.traj_stride;
+        const bool out64 = (p.flags & LA_SIM_TRAJ_F64) != 0;
+        float2* out = reinterpret_cast<float2*>(p.traj) + (size_t)row * T;
+        double2* out_d = reinterpret_cast<double2*>(p.traj) + (size_t)row * T;
+#pragma unroll 1
+        for (int r = 0; r * 32 < T; ++r) {
+          const int t = r * 32 + lane;
+          const bool act = t < T;
+          const int lk = solve64(W, C, p.crank_cs, t, act);
+          ++rounds;
+          const RoundLock L = round_lock(act, lk);
+          if (L.src >= 0) {
+            first_t = r * 32 + L.src;
+            first_j = H.tg[L.step];
+            break;
+          }
+          if (act) {
+#pragma unroll 1
+            for (int j = 0; j < C.n; ++j) {
+              const double2 v = W.p64(j);
+              if (out64) __stcs(out_d + (size_t)j * T + t, v);
+              else st_cs(out + (size_t)j * T + t, make_float2((float)v.x, (float)v.y));
+            }
+          }
+        }
+      } else {
+        const int nf = coarse ? 3 * (T / 4) : T;
+#pragma unroll 1
+        for (int r = 0; r * 32 < nf; ++r) {
+          const int i = r * 32 + lane;
+          const bool act = i < nf;
+          const int t = coarse ? fine_angle(i) : i;
+          const int lk = screen(t, act);
+          ++rounds;
+          const RoundLock L = round_lock(act, lk);
+          if (L.src >= 0) {
+            const int is = r * 32 + L.src;
+            first_t = coarse ? fine_angle(is) : is;
+            first_j = H.tg[L.step];
+            break;
+          }
+        }
+      }
+    }
+    if (lane == 0) {
+      if (p.first_t) p.first_t[item] = first_t;
+      if (p.first_joint) p.first_joint[item] = first_j;
+      if (p.low_t) p.low_t[item] = low_t;
+      if (p.low_joint) p.low_joint[item] = low_j;
+    }
+    n_angles += 32ull * rounds;
+    n_dyads += 32ull * rounds * (unsigned long long)C.ns;
+    ++n_cand;
+  }
+  if (p.counters) {
+    unsigned long long f = n_fix;
+    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(FULL, f, o);
+    if (lane == 0) {
+      atomicAdd(p.counters + 0, f);
+      atomicAdd(p.counters + 1, n_angles);
+      atomicAdd(p.counters + 2, n_dyads);
+      atomicAdd(p.counters + 3, n_cand);
+    }
+  }
+}
+
+__global__ void geometry_kernel(const double* __restrict__ pos0, const int32_t* __restrict__ topo,
+                                const la_plan* __restrict__ plans, int64_t B, int32_t pos_stride,
+                                double* r_a, double* r_b, double* branch) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * NS) return;
+  const long long b = i / NS;
+  const int s = (int)(i % NS);
+  const la_plan* pl = plans + (topo ? topo[b] : 0);
+  double ra = 0.0, rb = 0.0, br = 0.0;
+  if (s < pl->nsteps) {
+    const double* P = pos0 + (size_t)b * pos_stride * 2;
+    const int t = pl->step[s][0], a = pl->step[s][1], c = pl->step[s][2];
+    const double ax = P[2 * a], ay = P[2 * a + 1], bx = P[2 * c], by = P[2 * c + 1];
+    const double tx = P[2 * t], ty = P[2 * t + 1];
+    ra = hypot(dsub(tx, ax), dsub(ty, ay));
+    rb = hypot(dsub(tx, bx), dsub(ty, by));
+    const double cross = dsub(dmul(dsub(bx, ax), dsub(ty, ay)), dmul(dsub(by, ay), dsub(tx, ax)));
+    br = cross >= 0.0 ? 1.0 : -1.0;
+  }
+  r_a[i] = ra;
+  r_b[i] = rb;
+  branch[i] = br;
+}
+
+__global__ void dyad_kernel(const double* __restrict__ pa, const double* __restrict__ pb,
+                            const double* __restrict__ ra_, const double* __restrict__ rb_,
+                            const double* __restrict__ br_, int64_t n, double* out, int32_t* ok) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double dx = dsub(pb[2 * i], pa[2 * i]);
+  const double dy = dsub(pb[2 * i + 1], pa[2 * i + 1]);
+  const double d = hypot(dx, dy);
+  const double ra = ra_[i], rb = rb_[i];
+  const double eps = 1e-9;
+  if (d < eps || d > dadd(dadd(ra, rb), eps) || d < dsub(fabs(dsub(ra, rb)), eps)) {
+    ok[i] = 0;
+    out[2 * i] = __longlong_as_double(0x7ff8000000000000ll);
+    out[2 * i + 1] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  const double x = ddiv(dsub(dadd(dmul(d, d), dmul(ra, ra)), dmul(rb, rb)), dmul(2.0, d));
+  const double h = __dsqrt_rn(fmax(dsub(dmul(ra, ra), dmul(x, x)), 0.0));
+  const double ux = ddiv(dx, d), uy = ddiv(dy, d);
+  const double bh = dmul(br_[i], h);
+  // dyad_solve (solver.py:139): p_a + x*u - branch*h*u_perp, evaluated as
+  // (pa + x*ux) - (branch*h)*uy  /  (pa + x*uy) + (branch*h)*ux
+  out[2 * i] = dsub(dadd(pa[2 * i], dmul(x, ux)), dmul(bh, uy));
+  out[2 * i + 1] = dadd(dadd(pa[2 * i + 1], dmul(x, uy)), dmul(bh, ux));
+  ok[i] = 1;
+}
+
+// ---------------------------------------------------------------- compaction
+constexpr int CP_THREADS = 1024;  // one tile = 1024 candidates
+
+__global__ void compact_count(const int32_t* __restrict__ first_t, int64_t B, int32_t T,
+                              int32_t* tile_count) {
+  const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
+  const bool v = i < B && first_t[i] == T;
+  const unsigned bal = __ballot_sync(FULL, v);
+  __shared__ int wsum[CP_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int s = wsum[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (threadIdx.x == 0) tile_count[blockIdx.x] = s;
+  }
+}
+
+// single-block exclusive scan over tile counts (tiles <= a few 10^5)
+__global__ void compact_scan(int32_t* tile_count, long long ntiles, int64_t* total) {
+  __shared__ long long carry;
+  __shared__ long long wsum[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (long long base = 0; base < ntiles; base += 1024) {
+    const long long i = base + threadIdx.x;
+    long long v = i < ntiles ? tile_count[i] : 0;
+    // inclusive warp scan
+    long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(FULL, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      long long s = wsum[threadIdx.x];
+      for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(FULL, s, o);
+        if (threadIdx.x >= o) s += y;
+      }
+      wsum[threadIdx.x] = s;
+    }
+    __syncthreads();
+    const long long wbase = (threadIdx.x >= 32) ? wsum[(threadIdx.x >> 5) - 1] : 0;
+    const long long excl = carry + wbase + x - v;
+    __syncthreads();
+    if (i < ntiles) tile_count[i] = (int32_t)excl;  // offsets fit: B < 2^31 per launch
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void compact_scatter(const int32_t* __restrict__ first_t, int64_t B, int32_t T,
+                                const int32_t* __restrict__ tile_off, int64_t* out) {
+  const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
+  const bool v = i < B && first_t[i] == T;
+  const unsigned bal = __ballot_sync(FULL, v);
+  __shared__ int wsum[CP_THREADS / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) wsum[w] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int s = wsum[lane];
+    int x = s;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    wsum[lane] = x - s;
+  }
+  __syncthreads();
+  if (v) {
+    const long long pos = (long long)tile_off[blockIdx.x] + wsum[w] + __popc(bal & ((1u << lane) - 1u));
+    out[pos] = i;
+  }
+}
+
+}  // namespace
+}  // namespace la
+
+using namespace la;
+
+extern "C" {
+
+int la_simulate(const la_sim_args* a, void* stream) {
+  if (!a) return fail(LA_EINVAL, "la_simulate: null args");
+  if (a->B < 0 || a->G < 1 || a->T < 1 || a->T > 1000000)
+    return fail(LA_EINVAL, "la_simulate: bad sizes B=%lld G=%d T=%d", (long long)a->B, a->G, a->T);
+  if (a->pos_stride < 2 || a->pos_stride > 4096) return fail(LA_EINVAL, "la_simulate: bad pos_stride");
+  if (!a->pos0 || !a->plans || !a->crank_cs) return fail(LA_EINVAL, "la_simulate: null buffer");
+  if (!a->cand && (!a->first_t || !a->first_joint)) return fail(LA_EINVAL, "la_simulate: null outputs");
+  if (a->cand_count && !a->cand) return fail(LA_EINVAL, "la_simulate: cand_count without cand");
+  const bool write = (a->flags & LA_SIM_WRITE_TRAJ) != 0;
+  if (write && !a->traj) return fail(LA_EINVAL, "la_simulate: WRITE_TRAJ without traj");
+  if (a->B == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool f64 = (a->flags & LA_SIM_FP64) != 0;
+  const int njmax = a->pos_stride < NJ ? a->pos_stride : NJ;
+  const size_t smem = (sizeof(WarpHead) + (size_t)njmax * 32 * sizeof(double2)) * SIM_WARPS;
+  auto kern = write ? (f64 ? sim_kernel<true, true> : sim_kernel<true, false>)
+                    : (f64 ? sim_kernel<false, true> : sim_kernel<false, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail((int)e, "la_simulate: smem attr: %s", cudaGetErrorString(e));
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SIM_THREADS, smem);
+  if (e != cudaSuccess) return fail((int)e, "la_simulate: occupancy: %s", cudaGetErrorString(e));
+  const int sms = sm_count();
+  if (sms <= 0) return fail(LA_EINVAL, "la_simulate: no device");
+  long long want = (a->B + SIM_WARPS - 1) / SIM_WARPS;
+  long long grid = (long long)sms * (occ > 0 ? occ : 1);
+  if (grid > want) grid = want;
+  const la_sim_args p = *a;
+  kern<<<(unsigned)grid, SIM_THREADS, smem, s>>>(p, njmax);
+  return cuda_status("la_simulate");
+}
+
+int la_plan_geometry(const double* pos0, const int32_t* topo, const la_plan* plans, int64_t B,
+                     int32_t G, int32_t pos_stride, double* r_a, double* r_b, double* branch,
+                     void* stream) {
+  if (B < 0 || G < 1 || !pos0 || !plans || !r_a || !r_b || !branch)
+    return fail(LA_EINVAL, "la_plan_geometry: bad args");
+  if (B == 0) return 0;
+  const long long n = B * NS;
+  geometry_kernel<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      pos0, topo, plans, B, pos_stride, r_a, r_b, branch);
+  return cuda_status("la_plan_geometry");
+}
+
+int la_dyad_solve(const double* pa, const double* pb, const double* r_a, const double* r_b,
+                  const double* branch, int64_t n, double* out, int32_t* ok, void* stream) {
+  if (n < 0 || !pa || !pb || !r_a || !r_b || !branch || !out || !ok)
+    return fail(LA_EINVAL, "la_dyad_solve: bad args");
+  if (n == 0) return 0;
+  dyad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      pa, pb, r_a, r_b, branch, n, out, ok);
+  return cuda_status("la_dyad_solve");
+}
+
+size_t la_compact_workspace(int64_t B) {
+  const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
+  return (size_t)(tiles > 0 ? tiles : 1) * sizeof(int32_t);
+}
+
+int la_compact_valid(const int32_t* first_t, int64_t B, int32_t T, int64_t* valid_idx,
+                     int64_t* valid_count, void* ws, size_t ws_bytes, void* stream) {
+  if (B < 0 || B >= (1ll << 31) || !first_t || !valid_idx || !valid_count)
+    return fail(LA_EINVAL, "la_compact_valid: bad args");
+  if (ws_bytes < la_compact_workspace(B) || !ws) return fail(LA_EWS, "la_compact_valid: workspace");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (B == 0) {
+    cudaMemsetAsync(valid_count, 0, sizeof(int64_t), s);
+    return cuda_status("la_compact_valid");
+  }
+  const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
+  int32_t* tc = static_cast<int32_t*>(ws);
+  compact_count<<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, tc);
+  compact_scan<<<1, 1024, 0, s>>>(tc, tiles, valid_count);
+  compact_scatter<<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, tc, valid_idx);
+  return cuda_status("la_compact_valid");
+}
+
+}  // extern "C"

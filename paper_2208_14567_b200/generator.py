@@ -1,0 +1,272 @@
+"""Rejection-sampling driver around the GPU validity screen.
+
+Reference: linkatlas generator.py.  Topology growth and candidate-pose
+sampling (generator.py:156-238) are host code that consume numpy PCG64
+streams exactly as the reference does, so seeded runs produce the same
+topologies and poses.  The two-fidelity gate inside ``find_valid_variant``
+(generator.py:241-283: T_low = 50 sweep, survivors confirmed at T_high =
+200) runs on the device: one coarse-first ``la_simulate`` launch screens a
+whole look-ahead window of candidate batches, and the host walks the flags
+in stream order to reproduce ``attempts`` and the negative-sample draws bit
+for bit.  The pose stream is drawn ahead and rewound so the caller's RNG
+ends in the same state as after the reference loop.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2208_14567_b200 import _native as N
+from paper_2208_14567_b200.curves import plan_ancestry
+from paper_2208_14567_b200.mechanism import ARM_PIVOT, ARM_TIP, JointType, Mechanism, apply_Ng, apply_Ns, \
+    initial_mechanism
+from paper_2208_14567_b200.solver import PlanTable, SolutionPlan, Trajectory, compile_order, simulate_tensors
+
+
+class GenerationError(RuntimeError):
+    pass
+
+
+@dataclass
+class GenerationConfig:
+    """generator.py:31-57."""
+
+    count: int
+    n_min: int = 8
+    n_max: int = 20
+    ng_probability: float = 0.25
+    variants_per_topology: int = 5
+    T_low: int = 50
+    T_high: int = 200
+    max_attempts: int = 5000
+    seed: int = 0
+    workers: int = 1
+    negative_rate: float = 0.0
+    topology_retries: int = 1000
+    batch: int = 256
+
+    def __post_init__(self):
+        if self.n_min < 4:
+            raise ValueError("n_min must be >= 4")
+        if self.n_max < self.n_min:
+            raise ValueError("n_max < n_min")
+        if self.variants_per_topology < 1:
+            raise ValueError("variants_per_topology must be >= 1")
+        if not self.T_low < self.T_high:
+            raise ValueError("T_low must be < T_high")
+        if self.max_attempts < 1:
+            raise ValueError("max_attempts must be >= 1")
+
+
+@dataclass
+class GenerationStats:
+    """Mergeable tallies keyed by joint count (generator.py:60-131)."""
+
+    simulated_by_n: dict[int, int] = field(default_factory=dict)
+    accepted_by_n: dict[int, int] = field(default_factory=dict)
+    attempts_samples: dict[int, list[int]] = field(default_factory=dict)
+    topologies_discarded: int = 0
+
+    @property
+    def simulated(self) -> int:
+        return sum(self.simulated_by_n.values())
+
+    @property
+    def accepted(self) -> int:
+        return sum(self.accepted_by_n.values())
+
+    @property
+    def locking(self) -> int:
+        return self.simulated - self.accepted
+
+    def record_success(self, n: int, attempts: int) -> None:
+        self.simulated_by_n[n] = self.simulated_by_n.get(n, 0) + attempts
+        self.accepted_by_n[n] = self.accepted_by_n.get(n, 0) + 1
+        self.attempts_samples.setdefault(n, []).append(attempts)
+
+    def record_failure(self, n: int, attempts: int) -> None:
+        self.simulated_by_n[n] = self.simulated_by_n.get(n, 0) + attempts
+
+    def mean_attempts(self, n: int) -> float:
+        acc = self.accepted_by_n.get(n, 0)
+        return math.nan if acc == 0 else self.simulated_by_n.get(n, 0) / acc
+
+    def median_attempts(self, n: int) -> float:
+        s = self.attempts_samples.get(n, [])
+        return float(np.median(s)) if s else math.nan
+
+    def rejection_rate(self, n: int) -> float:
+        sim = self.simulated_by_n.get(n, 0)
+        return math.nan if sim == 0 else 1.0 - self.accepted_by_n.get(n, 0) / sim
+
+    def merge(self, other: "GenerationStats") -> None:
+        for n, v in other.simulated_by_n.items():
+            self.simulated_by_n[n] = self.simulated_by_n.get(n, 0) + v
+        for n, v in other.accepted_by_n.items():
+            self.accepted_by_n[n] = self.accepted_by_n.get(n, 0) + v
+        for n, v in other.attempts_samples.items():
+            self.attempts_samples.setdefault(n, []).extend(v)
+        self.topologies_discarded += other.topologies_discarded
+
+
+@dataclass
+class NegativeSample:
+    mechanism: Mechanism
+    locking_step: int
+
+
+@dataclass
+class VariantResult:
+    mechanism: Mechanism
+    trajectory: Trajectory
+    attempts: int
+
+
+# ------------------------------------------------------------ topology (host)
+def _grow_topology(rng: np.random.Generator, n: int, ng_probability: float) -> Mechanism | None:
+    """Terminal-tracking constrained growth (generator.py:156-197).
+
+    Consumes ``rng`` exactly like the reference: one ``random()`` per
+    operation while slack >= 2, one ``integers(len(pairs))`` per simple op.
+    """
+    mech = initial_mechanism()
+    terminals = {1, 2}
+    while mech.n < n:
+        left = n - mech.n
+        slack = left - len(terminals) + 1
+        if slack < 0:
+            return None
+        if slack >= 2 and rng.random() < ng_probability:
+            mech = apply_Ng(mech)
+            terminals.add(mech.n - 1)
+            continue
+        need = max(0, 2 - slack)
+        last_op = left == 1
+        is_fixed = mech.types == JointType.FIXED
+        cands = []
+        for i in range(mech.n):
+            for j in range(i + 1, mech.n):
+                if is_fixed[i] and is_fixed[j]:
+                    continue
+                if last_op and (is_fixed[i] or is_fixed[j]):
+                    continue
+                if (i in terminals) + (j in terminals) < need:
+                    continue
+                cands.append((i, j))
+        if not cands:
+            return None
+        i, j = cands[int(rng.integers(len(cands)))]
+        mech = apply_Ns(mech, i, j)
+        terminals.difference_update((i, j))
+        terminals.add(mech.n - 1)
+    return mech
+
+
+def _plan_of(mech: Mechanism) -> SolutionPlan:
+    fixed, steps = compile_order(mech.adjacency, mech.types)
+    return SolutionPlan(mech.n, fixed, steps, None, None, None)
+
+
+def sample_topology(rng: np.random.Generator, n: int, ng_probability: float = 0.25,
+                    retries: int = 1000) -> tuple[Mechanism, SolutionPlan]:
+    """Grow until the plan's last joint depends on every joint and rides no
+    ground pin (generator.py:200-222)."""
+    for _ in range(retries):
+        mech = _grow_topology(rng, n, ng_probability)
+        if mech is None:
+            continue
+        plan = _plan_of(mech)
+        if not plan.steps:
+            continue
+        last = plan.steps[-1].target
+        if np.any(mech.types[mech.neighbors(last)] == JointType.FIXED):
+            continue
+        if len(plan_ancestry(plan, last)) != n:
+            continue
+        return mech, plan
+    raise GenerationError(f"no valid topology with n={n} after {retries} tries")
+
+
+def sample_positions(topology: Mechanism, rng: np.random.Generator) -> np.ndarray:
+    """generator.py:225-231."""
+    pos = rng.uniform(size=(topology.n, 2))
+    pos[0] = ARM_PIVOT
+    pos[1] = ARM_TIP
+    return pos
+
+
+def _sample_positions_batch(n: int, k: int, rng: np.random.Generator) -> np.ndarray:
+    """generator.py:234-238."""
+    pos = rng.uniform(size=(k, n, 2))
+    pos[:, 0] = ARM_PIVOT
+    pos[:, 1] = ARM_TIP
+    return pos
+
+
+# ------------------------------------------------------------ GPU gate driver
+def find_valid_variant(topology: Mechanism, plan: SolutionPlan, rng: np.random.Generator,
+                       max_attempts: int = 5000, T_low: int = 50, T_high: int = 200, batch: int = 256,
+                       negative_rate: float = 0.0, neg_rng: np.random.Generator | None = None,
+                       negatives: list[NegativeSample] | None = None, lookahead: int = 16) -> VariantResult | None:
+    """Rejection-sample poses until one passes the two-fidelity gate
+    (generator.py:241-283); returns the accepted mechanism, its T_high
+    trajectory and the number of candidates consumed, or None at the cap."""
+    torch = N.require_cuda()
+    n = topology.n
+    table = PlanTable([plan])
+    fused = T_high == 4 * T_low
+    consumed = 0
+    while consumed < max_attempts:
+        # draw a look-ahead window of whole reference batches in one go
+        sizes = []
+        left = max_attempts - consumed
+        for _ in range(max(1, lookahead)):
+            if left <= 0:
+                break
+            sizes.append(min(batch, left))
+            left -= sizes[-1]
+        state = rng.bit_generator.state
+        chunks = [_sample_positions_batch(n, k, rng) for k in sizes]
+        cand = np.concatenate(chunks)
+        dpos = torch.from_numpy(cand).cuda()
+        if fused:
+            res = simulate_tensors(dpos, table, T_high, write_traj=False, low=True)
+            low_t = res["low_t"].cpu().numpy()
+            high_ok = res["first_t"].cpu().numpy() == T_high
+        else:
+            lo = simulate_tensors(dpos, table, T_low, write_traj=False)
+            hi = simulate_tensors(dpos, table, T_high, write_traj=False)
+            ft = lo["first_t"].cpu().numpy()
+            low_t = np.where(ft < T_low, ft, -1)
+            high_ok = hi["first_t"].cpu().numpy() == T_high
+        base = 0
+        for bi, k in enumerate(sizes):
+            for idx in range(k):
+                g = base + idx
+                if low_t[g] >= 0:
+                    if negatives is not None and negative_rate > 0.0 and neg_rng is not None:
+                        if neg_rng.random() < negative_rate:
+                            negatives.append(NegativeSample(topology.with_positions(cand[g]), int(low_t[g])))
+                    continue
+                if not high_ok[g]:
+                    continue
+                # success: rewind the pose stream to the end of this batch
+                rng.bit_generator.state = state
+                for kk in sizes[:bi + 1]:
+                    _sample_positions_batch(n, kk, rng)
+                traj = _trajectory(cand[g], table, T_high)
+                return VariantResult(mechanism=topology.with_positions(cand[g]), trajectory=traj,
+                                     attempts=consumed + idx + 1)
+            consumed += k
+            base += k
+    return None
+
+
+def _trajectory(pos: np.ndarray, table: PlanTable, T: int) -> Trajectory:
+    torch = N.require_cuda()
+    dpos = torch.from_numpy(np.ascontiguousarray(pos[None])).cuda()
+    res = simulate_tensors(dpos, table, T, write_traj=True, traj_stride=pos.shape[0], traj_f64=True)
+    return Trajectory(res["traj"].view(pos.shape[0], T, 2).cpu().numpy())

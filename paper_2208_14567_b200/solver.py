@@ -1,0 +1,410 @@
+"""Drop-in solver API backed by the sm_100a simulation kernel.
+
+Reference: linkatlas solver.py.  The signatures, result types and error
+behaviour of ``compile_plan``, ``plan_geometry``, ``dyad_solve``,
+``simulate``, ``simulate_batch`` and ``check_feasible`` are kept; the numpy
+bodies (solver.py:105-249) are replaced by ``la_simulate`` /
+``la_plan_geometry`` / ``la_dyad_solve`` (include/links_b200.h).  The
+topology walk of ``compile_plan`` (solver.py:71-102) stays host code: it is
+integer work done once per topology, not per candidate.
+
+Tensor-level entry points (``PlanTable``, ``simulate_tensors``) serve mixed
+topologies in one launch and keep results on the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2208_14567_b200 import _native as N
+from paper_2208_14567_b200.mechanism import JointType, Mechanism
+
+LOCK_EPS = 1e-9                 # solver.py:19 (the kernels hard-code the same)
+DEFAULT_FIXUP_TAU = 2e-4        # f64 redo threshold on the dyad margin (unit-box lengths)
+
+
+class PlanError(ValueError):
+    """Topology not dyadically solvable or initial pose degenerate (solver.py:22)."""
+
+
+@dataclass(frozen=True)
+class PlanStep:
+    target: int
+    a: int
+    b: int
+
+
+@dataclass(frozen=True)
+class SolutionPlan:
+    n: int
+    fixed: tuple[int, ...]
+    steps: tuple[PlanStep, ...]
+    r_a: np.ndarray | None
+    r_b: np.ndarray | None
+    branch: np.ndarray | None
+
+    @property
+    def coverage(self) -> frozenset[int]:
+        return frozenset(self.fixed) | {1} | {s.target for s in self.steps}
+
+
+@dataclass(frozen=True)
+class Trajectory:
+    positions: np.ndarray  # (n, T, 2)
+
+    @property
+    def T(self) -> int:
+        return self.positions.shape[1]
+
+    @property
+    def n(self) -> int:
+        return self.positions.shape[0]
+
+
+@dataclass(frozen=True)
+class Locking:
+    step: int
+    joint: int
+
+
+SimOutcome = Trajectory | Locking
+
+
+# ------------------------------------------------------------ host: topology
+def compile_order(adjacency: np.ndarray, types: np.ndarray) -> tuple[tuple[int, ...], tuple[PlanStep, ...]]:
+    """The two-known-neighbours walk of solver.py:71-94 on the joint graph.
+
+    Seeds are every Fixed joint plus the crank tip; each pass scans unknown
+    joints in ascending order and a joint with >= 2 known neighbours joins
+    (with its first two known neighbours) immediately.  Raises PlanError on a
+    stall.
+    """
+    adj = np.asarray(adjacency)
+    n = adj.shape[0]
+    fixed = tuple(int(k) for k in np.flatnonzero(np.asarray(types) == JointType.FIXED))
+    known = np.zeros(n, dtype=bool)
+    known[list(fixed)] = True
+    if n > 1:
+        known[1] = True
+    todo = [k for k in range(n) if not known[k]]
+    nbrs = [np.flatnonzero(adj[k]) for k in range(n)]
+    steps: list[PlanStep] = []
+    while todo:
+        moved = False
+        rest = []
+        for k in todo:
+            kn = [int(v) for v in nbrs[k] if known[v]]
+            if len(kn) >= 2:
+                steps.append(PlanStep(k, kn[0], kn[1]))
+                known[k] = True
+                moved = True
+            else:
+                rest.append(k)
+        if not moved:
+            raise PlanError(f"not dyadically solvable: joints {sorted(rest)} unreachable")
+        todo = rest
+    return fixed, tuple(steps)
+
+
+def compile_plan(mech: Mechanism) -> SolutionPlan:
+    """Solve order + (when the pose is set) its geometry (solver.py:71-102).
+
+    The geometry is computed by ``la_plan_geometry`` on the device.
+    """
+    fixed, steps = compile_order(mech.adjacency, mech.types)
+    bare = SolutionPlan(mech.n, fixed, steps, None, None, None)
+    if np.isnan(mech.positions0).any():
+        return bare
+    r_a, r_b, branch = plan_geometry(bare, mech.positions0)
+    if np.any((r_a < LOCK_EPS) | (r_b < LOCK_EPS)):
+        raise PlanError("degenerate branch: zero-length bar at initial pose")
+    return SolutionPlan(mech.n, fixed, steps, r_a, r_b, branch)
+
+
+# ------------------------------------------------------------ plan tables
+def _pack_plan(plan: SolutionPlan) -> bytes:
+    if plan.n > N.LA_MAX_JOINTS:
+        raise ValueError(f"mechanisms up to {N.LA_MAX_JOINTS} joints are supported (got {plan.n})")
+    if len(plan.steps) > N.LA_MAX_STEPS:
+        raise ValueError(f"plans up to {N.LA_MAX_STEPS} dyad steps are supported")
+    rec = N.LaPlan()
+    rec.n = plan.n
+    rec.nsteps = len(plan.steps)
+    mask = 0
+    for j in plan.fixed:
+        mask |= 1 << int(j)
+    rec.fixed_mask = mask
+    for s, st in enumerate(plan.steps):
+        rec.step[s][0], rec.step[s][1], rec.step[s][2] = st.target, st.a, st.b
+    return bytes(rec)
+
+
+@dataclass
+class PlanTable:
+    """Device-resident array of compiled plans (la_plan records, 64 B each)."""
+
+    plans: list[SolutionPlan]
+    device: object = None
+    _dev: object = field(default=None, repr=False)
+
+    @property
+    def G(self) -> int:
+        return len(self.plans)
+
+    @property
+    def max_n(self) -> int:
+        return max(p.n for p in self.plans)
+
+    def host_bytes(self) -> np.ndarray:
+        return np.frombuffer(b"".join(_pack_plan(p) for p in self.plans), dtype=np.uint8)
+
+    def tensor(self):
+        torch = N.require_cuda()
+        if self._dev is None:
+            dev = self.device if self.device is not None else torch.device("cuda")
+            self._dev = torch.from_numpy(self.host_bytes().copy()).to(dev)
+        return self._dev
+
+
+_CRANK: dict = {}
+
+
+def crank_table(T: int, device=None):
+    """cos/sin of theta_t = 2*pi*t/T exactly as solver.py:156-158 computes
+    them (numpy f64), interleaved [T][2] on the device (cached)."""
+    torch = N.require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = (int(T), str(dev))
+    t = _CRANK.get(key)
+    if t is None:
+        th = 2.0 * np.pi * np.arange(T) / T
+        cs = np.stack([np.cos(th), np.sin(th)], axis=1)
+        t = torch.from_numpy(np.ascontiguousarray(cs)).to(dev)
+        _CRANK[key] = t
+    return t
+
+
+# ------------------------------------------------------------ device entry
+def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_traj: bool = True,
+                     traj=None, traj_stride: int | None = None, traj_row=None, low: bool = False,
+                     traj_f64: bool = False, cand=None, cand_count=None,
+                     fixup_tau: float = DEFAULT_FIXUP_TAU, fp64: bool = False, gate_only: bool = False,
+                     coarse: bool = True, counters=None, stream=None) -> dict:
+    """Launch la_simulate on device tensors.
+
+    pos0: (B, S, 2) float64 CUDA tensor (S >= every plan's n); topo: (B,)
+    int32 plan indices or None (all plan 0).  Returns a dict with
+    ``first_t`` / ``first_joint`` (int32, (B,)), ``traj`` ((rows, T, 2)
+    float32 — float64 with ``traj_f64`` — when written) and ``low_t`` /
+    ``low_joint`` when ``low``.  ``cand`` (int64 device indices, optional
+    device count ``cand_count``) gathers the work items; outputs are then
+    indexed by work item.
+    """
+    torch = N.require_cuda()
+    lib = N.load()
+    if pos0.dtype != torch.float64 or not pos0.is_cuda or pos0.dim() != 3 or pos0.shape[2] != 2:
+        raise ValueError("pos0 must be a (B, S, 2) float64 CUDA tensor")
+    pos0 = pos0.contiguous()
+    B, S, _ = pos0.shape
+    if S < table.max_n:
+        raise ValueError("pos0 row stride smaller than a plan's joint count")
+    dev = pos0.device
+    if topo is not None:
+        topo = topo.to(device=dev, dtype=torch.int32).contiguous()
+    ts = int(traj_stride if traj_stride is not None else table.max_n)
+    items = B if cand is None else cand.numel()
+    if cand is not None:
+        cand = cand.to(device=dev, dtype=torch.int64).contiguous()
+    out = {
+        "first_t": torch.empty(items, dtype=torch.int32, device=dev),
+        "first_joint": torch.empty(items, dtype=torch.int32, device=dev),
+    }
+    if write_traj:
+        if traj is None:
+            rows = items * ts if traj_row is None else None
+            if rows is None:
+                raise ValueError("traj_row requires an explicit traj buffer")
+            traj = torch.empty((rows, T, 2), dtype=torch.float64 if traj_f64 else torch.float32, device=dev)
+        elif traj.dtype != (torch.float64 if traj_f64 else torch.float32):
+            raise ValueError("traj dtype does not match traj_f64")
+        out["traj"] = traj
+    if low:
+        out["low_t"] = torch.empty(items, dtype=torch.int32, device=dev)
+        out["low_joint"] = torch.empty(items, dtype=torch.int32, device=dev)
+    flags = 0
+    if write_traj:
+        flags |= N.LA_SIM_WRITE_TRAJ
+    if fp64:
+        flags |= N.LA_SIM_FP64
+    if gate_only:
+        flags |= N.LA_SIM_GATE_ONLY
+    if not coarse:
+        flags |= N.LA_SIM_NO_COARSE
+    if traj_f64:
+        flags |= N.LA_SIM_TRAJ_F64
+    a = N.LaSimArgs()
+    a.pos0 = pos0.data_ptr()
+    a.topo = N.ptr(topo)
+    a.plans = table.tensor().data_ptr()
+    a.crank_cs = crank_table(T, dev).data_ptr()
+    a.B, a.G, a.pos_stride, a.T, a.traj_stride = B, table.G, S, T, ts
+    a.traj = N.ptr(out.get("traj"))
+    a.traj_row = N.ptr(traj_row)
+    a.cand = N.ptr(cand)
+    a.cand_count = N.ptr(cand_count)
+    a.first_t = out["first_t"].data_ptr()
+    a.first_joint = out["first_joint"].data_ptr()
+    a.low_t = N.ptr(out.get("low_t"))
+    a.low_joint = N.ptr(out.get("low_joint"))
+    a.counters = N.ptr(counters)
+    a.fixup_tau = float(fixup_tau)
+    a.flags = flags
+    N.check(lib.la_simulate(a, N.stream_ptr(stream)), "la_simulate")
+    return out
+
+
+def compact_valid(first_t, T: int, stream=None):
+    """Ascending indices of candidates with first_t == T (la_compact_valid)."""
+    torch = N.require_cuda()
+    lib = N.load()
+    B = first_t.numel()
+    idx = torch.empty(max(B, 1), dtype=torch.int64, device=first_t.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=first_t.device)
+    wsb = int(lib.la_compact_workspace(B))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=first_t.device)
+    N.check(lib.la_compact_valid(first_t.data_ptr(), B, T, idx.data_ptr(), cnt.data_ptr(),
+                                 ws.data_ptr(), wsb, N.stream_ptr(stream)), "la_compact_valid")
+    return idx, cnt
+
+
+def simulate_compact(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None, traj_f64: bool = False,
+                     fixup_tau: float = DEFAULT_FIXUP_TAU, stream=None) -> dict:
+    """Batch simulation with compacted output, all on device, no host sync.
+
+    1. screen every candidate (fp32 + f64 fix-up, coarse-first, exact
+       first lock) -> first_t / first_joint;
+    2. ordered compaction of the valid ones (la_compact_valid);
+    3. replay only the valid candidates in f64 over all T angles, writing
+       their paths densely: valid candidate v occupies rows
+       [v * stride, (v + 1) * stride) of ``traj``.
+
+    Returns first_t, first_joint (B,), valid_idx (B,) int64 (first
+    ``valid_count`` entries meaningful), valid_count (1,) int64 (device) and
+    traj ((B * stride, T, 2) worst-case buffer).
+    """
+    torch = N.require_cuda()
+    B, S, _ = pos0.shape
+    stride = table.max_n
+    res = simulate_tensors(pos0, table, T, topo, write_traj=False, fixup_tau=fixup_tau, stream=stream)
+    idx, cnt = compact_valid(res["first_t"], T, stream=stream)
+    if traj is None:
+        traj = torch.empty((max(B, 1) * stride, T, 2), dtype=torch.float64 if traj_f64 else torch.float32,
+                           device=pos0.device)
+    simulate_tensors(pos0, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, traj_f64=traj_f64,
+                     cand=idx, cand_count=cnt, coarse=False, fixup_tau=fixup_tau, stream=stream)
+    res.update(valid_idx=idx, valid_count=cnt, traj=traj, stride=stride)
+    return res
+
+
+# ------------------------------------------------------------ drop-in API
+def plan_geometry(plan: SolutionPlan, positions0: np.ndarray):
+    """Per-step r_a, r_b, branch for one pose (solver.py:105-120), on device."""
+    torch = N.require_cuda()
+    lib = N.load()
+    pos = np.ascontiguousarray(np.asarray(positions0, dtype=np.float64))
+    S = len(plan.steps)
+    if S == 0:
+        e = np.zeros(0)
+        return e, e.copy(), e.copy()
+    table = PlanTable([plan])
+    dpos = torch.from_numpy(pos.reshape(1, -1, 2)).cuda()
+    outs = [torch.empty((1, N.LA_MAX_STEPS), dtype=torch.float64, device=dpos.device) for _ in range(3)]
+    N.check(lib.la_plan_geometry(dpos.data_ptr(), None, table.tensor().data_ptr(), 1, 1, pos.shape[0],
+                                 outs[0].data_ptr(), outs[1].data_ptr(), outs[2].data_ptr(),
+                                 N.stream_ptr()), "la_plan_geometry")
+    r_a, r_b, br = (o[0, :S].cpu().numpy() for o in outs)
+    return r_a, r_b, br
+
+
+def dyad_solve(p_a, p_b, r_a: float, r_b: float, branch: float):
+    """Circle-circle intersection (solver.py:123-139) via la_dyad_solve.
+
+    Returns an (x, y) tuple or None when the circles do not meet.
+    """
+    torch = N.require_cuda()
+    lib = N.load()
+    dev = torch.device("cuda")
+    pa = torch.tensor([[float(p_a[0]), float(p_a[1])]], dtype=torch.float64, device=dev)
+    pb = torch.tensor([[float(p_b[0]), float(p_b[1])]], dtype=torch.float64, device=dev)
+    ra = torch.tensor([float(r_a)], dtype=torch.float64, device=dev)
+    rb = torch.tensor([float(r_b)], dtype=torch.float64, device=dev)
+    br = torch.tensor([float(branch)], dtype=torch.float64, device=dev)
+    out = torch.empty((1, 2), dtype=torch.float64, device=dev)
+    ok = torch.empty(1, dtype=torch.int32, device=dev)
+    N.check(lib.la_dyad_solve(pa.data_ptr(), pb.data_ptr(), ra.data_ptr(), rb.data_ptr(), br.data_ptr(), 1,
+                              out.data_ptr(), ok.data_ptr(), N.stream_ptr()), "la_dyad_solve")
+    if int(ok.item()) == 0:
+        return None
+    o = out.cpu().numpy()[0]
+    return (float(o[0]), float(o[1]))
+
+
+def _outcomes(res: dict, T: int, n: int) -> list[SimOutcome]:
+    ft = res["first_t"].cpu().numpy()
+    fj = res["first_joint"].cpu().numpy()
+    traj = res.get("traj")
+    P = None
+    if traj is not None and (ft == T).any():
+        P = traj.view(-1, n, T, 2).cpu().numpy().astype(np.float64, copy=False)
+    outs: list[SimOutcome] = []
+    for b in range(len(ft)):
+        if ft[b] < T:
+            outs.append(Locking(step=int(ft[b]), joint=int(fj[b])))
+        else:
+            outs.append(Trajectory(P[b]))
+    return outs
+
+
+def simulate_batch(positions0_batch: np.ndarray, plan: SolutionPlan, T: int = 200, *,
+                   fixup_tau: float = DEFAULT_FIXUP_TAU) -> list[SimOutcome]:
+    """Replay one plan over a batch of poses (solver.py:172-239) on the GPU.
+
+    Trajectories are computed in f64 on the device in the reference's
+    operation order and returned as (n, T, 2) float64 arrays; lock flags
+    follow the reference rule (fp32 screen with f64 replay near any lock).
+    """
+    torch = N.require_cuda()
+    pos = np.asarray(positions0_batch, dtype=np.float64)
+    if pos.ndim != 3 or pos.shape[2] != 2:
+        raise ValueError("positions0_batch must be (B, n, 2)")
+    B, n, _ = pos.shape
+    if B == 0:
+        return []
+    dpos = torch.from_numpy(np.ascontiguousarray(pos)).cuda()
+    res = simulate_tensors(dpos, PlanTable([plan]), T, write_traj=True, traj_stride=n, fixup_tau=fixup_tau,
+                           traj_f64=True)
+    return _outcomes(res, T, n)
+
+
+def simulate(mech: Mechanism, plan: SolutionPlan, T: int = 200) -> SimOutcome:
+    """Single-mechanism replay (solver.py:142-169): a batch of one."""
+    return simulate_batch(mech.positions0[None, :, :], plan, T)[0]
+
+
+def check_feasible(mech: Mechanism, plan: SolutionPlan, T_low: int = 50, T_high: int = 200) -> bool:
+    """Two-fidelity gate (solver.py:242-249): T_low sweep, then T_high."""
+    torch = N.require_cuda()
+    dpos = torch.from_numpy(np.ascontiguousarray(mech.positions0[None, :, :], dtype=np.float64)).cuda()
+    table = PlanTable([plan])
+    if T_high == 4 * T_low:
+        # the T_low angles are every 4th T_high angle (bit-identical thetas):
+        # one coarse-first launch answers both sweeps
+        res = simulate_tensors(dpos, table, T_high, write_traj=False, low=True)
+        return bool(int(res["low_t"].item()) < 0 and int(res["first_t"].item()) == T_high)
+    lo = simulate_tensors(dpos, table, T_low, write_traj=False)
+    if int(lo["first_t"].item()) < T_low:
+        return False
+    hi = simulate_tensors(dpos, table, T_high, write_traj=False)
+    return int(hi["first_t"].item()) == T_high

@@ -23,3 +23,11 @@ def golden():
         return dict(np.load(os.path.join(GOLDEN, name), allow_pickle=False))
 
     return load
+
+
+def pytest_sessionstart(session):
+    # build the in-tree CUDA library if it is missing or older than its sources
+    from paper_2208_14567_b200 import build_lib
+
+    if build_lib.needs_build():
+        build_lib.build()

@@ -1,0 +1,155 @@
+"""GPU parity of the chamfer scan / retrieval against the reference atlas
+fixture and the oracle; chamfer tolerance 1e-4 x bbox diagonal, top-k ids
+equal except swaps between entries whose f64 distances differ by less than
+that tolerance."""
+
+import numpy as np
+import pytest
+
+from oracle import links_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def atlas_fx(golden):
+    from paper_2208_14567_b200 import Atlas
+    from paper_2208_14567_b200.workloads import four_bar
+
+    g = golden("atlas_golden.npz")
+    N = len(g["points"])
+    mechs = {i: four_bar() for i in range(N)}
+    atlas = Atlas(g["points"], np.arange(N), np.full(N, 3), mechs, seed=int(g["seed"]))
+    return g, atlas
+
+
+def ids_match(got_ids, got_d, want_ids, ref_d, tol=TOL):
+    """Equal ids, allowing swaps among entries within tol of each other."""
+    if len(got_ids) != len(want_ids):
+        return False
+    for a, b in zip(got_ids, want_ids):
+        if a != b and abs(ref_d[a] - ref_d[b]) >= tol:
+            return False
+    return True
+
+
+def test_order_and_exact_index(torch, atlas_fx):
+    g, atlas = atlas_fx
+    assert np.array_equal(atlas.order, g["order"])
+    assert atlas.exact_index(g["points"][17]) == 17
+    assert atlas.exact_index(g["query1"]) is None
+
+
+def test_retrieve_matches_reference(torch, atlas_fx):
+    g, atlas = atlas_fx
+    hits = g["hits"]
+    for qi in range(4):
+        q = g[f"query{qi}"]
+        ref_d = O.chamfer_direct_block(g["points"], q) if q.shape == g["points"].shape[1:] else \
+            np.array([O.chamfer(q, p) for p in g["points"]])
+        for ci, (k, thr) in enumerate(zip(g["cases_k"], g["cases_thr"])):
+            want = hits[(hits[:, 0] == qi) & (hits[:, 1] == ci)]
+            got = atlas.retrieve(q, k=int(k), threshold=float(thr))
+            gid = [h.mech_id for h in got]
+            wid = want[:, 3].astype(int).tolist()
+            assert ids_match(gid, [h.distance for h in got], wid, ref_d), (qi, ci, gid, wid)
+            for h, w in zip(got, want):
+                assert abs(h.distance - w[4]) <= TOL
+                if abs(ref_d[h.mech_id] - thr) > TOL:
+                    assert h.above_threshold == bool(w[5])
+                assert h.mechanism.n <= 4
+    # self retrieval: exact 0.0 and not above threshold
+    for i in [0, 200, 399]:
+        h = atlas.retrieve(g["points"][i], k=1)
+        assert h[0].distance == 0.0 and h[0].mech_id == i and not h[0].above_threshold
+
+
+def test_brute_force_ordering(torch, atlas_fx):
+    g, atlas = atlas_fx
+    q = g["query1"]
+    full = atlas.retrieve(q, k=len(atlas), threshold=np.inf)
+    ref_d = O.chamfer_direct_block(g["points"], q)
+    got = [h.mech_id for h in full]
+    assert ids_match(got, None, g["brute_ids"].tolist(), ref_d)
+    assert np.max(np.abs(np.array([h.distance for h in full]) - g["brute_d"])) <= TOL
+
+
+def test_empty_and_padding(torch):
+    from paper_2208_14567_b200 import Atlas
+
+    a = Atlas(np.zeros((0, 0, 2)), np.zeros(0), np.zeros(0), {}, seed=0)
+    assert a.retrieve(np.array([[0.0, 0.0], [1.0, 0.0]])) == []
+
+
+def test_scan_topk_vs_oracle_large(torch):
+    """Exhaustive top-10 over 200k Fourier curves (C4 shape) vs the oracle
+    distances of the same fp32-stored curves."""
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_curves_device, fourier_db
+
+    N, P = 200_000, 200
+    db = fourier_db(N, P, seed=5, chunk=1 << 16)
+    q = fourier_db(1, P, seed=77)[0]
+    res = chamfer_scan(db, q[None], k=10, threshold=0.0, dense=True)
+    torch.cuda.synchronize()
+    dense = res["all_d"][0].cpu().numpy()
+    top_id = res["top_id"][0].cpu().numpy()
+    top_d = res["top_d"][0].cpu().numpy()
+    # top list equals the ordering of the dense distances
+    want = np.lexsort((np.arange(N), dense))[:10]
+    assert np.array_equal(top_id, want)
+    assert np.array_equal(top_d, dense[want])
+    # oracle on a subset: the top-10 plus 2000 random records
+    dbh = db.cpu().numpy().astype(np.float64)
+    qh = q.cpu().numpy().astype(np.float64)
+    sub = np.unique(np.concatenate([want, np.random.default_rng(0).choice(N, 2000, replace=False)]))
+    ref = O.chamfer_direct_block(dbh[sub], qh)
+    assert np.max(np.abs(dense[sub] - ref)) <= TOL
+    assert int(res["n_hits"][0].item()) == 0
+
+
+def test_scan_threshold_mode_and_shards(torch):
+    """Threshold mode (first hits in scan order + padding) and the
+    shard decomposition used by the multi-GPU merge give the same answer
+    as one scan over everything."""
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.dist import local_scan_plan, merge_lists
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    N, P = 30_000, 64
+    db = fourier_db(N, P, seed=9, chunk=1 << 14)
+    qs = fourier_db(3, P, seed=10)
+    order = np.random.default_rng(4).permutation(N)
+    dorder = torch.from_numpy(order).cuda()
+    res = chamfer_scan(db, qs, k=7, threshold=0.25, order=dorder, dense=True)
+    dense = res["all_d"].cpu().numpy()
+    pos_of = np.empty(N, dtype=np.int64)
+    pos_of[order] = np.arange(N)
+    for qi in range(3):
+        d = dense[qi]
+        hit = np.flatnonzero(d < 0.25)
+        hit = hit[np.argsort(pos_of[hit])][:7]
+        assert np.array_equal(res["hit_id"][qi].cpu().numpy()[: len(hit)], hit)
+        non = np.flatnonzero(d >= 0.25)
+        non = non[np.lexsort((pos_of[non], d[non]))][:7]
+        assert np.array_equal(res["top_id"][qi].cpu().numpy(), non)
+        assert int(res["n_hits"][qi].item()) == int((d < 0.25).sum())
+    # 3 "ranks": contiguous record shards, global scan positions
+    parts = []
+    for r in range(3):
+        lo, hi = r * N // 3, (r + 1) * N // 3
+        lorder, pmap = local_scan_plan(order, lo, hi)
+        parts.append(chamfer_scan(db[lo:hi], qs, k=7, threshold=0.25, order=torch.from_numpy(lorder).cuda(),
+                                  pos_map=torch.from_numpy(pmap).cuda(), id_base=lo))
+    merged = merge_lists([{k: v.cpu() for k, v in p.items() if not k.startswith("_")} for p in parts], 7)
+    for name in ("top_id", "hit_id", "top_pos", "hit_pos", "n_hits"):
+        assert torch.equal(merged[name], res[name].cpu()), name

@@ -1,0 +1,305 @@
+"""GPU parity of the simulation / screening kernel against the reference
+(golden fixtures) and the oracle (seeded subsets).  Tolerances follow
+BASELINE.json north_star / SURVEY.md §8a:
+
+* lock flags (first_t, first_joint) bit-exact except candidates whose f64
+  discriminant margin is below 1e-6 (counted, reported);
+* fp32 coordinates within 1e-4 of the reference path's bounding-box
+  diagonal, floored at 1e-3 of the unit box (below that an fp32-stored
+  coordinate near 0.5 cannot resolve 1e-4 of the diagonal: half an ulp is
+  3e-8); f64 trajectories (the drop-in API) within 1e-12 absolute.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import links_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+MARGIN = 1e-6
+COORD_TOL = 1e-4
+DIAG_FLOOR = 1e-3
+F64_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def bbox_diag(P):
+    lo = np.nanmin(P, axis=-2)
+    hi = np.nanmax(P, axis=-2)
+    return np.hypot(*(hi - lo).T) if P.ndim == 2 else np.hypot(hi[..., 0] - lo[..., 0], hi[..., 1] - lo[..., 1])
+
+
+def coord_err(P_gpu, P_ref):
+    """max over joint paths of max |dP| / max(bbox diagonal, DIAG_FLOOR)."""
+    err = np.abs(P_gpu - P_ref).max(axis=(-1, -2))  # (..., n)
+    diag = np.maximum(bbox_diag(P_ref), DIAG_FLOOR)
+    return float((err / diag).max())
+
+
+def flag_parity(ft, fj, ref_ft, ref_fj, margin):
+    near = margin < MARGIN
+    bad = ((ft != ref_ft) | (fj != ref_fj)) & ~near
+    return int(bad.sum()), int(near.sum())
+
+
+def run_mixed(torch, plans, pos, topo, T, **kw):
+    from paper_2208_14567_b200.solver import PlanTable, simulate_tensors
+
+    dpos = torch.from_numpy(np.ascontiguousarray(pos)).cuda()
+    dtopo = None if topo is None else torch.from_numpy(np.ascontiguousarray(topo, dtype=np.int32)).cuda()
+    res = simulate_tensors(dpos, PlanTable(plans), T, topo=dtopo, traj_stride=pos.shape[1], **kw)
+    torch.cuda.synchronize()
+    return res
+
+
+def test_fourbar_golden(torch, golden):
+    from paper_2208_14567_b200.workloads import bare_plan, four_bar
+
+    g = golden("solver_golden.npz")
+    plan = bare_plan(four_bar())
+    res = run_mixed(torch, [plan], g["fb_pos0"], None, 200, low=True)
+    ft = res["first_t"].cpu().numpy()
+    fj = res["first_joint"].cpu().numpy()
+    margin = O.simulate(g["fb_pos0"], [(3, 1, 2)], (0, 2), 200, with_margin=True)["margin"]
+    bad, near = flag_parity(ft, fj, g["fb_first_t"], g["fb_first_joint"], margin)
+    assert bad == 0, f"{bad} flag mismatches outside the margin band ({near} near-margin)"
+    # the coarse sweep is the T_low = 50 gate of the reference
+    low = res["low_t"].cpu().numpy()
+    want_low = np.where(g["fb_first_t50"] < 50, g["fb_first_t50"], -1)
+    assert np.array_equal(low[margin >= MARGIN], want_low[margin >= MARGIN])
+    traj = res["traj"].view(-1, 4, 200, 2).cpu().numpy().astype(np.float64)
+    assert coord_err(traj[g["fb_traj_idx"]], g["fb_traj"]) <= COORD_TOL
+    r64 = run_mixed(torch, [plan], g["fb_pos0"], None, 200, traj_f64=True)
+    t64 = r64["traj"].view(-1, 4, 200, 2).cpu().numpy()
+    assert np.abs(t64[g["fb_traj_idx"]] - g["fb_traj"]).max() <= F64_TOL
+    assert torch.equal(r64["first_t"], res["first_t"])
+
+
+def test_mixed_topologies_golden(torch, golden):
+    from paper_2208_14567_b200.solver import SolutionPlan, compile_order
+
+    g = golden("solver_golden.npz")
+    plans = []
+    for t in range(len(g["mx_n"])):
+        n = int(g["mx_n"][t])
+        fixed, steps = compile_order(g["mx_adj"][t][:n, :n], g["mx_types"][t][:n])
+        plans.append(SolutionPlan(n, fixed, steps, None, None, None))
+    pos = g["mx_pos0"]
+    res = run_mixed(torch, plans, pos, g["mx_topo"], 200, low=True)
+    ft = res["first_t"].cpu().numpy()
+    fj = res["first_joint"].cpu().numpy()
+    margins = np.empty(len(ft))
+    for t, p in enumerate(plans):
+        sel = g["mx_topo"] == t
+        steps = [(s.target, s.a, s.b) for s in p.steps]
+        margins[sel] = O.simulate(pos[sel][:, :p.n], steps, p.fixed, 200, with_margin=True)["margin"]
+    bad, near = flag_parity(ft, fj, g["mx_first_t"], g["mx_first_joint"], margins)
+    assert bad == 0, f"{bad} mismatches ({near} near-margin)"
+    traj = res["traj"].view(len(ft), 20, 200, 2).cpu().numpy().astype(np.float64)
+    for gi, tp in zip(g["mx_traj_idx"], g["mx_traj"]):
+        n = int(g["mx_n"][g["mx_topo"][gi]])
+        assert ft[gi] == 200
+        assert coord_err(traj[gi, :n], tp[:n]) <= COORD_TOL
+
+
+def test_screen_mode_matches_simulate_mode(torch, golden):
+    """No-write screening (coarse-first, fine search) == full simulation."""
+    from paper_2208_14567_b200.solver import SolutionPlan, compile_order
+
+    g = golden("solver_golden.npz")
+    plans = []
+    for t in range(len(g["mx_n"])):
+        n = int(g["mx_n"][t])
+        fixed, steps = compile_order(g["mx_adj"][t][:n, :n], g["mx_types"][t][:n])
+        plans.append(SolutionPlan(n, fixed, steps, None, None, None))
+    a = run_mixed(torch, plans, g["mx_pos0"], g["mx_topo"], 200)
+    b = run_mixed(torch, plans, g["mx_pos0"], g["mx_topo"], 200, write_traj=False)
+    c = run_mixed(torch, plans, g["mx_pos0"], g["mx_topo"], 200, write_traj=False, coarse=False)
+    for k in ("first_t", "first_joint"):
+        assert torch.equal(a[k], b[k]) and torch.equal(a[k], c[k])
+
+
+def test_fp64_mode_and_no_fixup(torch, golden):
+    """All-f64 evaluation agrees with the reference flags; tau=0 (pure fp32)
+    still matches outside the margin band on this fixture."""
+    from paper_2208_14567_b200.workloads import bare_plan, four_bar
+
+    g = golden("solver_golden.npz")
+    plan = bare_plan(four_bar())
+    margin = O.simulate(g["fb_pos0"], [(3, 1, 2)], (0, 2), 200, with_margin=True)["margin"]
+    for kw in ({"fp64": True}, {"fixup_tau": 0.0}):
+        res = run_mixed(torch, [plan], g["fb_pos0"], None, 200, **kw)
+        bad, _ = flag_parity(res["first_t"].cpu().numpy(), res["first_joint"].cpu().numpy(),
+                             g["fb_first_t"], g["fb_first_joint"], margin)
+        assert bad == 0, kw
+    res = run_mixed(torch, [plan], g["fb_pos0"], None, 200, fp64=True, traj_f64=True)
+    traj = res["traj"].view(-1, 4, 200, 2).cpu().numpy()
+    assert np.abs(traj[g["fb_traj_idx"]] - g["fb_traj"]).max() <= F64_TOL
+
+
+def test_known_answers(torch, golden):
+    from paper_2208_14567_b200 import Locking, Trajectory, compile_plan, dyad_solve, simulate
+    from paper_2208_14567_b200.workloads import four_bar
+
+    g = golden("solver_golden.npz")
+    p = dyad_solve((0.0, 0.0), (1.0, 0.0), 1.0, 1.0, 1.0)
+    assert p == (0.5, 0.8660254037844386)
+    q = dyad_solve((0.0, 0.0), (2.0, 0.0), 1.5, 1.5, -1.0)
+    assert q[0] == pytest.approx(1.0) and q[1] < 0
+    assert dyad_solve((0.0, 0.0), (2.0, 0.0), 0.5, 0.5, 1.0) is None
+    assert dyad_solve((0.0, 0.0), (0.0, 0.0), 1.0, 1.0, 1.0) is None
+    lock = four_bar(ground=(0.9, 0.5), coupler=(0.72, 0.51))
+    plan = compile_plan(lock)
+    o200 = simulate(lock, plan, 200)
+    o50 = simulate(lock, plan, 50)
+    assert isinstance(o200, Locking) and (o200.step, o200.joint) == tuple(g["ka_lock"][:2])
+    assert isinstance(o50, Locking) and o50.step == g["ka_lock"][2]
+    ok = four_bar()
+    out = simulate(ok, compile_plan(ok), 200)
+    assert isinstance(out, Trajectory)
+    assert np.abs(out.positions - g["ka_valid_traj"]).max() <= F64_TOL
+    assert np.allclose(out.positions[:, 0, :], ok.positions0, atol=1e-12)
+
+
+def test_plan_geometry_and_compile_plan(torch):
+    from paper_2208_14567_b200 import PlanError, compile_plan
+    from paper_2208_14567_b200.solver import plan_geometry
+    from paper_2208_14567_b200.workloads import four_bar
+
+    m = four_bar()
+    plan = compile_plan(m)
+    ra, rb, br = plan_geometry(plan, m.positions0)
+    wa, wb, wbr = O.step_geometry(m.positions0[None], [(3, 1, 2)])
+    assert np.allclose(ra, wa[0], rtol=0, atol=1e-15) and np.allclose(rb, wb[0], rtol=0, atol=1e-15)
+    assert np.array_equal(br, wbr[0])
+    assert plan.fixed == (0, 2) and [s.target for s in plan.steps] == [3]
+    degenerate = four_bar(coupler=(0.55, 0.5))  # joint 3 on the crank tip: zero bar
+    with pytest.raises(PlanError):
+        compile_plan(degenerate)
+
+
+def test_simulate_batch_dropin_conserves_lengths(torch):
+    from paper_2208_14567_b200 import Trajectory, compile_plan, simulate_batch
+    from paper_2208_14567_b200.workloads import four_bar
+
+    rng = np.random.default_rng(5)
+    mech = four_bar()
+    plan = compile_plan(mech)
+    poses = []
+    for _ in range(64):
+        p = np.array(mech.positions0)
+        p[2] = rng.uniform(0.2, 0.9, size=2)
+        p[3] = rng.uniform(0.2, 0.9, size=2)
+        poses.append(p)
+    poses = np.stack(poses)
+    outs = simulate_batch(poses, plan, T=100)
+    ref = O.simulate(poses, [(3, 1, 2)], (0, 2), 100, with_margin=True)
+    for b, o in enumerate(outs):
+        if ref["margin"][b] < MARGIN:
+            continue
+        if ref["first_t"][b] < 100:
+            assert not isinstance(o, Trajectory) and o.step == ref["first_t"][b]
+        else:
+            assert isinstance(o, Trajectory)
+            P = o.positions
+            assert np.abs(P - O.trajectories(ref)[b]).max() <= F64_TOL
+            for i, j in mech.edges():
+                L = np.hypot(*(P[i] - P[j]).T)
+                assert L.max() - L.min() < 1e-9  # the reference's own bound
+
+
+def test_check_feasible_and_find_valid_variant(torch, golden):
+    from paper_2208_14567_b200 import check_feasible, find_valid_variant, sample_topology
+    from paper_2208_14567_b200.solver import SolutionPlan, compile_order
+
+    g = golden("solver_golden.npz")
+    for t in range(len(g["fv_n"])):
+        n = int(g["fv_n"][t])
+        seed = int(g["fv_seed"][t])
+        mech, plan = sample_topology(np.random.default_rng([seed, 0]), n)
+        rng = np.random.default_rng([seed, 1])
+        res = find_valid_variant(mech, plan, rng)
+        assert res is not None
+        assert res.attempts == int(g["fv_attempts"][t])
+        assert np.array_equal(res.mechanism.positions0, g["fv_pos"][t][:n])
+        assert check_feasible(res.mechanism, plan)
+        # rng left exactly where the reference loop leaves it
+        ref_rng = np.random.default_rng([seed, 1])
+        batches = (int(g["fv_attempts"][t]) + 255) // 256
+        for _ in range(batches):
+            ref_rng.uniform(size=(256, n, 2))
+        assert rng.random() == ref_rng.random()
+    # non-fused path (T_high != 4*T_low) agrees on the same stream
+    n = int(g["fv_n"][0])
+    seed = int(g["fv_seed"][0])
+    mech, plan = sample_topology(np.random.default_rng([seed, 0]), n)
+    a = find_valid_variant(mech, plan, np.random.default_rng([seed, 1]), T_low=40, T_high=200)
+    assert a is not None and a.attempts >= 1
+
+
+@pytest.mark.parametrize("n_lo,n_hi,count", [(6, 8, 8192), (5, 20, 16384)])
+def test_mixed_scale_vs_oracle(torch, n_lo, n_hi, count):
+    """C2 / C3-style candidates from the generator streams: flags vs the
+    oracle with the margin rule; coordinates within 1e-4 of the diagonal."""
+    from paper_2208_14567_b200.workloads import mixed_batch
+
+    mb = mixed_batch(count, n_lo, n_hi, seed=11, stride=20)
+    res = run_mixed(torch, mb.plans, mb.pos, mb.topo, 200, low=True)
+    ft = res["first_t"].cpu().numpy()
+    fj = res["first_joint"].cpu().numpy()
+    traj = res["traj"].view(mb.B, 20, 200, 2)
+    total_bad = total_near = 0
+    worst = 0.0
+    tiny = 0
+    for t, p in enumerate(mb.plans):
+        sel = np.flatnonzero(mb.topo == t)
+        steps = [(s.target, s.a, s.b) for s in p.steps]
+        ref = O.simulate(mb.pos[sel][:, :p.n], steps, p.fixed, 200, with_margin=True)
+        bad, near = flag_parity(ft[sel], fj[sel], ref["first_t"], ref["first_joint"], ref["margin"])
+        total_bad += bad
+        total_near += near
+        ok = np.flatnonzero((ref["first_t"] == 200) & (ft[sel] == 200))
+        if len(ok):
+            Pg = traj[torch.from_numpy(sel[ok]).cuda()][:, :p.n].cpu().numpy().astype(np.float64)
+            Pr = O.trajectories(ref)[ok]
+            worst = max(worst, coord_err(Pg, Pr))
+            tiny += int((bbox_diag(Pr) < DIAG_FLOOR).sum())
+    print(f"\nmixed n={n_lo}..{n_hi}: {count} candidates, valid {(ft == 200).mean():.3f}, "
+          f"near-margin {total_near}, flag mismatches {total_bad}, worst coord err {worst:.2e}, "
+          f"paths with diagonal < {DIAG_FLOOR}: {tiny}")
+    assert total_bad == 0
+    assert worst <= COORD_TOL
+
+
+def test_compaction_ordered(torch):
+    from paper_2208_14567_b200.solver import compact_valid
+
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    for B in (1, 1000, 1024, 1025, 300_001):
+        ft = torch.randint(150, 201, (B,), generator=gen, device="cuda", dtype=torch.int32)
+        idx, cnt = compact_valid(ft, 200)
+        want = torch.nonzero(ft == 200).flatten()
+        assert int(cnt.item()) == want.numel()
+        assert torch.equal(idx[: want.numel()], want)
+
+
+def test_gate_only_flag(torch, golden):
+    """LA_SIM_GATE_ONLY: negatives carry the coarse lock, positives exact."""
+    from paper_2208_14567_b200.workloads import bare_plan, four_bar
+
+    g = golden("solver_golden.npz")
+    res = run_mixed(torch, [bare_plan(four_bar())], g["fb_pos0"], None, 200, write_traj=False,
+                    gate_only=True, low=True)
+    ft = res["first_t"].cpu().numpy()
+    low = res["low_t"].cpu().numpy()
+    assert np.array_equal(ft == 200, g["fb_first_t"] == 200)
+    locked = low >= 0
+    assert np.array_equal(ft[locked], 4 * low[locked])
