@@ -23,7 +23,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -61,62 +60,74 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled through NVML every
+    2 ms in a background thread; only samples taken while ``timed`` is set
+    count as "during the timed region"."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines: list[str] = []
-        self.t = None
-
-    def __enter__(self):
+    def __init__(self, torch, device_index: int):
+        self.timed = False
+        self.samples = []
+        self.all = []
+        self._stop = threading.Event()
+        self.handle = None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            h = None
+            try:
+                uuid = str(torch.cuda.get_device_properties(device_index).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.handle = h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.handle = None
+            self.max_mhz = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def start(self):
+        if self.handle is not None:
             self.t.start()
-        except OSError:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
             try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-            if self.t is not None:
-                self.t.join(timeout=2)
+                mhz = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+            except Exception:
+                break
+            rec = (mhz, rs)
+            self.all.append(rec)
+            if self.timed:
+                self.samples.append(rec)
+            time.sleep(0.002)
+
+    def stop(self):
+        self._stop.set()
+        if self.t.is_alive():
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, v in zip(names, parts[4:8]):
-                if v.lower().startswith("active"):
+        src = self.samples if self.samples else self.all
+        if not src:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        reasons = set()
+        for _, rs in src:
+            for name, bit in self.REASONS:
+                if rs & bit:
                     reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(m for m, _ in src), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(src),
+                "window": "timed regions" if self.samples else "whole run (timed regions too short)",
+                "source": "NVML (nvmlDeviceGetClockInfo / GetCurrentClocksEventReasons), 2 ms"}
 
 
 class Timer:
@@ -167,7 +178,7 @@ def c2_inputs(rank: int):
     return mixed_batch(C2_COUNT, 6, 8, seed=2208 + rank, stride=8)
 
 
-def bench_c2(torch, args, rank, world, peaks, flush):
+def bench_c2(torch, args, rank, world, peaks, flush, clk):
     from paper_2208_14567_b200.solver import simulate_compact, simulate_tensors
 
     mb = c2_inputs(rank)
@@ -213,12 +224,13 @@ def bench_c2(torch, args, rank, world, peaks, flush):
 
     spans = []
     barrier(torch, world)
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        for _ in range(args.steps):
-            flush()
-            tm = Timer(torch, stream)
-            step(tm)
-            spans.append(tm.spans())
+    clk.timed = True
+    for _ in range(args.steps):
+        flush()
+        tm = Timer(torch, stream)
+        step(tm)
+        spans.append(tm.spans())
+    clk.timed = False
     barrier(torch, world)
     ms = statistics.mean(s["total"] for s in spans)
     ms = max_over_ranks(torch, ms, world)
@@ -244,7 +256,7 @@ def bench_c2(torch, args, rank, world, peaks, flush):
     return {
         "value": value, "ms": ms, "valid": valid, "B": mb.B, "kernels_ms": {
             "screen": k_screen, "compact": k_compact, "paths": k_paths},
-        "roofline": dominant, "roofline_kernels": [rl_screen, rl_paths], "clocks": clk.summary(),
+        "roofline": dominant, "roofline_kernels": [rl_screen, rl_paths],
         "launches_per_step": 5, "path_dyads": path_dyads, "mb": mb, "table": table,
     }
 
@@ -300,7 +312,7 @@ def e2e_c2(torch, args, mb, table, world):
 
 
 # ----------------------------------------------------------------- C3
-def bench_c3(torch, args, rank, world, peaks, flush):
+def bench_c3(torch, args, rank, world, peaks, flush, clk):
     from paper_2208_14567_b200.solver import PlanTable, compact_valid, simulate_tensors
     from paper_2208_14567_b200.workloads import device_poses, topology_pool
 
@@ -331,11 +343,13 @@ def bench_c3(torch, args, rank, world, peaks, flush):
     valid = int(cnt.item())
     spans = []
     barrier(torch, world)
+    clk.timed = True
     for _ in range(args.steps):
         flush()
         tm = Timer(torch, stream)
         step(tm)
         spans.append(tm.spans())
+    clk.timed = False
     barrier(torch, world)
     ms = max_over_ranks(torch, statistics.mean(s["total"] for s in spans), world)
     k = statistics.mean(s["screen"] for s in spans)
@@ -353,7 +367,7 @@ def bench_c3(torch, args, rank, world, peaks, flush):
 
 
 # ----------------------------------------------------------------- C4
-def bench_c4(torch, args, rank, world, peaks, flush):
+def bench_c4(torch, args, rank, world, peaks, flush, clk):
     from paper_2208_14567_b200.atlas import chamfer_scan
     from paper_2208_14567_b200.dist import gather_merge
     from paper_2208_14567_b200.workloads import fourier_db
@@ -380,11 +394,13 @@ def bench_c4(torch, args, rank, world, peaks, flush):
         step()
     spans = []
     barrier(torch, world)
+    clk.timed = True
     for _ in range(args.steps):
         flush()
         tm = Timer(torch, stream)
         step(tm)
         spans.append(tm.spans())
+    clk.timed = False
     barrier(torch, world)
     ms = max_over_ranks(torch, statistics.mean(s["total"] for s in spans), world)
     kscan = statistics.mean(s["scan"] for s in spans)
@@ -528,18 +544,24 @@ def main():
     _native.load(build_if_missing=False)
     peaks, peaks_src = load_peaks()
     flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    read_buf = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
     def flush():
+        # write a buffer 4x the L2, then stream-read another so the L2 holds
+        # clean lines (no dirty write-back charged to the timed kernels)
         flush_buf.zero_()
+        read_buf.sum()
 
     skip = set(filter(None, args.skip.split(",")))
-    c2 = bench_c2(torch, args, rank, world, peaks, flush)
+    clk = ClockSampler(torch, local).start()
+    c2 = bench_c2(torch, args, rank, world, peaks, flush, clk)
     e2e = e2e_c2(torch, args, c2["mb"], c2["table"], world)
     secondary = {}
     if "c3" not in skip:
-        secondary["screen"] = bench_c3(torch, args, rank, world, peaks, flush)
+        secondary["screen"] = bench_c3(torch, args, rank, world, peaks, flush, clk)
     if "c4" not in skip:
-        secondary["chamfer"] = bench_c4(torch, args, rank, world, peaks, flush)
+        secondary["chamfer"] = bench_c4(torch, args, rank, world, peaks, flush, clk)
+    clk.stop()
     cpu = None
     if rank == 0 and world == 1 and "cpu" not in skip:
         cpu = cpu_baseline_c2(c2["mb"])
@@ -553,7 +575,7 @@ def main():
             "config": {"workload": "C2: 100,000 candidates/GPU of 6-8 joints (reference random-topology "
                                    "operator, 256 per topology), T=200, paths of all joints of valid "
                                    "candidates (fp32) + lock flags of all", "l2": "flushed between steps "
-                                   f"({L2_FLUSH_BYTES >> 20} MiB write)", "parallelism": f"dp{world}",
+                                   f"({L2_FLUSH_BYTES >> 20} MiB write + {L2_FLUSH_BYTES >> 20} MiB read)", "parallelism": f"dp{world}",
                        "valid_per_gpu": c2["valid"]},
             "roofline": {**rl, "peak_source": peaks_src},
             "roofline_kernels": c2["roofline_kernels"],
@@ -562,7 +584,7 @@ def main():
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind",
                                                                            "sample")},
             "gpu_launches": c2["launches_per_step"] * args.steps,
-            "clocks": c2["clocks"],
+            "clocks": clk.summary(),
             "secondary": secondary,
             "published": {"paper_v100_sims_per_s": 54855, "paper_80thread_cpu_sims_per_s": 17995,
                           "note": "PAPER.md:208-211, 10,000-mechanism Table-1 workload (other config)"},

@@ -37,19 +37,36 @@ constexpr int NS = LA_MAX_STEPS;
 constexpr int SIM_WARPS = 8;
 constexpr int SIM_THREADS = SIM_WARPS * 32;
 
-// Per-warp shared memory: step geometry + initial pose, followed by a joint
+// Per-warp shared memory: step records + initial pose, followed by a joint
 // position column block pos[joint][lane] sized for the batch's largest n.
 // The block is viewed as float2 (fp32 screen rounds) or double2 (f64 rounds).
+struct __align__(16) StepRec {
+  float sp;              // ra + rb           (fp32 margin test)
+  float df;              // |ra - rb|
+  float c2;              // ra^2 - rb^2
+  float ra2;             // ra^2
+  float br;              // branch sign
+  uint32_t a_off;        // byte offset of joint a's float2 column
+  uint32_t b_off;
+  uint32_t t_off;
+};
+
+struct __align__(16) StepRec64 {
+  double hi;             // (ra + rb) + LOCK_EPS   (solver.py:213, same rounding)
+  double lo;             // |ra - rb| - LOCK_EPS
+  double ra2;            // ra * ra
+  double rb2;            // rb * rb
+  double br;             // branch sign
+  double _pad;
+};
+
 struct __align__(16) WarpHead {
+  StepRec st[NS];
+  StepRec64 st64[NS];
   double2 p0[NJ];        // f64 initial pose
-  double dra[NS], drb[NS], dbr[NS];
-  float sp[NS];          // ra + rb
-  float df[NS];          // |ra - rb|
-  float c2[NS];          // ra^2 - rb^2
-  float ra2[NS];         // ra^2
-  float br[NS];          // branch sign
   int8_t tg[NS], ia[NS], ib[NS];
-  int8_t _pad[10];
+  int8_t nstatic;
+  int8_t statics[NJ + 1];  // joints that never move (fixed + pivot)
 };
 
 struct Warp {
@@ -66,31 +83,62 @@ struct Warp {
 
 struct SimCtx {
   int n, ns;
-  uint32_t fixed;
   double r1;
   float tau;
 };
 
-// f64 replay of one angle mirroring solver.py:180-231 operation by operation
-// (np.hypot; (d*d + ra*ra - rb*rb) / (2*d); sqrt(max(ra*ra - x*x, 0)); ...),
-// the lock test with LOCK_EPS = 1e-9 (solver.py:19, 213).  Positions live in
-// the caller-provided accessor; returns the first locking step or -1.
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// f64 reciprocal square root: MUFU.RSQ64H seed + two Newton steps
+// (relative error ~1e-16; not correctly rounded, see dyads_f64)
+__device__ __forceinline__ double rsqrt_f64(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double e = fma(-h, y * y, 0.5);
+    y = fma(y, e, y);
+  }
+  return y;
+}
+
+// f64 dyad replay of one angle in the reference's operation order
+// (solver.py:205-231): the lock test d < eps | d > (ra+rb)+eps |
+// d < |ra-rb|-eps with LOCK_EPS = 1e-9 (solver.py:19, 213),
+// x = ((d*d + ra*ra) - rb*rb) / (2d), h = sqrt(max(ra*ra - x*x, 0)),
+// p = p_a + x*u - branch*h*u_perp.  d and 1/d come from one Newton-refined
+// reciprocal square root instead of np.hypot and three IEEE divisions: each
+// differs from the numpy value by an ulp or two (the parity tests hold f64
+// trajectories to 1e-12 of the reference).
 template <typename Get, typename Put>
 __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get get, Put put) {
   const double eps = 1e-9;
 #pragma unroll 1
   for (int s = 0; s < C.ns; ++s) {
     const int a = H.ia[s], b = H.ib[s], t = H.tg[s];
+    const StepRec64& g = H.st64[s];
     const double2 pa = get(a), pb = get(b);
     const double dx = dsub(pb.x, pa.x);
     const double dy = dsub(pb.y, pa.y);
-    const double d = hypot(dx, dy);
-    const double ra = H.dra[s], rb = H.drb[s];
-    if (d < eps || d > dadd(dadd(ra, rb), eps) || d < dsub(fabs(dsub(ra, rb)), eps)) return s;
-    const double x = ddiv(dsub(dadd(dmul(d, d), dmul(ra, ra)), dmul(rb, rb)), dmul(2.0, d));
-    const double h = __dsqrt_rn(fmax(dsub(dmul(ra, ra), dmul(x, x)), 0.0));
-    const double ux = ddiv(dx, d), uy = ddiv(dy, d);
-    const double bh = dmul(H.dbr[s], h);
+    const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
+    const double inv = rsqrt_f64(d2);
+    const double d = dmul(d2, inv);
+    if (!(d >= eps) || d > g.hi || d < g.lo) return s;
+    const double x = dmul(dsub(dadd(dmul(d, d), g.ra2), g.rb2), dmul(0.5, inv));
+    const double h2 = dsub(g.ra2, dmul(x, x));
+    const double h = h2 > 0.0 ? dmul(h2, rsqrt_f64(h2)) : 0.0;
+    const double ux = dmul(dx, inv), uy = dmul(dy, inv);
+    const double bh = dmul(g.br, h);
     put(t, make_double2(dsub(dadd(pa.x, dmul(x, ux)), dmul(bh, uy)),
                         dadd(dadd(pa.y, dmul(x, uy)), dmul(bh, ux))));
   }
@@ -107,7 +155,10 @@ __device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, dou
   double2 q[NJ];
   const WarpHead& H = *W.h;
 #pragma unroll 1
-  for (int j = 0; j < C.n; ++j) q[j] = H.p0[j];
+  for (int k = 0; k < H.nstatic; ++k) {
+    const int j = H.statics[k];
+    q[j] = H.p0[j];
+  }
   q[1] = crank_tip(H, C, ct, st);
   W.p32(1) = make_float2((float)q[1].x, (float)q[1].y);
   return dyads_f64(H, C, [&](int j) { return q[j]; },
@@ -118,9 +169,10 @@ __device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, dou
 }
 
 // fp32 angle evaluation with f64 fix-up.  A lane whose dyad margin
-// M = min(ra + rb - d, d - |ra - rb|) (unit-box lengths) satisfies |M| < tau
-// at or before its first lock is replayed in f64, so every lock decision and
-// every position fed forward is either clear of fp32 error or f64-exact.
+// M = min(ra + rb - d, d - |ra - rb|) (unit-box lengths) has |M| < tau at or
+// before its first lock (or is NaN) is replayed in f64, so every lock
+// decision and every position fed forward is either clear of fp32 error or
+// f64-exact.
 __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const double* __restrict__ cs, int t,
                                        bool active, unsigned long long& n_fix) {
   const WarpHead& H = *W.h;
@@ -133,32 +185,29 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
     const double2 tip = crank_tip(H, C, ct, st);
     W.p32(1) = make_float2((float)tip.x, (float)tip.y);
     const float tau = C.tau;
+    unsigned char* col = W.cols + W.lane * 8;
 #pragma unroll 1
     for (int s = 0; s < C.ns; ++s) {
-      const int a = H.ia[s], b = H.ib[s], tg = H.tg[s];
-      const float2 pa = W.p32(a);
-      const float2 pb = W.p32(b);
+      const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
+      const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].br);
+      const float2 pa = *reinterpret_cast<const float2*>(col + g1.y);
+      const float2 pb = *reinterpret_cast<const float2*>(col + g1.z);
       const float dx = pb.x - pa.x, dy = pb.y - pa.y;
       const float d2 = fmaf(dy, dy, dx * dx);
-      if (!(d2 > 1e-16f)) {  // (near-)coincident joints: let f64 decide
-        fix = true;
-        lk = s;
-        break;
-      }
-      const float inv_d = rsqrtf(d2);
-      const float d = d2 * inv_d;
-      const float m = fminf(H.sp[s] - d, d - H.df[s]);
-      if (fabsf(m) < tau) fix = true;
+      const float inv = rsqrt_approx(d2);
+      const float d = d2 * inv;
+      const float m = fminf(g0.x - d, d - g0.y);
+      fix |= !(fabsf(m) >= tau);  // NaN (coincident joints) -> f64 decides
       if (m < 0.0f) {
         lk = s;
         break;
       }
-      const float x = (d2 + H.c2[s]) * (0.5f * inv_d);
-      const float h2 = fmaxf(fmaf(-x, x, H.ra2[s]), 0.0f);
-      const float h = h2 > 0.0f ? h2 * rsqrtf(h2) : 0.0f;
-      const float ux = dx * inv_d, uy = dy * inv_d;
-      const float bh = H.br[s] * h;
-      W.p32(tg) = make_float2(fmaf(-bh, uy, fmaf(x, ux, pa.x)), fmaf(bh, ux, fmaf(x, uy, pa.y)));
+      const float x = (d2 + g0.z) * (0.5f * inv);
+      const float h = sqrt_approx(fmaxf(fmaf(-x, x, g0.w), 0.0f));
+      const float xi = x * inv;
+      const float hb = __uint_as_float(g1.x) * h * inv;
+      *reinterpret_cast<float2*>(col + g1.w) =
+          make_float2(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)));
     }
   }
   if (__any_sync(FULL, fix)) {
@@ -179,16 +228,22 @@ __device__ __forceinline__ int solve64(const Warp& W, const SimCtx& C, const dou
   return dyads_f64(H, C, [&](int j) { return W.p64(j); }, [&](int j, double2 v) { W.p64(j) = v; });
 }
 
-__device__ __forceinline__ void fill_static32(const Warp& W, const SimCtx& C) {
+__device__ __forceinline__ void fill_static32(const Warp& W) {
+  const WarpHead& H = *W.h;
 #pragma unroll 1
-  for (int j = 0; j < C.n; ++j)
-    if ((C.fixed >> j) & 1u) W.p32(j) = make_float2((float)W.h->p0[j].x, (float)W.h->p0[j].y);
+  for (int k = 0; k < H.nstatic; ++k) {
+    const int j = H.statics[k];
+    W.p32(j) = make_float2((float)H.p0[j].x, (float)H.p0[j].y);
+  }
 }
 
-__device__ __forceinline__ void fill_static64(const Warp& W, const SimCtx& C) {
+__device__ __forceinline__ void fill_static64(const Warp& W) {
+  const WarpHead& H = *W.h;
 #pragma unroll 1
-  for (int j = 0; j < C.n; ++j)
-    if ((C.fixed >> j) & 1u) W.p64(j) = W.h->p0[j];
+  for (int k = 0; k < H.nstatic; ++k) {
+    const int j = H.statics[k];
+    W.p64(j) = H.p0[j];
+  }
 }
 
 // first locking lane of a round -> (angle index within the round's list, step)
@@ -207,11 +262,16 @@ __device__ __forceinline__ RoundLock round_lock(bool active, int lk) {
 __device__ __forceinline__ int fine_angle(int i) { return (i / 3) * 4 + 1 + (i % 3); }
 
 template <bool WRITE, bool SCREEN64>
+__host__ __device__ constexpr size_t col_bytes() {
+  return (WRITE || SCREEN64) ? sizeof(double2) : sizeof(float2);
+}
+
+template <bool WRITE, bool SCREEN64>
 __global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, int njmax) {
   extern __shared__ __align__(16) unsigned char sim_smem_raw[];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const size_t per_warp = sizeof(WarpHead) + (size_t)njmax * 32 * sizeof(double2);
+  const size_t per_warp = sizeof(WarpHead) + (size_t)njmax * 32 * col_bytes<WRITE, SCREEN64>();
   Warp W;
   W.h = reinterpret_cast<WarpHead*>(sim_smem_raw + per_warp * w);
   W.cols = sim_smem_raw + per_warp * w + sizeof(WarpHead);
@@ -232,7 +292,7 @@ __global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, i
     C.n = pl->n;
     C.ns = pl->nsteps;
     C.tau = p.fixup_tau;
-    C.fixed = pl->fixed_mask | 1u;  // joint 0 is static (solver.py:183)
+    const uint32_t fixed = pl->fixed_mask | 1u;  // joint 0 is static (solver.py:183)
     if (C.n > njmax || C.n < 2 || C.ns > NS || C.ns < 0) {
       // plan does not fit the launch (n > pos_stride): flag, do not touch smem
       if (lane == 0) {
@@ -249,29 +309,51 @@ __global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, i
       H.ia[lane] = pl->step[lane][1];
       H.ib[lane] = pl->step[lane][2];
     }
+    {
+      // static joints (1 is the crank tip even if typed Fixed)
+      const bool is_static = lane < C.n && lane != 1 && ((fixed >> lane) & 1u);
+      const unsigned bal = __ballot_sync(FULL, is_static);
+      if (is_static) H.statics[__popc(bal & ((1u << lane) - 1u))] = (int8_t)lane;
+      if (lane == 0) H.nstatic = (int8_t)__popc(bal);
+    }
     __syncwarp();
     if (lane < C.ns) {
       // plan_geometry (solver.py:105-120), f64
       const double2 pa = H.p0[H.ia[lane]], pb = H.p0[H.ib[lane]], pt = H.p0[H.tg[lane]];
-      const double ra = hypot(dsub(pt.x, pa.x), dsub(pt.y, pa.y));
-      const double rb = hypot(dsub(pt.x, pb.x), dsub(pt.y, pb.y));
+      const double ax = dsub(pt.x, pa.x), ay = dsub(pt.y, pa.y);
+      const double bx = dsub(pt.x, pb.x), by = dsub(pt.y, pb.y);
+      // np.hypot in the reference; sqrt of the sum agrees to an ulp
+      const double ra = __dsqrt_rn(dadd(dmul(ax, ax), dmul(ay, ay)));
+      const double rb = __dsqrt_rn(dadd(dmul(bx, bx), dmul(by, by)));
       const double cross = dsub(dmul(dsub(pb.x, pa.x), dsub(pt.y, pa.y)),
                                 dmul(dsub(pb.y, pa.y), dsub(pt.x, pa.x)));
       const double br = cross >= 0.0 ? 1.0 : -1.0;
-      H.dra[lane] = ra;
-      H.drb[lane] = rb;
-      H.dbr[lane] = br;
-      const float fra = (float)ra, frb = (float)rb;
-      H.sp[lane] = (float)(ra + rb);
-      H.df[lane] = (float)fabs(ra - rb);
-      H.c2[lane] = (float)(ra * ra - rb * rb);
-      H.ra2[lane] = fra * fra;
-      H.br[lane] = (float)br;
+      StepRec64 r64;
+      r64.hi = dadd(dadd(ra, rb), 1e-9);
+      r64.lo = dsub(fabs(dsub(ra, rb)), 1e-9);
+      r64.ra2 = dmul(ra, ra);
+      r64.rb2 = dmul(rb, rb);
+      r64.br = br;
+      r64._pad = 0.0;
+      H.st64[lane] = r64;
+      StepRec r;
+      r.sp = (float)(ra + rb);
+      r.df = (float)fabs(ra - rb);
+      r.c2 = (float)(ra * ra - rb * rb);
+      r.ra2 = (float)ra * (float)ra;
+      r.br = (float)br;
+      r.a_off = (uint32_t)H.ia[lane] * 32u * (uint32_t)sizeof(float2);
+      r.b_off = (uint32_t)H.ib[lane] * 32u * (uint32_t)sizeof(float2);
+      r.t_off = (uint32_t)H.tg[lane] * 32u * (uint32_t)sizeof(float2);
+      H.st[lane] = r;
     }
-    C.r1 = hypot(dsub(H.p0[1].x, H.p0[0].x), dsub(H.p0[1].y, H.p0[0].y));
+    {
+      const double dx = dsub(H.p0[1].x, H.p0[0].x), dy = dsub(H.p0[1].y, H.p0[0].y);
+      C.r1 = __dsqrt_rn(dadd(dmul(dx, dx), dmul(dy, dy)));
+    }
     __syncwarp();
-    if (SCREEN64) fill_static64(W, C);
-    else fill_static32(W, C);
+    if (SCREEN64) fill_static64(W);
+    else fill_static32(W);
     __syncwarp();
 
     auto screen = [&](int t, bool act) -> int {
@@ -325,7 +407,7 @@ __global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, i
         // all T angles in natural order, f64, coalesced float2 stores
         if (!SCREEN64) {
           __syncwarp();
-          fill_static64(W, C);
+          fill_static64(W);
         }
         const long long row = p.traj_row ? p.traj_row[item] : item * (long long)p.traj_stride;
         const bool out64 = (p.flags & LA_SIM_TRAJ_F64) != 0;
@@ -544,7 +626,8 @@ int la_simulate(const la_sim_args* a, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool f64 = (a->flags & LA_SIM_FP64) != 0;
   const int njmax = a->pos_stride < NJ ? a->pos_stride : NJ;
-  const size_t smem = (sizeof(WarpHead) + (size_t)njmax * 32 * sizeof(double2)) * SIM_WARPS;
+  const size_t colb = (write || f64) ? sizeof(double2) : sizeof(float2);
+  const size_t smem = (sizeof(WarpHead) + (size_t)njmax * 32 * colb) * SIM_WARPS;
   auto kern = write ? (f64 ? sim_kernel<true, true> : sim_kernel<true, false>)
                     : (f64 ? sim_kernel<false, true> : sim_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

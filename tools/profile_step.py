@@ -1,0 +1,56 @@
+"""Small fixed workloads for ncu captures (one GPU).
+
+    python tools/profile_step.py c2      # screen + compaction + f64 path replay, 100k candidates
+    python tools/profile_step.py c3      # screen of 1M candidates, 5-20 joints
+    python tools/profile_step.py c4      # chamfer scan, 1 query x 1M curves
+    python tools/profile_step.py norm    # normalise 200k fp32 paths
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2208_14567_b200 import _native  # noqa: E402
+
+_native.load(build_if_missing=False)
+what = sys.argv[1] if len(sys.argv) > 1 else "c2"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+if what == "c2":
+    from paper_2208_14567_b200.solver import simulate_compact
+    from paper_2208_14567_b200.workloads import mixed_batch
+
+    mb = mixed_batch(100_000, 6, 8, seed=2208, stride=8)
+    pos = torch.from_numpy(mb.pos).cuda()
+    topo = torch.from_numpy(mb.topo).cuda()
+    table = mb.table()
+    for _ in range(reps):
+        simulate_compact(pos, table, 200, topo)
+elif what == "c3":
+    from paper_2208_14567_b200.solver import PlanTable, simulate_tensors
+    from paper_2208_14567_b200.workloads import device_poses, topology_pool
+
+    mechs, plans = topology_pool(256, 5, 20, seed=3000)
+    table = PlanTable(plans)
+    B = 1_000_000
+    topo = (torch.arange(B, device="cuda") // 256 % len(plans)).to(torch.int32)
+    pos = device_poses(topo, plans, 20, seed=77)
+    for _ in range(reps):
+        simulate_tensors(pos, table, 200, topo, write_traj=False)
+elif what == "c4":
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    db = fourier_db(1_000_000, 200, seed=4000)
+    q = fourier_db(1, 200, seed=999)
+    for _ in range(reps):
+        chamfer_scan(db, q, k=10)
+elif what == "norm":
+    from paper_2208_14567_b200.curves import normalize_tensors
+    from paper_2208_14567_b200.workloads import fourier_curves_device
+
+    raw = fourier_curves_device(200_000, 200, seed=5, dtype=torch.float32)
+    for _ in range(reps):
+        normalize_tensors(raw)
+torch.cuda.synchronize()
+print("ok", what)
