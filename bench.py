@@ -3,7 +3,8 @@
 Headline (BASELINE.json metric / configs[1]): mechanism simulations per second
 for 100,000 seeded 6-8-joint candidates per GPU (reference generator streams),
 200 crank angles, all joint paths of the valid ones + lock flags of all
-(``simulate_compact``: screen -> ordered compaction -> f64 path replay).
+(one sim_kernel pass: fp32 coarse-first screen, exact first lock, f64 replay
+of the survivors writing fp32 paths; then the ordered valid-candidate list).
 Secondary lines inside the same JSON object: the validity screen at scale
 (configs[2]) and chamfer curve-pairs/sec (configs[3], 1 query x 10M curves).
 
@@ -190,36 +191,29 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
     traj = torch.empty((mb.B * stride, T, 2), dtype=torch.float32, device="cuda")
 
     def step(timer=None):
+        # one pass: coarse fp32 screen, exact first lock for the locked ones,
+        # f64 replay + fp32 path stores for the survivors (rows b*stride..),
+        # then the ordered list of valid candidates
         if timer:
             timer.mark("start")
-        res = simulate_tensors(pos, table, T, topo, write_traj=False)
+        res = simulate_tensors(pos, table, T, topo, write_traj=True, traj=traj, traj_stride=stride)
         if timer:
-            timer.mark("screen")
+            timer.mark("sim")
         from paper_2208_14567_b200.solver import compact_valid
 
         idx, cnt = compact_valid(res["first_t"], T)
         if timer:
             timer.mark("compact")
-        simulate_tensors(pos, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, cand=idx,
-                         cand_count=cnt, coarse=False)
-        if timer:
-            timer.mark("paths")
         return res, idx, cnt
 
     for _ in range(args.warmup):
         step()
     # dyad counters + valid count from one instrumented (untimed) pass
-    cnt_buf = torch.zeros(4, dtype=torch.int64, device="cuda")
-    r0 = simulate_tensors(pos, table, T, topo, write_traj=False, counters=cnt_buf)
+    cnt_buf = torch.zeros(8, dtype=torch.int64, device="cuda")
+    r0 = simulate_tensors(pos, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, counters=cnt_buf)
     valid = int((r0["first_t"] == T).sum().item())
-    screen_dyads = int(cnt_buf[2].item())
-    cnt_p = torch.zeros(4, dtype=torch.int64, device="cuda")
-    from paper_2208_14567_b200.solver import compact_valid
-
-    idx0, c0 = compact_valid(r0["first_t"], T)
-    simulate_tensors(pos, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, cand=idx0,
-                     cand_count=c0, coarse=False, counters=cnt_p)
-    path_dyads = int(cnt_p[2].item())
+    cb = cnt_buf.cpu().numpy()
+    screen_dyads = int(cb[6])          # fp32 dyads executed by active lanes (to the first lock)
     n_valid_rows = int(mb.n[(r0["first_t"] == T).cpu().numpy()].sum())
 
     spans = []
@@ -234,30 +228,29 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
     barrier(torch, world)
     ms = statistics.mean(s["total"] for s in spans)
     ms = max_over_ranks(torch, ms, world)
-    k_screen = statistics.mean(s["screen"] for s in spans)
-    k_paths = statistics.mean(s["paths"] for s in spans)
+    k_sim = statistics.mean(s["sim"] for s in spans)
     k_compact = statistics.mean(s["compact"] for s in spans)
     value = world * mb.B / (ms / 1e3)
 
-    # roofline per kernel
+    # roofline of the dominant kernel: bytes the output contract requires
+    # (paths of every joint of the valid candidates, flags of all, poses in)
     sm_clock = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12  # TFLOP/s nominal at max clock
-    path_bytes = n_valid_rows * T * 8 + valid * stride * 16 + valid * 8 * 2
+    alg_bytes = n_valid_rows * T * 8 + mb.B * (8 + 4) + int(mb.n.sum()) * 16
+    rl_sim = {"kernel": "sim_kernel<WRITE> (fp32 screen + f64 path replay)", "bound": "hbm",
+              "achieved": alg_bytes / (k_sim / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+              "algorithmic_bytes": alg_bytes, "ms": k_sim, "traffic": None}
+    rl_sim["frac"] = rl_sim["achieved"] / rl_sim["peak"]
     screen_flops = DYAD_FLOPS * screen_dyads
-    rl_paths = {"kernel": "sim_kernel<WRITE> (f64 path replay)", "bound": "hbm",
-                "achieved": path_bytes / (k_paths / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "algorithmic_bytes": path_bytes, "ms": k_paths, "traffic": None}
-    rl_paths["frac"] = rl_paths["achieved"] / rl_paths["peak"]
-    rl_screen = {"kernel": "sim_kernel<SCREEN> (fp32 + f64 fix-up)", "bound": "fp32",
-                 "achieved": screen_flops / (k_screen / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
-                 "algorithmic_flops": screen_flops, "dyads": screen_dyads, "ms": k_screen, "traffic": None}
-    rl_screen["frac"] = rl_screen["achieved"] / rl_screen["peak"]
-    dominant = rl_paths if k_paths >= k_screen else rl_screen
+    rl_fp32 = {"kernel": "sim_kernel<WRITE> fp32 screen share", "bound": "fp32",
+               "achieved": screen_flops / (k_sim / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+               "algorithmic_flops": screen_flops, "dyads": screen_dyads, "lane_angles": int(cb[5]),
+               "f64_replay_lane_angles": int(cb[0]), "rounds_with_replay": int(cb[4]), "ms": k_sim}
+    rl_fp32["frac"] = rl_fp32["achieved"] / rl_fp32["peak"]
     return {
-        "value": value, "ms": ms, "valid": valid, "B": mb.B, "kernels_ms": {
-            "screen": k_screen, "compact": k_compact, "paths": k_paths},
-        "roofline": dominant, "roofline_kernels": [rl_screen, rl_paths],
-        "launches_per_step": 5, "path_dyads": path_dyads, "mb": mb, "table": table,
+        "value": value, "ms": ms, "valid": valid, "B": mb.B, "kernels_ms": {"sim": k_sim, "compact": k_compact},
+        "roofline": rl_sim, "roofline_kernels": [rl_sim, rl_fp32],
+        "launches_per_step": 4, "mb": mb, "table": table,
     }
 
 
@@ -337,7 +330,7 @@ def bench_c3(torch, args, rank, world, peaks, flush, clk):
 
     for _ in range(args.warmup):
         step()
-    cbuf = torch.zeros(4, dtype=torch.int64, device="cuda")
+    cbuf = torch.zeros(8, dtype=torch.int64, device="cuda")
     res, cnt = step(counters=cbuf)
     c = cbuf.cpu().numpy()
     valid = int(cnt.item())
@@ -355,13 +348,14 @@ def bench_c3(torch, args, rank, world, peaks, flush, clk):
     k = statistics.mean(s["screen"] for s in spans)
     sm_clock = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12
-    flops = DYAD_FLOPS * int(c[2])
+    flops = DYAD_FLOPS * int(c[6])
     rl = {"kernel": "sim_kernel<SCREEN>", "bound": "fp32", "achieved": flops / (k / 1e3) / 1e12,
           "peak": fp32_peak, "unit": "TFLOP/s", "frac": flops / (k / 1e3) / 1e12 / fp32_peak,
-          "algorithmic_flops": flops, "dyads": int(c[2]), "ms": k, "traffic": None}
+          "algorithmic_flops": flops, "dyads": int(c[6]), "warp_dyad_slots": int(c[2]), "ms": k, "traffic": None}
     return {"metric": SCREEN_METRIC, "value": world * C3_COUNT / (ms / 1e3), "unit": "candidates/s",
             "ms_per_step": ms, "valid_frac": valid / C3_COUNT, "fixup_lane_angles": int(c[0]),
-            "angles_evaluated": int(c[1]), "topologies": G, "roofline": rl, "launches_per_step": 4,
+            "angles_evaluated": int(c[5]), "rounds_with_replay": int(c[4]), "topologies": G, "roofline": rl,
+            "launches_per_step": 4,
             "config": {"workload": "C3: 10M candidates/GPU, 5-20 joints padded to 20, 256 per topology "
                                    "(1024-topology generator pool), poses U[0,1)^2 on device, T=200"}}
 

@@ -68,7 +68,7 @@ typedef struct la_sim_args {
   int64_t B;
   int32_t G;
   int32_t pos_stride;         /* joints per pose row (>= every plan's n)      */
-  int32_t T;                  /* crank angles per revolution                  */
+  int32_t T;                  /* crank angles per revolution (<= 2048)        */
   int32_t traj_stride;        /* joint rows per candidate in traj             */
   void* traj;                 /* (device) [rows][T][2] f32 (f64 with
                                  LA_SIM_TRAJ_F64), or NULL                    */
@@ -87,9 +87,13 @@ typedef struct la_sim_args {
   int32_t* low_t;             /* (device, optional) [B] lock step of the T/4
                                  coarse sweep (T_low semantics), -1 if none   */
   int32_t* low_joint;         /* (device, optional) [B]                       */
-  unsigned long long* counters; /* (device, optional) [4]: fp64 fix-up
-                                 lane-angles, angles evaluated, dyads
-                                 executed, candidates processed              */
+  unsigned long long* counters; /* (device, optional) [8] accumulated:
+                                 0 f64 fix-up lane-angles, 1 warp lane-slots
+                                 (32 x rounds), 2 warp dyad-slots (32 x rounds
+                                 x S), 3 candidates, 4 rounds with an f64
+                                 replay, 5 active lane-angles of fp32
+                                 rounds, 6 fp32 dyads executed (to the
+                                 first lock), 7 reserved                      */
   float fixup_tau;            /* fp32 screen: redo an angle in f64 when a
                                  dyad's margin min(ra+rb-d, d-|ra-rb|) is
                                  within tau (unit-box lengths) of a lock;

@@ -85,6 +85,8 @@ struct SimCtx {
   int n, ns;
   double r1;
   float tau;
+  float r1f;
+  float2 p0f;
 };
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
@@ -170,24 +172,28 @@ __device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, dou
 
 // fp32 angle evaluation with f64 fix-up.  A lane whose dyad margin
 // M = min(ra + rb - d, d - |ra - rb|) (unit-box lengths) has |M| < tau at or
-// before its first lock (or is NaN) is replayed in f64, so every lock
-// decision and every position fed forward is either clear of fp32 error or
-// f64-exact.
-__device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const double* __restrict__ cs, int t,
-                                       bool active, unsigned long long& n_fix) {
+// before its first lock (or is NaN) is ambiguous.  Angles increase with the
+// lane index in every round, so only ambiguous lanes BELOW the round's first
+// certain lock can change the round's outcome; those are replayed in f64
+// (the others cannot lower the first locking angle).  Every lock decision
+// that reaches the result is therefore clear of fp32 error or f64-exact.
+struct Ctr {
+  unsigned int fix_lanes = 0, replay_rounds = 0, lane_angles = 0, lane_dyads = 0;
+};
+
+__device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const double* __restrict__ cs,
+                                       const float2* __restrict__ cs32, int t, bool active, Ctr& ctr) {
   const WarpHead& H = *W.h;
   int lk = -1;
   bool fix = false;
-  double ct = 0.0, st = 0.0;
   if (active) {
-    ct = cs[2 * t];
-    st = cs[2 * t + 1];
-    const double2 tip = crank_tip(H, C, ct, st);
-    W.p32(1) = make_float2((float)tip.x, (float)tip.y);
+    const float2 c = cs32[t];
+    W.p32(1) = make_float2(fmaf(C.r1f, c.x, C.p0f.x), fmaf(C.r1f, c.y, C.p0f.y));
     const float tau = C.tau;
     unsigned char* col = W.cols + W.lane * 8;
+    int s = 0;
 #pragma unroll 1
-    for (int s = 0; s < C.ns; ++s) {
+    for (; s < C.ns; ++s) {
       const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
       const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].br);
       const float2 pa = *reinterpret_cast<const float2*>(col + g1.y);
@@ -209,12 +215,20 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
       *reinterpret_cast<float2*>(col + g1.w) =
           make_float2(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)));
     }
+    ++ctr.lane_angles;
+    ctr.lane_dyads += (unsigned)(s < C.ns ? s + 1 : C.ns);
   }
-  if (__any_sync(FULL, fix)) {
-    if (fix) {
-      lk = replay_f64_local(W, C, ct, st);
-      ++n_fix;
+  const unsigned certain = __ballot_sync(FULL, active && lk >= 0 && !fix);
+  const unsigned below = certain ? ((1u << (__ffs(certain) - 1)) - 1u) : FULL;
+  const unsigned need = __ballot_sync(FULL, active && fix) & below;
+  if (need) {
+    if ((need >> W.lane) & 1u) {
+      lk = replay_f64_local(W, C, cs[2 * t], cs[2 * t + 1]);
+      ++ctr.fix_lanes;
     }
+    if (W.lane == 0) ++ctr.replay_rounds;
+  } else if (active && fix) {
+    lk = -1;  // above a certain lock: irrelevant to this round's outcome
   }
   return lk;
 }
@@ -267,21 +281,28 @@ __host__ __device__ constexpr size_t col_bytes() {
 }
 
 template <bool WRITE, bool SCREEN64>
-__global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, int njmax) {
+__global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p, int njmax) {
   extern __shared__ __align__(16) unsigned char sim_smem_raw[];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
+  const int T = p.T;
+  // fp32 copy of the crank table for the screen rounds (f64 stays global)
+  float2* cs32 = reinterpret_cast<float2*>(sim_smem_raw);
+  const size_t cs_bytes = ((size_t)T * sizeof(float2) + 15) & ~(size_t)15;
+  for (int t = threadIdx.x; t < T; t += SIM_THREADS)
+    cs32[t] = make_float2((float)p.crank_cs[2 * t], (float)p.crank_cs[2 * t + 1]);
+  __syncthreads();
   const size_t per_warp = sizeof(WarpHead) + (size_t)njmax * 32 * col_bytes<WRITE, SCREEN64>();
   Warp W;
-  W.h = reinterpret_cast<WarpHead*>(sim_smem_raw + per_warp * w);
-  W.cols = sim_smem_raw + per_warp * w + sizeof(WarpHead);
+  W.h = reinterpret_cast<WarpHead*>(sim_smem_raw + cs_bytes + per_warp * w);
+  W.cols = sim_smem_raw + cs_bytes + per_warp * w + sizeof(WarpHead);
   W.lane = lane;
   WarpHead& H = *W.h;
   const long long nwarps = (long long)gridDim.x * SIM_WARPS;
-  const int T = p.T;
   const bool coarse = !(p.flags & LA_SIM_NO_COARSE) && (T % 4 == 0) && T >= 8;
   const bool gate_only = (p.flags & LA_SIM_GATE_ONLY) != 0;
-  unsigned long long n_fix = 0, n_angles = 0, n_dyads = 0, n_cand = 0;
+  Ctr ctr;
+  unsigned long long n_angles = 0, n_dyads = 0, n_cand = 0;
 
   const long long nitems = p.cand_count ? *p.cand_count : p.B;
   for (long long item = (long long)blockIdx.x * SIM_WARPS + w; item < nitems; item += nwarps) {
@@ -322,9 +343,11 @@ __global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, i
       const double2 pa = H.p0[H.ia[lane]], pb = H.p0[H.ib[lane]], pt = H.p0[H.tg[lane]];
       const double ax = dsub(pt.x, pa.x), ay = dsub(pt.y, pa.y);
       const double bx = dsub(pt.x, pb.x), by = dsub(pt.y, pb.y);
-      // np.hypot in the reference; sqrt of the sum agrees to an ulp
-      const double ra = __dsqrt_rn(dadd(dmul(ax, ax), dmul(ay, ay)));
-      const double rb = __dsqrt_rn(dadd(dmul(bx, bx), dmul(by, by)));
+      // np.hypot in the reference; a Newton-refined sqrt of the sum agrees
+      // to an ulp or two
+      const double a2 = dadd(dmul(ax, ax), dmul(ay, ay)), b2 = dadd(dmul(bx, bx), dmul(by, by));
+      const double ra = a2 > 0.0 ? dmul(a2, rsqrt_f64(a2)) : 0.0;
+      const double rb = b2 > 0.0 ? dmul(b2, rsqrt_f64(b2)) : 0.0;
       const double cross = dsub(dmul(dsub(pb.x, pa.x), dsub(pt.y, pa.y)),
                                 dmul(dsub(pb.y, pa.y), dsub(pt.x, pa.x)));
       const double br = cross >= 0.0 ? 1.0 : -1.0;
@@ -349,7 +372,10 @@ __global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, i
     }
     {
       const double dx = dsub(H.p0[1].x, H.p0[0].x), dy = dsub(H.p0[1].y, H.p0[0].y);
-      C.r1 = __dsqrt_rn(dadd(dmul(dx, dx), dmul(dy, dy)));
+      const double r2 = dadd(dmul(dx, dx), dmul(dy, dy));
+      C.r1 = r2 > 0.0 ? dmul(r2, rsqrt_f64(r2)) : 0.0;
+      C.r1f = (float)C.r1;
+      C.p0f = make_float2((float)H.p0[0].x, (float)H.p0[0].y);
     }
     __syncwarp();
     if (SCREEN64) fill_static64(W);
@@ -358,7 +384,7 @@ __global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, i
 
     auto screen = [&](int t, bool act) -> int {
       if (SCREEN64) return solve64(W, C, p.crank_cs, t, act);
-      return solve32(W, C, p.crank_cs, t, act, n_fix);
+      return solve32(W, C, p.crank_cs, cs32, t, act, ctr);
     };
 
     int first_t = T, first_j = -1, low_t = -1, low_j = -1;
@@ -464,13 +490,21 @@ __global__ void __launch_bounds__(SIM_THREADS) sim_kernel(const la_sim_args p, i
     ++n_cand;
   }
   if (p.counters) {
-    unsigned long long f = n_fix;
-    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(FULL, f, o);
+    unsigned long long f = ctr.fix_lanes, la = ctr.lane_angles, ld = ctr.lane_dyads;
+    const unsigned long long rr = ctr.replay_rounds;
+    for (int o = 16; o > 0; o >>= 1) {
+      f += __shfl_xor_sync(FULL, f, o);
+      la += __shfl_xor_sync(FULL, la, o);
+      ld += __shfl_xor_sync(FULL, ld, o);
+    }
     if (lane == 0) {
       atomicAdd(p.counters + 0, f);
       atomicAdd(p.counters + 1, n_angles);
       atomicAdd(p.counters + 2, n_dyads);
       atomicAdd(p.counters + 3, n_cand);
+      atomicAdd(p.counters + 4, rr);
+      atomicAdd(p.counters + 5, la);
+      atomicAdd(p.counters + 6, ld);
     }
   }
 }
@@ -626,8 +660,10 @@ int la_simulate(const la_sim_args* a, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool f64 = (a->flags & LA_SIM_FP64) != 0;
   const int njmax = a->pos_stride < NJ ? a->pos_stride : NJ;
+  if (a->T > 2048) return fail(LA_ERANGE, "la_simulate: T=%d beyond 2048", a->T);
   const size_t colb = (write || f64) ? sizeof(double2) : sizeof(float2);
-  const size_t smem = (sizeof(WarpHead) + (size_t)njmax * 32 * colb) * SIM_WARPS;
+  const size_t cs_bytes = ((size_t)a->T * sizeof(float2) + 15) & ~(size_t)15;
+  const size_t smem = cs_bytes + (sizeof(WarpHead) + (size_t)njmax * 32 * colb) * SIM_WARPS;
   auto kern = write ? (f64 ? sim_kernel<true, true> : sim_kernel<true, false>)
                     : (f64 ? sim_kernel<false, true> : sim_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -233,6 +233,8 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
     if low:
         out["low_t"] = torch.empty(items, dtype=torch.int32, device=dev)
         out["low_joint"] = torch.empty(items, dtype=torch.int32, device=dev)
+    if counters is not None and (counters.numel() < 8 or counters.dtype != torch.int64 or not counters.is_cuda):
+        raise ValueError("counters must be an int64 CUDA tensor with >= 8 entries")
     flags = 0
     if write_traj:
         flags |= N.LA_SIM_WRITE_TRAJ

@@ -16,7 +16,7 @@ for (lo, hi, cnt_c) in [(6, 8, 16384), (5, 20, 32768)]:
         refs[t] = (sel, O.simulate(mb.pos[sel][:, :p.n], steps, p.fixed, 200, with_margin=True))
     for tau in [0.0, 1e-6, 1e-5, 3e-5, 1e-4, 1e-3]:
         for write in (False, True):
-            cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+            cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
             res = simulate_tensors(dpos, PlanTable(mb.plans), 200, topo=dtopo, traj_stride=20, fixup_tau=tau, counters=cnt, write_traj=write)
             ft = res["first_t"].cpu().numpy(); fj = res["first_joint"].cpu().numpy()
             bad = 0; near = 0; worst = 0.0
