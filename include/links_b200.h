@@ -159,7 +159,10 @@ int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P,
  *   top_*: best k non-hits (d >= threshold) by (d, scan position)
  *   hit_*: first k hits (d < threshold) by scan position
  * Exhaustive top-k is threshold = 0.                                        */
-#define LA_CH_EXPANSION 1u   /* |a|^2+|q|^2-2a.q inner loop + direct re-check */
+#define LA_CH_EXPANSION 1u   /* |a|^2+|q|^2-2a.q inner loop (FFMA2) with a
+                                per-curve rounding bound; curves whose bound
+                                exceeds fixup_below are redone with direct
+                                differences                                  */
 
 typedef struct la_chamfer_args {
   const float* db;            /* (device) [N][P][2] f32 normalised curves     */
@@ -184,8 +187,9 @@ typedef struct la_chamfer_args {
   void* ws;
   size_t ws_bytes;
   uint32_t flags;             /* LA_CH_*                                      */
-  float fixup_below;          /* expansion mode: recompute pairs with d below
-                                 this by direct differences                  */
+  float fixup_below;          /* expansion mode: max tolerated error bound on a
+                                 curve's distance (e.g. 5e-5) before the
+                                 direct-difference recomputation             */
 } la_chamfer_args;
 
 size_t la_chamfer_workspace(const la_chamfer_args* args);

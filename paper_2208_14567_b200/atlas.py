@@ -50,7 +50,8 @@ class RetrievalHit:
 # ------------------------------------------------------------ device scan
 def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None, pos_begin: int = 0,
                  pos_end: int | None = None, id_base: int = 0, pos_base: int = 0, pos_map=None,
-                 exclude_id: int = -1, dense: bool = False, all_d=None, stream=None) -> dict:
+                 exclude_id: int = -1, dense: bool = False, all_d=None, expansion: bool = True,
+                 fix_tol: float = 5e-5, stream=None) -> dict:
     """One la_chamfer_topk launch.
 
     db: (N, P, 2) float32 CUDA tensor; queries: (NQ, Q, 2) float32.  order:
@@ -58,7 +59,11 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     Returns ``top_d``/``top_id``/``top_pos`` (NQ, k): best non-hits by
     (d, pos); ``hit_d``/``hit_id``/``hit_pos``: first k hits (d < threshold)
     by pos; ``n_hits`` (NQ,); ``all_d`` (NQ, N) when ``dense``.
-    Missing entries have id -1 and d = inf.
+    Missing entries have id -1 and d = inf.  ``expansion`` selects the
+    |a|^2+|q|^2-2a.q inner loop (FFMA2) with a per-curve rigorous rounding
+    bound; curves whose bound exceeds ``fix_tol`` are recomputed with direct
+    differences, so every distance is within fix_tol of the exact fp32-input
+    value.
     """
     torch = N.require_cuda()
     lib = N.load()
@@ -103,8 +108,8 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
         setattr(a, name, N.ptr(out.get(name)))
     a.n_hits = out["n_hits"].data_ptr()
     a.all_d = N.ptr(all_d)
-    a.flags = 0
-    a.fixup_below = 0.0
+    a.flags = N.LA_CH_EXPANSION if expansion else 0
+    a.fixup_below = float(fix_tol)
     wsb = int(lib.la_chamfer_workspace(a))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     a.ws, a.ws_bytes = ws.data_ptr(), wsb

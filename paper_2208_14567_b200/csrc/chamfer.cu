@@ -157,38 +157,218 @@ __device__ __forceinline__ void list_init(WarpList& L) {
 }
 
 // ------------------------------------------------------------ fast path
+// Expanded, pair-swizzled database curve in shared memory: for point pairs
+// (2i, 2i+1), centred coordinates a' = a - (0.5, 0.5):
+//   ex[i] = (-2x'_0, -2x'_1, -2y'_0, -2y'_1),  en[i] = (|a'_0|^2, |a'_1|^2)
+// so  w(a, q) = |a'|^2 - 2 a'.q' + |q'|^2 = |a - q|^2  is two FFMA2 + one
+// FADD2 per pair of query slots, and 0.5 * ex recovers -a' exactly for the
+// direct-difference re-check.
+constexpr float FAR_N = 1.0e30f;   // |a'|^2 of padding points: never a minimum
+constexpr float U32 = 5.9604645e-8f;  // 2^-24, fp32 unit roundoff
+
 template <int QS>
-__global__ void __launch_bounds__(CT) chamfer_scan_kernel(const ScanCtx c) {
-  __shared__ __align__(128) float2 buf[CW][2][PMAX];
-  __shared__ __align__(8) uint64_t bars[CW][2];
+struct QueryRegs {
+  static constexpr int NP = QS / 2;
+  float2 qx[NP > 0 ? NP : 1], qy[NP > 0 ? NP : 1], qn[NP > 0 ? NP : 1];
+  float tx = 0.f, ty = 0.f, tn = FAR_N;  // odd tail slot
+  float r2 = 0.f;                        // max |q'|^2
+};
+
+// expanded-form minima for one database point pair (a0 = 2i, a1 = 2i+1)
+template <int QS, bool DIRECT>
+__device__ __forceinline__ void pair_minima(const QueryRegs<QS>& Q, const float4 ex, const float2 en,
+                                            float2 (&cmin)[QS / 2 > 0 ? QS / 2 : 1], float& cmint, float& rm0,
+                                            float& rm1) {
+  constexpr int NP = QS / 2;
+  rm0 = INFINITY;
+  rm1 = INFINITY;
+#pragma unroll
+  for (int s = 0; s < NP; ++s) {
+    float2 w0, w1;
+    if (DIRECT) {
+      const float2 dx0 = __ffma2_rn(make_float2(ex.x, ex.x), make_float2(0.5f, 0.5f), Q.qx[s]);
+      const float2 dy0 = __ffma2_rn(make_float2(ex.z, ex.z), make_float2(0.5f, 0.5f), Q.qy[s]);
+      const float2 dx1 = __ffma2_rn(make_float2(ex.y, ex.y), make_float2(0.5f, 0.5f), Q.qx[s]);
+      const float2 dy1 = __ffma2_rn(make_float2(ex.w, ex.w), make_float2(0.5f, 0.5f), Q.qy[s]);
+      w0 = __ffma2_rn(dy0, dy0, __fmul2_rn(dx0, dx0));
+      w1 = __ffma2_rn(dy1, dy1, __fmul2_rn(dx1, dx1));
+    } else {
+      w0 = __fadd2_rn(__ffma2_rn(Q.qy[s], make_float2(ex.z, ex.z),
+                                 __ffma2_rn(Q.qx[s], make_float2(ex.x, ex.x), make_float2(en.x, en.x))),
+                      Q.qn[s]);
+      w1 = __fadd2_rn(__ffma2_rn(Q.qy[s], make_float2(ex.w, ex.w),
+                                 __ffma2_rn(Q.qx[s], make_float2(ex.y, ex.y), make_float2(en.y, en.y))),
+                      Q.qn[s]);
+    }
+    cmin[s].x = min3f(cmin[s].x, w0.x, w1.x);
+    cmin[s].y = min3f(cmin[s].y, w0.y, w1.y);
+    rm0 = min3f(rm0, w0.x, w0.y);
+    rm1 = min3f(rm1, w1.x, w1.y);
+  }
+  if (QS & 1) {
+    // tail slot against both points at once: pairs over (a0, a1)
+    float2 w;
+    if (DIRECT) {
+      const float2 dx = __ffma2_rn(make_float2(ex.x, ex.y), make_float2(0.5f, 0.5f), make_float2(Q.tx, Q.tx));
+      const float2 dy = __ffma2_rn(make_float2(ex.z, ex.w), make_float2(0.5f, 0.5f), make_float2(Q.ty, Q.ty));
+      w = __ffma2_rn(dy, dy, __fmul2_rn(dx, dx));
+    } else {
+      w = __fadd2_rn(__ffma2_rn(make_float2(Q.ty, Q.ty), make_float2(ex.z, ex.w),
+                                __ffma2_rn(make_float2(Q.tx, Q.tx), make_float2(ex.x, ex.y), en)),
+                     make_float2(Q.tn, Q.tn));
+    }
+    cmint = min3f(cmint, w.x, w.y);
+    rm0 = fminf(rm0, w.x);
+    rm1 = fminf(rm1, w.y);
+  }
+}
+
+// |sqrt(m_true) - sqrt(m)| bound when |m_true - m| <= delta
+__device__ __forceinline__ float sqrt_err(float m, float delta) {
+  return sqrtf(fmaxf(m, 0.f) + delta) - sqrtf(fmaxf(m - delta, 0.f));
+}
+
+// One curve against the register-resident query: returns the chamfer value
+// and (EXPANSION) a rigorous bound on its fp32 expansion error.
+template <int QS, bool DIRECT>
+__device__ __forceinline__ float curve_chamfer(const QueryRegs<QS>& Q, const float4* __restrict__ ex,
+                                               const float2* __restrict__ en, int P, int Q_, int lane,
+                                               float delta, float& err, float* rowbuf) {
+  constexpr int NP = QS / 2;
+  float2 cmin[NP > 0 ? NP : 1];
+#pragma unroll
+  for (int s = 0; s < NP; ++s) cmin[s] = make_float2(INFINITY, INFINITY);
+  float cmint = INFINITY;
+  float row_sum = 0.f, row_err = 0.f;
+  const int Ppad = (P + 31) & ~31;
+  const bool leader = lane == 0;
+#pragma unroll 1
+  for (int a0 = 0; a0 < Ppad; a0 += 32) {
+#pragma unroll
+    for (int u = 0; u < 32; u += 2) {
+      const int i = (a0 + u) >> 1;
+      float rm0, rm1;
+      pair_minima<QS, DIRECT>(Q, ex[i], en[i], cmin, cmint, rm0, rm1);
+      // signed-int REDUX on the float bits: any negative rounding residue
+      // (expansion form) sorts below every positive value and is clamped
+      // to zero after the chunk
+      const int r0 = __reduce_min_sync(FULL, __float_as_int(rm0));
+      const int r1 = __reduce_min_sync(FULL, __float_as_int(rm1));
+      if (leader) {
+        rowbuf[u] = __int_as_float(r0);
+        rowbuf[u + 1] = __int_as_float(r1);
+      }
+    }
+    __syncwarp();
+    const float mine = fmaxf(rowbuf[lane], 0.f);
+    __syncwarp();
+    if (a0 + lane < P) {
+      row_sum += sqrtf(mine);
+      if (!DIRECT) row_err += sqrt_err(mine, delta);
+    }
+  }
+  float col_sum = 0.f, col_err = 0.f;
+#pragma unroll
+  for (int s = 0; s < NP; ++s) {
+    if (lane + 32 * (2 * s) < Q_) {
+      col_sum += sqrtf(fmaxf(cmin[s].x, 0.f));
+      if (!DIRECT) col_err += sqrt_err(cmin[s].x, delta);
+    }
+    if (lane + 32 * (2 * s + 1) < Q_) {
+      col_sum += sqrtf(fmaxf(cmin[s].y, 0.f));
+      if (!DIRECT) col_err += sqrt_err(cmin[s].y, delta);
+    }
+  }
+  if ((QS & 1) && lane + 32 * (QS - 1) < Q_) {
+    col_sum += sqrtf(fmaxf(cmint, 0.f));
+    if (!DIRECT) col_err += sqrt_err(cmint, delta);
+  }
+  if (!DIRECT) err = warp_sum(row_err) / (float)P + warp_sum(col_err) / (float)Q_;
+  return warp_sum(row_sum) / (float)P + warp_sum(col_sum) / (float)Q_;
+}
+
+template <int QS>
+__device__ void load_query(QueryRegs<QS>& Q, const float2* __restrict__ qsrc, int Qn, int lane) {
+  constexpr int NP = QS / 2;
+  float qr2 = 0.f;
+#pragma unroll
+  for (int s = 0; s < NP; ++s) {
+    const int i0 = lane + 32 * (2 * s), i1 = lane + 32 * (2 * s + 1);
+    float2 v0 = make_float2(BIG, BIG), v1 = make_float2(BIG, BIG);
+    float n0 = FAR_N, n1 = FAR_N;
+    if (i0 < Qn) {
+      v0 = qsrc[i0];
+      v0.x -= 0.5f;
+      v0.y -= 0.5f;
+      n0 = fmaf(v0.y, v0.y, v0.x * v0.x);
+      qr2 = fmaxf(qr2, n0);
+    }
+    if (i1 < Qn) {
+      v1 = qsrc[i1];
+      v1.x -= 0.5f;
+      v1.y -= 0.5f;
+      n1 = fmaf(v1.y, v1.y, v1.x * v1.x);
+      qr2 = fmaxf(qr2, n1);
+    }
+    Q.qx[s] = make_float2(v0.x, v1.x);
+    Q.qy[s] = make_float2(v0.y, v1.y);
+    Q.qn[s] = make_float2(n0, n1);
+  }
+  if (QS & 1) {
+    const int it = lane + 32 * (QS - 1);
+    Q.tx = BIG;
+    Q.ty = BIG;
+    Q.tn = FAR_N;
+    if (it < Qn) {
+      Q.tx = qsrc[it].x - 0.5f;
+      Q.ty = qsrc[it].y - 0.5f;
+      Q.tn = fmaf(Q.ty, Q.ty, Q.tx * Q.tx);
+      qr2 = fmaxf(qr2, Q.tn);
+    }
+  }
+  Q.r2 = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(qr2)));
+}
+
+// rare path: direct differences for a curve whose expansion error bound is
+// too large (near-duplicates); own register file, query reloaded from L2
+template <int QS>
+__device__ __noinline__ float direct_chamfer(const float2* __restrict__ qsrc, int Qn, const float4* ex,
+                                             const float2* en, int P, int lane, float* rowbuf) {
+  QueryRegs<QS> Q;
+  load_query<QS>(Q, qsrc, Qn, lane);
+  float dummy;
+  return curve_chamfer<QS, true>(Q, ex, en, P, Qn, lane, 0.f, dummy, rowbuf);
+}
+
+constexpr size_t SCAN_SMEM_PER_WARP =
+    2 * PMAX * sizeof(float2) + (PMAX / 2) * (sizeof(float4) + sizeof(float2)) + 32 * sizeof(float);
+constexpr size_t SCAN_SMEM = CW * SCAN_SMEM_PER_WARP + CW * 2 * sizeof(uint64_t);
+
+template <int QS>
+__global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
+  extern __shared__ __align__(128) unsigned char scan_smem[];
+  auto raw = reinterpret_cast<float2(*)[2][PMAX]>(scan_smem);                                  // [CW][2][PMAX]
+  auto exs = reinterpret_cast<float4(*)[PMAX / 2]>(scan_smem + CW * 2 * PMAX * sizeof(float2));  // [CW][PMAX/2]
+  auto ens = reinterpret_cast<float2(*)[PMAX / 2]>(scan_smem + CW * 2 * PMAX * sizeof(float2) +
+                                                   CW * (PMAX / 2) * sizeof(float4));
+  float* rowbuf = reinterpret_cast<float*>(scan_smem + CW * 2 * PMAX * sizeof(float2) +
+                                           CW * (PMAX / 2) * (sizeof(float4) + sizeof(float2))) +
+                  32 * (threadIdx.x >> 5);
+  auto bars = reinterpret_cast<uint64_t(*)[2]>(scan_smem + CW * SCAN_SMEM_PER_WARP);
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int qi = blockIdx.y;
   const la_chamfer_args& A = c.a;
-  const int P = A.P, Q = A.Q;
+  const int P = A.P, Qn = A.Q;
   const int gw = blockIdx.x * CW + w;
   const long long stride = (long long)gridDim.x * CW;
+  const bool expansion = (A.flags & LA_CH_EXPANSION) != 0;
+  const float fix_tol = A.fixup_below;
 
-  // query slots in registers (packed pairs), padding far away
-  constexpr int NP = QS / 2;
-  float2 qx2[NP > 0 ? NP : 1], qy2[NP > 0 ? NP : 1];
-  float qxt = BIG, qyt = BIG;  // odd tail slot
-  const float2* qsrc = reinterpret_cast<const float2*>(A.queries) + (size_t)qi * Q;
-#pragma unroll
-  for (int s = 0; s < NP; ++s) {
-    const int i0 = lane + 32 * (2 * s), i1 = lane + 32 * (2 * s + 1);
-    const float2 v0 = i0 < Q ? qsrc[i0] : make_float2(BIG, BIG);
-    const float2 v1 = i1 < Q ? qsrc[i1] : make_float2(BIG, BIG);
-    qx2[s] = make_float2(v0.x, v1.x);
-    qy2[s] = make_float2(v0.y, v1.y);
-  }
-  if (QS & 1) {
-    const int it = lane + 32 * (QS - 1);
-    if (it < Q) {
-      qxt = qsrc[it].x;
-      qyt = qsrc[it].y;
-    }
-  }
+  // query slots in registers, centred at (0.5, 0.5); padding far away
+  QueryRegs<QS> Q;
+  const float2* qsrc = reinterpret_cast<const float2*>(A.queries) + (size_t)qi * Qn;
+  load_query<QS>(Q, qsrc, Qn, lane);
 
   WarpList top, hit;
   list_init(top);
@@ -197,7 +377,9 @@ __global__ void __launch_bounds__(CT) chamfer_scan_kernel(const ScanCtx c) {
 
   const long long first = A.pos_begin + gw;
   const long long count = first < A.pos_end ? (A.pos_end - first + stride - 1) / stride : 0;
+  const bool use_tma = (P % 2) == 0;
   const uint32_t bytes = (uint32_t)P * 8u;
+  const int Ppad = (P + 31) & ~31;
   if (lane == 0) {
     mbar_init(&bars[w][0], 1);
     mbar_init(&bars[w][1], 1);
@@ -205,79 +387,74 @@ __global__ void __launch_bounds__(CT) chamfer_scan_kernel(const ScanCtx c) {
   }
   __syncwarp();
   auto rec_of = [&](long long pos) -> long long { return A.order ? A.order[pos] : pos; };
-  if (count > 0 && lane == 0) {
+  if (use_tma && count > 0 && lane == 0) {
     const long long id = rec_of(first);
     mbar_expect_tx(&bars[w][0], bytes);
-    tma_load_1d(&buf[w][0][0], A.db + (size_t)id * P * 2, bytes, &bars[w][0]);
+    tma_load_1d(&raw[w][0][0], A.db + (size_t)id * P * 2, bytes, &bars[w][0]);
   }
-  uint32_t phase = 0;  // bit b: parity of buffer b
+  uint32_t phase = 0;
 
   for (long long it = 0; it < count; ++it) {
     const int bi = (int)(it & 1);
     const long long pos = first + it * stride;
     const long long id = rec_of(pos);
     __syncwarp();
-    if (it + 1 < count && lane == 0) {
-      fence_proxy_async();
-      const long long nid = rec_of(pos + stride);
-      mbar_expect_tx(&bars[w][bi ^ 1], bytes);
-      tma_load_1d(&buf[w][bi ^ 1][0], A.db + (size_t)nid * P * 2, bytes, &bars[w][bi ^ 1]);
-    }
-    mbar_wait(&bars[w][bi], (phase >> bi) & 1u);
-    phase ^= (1u << bi);
-    if (id == A.exclude_id) continue;
-
-    float2 cmin[NP > 0 ? NP : 1];
-#pragma unroll
-    for (int s = 0; s < NP; ++s) cmin[s] = make_float2(INFINITY, INFINITY);
-    float cmint = INFINITY;
-    float row_sum = 0.0f;
-    const float4* cur = reinterpret_cast<const float4*>(&buf[w][bi][0]);
-#pragma unroll 1
-    for (int a0 = 0; a0 < P; a0 += 32) {
-      float mine = 0.0f;
-#pragma unroll
-      for (int u = 0; u < 32; u += 2) {
-        if (a0 + u < P) {
-          const float4 pp = cur[(a0 + u) >> 1];
-          const float2 ax0 = make_float2(-pp.x, -pp.x), ay0 = make_float2(-pp.y, -pp.y);
-          const float2 ax1 = make_float2(-pp.z, -pp.z), ay1 = make_float2(-pp.w, -pp.w);
-          float rm0 = INFINITY, rm1 = INFINITY;
-#pragma unroll
-          for (int s = 0; s < NP; ++s) {
-            const float2 dx0 = __fadd2_rn(qx2[s], ax0), dy0 = __fadd2_rn(qy2[s], ay0);
-            const float2 dx1 = __fadd2_rn(qx2[s], ax1), dy1 = __fadd2_rn(qy2[s], ay1);
-            const float2 d0 = __ffma2_rn(dy0, dy0, __fmul2_rn(dx0, dx0));
-            const float2 d1 = __ffma2_rn(dy1, dy1, __fmul2_rn(dx1, dx1));
-            cmin[s].x = min3f(cmin[s].x, d0.x, d1.x);
-            cmin[s].y = min3f(cmin[s].y, d0.y, d1.y);
-            rm0 = min3f(rm0, d0.x, d0.y);
-            rm1 = min3f(rm1, d1.x, d1.y);
-          }
-          if (QS & 1) {
-            const float ex0 = qxt - pp.x, ey0 = qyt - pp.y;
-            const float ex1 = qxt - pp.z, ey1 = qyt - pp.w;
-            const float e0 = fmaf(ey0, ey0, ex0 * ex0), e1 = fmaf(ey1, ey1, ex1 * ex1);
-            cmint = min3f(cmint, e0, e1);
-            rm0 = fminf(rm0, e0);
-            rm1 = fminf(rm1, e1);
-          }
-          const float r0 = __uint_as_float(__reduce_min_sync(FULL, __float_as_uint(rm0)));
-          const float r1 = __uint_as_float(__reduce_min_sync(FULL, __float_as_uint(rm1)));
-          if (lane == u) mine = r0;
-          if (lane == u + 1) mine = r1;
-        }
+    const float2* cur;
+    if (use_tma) {
+      if (it + 1 < count && lane == 0) {
+        fence_proxy_async();
+        const long long nid = rec_of(pos + stride);
+        mbar_expect_tx(&bars[w][bi ^ 1], bytes);
+        tma_load_1d(&raw[w][bi ^ 1][0], A.db + (size_t)nid * P * 2, bytes, &bars[w][bi ^ 1]);
       }
-      if (a0 + lane < P) row_sum += sqrtf(mine);
+      mbar_wait(&bars[w][bi], (phase >> bi) & 1u);
+      phase ^= (1u << bi);
+      cur = &raw[w][bi][0];
+    } else {
+      const float2* src = reinterpret_cast<const float2*>(A.db) + (size_t)id * P;
+      for (int k = lane; k < P; k += 32) raw[w][0][k] = src[k];
+      __syncwarp();
+      cur = &raw[w][0][0];
     }
-    float col_sum = 0.0f;
-#pragma unroll
-    for (int s = 0; s < NP; ++s) {
-      if (lane + 32 * (2 * s) < Q) col_sum += sqrtf(cmin[s].x);
-      if (lane + 32 * (2 * s + 1) < Q) col_sum += sqrtf(cmin[s].y);
+    if (id == A.exclude_id) continue;
+    // expand + swizzle (each lane handles pairs lane, lane+32, ...)
+    float ar2 = 0.f;
+    for (int i = lane; i < Ppad / 2; i += 32) {
+      // padding points sit far away in both forms (-0.5*ex = 1e18, |a'|^2 = 1e30)
+      float4 e4 = make_float4(-2.f * BIG, -2.f * BIG, -2.f * BIG, -2.f * BIG);
+      float2 n2 = make_float2(FAR_N, FAR_N);
+      if (2 * i < P) {
+        const float2 p0 = cur[2 * i];
+        const float x = p0.x - 0.5f, y = p0.y - 0.5f;
+        e4.x = -2.f * x;
+        e4.z = -2.f * y;
+        n2.x = fmaf(y, y, x * x);
+        ar2 = fmaxf(ar2, n2.x);
+      }
+      if (2 * i + 1 < P) {
+        const float2 p1 = cur[2 * i + 1];
+        const float x = p1.x - 0.5f, y = p1.y - 0.5f;
+        e4.y = -2.f * x;
+        e4.w = -2.f * y;
+        n2.y = fmaf(y, y, x * x);
+        ar2 = fmaxf(ar2, n2.y);
+      }
+      exs[w][i] = e4;
+      ens[w][i] = n2;
     }
-    if ((QS & 1) && lane + 32 * (QS - 1) < Q) col_sum += sqrtf(cmint);
-    const float d = warp_sum(row_sum) / (float)P + warp_sum(col_sum) / (float)Q;
+    ar2 = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(ar2)));
+    __syncwarp();
+    float d;
+    if (expansion) {
+      // rounding of the FFMA2/FADD2 chain is <= 18 u R^2
+      const float delta = 20.f * U32 * fmaxf(ar2, Q.r2);
+      float err = 0.f;
+      d = curve_chamfer<QS, false>(Q, exs[w], ens[w], P, Qn, lane, delta, err, rowbuf);
+      if (!(err <= fix_tol)) d = direct_chamfer<QS>(qsrc, Qn, exs[w], ens[w], P, lane, rowbuf);
+    } else {
+      float dummy;
+      d = curve_chamfer<QS, true>(Q, exs[w], ens[w], P, Qn, lane, 0.f, dummy, rowbuf);
+    }
     if (A.all_d && lane == 0) A.all_d[(size_t)qi * A.N + id] = d;
     const long long rpos = A.pos_map ? A.pos_map[pos] : pos + A.pos_base;
     consider(top, hit, nhit, c, lane, d, rpos, id + A.id_base);
@@ -441,7 +618,7 @@ struct Plan {
 Plan make_plan(const la_chamfer_args* a) {
   Plan p{};
   const long long npos = a->pos_end - a->pos_begin;
-  p.fast = (a->P % 2 == 0) && a->P <= PMAX && a->Q <= 256 && a->Q >= 1;
+  p.fast = a->P <= PMAX && a->Q <= 256 && a->Q >= 1;
   p.qs = (a->Q + 31) / 32;
   int sms = sm_count();
   if (sms <= 0) sms = 148;
@@ -505,8 +682,12 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
   const dim3 grid(p.grid, a->NQ);
   if (p.fast) {
     switch (p.qs) {
-#define LA_CASE(QSV) \
-  case QSV: chamfer_scan_kernel<QSV><<<grid, CT, 0, s>>>(c); break;
+#define LA_CASE(QSV)                                                                                   \
+  case QSV:                                                                                            \
+    cudaFuncSetAttribute(chamfer_scan_kernel<QSV>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                         (int)SCAN_SMEM);                                                             \
+    chamfer_scan_kernel<QSV><<<grid, CT, SCAN_SMEM, s>>>(c);                                          \
+    break;
       LA_CASE(1) LA_CASE(2) LA_CASE(3) LA_CASE(4) LA_CASE(5) LA_CASE(6) LA_CASE(7) LA_CASE(8)
 #undef LA_CASE
       default: return fail(LA_ERANGE, "la_chamfer_topk: Q=%d", a->Q);
