@@ -26,6 +26,7 @@ LA_SIM_NO_COARSE = 8
 LA_SIM_TRAJ_F64 = 16
 
 LA_CH_EXPANSION = 1
+LA_CH_SCALAR_PIPE = 2
 
 EXPORTS = (
     "la_simulate",

@@ -174,8 +174,10 @@ struct QueryRegs {
   float r2 = 0.f;                        // max |q'|^2
 };
 
-// expanded-form minima for one database point pair (a0 = 2i, a1 = 2i+1)
-template <int QS, bool DIRECT>
+// expanded-form minima for one database point pair (a0 = 2i, a1 = 2i+1).
+// SCALAR selects one-lane FFMA/FADD/FMUL instead of the f32x2 forms (the
+// two issue very differently against FMNMX3 on sm_100a; see tools/micro).
+template <int QS, bool DIRECT, bool SCALAR>
 __device__ __forceinline__ void pair_minima(const QueryRegs<QS>& Q, const float4 ex, const float2 en,
                                             float2 (&cmin)[QS / 2 > 0 ? QS / 2 : 1], float& cmint, float& rm0,
                                             float& rm1) {
@@ -185,7 +187,20 @@ __device__ __forceinline__ void pair_minima(const QueryRegs<QS>& Q, const float4
 #pragma unroll
   for (int s = 0; s < NP; ++s) {
     float2 w0, w1;
-    if (DIRECT) {
+    if (SCALAR) {
+      if (DIRECT) {
+        float dx, dy;
+        dx = fmaf(ex.x, 0.5f, Q.qx[s].x); dy = fmaf(ex.z, 0.5f, Q.qy[s].x); w0.x = fmaf(dy, dy, dx * dx);
+        dx = fmaf(ex.x, 0.5f, Q.qx[s].y); dy = fmaf(ex.z, 0.5f, Q.qy[s].y); w0.y = fmaf(dy, dy, dx * dx);
+        dx = fmaf(ex.y, 0.5f, Q.qx[s].x); dy = fmaf(ex.w, 0.5f, Q.qy[s].x); w1.x = fmaf(dy, dy, dx * dx);
+        dx = fmaf(ex.y, 0.5f, Q.qx[s].y); dy = fmaf(ex.w, 0.5f, Q.qy[s].y); w1.y = fmaf(dy, dy, dx * dx);
+      } else {
+        w0.x = fmaf(Q.qy[s].x, ex.z, fmaf(Q.qx[s].x, ex.x, en.x)) + Q.qn[s].x;
+        w0.y = fmaf(Q.qy[s].y, ex.z, fmaf(Q.qx[s].y, ex.x, en.x)) + Q.qn[s].y;
+        w1.x = fmaf(Q.qy[s].x, ex.w, fmaf(Q.qx[s].x, ex.y, en.y)) + Q.qn[s].x;
+        w1.y = fmaf(Q.qy[s].y, ex.w, fmaf(Q.qx[s].y, ex.y, en.y)) + Q.qn[s].y;
+      }
+    } else if (DIRECT) {
       const float2 dx0 = __ffma2_rn(make_float2(ex.x, ex.x), make_float2(0.5f, 0.5f), Q.qx[s]);
       const float2 dy0 = __ffma2_rn(make_float2(ex.z, ex.z), make_float2(0.5f, 0.5f), Q.qy[s]);
       const float2 dx1 = __ffma2_rn(make_float2(ex.y, ex.y), make_float2(0.5f, 0.5f), Q.qx[s]);
@@ -208,7 +223,18 @@ __device__ __forceinline__ void pair_minima(const QueryRegs<QS>& Q, const float4
   if (QS & 1) {
     // tail slot against both points at once: pairs over (a0, a1)
     float2 w;
-    if (DIRECT) {
+    if (SCALAR) {
+      if (DIRECT) {
+        float dx = fmaf(ex.x, 0.5f, Q.tx), dy = fmaf(ex.z, 0.5f, Q.ty);
+        w.x = fmaf(dy, dy, dx * dx);
+        dx = fmaf(ex.y, 0.5f, Q.tx);
+        dy = fmaf(ex.w, 0.5f, Q.ty);
+        w.y = fmaf(dy, dy, dx * dx);
+      } else {
+        w.x = fmaf(Q.ty, ex.z, fmaf(Q.tx, ex.x, en.x)) + Q.tn;
+        w.y = fmaf(Q.ty, ex.w, fmaf(Q.tx, ex.y, en.y)) + Q.tn;
+      }
+    } else if (DIRECT) {
       const float2 dx = __ffma2_rn(make_float2(ex.x, ex.y), make_float2(0.5f, 0.5f), make_float2(Q.tx, Q.tx));
       const float2 dy = __ffma2_rn(make_float2(ex.z, ex.w), make_float2(0.5f, 0.5f), make_float2(Q.ty, Q.ty));
       w = __ffma2_rn(dy, dy, __fmul2_rn(dx, dx));
@@ -230,7 +256,7 @@ __device__ __forceinline__ float sqrt_err(float m, float delta) {
 
 // One curve against the register-resident query: returns the chamfer value
 // and (EXPANSION) a rigorous bound on its fp32 expansion error.
-template <int QS, bool DIRECT>
+template <int QS, bool DIRECT, bool SCALAR = false>
 __device__ __forceinline__ float curve_chamfer(const QueryRegs<QS>& Q, const float4* __restrict__ ex,
                                                const float2* __restrict__ en, int P, int Q_, int lane,
                                                float delta, float& err, float* rowbuf) {
@@ -248,7 +274,7 @@ __device__ __forceinline__ float curve_chamfer(const QueryRegs<QS>& Q, const flo
     for (int u = 0; u < 32; u += 2) {
       const int i = (a0 + u) >> 1;
       float rm0, rm1;
-      pair_minima<QS, DIRECT>(Q, ex[i], en[i], cmin, cmint, rm0, rm1);
+      pair_minima<QS, DIRECT, SCALAR>(Q, ex[i], en[i], cmin, cmint, rm0, rm1);
       // signed-int REDUX on the float bits: any negative rounding residue
       // (expansion form) sorts below every positive value and is clamped
       // to zero after the chunk
@@ -449,11 +475,17 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
       // rounding of the FFMA2/FADD2 chain is <= 18 u R^2
       const float delta = 20.f * U32 * fmaxf(ar2, Q.r2);
       float err = 0.f;
-      d = curve_chamfer<QS, false>(Q, exs[w], ens[w], P, Qn, lane, delta, err, rowbuf);
+      if (A.flags & LA_CH_SCALAR_PIPE)
+        d = curve_chamfer<QS, false, true>(Q, exs[w], ens[w], P, Qn, lane, delta, err, rowbuf);
+      else
+        d = curve_chamfer<QS, false>(Q, exs[w], ens[w], P, Qn, lane, delta, err, rowbuf);
       if (!(err <= fix_tol)) d = direct_chamfer<QS>(qsrc, Qn, exs[w], ens[w], P, lane, rowbuf);
     } else {
       float dummy;
-      d = curve_chamfer<QS, true>(Q, exs[w], ens[w], P, Qn, lane, 0.f, dummy, rowbuf);
+      if (A.flags & LA_CH_SCALAR_PIPE)
+        d = curve_chamfer<QS, true, true>(Q, exs[w], ens[w], P, Qn, lane, 0.f, dummy, rowbuf);
+      else
+        d = curve_chamfer<QS, true>(Q, exs[w], ens[w], P, Qn, lane, 0.f, dummy, rowbuf);
     }
     if (A.all_d && lane == 0) A.all_d[(size_t)qi * A.N + id] = d;
     const long long rpos = A.pos_map ? A.pos_map[pos] : pos + A.pos_base;

@@ -19,6 +19,8 @@ __global__ void k(float* out, float a, float b, int iters) {
       if (MODE == 6) { x[i].x = fmaf(x[i].x, a, x[(i + 1) & 7].x); s[i] = fminf(fminf(s[i], s[(i + 1) & 7]), s[(i + 2) & 7]); }
       if (MODE == 7) { x[i].x = fmaf(x[i].x, a, x[(i + 1) & 7].x); x[i].y = fmaf(x[i].y, b, x[(i + 2) & 7].y); s[i] = fminf(fminf(s[i], s[(i + 1) & 7]), s[(i + 2) & 7]); }
       if (MODE == 8) { x[i].x = fmaf(x[i].x, a, x[(i + 1) & 7].x); s[i] = fminf(s[i], s[(i + 1) & 7]); }
+      if (MODE == 10) { s[i] = __int_as_float(__reduce_min_sync(0xffffffffu, __float_as_int(s[i]) + i)); }
+      if (MODE == 11) { x[i].x = fmaf(x[i].x, a, x[(i + 1) & 7].x); x[i].y = fmaf(x[i].y, b, x[(i + 2) & 7].y); x[(i+4)&7].x = fmaf(x[i].y, a, x[(i + 3) & 7].x); s[i] = __int_as_float(__reduce_min_sync(0xffffffffu, __float_as_int(s[i]) + i)); }
       if (MODE == 9) { x[i] = __ffma2_rn(x[i], make_float2(s[(i+5)&7], s[(i+5)&7]), make_float2(s[(i+3)&7], s[(i+3)&7])); s[i] = fminf(fminf(s[i], s[(i + 1) & 7]), s[(i + 2) & 7]); }
     }
   }
@@ -35,18 +37,15 @@ template <int MODE> void run(const char* name, int warps) {
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  double instr = 148.0 * warps * iters * 8 * (MODE == 5 || MODE == 6 || MODE == 8 || MODE == 9 ? 2 : MODE == 7 ? 3 : 1);
+  double instr = 148.0 * warps * iters * 8 * (MODE == 5 || MODE == 6 || MODE == 8 || MODE == 9 ? 2 : MODE == 7 ? 3 : MODE == 11 ? 4 : 1);
   double cyc = ms * 1e-3 * clk * 1e3;
   printf("%-28s warps/SM=%2d  warp-instr per SM-cycle = %.3f  (%.1f us)\n", name, warps, instr / 148 / cyc, ms * 1e3);
   cudaFree(out);
 }
 int main() {
   for (int w : {16, 32}) {
-    run<5>("FFMA2 + FMNMX3 mix", w);
-    run<6>("FFMA + FMNMX3 (1:1)", w);
-    run<7>("2 FFMA + FMNMX3 (2:1)", w);
-    run<8>("FFMA + FMNMX (1:1)", w);
-    run<9>("FFMA2 bcast + FMNMX3", w);
+    run<10>("REDUX.MIN.S32", w);
+    run<11>("3 FFMA + REDUX", w);
   }
   return 0;
 }
