@@ -74,10 +74,13 @@ typedef struct la_sim_args {
                                  LA_SIM_TRAJ_F64), or NULL                    */
   const int64_t* traj_row;    /* (device) [B] first row of work item i, or
                                  NULL => i * traj_stride                      */
-  const int64_t* cand;        /* (device, optional) [B] candidate index of work
-                                 item i (gather); outputs stay indexed by i  */
+  const int64_t* cand;        /* (device, optional) [n_cand] candidate index
+                                 of work item i (gather); outputs are indexed
+                                 by i                                        */
+  int64_t n_cand;             /* entries of cand (work items when cand set)   */
   const int64_t* cand_count;  /* (device, optional) number of valid entries of
-                                 cand (<= B), read on device: no host sync    */
+                                 cand (<= n_cand), read on device: no host
+                                 sync                                         */
   int32_t* first_t;           /* (device, optional with cand) [B] first
                                  locking angle, T if valid; -1 (with joint
                                  -2) if the plan has more joints than

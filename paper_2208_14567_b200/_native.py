@@ -71,6 +71,7 @@ class LaSimArgs(C.Structure):
         ("traj", C.c_void_p),
         ("traj_row", C.c_void_p),
         ("cand", C.c_void_p),
+        ("n_cand", C.c_int64),
         ("cand_count", C.c_void_p),
         ("first_t", C.c_void_p),
         ("first_joint", C.c_void_p),

@@ -304,7 +304,11 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
   Ctr ctr;
   unsigned long long n_angles = 0, n_dyads = 0, n_cand = 0;
 
-  const long long nitems = p.cand_count ? *p.cand_count : p.B;
+  long long nitems = p.cand ? p.n_cand : p.B;
+  if (p.cand_count) {
+    const long long c = *p.cand_count;
+    nitems = c < nitems ? c : nitems;
+  }
   for (long long item = (long long)blockIdx.x * SIM_WARPS + w; item < nitems; item += nwarps) {
     const long long b = p.cand ? p.cand[item] : item;
     const int g = p.topo ? p.topo[b] : 0;
@@ -654,9 +658,11 @@ int la_simulate(const la_sim_args* a, void* stream) {
   if (!a->pos0 || !a->plans || !a->crank_cs) return fail(LA_EINVAL, "la_simulate: null buffer");
   if (!a->cand && (!a->first_t || !a->first_joint)) return fail(LA_EINVAL, "la_simulate: null outputs");
   if (a->cand_count && !a->cand) return fail(LA_EINVAL, "la_simulate: cand_count without cand");
+  if (a->cand && a->n_cand < 0) return fail(LA_EINVAL, "la_simulate: bad n_cand");
   const bool write = (a->flags & LA_SIM_WRITE_TRAJ) != 0;
   if (write && !a->traj) return fail(LA_EINVAL, "la_simulate: WRITE_TRAJ without traj");
-  if (a->B == 0) return 0;
+  const long long items = a->cand ? a->n_cand : a->B;
+  if (a->B == 0 || items == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool f64 = (a->flags & LA_SIM_FP64) != 0;
   const int njmax = a->pos_stride < NJ ? a->pos_stride : NJ;
@@ -673,7 +679,7 @@ int la_simulate(const la_sim_args* a, void* stream) {
   if (e != cudaSuccess) return fail((int)e, "la_simulate: occupancy: %s", cudaGetErrorString(e));
   const int sms = sm_count();
   if (sms <= 0) return fail(LA_EINVAL, "la_simulate: no device");
-  long long want = (a->B + SIM_WARPS - 1) / SIM_WARPS;
+  long long want = (items + SIM_WARPS - 1) / SIM_WARPS;
   long long grid = (long long)sms * (occ > 0 ? occ : 1);
   if (grid > want) grid = want;
   const la_sim_args p = *a;

@@ -255,6 +255,7 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
     a.traj = N.ptr(out.get("traj"))
     a.traj_row = N.ptr(traj_row)
     a.cand = N.ptr(cand)
+    a.n_cand = items if cand is not None else 0
     a.cand_count = N.ptr(cand_count)
     a.first_t = out["first_t"].data_ptr()
     a.first_joint = out["first_joint"].data_ptr()

@@ -303,3 +303,32 @@ def test_gate_only_flag(torch, golden):
     assert np.array_equal(ft == 200, g["fb_first_t"] == 200)
     locked = low >= 0
     assert np.array_equal(ft[locked], 4 * low[locked])
+
+
+def test_cand_gather_and_device_count(torch, golden):
+    """Work-item gathering: cand subset (no count) and cand + device count
+    give the full-batch results at the gathered indices."""
+    from paper_2208_14567_b200.solver import PlanTable, SolutionPlan, compile_order, simulate_tensors
+
+    g = golden("solver_golden.npz")
+    plans = []
+    for t in range(len(g["mx_n"])):
+        n = int(g["mx_n"][t])
+        fixed, steps = compile_order(g["mx_adj"][t][:n, :n], g["mx_types"][t][:n])
+        plans.append(SolutionPlan(n, fixed, steps, None, None, None))
+    full = run_mixed(torch, plans, g["mx_pos0"], g["mx_topo"], 200)
+    sel = torch.from_numpy(np.random.default_rng(1).choice(len(g["mx_topo"]), 300, replace=False)).cuda()
+    pos = torch.from_numpy(g["mx_pos0"]).cuda()
+    topo = torch.from_numpy(g["mx_topo"]).cuda()
+    part = simulate_tensors(pos, PlanTable(plans), 200, topo, traj_stride=20, cand=sel)
+    assert torch.equal(part["first_t"], full["first_t"][sel])
+    ok = (part["first_t"] == 200).nonzero().flatten()
+    a = part["traj"].view(300, 20, 200, 2)[ok]
+    b = full["traj"].view(-1, 20, 200, 2)[sel[ok]]
+    for i in range(len(ok)):
+        n = plans[int(g["mx_topo"][int(sel[ok[i]])])].n
+        assert torch.equal(a[i, :n], b[i, :n])
+    cnt = torch.tensor([100], dtype=torch.int64, device="cuda")
+    part2 = simulate_tensors(pos, PlanTable(plans), 200, topo, write_traj=False, cand=sel, cand_count=cnt)
+    torch.cuda.synchronize()
+    assert torch.equal(part2["first_t"][:100], full["first_t"][sel[:100]])

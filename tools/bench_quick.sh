@@ -10,6 +10,9 @@ print([(r["kernel"], round(r["frac"], 3)) for r in d["roofline_kernels"]], d["cl
 s = d["secondary"]
 if "screen" in s:
     print("C3 cand/s %.3e frac %.3f fixups %.4f" % (s["screen"]["value"], s["screen"]["roofline"]["frac"], s["screen"]["fixup_lane_angles"] / s["screen"]["angles_evaluated"]))
+if "end_to_end" in s:
+    e = s["end_to_end"]
+    print("C5 cand/s %.3e" % e["value"], {k: round(v, 3) for k, v in e["stages_ms"].items()}, "valid", e["valid_per_gpu"], "curves", e["curves_per_gpu"], "norm frac %.3f" % e["normalize"]["frac_fp32"], "chamfer pairs/s %.3e" % e["chamfer"]["pairs/s"])
 if "chamfer" in s:
     print("C4 pairs/s %.3e frac %.3f" % (s["chamfer"]["value"], s["chamfer"]["roofline"]["frac"]))
 PY
