@@ -55,7 +55,7 @@ struct __align__(16) StepRec64 {
   double hi;             // (ra + rb) + LOCK_EPS   (solver.py:213, same rounding)
   double lo;             // |ra - rb| - LOCK_EPS
   double ra2;            // ra * ra
-  double rb2;            // rb * rb
+  double c2;             // ra * ra - rb * rb
   double br;             // branch sign
   double _pad;
 };
@@ -114,14 +114,14 @@ __device__ __forceinline__ double rsqrt_f64(double x) {
   return y;
 }
 
-// f64 dyad replay of one angle in the reference's operation order
-// (solver.py:205-231): the lock test d < eps | d > (ra+rb)+eps |
-// d < |ra-rb|-eps with LOCK_EPS = 1e-9 (solver.py:19, 213),
-// x = ((d*d + ra*ra) - rb*rb) / (2d), h = sqrt(max(ra*ra - x*x, 0)),
-// p = p_a + x*u - branch*h*u_perp.  d and 1/d come from one Newton-refined
-// reciprocal square root instead of np.hypot and three IEEE divisions: each
-// differs from the numpy value by an ulp or two (the parity tests hold f64
-// trajectories to 1e-12 of the reference).
+// f64 dyad replay of one angle (solver.py:205-231): the lock test
+// d < eps | d > (ra+rb)+eps | d < |ra-rb|-eps with LOCK_EPS = 1e-9
+// (solver.py:19, 213) on the same f64 bounds, then
+// x = (d*d + ra*ra - rb*rb) / (2d), h = sqrt(max(ra*ra - x*x, 0)),
+// p = p_a + x*u - branch*h*u_perp.  The arithmetic is contracted (DFMA) and
+// d, 1/d, h come from Newton-refined reciprocal square roots instead of
+// np.hypot / IEEE division / sqrt: results differ from numpy's by a few ulp
+// (the parity tests hold f64 trajectories to 1e-12 of the reference).
 template <typename Get, typename Put>
 __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get get, Put put) {
   const double eps = 1e-9;
@@ -130,19 +130,18 @@ __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get
     const int a = H.ia[s], b = H.ib[s], t = H.tg[s];
     const StepRec64& g = H.st64[s];
     const double2 pa = get(a), pb = get(b);
-    const double dx = dsub(pb.x, pa.x);
-    const double dy = dsub(pb.y, pa.y);
-    const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
+    const double dx = pb.x - pa.x;
+    const double dy = pb.y - pa.y;
+    const double d2 = fma(dy, dy, dx * dx);
     const double inv = rsqrt_f64(d2);
-    const double d = dmul(d2, inv);
+    const double d = d2 * inv;
     if (!(d >= eps) || d > g.hi || d < g.lo) return s;
-    const double x = dmul(dsub(dadd(dmul(d, d), g.ra2), g.rb2), dmul(0.5, inv));
-    const double h2 = dsub(g.ra2, dmul(x, x));
-    const double h = h2 > 0.0 ? dmul(h2, rsqrt_f64(h2)) : 0.0;
-    const double ux = dmul(dx, inv), uy = dmul(dy, inv);
-    const double bh = dmul(g.br, h);
-    put(t, make_double2(dsub(dadd(pa.x, dmul(x, ux)), dmul(bh, uy)),
-                        dadd(dadd(pa.y, dmul(x, uy)), dmul(bh, ux))));
+    const double x = fma(d, d, g.c2) * (0.5 * inv);
+    const double h2 = fma(-x, x, g.ra2);
+    const double h = h2 > 0.0 ? h2 * rsqrt_f64(h2) : 0.0;
+    const double xi = x * inv;
+    const double hb = g.br * h * inv;
+    put(t, make_double2(fma(-hb, dy, fma(xi, dx, pa.x)), fma(hb, dx, fma(xi, dy, pa.y))));
   }
   return -1;
 }
@@ -359,7 +358,7 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
       r64.hi = dadd(dadd(ra, rb), 1e-9);
       r64.lo = dsub(fabs(dsub(ra, rb)), 1e-9);
       r64.ra2 = dmul(ra, ra);
-      r64.rb2 = dmul(rb, rb);
+      r64.c2 = dsub(dmul(ra, ra), dmul(rb, rb));
       r64.br = br;
       r64._pad = 0.0;
       H.st64[lane] = r64;
