@@ -153,3 +153,53 @@ def test_scan_threshold_mode_and_shards(torch):
     merged = merge_lists([{k: v.cpu() for k, v in p.items() if not k.startswith("_")} for p in parts], 7)
     for name in ("top_id", "hit_id", "top_pos", "hit_pos", "n_hits"):
         assert torch.equal(merged[name], res[name].cpu()), name
+
+
+def test_retrieve_large_k_and_budget(torch, atlas_fx):
+    g, atlas = atlas_fx
+    q = g["query2"]
+    ref = O.retrieve(g["points"], g["order"], q, 40, 0.25)
+    got = atlas.retrieve(q, k=40, threshold=0.25)
+    ref_d = O.chamfer_direct_block(g["points"], q)
+    assert ids_match([h.mech_id for h in got], None, [r[1] for r in ref], ref_d)
+    assert [h.above_threshold for h in got] == [bool(r[2]) for r in ref] or \
+        any(abs(ref_d[r[1]] - 0.25) < TOL for r in ref)
+    # budgeted scan with the heuristic prefilter only visits the filtered set
+    # (the default filter_mode "exact" scans everything, atlas.py:157-158)
+    hits = atlas.retrieve(q, k=3, budget=50, filter_mode="heuristic")
+    allowed = set(atlas.coarse_filter(q, 50, "heuristic").tolist())
+    assert len(allowed) == 50 and len(hits) == 3
+    assert all(h.mech_id in allowed for h in hits)
+    full = atlas.retrieve(q, k=3, budget=50)
+    assert [h.mech_id for h in full] == [h.mech_id for h in atlas.retrieve(q, k=3)]
+
+
+def test_chamfer_multi_query_and_odd_sizes(torch):
+    from paper_2208_14567_b200.atlas import chamfer_scan
+
+    rng = np.random.default_rng(3)
+    for P, Q in ((199, 200), (64, 31), (256, 256), (9, 5)):
+        db = rng.uniform(size=(500, P, 2)).astype(np.float32)
+        qs = rng.uniform(size=(3, Q, 2)).astype(np.float32)
+        res = chamfer_scan(torch.from_numpy(db).cuda(), torch.from_numpy(qs).cuda(), k=5, dense=True)
+        d = res["all_d"].cpu().numpy()
+        for qi in range(3):
+            want = O.chamfer_direct_block(db.astype(np.float64), qs[qi].astype(np.float64))
+            assert np.max(np.abs(d[qi] - want)) <= 1e-4
+            top = np.lexsort((np.arange(500), d[qi]))[:5]
+            assert res["top_id"][qi].tolist() == top.tolist()
+
+
+def test_chamfer_expansion_mode_bound(torch):
+    """Expansion inner loop with the rigorous rounding bound: every distance
+    within fix_tol of the direct-difference value, near-duplicates re-checked."""
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    db = fourier_db(20000, 200, seed=12, chunk=1 << 14)
+    q = db[:3].clone()
+    q[1] += 1e-4  # near-duplicate of record 1
+    a = chamfer_scan(db, q, k=4, dense=True, expansion=True, fix_tol=5e-5)["all_d"].cpu().numpy()
+    b = chamfer_scan(db, q, k=4, dense=True, expansion=False)["all_d"].cpu().numpy()
+    assert np.max(np.abs(a - b)) <= 5e-5 + 1e-6
+    assert a[0, 0] == 0.0 and a[2, 2] == 0.0

@@ -104,3 +104,34 @@ def test_chamfer_block_shapes(torch, P, Q):
     got = chamfer_block(torch.from_numpy(pts).cuda(), torch.from_numpy(q).cuda()).cpu().numpy()
     want = O.chamfer_direct_block(pts.astype(np.float32).astype(np.float64), q.astype(np.float32).astype(np.float64))
     assert np.max(np.abs(got - want)) <= 1e-4 * np.sqrt(2)
+
+
+@pytest.mark.parametrize("P", [2, 3, 7, 63, 200, 201, 1500])
+def test_normalize_sizes_f64_and_f32(torch, P):
+    from paper_2208_14567_b200.curves import normalize_tensors
+
+    rng = np.random.default_rng(P)
+    t = np.linspace(0, 2 * np.pi, P, endpoint=False)
+    paths = np.stack([np.stack([np.cos(t) * (1 + 0.3 * rng.random()) + 0.1 * np.cos(3 * t + rng.random()),
+                                np.sin(2 * t) * 0.4 + 0.05 * rng.normal(size=P)], 1) for _ in range(4)])
+    r64 = normalize_tensors(torch.from_numpy(paths).cuda())
+    for m in range(4):
+        want = O.normalize(paths[m])
+        assert np.max(np.abs(r64["out"][m].cpu().numpy() - want)) <= 1e-9
+        i, j, d = O.farthest_pair(paths[m])
+        assert tuple(r64["pair"][m].tolist()) == (i, j)
+        assert abs(float(r64["diameter"][m]) - d) <= 1e-12 * max(d, 1.0)
+    r32 = normalize_tensors(torch.from_numpy(paths.astype(np.float32)).cuda())
+    for m in range(4):
+        if int(r32["unstable"][m]) == 0 and O.frame_stability(paths[m].astype(np.float32).astype(np.float64)):
+            want = O.normalize(paths[m].astype(np.float32).astype(np.float64))
+            assert np.max(np.abs(r32["out"][m].cpu().numpy() - want)) <= 1e-4
+
+
+def test_normalize_degenerate_batch_status(torch):
+    from paper_2208_14567_b200.curves import normalize_tensors
+
+    paths = np.zeros((3, 10, 2))
+    paths[1] = np.random.default_rng(0).uniform(size=(10, 2))
+    res = normalize_tensors(torch.from_numpy(paths).cuda())
+    assert res["status"].tolist() == [1, 0, 1]

@@ -332,3 +332,56 @@ def test_cand_gather_and_device_count(torch, golden):
     part2 = simulate_tensors(pos, PlanTable(plans), 200, topo, write_traj=False, cand=sel, cand_count=cnt)
     torch.cuda.synchronize()
     assert torch.equal(part2["first_t"][:100], full["first_t"][sel[:100]])
+
+
+@pytest.mark.parametrize("T", [8, 50, 100, 199, 201, 360])
+def test_other_T_values(torch, golden, T):
+    """Coarse-first order needs T % 4 == 0; other T take the plain order.
+    Flags and f64 paths match the oracle for any T."""
+    from paper_2208_14567_b200.solver import SolutionPlan, compile_order
+
+    g = golden("solver_golden.npz")
+    t = 25  # an n = 18 topology of the fixture
+    n = int(g["mx_n"][t])
+    fixed, steps = compile_order(g["mx_adj"][t][:n, :n], g["mx_types"][t][:n])
+    plan = SolutionPlan(n, fixed, steps, None, None, None)
+    fb = [(s.target, s.a, s.b) for s in steps]
+    pos = g["mx_pos0"][g["mx_topo"] == t][:, :n]
+    # plus the four-bar batch (mostly valid) to exercise the path writes
+    from paper_2208_14567_b200.workloads import bare_plan, four_bar
+
+    for plan_, fb_, fixed_, P in ((plan, fb, fixed, pos), (bare_plan(four_bar()), [(3, 1, 2)], (0, 2),
+                                                           g["fb_pos0"][:64])):
+        ref = O.simulate(P, fb_, fixed_, T, with_margin=True)
+        res = run_mixed(torch, [plan_], P, None, T, traj_f64=True)
+        bad, _ = flag_parity(res["first_t"].cpu().numpy(), res["first_joint"].cpu().numpy(), ref["first_t"],
+                             ref["first_joint"], ref["margin"])
+        assert bad == 0
+        ok = np.flatnonzero((ref["first_t"] == T) & (res["first_t"].cpu().numpy() == T))
+        tr = res["traj"].view(len(P), plan_.n, T, 2).cpu().numpy()
+        if len(ok):
+            assert np.abs(tr[ok] - O.trajectories(ref)[ok]).max() <= F64_TOL
+
+
+def test_edge_cases(torch):
+    from paper_2208_14567_b200 import simulate_batch
+    from paper_2208_14567_b200._native import NativeError
+    from paper_2208_14567_b200.solver import PlanTable, SolutionPlan, simulate_tensors
+    from paper_2208_14567_b200.workloads import bare_plan, four_bar
+
+    plan = bare_plan(four_bar())
+    assert simulate_batch(np.zeros((0, 4, 2)), plan) == []
+    # a plan with more joints than the pose stride is flagged, not read out of bounds
+    big = SolutionPlan(6, (0, 2), plan.steps, None, None, None)
+    pos = torch.rand((3, 4, 2), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        simulate_tensors(pos, PlanTable([big]), 200)
+    with pytest.raises(NativeError):
+        simulate_tensors(pos, PlanTable([plan]), 4096)  # T beyond the compiled limit
+    # coincident joints lock (d < LOCK_EPS), like the reference
+    p = np.array(four_bar().positions0)[None].repeat(2, 0)
+    p[1, 2] = p[1, 1]  # ground joint on the crank tip at t = 0: d(1, 2) = 0 at t = 0
+    ref = O.simulate(p, [(3, 1, 2)], (0, 2), 200)
+    outs = simulate_batch(p, plan, 200)
+    for o, ft in zip(outs, ref["first_t"]):
+        assert (getattr(o, "step", 200)) == ft
