@@ -603,7 +603,8 @@ def run_reference(args):
             "data": "synthetic (seeded reference-generator streams)",
             "config": {"workload": "C2: 100,000 candidates of 6-8 joints, 256 per topology, T=200",
                        "parallelism": f"cpu fork pool x{cb['cores']}"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {"value": value, "unit": "simulations/s", "cores": cb["cores"], "kind": cb["kind"],
+                             "sample": cb["sample"]},
             "e2e": {"value": value, "unit": "simulations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
