@@ -17,6 +17,8 @@
 // best competing distance, which drives the frame-stability flag.  The
 // O(P) frame transform and the variance run in f64.
 #include "common.cuh"
+#include <climits>
+#include <type_traits>
 
 namespace la {
 namespace {
@@ -325,6 +327,242 @@ __global__ void __launch_bounds__(NT) circle_kernel(const void* paths, int64_t M
   }
 }
 
+// ---------------------------------------------------------------------------
+// fp32 batch path: one WARP per curve (P <= 256), two passes over the full
+// P x P distance matrix with register blocking — each lane holds up to 8
+// rows (points l, l+32, ...) packed in f32x2 pairs and every column point is
+// a shared-memory broadcast, so a column costs one LDS for 8 pair distances.
+//   pass 1: M = max d^2 (FMNMX3 chains, REDUX.MAX on the float bits)
+//   pass 2: pairs i < j with d^2 >= M (1 - rel)^2 -> near-max count (frame
+//           stability) and the lexicographically smallest pair with d^2 == M
+// then the f64 frame transform / bbox / half-turn rule / variance with warp
+// shuffles only (no CTA barriers).
+constexpr int NW_WARPS = 8;
+constexpr int NW_PMAX = 256;
+
+__device__ __forceinline__ double warp_min_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_norm_args p) {
+  __shared__ __align__(16) float2 pts[NW_WARPS][NW_PMAX];
+  __shared__ __align__(16) float4 cen[NW_WARPS][NW_PMAX];  // (x', y', |p'|^2, 0), centred at point 0
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int P = p.P;
+  const int R2 = (P + 63) / 64;  // packed row pairs per lane (<= 4)
+  for (long long m = (long long)blockIdx.x * NW_WARPS + w; m < p.M; m += (long long)gridDim.x * NW_WARPS) {
+    const long long row = p.src_row ? p.src_row[m] : m;
+    const float2* src = static_cast<const float2*>(p.paths) + (size_t)row * P;
+    __syncwarp();
+    const float2 o = src[0];
+    for (int k = lane; k < P; k += 32) {
+      const float2 v = src[k];
+      pts[w][k] = v;
+      const float x = v.x - o.x, y = v.y - o.y;
+      cen[w][k] = make_float4(x, y, fmaf(y, y, x * x), 0.f);
+    }
+    __syncwarp();
+    // rows l + 64q and l + 64q + 32 packed as f32x2; padding rows duplicate
+    // point 0 (cannot raise the max; masked in pass 2)
+    float2 xr[4], yr[4], nr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i0 = lane + 64 * q, i1 = i0 + 32;
+      const float4 a = cen[w][(q < R2 && i0 < P) ? i0 : 0], b = cen[w][(q < R2 && i1 < P) ? i1 : 0];
+      xr[q] = make_float2(a.x, b.x);
+      yr[q] = make_float2(a.y, b.y);
+      nr[q] = make_float2(a.z, b.z);
+    }
+    // d^2(i, j) = (|p_i|^2 - 2 p_i.p_j) + |p_j|^2 in the expansion form: two
+    // FFMA2 per row pair, the column's |p_j|^2 added once.  Both passes use
+    // the identical expression, so the pass-1 maximum is reproduced exactly.
+    // Pairs i < j only: row pair q holds rows >= 64q.
+    float M = -INFINITY;
+    // column j needs row pairs q < ceil(j / 64): walk the columns in segments
+    // with a compile-time pair count (predicated-off groups would still issue)
+    auto pass1 = [&](auto NQc, int j0, int j1) {
+      constexpr int NQ = decltype(NQc)::value;
+#pragma unroll 2
+      for (int j = j0; j < j1; ++j) {
+        const float4 c = cen[w][j];
+        const float2 m2x = make_float2(-2.f * c.x, -2.f * c.x), m2y = make_float2(-2.f * c.y, -2.f * c.y);
+        float cm = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const float2 t = __ffma2_rn(yr[q], m2y, __ffma2_rn(xr[q], m2x, nr[q]));
+          cm = fmaxf(fmaxf(cm, t.x), t.y);
+        }
+        M = fmaxf(M, cm + c.z);
+      }
+    };
+    pass1(std::integral_constant<int, 1>{}, 1, min(P, 65));
+    if (R2 >= 2) pass1(std::integral_constant<int, 2>{}, 65, min(P, 129));
+    if (R2 >= 3) pass1(std::integral_constant<int, 3>{}, 129, min(P, 193));
+    if (R2 >= 4) pass1(std::integral_constant<int, 4>{}, 193, P);
+    M = __int_as_float(__reduce_max_sync(FULL, __float_as_int(M)));  // M >= 0 in practice
+    const float thr = (float)((double)M * (1.0 - p.rel_tol) * (1.0 - p.rel_tol));
+    // pass 2: (a) the lexicographically smallest pair with d^2 == M (only
+    // columns whose maximum reaches M are inspected) and (b) whether a
+    // second pair lies within the near-tie band — counting stops as soon as
+    // the warp has seen two (near-circles would otherwise inspect every
+    // column).
+    int cnt = 0, key = INT_MAX;
+    bool two = false;
+    auto pass2 = [&](auto NQc, int j0, int j1) {
+      constexpr int NQ = decltype(NQc)::value;
+#pragma unroll 2
+      for (int j = j0; j < j1; ++j) {
+        const float4 c = cen[w][j];
+        const float2 m2x = make_float2(-2.f * c.x, -2.f * c.x), m2y = make_float2(-2.f * c.y, -2.f * c.y);
+        float2 tv[NQ];
+        float cm = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          tv[q] = __ffma2_rn(yr[q], m2y, __ffma2_rn(xr[q], m2x, nr[q]));
+          cm = fmaxf(fmaxf(cm, tv[q].x), tv[q].y);
+        }
+        const float top = cm + c.z;
+        if (top >= M) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const int i0 = lane + 64 * q, i1 = i0 + 32;
+            if (i0 < j && i0 < P && tv[q].x + c.z == M) key = min(key, i0 * P + j);
+            if (i1 < j && i1 < P && tv[q].y + c.z == M) key = min(key, i1 * P + j);
+          }
+        }
+        const bool near = !two && top >= thr;
+        if (__any_sync(FULL, near)) {
+          if (near) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              const int i0 = lane + 64 * q, i1 = i0 + 32;
+              cnt += (i0 < j && i0 < P && tv[q].x + c.z >= thr) ? 1 : 0;
+              cnt += (i1 < j && i1 < P && tv[q].y + c.z >= thr) ? 1 : 0;
+            }
+          }
+          two = __reduce_add_sync(FULL, cnt) >= 2;
+        }
+      }
+    };
+    pass2(std::integral_constant<int, 1>{}, 1, min(P, 65));
+    if (R2 >= 2) pass2(std::integral_constant<int, 2>{}, 65, min(P, 129));
+    if (R2 >= 3) pass2(std::integral_constant<int, 3>{}, 129, min(P, 193));
+    if (R2 >= 4) pass2(std::integral_constant<int, 4>{}, 193, P);
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+    key = __reduce_min_sync(FULL, key);
+    const int pi_ = key == INT_MAX ? 0 : key / P, pj_ = key == INT_MAX ? 0 : key % P;
+    // ---- f64 frame (curves.py:56-71)
+    const double2 Pi = make_double2(pts[w][pi_].x, pts[w][pi_].y);
+    const double2 Pj = make_double2(pts[w][pj_].x, pts[w][pj_].y);
+    const double vx = Pj.x - Pi.x, vy = Pj.y - Pi.y;
+    const double d = sqrt(vx * vx + vy * vy);
+    if (!(d > 0.0) || !(M > 0.f)) {
+      if (lane == 0) {
+        p.status[m] = 1;
+        if (p.pair) { p.pair[2 * m] = 0; p.pair[2 * m + 1] = 0; }
+        if (p.diameter) p.diameter[m] = 0.0;
+        if (p.unstable) p.unstable[m] = 1;
+        if (p.is_circle) p.is_circle[m] = 0;
+        if (p.circle_var) p.circle_var[m] = 0.0;
+      }
+      continue;
+    }
+    const double id = 1.0 / d;
+    const double c = vx * id, sn = vy * id;
+    auto base = [&](int k) -> double2 {
+      const double u = (double)pts[w][k].x - Pi.x, v = (double)pts[w][k].y - Pi.y;
+      return make_double2((u * c + v * sn) * id, (u * -sn + v * c) * id);
+    };
+    double lox = INFINITY, loy = INFINITY, hix = -INFINITY, hiy = -INFINITY;
+    double ilx = INFINITY, ily = INFINITY, ihx = -INFINITY, ihy = -INFINITY;
+    for (int k = lane; k < P; k += 32) {
+      const double2 b = base(k);
+      lox = fmin(lox, b.x); hix = fmax(hix, b.x);
+      loy = fmin(loy, b.y); hiy = fmax(hiy, b.y);
+      if (p.bbox) {
+        ilx = fmin(ilx, (double)pts[w][k].x); ihx = fmax(ihx, (double)pts[w][k].x);
+        ily = fmin(ily, (double)pts[w][k].y); ihy = fmax(ihy, (double)pts[w][k].y);
+      }
+    }
+    lox = warp_min_d(lox); loy = warp_min_d(loy);
+    hix = warp_max_d(hix); hiy = warp_max_d(hiy);
+    const double mx = (lox + hix) * 0.5, my = (loy + hiy) * 0.5;
+    bool use_a;
+    {
+      const double2 b0 = base(0);
+      const double ex = b0.x - mx, ey = b0.y - my;
+      const double ax = (ex + 0.5) - 0.5, ay = (ey + 0.5) - 0.5;
+      const double bx = (-ex + 0.5) - 0.5, by = (-ey + 0.5) - 0.5;
+      double aa = atan2(ay, ax), ab = atan2(by, bx);
+      if (aa < 0.0) aa += 6.283185307179586;
+      if (ab < 0.0) ab += 6.283185307179586;
+      if (fabs(aa - ab) <= 1e-12) {
+        double ma = 0.0, mb = 0.0;
+        for (int k = lane; k < P; k += 32) {
+          const double e = base(k).y - my;
+          ma += fmax((e + 0.5) - 0.5, 0.0);
+          mb += fmax((-e + 0.5) - 0.5, 0.0);
+        }
+        use_a = warp_sum_d(ma) >= warp_sum_d(mb);
+      } else {
+        use_a = aa < ab;
+      }
+    }
+    double rsum = 0.0;
+    double y0 = 0.0;
+    for (int k = lane; k < P; k += 32) {
+      const double2 b = base(k);
+      const double ex = b.x - mx, ey = b.y - my;
+      const double ox = use_a ? ex + 0.5 : -ex + 0.5;
+      const double oy = use_a ? ey + 0.5 : -ey + 0.5;
+      if (k == 0) y0 = oy;
+      if (p.out_f64) reinterpret_cast<double2*>(p.out)[(size_t)m * P + k] = make_double2(ox, oy);
+      else reinterpret_cast<float2*>(p.out)[(size_t)m * P + k] = make_float2((float)ox, (float)oy);
+      rsum += sqrt((ox - 0.5) * (ox - 0.5) + (oy - 0.5) * (oy - 0.5));
+    }
+    y0 = __shfl_sync(FULL, y0, 0);
+    double var = 0.0;
+    if (p.is_circle || p.circle_var) {
+      const double mean = warp_sum_d(rsum) / (double)P;
+      double acc = 0.0;
+      for (int k = lane; k < P; k += 32) {
+        const double2 b = base(k);
+        const double ex = b.x - mx, ey = b.y - my;
+        const double ox = use_a ? ex + 0.5 : -ex + 0.5;
+        const double oy = use_a ? ey + 0.5 : -ey + 0.5;
+        const double dr = sqrt((ox - 0.5) * (ox - 0.5) + (oy - 0.5) * (oy - 0.5)) - mean;
+        acc += dr * dr;
+      }
+      var = warp_sum_d(acc) / (double)P;
+    }
+    if (p.bbox) {
+      ilx = warp_min_d(ilx); ily = warp_min_d(ily);
+      ihx = warp_max_d(ihx); ihy = warp_max_d(ihy);
+    }
+    if (lane == 0) {
+      p.status[m] = 0;
+      if (p.pair) { p.pair[2 * m] = pi_; p.pair[2 * m + 1] = pj_; }
+      if (p.diameter) p.diameter[m] = d;
+      if (p.is_circle) p.is_circle[m] = var < 5e-4 ? 1 : 0;
+      if (p.circle_var) p.circle_var[m] = var;
+      if (p.unstable) p.unstable[m] = (cnt > 1 || fabs(y0 - 0.5) < p.y_tol) ? 1 : 0;
+      if (p.bbox) {
+        p.bbox[4 * m] = ilx; p.bbox[4 * m + 1] = ily;
+        p.bbox[4 * m + 2] = ihx; p.bbox[4 * m + 3] = ihy;
+      }
+    }
+  }
+}
+
 }  // namespace
 }  // namespace la
 
@@ -360,6 +598,11 @@ extern "C" int la_normalize(const la_norm_args* a, void* stream) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(normalize_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     normalize_kernel<double><<<(unsigned)grid, NT, smem, s>>>(*a);
+  } else if (a->P <= NW_PMAX) {
+    long long g2 = (a->M + NW_WARPS - 1) / NW_WARPS;
+    const long long cap2 = (long long)sms * 8;
+    if (g2 > cap2) g2 = cap2;
+    normalize_warp_kernel<<<(unsigned)g2, NW_WARPS * 32, 0, s>>>(*a);
   } else {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(normalize_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -52,5 +52,17 @@ elif what == "norm":
     raw = fourier_curves_device(200_000, 200, seed=5, dtype=torch.float32)
     for _ in range(reps):
         normalize_tensors(raw)
+elif what == "c5":
+    import bench as B
+
+    class A:
+        steps = 1
+        warmup = 1
+
+    class Clk:
+        timed = False
+
+    out = B.bench_c5(torch, A, 0, 1, {"sm_max_mhz": 1965.0, "hbm_gbs": 6551.7}, lambda: None, Clk)
+    print({k: round(v, 3) for k, v in out["stages_ms"].items()})
 torch.cuda.synchronize()
 print("ok", what)
