@@ -53,6 +53,15 @@ def env_rank():
         int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def load_traffic():
+    """DRAM bytes per launch measured by ncu (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -238,9 +247,11 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
     sm_clock = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12  # TFLOP/s nominal at max clock
     alg_bytes = n_valid_rows * T * 8 + mb.B * (8 + 4) + int(mb.n.sum()) * 16
+    tr = load_traffic().get("sim_kernel_write_c2", {})
     rl_sim = {"kernel": "sim_kernel<WRITE> (fp32 screen + f64 path replay)", "bound": "hbm",
               "achieved": alg_bytes / (k_sim / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-              "algorithmic_bytes": alg_bytes, "ms": k_sim, "traffic": None}
+              "algorithmic_bytes": alg_bytes, "ms": k_sim, "traffic": tr.get("per_launch_bytes"),
+              "traffic_source": "profiles/traffic.json (ncu --set full, same workload)" if tr else None}
     rl_sim["frac"] = rl_sim["achieved"] / rl_sim["peak"]
     screen_flops = DYAD_FLOPS * screen_dyads
     rl_fp32 = {"kernel": "sim_kernel<WRITE> fp32 screen share", "bound": "fp32",
@@ -409,10 +420,16 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
     sm_clock = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12
     flops = PAIR_FLOPS * C4_COUNT
+    trc = load_traffic().get("chamfer_scan_c4_1M", {})
     rl = {"kernel": "chamfer_scan_kernel<7>", "bound": "fp32", "achieved": flops / (kscan / 1e3) / 1e12,
           "peak": fp32_peak, "unit": "TFLOP/s", "frac": flops / (kscan / 1e3) / 1e12 / fp32_peak,
-          "algorithmic_flops": flops, "ms": kscan, "traffic": None,
-          "hbm_bytes_algorithmic": C4_COUNT * C4_P * 8}
+          "algorithmic_flops": flops, "ms": kscan,
+          "traffic": (trc["per_launch_bytes"] / trc["curves"] * C4_COUNT) if trc else None,
+          "traffic_note": "ncu DRAM bytes per curve (1M-curve capture) x curves per launch" if trc else None,
+          "hbm_bytes_algorithmic": C4_COUNT * C4_P * 8,
+          "measured_mix_ceiling_pairs_per_s": 1.40e8,
+          "measured_mix_ceiling_note": "tools/micro/chamfer_inner.cu: FFMA2+FMNMX3 inner loop alone, no row "
+                                       "reduction, 224 slots"}
     # e2e: host query -> scan -> merged top-k back to the host
     qh = q.cpu().pin_memory()
     times = []
