@@ -52,19 +52,20 @@ struct __align__(16) StepRec {
 };
 
 struct __align__(16) StepRec64 {
+  uint32_t idx;          // target | a << 8 | b << 16
+  uint32_t _u;
+  double br;             // branch sign
   double hi;             // (ra + rb) + LOCK_EPS   (solver.py:213, same rounding)
   double lo;             // |ra - rb| - LOCK_EPS
   double ra2;            // ra * ra
   double c2;             // ra * ra - rb * rb
-  double br;             // branch sign
-  double _pad;
 };
 
 struct __align__(16) WarpHead {
   StepRec st[NS];
   StepRec64 st64[NS];
   double2 p0[NJ];        // f64 initial pose
-  int8_t tg[NS], ia[NS], ib[NS];
+  int8_t tg[NS];
   int8_t nstatic;
   int8_t statics[NJ + 1];  // joints that never move (fixed + pivot)
 };
@@ -127,20 +128,27 @@ __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get
   const double eps = 1e-9;
 #pragma unroll 1
   for (int s = 0; s < C.ns; ++s) {
-    const int a = H.ia[s], b = H.ib[s], t = H.tg[s];
     const StepRec64& g = H.st64[s];
+    const uint4 w0 = *reinterpret_cast<const uint4*>(&g);  // idx, _, br
+    const int t = w0.x & 0xff, a = (w0.x >> 8) & 0xff, b = w0.x >> 16;
+    const double br = __hiloint2double((int)w0.w, (int)w0.z);
     const double2 pa = get(a), pb = get(b);
+    const double2 hl = *reinterpret_cast<const double2*>(&g.hi);
+    const double2 rc = *reinterpret_cast<const double2*>(&g.ra2);
     const double dx = pb.x - pa.x;
     const double dy = pb.y - pa.y;
     const double d2 = fma(dy, dy, dx * dx);
     const double inv = rsqrt_f64(d2);
     const double d = d2 * inv;
-    if (!(d >= eps) || d > g.hi || d < g.lo) return s;
-    const double x = fma(d, d, g.c2) * (0.5 * inv);
-    const double h2 = fma(-x, x, g.ra2);
-    const double h = h2 > 0.0 ? h2 * rsqrt_f64(h2) : 0.0;
+    const bool lock = !(d >= eps) | (d > hl.x) | (d < hl.y);
+    if (lock) return s;
+    const double x = fma(d, d, rc.y) * (0.5 * inv);
+    const double h2 = fma(-x, x, rc.x);
+    const double h2c = fmax(h2, 1e-300);
+    const double hh = h2c * rsqrt_f64(h2c);
+    const double h = h2 > 0.0 ? hh : 0.0;
     const double xi = x * inv;
-    const double hb = g.br * h * inv;
+    const double hb = br * h * inv;
     put(t, make_double2(fma(-hb, dy, fma(xi, dx, pa.x)), fma(hb, dx, fma(xi, dy, pa.y))));
   }
   return -1;
@@ -328,10 +336,12 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
     const double* P0 = p.pos0 + (size_t)b * p.pos_stride * 2;
     __syncwarp();
     if (lane < C.n) H.p0[lane] = make_double2(P0[2 * lane], P0[2 * lane + 1]);
+    int it_ = 0, ia_ = 0, ib_ = 0;
     if (lane < C.ns) {
-      H.tg[lane] = pl->step[lane][0];
-      H.ia[lane] = pl->step[lane][1];
-      H.ib[lane] = pl->step[lane][2];
+      it_ = (uint8_t)pl->step[lane][0];
+      ia_ = (uint8_t)pl->step[lane][1];
+      ib_ = (uint8_t)pl->step[lane][2];
+      H.tg[lane] = (int8_t)it_;
     }
     {
       // static joints (1 is the crank tip even if typed Fixed)
@@ -343,7 +353,7 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
     __syncwarp();
     if (lane < C.ns) {
       // plan_geometry (solver.py:105-120), f64
-      const double2 pa = H.p0[H.ia[lane]], pb = H.p0[H.ib[lane]], pt = H.p0[H.tg[lane]];
+      const double2 pa = H.p0[ia_], pb = H.p0[ib_], pt = H.p0[it_];
       const double ax = dsub(pt.x, pa.x), ay = dsub(pt.y, pa.y);
       const double bx = dsub(pt.x, pb.x), by = dsub(pt.y, pb.y);
       // np.hypot in the reference; a Newton-refined sqrt of the sum agrees
@@ -355,12 +365,13 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
                                 dmul(dsub(pb.y, pa.y), dsub(pt.x, pa.x)));
       const double br = cross >= 0.0 ? 1.0 : -1.0;
       StepRec64 r64;
+      r64.idx = (uint32_t)it_ | ((uint32_t)ia_ << 8) | ((uint32_t)ib_ << 16);
+      r64._u = 0;
       r64.hi = dadd(dadd(ra, rb), 1e-9);
       r64.lo = dsub(fabs(dsub(ra, rb)), 1e-9);
       r64.ra2 = dmul(ra, ra);
       r64.c2 = dsub(dmul(ra, ra), dmul(rb, rb));
       r64.br = br;
-      r64._pad = 0.0;
       H.st64[lane] = r64;
       StepRec r;
       r.sp = (float)(ra + rb);
@@ -368,9 +379,9 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
       r.c2 = (float)(ra * ra - rb * rb);
       r.ra2 = (float)ra * (float)ra;
       r.br = (float)br;
-      r.a_off = (uint32_t)H.ia[lane] * 32u * (uint32_t)sizeof(float2);
-      r.b_off = (uint32_t)H.ib[lane] * 32u * (uint32_t)sizeof(float2);
-      r.t_off = (uint32_t)H.tg[lane] * 32u * (uint32_t)sizeof(float2);
+      r.a_off = (uint32_t)ia_ * 32u * (uint32_t)sizeof(float2);
+      r.b_off = (uint32_t)ib_ * 32u * (uint32_t)sizeof(float2);
+      r.t_off = (uint32_t)it_ * 32u * (uint32_t)sizeof(float2);
       H.st[lane] = r;
     }
     {
