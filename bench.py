@@ -3,8 +3,9 @@
 Headline (BASELINE.json metric / configs[1]): mechanism simulations per second
 for 100,000 seeded 6-8-joint candidates per GPU (reference generator streams),
 200 crank angles, all joint paths of the valid ones + lock flags of all
-(one sim_kernel pass: fp32 coarse-first screen, exact first lock, f64 replay
-of the survivors writing fp32 paths; then the ordered valid-candidate list).
+(``simulate_deferred``: fp32 coarse-first screen with exact first lock of the
+locked candidates -> compaction of the coarse survivors -> f64 write-only
+replay writing their fp32 paths densely -> ordered valid-candidate list).
 Secondary lines inside the same JSON object: the validity screen at scale
 (configs[2]) and chamfer curve-pairs/sec (configs[3], 1 query x 10M curves).
 
@@ -45,6 +46,7 @@ DYAD_FLOPS = 21          # FP32 flops per dyad solve
 PAIR_FLOPS = 200_000     # 40,000 point pairs x 5 flops
 L2_FLUSH_BYTES = 512 << 20
 GATE_C3 = os.environ.get("LA_BENCH_C3_EXACT", "0") != "1"
+C2_PIPELINE = os.environ.get("LA_BENCH_C2_PIPELINE", "deferred")
 
 
 # ----------------------------------------------------------------- helpers
@@ -200,17 +202,22 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
     stride = table.max_n
     traj = torch.empty((mb.B * stride, T, 2), dtype=torch.float32, device="cuda")
 
+    from paper_2208_14567_b200.solver import compact_valid, simulate_deferred
+
     def step(timer=None):
+        if timer:
+            timer.mark("start")
+        if C2_PIPELINE == "deferred":
+            # fp32 screen (coarse survivors deferred) -> compaction -> f64
+            # write-only replay of the survivors (dense paths) -> valid list
+            res = simulate_deferred(pos, table, T, topo, traj=traj, timer=timer)
+            return res, res["valid_idx"], res["valid_count"]
         # one pass: coarse fp32 screen, exact first lock for the locked ones,
         # f64 replay + fp32 path stores for the survivors (rows b*stride..),
         # then the ordered list of valid candidates
-        if timer:
-            timer.mark("start")
         res = simulate_tensors(pos, table, T, topo, write_traj=True, traj=traj, traj_stride=stride)
         if timer:
             timer.mark("sim")
-        from paper_2208_14567_b200.solver import compact_valid
-
         idx, cnt = compact_valid(res["first_t"], T)
         if timer:
             timer.mark("compact")
@@ -238,7 +245,10 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
     barrier(torch, world)
     ms = statistics.mean(s["total"] for s in spans)
     ms = max_over_ranks(torch, ms, world)
-    k_sim = statistics.mean(s["sim"] for s in spans)
+    if C2_PIPELINE == "deferred":
+        k_sim = statistics.mean(s["screen"] + s["paths"] for s in spans)
+    else:
+        k_sim = statistics.mean(s["sim"] for s in spans)
     k_compact = statistics.mean(s["compact"] for s in spans)
     value = world * mb.B / (ms / 1e3)
 
@@ -248,7 +258,7 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12  # TFLOP/s nominal at max clock
     alg_bytes = n_valid_rows * T * 8 + mb.B * (8 + 4) + int(mb.n.sum()) * 16
     tr = load_traffic().get("sim_kernel_write_c2", {})
-    rl_sim = {"kernel": "sim_kernel<WRITE> (fp32 screen + f64 path replay)", "bound": "hbm",
+    rl_sim = {"kernel": "sim_kernel screen + write-only (fp32 screen + f64 path replay)", "bound": "hbm",
               "achieved": alg_bytes / (k_sim / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
               "algorithmic_bytes": alg_bytes, "ms": k_sim, "traffic": tr.get("per_launch_bytes"),
               "traffic_source": "profiles/traffic.json (ncu --set full, same workload)" if tr else None}
@@ -260,7 +270,9 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
                "f64_replay_lane_angles": int(cb[0]), "rounds_with_replay": int(cb[4]), "ms": k_sim}
     rl_fp32["frac"] = rl_fp32["achieved"] / rl_fp32["peak"]
     return {
-        "value": value, "ms": ms, "valid": valid, "B": mb.B, "kernels_ms": {"sim": k_sim, "compact": k_compact},
+        "value": value, "ms": ms, "valid": valid, "B": mb.B, "kernels_ms": {"sim": k_sim, "compact": k_compact, **({k: statistics.mean(s_[k] for s_ in spans)
+                                                                  for k in ("screen", "paths")}
+                                                               if C2_PIPELINE == "deferred" else {})},
         "roofline": rl_sim, "roofline_kernels": [rl_sim, rl_fp32],
         "launches_per_step": 4, "mb": mb, "table": table,
     }
@@ -268,9 +280,9 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
 
 def e2e_c2(torch, args, mb, table, world):
     """Same pipeline through the public API with pinned host buffers: H2D of
-    the poses + plan indices, the three kernels, D2H of the flags, the valid
-    count and the valid candidates' paths."""
-    from paper_2208_14567_b200.solver import simulate_compact
+    the poses + plan indices + plan table, the kernels, D2H of the flags of
+    all candidates, and the paths (+ ids) of the coarse survivors."""
+    from paper_2208_14567_b200.solver import simulate_deferred
 
     pos_h = torch.from_numpy(mb.pos).pin_memory()
     topo_h = torch.from_numpy(mb.topo).pin_memory()
@@ -284,18 +296,22 @@ def e2e_c2(torch, args, mb, table, world):
     stream = torch.cuda.current_stream()
     stats = {}
 
+    idx_h = torch.empty(mb.B, dtype=torch.int64).pin_memory()
+
     def step():
         pos = pos_h.cuda(non_blocking=True)
         topo = topo_h.cuda(non_blocking=True)
-        res = simulate_compact(pos, table, T, topo, traj=traj)
+        res = simulate_deferred(pos, table, T, topo, traj=traj)
         ft_h.copy_(res["first_t"], non_blocking=True)
         fj_h.copy_(res["first_joint"], non_blocking=True)
-        cnt_h.copy_(res["valid_count"], non_blocking=True)
+        cnt_h.copy_(res["pend_count"], non_blocking=True)
         stream.synchronize()
-        n = int(cnt_h.item()) * stride
-        out_traj[:n].copy_(traj[:n], non_blocking=True)
+        npend = int(cnt_h.item())
+        n = npend * stride
+        out_traj[:n].copy_(traj[:n], non_blocking=True)          # paths of the coarse survivors
+        idx_h[:npend].copy_(res["pend_idx"][:npend], non_blocking=True)  # their candidate ids
         stats["h2d"] = pos_h.numel() * 8 + topo_h.numel() * 4 + table.G * 64
-        stats["d2h"] = mb.B * 8 + 8 + n * T * 8
+        stats["d2h"] = mb.B * 8 + 8 + n * T * 8 + npend * 8
         return res
 
     for _ in range(max(1, args.warmup)):

@@ -55,6 +55,14 @@ typedef struct la_plan {
                                       search for coarse-locked candidates      */
 #define LA_SIM_NO_COARSE 8u        /* disable the coarse-first angle order     */
 #define LA_SIM_TRAJ_F64 16u        /* traj holds f64 (T,2) rows instead of f32 */
+#define LA_SIM_DEFER 32u           /* screen only: coarse survivors are left
+                                      undecided, first_t = LA_PENDING         */
+#define LA_SIM_SCATTER 64u         /* flags written at the candidate index
+                                      cand[i] instead of the work item i      */
+#define LA_SIM_WRITE_ONLY 128u     /* no screening: all T angles in f64 in
+                                      natural order, exact first lock, paths
+                                      written (needs LA_SIM_WRITE_TRAJ)       */
+#define LA_PENDING (-3)            /* first_t of a deferred coarse survivor    */
 
 /* Batched replay of compiled plans over (candidate x crank angle).
  * Replaces simulate_batch (solver.py:172-239) and, with coarse-first order,

@@ -24,6 +24,10 @@ LA_SIM_FP64 = 2
 LA_SIM_GATE_ONLY = 4
 LA_SIM_NO_COARSE = 8
 LA_SIM_TRAJ_F64 = 16
+LA_SIM_DEFER = 32
+LA_SIM_SCATTER = 64
+LA_SIM_WRITE_ONLY = 128
+LA_PENDING = -3
 
 LA_CH_EXPANSION = 1
 LA_CH_SCALAR_PIPE = 2

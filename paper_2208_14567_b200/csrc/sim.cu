@@ -287,7 +287,7 @@ __host__ __device__ constexpr size_t col_bytes() {
   return (WRITE || SCREEN64) ? sizeof(double2) : sizeof(float2);
 }
 
-template <bool WRITE, bool SCREEN64>
+template <bool WRITE, bool SCREEN64, bool WONLY = false>
 __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p, int njmax) {
   extern __shared__ __align__(16) unsigned char sim_smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -306,8 +306,10 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
   W.lane = lane;
   WarpHead& H = *W.h;
   const long long nwarps = (long long)gridDim.x * SIM_WARPS;
-  const bool coarse = !(p.flags & LA_SIM_NO_COARSE) && (T % 4 == 0) && T >= 8;
+  const bool coarse = !WONLY && !(p.flags & LA_SIM_NO_COARSE) && (T % 4 == 0) && T >= 8;
   const bool gate_only = (p.flags & LA_SIM_GATE_ONLY) != 0;
+  const bool defer = !WRITE && (p.flags & LA_SIM_DEFER) != 0;
+  const bool scatter = (p.flags & LA_SIM_SCATTER) != 0;
   Ctr ctr;
   unsigned long long n_angles = 0, n_dyads = 0, n_cand = 0;
 
@@ -392,12 +394,12 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
       C.p0f = make_float2((float)H.p0[0].x, (float)H.p0[0].y);
     }
     __syncwarp();
-    if (SCREEN64) fill_static64(W);
+    if (SCREEN64 || WONLY) fill_static64(W);
     else fill_static32(W);
     __syncwarp();
 
     auto screen = [&](int t, bool act) -> int {
-      if (SCREEN64) return solve64(W, C, p.crank_cs, t, act);
+      if (SCREEN64 || WONLY) return solve64(W, C, p.crank_cs, t, act);
       return solve32(W, C, p.crank_cs, cs32, t, act, ctr);
     };
 
@@ -442,10 +444,13 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
         }
       }
     }
-    if (!locked) {
+    if (!locked && defer) {
+      first_t = LA_PENDING;  // coarse survivor: decided by a later f64 pass
+      first_j = -1;
+    } else if (!locked) {
       if (WRITE) {
         // all T angles in natural order, f64, coalesced float2 stores
-        if (!SCREEN64) {
+        if (!SCREEN64 && !WONLY) {
           __syncwarp();
           fill_static64(W);
         }
@@ -494,10 +499,11 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
       }
     }
     if (lane == 0) {
-      if (p.first_t) p.first_t[item] = first_t;
-      if (p.first_joint) p.first_joint[item] = first_j;
-      if (p.low_t) p.low_t[item] = low_t;
-      if (p.low_joint) p.low_joint[item] = low_j;
+      const long long o = scatter && p.cand ? p.cand[item] : item;
+      if (p.first_t) p.first_t[o] = first_t;
+      if (p.first_joint) p.first_joint[o] = first_j;
+      if (p.low_t) p.low_t[o] = low_t;
+      if (p.low_joint) p.low_joint[o] = low_j;
     }
     n_angles += 32ull * rounds;
     n_dyads += 32ull * rounds * (unsigned long long)C.ns;
@@ -678,10 +684,14 @@ int la_simulate(const la_sim_args* a, void* stream) {
   const int njmax = a->pos_stride < NJ ? a->pos_stride : NJ;
   if (a->T > 2048) return fail(LA_ERANGE, "la_simulate: T=%d beyond 2048", a->T);
   const size_t colb = (write || f64) ? sizeof(double2) : sizeof(float2);
+  if ((a->flags & LA_SIM_SCATTER) && !a->cand) return fail(LA_EINVAL, "la_simulate: SCATTER needs cand");
   const size_t cs_bytes = ((size_t)a->T * sizeof(float2) + 15) & ~(size_t)15;
   const size_t smem = cs_bytes + (sizeof(WarpHead) + (size_t)njmax * 32 * colb) * SIM_WARPS;
-  auto kern = write ? (f64 ? sim_kernel<true, true> : sim_kernel<true, false>)
-                    : (f64 ? sim_kernel<false, true> : sim_kernel<false, false>);
+  const bool wonly = (a->flags & LA_SIM_WRITE_ONLY) != 0;
+  if (wonly && !write) return fail(LA_EINVAL, "la_simulate: WRITE_ONLY needs WRITE_TRAJ");
+  auto kern = wonly ? sim_kernel<true, false, true>
+              : write ? (f64 ? sim_kernel<true, true> : sim_kernel<true, false>)
+                      : (f64 ? sim_kernel<false, true> : sim_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail((int)e, "la_simulate: smem attr: %s", cudaGetErrorString(e));
   int occ = 0;

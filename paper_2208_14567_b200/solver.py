@@ -191,7 +191,8 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
                      traj=None, traj_stride: int | None = None, traj_row=None, low: bool = False,
                      traj_f64: bool = False, cand=None, cand_count=None,
                      fixup_tau: float = DEFAULT_FIXUP_TAU, fp64: bool = False, gate_only: bool = False,
-                     coarse: bool = True, counters=None, stream=None) -> dict:
+                     coarse: bool = True, counters=None, stream=None, _extra_flags: int = 0,
+                     _outputs=None) -> dict:
     """Launch la_simulate on device tensors.
 
     pos0: (B, S, 2) float64 CUDA tensor (S >= every plan's n); topo: (B,)
@@ -217,10 +218,13 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
     items = B if cand is None else cand.numel()
     if cand is not None:
         cand = cand.to(device=dev, dtype=torch.int64).contiguous()
-    out = {
-        "first_t": torch.empty(items, dtype=torch.int32, device=dev),
-        "first_joint": torch.empty(items, dtype=torch.int32, device=dev),
-    }
+    if _outputs is not None:  # caller-provided flag buffers (scatter mode)
+        out = {"first_t": _outputs[0], "first_joint": _outputs[1]}
+    else:
+        out = {
+            "first_t": torch.empty(items, dtype=torch.int32, device=dev),
+            "first_joint": torch.empty(items, dtype=torch.int32, device=dev),
+        }
     if write_traj:
         if traj is None:
             rows = items * ts if traj_row is None else None
@@ -246,6 +250,7 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
         flags |= N.LA_SIM_NO_COARSE
     if traj_f64:
         flags |= N.LA_SIM_TRAJ_F64
+    flags |= int(_extra_flags)
     a = N.LaSimArgs()
     a.pos0 = pos0.data_ptr()
     a.topo = N.ptr(topo)
@@ -280,6 +285,45 @@ def compact_valid(first_t, T: int, stream=None):
     N.check(lib.la_compact_valid(first_t.data_ptr(), B, T, idx.data_ptr(), cnt.data_ptr(),
                                  ws.data_ptr(), wsb, N.stream_ptr(stream)), "la_compact_valid")
     return idx, cnt
+
+
+def simulate_deferred(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None,
+                      fixup_tau: float = DEFAULT_FIXUP_TAU, stream=None, timer=None) -> dict:
+    """Two specialised launches, no host sync:
+
+    1. fp32 screen (coarse-first, exact first lock for coarse-locked
+       candidates); coarse survivors are left pending (first_t = LA_PENDING);
+    2. ordered compaction of the pending candidates;
+    3. f64 write-only replay of the pending ones (all T angles, exact first
+       lock, fp32 paths written densely: pending item i owns rows
+       [i * stride, (i + 1) * stride)); flags scattered back to the
+       candidates' own slots;
+    4. ordered compaction of the valid candidates.
+
+    Returns first_t / first_joint (B,), pend_idx / pend_count (the row map of
+    ``traj``), valid_idx / valid_count and traj.
+    """
+    torch = N.require_cuda()
+    B, S, _ = pos0.shape
+    stride = table.max_n
+    res = simulate_tensors(pos0, table, T, topo, write_traj=False, fixup_tau=fixup_tau, stream=stream,
+                           _extra_flags=N.LA_SIM_DEFER)
+    if timer:
+        timer.mark("screen")
+    pend, pcnt = compact_valid(res["first_t"], N.LA_PENDING, stream=stream)
+    if traj is None:
+        traj = torch.empty((max(B, 1) * stride, T, 2), dtype=torch.float32, device=pos0.device)
+    simulate_tensors(pos0, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, cand=pend,
+                     cand_count=pcnt, fixup_tau=fixup_tau, stream=stream,
+                     _extra_flags=N.LA_SIM_WRITE_ONLY | N.LA_SIM_SCATTER,
+                     _outputs=(res["first_t"], res["first_joint"]))
+    if timer:
+        timer.mark("paths")
+    vidx, vcnt = compact_valid(res["first_t"], T, stream=stream)
+    if timer:
+        timer.mark("compact")
+    res.update(pend_idx=pend, pend_count=pcnt, valid_idx=vidx, valid_count=vcnt, traj=traj, stride=stride)
+    return res
 
 
 def simulate_compact(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None, traj_f64: bool = False,

@@ -385,3 +385,29 @@ def test_edge_cases(torch):
     outs = simulate_batch(p, plan, 200)
     for o, ft in zip(outs, ref["first_t"]):
         assert (getattr(o, "step", 200)) == ft
+
+
+def test_deferred_pipeline_matches_single_pass(torch):
+    """screen(defer) -> compact -> f64 write-only scatter == single pass."""
+    from paper_2208_14567_b200.solver import simulate_deferred
+    from paper_2208_14567_b200.workloads import mixed_batch
+
+    mb = mixed_batch(6000, 5, 20, seed=21, stride=20)
+    pos = torch.from_numpy(mb.pos).cuda()
+    topo = torch.from_numpy(mb.topo).cuda()
+    ref = run_mixed(torch, mb.plans, mb.pos, mb.topo, 200)
+    res = simulate_deferred(pos, mb.table(), 200, topo)
+    torch.cuda.synchronize()
+    assert torch.equal(res["first_t"], ref["first_t"])
+    assert torch.equal(res["first_joint"], ref["first_joint"])
+    np_ = int(res["pend_count"].item())
+    pend = res["pend_idx"][:np_]
+    assert bool((ref["first_t"][pend] > 0).all())
+    ok = (res["first_t"][pend] == 200).nonzero().flatten()
+    a = res["traj"].view(-1, 20, 200, 2)[ok]
+    b = ref["traj"].view(-1, 20, 200, 2)[pend[ok]]
+    for i in range(len(ok)):
+        n = int(mb.n[int(pend[ok[i]])])
+        assert torch.equal(a[i, :n], b[i, :n])
+    nv = int(res["valid_count"].item())
+    assert torch.equal(res["valid_idx"][:nv], (ref["first_t"] == 200).nonzero().flatten())
