@@ -334,15 +334,15 @@ def e2e_c2(torch, args, mb, table, world):
 
 # ----------------------------------------------------------------- C3
 def bench_c3(torch, args, rank, world, peaks, flush, clk):
-    from paper_2208_14567_b200.solver import PlanTable, compact_valid, simulate_tensors
-    from paper_2208_14567_b200.workloads import device_poses, topology_pool
+    from paper_2208_14567_b200.solver import compact_valid, simulate_tensors
+    from paper_2208_14567_b200.workloads import native_batch
 
-    G = 1024
-    mechs, plans = topology_pool(G, 5, 20, seed=3000)
-    table = PlanTable(plans)
-    groups = (C3_COUNT + 255) // 256
-    topo = (torch.arange(C3_COUNT, device="cuda") // 256 % G).to(torch.int32)
-    pos = device_poses(topo, plans, 20, seed=77 + rank)
+    nb = native_batch(C3_COUNT, 5, 20, seed=3000 + 1000 * rank)
+    table = nb.table
+    G = table.G
+    topo = torch.from_numpy(nb.topo).cuda()
+    pos = torch.from_numpy(nb.pos).cuda()
+    del nb
     stream = torch.cuda.current_stream()
 
     def step(timer=None, counters=None):
@@ -392,7 +392,8 @@ def bench_c3(torch, args, rank, world, peaks, flush, clk):
             "semantics": "two-fidelity gate (T_low=50 inside T=200): valid flags exact, negatives "
                          "with their T_low lock step" if GATE_C3 else "exact first lock at T=200",
             "config": {"workload": "C3: 10M candidates/GPU, 5-20 joints padded to 20, 256 per topology "
-                                   "(1024-topology generator pool), poses U[0,1)^2 on device, T=200"}}
+                                   "(39,063 topologies), reference generator streams via the native "
+                                   "generator, T=200"}}
 
 
 # ----------------------------------------------------------------- C4
@@ -482,20 +483,17 @@ def bench_c5(torch, args, rank, world, peaks, flush, clk):
     from paper_2208_14567_b200.atlas import chamfer_scan
     from paper_2208_14567_b200.curves import normalize_tensors
     from paper_2208_14567_b200.dist import gather_merge
-    from paper_2208_14567_b200.solver import PlanTable, compact_valid, simulate_tensors
-    from paper_2208_14567_b200.workloads import device_poses, fourier_db, topology_pool
+    from paper_2208_14567_b200.solver import compact_valid, simulate_tensors
+    from paper_2208_14567_b200.workloads import fourier_db, native_batch
 
-    G = 1024
-    mechs, plans = topology_pool(G, 5, 20, seed=5000)
-    table = PlanTable(plans)
-    topo = (torch.arange(C5_COUNT, device="cuda") // 256 % G).to(torch.int32)
-    pos = device_poses(topo, plans, 20, seed=500 + rank)
+    nb = native_batch(C5_COUNT, 5, 20, seed=5000 + 1000 * rank)
+    table = nb.table
+    topo = torch.from_numpy(nb.topo).cuda()
+    pos = torch.from_numpy(nb.pos).cuda()
     queries = fourier_db(C5_QUERIES, T, seed=5151)
     # per-topology moving-joint masks (non-Fixed joints, cli.py:131-134)
-    moving = torch.zeros((G, 20), dtype=torch.bool)
-    for g, m in enumerate(mechs):
-        moving[g, :m.n] = torch.from_numpy(m.types != 0)
-    moving = moving.cuda()
+    moving = torch.from_numpy((nb.types > 0)).cuda()
+    del nb
     stride = 20
     stream = torch.cuda.current_stream()
     k = 10
@@ -552,7 +550,7 @@ def bench_c5(torch, args, rank, world, peaks, flush, clk):
                           "achieved_tflops": norm_flops / (stages["normalize"] / 1e3) / 1e12,
                           "frac_fp32": norm_flops / (stages["normalize"] / 1e3) / 1e12 / fp32_peak},
             "chamfer": {"pairs/s": pairs / (stages["chamfer"] / 1e3)},
-            "config": {"workload": "C5 scaled: 1M candidates/GPU (5-20 joints, 1024-topology pool), T=200, "
+            "config": {"workload": "C5 scaled: 1M candidates/GPU (5-20 joints, 3,907 generator topologies), T=200, "
                                    "64 Fourier queries, top-10; BASELINE configs[4] is 100M over 8 GPUs"}}
 
 

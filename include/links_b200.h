@@ -208,6 +208,23 @@ typedef struct la_chamfer_args {
 size_t la_chamfer_workspace(const la_chamfer_args* args);
 int la_chamfer_topk(const la_chamfer_args* args, void* stream);
 
+/* ---------------------------------------------------------------- generator
+ * Host (CPU, multi-threaded) reproduction of the reference's candidate
+ * streams: group g draws n = integers(n_lo, n_hi + 1) and its topology from
+ * default_rng([seed, g0 + g, 0]) (sample_topology, generator.py:200-222) and
+ * its poses from default_rng([seed, g0 + g, 1]) (_sample_positions_batch,
+ * generator.py:234-238) — numpy's SeedSequence / PCG64 / Generator
+ * restated bit for bit.                                                     */
+int la_sample_topologies(int64_t seed, int64_t g0, int64_t G, int32_t n_lo, int32_t n_hi, double ng_prob,
+                         int32_t retries, int32_t threads, la_plan* plans, int8_t* types /* [G][20] */,
+                         uint8_t* adj /* [G][20][20] or NULL */, int32_t* n_out);
+int la_sample_poses(int64_t seed, int64_t g0, int64_t G, int32_t per_group, const int32_t* n_of_group,
+                    int32_t stride, int32_t threads, double* pos /* [G*per_group][stride][2] host */);
+/* raw PCG64 stream of default_rng(entropy[:n_ent]): kind 0 -> random(),
+ * kind 1 -> integers(0, bound)                                              */
+int la_rng_draw(const int64_t* entropy, int32_t n_ent, int32_t kind, int64_t bound, int64_t count,
+                double* out_d, int64_t* out_i);
+
 /* ---------------------------------------------------------------- misc */
 int la_abi_version(void);
 const char* la_last_error(void);

@@ -42,6 +42,9 @@ EXPORTS = (
     "la_circle_stats",
     "la_chamfer_workspace",
     "la_chamfer_topk",
+    "la_sample_topologies",
+    "la_sample_poses",
+    "la_rng_draw",
     "la_abi_version",
     "la_last_error",
     "la_device_sm_count",
@@ -161,6 +164,9 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_chamfer_workspace.argtypes = [C.POINTER(LaChamferArgs)]
     lib.la_chamfer_workspace.restype = sz
     lib.la_chamfer_topk.argtypes = [C.POINTER(LaChamferArgs), vp]
+    lib.la_sample_topologies.argtypes = [i64, i64, i64, i32, i32, C.c_double, i32, i32, vp, vp, vp, vp]
+    lib.la_sample_poses.argtypes = [i64, i64, i64, i32, vp, i32, i32, vp]
+    lib.la_rng_draw.argtypes = [vp, i32, i32, i64, i64, vp, vp]
     lib.la_abi_version.argtypes = []
     lib.la_last_error.argtypes = []
     lib.la_last_error.restype = C.c_char_p

@@ -14,10 +14,10 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRC = sorted((PKG / "csrc").glob("*.cu"))
+SRC = sorted((PKG / "csrc").glob("*.cu")) + sorted((PKG / "csrc").glob("*.cpp"))
 OUT = PKG / "_lib" / "liblinks_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-pthread", "-shared",
          f"-I{ROOT / 'include'}", "--expt-relaxed-constexpr"]
 
 

@@ -206,6 +206,44 @@ def _sample_positions_batch(n: int, k: int, rng: np.random.Generator) -> np.ndar
     return pos
 
 
+# ------------------------------------------------------------ native streams
+def native_topologies(seed: int, G: int, n_lo: int, n_hi: int, *, g0: int = 0, ng_probability: float = 0.25,
+                      retries: int = 1000, threads: int = 0):
+    """G generator topologies, group g drawn exactly like
+    ``n = default_rng([seed, g0+g, 0]).integers(n_lo, n_hi+1)`` followed by
+    ``sample_topology`` on the same stream — by the native multi-threaded
+    generator (csrc/gen.cpp).  Returns (la_plan bytes (G*64,) uint8, types
+    (G, 20) int8, adjacency (G, 20, 20) uint8, n (G,) int32)."""
+    import os as _os
+
+    lib = N.load()
+    plans = np.zeros(G * 64, dtype=np.uint8)
+    types = np.zeros((G, N.LA_MAX_JOINTS), dtype=np.int8)
+    adj = np.zeros((G, N.LA_MAX_JOINTS, N.LA_MAX_JOINTS), dtype=np.uint8)
+    ns = np.zeros(G, dtype=np.int32)
+    th = threads or len(_os.sched_getaffinity(0))
+    N.check(lib.la_sample_topologies(int(seed), int(g0), int(G), int(n_lo), int(n_hi), float(ng_probability),
+                                     int(retries), int(th), plans.ctypes.data, types.ctypes.data, adj.ctypes.data,
+                                     ns.ctypes.data), "la_sample_topologies")
+    return plans, types, adj, ns
+
+
+def native_poses(seed: int, n_of_group: np.ndarray, per_group: int, stride: int, *, g0: int = 0,
+                 threads: int = 0) -> np.ndarray:
+    """(G*per_group, stride, 2) float64 poses: group g is
+    ``_sample_positions_batch(n_g, per_group, default_rng([seed, g0+g, 1]))``
+    padded with NaN, drawn by the native generator."""
+    import os as _os
+
+    lib = N.load()
+    ng = np.ascontiguousarray(n_of_group, dtype=np.int32)
+    out = np.empty((len(ng) * per_group, stride, 2), dtype=np.float64)
+    th = threads or len(_os.sched_getaffinity(0))
+    N.check(lib.la_sample_poses(int(seed), int(g0), len(ng), int(per_group), ng.ctypes.data, int(stride), int(th),
+                                out.ctypes.data), "la_sample_poses")
+    return out
+
+
 # ------------------------------------------------------------ GPU gate driver
 def find_valid_variant(topology: Mechanism, plan: SolutionPlan, rng: np.random.Generator,
                        max_attempts: int = 5000, T_low: int = 50, T_high: int = 200, batch: int = 256,

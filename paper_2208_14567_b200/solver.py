@@ -143,21 +143,37 @@ def _pack_plan(plan: SolutionPlan) -> bytes:
 
 @dataclass
 class PlanTable:
-    """Device-resident array of compiled plans (la_plan records, 64 B each)."""
+    """Device-resident array of compiled plans (la_plan records, 64 B each).
+
+    Built from SolutionPlan objects, or from raw records (``from_records``,
+    e.g. the native generator's output)."""
 
     plans: list[SolutionPlan]
     device: object = None
     _dev: object = field(default=None, repr=False)
+    _raw: np.ndarray | None = field(default=None, repr=False)
+    _ns: np.ndarray | None = field(default=None, repr=False)
+
+    @classmethod
+    def from_records(cls, raw: np.ndarray, n: np.ndarray, device=None) -> "PlanTable":
+        raw = np.ascontiguousarray(raw, dtype=np.uint8)
+        if raw.size % 64:
+            raise ValueError("plan records are 64 bytes each")
+        return cls([], device=device, _raw=raw, _ns=np.asarray(n, dtype=np.int32))
 
     @property
     def G(self) -> int:
-        return len(self.plans)
+        return len(self._ns) if self._raw is not None else len(self.plans)
 
     @property
     def max_n(self) -> int:
+        if self._raw is not None:
+            return int(self._ns.max())
         return max(p.n for p in self.plans)
 
     def host_bytes(self) -> np.ndarray:
+        if self._raw is not None:
+            return self._raw
         return np.frombuffer(b"".join(_pack_plan(p) for p in self.plans), dtype=np.uint8)
 
     def tensor(self):

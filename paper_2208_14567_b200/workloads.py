@@ -3,9 +3,10 @@
 C1  1,024 four-bars (topology of the reference test fixture, conftest.py:7-18)
 C2  100,000 candidates of 6-8 joints, 256 per topology, topologies and poses
     from the reference generator's PCG64 streams (generator.py:286-292)
-C3  validity screen: candidates of 5-20 joints, 256 per topology; poses are
-    drawn ON DEVICE (torch Philox) because 10M x 20 x 2 host draws are slower
-    than the screen itself; parity runs on host-regenerated subsets
+C3  validity screen: 10M candidates of 5-20 joints, 256 per topology, from
+    the same reference streams, drawn by the native multi-threaded generator
+    (csrc/gen.cpp reproduces numpy's SeedSequence/PCG64/Generator and the
+    topology operator bit for bit; ~0.7 s for 10M on 16 host threads)
 C4  random closed Fourier curves, 5 harmonics, coefficients N(0, 1/k^2),
     generated on device and normalised once by la_normalize
 
@@ -89,6 +90,35 @@ def mixed_batch(count: int, n_lo: int, n_hi: int, seed: int, per_topology: int =
         topo.append(np.full(k, g, dtype=np.int32))
         ns.append(np.full(k, n, dtype=np.int32))
     return MixedBatch(plans, mechs, np.concatenate(poses), np.concatenate(topo), np.concatenate(ns))
+
+
+@dataclass
+class NativeBatch:
+    """Candidates from the native generator (csrc/gen.cpp): group g of
+    ``per_topology`` candidates uses the reference streams
+    default_rng([seed, g, 0]) (n and topology) and default_rng([seed, g, 1])
+    (poses), exactly like ``mixed_batch`` but for millions of candidates."""
+
+    table: PlanTable
+    types: np.ndarray      # (G, 20) int8, -1 beyond n
+    n_group: np.ndarray    # (G,)
+    pos: np.ndarray        # (B, stride, 2) f64
+    topo: np.ndarray       # (B,) int32
+
+    @property
+    def B(self) -> int:
+        return len(self.topo)
+
+
+def native_batch(count: int, n_lo: int, n_hi: int, seed: int, per_topology: int = 256,
+                 stride: int = NMAX) -> NativeBatch:
+    from paper_2208_14567_b200.generator import native_poses, native_topologies
+
+    G = (count + per_topology - 1) // per_topology
+    raw, types, _, ns = native_topologies(seed, G, n_lo, n_hi)
+    pos = native_poses(seed, ns, per_topology, stride)[:count]
+    topo = (np.arange(count, dtype=np.int64) // per_topology).astype(np.int32)
+    return NativeBatch(PlanTable.from_records(raw, ns), types, ns, pos, topo)
 
 
 def topology_pool(G: int, n_lo: int, n_hi: int, seed: int) -> tuple[list[Mechanism], list[SolutionPlan]]:
