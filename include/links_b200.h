@@ -220,6 +220,29 @@ int la_sample_topologies(int64_t seed, int64_t g0, int64_t G, int32_t n_lo, int3
                          uint8_t* adj /* [G][20][20] or NULL */, int32_t* n_out);
 int la_sample_poses(int64_t seed, int64_t g0, int64_t G, int32_t per_group, const int32_t* n_of_group,
                     int32_t stride, int32_t threads, double* pos /* [G*per_group][stride][2] host */);
+/* Dataset-generation engine (GenerationRun / _generate_slot /
+ * find_valid_variant, generator.py:241-375): a caller-owned host object that
+ * holds every slot's topology / pose / negative PCG64 streams and replays the
+ * reference control flow exactly; the GPU answers the two-fidelity gate for
+ * look-ahead windows (la_simulate with LA_SIM_GATE_ONLY and low_t).       */
+typedef struct la_gen_cfg {
+  int64_t seed;
+  int32_t n_min, n_max;
+  double ng_prob;
+  int32_t variants, T_low, T_high, max_attempts, retries, batch;
+  double negative_rate;
+} la_gen_cfg;
+void* la_gen_create(const la_gen_cfg* cfg, int64_t slot0, int64_t n_slots);
+void la_gen_destroy(void* engine);
+int64_t la_gen_window(void* engine, int32_t lookahead, int64_t cap, int32_t threads, double* pos /* [cap][20][2] */,
+                      int32_t* cand_plan /* [cap] */, la_plan* plans /* [n_slots] */, int32_t* n_plans);
+int la_gen_consume(void* engine, const double* pos, const int32_t* first_t, const int32_t* low_t);
+int64_t la_gen_count(void* engine, int32_t what /* 0 records, 1 negatives */);
+int la_gen_records(void* engine, int64_t* meta /* [R][4] */, double* pos, la_plan* plans, uint8_t* adj,
+                   int8_t* types);
+int la_gen_negatives(void* engine, int64_t* meta /* [R][3] */, double* pos, uint8_t* adj, int8_t* types);
+int la_gen_stats(void* engine, int64_t* by_n /* [21][2] */, int64_t* discarded);
+
 /* raw PCG64 stream of default_rng(entropy[:n_ent]): kind 0 -> random(),
  * kind 1 -> integers(0, bound)                                              */
 int la_rng_draw(const int64_t* entropy, int32_t n_ent, int32_t kind, int64_t bound, int64_t count,

@@ -45,6 +45,14 @@ EXPORTS = (
     "la_sample_topologies",
     "la_sample_poses",
     "la_rng_draw",
+    "la_gen_create",
+    "la_gen_destroy",
+    "la_gen_window",
+    "la_gen_consume",
+    "la_gen_count",
+    "la_gen_records",
+    "la_gen_negatives",
+    "la_gen_stats",
     "la_abi_version",
     "la_last_error",
     "la_device_sm_count",
@@ -62,6 +70,22 @@ class LaPlan(C.Structure):
 
 
 assert C.sizeof(LaPlan) == 64
+
+
+class LaGenCfg(C.Structure):
+    _fields_ = [
+        ("seed", C.c_int64),
+        ("n_min", C.c_int32),
+        ("n_max", C.c_int32),
+        ("ng_prob", C.c_double),
+        ("variants", C.c_int32),
+        ("T_low", C.c_int32),
+        ("T_high", C.c_int32),
+        ("max_attempts", C.c_int32),
+        ("retries", C.c_int32),
+        ("batch", C.c_int32),
+        ("negative_rate", C.c_double),
+    ]
 
 
 class LaSimArgs(C.Structure):
@@ -167,12 +191,25 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_sample_topologies.argtypes = [i64, i64, i64, i32, i32, C.c_double, i32, i32, vp, vp, vp, vp]
     lib.la_sample_poses.argtypes = [i64, i64, i64, i32, vp, i32, i32, vp]
     lib.la_rng_draw.argtypes = [vp, i32, i32, i64, i64, vp, vp]
+    lib.la_gen_create.argtypes = [C.POINTER(LaGenCfg), i64, i64]
+    lib.la_gen_create.restype = vp
+    lib.la_gen_destroy.argtypes = [vp]
+    lib.la_gen_destroy.restype = None
+    lib.la_gen_window.argtypes = [vp, i32, i64, i32, vp, vp, vp, vp]
+    lib.la_gen_window.restype = i64
+    lib.la_gen_consume.argtypes = [vp, vp, vp, vp]
+    lib.la_gen_count.argtypes = [vp, i32]
+    lib.la_gen_count.restype = i64
+    lib.la_gen_records.argtypes = [vp, vp, vp, vp, vp, vp]
+    lib.la_gen_negatives.argtypes = [vp, vp, vp, vp, vp]
+    lib.la_gen_stats.argtypes = [vp, vp, vp]
     lib.la_abi_version.argtypes = []
     lib.la_last_error.argtypes = []
     lib.la_last_error.restype = C.c_char_p
     lib.la_device_sm_count.argtypes = []
     for name in EXPORTS:
-        if name not in ("la_last_error", "la_compact_workspace", "la_chamfer_workspace"):
+        if name not in ("la_last_error", "la_compact_workspace", "la_chamfer_workspace", "la_gen_create",
+                        "la_gen_destroy", "la_gen_window", "la_gen_count"):
             getattr(lib, name).restype = C.c_int
 
 
@@ -223,3 +260,7 @@ def stream_ptr(stream=None) -> int:
 
 def ptr(t) -> int | None:
     return None if t is None else int(t.data_ptr())
+
+
+def last_error() -> str:
+    return load().la_last_error().decode(errors="replace")

@@ -14,6 +14,7 @@
 // the buffered 32-bit stream).
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -402,6 +403,361 @@ int la_rng_draw(const int64_t* entropy, int32_t n_ent, int32_t kind, int64_t bou
     if (kind == 0) out_d[i] = r.random();
     else out_i[i] = r.integers(0, bound);
   }
+  return 0;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Dataset-generation engine: GenerationRun / _generate_slot /
+// find_valid_variant (generator.py:241-375) with the two-fidelity gate
+// evaluated on the GPU.  The host engine owns every slot's three PCG64
+// streams (topology, poses, negatives) and replays the reference control
+// flow exactly; the device only answers "T_low lock step / valid at T_high"
+// for look-ahead windows of candidate batches drawn from a COPY of each
+// slot's pose stream (the real stream advances only by what the reference
+// consumes).
+// ===========================================================================
+namespace {
+
+struct Accepted {
+  double pos[LA_MAX_JOINTS][2];
+  int64_t attempts;
+};
+
+struct Batch {
+  int64_t first = 0;  // index of its first candidate in the window
+  int k = 0;          // candidates
+  Pcg64 after;        // pose stream state after drawing it
+  explicit Batch(const Pcg64& r) : after(r) {}
+};
+
+struct Slot {
+  int64_t id;
+  Pcg64 topo, pos, neg;
+  int n = 0;
+  Mech mech;
+  Plan plan;
+  int state = 0;           // 0 need topology, 1 searching, 2 done, 3 failed
+  int tries = 0;           // topologies sampled
+  int64_t consumed = 0;    // candidates consumed by the current variant
+  std::vector<Accepted> acc;
+  std::vector<Batch> win;  // current look-ahead window
+  int64_t plan_slot = -1;  // plan index of this slot in the last window
+  Slot(int64_t s, int64_t seed) : id(s), topo(stream(seed, s, 0)), pos(stream(seed, s, 1)), neg(stream(seed, s, 2)) {}
+};
+
+struct Record {
+  int64_t slot, variant, attempts;
+  Mech mech;
+  Plan plan;
+  double pos[LA_MAX_JOINTS][2];
+};
+
+struct Negative {
+  int64_t slot, step;
+  Mech mech;
+  double pos[LA_MAX_JOINTS][2];
+};
+
+struct Engine {
+  la_gen_cfg cfg;
+  std::vector<Slot> slots;
+  std::vector<Record> records;      // per slot in order (filled at slot completion)
+  std::vector<std::vector<Record>> slot_records;
+  std::vector<std::vector<Negative>> slot_negs;
+  int64_t sim_by_n[LA_MAX_JOINTS + 1] = {0};
+  int64_t acc_by_n[LA_MAX_JOINTS + 1] = {0};
+  int64_t discarded = 0;
+  std::vector<std::vector<int64_t>> succ_attempts;  // per slot: attempts of recorded successes
+  std::vector<int64_t> slot_sim;                      // per slot simulated count (for stats merge order)
+  int error = 0;
+  char err[200] = "";
+};
+
+void draw_pose(Pcg64& r, int n, double* row /* [20][2] */) {
+  for (int j = 0; j < n; ++j) {
+    row[2 * j] = r.random();
+    row[2 * j + 1] = r.random();
+  }
+  row[0] = 0.5;
+  row[1] = 0.5;
+  row[2] = 0.55;
+  row[3] = 0.5;
+  for (int j = n; j < LA_MAX_JOINTS; ++j) row[2 * j] = row[2 * j + 1] = NAN;
+}
+
+la_plan to_rec(const Mech& m, const Plan& p) {
+  la_plan rec;
+  std::memset(&rec, 0, sizeof(rec));
+  rec.n = (int16_t)m.n;
+  rec.nsteps = (int16_t)p.ns;
+  uint32_t fm = 0;
+  for (int k = 0; k < m.n; ++k)
+    if (m.type[k] == FIXED) fm |= 1u << k;
+  rec.fixed_mask = fm;
+  for (int s = 0; s < p.ns; ++s)
+    for (int c = 0; c < 3; ++c) rec.step[s][c] = p.st[s][c];
+  return rec;
+}
+
+// next topology of a slot (sample_topology on the slot's topology stream)
+bool next_topology(Engine& E, Slot& S) {
+  if (S.tries >= E.cfg.retries) return false;
+  ++S.tries;
+  if (!sample_topology(S.topo, S.n, E.cfg.ng_prob, E.cfg.retries, S.mech, S.plan)) return false;
+  S.acc.clear();
+  S.consumed = 0;
+  S.win.clear();
+  S.state = 1;
+  return true;
+}
+
+int batch_size(const Engine& E, int64_t consumed) {
+  const int64_t left = E.cfg.max_attempts - consumed;
+  return (int)(left < E.cfg.batch ? left : E.cfg.batch);
+}
+
+}  // namespace
+
+extern "C" {
+
+void* la_gen_create(const la_gen_cfg* cfg, int64_t slot0, int64_t n_slots) {
+  if (!cfg || n_slots < 0 || cfg->n_min < 4 || cfg->n_max < cfg->n_min || cfg->n_max > LA_MAX_JOINTS ||
+      cfg->variants < 1 || cfg->batch < 1 || cfg->max_attempts < 1 || cfg->retries < 1 || cfg->seed < 0) {
+    la::set_error("la_gen_create: bad configuration");
+    return nullptr;
+  }
+  Engine* E = new Engine();
+  E->cfg = *cfg;
+  E->slots.reserve((size_t)n_slots);
+  for (int64_t s = 0; s < n_slots; ++s) {
+    E->slots.emplace_back(slot0 + s, cfg->seed);
+    Slot& S = E->slots.back();
+    S.n = (int)S.topo.integers(cfg->n_min, (int64_t)cfg->n_max + 1);
+    if (!next_topology(*E, S)) S.state = 3;
+  }
+  E->slot_records.resize((size_t)n_slots);
+  E->slot_negs.resize((size_t)n_slots);
+  E->succ_attempts.resize((size_t)n_slots);
+  for (auto& S : E->slots)
+    if (S.state == 3) {
+      E->error = LA_ERANGE;
+      snprintf(E->err, sizeof(E->err), "slot %lld: no valid topology with n=%d", (long long)S.id, S.n);
+    }
+  return E;
+}
+
+void la_gen_destroy(void* h) { delete static_cast<Engine*>(h); }
+
+// Draw the next look-ahead window: for every searching slot, up to
+// `lookahead` consecutive batches of its current variant schedule, drawn from
+// a copy of its pose stream.  Writes poses [cand][20][2], the plan index of
+// each candidate and the plan table (one record per slot in the window).
+// Slots that would overflow `cap` wait for the next window.  Returns the
+// candidate count, 0 when every slot is done, <0 on error.
+int64_t la_gen_window(void* h, int32_t lookahead, int64_t cap, int32_t threads, double* pos, int32_t* cand_plan,
+                      la_plan* plans, int32_t* n_plans) {
+  Engine& E = *static_cast<Engine*>(h);
+  if (E.error) {
+    la::set_error("%s", E.err);
+    return E.error;
+  }
+  if (lookahead < 1) lookahead = 1;
+  int64_t total = 0;
+  int np = 0;
+  std::vector<Slot*> act;
+  std::vector<int64_t> base;
+  for (auto& S : E.slots) {
+    S.win.clear();
+    if (S.state != 1) continue;
+    int64_t consumed = S.consumed, need = 0;
+    std::vector<Batch> w;
+    for (int i = 0; i < lookahead; ++i) {
+      const int k = batch_size(E, consumed);
+      if (k <= 0) break;
+      Batch b(S.pos);
+      b.first = total + need;
+      b.k = k;
+      w.push_back(b);
+      need += k;
+      consumed += k;
+    }
+    if (total + need > cap) {
+      if (total > 0) break;
+      la::set_error("la_gen_window: one batch (%lld) exceeds cap %lld", (long long)need, (long long)cap);
+      return LA_EWS;
+    }
+    S.plan_slot = np;
+    plans[np++] = to_rec(S.mech, S.plan);
+    S.win.swap(w);
+    act.push_back(&S);
+    total += need;
+  }
+  parallel_for((int64_t)act.size(), threads, [&](int64_t a) {
+    Slot& S = *act[a];
+    Pcg64 r = S.pos;
+    for (auto& b : S.win) {
+      for (int c = 0; c < b.k; ++c) {
+        const int64_t off = b.first + c;
+        draw_pose(r, S.n, pos + (size_t)off * LA_MAX_JOINTS * 2);
+        cand_plan[off] = (int32_t)S.plan_slot;
+      }
+      b.after = r;
+    }
+  });
+  *n_plans = np;
+  return total;
+}
+
+// Walk the device flags of the last window in each slot's stream order:
+// first_t[c] == T_high -> valid; low_t[c] >= 0 -> locked at T_low (step).
+int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int32_t* low_t) {
+  Engine& E = *static_cast<Engine*>(h);
+  const la_gen_cfg& cfg = E.cfg;
+  for (size_t si = 0; si < E.slots.size(); ++si) {
+    Slot& S = E.slots[si];
+    if (S.state != 1 || S.win.empty()) continue;
+    size_t used = 0;  // batches fully consumed
+    bool restart_window = false;
+    for (size_t bi = 0; bi < S.win.size() && S.state == 1 && !restart_window; ++bi) {
+      const Batch& b = S.win[bi];
+      if (b.k != batch_size(E, S.consumed)) {  // schedule changed (new variant near the cap)
+        restart_window = true;
+        break;
+      }
+      int hit = -1;
+      for (int c = 0; c < b.k; ++c) {
+        const int64_t g = b.first + c;
+        if (low_t[g] >= 0) {  // T_low lock: negative sample draw (generator.py:267-272)
+          if (cfg.negative_rate > 0.0 && S.neg.random() < cfg.negative_rate) {
+            Negative ng;
+            ng.slot = S.id;
+            ng.step = low_t[g];
+            ng.mech = S.mech;
+            std::memcpy(ng.pos, pos + (size_t)g * LA_MAX_JOINTS * 2, sizeof(ng.pos));
+            E.slot_negs[si].push_back(ng);
+          }
+          continue;
+        }
+        if (first_t[g] != cfg.T_high) continue;
+        hit = c;
+        break;
+      }
+      S.pos = b.after;  // the reference draws whole batches
+      ++used;
+      if (hit >= 0) {
+        Accepted a;
+        std::memcpy(a.pos, pos + (size_t)(b.first + hit) * LA_MAX_JOINTS * 2, sizeof(a.pos));
+        a.attempts = S.consumed + hit + 1;
+        S.acc.push_back(a);
+        S.consumed = 0;
+        if ((int)S.acc.size() == cfg.variants) {
+          for (size_t v = 0; v < S.acc.size(); ++v) {
+            Record r;
+            r.slot = S.id;
+            r.variant = (int64_t)v;
+            r.attempts = S.acc[v].attempts;
+            r.mech = S.mech;
+            r.plan = S.plan;
+            std::memcpy(r.pos, S.acc[v].pos, sizeof(r.pos));
+            E.slot_records[si].push_back(r);
+            E.sim_by_n[S.n] += r.attempts;
+            E.acc_by_n[S.n] += 1;
+            E.succ_attempts[si].push_back(r.attempts);
+          }
+          S.state = 2;
+        }
+        continue;  // next variant continues on the next batch of the window
+      }
+      S.consumed += b.k;
+      if (S.consumed >= cfg.max_attempts) {  // variant failed: discard topology (generator.py:581-583)
+        int64_t wasted = cfg.max_attempts;
+        for (auto& a : S.acc) wasted += a.attempts;
+        E.sim_by_n[S.n] += wasted;
+        E.discarded += 1;
+        if (!next_topology(E, S)) {
+          S.state = 3;
+          E.error = LA_ERANGE;
+          snprintf(E.err, sizeof(E.err), "slot %lld: no topology with feasible variants (n=%d)",
+                   (long long)S.id, S.n);
+        }
+        restart_window = true;  // next_topology cleared the window
+      }
+    }
+    (void)used;
+    S.win.clear();  // unconsumed look-ahead is dropped; the real stream sits after the last consumed batch
+  }
+  if (E.error) {
+    la::set_error("%s", E.err);
+    return E.error;
+  }
+  return 0;
+}
+
+int64_t la_gen_count(void* h, int32_t what) {
+  Engine& E = *static_cast<Engine*>(h);
+  int64_t n = 0;
+  if (what == 0)
+    for (auto& v : E.slot_records) n += (int64_t)v.size();
+  else
+    for (auto& v : E.slot_negs) n += (int64_t)v.size();
+  return n;
+}
+
+// records in slot order: meta [R][4] (slot, variant, attempts, n), poses
+// [R][20][2], plans [R], adjacency [R][20][20], types [R][20]
+int la_gen_records(void* h, int64_t* meta, double* pos, la_plan* plans, uint8_t* adj, int8_t* types) {
+  Engine& E = *static_cast<Engine*>(h);
+  int64_t r = 0;
+  for (auto& v : E.slot_records)
+    for (auto& rec : v) {
+      meta[4 * r] = rec.slot;
+      meta[4 * r + 1] = rec.variant;
+      meta[4 * r + 2] = rec.attempts;
+      meta[4 * r + 3] = rec.mech.n;
+      std::memcpy(pos + (size_t)r * LA_MAX_JOINTS * 2, rec.pos, sizeof(rec.pos));
+      plans[r] = to_rec(rec.mech, rec.plan);
+      for (int i = 0; i < LA_MAX_JOINTS; ++i) {
+        types[r * LA_MAX_JOINTS + i] = i < rec.mech.n ? rec.mech.type[i] : (int8_t)-1;
+        for (int j = 0; j < LA_MAX_JOINTS; ++j)
+          adj[(r * LA_MAX_JOINTS + i) * LA_MAX_JOINTS + j] =
+              (i < rec.mech.n && j < rec.mech.n) ? (uint8_t)((rec.mech.adj[i] >> j) & 1u) : 0;
+      }
+      ++r;
+    }
+  return 0;
+}
+
+// negatives in slot order: meta [R][3] (slot, locking step, n), poses [R][20][2]
+int la_gen_negatives(void* h, int64_t* meta, double* pos, uint8_t* adj, int8_t* types) {
+  Engine& E = *static_cast<Engine*>(h);
+  int64_t r = 0;
+  for (auto& v : E.slot_negs)
+    for (auto& ng : v) {
+      meta[3 * r] = ng.slot;
+      meta[3 * r + 1] = ng.step;
+      meta[3 * r + 2] = ng.mech.n;
+      std::memcpy(pos + (size_t)r * LA_MAX_JOINTS * 2, ng.pos, sizeof(ng.pos));
+      for (int i = 0; i < LA_MAX_JOINTS; ++i) {
+        types[r * LA_MAX_JOINTS + i] = i < ng.mech.n ? ng.mech.type[i] : (int8_t)-1;
+        for (int j = 0; j < LA_MAX_JOINTS; ++j)
+          adj[(r * LA_MAX_JOINTS + i) * LA_MAX_JOINTS + j] =
+              (i < ng.mech.n && j < ng.mech.n) ? (uint8_t)((ng.mech.adj[i] >> j) & 1u) : 0;
+      }
+      ++r;
+    }
+  return 0;
+}
+
+// stats: out [21][2] simulated / accepted by joint count; *discarded
+int la_gen_stats(void* h, int64_t* out, int64_t* discarded) {
+  Engine& E = *static_cast<Engine*>(h);
+  for (int n = 0; n <= LA_MAX_JOINTS; ++n) {
+    out[2 * n] = E.sim_by_n[n];
+    out[2 * n + 1] = E.acc_by_n[n];
+  }
+  *discarded = E.discarded;
   return 0;
 }
 

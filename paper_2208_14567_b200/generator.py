@@ -14,6 +14,7 @@ ends in the same state as after the reference loop.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 from dataclasses import dataclass, field
 
@@ -24,6 +25,8 @@ from paper_2208_14567_b200.curves import plan_ancestry
 from paper_2208_14567_b200.mechanism import ARM_PIVOT, ARM_TIP, JointType, Mechanism, apply_Ng, apply_Ns, \
     initial_mechanism
 from paper_2208_14567_b200.solver import PlanTable, SolutionPlan, Trajectory, compile_order, simulate_tensors
+
+NMAX = N.LA_MAX_JOINTS
 
 
 class GenerationError(RuntimeError):
@@ -308,3 +311,171 @@ def _trajectory(pos: np.ndarray, table: PlanTable, T: int) -> Trajectory:
     dpos = torch.from_numpy(np.ascontiguousarray(pos[None])).cuda()
     res = simulate_tensors(dpos, table, T, write_traj=True, traj_stride=pos.shape[0], traj_f64=True)
     return Trajectory(res["traj"].view(pos.shape[0], T, 2).cpu().numpy())
+
+
+# ------------------------------------------------------------ dataset generation
+@dataclass
+class GeneratedRecord:
+    """generator.py:148-153."""
+
+    slot: int
+    variant: int
+    mechanism: Mechanism
+    trajectory: Trajectory
+    attempts: int
+
+
+def _mechanisms(adj: np.ndarray, types: np.ndarray, pos: np.ndarray, n: np.ndarray) -> list[Mechanism]:
+    return [Mechanism(adj[i, :n[i], :n[i]].copy(), types[i, :n[i]].astype(np.int8), pos[i, :n[i]].copy())
+            for i in range(len(n))]
+
+
+class GenerationRun:
+    """Dataset generation (generator.py:336-375) with the slot loop in the
+    native engine and the two-fidelity gate on the GPU.
+
+    Each block of slots is one ``la_gen_*`` engine: it draws look-ahead
+    windows of whole reference batches from copies of every searching slot's
+    pose stream, one ``la_simulate`` launch (gate mode, coarse T_low lock
+    step) screens the window, and the engine walks the flags in each slot's
+    stream order.  Records, ``attempts``, negatives and stats are identical to
+    the reference run with ``workers=1`` (records come out in slot order for
+    any ``workers``; the reference's pool order is not deterministic).
+    Trajectories of accepted variants are f64 T_high paths from la_simulate.
+    """
+
+    def __init__(self, config: GenerationConfig, *, lookahead: int = 4, slot_block: int = 1 << 14,
+                 window_cap: int = 1 << 21, threads: int | None = None, device=None):
+        self.config = config
+        self.stats = GenerationStats()
+        self.negatives: list[NegativeSample] = []
+        self.lookahead = int(lookahead)
+        self.slot_block = int(slot_block)
+        self.window_cap = int(window_cap)
+        self.threads = threads
+        self.device = device
+        self.windows = 0         # GPU launches of the gate
+        self.screened = 0        # candidates screened on the GPU (>= stats.simulated)
+
+    def _cfg(self) -> N.LaGenCfg:
+        c = self.config
+        return N.LaGenCfg(int(c.seed), int(c.n_min), int(c.n_max), float(c.ng_probability),
+                          int(c.variants_per_topology), int(c.T_low), int(c.T_high), int(c.max_attempts),
+                          int(c.topology_retries), int(c.batch), float(c.negative_rate))
+
+    def _run_block(self, slot0: int, nslots: int):
+        import os as _os
+
+        torch = N.require_cuda()
+        lib = N.load()
+        c = self.config
+        dev = self.device or torch.device("cuda")
+        cfg = self._cfg()
+        eng = lib.la_gen_create(C.byref(cfg), int(slot0), int(nslots))
+        if not eng:
+            raise ValueError(N.last_error())
+        th = self.threads or len(_os.sched_getaffinity(0))
+        fused = c.T_high == 4 * c.T_low
+        try:
+            per_window = min(self.window_cap, max(c.batch, nslots * self.lookahead * c.batch))
+            pos_h = torch.empty((per_window, NMAX, 2), dtype=torch.float64).pin_memory()
+            plan_h = torch.empty(per_window, dtype=torch.int32).pin_memory()
+            plans_h = np.zeros((nslots, 64), dtype=np.uint8)
+            flags_h = torch.empty((2, per_window), dtype=torch.int32).pin_memory()
+            n_plans = C.c_int32(0)
+            pos_d = torch.empty((per_window, NMAX, 2), dtype=torch.float64, device=dev)
+            while True:
+                m = lib.la_gen_window(eng, self.lookahead, per_window, th, pos_h.data_ptr(), plan_h.data_ptr(),
+                                      plans_h.ctypes.data, C.byref(n_plans))
+                if m < 0:
+                    raise GenerationError(N.last_error())
+                if m == 0:
+                    break
+                np_ = n_plans.value
+                ns = plans_h[:np_, :2].copy().view(np.int16)[:, 0].astype(np.int32)
+                table = PlanTable.from_records(plans_h[:np_].reshape(-1), ns, device=dev)
+                pd = pos_d[:m]
+                pd.copy_(pos_h[:m], non_blocking=True)
+                topo = plan_h[:m].to(dev, non_blocking=True)
+                if fused:
+                    res = simulate_tensors(pd, table, c.T_high, topo, write_traj=False, low=True, gate_only=True)
+                    flags_h[0, :m].copy_(res["first_t"], non_blocking=True)
+                    flags_h[1, :m].copy_(res["low_t"], non_blocking=True)
+                else:
+                    lo = simulate_tensors(pd, table, c.T_low, topo, write_traj=False)
+                    hi = simulate_tensors(pd, table, c.T_high, topo, write_traj=False)
+                    flags_h[0, :m].copy_(hi["first_t"], non_blocking=True)
+                    ft = lo["first_t"]
+                    flags_h[1, :m].copy_(torch.where(ft < c.T_low, ft, torch.full_like(ft, -1)), non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+                self.windows += 1
+                self.screened += int(m)
+                rc = lib.la_gen_consume(eng, pos_h.data_ptr(), flags_h[0].data_ptr(), flags_h[1].data_ptr())
+                if rc != 0:
+                    raise GenerationError(N.last_error())
+            # records, negatives, stats
+            R = lib.la_gen_count(eng, 0)
+            meta = np.zeros((R, 4), dtype=np.int64)
+            rpos = np.zeros((R, NMAX, 2))
+            rplans = np.zeros((R, 64), dtype=np.uint8)
+            radj = np.zeros((R, NMAX, NMAX), dtype=np.uint8)
+            rtypes = np.zeros((R, NMAX), dtype=np.int8)
+            N.check(lib.la_gen_records(eng, meta.ctypes.data, rpos.ctypes.data, rplans.ctypes.data,
+                                       radj.ctypes.data, rtypes.ctypes.data), "la_gen_records")
+            Q = lib.la_gen_count(eng, 1)
+            nmeta = np.zeros((Q, 3), dtype=np.int64)
+            npos = np.zeros((Q, NMAX, 2))
+            nadj = np.zeros((Q, NMAX, NMAX), dtype=np.uint8)
+            ntypes = np.zeros((Q, NMAX), dtype=np.int8)
+            N.check(lib.la_gen_negatives(eng, nmeta.ctypes.data, npos.ctypes.data, nadj.ctypes.data,
+                                         ntypes.ctypes.data), "la_gen_negatives")
+            by_n = np.zeros((NMAX + 1, 2), dtype=np.int64)
+            disc = C.c_int64(0)
+            N.check(lib.la_gen_stats(eng, by_n.ctypes.data, C.byref(disc)), "la_gen_stats")
+        finally:
+            lib.la_gen_destroy(eng)
+        st = GenerationStats()
+        for n in range(NMAX + 1):
+            if by_n[n, 0] or by_n[n, 1]:
+                st.simulated_by_n[n] = int(by_n[n, 0])
+                st.accepted_by_n[n] = int(by_n[n, 1])
+        for i in range(R):
+            st.attempts_samples.setdefault(int(meta[i, 3]), []).append(int(meta[i, 2]))
+        st.topologies_discarded = int(disc.value)
+        negs = [NegativeSample(m, int(s)) for m, s in
+                zip(_mechanisms(nadj, ntypes, npos, nmeta[:, 2]), nmeta[:, 1])]
+        # T_high trajectories of the accepted variants, f64, one launch
+        trajs = np.zeros((R, 0, c.T_high, 2))
+        if R:
+            ns = meta[:, 3].astype(np.int32)
+            table = PlanTable.from_records(rplans.reshape(-1), ns, device=dev)
+            pd = torch.from_numpy(rpos).to(dev)
+            topo = torch.arange(R, dtype=torch.int32, device=dev)
+            res = simulate_tensors(pd, table, c.T_high, topo, write_traj=True, traj_stride=NMAX, traj_f64=True)
+            if not bool((res["first_t"] == c.T_high).all()):
+                raise GenerationError("accepted variant locks at T_high on replay")
+            trajs = res["traj"].view(R, NMAX, c.T_high, 2).cpu().numpy()
+        mechs = _mechanisms(radj, rtypes, rpos, meta[:, 3])
+        recs = [GeneratedRecord(int(meta[i, 0]), int(meta[i, 1]), mechs[i],
+                                Trajectory(trajs[i, :int(meta[i, 3])].copy()), int(meta[i, 2])) for i in range(R)]
+        return recs, st, negs
+
+    def records(self):
+        c = self.config
+        slots = (c.count + c.variants_per_topology - 1) // c.variants_per_topology
+        emitted = 0
+        for s0 in range(0, slots, self.slot_block):
+            recs, st, negs = self._run_block(s0, min(self.slot_block, slots - s0))
+            self.stats.merge(st)
+            self.negatives.extend(negs)
+            for rec in recs:
+                if emitted >= c.count:
+                    return
+                emitted += 1
+                yield rec
+
+
+def generate_dataset(config: GenerationConfig, **kw):
+    """generator.py:378-383: (record iterator, run object)."""
+    run = GenerationRun(config, **kw)
+    return run.records(), run

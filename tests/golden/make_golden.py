@@ -273,9 +273,47 @@ def atlas_fixture():
     np.savez_compressed(OUT / "atlas_golden.npz", **d)
 
 
+def generator_fixture():
+    """GenerationRun (generator.py:336-375) records, stats and negatives."""
+    d = {"versions": versions()}
+    cases = [dict(count=30, seed=21), dict(count=12, seed=5, negative_rate=0.05),
+             dict(count=20, seed=77, n_min=5, n_max=9, variants_per_topology=2, max_attempts=300)]
+    for ci, kw in enumerate(cases):
+        cfg = ref_gen.GenerationConfig(**kw)
+        run = ref_gen.GenerationRun(cfg)
+        recs = list(run.records())
+        pos = np.full((len(recs), NMAX, 2), np.nan)
+        meta = np.zeros((len(recs), 4), dtype=np.int64)  # slot, variant, attempts, n
+        adj = np.zeros((len(recs), NMAX, NMAX), dtype=np.uint8)
+        for i, r in enumerate(recs):
+            n = r.mechanism.n
+            pos[i, :n] = r.mechanism.positions0
+            adj[i, :n, :n] = r.mechanism.adjacency
+            meta[i] = (r.slot, r.variant, r.attempts, n)
+        d[f"g{ci}_pos"] = pos
+        d[f"g{ci}_meta"] = meta
+        d[f"g{ci}_adj"] = adj
+        d[f"g{ci}_traj_last"] = np.stack([r.trajectory.positions[-1] for r in recs])  # last joint path
+        st = run.stats
+        sizes = sorted(st.simulated_by_n)
+        d[f"g{ci}_stats"] = np.array([[n, st.simulated_by_n.get(n, 0), st.accepted_by_n.get(n, 0)] for n in sizes])
+        d[f"g{ci}_discarded"] = np.array(st.topologies_discarded)
+        neg = np.full((len(run.negatives), NMAX, 2), np.nan)
+        negstep = np.array([x.locking_step for x in run.negatives], dtype=np.int64)
+        for i, x in enumerate(run.negatives):
+            neg[i, :x.mechanism.n] = x.mechanism.positions0
+        d[f"g{ci}_neg"] = neg
+        d[f"g{ci}_negstep"] = negstep
+        d[f"g{ci}_cfg"] = np.array([cfg.count, cfg.seed, cfg.n_min, cfg.n_max, cfg.variants_per_topology,
+                                     cfg.T_low, cfg.T_high, cfg.max_attempts, cfg.batch, cfg.topology_retries])
+        d[f"g{ci}_rates"] = np.array([cfg.ng_probability, cfg.negative_rate])
+    np.savez_compressed(OUT / "generator_golden.npz", **d)
+
+
 if __name__ == "__main__":
     sol = solver_fixture()
     curves_fixture(sol)
     atlas_fixture()
+    generator_fixture()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -1,0 +1,132 @@
+"""Host logic of the dataset-generation engine (la_gen_*) against the
+reference GenerationRun fixtures, with the ORACLE answering the two-fidelity
+gate on CPU (the GPU answers it in tests/test_gpu_generator.py).  The engine
+must reproduce records (slot, variant, attempts, poses), negatives and stats
+bit for bit — only the gate evaluation differs between the two tests."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import links_oracle as O
+from paper_2208_14567_b200 import _native as N
+
+NMAX = N.LA_MAX_JOINTS
+
+
+def _cfg(g, ci):
+    cfg = g[f"g{ci}_cfg"]
+    rates = g[f"g{ci}_rates"]
+    count, seed, n_min, n_max, vpt, T_low, T_high, max_att, batch, retries = (int(x) for x in cfg)
+    return count, N.LaGenCfg(seed, n_min, n_max, float(rates[0]), vpt, T_low, T_high, max_att, retries, batch,
+                             float(rates[1]))
+
+
+def _oracle_gate(pos, cand_plan, plans, m, T_low, T_high):
+    """first_t at T_high and the T_low lock step (-1 if none) per candidate."""
+    first = np.empty(m, dtype=np.int32)
+    low = np.empty(m, dtype=np.int32)
+    for p in np.unique(cand_plan[:m]):
+        rec = plans[p]
+        n = int(rec.n)
+        steps = [tuple(int(v) for v in rec.step[s]) for s in range(rec.nsteps)]
+        fixed = [k for k in range(n) if (rec.fixed_mask >> k) & 1]
+        idx = np.nonzero(cand_plan[:m] == p)[0]
+        x = pos[idx, :n]
+        lo = O.simulate(x, steps, fixed, T_low)["first_t"]
+        hi = O.simulate(x, steps, fixed, T_high)["first_t"]
+        low[idx] = np.where(lo < T_low, lo, -1)
+        first[idx] = hi
+    return first, low
+
+
+def run_engine(cfg, count, lookahead=3, cap=1 << 16):
+    lib = N.load()
+    slots = (count + cfg.variants - 1) // cfg.variants
+    eng = lib.la_gen_create(C.byref(cfg), 0, slots)
+    assert eng
+    try:
+        pos = np.zeros((cap, NMAX, 2))
+        cand_plan = np.zeros(cap, dtype=np.int32)
+        plans = (N.LaPlan * slots)()
+        n_plans = C.c_int32(0)
+        windows = 0
+        while True:
+            m = lib.la_gen_window(eng, lookahead, cap, 2, pos.ctypes.data, cand_plan.ctypes.data, plans,
+                                  C.byref(n_plans))
+            assert m >= 0, N.last_error()
+            if m == 0:
+                break
+            windows += 1
+            first, low = _oracle_gate(pos, cand_plan, plans, m, cfg.T_low, cfg.T_high)
+            assert lib.la_gen_consume(eng, pos.ctypes.data, first.ctypes.data, low.ctypes.data) == 0
+        R = lib.la_gen_count(eng, 0)
+        meta = np.zeros((R, 4), dtype=np.int64)
+        rpos = np.zeros((R, NMAX, 2))
+        rplans = (N.LaPlan * max(R, 1))()
+        adj = np.zeros((R, NMAX, NMAX), dtype=np.uint8)
+        types = np.zeros((R, NMAX), dtype=np.int8)
+        assert lib.la_gen_records(eng, meta.ctypes.data, rpos.ctypes.data, rplans, adj.ctypes.data,
+                                  types.ctypes.data) == 0
+        Q = lib.la_gen_count(eng, 1)
+        nmeta = np.zeros((Q, 3), dtype=np.int64)
+        npos = np.zeros((Q, NMAX, 2))
+        assert lib.la_gen_negatives(eng, nmeta.ctypes.data, npos.ctypes.data,
+                                    np.zeros((Q, NMAX, NMAX), dtype=np.uint8).ctypes.data,
+                                    np.zeros((Q, NMAX), dtype=np.int8).ctypes.data) == 0
+        by_n = np.zeros((NMAX + 1, 2), dtype=np.int64)
+        disc = C.c_int64(0)
+        assert lib.la_gen_stats(eng, by_n.ctypes.data, C.byref(disc)) == 0
+    finally:
+        lib.la_gen_destroy(eng)
+    return dict(meta=meta, pos=rpos, adj=adj, nmeta=nmeta, npos=npos, by_n=by_n, disc=disc.value, windows=windows)
+
+
+def check_against_golden(g, ci, out, count):
+    meta = out["meta"][:count]
+    assert np.array_equal(meta, g[f"g{ci}_meta"])
+    want_pos = g[f"g{ci}_pos"]
+    for i, n in enumerate(meta[:, 3]):
+        assert np.array_equal(out["pos"][i, :n], want_pos[i, :n])
+        assert np.array_equal(out["adj"][i, :n, :n], g[f"g{ci}_adj"][i, :n, :n])
+    stats = g[f"g{ci}_stats"]
+    got = np.array([[n, out["by_n"][n, 0], out["by_n"][n, 1]] for n in stats[:, 0]])
+    assert np.array_equal(got, stats)
+    assert int(out["by_n"][:, 0].sum()) == int(stats[:, 1].sum())
+    assert out["disc"] == int(g[f"g{ci}_discarded"])
+    negstep = g[f"g{ci}_negstep"]
+    assert np.array_equal(out["nmeta"][:, 1], negstep)
+    for i, n in enumerate(out["nmeta"][:, 2]):
+        assert np.array_equal(out["npos"][i, :n], g[f"g{ci}_neg"][i, :n])
+
+
+@pytest.mark.parametrize("ci", [0, 1, 2])
+def test_engine_matches_reference_run(golden, ci):
+    g = golden("generator_golden.npz")
+    count, cfg = _cfg(g, ci)
+    out = run_engine(cfg, count)
+    check_against_golden(g, ci, out, count)
+
+
+def test_engine_lookahead_invariance(golden):
+    """Look-ahead depth and window cap change only how much is screened."""
+    g = golden("generator_golden.npz")
+    count, cfg = _cfg(g, 2)
+    a = run_engine(cfg, count, lookahead=1)
+    b = run_engine(cfg, count, lookahead=7, cap=2048)
+    for k in ("meta", "pos", "nmeta", "npos", "by_n"):
+        assert np.array_equal(a[k], b[k], equal_nan=True)
+    assert a["windows"] >= 2 and b["windows"] >= 2
+
+
+def test_engine_bad_config():
+    lib = N.load()
+    cfg = N.LaGenCfg(0, 3, 8, 0.25, 5, 50, 200, 5000, 1000, 256, 0.0)
+    assert not lib.la_gen_create(C.byref(cfg), 0, 4)
+    cfg = N.LaGenCfg(0, 20, 20, 0.25, 5, 50, 200, 5000, 1000, 256, 0.0)
+    eng = lib.la_gen_create(C.byref(cfg), 0, 0)
+    assert eng
+    n_plans = C.c_int32(0)
+    assert lib.la_gen_window(eng, 2, 16, 1, None, None, None, C.byref(n_plans)) == 0
+    lib.la_gen_destroy(eng)
