@@ -472,6 +472,7 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
 
 # ----------------------------------------------------------------- C5 (scaled)
 C5_COUNT = 1_000_000
+GEN_COUNT = 50_000
 C5_QUERIES = 64
 
 
@@ -552,6 +553,45 @@ def bench_c5(torch, args, rank, world, peaks, flush, clk):
             "chamfer": {"pairs/s": pairs / (stages["chamfer"] / 1e3)},
             "config": {"workload": "C5 scaled: 1M candidates/GPU (5-20 joints, 3,907 generator topologies), T=200, "
                                    "64 Fourier queries, top-10; BASELINE configs[4] is 100M over 8 GPUs"}}
+
+
+def bench_gen(torch, args, rank, world, peaks, flush, clk):
+    """Dataset generation (generator.py:286-375, default GenerationConfig:
+    n in 8..20, 5 variants per topology, T_low 50 / T_high 200, 5,000-attempt
+    cap, batches of 256): native slot engine + device-drawn poses + GPU gate;
+    accepted T_high paths left on the device.  Slots are sharded by rank
+    (each rank its own slot range, no collective).  Host+device wall time
+    bracketed by device syncs; this stage is host-coupled by design."""
+    from paper_2208_14567_b200.generator import GenerationConfig, GenerationRun
+
+    slots = GEN_COUNT // 5
+
+    def run(count, s0, s1):
+        cfg = GenerationConfig(count=count, seed=2208)
+        r = GenerationRun(cfg, traj_on_device=True, lookahead=8, slot_range=(s0, s1))
+        R = sum(b.R for b in r.blocks())
+        return r, R
+
+    run(500, 10**6, 10**6 + 100)  # warm-up (other slots)
+    barrier(torch, world)
+    torch.cuda.synchronize()
+    clk.timed = True
+    t0 = time.perf_counter()
+    r, R = run(GEN_COUNT * world, rank * slots, (rank + 1) * slots)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    clk.timed = False
+    dt = max_over_ranks(torch, dt * 1e3, world) / 1e3
+    st = r.stats
+    return {"metric": "dataset generation: accepted records/sec (reference GenerationRun semantics)",
+            "value": world * R / dt, "unit": "records/s", "seconds": dt,
+            "simulated_candidates_per_s": world * st.simulated / dt,
+            "screened_candidates_per_s": world * r.screened / dt,
+            "records_per_gpu": R, "simulated_per_gpu": st.simulated, "discarded_topologies": st.topologies_discarded,
+            "windows": r.windows, "host_ms": {k: v * 1e3 for k, v in r.timings.items()},
+            "reference_cpu": {"candidates_per_s_per_thread": 24500, "source": "SURVEY.md probe P3 (gated, 1 thread)"},
+            "config": {"workload": f"{GEN_COUNT} records/GPU, default GenerationConfig, seed 2208, slots sharded "
+                                   "by rank, trajectories kept on device"}}
 
 
 # ----------------------------------------------------------------- CPU baseline
@@ -647,7 +687,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--skip", default="", help="comma list of c3,c4,cpu to skip")
+    ap.add_argument("--skip", default="", help="comma list of c3,c4,c5,gen,cpu to skip")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -684,6 +724,8 @@ def main():
         secondary["chamfer"] = bench_c4(torch, args, rank, world, peaks, flush, clk)
     if "c5" not in skip:
         secondary["end_to_end"] = bench_c5(torch, args, rank, world, peaks, flush, clk)
+    if "gen" not in skip:
+        secondary["generation"] = bench_gen(torch, args, rank, world, peaks, flush, clk)
     clk.stop()
     cpu = None
     if rank == 0 and world == 1 and "cpu" not in skip:

@@ -236,6 +236,21 @@ void* la_gen_create(const la_gen_cfg* cfg, int64_t slot0, int64_t n_slots);
 void la_gen_destroy(void* engine);
 int64_t la_gen_window(void* engine, int32_t lookahead, int64_t cap, int32_t threads, double* pos /* [cap][20][2] */,
                       int32_t* cand_plan /* [cap] */, la_plan* plans /* [n_slots] */, int32_t* n_plans);
+/* Device-drawn window: one descriptor per reference batch; candidate c of
+ * the batch is the c-th pose of the stream starting at `state`.          */
+typedef struct la_gen_batch {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo; /* PCG64 128-bit state / increment */
+  int64_t first;                               /* first candidate index in window  */
+  int32_t k, n, plan, _pad;
+} la_gen_batch;
+int64_t la_gen_window_dev(void* engine, int32_t lookahead, int64_t cap, la_gen_batch* batches /* host */,
+                          int64_t max_batches, int64_t* n_batches, la_plan* plans, int32_t* n_plans);
+/* device kernel: poses [cand][stride][2] f64 (pivot/tip pinned, NaN beyond
+ * n) and plan index per candidate, from device-resident descriptors       */
+int la_gen_poses(const la_gen_batch* batches, int64_t n_batches, int32_t stride, double* pos, int32_t* topo,
+                 void* stream);
+/* pos may be NULL for device-drawn windows (poses of accepted / negative
+ * candidates are redrawn on the host from the batch stream state)         */
 int la_gen_consume(void* engine, const double* pos, const int32_t* first_t, const int32_t* low_t);
 int64_t la_gen_count(void* engine, int32_t what /* 0 records, 1 negatives */);
 int la_gen_records(void* engine, int64_t* meta /* [R][4] */, double* pos, la_plan* plans, uint8_t* adj,

@@ -48,6 +48,8 @@ EXPORTS = (
     "la_gen_create",
     "la_gen_destroy",
     "la_gen_window",
+    "la_gen_window_dev",
+    "la_gen_poses",
     "la_gen_consume",
     "la_gen_count",
     "la_gen_records",
@@ -70,6 +72,23 @@ class LaPlan(C.Structure):
 
 
 assert C.sizeof(LaPlan) == 64
+
+
+class LaGenBatch(C.Structure):
+    _fields_ = [
+        ("state_hi", C.c_uint64),
+        ("state_lo", C.c_uint64),
+        ("inc_hi", C.c_uint64),
+        ("inc_lo", C.c_uint64),
+        ("first", C.c_int64),
+        ("k", C.c_int32),
+        ("n", C.c_int32),
+        ("plan", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+assert C.sizeof(LaGenBatch) == 56
 
 
 class LaGenCfg(C.Structure):
@@ -197,6 +216,9 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_gen_destroy.restype = None
     lib.la_gen_window.argtypes = [vp, i32, i64, i32, vp, vp, vp, vp]
     lib.la_gen_window.restype = i64
+    lib.la_gen_window_dev.argtypes = [vp, i32, i64, vp, i64, vp, vp, vp]
+    lib.la_gen_window_dev.restype = i64
+    lib.la_gen_poses.argtypes = [vp, i64, i32, vp, vp, vp]
     lib.la_gen_consume.argtypes = [vp, vp, vp, vp]
     lib.la_gen_count.argtypes = [vp, i32]
     lib.la_gen_count.restype = i64
@@ -209,7 +231,7 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_device_sm_count.argtypes = []
     for name in EXPORTS:
         if name not in ("la_last_error", "la_compact_workspace", "la_chamfer_workspace", "la_gen_create",
-                        "la_gen_destroy", "la_gen_window", "la_gen_count"):
+                        "la_gen_destroy", "la_gen_window", "la_gen_window_dev", "la_gen_count"):
             getattr(lib, name).restype = C.c_int
 
 

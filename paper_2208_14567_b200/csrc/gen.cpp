@@ -105,6 +105,20 @@ struct Pcg64 {
     step();
   }
   void step() { state = state * PCG_MULT + inc; }
+  // jump the LCG ahead by `delta` steps (square-and-multiply on the affine map)
+  void advance(u128 delta) {
+    u128 cm = PCG_MULT, cp = inc, am = 1, ap = 0;
+    while (delta) {
+      if (delta & 1u) {
+        am *= cm;
+        ap = ap * cm + cp;
+      }
+      cp = (cm + 1) * cp;
+      cm *= cm;
+      delta >>= 1;
+    }
+    state = am * state + ap;
+  }
   uint64_t next64() {
     step();
     const uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
@@ -428,8 +442,9 @@ struct Accepted {
 struct Batch {
   int64_t first = 0;  // index of its first candidate in the window
   int k = 0;          // candidates
+  Pcg64 start;        // pose stream state before drawing it
   Pcg64 after;        // pose stream state after drawing it
-  explicit Batch(const Pcg64& r) : after(r) {}
+  explicit Batch(const Pcg64& r) : start(r), after(r) {}
 };
 
 struct Slot {
@@ -518,6 +533,52 @@ int batch_size(const Engine& E, int64_t consumed) {
   return (int)(left < E.cfg.batch ? left : E.cfg.batch);
 }
 
+// Lay out the next look-ahead window: for every searching slot, up to
+// `lookahead` consecutive batches of its current variant schedule (batch
+// states chained from the slot's real pose stream).  Slots that would
+// overflow `cap` wait for the next window.  Returns the candidate count, 0
+// when every slot is done, <0 on error.
+int64_t layout(Engine& E, int32_t lookahead, int64_t cap, la_plan* plans, int32_t* n_plans,
+               std::vector<Slot*>& act) {
+  if (E.error) {
+    la::set_error("%s", E.err);
+    return E.error;
+  }
+  if (lookahead < 1) lookahead = 1;
+  int64_t total = 0;
+  int np = 0;
+  for (auto& S : E.slots) {
+    S.win.clear();
+    if (S.state != 1) continue;
+    int64_t consumed = S.consumed, need = 0;
+    std::vector<Batch> w;
+    Pcg64 r = S.pos;
+    for (int i = 0; i < lookahead; ++i) {
+      const int k = batch_size(E, consumed);
+      if (k <= 0) break;
+      Batch b(r);
+      b.first = total + need;
+      b.k = k;
+      r.advance((u128)k * (u128)(2 * S.n));
+      w.push_back(b);
+      need += k;
+      consumed += k;
+    }
+    if (total + need > cap) {
+      if (total > 0) break;
+      la::set_error("la_gen_window: one window (%lld) exceeds cap %lld", (long long)need, (long long)cap);
+      return LA_EWS;
+    }
+    S.plan_slot = np;
+    plans[np++] = to_rec(S.mech, S.plan);
+    S.win.swap(w);
+    act.push_back(&S);
+    total += need;
+  }
+  *n_plans = np;
+  return total;
+}
+
 }  // namespace
 
 extern "C" {
@@ -559,41 +620,9 @@ void la_gen_destroy(void* h) { delete static_cast<Engine*>(h); }
 int64_t la_gen_window(void* h, int32_t lookahead, int64_t cap, int32_t threads, double* pos, int32_t* cand_plan,
                       la_plan* plans, int32_t* n_plans) {
   Engine& E = *static_cast<Engine*>(h);
-  if (E.error) {
-    la::set_error("%s", E.err);
-    return E.error;
-  }
-  if (lookahead < 1) lookahead = 1;
-  int64_t total = 0;
-  int np = 0;
   std::vector<Slot*> act;
-  std::vector<int64_t> base;
-  for (auto& S : E.slots) {
-    S.win.clear();
-    if (S.state != 1) continue;
-    int64_t consumed = S.consumed, need = 0;
-    std::vector<Batch> w;
-    for (int i = 0; i < lookahead; ++i) {
-      const int k = batch_size(E, consumed);
-      if (k <= 0) break;
-      Batch b(S.pos);
-      b.first = total + need;
-      b.k = k;
-      w.push_back(b);
-      need += k;
-      consumed += k;
-    }
-    if (total + need > cap) {
-      if (total > 0) break;
-      la::set_error("la_gen_window: one batch (%lld) exceeds cap %lld", (long long)need, (long long)cap);
-      return LA_EWS;
-    }
-    S.plan_slot = np;
-    plans[np++] = to_rec(S.mech, S.plan);
-    S.win.swap(w);
-    act.push_back(&S);
-    total += need;
-  }
+  const int64_t total = layout(E, lookahead, cap, plans, n_plans, act);
+  if (total <= 0) return total;
   parallel_for((int64_t)act.size(), threads, [&](int64_t a) {
     Slot& S = *act[a];
     Pcg64 r = S.pos;
@@ -606,7 +635,39 @@ int64_t la_gen_window(void* h, int32_t lookahead, int64_t cap, int32_t threads, 
       b.after = r;
     }
   });
-  *n_plans = np;
+  return total;
+}
+
+// Same window, drawn on the device: one descriptor per batch (its pose
+// stream state, first candidate, size, joint count, plan index) for
+// la_gen_poses.  Candidate c of a batch uses stream draws [2nc, 2n(c+1)).
+int64_t la_gen_window_dev(void* h, int32_t lookahead, int64_t cap, la_gen_batch* batches, int64_t max_batches,
+                          int64_t* n_batches, la_plan* plans, int32_t* n_plans) {
+  Engine& E = *static_cast<Engine*>(h);
+  std::vector<Slot*> act;
+  const int64_t total = layout(E, lookahead, cap, plans, n_plans, act);
+  if (total <= 0) return total;
+  int64_t nb = 0;
+  for (Slot* S : act)
+    for (auto& b : S->win) {
+      if (nb >= max_batches) {
+        la::set_error("la_gen_window_dev: more than %lld batches", (long long)max_batches);
+        return LA_EWS;
+      }
+      la_gen_batch& d = batches[nb++];
+      d.state_hi = (uint64_t)(b.start.state >> 64);
+      d.state_lo = (uint64_t)b.start.state;
+      d.inc_hi = (uint64_t)(b.start.inc >> 64);
+      d.inc_lo = (uint64_t)b.start.inc;
+      d.first = b.first;
+      d.k = b.k;
+      d.n = S->n;
+      d.plan = (int32_t)S->plan_slot;
+      d._pad = 0;
+      b.after = b.start;
+      b.after.advance((u128)b.k * (u128)(2 * S->n));
+    }
+  *n_batches = nb;
   return total;
 }
 
@@ -615,6 +676,17 @@ int64_t la_gen_window(void* h, int32_t lookahead, int64_t cap, int32_t threads, 
 int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int32_t* low_t) {
   Engine& E = *static_cast<Engine*>(h);
   const la_gen_cfg& cfg = E.cfg;
+  // pose of candidate c of batch b: from the window buffer, or redrawn from
+  // the batch's stream state (device-drawn windows)
+  auto pose = [&](const Slot& S, const Batch& b, int c, double* row) {
+    if (pos) {
+      std::memcpy(row, pos + (size_t)(b.first + c) * LA_MAX_JOINTS * 2, sizeof(double) * LA_MAX_JOINTS * 2);
+      return;
+    }
+    Pcg64 r = b.start;
+    r.advance((u128)c * (u128)(2 * S.n));
+    draw_pose(r, S.n, row);
+  };
   for (size_t si = 0; si < E.slots.size(); ++si) {
     Slot& S = E.slots[si];
     if (S.state != 1 || S.win.empty()) continue;
@@ -635,7 +707,7 @@ int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int
             ng.slot = S.id;
             ng.step = low_t[g];
             ng.mech = S.mech;
-            std::memcpy(ng.pos, pos + (size_t)g * LA_MAX_JOINTS * 2, sizeof(ng.pos));
+            pose(S, b, c, &ng.pos[0][0]);
             E.slot_negs[si].push_back(ng);
           }
           continue;
@@ -648,7 +720,7 @@ int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int
       ++used;
       if (hit >= 0) {
         Accepted a;
-        std::memcpy(a.pos, pos + (size_t)(b.first + hit) * LA_MAX_JOINTS * 2, sizeof(a.pos));
+        pose(S, b, hit, &a.pos[0][0]);
         a.attempts = S.consumed + hit + 1;
         S.acc.push_back(a);
         S.consumed = 0;

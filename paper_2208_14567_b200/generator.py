@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -325,6 +326,34 @@ class GeneratedRecord:
     attempts: int
 
 
+@dataclass
+class GeneratedBlock:
+    """Records of a block of slots as arrays (slot order): meta (R, 4) =
+    slot, variant, attempts, n; pos0 (R, 20, 2); adjacency (R, 20, 20);
+    types (R, 20); traj (sum n, T_high, 2) f64 with record i in rows
+    row0[i]:row0[i+1] (a CUDA tensor with ``traj_on_device``, for pipelines
+    that normalise and index the paths without a host round trip)."""
+
+    meta: np.ndarray
+    pos0: np.ndarray
+    adjacency: np.ndarray
+    types: np.ndarray
+    traj: np.ndarray
+    row0: np.ndarray
+
+    @property
+    def R(self) -> int:
+        return len(self.meta)
+
+    def record(self, i: int) -> GeneratedRecord:
+        slot, variant, attempts, n = (int(x) for x in self.meta[i])
+        mech = Mechanism(self.adjacency[i, :n, :n].copy(), self.types[i, :n].copy(), self.pos0[i, :n].copy())
+        t = self.traj[self.row0[i]:self.row0[i + 1]]
+        if not isinstance(t, np.ndarray):
+            t = t.cpu().numpy()
+        return GeneratedRecord(slot, variant, mech, Trajectory(t), attempts)
+
+
 def _mechanisms(adj: np.ndarray, types: np.ndarray, pos: np.ndarray, n: np.ndarray) -> list[Mechanism]:
     return [Mechanism(adj[i, :n[i], :n[i]].copy(), types[i, :n[i]].astype(np.int8), pos[i, :n[i]].copy())
             for i in range(len(n))]
@@ -345,7 +374,8 @@ class GenerationRun:
     """
 
     def __init__(self, config: GenerationConfig, *, lookahead: int = 4, slot_block: int = 1 << 14,
-                 window_cap: int = 1 << 21, threads: int | None = None, device=None):
+                 window_cap: int = 1 << 21, threads: int | None = None, device=None, device_poses: bool = True,
+                 traj_on_device: bool = False, slot_range: tuple[int, int] | None = None):
         self.config = config
         self.stats = GenerationStats()
         self.negatives: list[NegativeSample] = []
@@ -354,6 +384,10 @@ class GenerationRun:
         self.window_cap = int(window_cap)
         self.threads = threads
         self.device = device
+        self.slot_range = slot_range  # (first, end) slots of this shard; records() then cuts at count per shard
+        self.traj_on_device = bool(traj_on_device)  # GeneratedBlock.traj stays a CUDA tensor
+        self.device_poses = bool(device_poses)  # poses drawn by la_gen_poses (else host threads + H2D)
+        self.timings = {"window": 0.0, "device": 0.0, "consume": 0.0, "finish": 0.0}  # host wall seconds
         self.windows = 0         # GPU launches of the gate
         self.screened = 0        # candidates screened on the GPU (>= stats.simulated)
 
@@ -378,25 +412,47 @@ class GenerationRun:
         fused = c.T_high == 4 * c.T_low
         try:
             per_window = min(self.window_cap, max(c.batch, nslots * self.lookahead * c.batch))
-            pos_h = torch.empty((per_window, NMAX, 2), dtype=torch.float64).pin_memory()
-            plan_h = torch.empty(per_window, dtype=torch.int32).pin_memory()
+            stride = int(c.n_max)
             plans_h = np.zeros((nslots, 64), dtype=np.uint8)
             flags_h = torch.empty((2, per_window), dtype=torch.int32).pin_memory()
             n_plans = C.c_int32(0)
-            pos_d = torch.empty((per_window, NMAX, 2), dtype=torch.float64, device=dev)
+            pos_d = torch.empty((per_window, stride, 2), dtype=torch.float64, device=dev)
+            topo_d = torch.empty(per_window, dtype=torch.int32, device=dev)
+            if self.device_poses:
+                max_b = nslots * self.lookahead
+                desc_h = torch.empty((max_b, C.sizeof(N.LaGenBatch)), dtype=torch.uint8).pin_memory()
+                desc_d = torch.empty_like(desc_h, device=dev)
+                nb = C.c_int64(0)
+            else:
+                pos_h = torch.empty((per_window, NMAX, 2), dtype=torch.float64).pin_memory()
+                plan_h = torch.empty(per_window, dtype=torch.int32).pin_memory()
+            tm = self.timings
             while True:
-                m = lib.la_gen_window(eng, self.lookahead, per_window, th, pos_h.data_ptr(), plan_h.data_ptr(),
-                                      plans_h.ctypes.data, C.byref(n_plans))
+                t0 = time.perf_counter()
+                if self.device_poses:
+                    m = lib.la_gen_window_dev(eng, self.lookahead, per_window, desc_h.data_ptr(), max_b, C.byref(nb),
+                                              plans_h.ctypes.data, C.byref(n_plans))
+                else:
+                    m = lib.la_gen_window(eng, self.lookahead, per_window, th, pos_h.data_ptr(), plan_h.data_ptr(),
+                                          plans_h.ctypes.data, C.byref(n_plans))
                 if m < 0:
                     raise GenerationError(N.last_error())
                 if m == 0:
                     break
+                t1 = time.perf_counter()
+                tm["window"] += t1 - t0
                 np_ = n_plans.value
                 ns = plans_h[:np_, :2].copy().view(np.int16)[:, 0].astype(np.int32)
                 table = PlanTable.from_records(plans_h[:np_].reshape(-1), ns, device=dev)
                 pd = pos_d[:m]
-                pd.copy_(pos_h[:m], non_blocking=True)
-                topo = plan_h[:m].to(dev, non_blocking=True)
+                topo = topo_d[:m]
+                if self.device_poses:
+                    desc_d[:nb.value].copy_(desc_h[:nb.value], non_blocking=True)
+                    N.check(lib.la_gen_poses(desc_d.data_ptr(), nb.value, stride, pd.data_ptr(), topo.data_ptr(),
+                                             N.stream_ptr()), "la_gen_poses")
+                else:
+                    pd.copy_(pos_h[:m, :stride], non_blocking=True)
+                    topo.copy_(plan_h[:m], non_blocking=True)
                 if fused:
                     res = simulate_tensors(pd, table, c.T_high, topo, write_traj=False, low=True, gate_only=True)
                     flags_h[0, :m].copy_(res["first_t"], non_blocking=True)
@@ -408,11 +464,16 @@ class GenerationRun:
                     ft = lo["first_t"]
                     flags_h[1, :m].copy_(torch.where(ft < c.T_low, ft, torch.full_like(ft, -1)), non_blocking=True)
                 torch.cuda.current_stream(dev).synchronize()
+                t2 = time.perf_counter()
+                tm["device"] += t2 - t1
                 self.windows += 1
                 self.screened += int(m)
-                rc = lib.la_gen_consume(eng, pos_h.data_ptr(), flags_h[0].data_ptr(), flags_h[1].data_ptr())
+                src = None if self.device_poses else pos_h.data_ptr()
+                rc = lib.la_gen_consume(eng, src, flags_h[0].data_ptr(), flags_h[1].data_ptr())
                 if rc != 0:
                     raise GenerationError(N.last_error())
+                tm["consume"] += time.perf_counter() - t2
+            t3 = time.perf_counter()
             # records, negatives, stats
             R = lib.la_gen_count(eng, 0)
             meta = np.zeros((R, 4), dtype=np.int64)
@@ -444,35 +505,46 @@ class GenerationRun:
         st.topologies_discarded = int(disc.value)
         negs = [NegativeSample(m, int(s)) for m, s in
                 zip(_mechanisms(nadj, ntypes, npos, nmeta[:, 2]), nmeta[:, 1])]
-        # T_high trajectories of the accepted variants, f64, one launch
-        trajs = np.zeros((R, 0, c.T_high, 2))
+        # T_high trajectories of the accepted variants (f64, n rows per
+        # record packed back to back), one launch, one D2H
+        ns = meta[:, 3].astype(np.int64)
+        row0 = np.zeros(R + 1, dtype=np.int64)
+        np.cumsum(ns, out=row0[1:])
+        traj = np.zeros((0, c.T_high, 2))
         if R:
-            ns = meta[:, 3].astype(np.int32)
-            table = PlanTable.from_records(rplans.reshape(-1), ns, device=dev)
-            pd = torch.from_numpy(rpos).to(dev)
+            table = PlanTable.from_records(rplans.reshape(-1), ns.astype(np.int32), device=dev)
+            pd = torch.from_numpy(rpos[:, :int(ns.max())].copy()).to(dev)
             topo = torch.arange(R, dtype=torch.int32, device=dev)
-            res = simulate_tensors(pd, table, c.T_high, topo, write_traj=True, traj_stride=NMAX, traj_f64=True)
+            tbuf = torch.empty((int(row0[-1]), c.T_high, 2), dtype=torch.float64, device=dev)
+            res = simulate_tensors(pd, table, c.T_high, topo, write_traj=True, traj=tbuf,
+                                   traj_row=torch.from_numpy(row0[:-1]).to(dev), traj_f64=True)
             if not bool((res["first_t"] == c.T_high).all()):
                 raise GenerationError("accepted variant locks at T_high on replay")
-            trajs = res["traj"].view(R, NMAX, c.T_high, 2).cpu().numpy()
-        mechs = _mechanisms(radj, rtypes, rpos, meta[:, 3])
-        recs = [GeneratedRecord(int(meta[i, 0]), int(meta[i, 1]), mechs[i],
-                                Trajectory(trajs[i, :int(meta[i, 3])].copy()), int(meta[i, 2])) for i in range(R)]
-        return recs, st, negs
+            traj = tbuf if self.traj_on_device else tbuf.cpu().numpy()
+        self.timings["finish"] += time.perf_counter() - t3
+        return GeneratedBlock(meta, rpos, radj, rtypes, traj, row0), st, negs
 
-    def records(self):
+    def blocks(self):
+        """Bulk output: one ``GeneratedBlock`` of arrays per slot block (all
+        records of those slots, before the ``count`` cut)."""
         c = self.config
-        slots = (c.count + c.variants_per_topology - 1) // c.variants_per_topology
-        emitted = 0
-        for s0 in range(0, slots, self.slot_block):
-            recs, st, negs = self._run_block(s0, min(self.slot_block, slots - s0))
+        lo, hi = self.slot_range or (0, (c.count + c.variants_per_topology - 1) // c.variants_per_topology)
+        for s0 in range(lo, hi, self.slot_block):
+            blk, st, negs = self._run_block(s0, min(self.slot_block, hi - s0))
             self.stats.merge(st)
             self.negatives.extend(negs)
-            for rec in recs:
-                if emitted >= c.count:
+            yield blk
+
+    def records(self):
+        """generator.py:346-375: GeneratedRecord per accepted variant, slot
+        order, cut at ``count``."""
+        emitted = 0
+        for blk in self.blocks():
+            for i in range(blk.R):
+                if emitted >= self.config.count:
                     return
                 emitted += 1
-                yield rec
+                yield blk.record(i)
 
 
 def generate_dataset(config: GenerationConfig, **kw):

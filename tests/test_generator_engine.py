@@ -41,7 +41,25 @@ def _oracle_gate(pos, cand_plan, plans, m, T_low, T_high):
     return first, low
 
 
-def run_engine(cfg, count, lookahead=3, cap=1 << 16):
+def _numpy_poses(batches, nb, m):
+    """Poses of a device-drawn window, drawn by numpy from the descriptors."""
+    pos = np.full((m, NMAX, 2), np.nan)
+    cand_plan = np.zeros(m, dtype=np.int32)
+    bg = np.random.PCG64()
+    for i in range(nb):
+        b = batches[i]
+        bg.state = {"bit_generator": "PCG64",
+                    "state": {"state": (b.state_hi << 64) | b.state_lo, "inc": (b.inc_hi << 64) | b.inc_lo},
+                    "has_uint32": 0, "uinteger": 0}
+        x = np.random.Generator(bg).uniform(size=(b.k, b.n, 2))
+        x[:, 0] = (0.5, 0.5)
+        x[:, 1] = (0.55, 0.5)
+        pos[b.first:b.first + b.k, :b.n] = x
+        cand_plan[b.first:b.first + b.k] = b.plan
+    return pos, cand_plan
+
+
+def run_engine(cfg, count, lookahead=3, cap=1 << 16, device_windows=False):
     lib = N.load()
     slots = (count + cfg.variants - 1) // cfg.variants
     eng = lib.la_gen_create(C.byref(cfg), 0, slots)
@@ -51,16 +69,24 @@ def run_engine(cfg, count, lookahead=3, cap=1 << 16):
         cand_plan = np.zeros(cap, dtype=np.int32)
         plans = (N.LaPlan * slots)()
         n_plans = C.c_int32(0)
+        batches = (N.LaGenBatch * 4096)()
+        nb = C.c_int64(0)
         windows = 0
         while True:
-            m = lib.la_gen_window(eng, lookahead, cap, 2, pos.ctypes.data, cand_plan.ctypes.data, plans,
-                                  C.byref(n_plans))
+            if device_windows:
+                m = lib.la_gen_window_dev(eng, lookahead, cap, batches, 4096, C.byref(nb), plans, C.byref(n_plans))
+            else:
+                m = lib.la_gen_window(eng, lookahead, cap, 2, pos.ctypes.data, cand_plan.ctypes.data, plans,
+                                      C.byref(n_plans))
             assert m >= 0, N.last_error()
             if m == 0:
                 break
             windows += 1
+            if device_windows:
+                pos, cand_plan = _numpy_poses(batches, nb.value, m)
             first, low = _oracle_gate(pos, cand_plan, plans, m, cfg.T_low, cfg.T_high)
-            assert lib.la_gen_consume(eng, pos.ctypes.data, first.ctypes.data, low.ctypes.data) == 0
+            src = None if device_windows else pos.ctypes.data
+            assert lib.la_gen_consume(eng, src, first.ctypes.data, low.ctypes.data) == 0
         R = lib.la_gen_count(eng, 0)
         meta = np.zeros((R, 4), dtype=np.int64)
         rpos = np.zeros((R, NMAX, 2))
@@ -106,6 +132,16 @@ def test_engine_matches_reference_run(golden, ci):
     g = golden("generator_golden.npz")
     count, cfg = _cfg(g, ci)
     out = run_engine(cfg, count)
+    check_against_golden(g, ci, out, count)
+
+
+@pytest.mark.parametrize("ci", [1, 2])
+def test_engine_device_windows(golden, ci):
+    """Descriptor windows (stream states jumped ahead on the host, poses of
+    accepted / negative candidates redrawn from them) give the same run."""
+    g = golden("generator_golden.npz")
+    count, cfg = _cfg(g, ci)
+    out = run_engine(cfg, count, lookahead=5, device_windows=True)
     check_against_golden(g, ci, out, count)
 
 

@@ -58,3 +58,55 @@ def test_generation_split_gate_and_blocks(golden):
                             max_attempts=400)
     recs = list(GenerationRun(cfg2).records())
     assert len(recs) == 8 and all(r.trajectory.positions.shape[1] == 120 for r in recs)
+
+
+def test_device_poses_bit_exact():
+    """la_gen_poses draws exactly numpy's uniform(size=(k, n, 2)) from a
+    jumped PCG64 state, pivot / tip pinned, NaN beyond n."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2208_14567_b200 import _native as N
+
+    lib = N.load()
+    rng = np.random.default_rng(99)
+    nb = 7
+    desc = (N.LaGenBatch * nb)()
+    want = []
+    first = 0
+    for i in range(nb):
+        bg = np.random.PCG64([int(x) for x in rng.integers(0, 2**31, size=3)])
+        st = bg.state["state"]
+        n, k = int(rng.integers(4, 21)), int(rng.integers(1, 600))
+        d = desc[i]
+        d.state_hi, d.state_lo = st["state"] >> 64, st["state"] & ((1 << 64) - 1)
+        d.inc_hi, d.inc_lo = st["inc"] >> 64, st["inc"] & ((1 << 64) - 1)
+        d.first, d.k, d.n, d.plan = first, k, n, i
+        x = np.random.Generator(bg).uniform(size=(k, n, 2))
+        x[:, 0] = (0.5, 0.5)
+        x[:, 1] = (0.55, 0.5)
+        want.append((first, k, n, x))
+        first += k
+    raw = np.frombuffer(bytes(desc), dtype=np.uint8)
+    dd = torch.from_numpy(raw.copy()).cuda()
+    pos = torch.empty((first, 20, 2), dtype=torch.float64, device="cuda")
+    topo = torch.empty(first, dtype=torch.int32, device="cuda")
+    N.check(lib.la_gen_poses(dd.data_ptr(), nb, 20, pos.data_ptr(), topo.data_ptr(), N.stream_ptr()), "poses")
+    got = pos.cpu().numpy()
+    tp = topo.cpu().numpy()
+    for i, (f, k, n, x) in enumerate(want):
+        assert np.array_equal(got[f:f + k, :n], x)
+        assert np.isnan(got[f:f + k, n:]).all()
+        assert (tp[f:f + k] == i).all()
+
+
+def test_host_and_device_windows_agree(golden):
+    g = golden("generator_golden.npz")
+    cfg = _config(g, 1)
+    a = GenerationRun(cfg, device_poses=False)
+    b = GenerationRun(cfg, device_poses=True, lookahead=9)
+    ra, rb = list(a.records()), list(b.records())
+    assert [(r.slot, r.variant, r.attempts) for r in ra] == [(r.slot, r.variant, r.attempts) for r in rb]
+    assert all(np.array_equal(x.mechanism.positions0, y.mechanism.positions0) for x, y in zip(ra, rb))
+    assert [x.locking_step for x in a.negatives] == [x.locking_step for x in b.negatives]
