@@ -231,6 +231,8 @@ typedef struct la_gen_cfg {
   double ng_prob;
   int32_t variants, T_low, T_high, max_attempts, retries, batch;
   double negative_rate;
+  int32_t threads; /* host threads for window layout / flag walks (0: 1) */
+  int32_t _pad;
 } la_gen_cfg;
 void* la_gen_create(const la_gen_cfg* cfg, int64_t slot0, int64_t n_slots);
 void la_gen_destroy(void* engine);

@@ -104,6 +104,8 @@ class LaGenCfg(C.Structure):
         ("retries", C.c_int32),
         ("batch", C.c_int32),
         ("negative_rate", C.c_double),
+        ("threads", C.c_int32),
+        ("_pad", C.c_int32),
     ]
 
 

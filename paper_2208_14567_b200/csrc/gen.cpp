@@ -459,6 +459,7 @@ struct Slot {
   std::vector<Accepted> acc;
   std::vector<Batch> win;  // current look-ahead window
   int64_t plan_slot = -1;  // plan index of this slot in the last window
+  int64_t sim = 0, nacc = 0, disc = 0;  // GenerationStats tallies of this slot (joint count n)
   Slot(int64_t s, int64_t seed) : id(s), topo(stream(seed, s, 0)), pos(stream(seed, s, 1)), neg(stream(seed, s, 2)) {}
 };
 
@@ -478,14 +479,8 @@ struct Negative {
 struct Engine {
   la_gen_cfg cfg;
   std::vector<Slot> slots;
-  std::vector<Record> records;      // per slot in order (filled at slot completion)
   std::vector<std::vector<Record>> slot_records;
   std::vector<std::vector<Negative>> slot_negs;
-  int64_t sim_by_n[LA_MAX_JOINTS + 1] = {0};
-  int64_t acc_by_n[LA_MAX_JOINTS + 1] = {0};
-  int64_t discarded = 0;
-  std::vector<std::vector<int64_t>> succ_attempts;  // per slot: attempts of recorded successes
-  std::vector<int64_t> slot_sim;                      // per slot simulated count (for stats merge order)
   int error = 0;
   char err[200] = "";
 };
@@ -600,7 +595,6 @@ void* la_gen_create(const la_gen_cfg* cfg, int64_t slot0, int64_t n_slots) {
   }
   E->slot_records.resize((size_t)n_slots);
   E->slot_negs.resize((size_t)n_slots);
-  E->succ_attempts.resize((size_t)n_slots);
   for (auto& S : E->slots)
     if (S.state == 3) {
       E->error = LA_ERANGE;
@@ -687,9 +681,10 @@ int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int
     r.advance((u128)c * (u128)(2 * S.n));
     draw_pose(r, S.n, row);
   };
-  for (size_t si = 0; si < E.slots.size(); ++si) {
-    Slot& S = E.slots[si];
-    if (S.state != 1 || S.win.empty()) continue;
+  // slots are independent: walk them in parallel, each in its own stream order
+  parallel_for((int64_t)E.slots.size(), cfg.threads, [&](int64_t si) {
+    Slot& S = E.slots[(size_t)si];
+    if (S.state != 1 || S.win.empty()) return;
     size_t used = 0;  // batches fully consumed
     bool restart_window = false;
     for (size_t bi = 0; bi < S.win.size() && S.state == 1 && !restart_window; ++bi) {
@@ -708,7 +703,7 @@ int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int
             ng.step = low_t[g];
             ng.mech = S.mech;
             pose(S, b, c, &ng.pos[0][0]);
-            E.slot_negs[si].push_back(ng);
+            E.slot_negs[(size_t)si].push_back(ng);
           }
           continue;
         }
@@ -733,33 +728,32 @@ int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int
             r.mech = S.mech;
             r.plan = S.plan;
             std::memcpy(r.pos, S.acc[v].pos, sizeof(r.pos));
-            E.slot_records[si].push_back(r);
-            E.sim_by_n[S.n] += r.attempts;
-            E.acc_by_n[S.n] += 1;
-            E.succ_attempts[si].push_back(r.attempts);
+            E.slot_records[(size_t)si].push_back(r);
+            S.sim += r.attempts;
+            S.nacc += 1;
           }
           S.state = 2;
         }
         continue;  // next variant continues on the next batch of the window
       }
       S.consumed += b.k;
-      if (S.consumed >= cfg.max_attempts) {  // variant failed: discard topology (generator.py:581-583)
+      if (S.consumed >= cfg.max_attempts) {  // variant failed: discard topology (generator.py:318-320)
         int64_t wasted = cfg.max_attempts;
         for (auto& a : S.acc) wasted += a.attempts;
-        E.sim_by_n[S.n] += wasted;
-        E.discarded += 1;
-        if (!next_topology(E, S)) {
-          S.state = 3;
-          E.error = LA_ERANGE;
-          snprintf(E.err, sizeof(E.err), "slot %lld: no topology with feasible variants (n=%d)",
-                   (long long)S.id, S.n);
-        }
+        S.sim += wasted;
+        S.disc += 1;
+        if (!next_topology(E, S)) S.state = 3;
         restart_window = true;  // next_topology cleared the window
       }
     }
     (void)used;
     S.win.clear();  // unconsumed look-ahead is dropped; the real stream sits after the last consumed batch
-  }
+  });
+  for (auto& S : E.slots)
+    if (S.state == 3 && !E.error) {
+      E.error = LA_ERANGE;
+      snprintf(E.err, sizeof(E.err), "slot %lld: no topology with feasible variants (n=%d)", (long long)S.id, S.n);
+    }
   if (E.error) {
     la::set_error("%s", E.err);
     return E.error;
@@ -825,11 +819,14 @@ int la_gen_negatives(void* h, int64_t* meta, double* pos, uint8_t* adj, int8_t* 
 // stats: out [21][2] simulated / accepted by joint count; *discarded
 int la_gen_stats(void* h, int64_t* out, int64_t* discarded) {
   Engine& E = *static_cast<Engine*>(h);
-  for (int n = 0; n <= LA_MAX_JOINTS; ++n) {
-    out[2 * n] = E.sim_by_n[n];
-    out[2 * n + 1] = E.acc_by_n[n];
+  for (int n = 0; n <= LA_MAX_JOINTS; ++n) out[2 * n] = out[2 * n + 1] = 0;
+  int64_t disc = 0;
+  for (auto& S : E.slots) {
+    out[2 * S.n] += S.sim;
+    out[2 * S.n + 1] += S.nacc;
+    disc += S.disc;
   }
-  *discarded = E.discarded;
+  *discarded = disc;
   return 0;
 }
 

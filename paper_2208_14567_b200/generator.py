@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -395,7 +396,8 @@ class GenerationRun:
         c = self.config
         return N.LaGenCfg(int(c.seed), int(c.n_min), int(c.n_max), float(c.ng_probability),
                           int(c.variants_per_topology), int(c.T_low), int(c.T_high), int(c.max_attempts),
-                          int(c.topology_retries), int(c.batch), float(c.negative_rate))
+                          int(c.topology_retries), int(c.batch), float(c.negative_rate),
+                          int(self.threads or len(os.sched_getaffinity(0))), 0)
 
     def _run_block(self, slot0: int, nslots: int):
         import os as _os

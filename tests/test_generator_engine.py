@@ -20,7 +20,7 @@ def _cfg(g, ci):
     rates = g[f"g{ci}_rates"]
     count, seed, n_min, n_max, vpt, T_low, T_high, max_att, batch, retries = (int(x) for x in cfg)
     return count, N.LaGenCfg(seed, n_min, n_max, float(rates[0]), vpt, T_low, T_high, max_att, retries, batch,
-                             float(rates[1]))
+                             float(rates[1]), 4, 0)  # 4 host threads: parallel flag walks
 
 
 def _oracle_gate(pos, cand_plan, plans, m, T_low, T_high):
