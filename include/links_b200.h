@@ -220,6 +220,21 @@ int la_sample_topologies(int64_t seed, int64_t g0, int64_t G, int32_t n_lo, int3
                          uint8_t* adj /* [G][20][20] or NULL */, int32_t* n_out);
 int la_sample_poses(int64_t seed, int64_t g0, int64_t G, int32_t per_group, const int32_t* n_of_group,
                     int32_t stride, int32_t threads, double* pos /* [G*per_group][stride][2] host */);
+/* Coarse prefilter (Atlas.coarse_filter, atlas.py:153-177).
+ * la_coarse_descriptors: paths [M][P][2] f64 -> desc [M][18] f64 = radial
+ *   histogram (16 bins over edges[0..16], host array = np.linspace(0, .75,
+ *   17), np.histogram semantics, / P) + bbox extent; bit-identical to
+ *   Atlas._descriptor (atlas.py:167-172).
+ * la_coarse_select: L1 distance to qdesc (device [18]) in numpy's summation
+ *   order, keeps the min(budget, M) smallest by (distance, index) and writes
+ *   them to out in scan order (order[] filtered; order NULL = identity);
+ *   optional dist_out [M].  Workspace from la_coarse_workspace(M).        */
+int la_coarse_descriptors(const double* paths, int64_t M, int32_t P, const double* edges /* host [17] */,
+                          double* desc, void* stream);
+size_t la_coarse_workspace(int64_t M);
+int la_coarse_select(const double* desc, int64_t M, const double* qdesc, int64_t budget, const int64_t* order,
+                     int64_t* out, double* dist_out, void* ws, size_t ws_bytes, void* stream);
+
 /* Dataset-generation engine (GenerationRun / _generate_slot /
  * find_valid_variant, generator.py:241-375): a caller-owned host object that
  * holds every slot's topology / pose / negative PCG64 streams and replays the

@@ -330,3 +330,27 @@ def topk_exhaustive(dists: np.ndarray, scan_pos: np.ndarray, k: int):
     ordering of test_atlas.py:106-118 / SURVEY.md §8a a-10."""
     key = np.lexsort((scan_pos, dists))
     return key[:k]
+
+
+# ---------------------------------------------------------------- coarse filter
+def coarse_descriptor(path: np.ndarray) -> np.ndarray:
+    """Radial-histogram + extent descriptor (atlas.py:167-172)."""
+    path = np.asarray(path, dtype=np.float64)
+    r = np.hypot(path[:, 0] - 0.5, path[:, 1] - 0.5)
+    hist, _ = np.histogram(r, bins=16, range=(0.0, 0.75))
+    hist = hist / max(len(r), 1)
+    extent = path.max(axis=0) - path.min(axis=0)
+    return np.concatenate([hist, extent])
+
+
+def coarse_filter(descriptors: np.ndarray, order: np.ndarray, qdesc: np.ndarray, budget: int) -> np.ndarray:
+    """Heuristic prefilter (atlas.py:153-166): the ``budget`` records with
+    the smallest descriptor L1 distance (stable argsort -> ties by index),
+    in scan order."""
+    if budget >= len(descriptors):
+        return order
+    dist = np.abs(descriptors - qdesc[None, :]).sum(axis=1)
+    keep = np.argsort(dist, kind="stable")[:budget]
+    mask = np.zeros(len(descriptors), dtype=bool)
+    mask[keep] = True
+    return order[mask[order]]

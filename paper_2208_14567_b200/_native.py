@@ -45,6 +45,9 @@ EXPORTS = (
     "la_sample_topologies",
     "la_sample_poses",
     "la_rng_draw",
+    "la_coarse_descriptors",
+    "la_coarse_workspace",
+    "la_coarse_select",
     "la_gen_create",
     "la_gen_destroy",
     "la_gen_window",
@@ -212,6 +215,10 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_sample_topologies.argtypes = [i64, i64, i64, i32, i32, C.c_double, i32, i32, vp, vp, vp, vp]
     lib.la_sample_poses.argtypes = [i64, i64, i64, i32, vp, i32, i32, vp]
     lib.la_rng_draw.argtypes = [vp, i32, i32, i64, i64, vp, vp]
+    lib.la_coarse_descriptors.argtypes = [vp, i64, i32, vp, vp, vp]
+    lib.la_coarse_workspace.argtypes = [i64]
+    lib.la_coarse_workspace.restype = sz
+    lib.la_coarse_select.argtypes = [vp, i64, vp, i64, vp, vp, vp, vp, sz, vp]
     lib.la_gen_create.argtypes = [C.POINTER(LaGenCfg), i64, i64]
     lib.la_gen_create.restype = vp
     lib.la_gen_destroy.argtypes = [vp]
@@ -232,7 +239,8 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_last_error.restype = C.c_char_p
     lib.la_device_sm_count.argtypes = []
     for name in EXPORTS:
-        if name not in ("la_last_error", "la_compact_workspace", "la_chamfer_workspace", "la_gen_create",
+        if name not in ("la_last_error", "la_compact_workspace", "la_chamfer_workspace", "la_coarse_workspace",
+                        "la_gen_create",
                         "la_gen_destroy", "la_gen_window", "la_gen_window_dev", "la_gen_count"):
             getattr(lib, name).restype = C.c_int
 

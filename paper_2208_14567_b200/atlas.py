@@ -118,6 +118,44 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     return out
 
 
+_EDGES = np.linspace(0.0, 0.75, 17)  # np.histogram(bins=16, range=(0, .75)) edges (atlas.py:169)
+
+
+def coarse_descriptors(paths) -> "torch.Tensor":
+    """Atlas._descriptor (atlas.py:167-172) for a (M, P, 2) float64 CUDA
+    tensor -> (M, 18) float64, bit-identical to the reference."""
+    torch = N.require_cuda()
+    lib = N.load()
+    if paths.dtype != torch.float64 or not paths.is_cuda or paths.dim() != 3 or paths.shape[2] != 2:
+        raise ValueError("paths must be a (M, P, 2) float64 CUDA tensor")
+    paths = paths.contiguous()
+    M, P, _ = paths.shape
+    desc = torch.empty((M, 18), dtype=torch.float64, device=paths.device)
+    N.check(lib.la_coarse_descriptors(paths.data_ptr(), M, P, _EDGES.ctypes.data, desc.data_ptr(), N.stream_ptr()),
+            "la_coarse_descriptors")
+    return desc
+
+
+def coarse_select(desc, qdesc, budget: int, order=None, *, return_dist: bool = False):
+    """Keep the ``budget`` records nearest ``qdesc`` in descriptor L1
+    distance, ties by index (stable argsort, atlas.py:162-166), returned in
+    scan order (``order`` filtered; identity when None).  Device int64."""
+    torch = N.require_cuda()
+    lib = N.load()
+    M = desc.shape[0]
+    k = int(min(max(budget, 0), M))
+    dev = desc.device
+    out = torch.empty(k, dtype=torch.int64, device=dev)
+    dist = torch.empty(M, dtype=torch.float64, device=dev) if return_dist else None
+    if order is not None:
+        order = order.to(device=dev, dtype=torch.int64).contiguous()
+    ws = torch.empty(max(int(lib.la_coarse_workspace(M)), 1), dtype=torch.uint8, device=dev)
+    q = qdesc.to(device=dev, dtype=torch.float64).contiguous().reshape(18)
+    N.check(lib.la_coarse_select(desc.contiguous().data_ptr(), M, q.data_ptr(), k, N.ptr(order), out.data_ptr(),
+                                 N.ptr(dist), ws.data_ptr(), ws.numel(), N.stream_ptr()), "la_coarse_select")
+    return (out, dist) if return_dist else out
+
+
 def assemble_hits(hit_d, hit_id, top_d, top_id, k, threshold, self_idx=None):
     """Host assembly of the retrieve() result from the device lists.
 
@@ -174,6 +212,7 @@ class Atlas:
         self._hash_order = np.argsort(h, kind="stable")
         self._hash_sorted = h[self._hash_order]
         self._dev = None
+        self._order_dev = None
 
     def __len__(self) -> int:
         return len(self.points)
@@ -231,26 +270,38 @@ class Atlas:
                 found = idx
         return found
 
-    # -- coarse prefilter (atlas.py:153-177; host, off the hot path) -------
+    # -- coarse prefilter (atlas.py:153-177) on the device -----------------
+    def device_descriptors(self, chunk: int = 1 << 18):
+        """(N, 18) f64 descriptors, computed once from the f64 curves."""
+        torch = N.require_cuda()
+        if self._descriptors is None:
+            desc = torch.empty((len(self), 18), dtype=torch.float64, device="cuda")
+            for c0 in range(0, len(self), chunk):
+                c1 = min(len(self), c0 + chunk)
+                desc[c0:c1] = coarse_descriptors(torch.from_numpy(self.points[c0:c1]).cuda())
+            self._descriptors = desc
+        return self._descriptors
+
+    def device_order(self):
+        torch = N.require_cuda()
+        if self._order_dev is None:
+            self._order_dev = torch.from_numpy(np.ascontiguousarray(self.order, dtype=np.int64)).cuda()
+        return self._order_dev
+
+    def _coarse_scan(self, query: np.ndarray, budget: int, mode: str):
+        """Device scan list (int64 tensor) of coarse_filter."""
+        torch = N.require_cuda()
+        if mode == "exact" or budget >= len(self):
+            return self.device_order()
+        q = np.ascontiguousarray(np.asarray(query, dtype=np.float64))
+        qd = coarse_descriptors(torch.from_numpy(q[None]).cuda())[0]
+        return coarse_select(self.device_descriptors(), qd, int(budget), self.device_order())
+
     def coarse_filter(self, query: np.ndarray, budget: int, mode: str = "heuristic") -> np.ndarray:
+        """Candidate record indices in scan order (atlas.py:153-164)."""
         if mode == "exact" or budget >= len(self):
             return self.order
-        if self._descriptors is None:
-            self._descriptors = np.stack([self._descriptor(p) for p in self.points])
-        qd = self._descriptor(query)
-        dist = np.abs(self._descriptors - qd[None, :]).sum(axis=1)
-        keep = np.argsort(dist, kind="stable")[:budget]
-        mask = np.zeros(len(self), dtype=bool)
-        mask[keep] = True
-        return self.order[mask[self.order]]
-
-    @staticmethod
-    def _descriptor(path: np.ndarray) -> np.ndarray:
-        r = np.hypot(path[:, 0] - 0.5, path[:, 1] - 0.5)
-        hist, _ = np.histogram(r, bins=16, range=(0.0, 0.75))
-        hist = hist / max(len(r), 1)
-        extent = path.max(axis=0) - path.min(axis=0)
-        return np.concatenate([hist, extent])
+        return self._coarse_scan(query, budget, mode).cpu().numpy()
 
     # -- search ----------------------------------------------------------
     def retrieve(self, query: np.ndarray, k: int = DEFAULT_K, threshold: float = DEFAULT_THRESHOLD,
@@ -263,15 +314,14 @@ class Atlas:
         query = np.asarray(query, dtype=np.float64)
         if not is_normalized(query):
             query = normalize(query)
-        scan = self.order if budget is None else self.coarse_filter(query, budget, filter_mode)
+        scan = self.device_order() if budget is None else self._coarse_scan(query, budget, filter_mode)
         self_idx = self.exact_index(query)
         if not (1 <= k <= N.LA_MAX_TOPK):
-            return self._retrieve_large(query, k, threshold, scan, self_idx)
+            return self._retrieve_large(query, k, threshold, scan.cpu().numpy(), self_idx)
         db = self.device_points()
         res = chamfer_scan(db, torch.from_numpy(query.astype(np.float32)).cuda()[None],
-                           k=int(k), threshold=threshold,
-                           order=torch.from_numpy(np.ascontiguousarray(scan, dtype=np.int64)).cuda(),
-                           pos_end=len(scan), exclude_id=-1 if self_idx is None else int(self_idx))
+                           k=int(k), threshold=threshold, order=scan,
+                           pos_end=int(scan.numel()), exclude_id=-1 if self_idx is None else int(self_idx))
         host = {n: res[n][0].cpu().numpy() for n in ("hit_d", "hit_id", "top_d", "top_id")}
         rows = assemble_hits(host["hit_d"], host["hit_id"], host["top_d"], host["top_id"], int(k), threshold,
                              self_idx)

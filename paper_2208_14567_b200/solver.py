@@ -382,7 +382,7 @@ def plan_geometry(plan: SolutionPlan, positions0: np.ndarray):
         e = np.zeros(0)
         return e, e.copy(), e.copy()
     table = PlanTable([plan])
-    dpos = torch.from_numpy(pos.reshape(1, -1, 2)).cuda()
+    dpos = torch.from_numpy(np.array(pos, dtype=np.float64).reshape(1, -1, 2)).cuda()
     outs = [torch.empty((1, N.LA_MAX_STEPS), dtype=torch.float64, device=dpos.device) for _ in range(3)]
     N.check(lib.la_plan_geometry(dpos.data_ptr(), None, table.tensor().data_ptr(), 1, 1, pos.shape[0],
                                  outs[0].data_ptr(), outs[1].data_ptr(), outs[2].data_ptr(),

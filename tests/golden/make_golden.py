@@ -270,6 +270,26 @@ def atlas_fixture():
     full = atlas.retrieve(queries[1], k=N, threshold=np.inf)
     d["brute_ids"] = np.array([h.mech_id for h in full])
     d["brute_d"] = np.array([h.distance for h in full])
+    # coarse prefilter (atlas.py:153-177): descriptors, filtered scan lists
+    # and budgeted heuristic retrievals, on an atlas with duplicated curves
+    # (tied descriptor distances) next to the plain one
+    d["descriptors"] = atlas._build_descriptors()
+    dup = np.concatenate([pts[:150], pts[:60], pts[100:130], pts[:60]])
+    recs2 = [CurveRecord(mech_id=i, joint_id=3, is_arc=False, is_circle=False, points=p.tolist())
+             for i, p in enumerate(dup)]
+    atlas2 = ref_atlas.Atlas.build(recs2, {i: mech for i in range(len(dup))}, seed=11)
+    d["dup_points"] = dup
+    d["dup_order"] = atlas2.order
+    d["dup_descriptors"] = atlas2._build_descriptors()
+    budgets = [1, 7, 50, 61, 200]
+    d["coarse_budgets"] = np.array(budgets)
+    for qi, q in enumerate(queries + [pts[5].copy()]):
+        d[f"coarse_q{qi}"] = q
+        for bi, b in enumerate(budgets):
+            d[f"coarse_{qi}_{bi}"] = atlas.coarse_filter(q, b)
+            d[f"coarse_dup_{qi}_{bi}"] = atlas2.coarse_filter(q, b)
+        hits = atlas2.retrieve(q, k=5, threshold=0.05, budget=61, filter_mode="heuristic")
+        d[f"coarse_hits_{qi}"] = np.array([(h.mech_id, h.distance, float(h.above_threshold)) for h in hits])
     np.savez_compressed(OUT / "atlas_golden.npz", **d)
 
 

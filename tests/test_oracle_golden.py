@@ -117,3 +117,20 @@ def test_atlas_scan_matches_reference(golden):
             assert [float(r[2]) for r in got] == want[:, 5].tolist()
     full = O.retrieve(pts, order, g["query1"], len(pts), np.inf)
     assert [r[1] for r in full] == g["brute_ids"].tolist()
+
+
+def test_oracle_coarse_filter_pinned(golden):
+    """Descriptors and heuristic scan lists equal the reference's, including
+    an atlas with duplicated curves (tied descriptor distances)."""
+    g = golden("atlas_golden.npz")
+    desc = np.stack([O.coarse_descriptor(p) for p in g["points"]])
+    assert np.array_equal(desc, g["descriptors"])
+    ddesc = np.stack([O.coarse_descriptor(p) for p in g["dup_points"]])
+    assert np.array_equal(ddesc, g["dup_descriptors"])
+    budgets = g["coarse_budgets"]
+    for qi in range(5):
+        q = g[f"coarse_q{qi}"]
+        qd = O.coarse_descriptor(q)
+        for bi, b in enumerate(budgets):
+            assert np.array_equal(O.coarse_filter(desc, g["order"], qd, int(b)), g[f"coarse_{qi}_{bi}"])
+            assert np.array_equal(O.coarse_filter(ddesc, g["dup_order"], qd, int(b)), g[f"coarse_dup_{qi}_{bi}"])
