@@ -62,6 +62,12 @@ typedef struct la_plan {
 #define LA_SIM_WRITE_ONLY 128u     /* no screening: all T angles in f64 in
                                       natural order, exact first lock, paths
                                       written (needs LA_SIM_WRITE_TRAJ)       */
+#define LA_SIM_EXACT64 256u        /* f64 rounds (writes, fix-up replays,
+                                      LA_SIM_FP64) in numpy's operation order
+                                      with IEEE ops + glibc hypot: paths and
+                                      flags bit-identical to simulate_batch.
+                                      Without it the f64 rounds use DFMA and
+                                      Newton rsqrt (a few ulp; ~2x faster)   */
 #define LA_PENDING (-3)            /* first_t of a deferred coarse survivor    */
 
 /* Batched replay of compiled plans over (candidate x crank angle).
@@ -234,6 +240,13 @@ int la_coarse_descriptors(const double* paths, int64_t M, int32_t P, const doubl
 size_t la_coarse_workspace(int64_t M);
 int la_coarse_select(const double* desc, int64_t M, const double* qdesc, int64_t budget, const int64_t* order,
                      int64_t* out, double* dist_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Curation keep rule (curation_keep, curves.py:104-110) for a batch of
+ * curve records on the device: keep[i] = !flagged[i] ||
+ * default_rng([seed, mech_ids[i], joint_ids[i]]).random() < keep_rate
+ * (ids >= 0).                                                            */
+int la_curation_keep(const int64_t* mech_ids, const int64_t* joint_ids, const uint8_t* flagged, int64_t n,
+                     int64_t seed, double keep_rate, uint8_t* keep, void* stream);
 
 /* Dataset-generation engine (GenerationRun / _generate_slot /
  * find_valid_variant, generator.py:241-375): a caller-owned host object that

@@ -354,3 +354,10 @@ def coarse_filter(descriptors: np.ndarray, order: np.ndarray, qdesc: np.ndarray,
     mask = np.zeros(len(descriptors), dtype=bool)
     mask[keep] = True
     return order[mask[order]]
+
+
+def curation_keep(mech_id: int, joint_id: int, flagged: bool, keep_rate: float, seed: int) -> bool:
+    """Record-keyed keep rule (curves.py:104-110)."""
+    if not flagged:
+        return True
+    return bool(np.random.default_rng([seed, mech_id, joint_id]).random() < keep_rate)

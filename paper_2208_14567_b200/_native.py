@@ -27,6 +27,7 @@ LA_SIM_TRAJ_F64 = 16
 LA_SIM_DEFER = 32
 LA_SIM_SCATTER = 64
 LA_SIM_WRITE_ONLY = 128
+LA_SIM_EXACT64 = 256
 LA_PENDING = -3
 
 LA_CH_EXPANSION = 1
@@ -48,6 +49,7 @@ EXPORTS = (
     "la_coarse_descriptors",
     "la_coarse_workspace",
     "la_coarse_select",
+    "la_curation_keep",
     "la_gen_create",
     "la_gen_destroy",
     "la_gen_window",
@@ -219,6 +221,7 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_coarse_workspace.argtypes = [i64]
     lib.la_coarse_workspace.restype = sz
     lib.la_coarse_select.argtypes = [vp, i64, vp, i64, vp, vp, vp, vp, sz, vp]
+    lib.la_curation_keep.argtypes = [vp, vp, vp, i64, i64, C.c_double, vp, vp]
     lib.la_gen_create.argtypes = [C.POINTER(LaGenCfg), i64, i64]
     lib.la_gen_create.restype = vp
     lib.la_gen_destroy.argtypes = [vp]

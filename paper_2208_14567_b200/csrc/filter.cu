@@ -29,30 +29,6 @@ struct Edges {
   double e[NBINS + 1];
 };
 
-// glibc's hypot for finite binary64 (Borges' corrected sqrt, non-FMA
-// kernel), the function numpy.hypot calls; explicit round-to-nearest ops so
-// nothing is contracted.  Bit-identical to np.hypot (checked on 2e7 pairs,
-// tests/test_gpu_filter.py).
-__device__ __forceinline__ double np_hypot(double x, double y) {
-  x = fabs(x);
-  y = fabs(y);
-  const double ax = x < y ? y : x;
-  const double ay = x < y ? x : y;
-  if (ay <= __dmul_rn(ax, 0x1p-54)) return __dadd_rn(ax, ay);
-  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
-  double t1, t2;
-  if (h <= __dmul_rn(2.0, ay)) {
-    const double d = __dsub_rn(h, ay);
-    t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, d), ax));
-    t2 = __dmul_rn(__dsub_rn(d, __dmul_rn(2.0, __dsub_rn(ax, ay))), d);
-  } else {
-    const double d = __dsub_rn(h, ax);
-    t1 = __dmul_rn(__dmul_rn(2.0, d), __dsub_rn(ax, __dmul_rn(2.0, ay)));
-    t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, d), ay), ay), __dmul_rn(d, d));
-  }
-  return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
-}
-
 // warp per curve
 __global__ void __launch_bounds__(256) descriptor_kernel(const double* __restrict__ paths, long long M, int P,
                                                           Edges ed, double* __restrict__ desc) {

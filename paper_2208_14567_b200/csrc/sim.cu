@@ -58,7 +58,7 @@ struct __align__(16) StepRec64 {
   double hi;             // (ra + rb) + LOCK_EPS   (solver.py:213, same rounding)
   double lo;             // |ra - rb| - LOCK_EPS
   double ra2;            // ra * ra
-  double c2;             // ra * ra - rb * rb
+  double rb2;            // rb * rb
 };
 
 struct __align__(16) WarpHead {
@@ -84,6 +84,7 @@ struct Warp {
 
 struct SimCtx {
   int n, ns;
+  bool exact;  // LA_SIM_EXACT64
   double r1;
   float tau;
   float r1f;
@@ -115,14 +116,19 @@ __device__ __forceinline__ double rsqrt_f64(double x) {
   return y;
 }
 
-// f64 dyad replay of one angle (solver.py:205-231): the lock test
-// d < eps | d > (ra+rb)+eps | d < |ra-rb|-eps with LOCK_EPS = 1e-9
-// (solver.py:19, 213) on the same f64 bounds, then
-// x = (d*d + ra*ra - rb*rb) / (2d), h = sqrt(max(ra*ra - x*x, 0)),
-// p = p_a + x*u - branch*h*u_perp.  The arithmetic is contracted (DFMA) and
-// d, 1/d, h come from Newton-refined reciprocal square roots instead of
-// np.hypot / IEEE division / sqrt: results differ from numpy's by a few ulp
-// (the parity tests hold f64 trajectories to 1e-12 of the reference).
+// f64 dyad replay of one angle (solver.py:205-231).
+//
+// Exact mode (LA_SIM_EXACT64): numpy's operation order with IEEE
+// round-to-nearest operations only (no contraction):
+//   d = hypot(dx, dy)                          (glibc algorithm, np_hypot)
+//   lock: d < eps | d > (ra+rb)+eps | d < |ra-rb|-eps   (LOCK_EPS 1e-9)
+//   x = ((d*d + ra*ra) - rb*rb) / (2*d);  h = sqrt(max(ra*ra - x*x, 0))
+//   ux = dx/d, uy = dy/d
+//   p = ((pa.x + x*ux) - (br*h)*uy,  (pa.y + x*uy) + (br*h)*ux)
+// so positions and lock decisions are bit-identical to simulate_batch.
+// Fast mode: the same formulas contracted to DFMA with d, 1/d and h from
+// Newton-refined MUFU reciprocal square roots (a few ulp from numpy; the
+// lock decision can differ only for margins within ~1e-15).
 template <typename Get, typename Put>
 __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get get, Put put) {
   const double eps = 1e-9;
@@ -134,22 +140,34 @@ __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get
     const double br = __hiloint2double((int)w0.w, (int)w0.z);
     const double2 pa = get(a), pb = get(b);
     const double2 hl = *reinterpret_cast<const double2*>(&g.hi);
-    const double2 rc = *reinterpret_cast<const double2*>(&g.ra2);
-    const double dx = pb.x - pa.x;
-    const double dy = pb.y - pa.y;
-    const double d2 = fma(dy, dy, dx * dx);
-    const double inv = rsqrt_f64(d2);
-    const double d = d2 * inv;
-    const bool lock = !(d >= eps) | (d > hl.x) | (d < hl.y);
-    if (lock) return s;
-    const double x = fma(d, d, rc.y) * (0.5 * inv);
-    const double h2 = fma(-x, x, rc.x);
-    const double h2c = fmax(h2, 1e-300);
-    const double hh = h2c * rsqrt_f64(h2c);
-    const double h = h2 > 0.0 ? hh : 0.0;
-    const double xi = x * inv;
-    const double hb = br * h * inv;
-    put(t, make_double2(fma(-hb, dy, fma(xi, dx, pa.x)), fma(hb, dx, fma(xi, dy, pa.y))));
+    const double2 rr = *reinterpret_cast<const double2*>(&g.ra2);
+    const double dx = dsub(pb.x, pa.x);
+    const double dy = dsub(pb.y, pa.y);
+    if (C.exact) {
+      const double d = np_hypot(dx, dy);
+      const bool lock = !(d >= eps) | (d > hl.x) | (d < hl.y);
+      if (lock) return s;
+      const double x = __ddiv_rn(dsub(dadd(dmul(d, d), rr.x), rr.y), dmul(2.0, d));
+      const double h = __dsqrt_rn(fmax(dsub(rr.x, dmul(x, x)), 0.0));
+      const double ux = __ddiv_rn(dx, d), uy = __ddiv_rn(dy, d);
+      const double bh = dmul(br, h);
+      put(t, make_double2(dsub(dadd(pa.x, dmul(x, ux)), dmul(bh, uy)),
+                          dadd(dadd(pa.y, dmul(x, uy)), dmul(bh, ux))));
+    } else {
+      const double d2 = fma(dy, dy, dx * dx);
+      const double inv = rsqrt_f64(d2);
+      const double d = d2 * inv;
+      const bool lock = !(d >= eps) | (d > hl.x) | (d < hl.y);
+      if (lock) return s;
+      const double x = fma(d, d, rr.x - rr.y) * (0.5 * inv);
+      const double h2 = fma(-x, x, rr.x);
+      const double h2c = fmax(h2, 1e-300);
+      const double hh = h2c * rsqrt_f64(h2c);
+      const double h = h2 > 0.0 ? hh : 0.0;
+      const double xi = x * inv;
+      const double hb = br * h * inv;
+      put(t, make_double2(fma(-hb, dy, fma(xi, dx, pa.x)), fma(hb, dx, fma(xi, dy, pa.y))));
+    }
   }
   return -1;
 }
@@ -326,6 +344,7 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
     C.n = pl->n;
     C.ns = pl->nsteps;
     C.tau = p.fixup_tau;
+    C.exact = (p.flags & LA_SIM_EXACT64) != 0;
     const uint32_t fixed = pl->fixed_mask | 1u;  // joint 0 is static (solver.py:183)
     if (C.n > njmax || C.n < 2 || C.ns > NS || C.ns < 0) {
       // plan does not fit the launch (n > pos_stride): flag, do not touch smem
@@ -358,11 +377,8 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
       const double2 pa = H.p0[ia_], pb = H.p0[ib_], pt = H.p0[it_];
       const double ax = dsub(pt.x, pa.x), ay = dsub(pt.y, pa.y);
       const double bx = dsub(pt.x, pb.x), by = dsub(pt.y, pb.y);
-      // np.hypot in the reference; a Newton-refined sqrt of the sum agrees
-      // to an ulp or two
-      const double a2 = dadd(dmul(ax, ax), dmul(ay, ay)), b2 = dadd(dmul(bx, bx), dmul(by, by));
-      const double ra = a2 > 0.0 ? dmul(a2, rsqrt_f64(a2)) : 0.0;
-      const double rb = b2 > 0.0 ? dmul(b2, rsqrt_f64(b2)) : 0.0;
+      // np.hypot, bit for bit (glibc algorithm, common.cuh)
+      const double ra = np_hypot(ax, ay), rb = np_hypot(bx, by);
       const double cross = dsub(dmul(dsub(pb.x, pa.x), dsub(pt.y, pa.y)),
                                 dmul(dsub(pb.y, pa.y), dsub(pt.x, pa.x)));
       const double br = cross >= 0.0 ? 1.0 : -1.0;
@@ -372,7 +388,7 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
       r64.hi = dadd(dadd(ra, rb), 1e-9);
       r64.lo = dsub(fabs(dsub(ra, rb)), 1e-9);
       r64.ra2 = dmul(ra, ra);
-      r64.c2 = dsub(dmul(ra, ra), dmul(rb, rb));
+      r64.rb2 = dmul(rb, rb);
       r64.br = br;
       H.st64[lane] = r64;
       StepRec r;
@@ -388,8 +404,7 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
     }
     {
       const double dx = dsub(H.p0[1].x, H.p0[0].x), dy = dsub(H.p0[1].y, H.p0[0].y);
-      const double r2 = dadd(dmul(dx, dx), dmul(dy, dy));
-      C.r1 = r2 > 0.0 ? dmul(r2, rsqrt_f64(r2)) : 0.0;
+      C.r1 = np_hypot(dx, dy);  // solver.py:180
       C.r1f = (float)C.r1;
       C.p0f = make_float2((float)H.p0[0].x, (float)H.p0[0].y);
     }
@@ -543,8 +558,8 @@ __global__ void geometry_kernel(const double* __restrict__ pos0, const int32_t* 
     const int t = pl->step[s][0], a = pl->step[s][1], c = pl->step[s][2];
     const double ax = P[2 * a], ay = P[2 * a + 1], bx = P[2 * c], by = P[2 * c + 1];
     const double tx = P[2 * t], ty = P[2 * t + 1];
-    ra = hypot(dsub(tx, ax), dsub(ty, ay));
-    rb = hypot(dsub(tx, bx), dsub(ty, by));
+    ra = np_hypot(dsub(tx, ax), dsub(ty, ay));
+    rb = np_hypot(dsub(tx, bx), dsub(ty, by));
     const double cross = dsub(dmul(dsub(bx, ax), dsub(ty, ay)), dmul(dsub(by, ay), dsub(tx, ax)));
     br = cross >= 0.0 ? 1.0 : -1.0;
   }
@@ -560,7 +575,7 @@ __global__ void dyad_kernel(const double* __restrict__ pa, const double* __restr
   if (i >= n) return;
   const double dx = dsub(pb[2 * i], pa[2 * i]);
   const double dy = dsub(pb[2 * i + 1], pa[2 * i + 1]);
-  const double d = hypot(dx, dy);
+  const double d = np_hypot(dx, dy);
   const double ra = ra_[i], rb = rb_[i];
   const double eps = 1e-9;
   if (d < eps || d > dadd(dadd(ra, rb), eps) || d < dsub(fabs(dsub(ra, rb)), eps)) {

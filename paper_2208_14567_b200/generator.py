@@ -276,12 +276,12 @@ def find_valid_variant(topology: Mechanism, plan: SolutionPlan, rng: np.random.G
         cand = np.concatenate(chunks)
         dpos = torch.from_numpy(cand).cuda()
         if fused:
-            res = simulate_tensors(dpos, table, T_high, write_traj=False, low=True)
+            res = simulate_tensors(dpos, table, T_high, write_traj=False, low=True, exact=True)
             low_t = res["low_t"].cpu().numpy()
             high_ok = res["first_t"].cpu().numpy() == T_high
         else:
-            lo = simulate_tensors(dpos, table, T_low, write_traj=False)
-            hi = simulate_tensors(dpos, table, T_high, write_traj=False)
+            lo = simulate_tensors(dpos, table, T_low, write_traj=False, exact=True)
+            hi = simulate_tensors(dpos, table, T_high, write_traj=False, exact=True)
             ft = lo["first_t"].cpu().numpy()
             low_t = np.where(ft < T_low, ft, -1)
             high_ok = hi["first_t"].cpu().numpy() == T_high
@@ -456,12 +456,13 @@ class GenerationRun:
                     pd.copy_(pos_h[:m, :stride], non_blocking=True)
                     topo.copy_(plan_h[:m], non_blocking=True)
                 if fused:
-                    res = simulate_tensors(pd, table, c.T_high, topo, write_traj=False, low=True, gate_only=True)
+                    res = simulate_tensors(pd, table, c.T_high, topo, write_traj=False, low=True, gate_only=True,
+                                           exact=True)
                     flags_h[0, :m].copy_(res["first_t"], non_blocking=True)
                     flags_h[1, :m].copy_(res["low_t"], non_blocking=True)
                 else:
-                    lo = simulate_tensors(pd, table, c.T_low, topo, write_traj=False)
-                    hi = simulate_tensors(pd, table, c.T_high, topo, write_traj=False)
+                    lo = simulate_tensors(pd, table, c.T_low, topo, write_traj=False, exact=True)
+                    hi = simulate_tensors(pd, table, c.T_high, topo, write_traj=False, exact=True)
                     flags_h[0, :m].copy_(hi["first_t"], non_blocking=True)
                     ft = lo["first_t"]
                     flags_h[1, :m].copy_(torch.where(ft < c.T_low, ft, torch.full_like(ft, -1)), non_blocking=True)

@@ -207,7 +207,8 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
                      traj=None, traj_stride: int | None = None, traj_row=None, low: bool = False,
                      traj_f64: bool = False, cand=None, cand_count=None,
                      fixup_tau: float = DEFAULT_FIXUP_TAU, fp64: bool = False, gate_only: bool = False,
-                     coarse: bool = True, counters=None, stream=None, _extra_flags: int = 0,
+                     coarse: bool = True, counters=None, stream=None, exact: bool | None = None,
+                     _extra_flags: int = 0,
                      _outputs=None) -> dict:
     """Launch la_simulate on device tensors.
 
@@ -217,7 +218,10 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
     float32 — float64 with ``traj_f64`` — when written) and ``low_t`` /
     ``low_joint`` when ``low``.  ``cand`` (int64 device indices, optional
     device count ``cand_count``) gathers the work items; outputs are then
-    indexed by work item.
+    indexed by work item.  ``exact`` (default: on for f64 paths or the
+    all-f64 mode) runs the f64 rounds in numpy's operation order with IEEE
+    operations (LA_SIM_EXACT64): f64 paths and the lock decisions of replayed
+    lanes are then bit-identical to the reference.
     """
     torch = N.require_cuda()
     lib = N.load()
@@ -266,6 +270,8 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
         flags |= N.LA_SIM_NO_COARSE
     if traj_f64:
         flags |= N.LA_SIM_TRAJ_F64
+    if exact if exact is not None else (traj_f64 or fp64):
+        flags |= N.LA_SIM_EXACT64
     flags |= int(_extra_flags)
     a = N.LaSimArgs()
     a.pos0 = pos0.data_ptr()
@@ -360,7 +366,8 @@ def simulate_compact(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=No
     torch = N.require_cuda()
     B, S, _ = pos0.shape
     stride = table.max_n
-    res = simulate_tensors(pos0, table, T, topo, write_traj=False, fixup_tau=fixup_tau, stream=stream)
+    res = simulate_tensors(pos0, table, T, topo, write_traj=False, fixup_tau=fixup_tau, stream=stream,
+                           exact=traj_f64)
     idx, cnt = compact_valid(res["first_t"], T, stream=stream)
     if traj is None:
         traj = torch.empty((max(B, 1) * stride, T, 2), dtype=torch.float64 if traj_f64 else torch.float32,
@@ -464,10 +471,10 @@ def check_feasible(mech: Mechanism, plan: SolutionPlan, T_low: int = 50, T_high:
     if T_high == 4 * T_low:
         # the T_low angles are every 4th T_high angle (bit-identical thetas):
         # one coarse-first launch answers both sweeps
-        res = simulate_tensors(dpos, table, T_high, write_traj=False, low=True)
+        res = simulate_tensors(dpos, table, T_high, write_traj=False, low=True, exact=True)
         return bool(int(res["low_t"].item()) < 0 and int(res["first_t"].item()) == T_high)
-    lo = simulate_tensors(dpos, table, T_low, write_traj=False)
+    lo = simulate_tensors(dpos, table, T_low, write_traj=False, exact=True)
     if int(lo["first_t"].item()) < T_low:
         return False
-    hi = simulate_tensors(dpos, table, T_high, write_traj=False)
+    hi = simulate_tensors(dpos, table, T_high, write_traj=False, exact=True)
     return int(hi["first_t"].item()) == T_high

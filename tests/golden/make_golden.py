@@ -330,10 +330,58 @@ def generator_fixture():
     np.savez_compressed(OUT / "generator_golden.npz", **d)
 
 
+def dataset_fixture():
+    """generate -> normalize -> curate chain of the CLI (cli.py:56-172):
+    curve records of every moving joint, the keep rule, and the exact bytes
+    of the reference's .ldjson writer for the kept curves and mechanisms."""
+    import tempfile
+
+    from linkatlas import records as ref_rec
+
+    d = {"versions": versions()}
+    cfg = ref_gen.GenerationConfig(count=24, seed=3, n_min=6, n_max=10, variants_per_topology=2, max_attempts=2000)
+    recs = list(ref_gen.GenerationRun(cfg).records())
+    curves, mrecs = [], []
+    for rec in recs:
+        mid = rec.slot * cfg.variants_per_topology + rec.variant
+        mech = rec.mechanism
+        mrecs.append(ref_rec.mechanism_to_record(mech, mid))
+        for j in range(mech.n):
+            if mech.types[j] == JointType.FIXED:
+                continue
+            pts = ref_curves.normalize(rec.trajectory.positions[j])
+            curves.append(ref_rec.CurveRecord(mech_id=mid, joint_id=j, is_arc=ref_curves.is_arc(mech, j),
+                                              is_circle=ref_curves.is_circle(pts), points=pts.tolist()))
+    keep_rate, seed = 0.3, 4
+    kept = list(ref_curves.curate(curves, keep_rate=keep_rate, seed=seed))
+    d["cfg"] = np.array([cfg.count, cfg.seed, cfg.n_min, cfg.n_max, cfg.variants_per_topology, cfg.max_attempts])
+    d["curate"] = np.array([keep_rate, seed])
+    d["mech_ids"] = np.array([c.mech_id for c in curves])
+    d["joint_ids"] = np.array([c.joint_id for c in curves])
+    d["is_arc"] = np.array([c.is_arc for c in curves])
+    d["is_circle"] = np.array([c.is_circle for c in curves])
+    d["points"] = np.array([c.points for c in curves])
+    d["kept"] = np.array([any(c is k for k in kept) for c in curves])
+    with tempfile.TemporaryDirectory() as tmp:
+        ref_rec.write_records(Path(tmp) / "c.ldjson", "curve", kept)
+        ref_rec.write_records(Path(tmp) / "m.ldjson", "mechanism", mrecs)
+        d["curves_ldjson"] = np.frombuffer((Path(tmp) / "c.ldjson").read_bytes(), dtype=np.uint8)
+        d["mechs_ldjson"] = np.frombuffer((Path(tmp) / "m.ldjson").read_bytes(), dtype=np.uint8)
+    # keep rule on wide ids (multi-word SeedSequence entropy)
+    rng = np.random.default_rng(8)
+    mids = np.concatenate([rng.integers(0, 2**31, 1000), rng.integers(2**32, 2**45, 1000), [0, 1, 2**32 - 1, 2**32]])
+    jids = rng.integers(0, 20, len(mids))
+    d["rule_mech"] = mids
+    d["rule_joint"] = jids
+    d["rule_keep"] = np.array([ref_curves.curation_keep(int(m), int(j), True, 0.5, 77) for m, j in zip(mids, jids)])
+    np.savez_compressed(OUT / "dataset_golden.npz", **d)
+
+
 if __name__ == "__main__":
     sol = solver_fixture()
     curves_fixture(sol)
     atlas_fixture()
     generator_fixture()
+    dataset_fixture()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

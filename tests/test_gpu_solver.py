@@ -411,3 +411,36 @@ def test_deferred_pipeline_matches_single_pass(torch):
         assert torch.equal(a[i, :n], b[i, :n])
     nv = int(res["valid_count"].item())
     assert torch.equal(res["valid_idx"][:nv], (ref["first_t"] == 200).nonzero().flatten())
+
+
+def test_bit_exact_f64_replay(torch, golden):
+    """The f64 rounds follow numpy's operation order with IEEE ops and
+    glibc's hypot: f64 paths are bit-identical to the reference, fp32 paths
+    are the reference's values rounded once, and every lock flag (margin
+    band included: those lanes are decided by the f64 replay) is exact."""
+    from paper_2208_14567_b200.solver import SolutionPlan, compile_order
+    from paper_2208_14567_b200.workloads import bare_plan, four_bar
+
+    g = golden("solver_golden.npz")
+    plan = bare_plan(four_bar())
+    r64 = run_mixed(torch, [plan], g["fb_pos0"], None, 200, traj_f64=True)
+    t64 = r64["traj"].view(-1, 4, 200, 2).cpu().numpy()
+    assert np.array_equal(t64[g["fb_traj_idx"]], g["fb_traj"])
+    assert np.array_equal(r64["first_t"].cpu().numpy(), g["fb_first_t"])
+    assert np.array_equal(r64["first_joint"].cpu().numpy(), g["fb_first_joint"])
+    plans = []
+    for t in range(len(g["mx_n"])):
+        n = int(g["mx_n"][t])
+        fixed, steps = compile_order(g["mx_adj"][t][:n, :n], g["mx_types"][t][:n])
+        plans.append(SolutionPlan(n, fixed, steps, None, None, None))
+    for kw in ({}, {"fp64": True}):
+        r32 = run_mixed(torch, plans, g["mx_pos0"], g["mx_topo"], 200, **kw)
+        assert np.array_equal(r32["first_t"].cpu().numpy(), g["mx_first_t"])
+        assert np.array_equal(r32["first_joint"].cpu().numpy(), g["mx_first_joint"])
+        t32 = r32["traj"].view(-1, 20, 200, 2).cpu().numpy()
+        r64 = run_mixed(torch, plans, g["mx_pos0"], g["mx_topo"], 200, traj_f64=True, **kw)
+        t64 = r64["traj"].view(-1, 20, 200, 2).cpu().numpy()
+        for gi, tp in zip(g["mx_traj_idx"], g["mx_traj"]):
+            n = int(g["mx_n"][g["mx_topo"][gi]])
+            assert np.array_equal(t64[gi, :n], tp[:n])
+            assert np.array_equal(t32[gi, :n], tp[:n].astype(np.float32))
