@@ -135,3 +135,18 @@ def test_normalize_degenerate_batch_status(torch):
     paths[1] = np.random.default_rng(0).uniform(size=(10, 2))
     res = normalize_tensors(torch.from_numpy(paths).cuda())
     assert res["status"].tolist() == [1, 0, 1]
+
+
+def test_normalize_f64_bit_exact(torch, golden):
+    """f64 la_normalize reproduces curves.normalize bit for bit (cdist
+    without contraction, OpenBLAS's FMA order for the rotation, IEEE
+    division) and np.var for is_circle (pairwise summation order)."""
+    from paper_2208_14567_b200.curves import normalize_tensors
+
+    g = golden("curves_golden.npz")
+    res = normalize_tensors(torch.from_numpy(g["paths"]).cuda(), out_f64=True)
+    out = res["out"].cpu().numpy()
+    same = [np.array_equal(o, w) for o, w in zip(out, g["normalized"])]
+    assert all(same), f"{len(same) - sum(same)} of {len(same)} curves differ"
+    assert np.array_equal(res["circle_var"].cpu().numpy(), g["circle_var"])
+    assert np.array_equal(res["is_circle"].cpu().numpy().astype(bool), g["is_circle"])

@@ -54,6 +54,12 @@ def test_pipeline_matches_reference_cli_chain(torch, golden, tmp_path):
     k = g["kept"]
     assert np.array_equal(kept.mech_ids, g["mech_ids"][k])
     assert np.array_equal(kept.joint_ids, g["joint_ids"][k])
+    # exact chain: the written file is byte-identical to the reference CLI's
+    assert np.array_equal(cb.points.cpu().numpy(), g["points"])
+    exact = tmp_path / "exact.ldjson"
+    R.write_curve_arrays(exact, kept.mech_ids, kept.joint_ids, kept.is_arc, kept.is_circle,
+                         kept.points.cpu().numpy())
+    assert exact.read_bytes() == np.asarray(g["curves_ldjson"], dtype=np.uint8).tobytes()
     # writer output parses to the reference's records (points to 1e-9)
     out = tmp_path / "c.ldjson"
     R.write_curve_arrays(out, kept.mech_ids, kept.joint_ids, kept.is_arc, kept.is_circle, kept.points.cpu().numpy())
