@@ -605,19 +605,33 @@ def bench_gen(torch, args, rank, world, peaks, flush, clk):
     def run(count, s0, s1):
         cfg = GenerationConfig(count=count, seed=2208)
         r = GenerationRun(cfg, traj_on_device=True, lookahead=8, slot_range=(s0, s1))
-        R = sum(b.R for b in r.blocks())
-        return r, R
+        blocks = list(r.blocks())
+        return r, sum(b.R for b in blocks), blocks
 
     run(500, 10**6, 10**6 + 100)  # warm-up (other slots)
     barrier(torch, world)
     torch.cuda.synchronize()
     clk.timed = True
     t0 = time.perf_counter()
-    r, R = run(GEN_COUNT * world, rank * slots, (rank + 1) * slots)
+    r, R, blocks = run(GEN_COUNT * world, rank * slots, (rank + 1) * slots)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    # cli normalize + curate over the generated block, on the device
+    from paper_2208_14567_b200.dataset import curate_batch, curves_from_block
+
+    t1 = time.perf_counter()
+    ncurves = nkept = 0
+    for b in blocks:
+        cb = curves_from_block(b, 5)
+        kept = curate_batch(cb, 0.005, 0)
+        ncurves += len(cb)
+        nkept += len(kept)
+    torch.cuda.synchronize()
+    dt_curves = time.perf_counter() - t1
     clk.timed = False
     dt = max_over_ranks(torch, dt * 1e3, world) / 1e3
+    dt_curves = max_over_ranks(torch, dt_curves * 1e3, world) / 1e3
+    del blocks
     st = r.stats
     return {"metric": "dataset generation: accepted records/sec (reference GenerationRun semantics)",
             "value": world * R / dt, "unit": "records/s", "seconds": dt,
@@ -625,6 +639,9 @@ def bench_gen(torch, args, rank, world, peaks, flush, clk):
             "screened_candidates_per_s": world * r.screened / dt,
             "records_per_gpu": R, "simulated_per_gpu": st.simulated, "discarded_topologies": st.topologies_discarded,
             "windows": r.windows, "host_ms": {k: v * 1e3 for k, v in r.timings.items()},
+            "curves": {"seconds": dt_curves, "curves_per_gpu": ncurves, "kept_per_gpu": nkept,
+                       "curves_per_s": world * ncurves / dt_curves,
+                       "note": "cli normalize (f64, bit-exact) + is_arc/is_circle + curate keep rule"},
             "reference_cpu": {"candidates_per_s_per_thread": 24500, "source": "SURVEY.md probe P3 (gated, 1 thread)"},
             "config": {"workload": f"{GEN_COUNT} records/GPU, default GenerationConfig, seed 2208, slots sharded "
                                    "by rank, trajectories kept on device"}}
