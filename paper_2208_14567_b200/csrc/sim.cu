@@ -84,7 +84,6 @@ struct Warp {
 
 struct SimCtx {
   int n, ns;
-  bool exact;  // LA_SIM_EXACT64
   double r1;
   float tau;
   float r1f;
@@ -129,7 +128,7 @@ __device__ __forceinline__ double rsqrt_f64(double x) {
 // Fast mode: the same formulas contracted to DFMA with d, 1/d and h from
 // Newton-refined MUFU reciprocal square roots (a few ulp from numpy; the
 // lock decision can differ only for margins within ~1e-15).
-template <typename Get, typename Put>
+template <bool EXACT, typename Get, typename Put>
 __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get get, Put put) {
   const double eps = 1e-9;
 #pragma unroll 1
@@ -143,7 +142,7 @@ __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get
     const double2 rr = *reinterpret_cast<const double2*>(&g.ra2);
     const double dx = dsub(pb.x, pa.x);
     const double dy = dsub(pb.y, pa.y);
-    if (C.exact) {
+    if (EXACT) {
       const double d = np_hypot(dx, dy);
       const bool lock = !(d >= eps) | (d > hl.x) | (d < hl.y);
       if (lock) return s;
@@ -178,6 +177,7 @@ __device__ __forceinline__ double2 crank_tip(const WarpHead& H, const SimCtx& C,
 
 // rare path of the fp32 screen: the whole angle again in f64, positions in
 // a lane-private array; rounded results go back to the fp32 column
+template <bool EXACT>
 __device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, double ct, double st) {
   double2 q[NJ];
   const WarpHead& H = *W.h;
@@ -188,7 +188,7 @@ __device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, dou
   }
   q[1] = crank_tip(H, C, ct, st);
   W.p32(1) = make_float2((float)q[1].x, (float)q[1].y);
-  return dyads_f64(H, C, [&](int j) { return q[j]; },
+  return dyads_f64<EXACT>(H, C, [&](int j) { return q[j]; },
                    [&](int j, double2 v) {
                      q[j] = v;
                      W.p32(j) = make_float2((float)v.x, (float)v.y);
@@ -206,6 +206,7 @@ struct Ctr {
   unsigned int fix_lanes = 0, replay_rounds = 0, lane_angles = 0, lane_dyads = 0;
 };
 
+template <bool EXACT>
 __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const double* __restrict__ cs,
                                        const float2* __restrict__ cs32, int t, bool active, Ctr& ctr) {
   const WarpHead& H = *W.h;
@@ -248,7 +249,7 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
   const unsigned need = __ballot_sync(FULL, active && fix) & below;
   if (need) {
     if ((need >> W.lane) & 1u) {
-      lk = replay_f64_local(W, C, cs[2 * t], cs[2 * t + 1]);
+      lk = replay_f64_local<EXACT>(W, C, cs[2 * t], cs[2 * t + 1]);
       ++ctr.fix_lanes;
     }
     if (W.lane == 0) ++ctr.replay_rounds;
@@ -259,12 +260,13 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
 }
 
 // f64 angle evaluation with positions in the warp's double2 column
+template <bool EXACT>
 __device__ __forceinline__ int solve64(const Warp& W, const SimCtx& C, const double* __restrict__ cs, int t,
                                        bool active) {
   if (!active) return -1;
   const WarpHead& H = *W.h;
   W.p64(1) = crank_tip(H, C, cs[2 * t], cs[2 * t + 1]);
-  return dyads_f64(H, C, [&](int j) { return W.p64(j); }, [&](int j, double2 v) { W.p64(j) = v; });
+  return dyads_f64<EXACT>(H, C, [&](int j) { return W.p64(j); }, [&](int j, double2 v) { W.p64(j) = v; });
 }
 
 __device__ __forceinline__ void fill_static32(const Warp& W) {
@@ -305,7 +307,7 @@ __host__ __device__ constexpr size_t col_bytes() {
   return (WRITE || SCREEN64) ? sizeof(double2) : sizeof(float2);
 }
 
-template <bool WRITE, bool SCREEN64, bool WONLY = false>
+template <bool WRITE, bool SCREEN64, bool WONLY, bool EXACT>
 __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p, int njmax) {
   extern __shared__ __align__(16) unsigned char sim_smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -344,7 +346,6 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
     C.n = pl->n;
     C.ns = pl->nsteps;
     C.tau = p.fixup_tau;
-    C.exact = (p.flags & LA_SIM_EXACT64) != 0;
     const uint32_t fixed = pl->fixed_mask | 1u;  // joint 0 is static (solver.py:183)
     if (C.n > njmax || C.n < 2 || C.ns > NS || C.ns < 0) {
       // plan does not fit the launch (n > pos_stride): flag, do not touch smem
@@ -377,8 +378,17 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
       const double2 pa = H.p0[ia_], pb = H.p0[ib_], pt = H.p0[it_];
       const double ax = dsub(pt.x, pa.x), ay = dsub(pt.y, pa.y);
       const double bx = dsub(pt.x, pb.x), by = dsub(pt.y, pb.y);
-      // np.hypot, bit for bit (glibc algorithm, common.cuh)
-      const double ra = np_hypot(ax, ay), rb = np_hypot(bx, by);
+      // np.hypot bit for bit (glibc algorithm, common.cuh) in exact mode;
+      // otherwise a Newton-refined sqrt of the sum (an ulp or two)
+      double ra, rb;
+      if (EXACT) {
+        ra = np_hypot(ax, ay);
+        rb = np_hypot(bx, by);
+      } else {
+        const double a2 = dadd(dmul(ax, ax), dmul(ay, ay)), b2 = dadd(dmul(bx, bx), dmul(by, by));
+        ra = a2 > 0.0 ? dmul(a2, rsqrt_f64(a2)) : 0.0;
+        rb = b2 > 0.0 ? dmul(b2, rsqrt_f64(b2)) : 0.0;
+      }
       const double cross = dsub(dmul(dsub(pb.x, pa.x), dsub(pt.y, pa.y)),
                                 dmul(dsub(pb.y, pa.y), dsub(pt.x, pa.x)));
       const double br = cross >= 0.0 ? 1.0 : -1.0;
@@ -404,7 +414,12 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
     }
     {
       const double dx = dsub(H.p0[1].x, H.p0[0].x), dy = dsub(H.p0[1].y, H.p0[0].y);
-      C.r1 = np_hypot(dx, dy);  // solver.py:180
+      if (EXACT) {
+        C.r1 = np_hypot(dx, dy);  // solver.py:180
+      } else {
+        const double r2 = dadd(dmul(dx, dx), dmul(dy, dy));
+        C.r1 = r2 > 0.0 ? dmul(r2, rsqrt_f64(r2)) : 0.0;
+      }
       C.r1f = (float)C.r1;
       C.p0f = make_float2((float)H.p0[0].x, (float)H.p0[0].y);
     }
@@ -414,8 +429,8 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
     __syncwarp();
 
     auto screen = [&](int t, bool act) -> int {
-      if (SCREEN64 || WONLY) return solve64(W, C, p.crank_cs, t, act);
-      return solve32(W, C, p.crank_cs, cs32, t, act, ctr);
+      if (SCREEN64 || WONLY) return solve64<EXACT>(W, C, p.crank_cs, t, act);
+      return solve32<EXACT>(W, C, p.crank_cs, cs32, t, act, ctr);
     };
 
     int first_t = T, first_j = -1, low_t = -1, low_j = -1;
@@ -477,7 +492,7 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
         for (int r = 0; r * 32 < T; ++r) {
           const int t = r * 32 + lane;
           const bool act = t < T;
-          const int lk = solve64(W, C, p.crank_cs, t, act);
+          const int lk = solve64<EXACT>(W, C, p.crank_cs, t, act);
           ++rounds;
           const RoundLock L = round_lock(act, lk);
           if (L.src >= 0) {
@@ -704,9 +719,14 @@ int la_simulate(const la_sim_args* a, void* stream) {
   const size_t smem = cs_bytes + (sizeof(WarpHead) + (size_t)njmax * 32 * colb) * SIM_WARPS;
   const bool wonly = (a->flags & LA_SIM_WRITE_ONLY) != 0;
   if (wonly && !write) return fail(LA_EINVAL, "la_simulate: WRITE_ONLY needs WRITE_TRAJ");
-  auto kern = wonly ? sim_kernel<true, false, true>
-              : write ? (f64 ? sim_kernel<true, true> : sim_kernel<true, false>)
-                      : (f64 ? sim_kernel<false, true> : sim_kernel<false, false>);
+  const bool exact = (a->flags & LA_SIM_EXACT64) != 0;
+  auto kern = exact ? (wonly ? sim_kernel<true, false, true, true>
+                             : write ? (f64 ? sim_kernel<true, true, false, true> : sim_kernel<true, false, false, true>)
+                                     : (f64 ? sim_kernel<false, true, false, true> : sim_kernel<false, false, false, true>))
+                    : (wonly ? sim_kernel<true, false, true, false>
+                             : write ? (f64 ? sim_kernel<true, true, false, false> : sim_kernel<true, false, false, false>)
+                                     : (f64 ? sim_kernel<false, true, false, false>
+                                            : sim_kernel<false, false, false, false>));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail((int)e, "la_simulate: smem attr: %s", cudaGetErrorString(e));
   int occ = 0;

@@ -1,6 +1,6 @@
 """Small fixed workloads for ncu captures (one GPU).
 
-    python tools/profile_step.py c2      # screen + compaction + f64 path replay, 100k candidates
+    python tools/profile_step.py c2      # bench C2 pipeline: deferred screen, compaction, path writes
     python tools/profile_step.py c3      # screen of 1M candidates, 5-20 joints
     python tools/profile_step.py c4      # chamfer scan, 1 query x 1M curves
     python tools/profile_step.py norm    # normalise 200k fp32 paths
@@ -17,7 +17,7 @@ _native.load(build_if_missing=False)
 what = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 if what == "c2":
-    from paper_2208_14567_b200.solver import simulate_compact
+    from paper_2208_14567_b200.solver import simulate_deferred
     from paper_2208_14567_b200.workloads import mixed_batch
 
     mb = mixed_batch(100_000, 6, 8, seed=2208, stride=8)
@@ -25,7 +25,7 @@ if what == "c2":
     topo = torch.from_numpy(mb.topo).cuda()
     table = mb.table()
     for _ in range(reps):
-        simulate_compact(pos, table, 200, topo)
+        simulate_deferred(pos, table, 200, topo)
 elif what == "c3":
     from paper_2208_14567_b200.solver import PlanTable, simulate_tensors
     from paper_2208_14567_b200.workloads import device_poses, topology_pool
