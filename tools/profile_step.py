@@ -4,6 +4,8 @@
     python tools/profile_step.py c3      # screen of 1M candidates, 5-20 joints
     python tools/profile_step.py c4      # chamfer scan, 1 query x 1M curves
     python tools/profile_step.py norm    # normalise 200k fp32 paths
+    python tools/profile_step.py filter  # coarse prefilter select over 10M descriptors
+    python tools/profile_step.py gen     # generation (device poses, gate) + curve pipeline
 """
 import os
 import sys
@@ -64,5 +66,23 @@ elif what == "c5":
 
     out = B.bench_c5(torch, A, 0, 1, {"sm_max_mhz": 1965.0, "hbm_gbs": 6551.7}, lambda: None, Clk)
     print({k: round(v, 3) for k, v in out["stages_ms"].items()})
+elif what == "filter":
+    from paper_2208_14567_b200.atlas import coarse_descriptors, coarse_select
+    from paper_2208_14567_b200.workloads import fourier_curves_device
+
+    raw = fourier_curves_device(1_000_000, 200, seed=6)
+    desc = coarse_descriptors(raw)
+    big = desc.repeat(10, 1)
+    order = torch.randperm(big.shape[0], device="cuda")
+    for _ in range(reps):
+        coarse_select(big, desc[7], big.shape[0] // 100, order)
+elif what == "gen":
+    from paper_2208_14567_b200.dataset import curate_batch, curves_from_block
+    from paper_2208_14567_b200.generator import GenerationConfig, GenerationRun
+
+    for _ in range(reps):
+        run = GenerationRun(GenerationConfig(count=5000, seed=1), traj_on_device=True, lookahead=8)
+        for b in run.blocks():
+            curate_batch(curves_from_block(b, 5), 0.005, 0)
 torch.cuda.synchronize()
 print("ok", what)
