@@ -59,10 +59,10 @@ def _numpy_poses(batches, nb, m):
     return pos, cand_plan
 
 
-def run_engine(cfg, count, lookahead=3, cap=1 << 16, device_windows=False):
+def run_engine(cfg, count, lookahead=3, cap=1 << 16, device_windows=False, slot0=0, nslots=None):
     lib = N.load()
-    slots = (count + cfg.variants - 1) // cfg.variants
-    eng = lib.la_gen_create(C.byref(cfg), 0, slots)
+    slots = (count + cfg.variants - 1) // cfg.variants if nslots is None else nslots
+    eng = lib.la_gen_create(C.byref(cfg), slot0, slots)
     assert eng
     try:
         pos = np.zeros((cap, NMAX, 2))
@@ -154,6 +154,23 @@ def test_engine_lookahead_invariance(golden):
     for k in ("meta", "pos", "nmeta", "npos", "by_n"):
         assert np.array_equal(a[k], b[k], equal_nan=True)
     assert a["windows"] >= 2 and b["windows"] >= 2
+
+
+def test_engine_slot_shards_concatenate(golden):
+    """Rank r of N owns a contiguous slot range (bench.py / GenerationRun
+    slot_range): shards generate independently and concatenate to the
+    single-engine run, stats summing -- no collective needed."""
+    g = golden("generator_golden.npz")
+    count, cfg = _cfg(g, 2)
+    slots = (count + cfg.variants - 1) // cfg.variants
+    whole = run_engine(cfg, count)
+    half = slots // 2
+    a = run_engine(cfg, count, slot0=0, nslots=half)
+    b = run_engine(cfg, count, slot0=half, nslots=slots - half)
+    assert np.array_equal(np.concatenate([a["meta"], b["meta"]]), whole["meta"])
+    assert np.array_equal(np.concatenate([a["pos"], b["pos"]]), whole["pos"], equal_nan=True)
+    assert np.array_equal(a["by_n"] + b["by_n"], whole["by_n"])
+    assert a["disc"] + b["disc"] == whole["disc"]
 
 
 def test_engine_bad_config():
