@@ -111,10 +111,14 @@ typedef struct la_sim_args {
                                  replay, 5 active lane-angles of fp32
                                  rounds, 6 fp32 dyads executed (to the
                                  first lock), 7 reserved                      */
-  float fixup_tau;            /* fp32 screen: redo an angle in f64 when a
-                                 dyad's margin min(ra+rb-d, d-|ra-rb|) is
-                                 within tau (unit-box lengths) of a lock;
-                                 trajectory rounds always run in f64         */
+  float fixup_tau;            /* fp32 screen: an angle is redone in f64
+                                 when a dyad's margin min(ra+rb-d, d-|ra-rb|)
+                                 is within tau + 3 E of a lock, E a running
+                                 first-order bound on the fp32 position
+                                 error (input rounding, per-dyad rounding,
+                                 amplification |x|(1+|x|/d)/h by flat
+                                 dyads); tau is the floor (default 2e-6).
+                                 Trajectory rounds always run in f64        */
   uint32_t flags;             /* LA_SIM_*                                     */
 } la_sim_args;
 

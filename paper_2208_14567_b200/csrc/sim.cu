@@ -95,6 +95,27 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// fp32 screen error model (solve32): input rounding of the f64 pose and
+// crank tip, per-dyad rounding of the fp32 evaluation (unit-box magnitudes,
+// rsqrt/sqrt approximations included), and the margin's sensitivity factor
+// with a safety factor of 2 on the first-order bound.
+#ifndef LA_ERR_STEP
+#define LA_ERR_STEP 5e-7f
+#endif
+#ifndef LA_MARGIN_K
+#define LA_MARGIN_K 3.0f
+#endif
+#ifndef LA_KAP_FULL
+#define LA_KAP_FULL 1
+#endif
+constexpr float kErr0 = 2e-7f;
+constexpr float kErrStep = LA_ERR_STEP;
+constexpr float kMarginK = LA_MARGIN_K;
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -217,6 +238,10 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
     W.p32(1) = make_float2(fmaf(C.r1f, c.x, C.p0f.x), fmaf(C.r1f, c.y, C.p0f.y));
     const float tau = C.tau;
     unsigned char* col = W.cols + W.lane * 8;
+    // running first-order bound on the fp32 position error of any joint
+    // placed so far (inputs rounded to fp32, then each dyad amplifies the
+    // error of its two parents by kappa and adds its own rounding)
+    float err = kErr0;
     int s = 0;
 #pragma unroll 1
     for (; s < C.ns; ++s) {
@@ -229,13 +254,22 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
       const float inv = rsqrt_approx(d2);
       const float d = d2 * inv;
       const float m = fminf(g0.x - d, d - g0.y);
-      fix |= !(fabsf(m) >= tau);  // NaN (coincident joints) -> f64 decides
+      // the margin moves by at most 2 err (d from two parents) + rounding
+      fix |= !(fabsf(m) >= fmaf(kMarginK, err, tau));  // NaN -> f64 decides
       if (m < 0.0f) {
         lk = s;
         break;
       }
       const float x = (d2 + g0.z) * (0.5f * inv);
       const float h = sqrt_approx(fmaxf(fmaf(-x, x, g0.w), 0.0f));
+      // amplification of parent errors by an ill-conditioned (flat) dyad:
+      // dh/dd = -(x/h)(1 - x/d), so |dh| <= |x| (1 + |x|/d) / h * |dd|;
+      // well-conditioned dyads move their target about as far as their
+      // parents moved (kappa ~ 1).  h -> 0 makes err infinite, so every
+      // later step of this angle is ambiguous and goes to the f64 replay.
+      const float ax = fabsf(x);
+      const float kap = fmaxf(1.0f, (LA_KAP_FULL ? ax * fmaf(ax, inv, 1.0f) : ax) * rcp_approx(h));
+      err = fmaf(kap, err, kErrStep);
       const float xi = x * inv;
       const float hb = __uint_as_float(g1.x) * h * inv;
       *reinterpret_cast<float2*>(col + g1.w) =

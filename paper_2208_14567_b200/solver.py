@@ -22,7 +22,7 @@ from paper_2208_14567_b200 import _native as N
 from paper_2208_14567_b200.mechanism import JointType, Mechanism
 
 LOCK_EPS = 1e-9                 # solver.py:19 (the kernels hard-code the same)
-DEFAULT_FIXUP_TAU = 2e-4        # f64 redo threshold on the dyad margin (unit-box lengths)
+DEFAULT_FIXUP_TAU = 2e-6  # floor of the error-model margin test (sim.cu solve32)
 
 
 class PlanError(ValueError):

@@ -444,3 +444,37 @@ def test_bit_exact_f64_replay(torch, golden):
             n = int(g["mx_n"][g["mx_topo"][gi]])
             assert np.array_equal(t64[gi, :n], tp[:n])
             assert np.array_equal(t32[gi, :n], tp[:n].astype(np.float32))
+
+
+@pytest.mark.parametrize("seed", [901, 902])
+def test_screen_flags_at_scale_vs_exact(torch, seed):
+    """1M generator candidates of 5-20 joints: the fp32 screen's lock flags
+    equal the all-f64 exact mode (bit-identical to the reference), except
+    candidates whose oracle margin is inside the 1e-6 band (none expected).
+    Long chains are where fp32 error amplification through flat dyads bites;
+    the screen's error model (sim.cu solve32) must send those to f64."""
+    from paper_2208_14567_b200.solver import simulate_tensors
+    from paper_2208_14567_b200.workloads import native_batch
+
+    nb = native_batch(1_000_000, 5, 20, seed=seed)
+    pos = torch.from_numpy(nb.pos).cuda()
+    topo = torch.from_numpy(nb.topo).cuda()
+    ref = simulate_tensors(pos, nb.table, 200, topo, write_traj=False, fp64=True, exact=True)
+    for kw in ({}, {"gate_only": True, "low": True}):
+        res = simulate_tensors(pos, nb.table, 200, topo, write_traj=False, **kw)
+        valid_ref = ref["first_t"] == 200
+        if kw:
+            bad = np.flatnonzero(((res["first_t"] == 200) != valid_ref).cpu().numpy())
+        else:
+            bad = np.flatnonzero(((res["first_t"] != ref["first_t"]) |
+                                  (res["first_joint"] != ref["first_joint"])).cpu().numpy())
+        raw = nb.table.host_bytes().reshape(-1, 64)
+        for i in bad:
+            rec = raw[int(nb.topo[i])]
+            n = int(rec[0:2].view(np.int16)[0])
+            ns = int(rec[2:4].view(np.int16)[0])
+            fm = int(rec[4:8].view(np.uint32)[0])
+            steps = [tuple(int(v) for v in s) for s in rec[8:8 + 3 * ns].astype(np.int8).reshape(ns, 3)]
+            fixed = [k for k in range(n) if (fm >> k) & 1]
+            m = O.simulate(nb.pos[i:i + 1, :n], steps, fixed, 200, with_margin=True)["margin"][0]
+            assert m < MARGIN, f"candidate {i}: flag mismatch with margin {m:.3e} ({kw})"
