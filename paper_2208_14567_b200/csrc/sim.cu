@@ -44,8 +44,8 @@ struct __align__(16) StepRec {
   float sp;              // ra + rb           (fp32 margin test)
   float df;              // |ra - rb|
   float c2;              // ra^2 - rb^2
-  float ra2;             // ra^2
-  float br;              // branch sign
+  float ra2;             // branch sign * ra^2 (|ra2| = ra^2)
+  uint32_t pmask;        // 1 << a | 1 << b (parents, for error tainting)
   uint32_t a_off;        // byte offset of joint a's float2 column
   uint32_t b_off;
   uint32_t t_off;
@@ -104,18 +104,9 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // crank tip, per-dyad rounding of the fp32 evaluation (unit-box magnitudes,
 // rsqrt/sqrt approximations included), and the margin's sensitivity factor
 // with a safety factor of 2 on the first-order bound.
-#ifndef LA_ERR_STEP
-#define LA_ERR_STEP 5e-7f
-#endif
-#ifndef LA_MARGIN_K
-#define LA_MARGIN_K 3.0f
-#endif
-#ifndef LA_KAP_FULL
-#define LA_KAP_FULL 1
-#endif
 constexpr float kErr0 = 2e-7f;
-constexpr float kErrStep = LA_ERR_STEP;
-constexpr float kMarginK = LA_MARGIN_K;
+constexpr float kErrStep = 5e-7f;
+constexpr float kMarginK = 3.0f;
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -241,12 +232,16 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
     // running first-order bound on the fp32 position error of any joint
     // placed so far (inputs rounded to fp32, then each dyad amplifies the
     // error of its two parents by kappa and adds its own rounding)
-    float err = kErr0;
+    float err = kErr0;  // bound for "clean" joints (no amplifying dyad upstream)
+    // joints downstream of an amplifying dyad carry the separate bound
+    // err_t; the bitmask (parents' bits precomputed per step) tracks them
+    float err_t = 0.0f;
+    unsigned taint = 0u;
     int s = 0;
 #pragma unroll 1
     for (; s < C.ns; ++s) {
       const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
-      const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].br);
+      const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].pmask);
       const float2 pa = *reinterpret_cast<const float2*>(col + g1.y);
       const float2 pb = *reinterpret_cast<const float2*>(col + g1.z);
       const float dx = pb.x - pa.x, dy = pb.y - pa.y;
@@ -254,24 +249,31 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
       const float inv = rsqrt_approx(d2);
       const float d = d2 * inv;
       const float m = fminf(g0.x - d, d - g0.y);
-      // the margin moves by at most 2 err (d from two parents) + rounding
-      fix |= !(fabsf(m) >= fmaf(kMarginK, err, tau));  // NaN -> f64 decides
+      const bool tp = (taint & g1.x) != 0u;
+      const float ep = tp ? fmaxf(err_t, err) : err;
+      // the margin moves by at most 2 ep (d from two parents) + rounding
+      fix |= !(fabsf(m) >= fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
       if (m < 0.0f) {
         lk = s;
         break;
       }
       const float x = (d2 + g0.z) * (0.5f * inv);
-      const float h = sqrt_approx(fmaxf(fmaf(-x, x, g0.w), 0.0f));
+      const float h = sqrt_approx(fmaxf(fmaf(-x, x, fabsf(g0.w)), 0.0f));
       // amplification of parent errors by an ill-conditioned (flat) dyad:
       // dh/dd = -(x/h)(1 - x/d), so |dh| <= |x| (1 + |x|/d) / h * |dd|;
       // well-conditioned dyads move their target about as far as their
-      // parents moved (kappa ~ 1).  h -> 0 makes err infinite, so every
-      // later step of this angle is ambiguous and goes to the f64 replay.
+      // parents moved (kappa ~ 1).  h -> 0 makes the bound infinite, so
+      // every later dependent step of this angle goes to the f64 replay.
       const float ax = fabsf(x);
-      const float kap = fmaxf(1.0f, (LA_KAP_FULL ? ax * fmaf(ax, inv, 1.0f) : ax) * rcp_approx(h));
-      err = fmaf(kap, err, kErrStep);
+      const float num = ax * fmaf(ax, inv, 1.0f);
+      if (tp || num > h) {  // amplifying dyad (kappa = num / h > 1) or tainted parent
+        err_t = fmaxf(err_t, fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep));
+        taint |= 1u << (g1.w >> 8);
+      } else {
+        err += kErrStep;
+      }
       const float xi = x * inv;
-      const float hb = __uint_as_float(g1.x) * h * inv;
+      const float hb = copysignf(h, g0.w) * inv;
       *reinterpret_cast<float2*>(col + g1.w) =
           make_float2(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)));
     }
@@ -439,8 +441,8 @@ __global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p
       r.sp = (float)(ra + rb);
       r.df = (float)fabs(ra - rb);
       r.c2 = (float)(ra * ra - rb * rb);
-      r.ra2 = (float)ra * (float)ra;
-      r.br = (float)br;
+      r.ra2 = br < 0.0 ? -((float)ra * (float)ra) : (float)ra * (float)ra;
+      r.pmask = (1u << ia_) | (1u << ib_);
       r.a_off = (uint32_t)ia_ * 32u * (uint32_t)sizeof(float2);
       r.b_off = (uint32_t)ib_ * 32u * (uint32_t)sizeof(float2);
       r.t_off = (uint32_t)it_ * 32u * (uint32_t)sizeof(float2);
