@@ -550,6 +550,26 @@ class GenerationRun:
                 yield blk.record(i)
 
 
+def rejection_curve(config: GenerationConfig, sizes: list[int], trials: int = 100) -> GenerationStats:
+    """Attempts-per-success study (generator.py:385-413): per joint count n,
+    `trials` fresh topologies from default_rng([seed, 7_000_000 + n, 0]),
+    each searched once for a valid pose on the shared stream
+    default_rng([seed, 7_000_000 + n, 1]) with the GPU gate."""
+    stats = GenerationStats()
+    for n in sizes:
+        rng_topo = np.random.default_rng([config.seed, 7_000_000 + n, 0])
+        rng_pos = np.random.default_rng([config.seed, 7_000_000 + n, 1])
+        for _ in range(trials):
+            topology, plan = sample_topology(rng_topo, n, config.ng_probability, config.topology_retries)
+            res = find_valid_variant(topology, plan, rng_pos, max_attempts=config.max_attempts,
+                                     T_low=config.T_low, T_high=config.T_high, batch=config.batch)
+            if res is None:
+                stats.record_failure(n, config.max_attempts)
+            else:
+                stats.record_success(n, res.attempts)
+    return stats
+
+
 def generate_dataset(config: GenerationConfig, **kw):
     """generator.py:378-383: (record iterator, run object)."""
     run = GenerationRun(config, **kw)

@@ -452,7 +452,7 @@ def simulate_batch(positions0_batch: np.ndarray, plan: SolutionPlan, T: int = 20
     B, n, _ = pos.shape
     if B == 0:
         return []
-    dpos = torch.from_numpy(np.ascontiguousarray(pos)).cuda()
+    dpos = torch.from_numpy(np.array(pos, dtype=np.float64, order="C")).cuda()
     res = simulate_tensors(dpos, PlanTable([plan]), T, write_traj=True, traj_stride=n, fixup_tau=fixup_tau,
                            traj_f64=True)
     return _outcomes(res, T, n)

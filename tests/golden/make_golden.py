@@ -327,6 +327,11 @@ def generator_fixture():
         d[f"g{ci}_cfg"] = np.array([cfg.count, cfg.seed, cfg.n_min, cfg.n_max, cfg.variants_per_topology,
                                      cfg.T_low, cfg.T_high, cfg.max_attempts, cfg.batch, cfg.topology_retries])
         d[f"g{ci}_rates"] = np.array([cfg.ng_probability, cfg.negative_rate])
+    # rejection_curve (generator.py:385-413)
+    rc = ref_gen.rejection_curve(ref_gen.GenerationConfig(count=1, seed=7, max_attempts=1500), [6, 9, 12], trials=6)
+    d["rc_sizes"] = np.array([6, 9, 12])
+    d["rc_stats"] = np.array([[n, rc.simulated_by_n.get(n, 0), rc.accepted_by_n.get(n, 0)] for n in (6, 9, 12)])
+    d["rc_samples"] = np.concatenate([np.array(rc.attempts_samples.get(n, []), dtype=np.int64) for n in (6, 9, 12)])
     np.savez_compressed(OUT / "generator_golden.npz", **d)
 
 
