@@ -106,7 +106,8 @@ def run_engine(cfg, count, lookahead=3, cap=1 << 16, device_windows=False, slot0
         assert lib.la_gen_stats(eng, by_n.ctypes.data, C.byref(disc)) == 0
     finally:
         lib.la_gen_destroy(eng)
-    return dict(meta=meta, pos=rpos, adj=adj, nmeta=nmeta, npos=npos, by_n=by_n, disc=disc.value, windows=windows)
+    return dict(meta=meta, pos=rpos, adj=adj, types=types, nmeta=nmeta, npos=npos, by_n=by_n, disc=disc.value,
+                windows=windows)
 
 
 def check_against_golden(g, ci, out, count):
@@ -183,3 +184,32 @@ def test_engine_bad_config():
     n_plans = C.c_int32(0)
     assert lib.la_gen_window(eng, 2, 16, 1, None, None, None, C.byref(n_plans)) == 0
     lib.la_gen_destroy(eng)
+
+
+def test_moving_joint_rows_follow_cli_normalize(golden):
+    """dataset.moving_joint_rows enumerates curves like cli.normalize
+    (cli.py:124-136): records in order, non-Fixed joints ascending, mech id
+    slot * variants + variant, is_arc = any Fixed neighbour (curves.py:87-92);
+    rows index the packed trajectory block."""
+    from paper_2208_14567_b200.dataset import moving_joint_rows
+    from paper_2208_14567_b200.generator import GeneratedBlock
+
+    g = golden("generator_golden.npz")
+    count, cfg = _cfg(g, 0)
+    out = run_engine(cfg, count)
+    meta, adj, types = out["meta"], out["adj"], out["types"]
+    ns = meta[:, 3]
+    row0 = np.zeros(len(ns) + 1, dtype=np.int64)
+    np.cumsum(ns, out=row0[1:])
+    blk = GeneratedBlock(meta, out["pos"], adj, types, np.zeros((0, 1, 2)), row0)
+    rows, mids, jids, arc = moving_joint_rows(blk, cfg.variants)
+    want = []
+    for i in range(len(meta)):
+        n = int(ns[i])
+        for j in range(n):
+            if types[i, j] == 0:
+                continue
+            nbrs = np.flatnonzero(adj[i, j, :n])
+            want.append((row0[i] + j, meta[i, 0] * cfg.variants + meta[i, 1], j, bool((types[i, nbrs] == 0).any())))
+    got = list(zip(rows.tolist(), mids.tolist(), jids.tolist(), arc.tolist()))
+    assert got == [tuple(int(x) if k < 3 else x for k, x in enumerate(w)) for w in want]
