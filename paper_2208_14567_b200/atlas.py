@@ -33,8 +33,7 @@ DEFAULT_THRESHOLD = 0.03   # atlas.py:30
 DEFAULT_K = 3              # atlas.py:31
 
 
-class FormatError(ValueError):
-    """A curve references a missing mechanism (records.py:26 semantics)."""
+from paper_2208_14567_b200.records import FormatError  # noqa: E402  (records.py:26; Atlas.build raises it)
 
 
 @dataclass
@@ -246,6 +245,38 @@ class Atlas:
                 stack[i] = outs[j]
         points = np.zeros((0, 0, 2)) if not stack else np.stack(stack)
         return cls(points, np.array(mech_ids), np.array(joint_ids), mechanisms, seed)
+
+    # -- persistence (atlas.py:114-149) ----------------------------------
+    def save(self, directory) -> None:
+        """meta.json + curves.ldjson (+ .npz sidecar) + mechanisms.ldjson in
+        the reference's record format."""
+        import json
+        from pathlib import Path
+
+        from paper_2208_14567_b200 import records as R
+
+        d = Path(directory)
+        d.mkdir(parents=True, exist_ok=True)
+        (d / "meta.json").write_text(json.dumps({"seed": self.seed, "size": len(self)}))
+        flags = np.zeros(len(self), dtype=bool)
+        R.write_curve_arrays(d / "curves.ldjson", self.mech_ids, self.joint_ids, flags, flags, self.points)
+        R.write_curves_npz_arrays(d / "curves.npz", self.mech_ids, self.joint_ids, flags, flags, self.points)
+        R.write_records(d / "mechanisms.ldjson", "mechanism",
+                        [R.mechanism_to_record(m, mid) for mid, m in sorted(self.mechanisms.items())])
+
+    @classmethod
+    def load(cls, directory) -> "Atlas":
+        import json
+        from pathlib import Path
+
+        from paper_2208_14567_b200 import records as R
+
+        d = Path(directory)
+        meta = json.loads((d / "meta.json").read_text())
+        npz = d / "curves.npz"
+        curves = R.read_curves_npz(npz) if npz.exists() else list(R.RecordReader(d / "curves.ldjson", "curve"))
+        mechs = {rec.id: R.record_to_mechanism(rec) for rec in R.RecordReader(d / "mechanisms.ldjson", "mechanism")}
+        return cls.build(curves, mechs, seed=meta["seed"])
 
     # -- device residency ------------------------------------------------
     def device_points(self):

@@ -290,6 +290,16 @@ def atlas_fixture():
             d[f"coarse_dup_{qi}_{bi}"] = atlas2.coarse_filter(q, b)
         hits = atlas2.retrieve(q, k=5, threshold=0.05, budget=61, filter_mode="heuristic")
         d[f"coarse_hits_{qi}"] = np.array([(h.mech_id, h.distance, float(h.above_threshold)) for h in hits])
+    # Atlas.save (atlas.py:114-134) output bytes of a small atlas
+    import tempfile
+
+    small_recs = [CurveRecord(mech_id=i, joint_id=3, is_arc=False, is_circle=False, points=p.tolist())
+                  for i, p in enumerate(pts[:12])]
+    small = ref_atlas.Atlas.build(small_recs, {i: mech for i in range(12)}, seed=5)
+    with tempfile.TemporaryDirectory() as tmp:
+        small.save(tmp)
+        for name in ("meta.json", "curves.ldjson", "mechanisms.ldjson"):
+            d["save_" + name.replace(".", "_")] = np.frombuffer((Path(tmp) / name).read_bytes(), dtype=np.uint8)
     np.savez_compressed(OUT / "atlas_golden.npz", **d)
 
 

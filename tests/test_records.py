@@ -77,3 +77,21 @@ def test_oracle_keep_rule_pinned(golden):
     kept = [O.curation_keep(int(m), int(j), bool(a or c), float(keep_rate), int(seed))
             for m, j, a, c in zip(g["mech_ids"], g["joint_ids"], g["is_arc"], g["is_circle"])]
     assert kept == list(g["kept"])
+
+
+def test_atlas_save_matches_reference_bytes(golden, tmp_path):
+    """Atlas.save writes the reference's files byte for byte; load round
+    trips (host only: no resampling, no device)."""
+    from paper_2208_14567_b200.atlas import Atlas
+    from paper_2208_14567_b200.workloads import four_bar
+
+    g = golden("atlas_golden.npz")
+    pts = g["points"][:12]
+    a = Atlas(pts, np.arange(12), np.full(12, 3), {i: four_bar() for i in range(12)}, seed=5)
+    a.save(tmp_path)
+    for name in ("meta.json", "curves.ldjson", "mechanisms.ldjson"):
+        assert (tmp_path / name).read_bytes() == _bytes(g["save_" + name.replace(".", "_")]), name
+    b = Atlas.load(tmp_path)
+    assert np.array_equal(b.points, a.points) and np.array_equal(b.order, a.order) and b.seed == 5
+    with pytest.raises(R.FormatError):
+        Atlas.build([R.CurveRecord(99, 3, False, False, pts[0].tolist())], {})
