@@ -608,7 +608,7 @@ def bench_gen(torch, args, rank, world, peaks, flush, clk):
         blocks = list(r.blocks())
         return r, sum(b.R for b in blocks), blocks
 
-    run(500, 10**6, 10**6 + 100)  # warm-up (other slots)
+    run(GEN_COUNT, 10**6, 10**6 + slots)  # warm-up at full size on other slots (allocator, streams, pinned)
     barrier(torch, world)
     torch.cuda.synchronize()
     clk.timed = True

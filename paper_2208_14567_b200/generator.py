@@ -360,6 +360,135 @@ def _mechanisms(adj: np.ndarray, types: np.ndarray, pos: np.ndarray, n: np.ndarr
             for i in range(len(n))]
 
 
+class _EngineLane:
+    """One la_gen engine with its own buffers and CUDA stream (GenerationRun
+    internals): submit() lays out the next window on the host and queues
+    poses -> gate -> flags D2H on the stream; wait_and_consume() waits for
+    that window and walks its flags."""
+
+    def __init__(self, run, lib, torch, dev, slot0: int, nslots: int):
+        import os as _os
+
+        self.run, self.lib, self.torch, self.dev = run, lib, torch, dev
+        c = run.config
+        self.c = c
+        cfg = run._cfg()
+        self.eng = lib.la_gen_create(C.byref(cfg), int(slot0), int(nslots))
+        if not self.eng:
+            raise ValueError(N.last_error())
+        self.th = run.threads or len(_os.sched_getaffinity(0))
+        self.fused = c.T_high == 4 * c.T_low
+        self.stream = torch.cuda.Stream(device=dev)
+        self.per_window = min(run.window_cap, max(c.batch, nslots * run.lookahead * c.batch))
+        self.stride = int(c.n_max)
+        self.plans_h = np.zeros((max(nslots, 1), 64), dtype=np.uint8)
+        self.flags_h = torch.empty((2, self.per_window), dtype=torch.int32).pin_memory()
+        self.n_plans = C.c_int32(0)
+        self.pos_d = torch.empty((self.per_window, self.stride, 2), dtype=torch.float64, device=dev)
+        self.topo_d = torch.empty(self.per_window, dtype=torch.int32, device=dev)
+        self.max_b = max(nslots * run.lookahead, 1)
+        if run.device_poses:
+            self.desc_h = torch.empty((self.max_b, C.sizeof(N.LaGenBatch)), dtype=torch.uint8).pin_memory()
+            self.desc_d = torch.empty_like(self.desc_h, device=dev)
+            self.nb = C.c_int64(0)
+        else:
+            self.pos_h = torch.empty((self.per_window, NMAX, 2), dtype=torch.float64).pin_memory()
+            self.plan_h = torch.empty(self.per_window, dtype=torch.int32).pin_memory()
+        self.active = True
+        self.m = 0
+        self.done = None
+        self.keep = None
+
+    def submit(self):
+        run, lib, torch, c = self.run, self.lib, self.torch, self.c
+        t0 = time.perf_counter()
+        if run.device_poses:
+            m = lib.la_gen_window_dev(self.eng, run.lookahead, self.per_window, self.desc_h.data_ptr(), self.max_b,
+                                      C.byref(self.nb), self.plans_h.ctypes.data, C.byref(self.n_plans))
+        else:
+            m = lib.la_gen_window(self.eng, run.lookahead, self.per_window, self.th, self.pos_h.data_ptr(),
+                                  self.plan_h.data_ptr(), self.plans_h.ctypes.data, C.byref(self.n_plans))
+        if m < 0:
+            raise GenerationError(N.last_error())
+        run.timings["window"] += time.perf_counter() - t0
+        if m == 0:
+            self.active = False
+            return
+        self.m = int(m)
+        np_ = self.n_plans.value
+        ns = self.plans_h[:np_, :2].copy().view(np.int16)[:, 0].astype(np.int32)
+        with torch.cuda.stream(self.stream):
+            table = PlanTable.from_records(self.plans_h[:np_].reshape(-1).copy(), ns, device=self.dev)
+            pd, topo = self.pos_d[:m], self.topo_d[:m]
+            sp = N.stream_ptr(self.stream)
+            if run.device_poses:
+                nb = self.nb.value
+                self.desc_d[:nb].copy_(self.desc_h[:nb], non_blocking=True)
+                N.check(self.lib.la_gen_poses(self.desc_d.data_ptr(), nb, self.stride, pd.data_ptr(), topo.data_ptr(),
+                                              sp), "la_gen_poses")
+            else:
+                pd.copy_(self.pos_h[:m, :self.stride], non_blocking=True)
+                topo.copy_(self.plan_h[:m], non_blocking=True)
+            if self.fused:
+                res = simulate_tensors(pd, table, c.T_high, topo, write_traj=False, low=True, gate_only=True,
+                                       exact=True, stream=self.stream)
+                self.flags_h[0, :m].copy_(res["first_t"], non_blocking=True)
+                self.flags_h[1, :m].copy_(res["low_t"], non_blocking=True)
+            else:
+                lo = simulate_tensors(pd, table, c.T_low, topo, write_traj=False, exact=True, stream=self.stream)
+                hi = simulate_tensors(pd, table, c.T_high, topo, write_traj=False, exact=True, stream=self.stream)
+                self.flags_h[0, :m].copy_(hi["first_t"], non_blocking=True)
+                ft = lo["first_t"]
+                self.flags_h[1, :m].copy_(torch.where(ft < c.T_low, ft, torch.full_like(ft, -1)), non_blocking=True)
+            self.keep = (table, res if self.fused else (lo, hi))  # alive until the stream is done
+            self.done = torch.cuda.Event()
+            self.done.record(self.stream)
+
+    def wait_and_consume(self):
+        run = self.run
+        t0 = time.perf_counter()
+        self.done.synchronize()
+        t1 = time.perf_counter()
+        run.timings["device"] += t1 - t0
+        run.windows += 1
+        run.screened += self.m
+        src = None if run.device_poses else self.pos_h.data_ptr()
+        rc = self.lib.la_gen_consume(self.eng, src, self.flags_h[0].data_ptr(), self.flags_h[1].data_ptr())
+        if rc != 0:
+            raise GenerationError(N.last_error())
+        self.keep = None
+        run.timings["consume"] += time.perf_counter() - t1
+
+    def results(self):
+        lib, eng = self.lib, self.eng
+        R = lib.la_gen_count(eng, 0)
+        meta = np.zeros((R, 4), dtype=np.int64)
+        rpos = np.zeros((R, NMAX, 2))
+        rplans = np.zeros((R, 64), dtype=np.uint8)
+        radj = np.zeros((R, NMAX, NMAX), dtype=np.uint8)
+        rtypes = np.zeros((R, NMAX), dtype=np.int8)
+        N.check(lib.la_gen_records(eng, meta.ctypes.data, rpos.ctypes.data, rplans.ctypes.data, radj.ctypes.data,
+                                   rtypes.ctypes.data), "la_gen_records")
+        Q = lib.la_gen_count(eng, 1)
+        nmeta = np.zeros((Q, 3), dtype=np.int64)
+        npos = np.zeros((Q, NMAX, 2))
+        nadj = np.zeros((Q, NMAX, NMAX), dtype=np.uint8)
+        ntypes = np.zeros((Q, NMAX), dtype=np.int8)
+        N.check(lib.la_gen_negatives(eng, nmeta.ctypes.data, npos.ctypes.data, nadj.ctypes.data,
+                                     ntypes.ctypes.data), "la_gen_negatives")
+        by_n = np.zeros((NMAX + 1, 2), dtype=np.int64)
+        disc = C.c_int64(0)
+        N.check(lib.la_gen_stats(eng, by_n.ctypes.data, C.byref(disc)), "la_gen_stats")
+        return meta, rpos, rplans, radj, rtypes, nmeta, npos, nadj, ntypes, by_n, int(disc.value)
+
+    def close(self):
+        if self.eng:
+            if self.done is not None:
+                self.done.synchronize()
+            self.lib.la_gen_destroy(self.eng)
+            self.eng = None
+
+
 class GenerationRun:
     """Dataset generation (generator.py:336-375) with the slot loop in the
     native engine and the two-fidelity gate on the GPU.
@@ -376,7 +505,8 @@ class GenerationRun:
 
     def __init__(self, config: GenerationConfig, *, lookahead: int = 4, slot_block: int = 1 << 14,
                  window_cap: int = 1 << 21, threads: int | None = None, device=None, device_poses: bool = True,
-                 traj_on_device: bool = False, slot_range: tuple[int, int] | None = None):
+                 traj_on_device: bool = False, slot_range: tuple[int, int] | None = None,
+                 overlap: bool = True):
         self.config = config
         self.stats = GenerationStats()
         self.negatives: list[NegativeSample] = []
@@ -385,6 +515,7 @@ class GenerationRun:
         self.window_cap = int(window_cap)
         self.threads = threads
         self.device = device
+        self.overlap = bool(overlap)  # two engines ping-ponged on two streams
         self.slot_range = slot_range  # (first, end) slots of this shard; records() then cuts at count per shard
         self.traj_on_device = bool(traj_on_device)  # GeneratedBlock.traj stays a CUDA tensor
         self.device_poses = bool(device_poses)  # poses drawn by la_gen_poses (else host threads + H2D)
@@ -400,104 +531,42 @@ class GenerationRun:
                           int(self.threads or len(os.sched_getaffinity(0))), 0)
 
     def _run_block(self, slot0: int, nslots: int):
-        import os as _os
-
         torch = N.require_cuda()
         lib = N.load()
         c = self.config
         dev = self.device or torch.device("cuda")
-        cfg = self._cfg()
-        eng = lib.la_gen_create(C.byref(cfg), int(slot0), int(nslots))
-        if not eng:
-            raise ValueError(N.last_error())
-        th = self.threads or len(_os.sched_getaffinity(0))
-        fused = c.T_high == 4 * c.T_low
+        # two engines over the two halves of the slot range, ping-ponged on
+        # two streams: one lane's host walk + window layout overlaps the
+        # other lane's gate launch (results identical: slots are independent
+        # and are concatenated in slot order)
+        nl = 2 if (self.overlap and nslots >= 2) else 1
+        cuts = [slot0 + (nslots * k) // nl for k in range(nl + 1)]
+        lanes = [_EngineLane(self, lib, torch, dev, cuts[k], cuts[k + 1] - cuts[k]) for k in range(nl)]
         try:
-            per_window = min(self.window_cap, max(c.batch, nslots * self.lookahead * c.batch))
-            stride = int(c.n_max)
-            plans_h = np.zeros((nslots, 64), dtype=np.uint8)
-            flags_h = torch.empty((2, per_window), dtype=torch.int32).pin_memory()
-            n_plans = C.c_int32(0)
-            pos_d = torch.empty((per_window, stride, 2), dtype=torch.float64, device=dev)
-            topo_d = torch.empty(per_window, dtype=torch.int32, device=dev)
-            if self.device_poses:
-                max_b = nslots * self.lookahead
-                desc_h = torch.empty((max_b, C.sizeof(N.LaGenBatch)), dtype=torch.uint8).pin_memory()
-                desc_d = torch.empty_like(desc_h, device=dev)
-                nb = C.c_int64(0)
-            else:
-                pos_h = torch.empty((per_window, NMAX, 2), dtype=torch.float64).pin_memory()
-                plan_h = torch.empty(per_window, dtype=torch.int32).pin_memory()
-            tm = self.timings
-            while True:
-                t0 = time.perf_counter()
-                if self.device_poses:
-                    m = lib.la_gen_window_dev(eng, self.lookahead, per_window, desc_h.data_ptr(), max_b, C.byref(nb),
-                                              plans_h.ctypes.data, C.byref(n_plans))
-                else:
-                    m = lib.la_gen_window(eng, self.lookahead, per_window, th, pos_h.data_ptr(), plan_h.data_ptr(),
-                                          plans_h.ctypes.data, C.byref(n_plans))
-                if m < 0:
-                    raise GenerationError(N.last_error())
-                if m == 0:
-                    break
-                t1 = time.perf_counter()
-                tm["window"] += t1 - t0
-                np_ = n_plans.value
-                ns = plans_h[:np_, :2].copy().view(np.int16)[:, 0].astype(np.int32)
-                table = PlanTable.from_records(plans_h[:np_].reshape(-1), ns, device=dev)
-                pd = pos_d[:m]
-                topo = topo_d[:m]
-                if self.device_poses:
-                    desc_d[:nb.value].copy_(desc_h[:nb.value], non_blocking=True)
-                    N.check(lib.la_gen_poses(desc_d.data_ptr(), nb.value, stride, pd.data_ptr(), topo.data_ptr(),
-                                             N.stream_ptr()), "la_gen_poses")
-                else:
-                    pd.copy_(pos_h[:m, :stride], non_blocking=True)
-                    topo.copy_(plan_h[:m], non_blocking=True)
-                if fused:
-                    res = simulate_tensors(pd, table, c.T_high, topo, write_traj=False, low=True, gate_only=True,
-                                           exact=True)
-                    flags_h[0, :m].copy_(res["first_t"], non_blocking=True)
-                    flags_h[1, :m].copy_(res["low_t"], non_blocking=True)
-                else:
-                    lo = simulate_tensors(pd, table, c.T_low, topo, write_traj=False, exact=True)
-                    hi = simulate_tensors(pd, table, c.T_high, topo, write_traj=False, exact=True)
-                    flags_h[0, :m].copy_(hi["first_t"], non_blocking=True)
-                    ft = lo["first_t"]
-                    flags_h[1, :m].copy_(torch.where(ft < c.T_low, ft, torch.full_like(ft, -1)), non_blocking=True)
-                torch.cuda.current_stream(dev).synchronize()
-                t2 = time.perf_counter()
-                tm["device"] += t2 - t1
-                self.windows += 1
-                self.screened += int(m)
-                src = None if self.device_poses else pos_h.data_ptr()
-                rc = lib.la_gen_consume(eng, src, flags_h[0].data_ptr(), flags_h[1].data_ptr())
-                if rc != 0:
-                    raise GenerationError(N.last_error())
-                tm["consume"] += time.perf_counter() - t2
+            for ln in lanes:
+                ln.submit()
+            while any(ln.active for ln in lanes):
+                for ln in lanes:
+                    if ln.active:
+                        ln.wait_and_consume()
+                        ln.submit()
             t3 = time.perf_counter()
-            # records, negatives, stats
-            R = lib.la_gen_count(eng, 0)
-            meta = np.zeros((R, 4), dtype=np.int64)
-            rpos = np.zeros((R, NMAX, 2))
-            rplans = np.zeros((R, 64), dtype=np.uint8)
-            radj = np.zeros((R, NMAX, NMAX), dtype=np.uint8)
-            rtypes = np.zeros((R, NMAX), dtype=np.int8)
-            N.check(lib.la_gen_records(eng, meta.ctypes.data, rpos.ctypes.data, rplans.ctypes.data,
-                                       radj.ctypes.data, rtypes.ctypes.data), "la_gen_records")
-            Q = lib.la_gen_count(eng, 1)
-            nmeta = np.zeros((Q, 3), dtype=np.int64)
-            npos = np.zeros((Q, NMAX, 2))
-            nadj = np.zeros((Q, NMAX, NMAX), dtype=np.uint8)
-            ntypes = np.zeros((Q, NMAX), dtype=np.int8)
-            N.check(lib.la_gen_negatives(eng, nmeta.ctypes.data, npos.ctypes.data, nadj.ctypes.data,
-                                         ntypes.ctypes.data), "la_gen_negatives")
-            by_n = np.zeros((NMAX + 1, 2), dtype=np.int64)
-            disc = C.c_int64(0)
-            N.check(lib.la_gen_stats(eng, by_n.ctypes.data, C.byref(disc)), "la_gen_stats")
+            parts = [ln.results() for ln in lanes]
         finally:
-            lib.la_gen_destroy(eng)
+            for ln in lanes:
+                ln.close()
+        meta = np.concatenate([p_[0] for p_ in parts])
+        rpos = np.concatenate([p_[1] for p_ in parts])
+        rplans = np.concatenate([p_[2] for p_ in parts])
+        radj = np.concatenate([p_[3] for p_ in parts])
+        rtypes = np.concatenate([p_[4] for p_ in parts])
+        nmeta = np.concatenate([p_[5] for p_ in parts])
+        npos = np.concatenate([p_[6] for p_ in parts])
+        nadj = np.concatenate([p_[7] for p_ in parts])
+        ntypes = np.concatenate([p_[8] for p_ in parts])
+        by_n = sum(p_[9] for p_ in parts)
+        disc = C.c_int64(sum(p_[10] for p_ in parts))
+        R = len(meta)
         st = GenerationStats()
         for n in range(NMAX + 1):
             if by_n[n, 0] or by_n[n, 1]:
