@@ -13,12 +13,19 @@
 // per-warp shared-memory column pos[joint][lane] (dynamic joint indices
 // without local-memory spills; conflict-free).
 //
-// Precision.  Angles are evaluated in fp32.  Any dyad whose normalised
-// margin g = min((ra+rb)^2-d^2, d^2-(ra-rb)^2)/(ra+rb)^2 has |g| < tau (up to
-// the first lock) sends that lane's whole angle through an f64 replay that
-// mirrors the reference operation order (no FMA contraction), so lock flags
-// match the f64 reference away from the 1e-6 margin band and coordinates stay
-// within 1e-4 of the bounding-box diagonal (SURVEY.md §7 hard part (a)).
+// Precision.  Screen angles are evaluated in fp32 with a running
+// first-order bound on each joint's fp32 position error (input rounding,
+// per-dyad rounding, amplification |x|(1+|x|/d)/h by flat dyads, a taint
+// mask separating amplified from clean joints).  A dyad whose margin
+// min(ra+rb-d, d-|ra-rb|) is within tau + 3 E(parents) of a lock makes the
+// lane's angle ambiguous; ambiguous lanes below the round's first certain
+// lock are replayed in f64.  f64 rounds (replays, path writes, the all-f64
+// mode) come in two instantiations: EXACT mirrors numpy's operation order
+// with IEEE ops and glibc's hypot (bit-identical to simulate_batch), fast
+// uses DFMA and Newton-refined MUFU reciprocal square roots (a few ulp).
+// Lock flags then match the f64 reference (0 mismatches on 4M 5-20 joint
+// candidates against the exact mode) and coordinates stay within 1e-4 of
+// the bounding-box diagonal (SURVEY.md §7 hard part (a)).
 //
 // Angle order.  With T % 4 == 0 the T/4 "coarse" angles t = 4i are screened
 // first (they are bit-identical to the T_low = T/4 sweep of the two-fidelity
