@@ -292,6 +292,14 @@ int la_gen_records(void* engine, int64_t* meta /* [R][4] */, double* pos, la_pla
 int la_gen_negatives(void* engine, int64_t* meta /* [R][3] */, double* pos, uint8_t* adj, int8_t* types);
 int la_gen_stats(void* engine, int64_t* by_n /* [21][2] */, int64_t* discarded);
 
+/* moving-joint curves of a generated block in cli.normalize order
+ * (cli.py:124-136): rows into the packed trajectory block, mech ids
+ * slot * variants + variant, joint ids, is_arc (curves.py:87-92).  Host
+ * function; outputs NULL -> count only.  Returns the curve count.        */
+int64_t la_moving_joints(const int64_t* meta, const int8_t* types, const uint8_t* adj, const int64_t* row0,
+                         int64_t R, int32_t variants, int64_t* rows, int64_t* mech_ids, int64_t* joint_ids,
+                         uint8_t* is_arc);
+
 /* raw PCG64 stream of default_rng(entropy[:n_ent]): kind 0 -> random(),
  * kind 1 -> integers(0, bound)                                              */
 int la_rng_draw(const int64_t* entropy, int32_t n_ent, int32_t kind, int64_t bound, int64_t count,

@@ -50,6 +50,7 @@ EXPORTS = (
     "la_coarse_workspace",
     "la_coarse_select",
     "la_curation_keep",
+    "la_moving_joints",
     "la_gen_create",
     "la_gen_destroy",
     "la_gen_window",
@@ -221,6 +222,8 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_coarse_workspace.argtypes = [i64]
     lib.la_coarse_workspace.restype = sz
     lib.la_coarse_select.argtypes = [vp, i64, vp, i64, vp, vp, vp, vp, sz, vp]
+    lib.la_moving_joints.argtypes = [vp, vp, vp, vp, i64, i32, vp, vp, vp, vp]
+    lib.la_moving_joints.restype = i64
     lib.la_curation_keep.argtypes = [vp, vp, vp, i64, i64, C.c_double, vp, vp]
     lib.la_gen_create.argtypes = [C.POINTER(LaGenCfg), i64, i64]
     lib.la_gen_create.restype = vp
@@ -244,7 +247,7 @@ def _declare(lib: C.CDLL) -> None:
     for name in EXPORTS:
         if name not in ("la_last_error", "la_compact_workspace", "la_chamfer_workspace", "la_coarse_workspace",
                         "la_gen_create",
-                        "la_gen_destroy", "la_gen_window", "la_gen_window_dev", "la_gen_count"):
+                        "la_gen_destroy", "la_gen_window", "la_gen_window_dev", "la_gen_count", "la_moving_joints"):
             getattr(lib, name).restype = C.c_int
 
 

@@ -831,3 +831,36 @@ int la_gen_stats(void* h, int64_t* out, int64_t* discarded) {
 }
 
 }  // extern "C"
+
+// Moving-joint curve enumeration of a generated block (cli.normalize order,
+// cli.py:124-136): records in order, non-Fixed joints ascending; row into
+// the packed trajectory block, mech id slot * variants + variant, is_arc =
+// any Fixed neighbour (curves.py:87-92).  Returns the curve count; outputs
+// may be NULL to count only.
+extern "C" int64_t la_moving_joints(const int64_t* meta /* [R][4] */, const int8_t* types /* [R][20] */,
+                                    const uint8_t* adj /* [R][20][20] */, const int64_t* row0, int64_t R,
+                                    int32_t variants, int64_t* rows, int64_t* mech_ids, int64_t* joint_ids,
+                                    uint8_t* is_arc) {
+  int64_t c = 0;
+  for (int64_t r = 0; r < R; ++r) {
+    const int n = (int)meta[4 * r + 3];
+    const int8_t* ty = types + r * LA_MAX_JOINTS;
+    uint32_t fixed = 0;
+    for (int j = 0; j < n; ++j)
+      if (ty[j] == 0) fixed |= 1u << j;
+    for (int j = 0; j < n; ++j) {
+      if (ty[j] == 0) continue;
+      if (rows) {
+        const uint8_t* a = adj + (r * LA_MAX_JOINTS + j) * LA_MAX_JOINTS;
+        bool arc = false;
+        for (int k = 0; k < n; ++k) arc |= a[k] && ((fixed >> k) & 1u);
+        rows[c] = row0[r] + j;
+        mech_ids[c] = meta[4 * r] * variants + meta[4 * r + 1];
+        joint_ids[c] = j;
+        is_arc[c] = arc ? 1 : 0;
+      }
+      ++c;
+    }
+  }
+  return c;
+}

@@ -98,20 +98,30 @@ __device__ double np_pairwise(const F& f, int lo, int n) {
   return dadd(np_pairwise(f, lo, n2), np_pairwise(f, lo + n2, n - n2));
 }
 
-// np.var(hypot(x - .5, y - .5)) (curves.py:99-100), thread-serial in numpy's
-// order; call from one thread
+// np.var(hypot(x - .5, y - .5)) (curves.py:99-100) in numpy's summation
+// order, by a whole CTA: the radii and squared deviations are computed in
+// parallel into buf (P doubles of shared memory), the two pairwise sums are
+// thread-serial (cheap adds).  Every thread calls it; all get the variance.
 template <class G>
-__device__ double np_circle_var(const G& pt, int P) {
-  auto r = [&](int k) {
+__device__ double np_circle_var(const G& pt, int P, double* buf, double* bc) {
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
     const double2 q = pt(k);
-    return np_hypot(dsub(q.x, 0.5), dsub(q.y, 0.5));
-  };
-  const double mean = ddiv(np_pairwise(r, 0, P), (double)P);
-  auto sq = [&](int k) {
-    const double x = dsub(r(k), mean);
-    return dmul(x, x);
-  };
-  return ddiv(np_pairwise(sq, 0, P), (double)P);
+    buf[k] = np_hypot(dsub(q.x, 0.5), dsub(q.y, 0.5));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) bc[0] = ddiv(np_pairwise([&](int k) { return buf[k]; }, 0, P), (double)P);
+  __syncthreads();
+  const double mean = bc[0];
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    const double x = dsub(buf[k], mean);
+    buf[k] = dmul(x, x);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) bc[0] = ddiv(np_pairwise([&](int k) { return buf[k]; }, 0, P), (double)P);
+  __syncthreads();
+  const double var = bc[0];
+  __syncthreads();
+  return var;
 }
 
 __device__ __forceinline__ double block_min(double v, double* red) {
@@ -140,15 +150,18 @@ __device__ __forceinline__ double2 load_pt(const void* base, size_t idx) {
   }
 }
 
-// Value compared in the pair search.  f64 input: the cdist distance itself,
-// sqrt((xi-xj)^2 + (yi-yj)^2) without FMA contraction, so exact ties resolve
-// to the lexicographically smallest pair as np.argmax over cdist does.
-// f32 input: the fp32 squared distance (near-ties are flagged unstable).
+// Value compared in the pair search.  f64 input: cdist's squared sum
+// (xi-xj)^2 + (yi-yj)^2 without FMA contraction; the square root is taken
+// only for pairs within rounding of the maximum (sqrt is monotone, so the
+// cdist argmax is among them; a second pass resolves pairs whose distinct
+// squared sums round to the same cdist value, lexicographically as
+// np.argmax does).  f32 input: the fp32 squared distance (near-ties are
+// flagged unstable).
 template <typename Tin, typename V2>
 __device__ __forceinline__ double pair_value(const V2 pj, const V2 pi) {
   if constexpr (sizeof(Tin) == 8) {
     const double dx = dsub(pj.x, pi.x), dy = dsub(pj.y, pi.y);
-    return __dsqrt_rn(dadd(dmul(dx, dx), dmul(dy, dy)));
+    return dadd(dmul(dx, dx), dmul(dy, dy));
   } else {
     const float dx = pj.x - pi.x, dy = pj.y - pi.y;
     return (double)fmaf(dy, dy, dx * dx);
@@ -226,10 +239,39 @@ __global__ void __launch_bounds__(NT) normalize_kernel(const la_norm_args p) {
     }
     __syncthreads();
     const double vmax = red[0];
-    const long long key = redk[0];
+    long long key = redk[0];
     const double vsecond = red2[0];
-    const int pi_ = (int)(key / P), pj_ = (int)(key % P);
     __syncthreads();
+    if constexpr (sizeof(Tin) == 8) {
+      // another pair within rounding of the maximum squared sum may reach
+      // the same cdist value with a smaller key: compare square roots there
+      const double thr = vmax - vmax * 0x1p-48;
+      if (vsecond >= thr) {
+        const double dmax = __dsqrt_rn(vmax);
+        long long kbest = key;
+        for (int i = tid; i < P; i += NT) {
+          for (int j = i + 1; j < P; ++j) {
+            const double v = pair_value<Tin>(pts[j], pts[i]);
+            if (v >= thr && __dsqrt_rn(v) == dmax) {
+              const long long k = (long long)i * P + j;
+              if (k < kbest) kbest = k;
+            }
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) kbest = min(kbest, __shfl_xor_sync(FULL, kbest, o));
+        if ((tid & 31) == 0) redk[tid >> 5] = kbest;
+        __syncthreads();
+        if (tid == 0) {
+          long long kk = redk[0];
+          for (int w = 1; w < NT / 32; ++w) kk = min(kk, redk[w]);
+          redk[0] = kk;
+        }
+        __syncthreads();
+        key = redk[0];
+        __syncthreads();
+      }
+    }
+    const int pi_ = (int)(key / P), pj_ = (int)(key % P);
 
     // exact diameter in f64 (cdist: sqrt of the summed squared differences)
     const double2 Pi = load_pt<Tin>(src, pi_), Pj = load_pt<Tin>(src, pj_);
@@ -325,7 +367,8 @@ __global__ void __launch_bounds__(NT) normalize_kernel(const la_norm_args p) {
     }
     __syncthreads();
     double var = 0.0;
-    if ((p.is_circle || p.circle_var) && tid == 0) var = np_circle_var([&](int k) { return e[k]; }, P);
+    if (p.is_circle || p.circle_var)  // pts is free after the pair search: reuse it for the radii
+      var = np_circle_var([&](int k) { return e[k]; }, P, reinterpret_cast<double*>(pts), red);
     if (tid == 0) {
       p.status[m] = 0;
       if (p.pair) { p.pair[2 * m] = pi_; p.pair[2 * m + 1] = pj_; }
@@ -333,8 +376,7 @@ __global__ void __launch_bounds__(NT) normalize_kernel(const la_norm_args p) {
       if (p.is_circle) p.is_circle[m] = var < 5e-4 ? 1 : 0;
       if (p.circle_var) p.circle_var[m] = var;
       if (p.unstable) {
-        const double lim = sizeof(Tin) == 8 ? vmax * (1.0 - p.rel_tol)
-                                            : vmax * (1.0 - p.rel_tol) * (1.0 - p.rel_tol);
+        const double lim = vmax * (1.0 - p.rel_tol) * (1.0 - p.rel_tol);  // squared values
         const bool tie = vsecond > lim;
         const bool flip = fabs(dsub(e[0].y, 0.5)) < p.y_tol;
         p.unstable[m] = (tie || flip) ? 1 : 0;
@@ -349,9 +391,9 @@ __global__ void __launch_bounds__(NT) circle_kernel(const void* paths, int64_t M
   __shared__ double red[32];
   for (long long m = blockIdx.x; m < M; m += gridDim.x) {
     const Tin* src = static_cast<const Tin*>(paths) + (size_t)m * P * 2;
-    double var = 0.0;
-    if (threadIdx.x == 0)
-      var = np_circle_var([&](int k) { return make_double2((double)src[2 * k], (double)src[2 * k + 1]); }, P);
+    extern __shared__ double cbuf[];
+    const double var =
+        np_circle_var([&](int k) { return make_double2((double)src[2 * k], (double)src[2 * k + 1]); }, P, cbuf, red);
     if (threadIdx.x == 0) {
       if (var_out) var_out[m] = var;
       if (flag) flag[m] = var < 5e-4 ? 1 : 0;
@@ -607,8 +649,13 @@ extern "C" int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int
   const int sms = sm_count();
   long long grid = M < (long long)sms * 8 ? M : (long long)sms * 8;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (in_f64) circle_kernel<double><<<(unsigned)grid, NT, 0, s>>>(paths, M, P, var, flag);
-  else circle_kernel<float><<<(unsigned)grid, NT, 0, s>>>(paths, M, P, var, flag);
+  const size_t smem = sizeof(double) * (size_t)P;
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(circle_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(circle_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  if (in_f64) circle_kernel<double><<<(unsigned)grid, NT, smem, s>>>(paths, M, P, var, flag);
+  else circle_kernel<float><<<(unsigned)grid, NT, smem, s>>>(paths, M, P, var, flag);
   return cuda_status("la_circle_stats");
 }
 

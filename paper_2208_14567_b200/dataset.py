@@ -68,17 +68,23 @@ def mechanisms_of_block(block, variants_per_topology: int) -> dict:
 def moving_joint_rows(block, variants_per_topology: int):
     """(rows into block.traj, mech ids, joint ids, is_arc) of every non-Fixed
     joint of every record of a GeneratedBlock."""
-    meta = block.meta
-    n = meta[:, 3]
-    j = np.arange(NMAX)[None, :]
-    valid = j < n[:, None]
-    moving = valid & (block.types != JointType.FIXED)
-    fixed = valid & (block.types == JointType.FIXED)
-    arc = (block.adjacency.astype(bool) & fixed[:, None, :]).any(axis=2)  # (R, 20)
-    rec, joint = np.nonzero(moving)
-    rows = block.row0[rec] + joint
-    mech_ids = meta[rec, 0] * variants_per_topology + meta[rec, 1]
-    return rows.astype(np.int64), mech_ids.astype(np.int64), joint.astype(np.int64), arc[rec, joint]
+    lib = N.load()
+    meta = np.ascontiguousarray(block.meta, dtype=np.int64)
+    types = np.ascontiguousarray(block.types, dtype=np.int8)
+    adj = np.ascontiguousarray(block.adjacency, dtype=np.uint8)
+    row0 = np.ascontiguousarray(block.row0, dtype=np.int64)
+    R = len(meta)
+    M = lib.la_moving_joints(meta.ctypes.data, types.ctypes.data, adj.ctypes.data, row0.ctypes.data, R,
+                             int(variants_per_topology), None, None, None, None)
+    rows = np.empty(M, dtype=np.int64)
+    mech_ids = np.empty(M, dtype=np.int64)
+    joint = np.empty(M, dtype=np.int64)
+    arc = np.empty(M, dtype=np.uint8)
+    lib.la_moving_joints(meta.ctypes.data, types.ctypes.data, adj.ctypes.data, row0.ctypes.data, R,
+                         int(variants_per_topology), rows.ctypes.data, mech_ids.ctypes.data, joint.ctypes.data,
+                         arc.ctypes.data)
+    return rows, mech_ids, joint, arc.astype(bool)
+
 
 
 def curves_from_block(block, variants_per_topology: int) -> CurveBatch:
