@@ -845,19 +845,19 @@ extern "C" int64_t la_moving_joints(const int64_t* meta /* [R][4] */, const int8
   for (int64_t r = 0; r < R; ++r) {
     const int n = (int)meta[4 * r + 3];
     const int8_t* ty = types + r * LA_MAX_JOINTS;
-    uint32_t fixed = 0;
-    for (int j = 0; j < n; ++j)
-      if (ty[j] == 0) fixed |= 1u << j;
+    uint8_t fixed[LA_MAX_JOINTS];  // 1 for Fixed joints < n (fixed-length: the arc test vectorises)
+    for (int k = 0; k < LA_MAX_JOINTS; ++k) fixed[k] = (k < n && ty[k] == 0) ? 1 : 0;
+    const int64_t base = row0[r], mid = meta[4 * r] * variants + meta[4 * r + 1];
     for (int j = 0; j < n; ++j) {
       if (ty[j] == 0) continue;
       if (rows) {
         const uint8_t* a = adj + (r * LA_MAX_JOINTS + j) * LA_MAX_JOINTS;
-        bool arc = false;
-        for (int k = 0; k < n; ++k) arc |= a[k] && ((fixed >> k) & 1u);
-        rows[c] = row0[r] + j;
-        mech_ids[c] = meta[4 * r] * variants + meta[4 * r + 1];
+        uint8_t acc = 0;
+        for (int k = 0; k < LA_MAX_JOINTS; ++k) acc |= (uint8_t)(a[k] & fixed[k]);
+        rows[c] = base + j;
+        mech_ids[c] = mid;
         joint_ids[c] = j;
-        is_arc[c] = arc ? 1 : 0;
+        is_arc[c] = acc ? 1 : 0;
       }
       ++c;
     }
