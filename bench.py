@@ -608,7 +608,8 @@ def bench_gen(torch, args, rank, world, peaks, flush, clk):
         blocks = list(r.blocks())
         return r, sum(b.R for b in blocks), blocks
 
-    run(GEN_COUNT, 10**6, 10**6 + slots)  # warm-up at full size on other slots (allocator, streams, pinned)
+    for w in range(2):  # warm-up at full size on other slots (allocator, streams, pinned buffers)
+        run(GEN_COUNT, 10**6 * (w + 1), 10**6 * (w + 1) + slots)
     barrier(torch, world)
     torch.cuda.synchronize()
     clk.timed = True

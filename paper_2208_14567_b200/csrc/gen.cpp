@@ -587,12 +587,13 @@ void* la_gen_create(const la_gen_cfg* cfg, int64_t slot0, int64_t n_slots) {
   Engine* E = new Engine();
   E->cfg = *cfg;
   E->slots.reserve((size_t)n_slots);
-  for (int64_t s = 0; s < n_slots; ++s) {
-    E->slots.emplace_back(slot0 + s, cfg->seed);
-    Slot& S = E->slots.back();
+  for (int64_t s = 0; s < n_slots; ++s) E->slots.emplace_back(slot0 + s, cfg->seed);
+  // first topology of every slot (independent streams: host threads)
+  parallel_for(n_slots, cfg->threads, [&](int64_t s) {
+    Slot& S = E->slots[(size_t)s];
     S.n = (int)S.topo.integers(cfg->n_min, (int64_t)cfg->n_max + 1);
     if (!next_topology(*E, S)) S.state = 3;
-  }
+  });
   E->slot_records.resize((size_t)n_slots);
   E->slot_negs.resize((size_t)n_slots);
   for (auto& S : E->slots)

@@ -360,13 +360,26 @@ def _mechanisms(adj: np.ndarray, types: np.ndarray, pos: np.ndarray, n: np.ndarr
             for i in range(len(n))]
 
 
+_PINNED: dict = {}
+
+
+def _pinned(torch, key, shape, dtype):
+    """Reusable pinned host buffer (cudaHostAlloc is slow; generation runs
+    allocate the same window buffers block after block)."""
+    t = _PINNED.get(key)
+    if t is None or t.dtype != dtype or t.numel() < int(np.prod(shape)):
+        t = torch.empty(int(np.prod(shape)), dtype=dtype).pin_memory()
+        _PINNED[key] = t
+    return t[:int(np.prod(shape))].view(*shape)
+
+
 class _EngineLane:
     """One la_gen engine with its own buffers and CUDA stream (GenerationRun
     internals): submit() lays out the next window on the host and queues
     poses -> gate -> flags D2H on the stream; wait_and_consume() waits for
     that window and walks its flags."""
 
-    def __init__(self, run, lib, torch, dev, slot0: int, nslots: int):
+    def __init__(self, run, lib, torch, dev, slot0: int, nslots: int, index: int = 0):
         import os as _os
 
         self.run, self.lib, self.torch, self.dev = run, lib, torch, dev
@@ -382,18 +395,18 @@ class _EngineLane:
         self.per_window = min(run.window_cap, max(c.batch, nslots * run.lookahead * c.batch))
         self.stride = int(c.n_max)
         self.plans_h = np.zeros((max(nslots, 1), 64), dtype=np.uint8)
-        self.flags_h = torch.empty((2, self.per_window), dtype=torch.int32).pin_memory()
+        self.flags_h = _pinned(torch, ("flags", index), (2, self.per_window), torch.int32)
         self.n_plans = C.c_int32(0)
         self.pos_d = torch.empty((self.per_window, self.stride, 2), dtype=torch.float64, device=dev)
         self.topo_d = torch.empty(self.per_window, dtype=torch.int32, device=dev)
         self.max_b = max(nslots * run.lookahead, 1)
         if run.device_poses:
-            self.desc_h = torch.empty((self.max_b, C.sizeof(N.LaGenBatch)), dtype=torch.uint8).pin_memory()
+            self.desc_h = _pinned(torch, ("desc", index), (self.max_b, C.sizeof(N.LaGenBatch)), torch.uint8)
             self.desc_d = torch.empty_like(self.desc_h, device=dev)
             self.nb = C.c_int64(0)
         else:
-            self.pos_h = torch.empty((self.per_window, NMAX, 2), dtype=torch.float64).pin_memory()
-            self.plan_h = torch.empty(self.per_window, dtype=torch.int32).pin_memory()
+            self.pos_h = _pinned(torch, ("pos", index), (self.per_window, NMAX, 2), torch.float64)
+            self.plan_h = _pinned(torch, ("plan", index), (self.per_window,), torch.int32)
         self.active = True
         self.m = 0
         self.done = None
@@ -415,6 +428,7 @@ class _EngineLane:
             self.active = False
             return
         self.m = int(m)
+        t1 = time.perf_counter()
         np_ = self.n_plans.value
         ns = self.plans_h[:np_, :2].copy().view(np.int16)[:, 0].astype(np.int32)
         with torch.cuda.stream(self.stream):
@@ -443,6 +457,7 @@ class _EngineLane:
             self.keep = (table, res if self.fused else (lo, hi))  # alive until the stream is done
             self.done = torch.cuda.Event()
             self.done.record(self.stream)
+        run.timings["enqueue"] = run.timings.get("enqueue", 0.0) + time.perf_counter() - t1
 
     def wait_and_consume(self):
         run = self.run
@@ -541,7 +556,9 @@ class GenerationRun:
         # and are concatenated in slot order)
         nl = 2 if (self.overlap and nslots >= 2) else 1
         cuts = [slot0 + (nslots * k) // nl for k in range(nl + 1)]
-        lanes = [_EngineLane(self, lib, torch, dev, cuts[k], cuts[k + 1] - cuts[k]) for k in range(nl)]
+        t_init = time.perf_counter()
+        lanes = [_EngineLane(self, lib, torch, dev, cuts[k], cuts[k + 1] - cuts[k], k) for k in range(nl)]
+        self.timings["init"] = self.timings.get("init", 0.0) + time.perf_counter() - t_init
         try:
             for ln in lanes:
                 ln.submit()
