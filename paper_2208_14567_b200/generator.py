@@ -407,6 +407,23 @@ class _EngineLane:
         else:
             self.pos_h = _pinned(torch, ("pos", index), (self.per_window, NMAX, 2), torch.float64)
             self.plan_h = _pinned(torch, ("plan", index), (self.per_window,), torch.int32)
+        # fused gate: one la_simulate per window straight from preallocated
+        # buffers (plan records through a pinned staging buffer)
+        self.plans_p = _pinned(torch, ("plans", index), (max(nslots, 1) * 64,), torch.uint8)
+        self.plans_d = torch.empty(max(nslots, 1) * 64, dtype=torch.uint8, device=dev)
+        self.flags_d = torch.empty((4, self.per_window), dtype=torch.int32, device=dev)
+        from paper_2208_14567_b200.solver import DEFAULT_FIXUP_TAU, crank_table
+
+        self.cs = crank_table(c.T_high, dev)
+        self.args = N.LaSimArgs()
+        a = self.args
+        a.pos0, a.topo, a.plans, a.crank_cs = self.pos_d.data_ptr(), self.topo_d.data_ptr(), \
+            self.plans_d.data_ptr(), self.cs.data_ptr()
+        a.pos_stride, a.T, a.traj_stride = self.stride, c.T_high, self.stride
+        a.first_t, a.first_joint = self.flags_d[0].data_ptr(), self.flags_d[1].data_ptr()
+        a.low_t, a.low_joint = self.flags_d[2].data_ptr(), self.flags_d[3].data_ptr()
+        a.fixup_tau = float(DEFAULT_FIXUP_TAU)
+        a.flags = N.LA_SIM_GATE_ONLY | N.LA_SIM_EXACT64
         self.active = True
         self.m = 0
         self.done = None
@@ -430,6 +447,23 @@ class _EngineLane:
         self.m = int(m)
         t1 = time.perf_counter()
         np_ = self.n_plans.value
+        if self.fused and run.device_poses:
+            with torch.cuda.stream(self.stream):
+                sp = N.stream_ptr(self.stream)
+                nb = self.nb.value
+                self.plans_p[:np_ * 64].numpy()[:] = self.plans_h[:np_].reshape(-1)
+                self.plans_d[:np_ * 64].copy_(self.plans_p[:np_ * 64], non_blocking=True)
+                self.desc_d[:nb].copy_(self.desc_h[:nb], non_blocking=True)
+                N.check(self.lib.la_gen_poses(self.desc_d.data_ptr(), nb, self.stride, self.pos_d.data_ptr(),
+                                              self.topo_d.data_ptr(), sp), "la_gen_poses")
+                self.args.B, self.args.G = int(m), int(np_)
+                N.check(self.lib.la_simulate(self.args, sp), "la_simulate")
+                self.flags_h[0, :m].copy_(self.flags_d[0, :m], non_blocking=True)
+                self.flags_h[1, :m].copy_(self.flags_d[2, :m], non_blocking=True)
+                self.done = torch.cuda.Event()
+                self.done.record(self.stream)
+            run.timings["enqueue"] = run.timings.get("enqueue", 0.0) + time.perf_counter() - t1
+            return
         ns = self.plans_h[:np_, :2].copy().view(np.int16)[:, 0].astype(np.int32)
         with torch.cuda.stream(self.stream):
             table = PlanTable.from_records(self.plans_h[:np_].reshape(-1).copy(), ns, device=self.dev)
