@@ -186,6 +186,8 @@ int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P,
                                 differences                                  */
 #define LA_CH_SCALAR_PIPE 2u /* one-lane FFMA/FADD inner loop instead of the
                                 f32x2 (FFMA2/FADD2) forms                    */
+#define LA_CH_TENSOR 8u      /* squared distances on tcgen05 (3xTF32 split,
+                                direct-difference recheck of small minima)   */
 
 typedef struct la_chamfer_args {
   const float* db;            /* (device) [N][P][2] f32 normalised curves     */

@@ -32,6 +32,7 @@ LA_PENDING = -3
 
 LA_CH_EXPANSION = 1
 LA_CH_SCALAR_PIPE = 2
+LA_CH_TENSOR = 8
 
 EXPORTS = (
     "la_simulate",

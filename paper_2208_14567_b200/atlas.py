@@ -50,7 +50,7 @@ class RetrievalHit:
 def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None, pos_begin: int = 0,
                  pos_end: int | None = None, id_base: int = 0, pos_base: int = 0, pos_map=None,
                  exclude_id: int = -1, dense: bool = False, all_d=None, expansion: bool = False,
-                 fix_tol: float = 5e-5, scalar_pipe: bool = False, stream=None) -> dict:
+                 fix_tol: float = 5e-5, scalar_pipe: bool = False, tensor: bool = False, stream=None) -> dict:
     """One la_chamfer_topk launch.
 
     db: (N, P, 2) float32 CUDA tensor; queries: (NQ, Q, 2) float32.  order:
@@ -107,7 +107,8 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
         setattr(a, name, N.ptr(out.get(name)))
     a.n_hits = out["n_hits"].data_ptr()
     a.all_d = N.ptr(all_d)
-    a.flags = (N.LA_CH_EXPANSION if expansion else 0) | (N.LA_CH_SCALAR_PIPE if scalar_pipe else 0)
+    a.flags = ((N.LA_CH_EXPANSION if expansion else 0) | (N.LA_CH_SCALAR_PIPE if scalar_pipe else 0)
+               | (N.LA_CH_TENSOR if tensor else 0))
     a.fixup_below = float(fix_tol)
     wsb = int(lib.la_chamfer_workspace(a))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)

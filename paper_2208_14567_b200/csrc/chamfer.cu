@@ -494,6 +494,476 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
   flush_lists(c, qi, gw, lane, top, hit, nhit);
 }
 
+// ------------------------------------------------------------ tensor-core path
+// (LA_CH_TENSOR; even P <= 256, Q <= 256)  Squared distances of all point
+// pairs come from tcgen05.mma.kind::tf32 as |a|^2 + |b|^2 - 2 a.b with a
+// 3xTF32 split (x = x_hi + x_lo, x_hi = x with the 13 low mantissa bits
+// cleared) packed into K = 16:
+//   A row (point a):  [a_hx, a_hy, a_hx, a_hy, a_lx, a_ly, n_ah, n_al, 1, 1, 0...]
+//   B row (point b):  [-2b_hx, -2b_hy, -2b_lx, -2b_ly, -2b_hx, -2b_hy, 1, 1, n_bh, n_bl, 0...]
+// (coordinates centred at (0.5, 0.5), n = |.|^2 split the same way; only the
+// a_lo.b_lo term, 2^-22 relative, is dropped).  Both directions are MMAs:
+// query rows x curve columns gives the query-side row minima, curve rows x
+// query columns the curve-side ones, each a thread-local minimum over a
+// TMEM row after tcgen05.ld.  Rows whose minimum falls below TC_RECHECK
+// (d < 0.007, where the expansion's cancellation could move sqrt(d^2) by
+// more than ~1e-5) are recomputed with direct differences from the raw
+// points.  One CTA = 8 warps, 256 TMEM columns (two CTAs share an SM: one
+// CTA's MMA overlaps the other's epilogue); one elected thread issues TMA
+// and MMA.  Operands are K-major in shared memory without swizzle: 8-row x
+// 16-byte core matrices, K-adjacent ones 128 B apart, 8-row groups 512 B.
+constexpr int TC_THREADS = 256;
+constexpr int TC_K = 16;
+constexpr int TC_ROWB = TC_K * 4;           // bytes per operand row
+constexpr int TC_OP = 256 * TC_ROWB;        // bytes per operand buffer (256 rows)
+#ifndef TC_RECHECK_V
+#define TC_RECHECK_V 1.0e-6f
+#endif
+constexpr float TC_RECHECK = TC_RECHECK_V;         // squared distance below which a row minimum is recomputed
+constexpr float TC_FAR = 1.0e30f;           // |b|^2 of padding columns: never a minimum
+constexpr size_t TC_SMEM = 8 * TC_OP + 4 * PMAX * sizeof(float2) + PMAX * sizeof(float2) + 1024 * sizeof(float) +
+                           26 * sizeof(uint64_t) + 2 * sizeof(uint32_t) + 4 * 16 * sizeof(float) + 64;
+
+__device__ __forceinline__ int tc_off(int r, int k) {
+  return (r >> 3) * 512 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
+}
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+// operand rows for a point (centred coordinates x, y); pad rows: zeros (A) or far (B)
+__device__ __forceinline__ void tc_rows(unsigned char* A, unsigned char* B, int r, bool real, float x, float y) {
+  float ra[TC_K], rb[TC_K];
+#pragma unroll
+  for (int k = 0; k < TC_K; ++k) ra[k] = rb[k] = 0.f;
+  if (real) {
+    const float hx = tf32_hi(x), hy = tf32_hi(y), lx = x - hx, ly = y - hy;
+    const float n = fmaf(y, y, x * x);
+    const float nh = tf32_hi(n), nl = n - nh;
+    ra[0] = hx; ra[1] = hy; ra[2] = hx; ra[3] = hy; ra[4] = lx; ra[5] = ly; ra[6] = nh; ra[7] = nl;
+    ra[8] = 1.f; ra[9] = 1.f;
+    rb[0] = -2.f * hx; rb[1] = -2.f * hy; rb[2] = -2.f * lx; rb[3] = -2.f * ly; rb[4] = -2.f * hx;
+    rb[5] = -2.f * hy; rb[6] = 1.f; rb[7] = 1.f; rb[8] = nh; rb[9] = nl;
+  } else {
+    rb[8] = TC_FAR;
+  }
+  if (A) {
+#pragma unroll
+    for (int k = 0; k < TC_K; k += 4)
+      *reinterpret_cast<float4*>(A + tc_off(r, k)) = make_float4(ra[k], ra[k + 1], ra[k + 2], ra[k + 3]);
+  }
+  if (B) {
+#pragma unroll
+    for (int k = 0; k < TC_K; k += 4)
+      *reinterpret_cast<float4*>(B + tc_off(r, k)) = make_float4(rb[k], rb[k + 1], rb[k + 2], rb[k + 3]);
+  }
+}
+
+__device__ __forceinline__ uint64_t tc_desc(uint32_t addr) {
+  return (uint64_t)((addr & 0x3FFFF) >> 4) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ uint32_t tc_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem, uint32_t a_addr, uint32_t b_addr, int n) {
+  const uint32_t idesc = tc_idesc(n);
+#pragma unroll
+  for (int ks = 0; ks < TC_K / 8; ++ks) {
+    const uint64_t ad = tc_desc(a_addr + ks * 256), bd = tc_desc(b_addr + ks * 256);
+    const uint32_t acc = ks > 0;
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+  }
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// min over 32 consecutive TMEM columns of this thread's row (one load, one wait)
+__device__ __forceinline__ float tc_min32(uint32_t taddr) {
+  uint32_t v[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  float m = INFINITY;
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) m = min3f(m, __uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+  return m;
+}
+
+// min over 8 consecutive TMEM columns of this thread's row
+__device__ __forceinline__ float tc_min8(uint32_t taddr) {
+  uint32_t v[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  float m = min3f(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]));
+  m = min3f(m, __uint_as_float(v[3]), __uint_as_float(v[4]));
+  m = min3f(m, __uint_as_float(v[5]), __uint_as_float(v[6]));
+  return fminf(m, __uint_as_float(v[7]));
+}
+
+// min over columns [c0, c1) of this thread's TMEM row: 64-column chunks as
+// two x32 loads behind one wait, 8-column tail chunks as x8 loads
+#define LA_TC_LD32(v, addr)                                                                                   \
+  asm volatile(                                                                                               \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"       \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"                            \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),      \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), \
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),           \
+        "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),           \
+        "=r"(v[30]), "=r"(v[31])                                                                              \
+      : "r"(addr))
+__device__ __forceinline__ float tc_rowmin(uint32_t tbase, int c0, int c1) {
+  float m0 = INFINITY, m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;  // independent chains
+  int col = c0;
+  for (; col + 32 <= c1;) {
+    uint32_t a[32];
+    LA_TC_LD32(a, tbase + (uint32_t)col);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      m0 = min3f(m0, __uint_as_float(a[j]), __uint_as_float(a[j + 1]));
+      m1 = min3f(m1, __uint_as_float(a[j + 2]), __uint_as_float(a[j + 3]));
+      m2 = min3f(m2, __uint_as_float(a[j + 4]), __uint_as_float(a[j + 5]));
+      m3 = min3f(m3, __uint_as_float(a[j + 6]), __uint_as_float(a[j + 7]));
+    }
+    col += 32;
+  }
+  for (; col < c1; col += 8) m0 = fminf(m0, tc_min8(tbase + (uint32_t)col));
+  return fminf(fminf(m0, m1), fminf(m2, m3));
+}
+
+
+// exact (direct-difference) minimum of |p - o_j|^2 over n points of o
+__device__ __forceinline__ float tc_direct_min(float2 p, const float2* o, int n) {
+  float m = INFINITY;
+  for (int j = 0; j < n; ++j) {
+    const float dx = p.x - o[j].x, dy = p.y - o[j].y;
+    m = fminf(m, fmaf(dy, dy, dx * dx));
+  }
+  return m;
+}
+
+// Warp-specialised pipeline, one CTA per SM (512 TMEM columns = two
+// 256-column accumulator slots):
+//   warp 8 (producer): TMA of raw curves and, from one elected lane, the
+//     MMAs; tile g = TPC c + t (curve c; t < MT1: query-row tiles, else
+//     curve-row tiles) goes into TMEM slot g & 1;
+//   warps 0-7 (epilogue): build each curve's operands (double-buffered),
+//     then per tile: warp w reads TMEM lanes 32 (w & 3).. for column half
+//     (w >> 2), row minima; warps w and w + 4 meet on a named barrier,
+//     warp w < 4 combines, rechecks small minima and accumulates.
+// Hand-offs are mbarriers: raw_full[4] (TMA, two curves ahead), op_full[2] (operands built),
+// op_empty[2] (last MMA of a curve done with its operands), tmem_full[2]
+// (MMA committed), tmem_empty[2] (8 epilogue warps done reading), raw_empty[4]
+// (epilogue done with a raw curve: TMA may refill it).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+constexpr int TC_GROUP_WARPS = 12;         // per epilogue group: 4 TMEM lane quarters x 3 column parts
+constexpr int TC_EPI_WARPS = 2 * TC_GROUP_WARPS;  // group 0 takes the even tiles (slot 0), group 1 the odd
+constexpr int TC_PRODUCER = TC_EPI_WARPS;      // warp index of the TMA/MMA warp
+constexpr int TC_SELECT = TC_EPI_WARPS + 1;    // warp index of the top-k warp
+constexpr int TC_CTA = (TC_EPI_WARPS + 2) * 32;
+constexpr int TC_RING = 4;                     // finished-curve ring (epilogue -> top-k warp)
+
+#ifdef LA_TC_PROF
+__device__ unsigned long long g_tc_prof[16];
+#define TCP_T0() long long _tp = clock64()
+#define TCP_ADD(i) do { long long _n = clock64(); atomicAdd(&g_tc_prof[i], (unsigned long long)(_n - _tp)); _tp = _n; } while (0)
+#else
+#define TCP_T0() do {} while (0)
+#define TCP_ADD(i) do {} while (0)
+#endif
+
+__global__ void __launch_bounds__(TC_CTA, 1) chamfer_tc_kernel(const ScanCtx c) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  unsigned char* qA = tsm;                 // query as A (rows = query points)
+  unsigned char* qB = tsm + TC_OP;         // query as B
+  unsigned char* cAb = tsm + 2 * TC_OP;    // curve as A, 3 buffers
+  unsigned char* cBb = tsm + 5 * TC_OP;    // curve as B, 3 buffers
+  auto raw = reinterpret_cast<float2(*)[PMAX]>(tsm + 8 * TC_OP);                          // [4][PMAX]
+  float2* qc = reinterpret_cast<float2*>(tsm + 8 * TC_OP + 4 * PMAX * sizeof(float2));    // centred query
+  float* part = reinterpret_cast<float*>(tsm + 8 * TC_OP + 5 * PMAX * sizeof(float2));    // [2][2][2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(part + 1024);
+  uint64_t* raw_full = bars;        // [4]
+  uint64_t* raw_empty = bars + 4;   // [4]
+  uint64_t* op_full = bars + 8;     // [3]
+  uint64_t* op_empty = bars + 11;   // [3]
+  uint64_t* tm_full = bars + 14;    // [2]
+  uint64_t* tm_empty = bars + 16;   // [2]
+  uint64_t* ring_full = bars + 18;  // [TC_RING]
+  uint64_t* ring_empty = bars + 22; // [TC_RING]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
+  float* red = reinterpret_cast<float*>(tmem_slot + 2);  // [TC_RING][2 groups][4 quarters][2] sums
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qi = blockIdx.y;
+  const la_chamfer_args& A = c.a;
+  const int P = A.P, Qn = A.Q;
+  const int N1 = (P + 15) & ~15, N2 = (Qn + 15) & ~15;
+  const int MT1 = (Qn + 127) / 128, MT2 = (P + 127) / 128;
+  const int TPC = MT1 + MT2;
+  const float2* qsrc = reinterpret_cast<const float2*>(A.queries) + (size_t)qi * Qn;
+  const int first = (int)(A.pos_begin + blockIdx.x);
+  const int stride = (int)gridDim.x;
+  const int count = first < A.pos_end ? (int)((A.pos_end - first + stride - 1) / stride) : 0;
+  const uint32_t bytes = (uint32_t)P * 8u;
+  auto rec_of = [&](long long pos) -> long long { return A.order ? A.order[pos] : pos; };
+
+  for (int r = tid; r < 256; r += TC_CTA) {
+    const bool real = r < Qn;
+    float2 q = make_float2(0.f, 0.f);
+    if (real) {
+      q = qsrc[r];
+      q.x -= 0.5f;
+      q.y -= 0.5f;
+      qc[r] = q;
+    }
+    tc_rows(r < 128 * MT1 ? qA : nullptr, r < N2 ? qB : nullptr, r, real, q.x, q.y);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], TC_EPI_WARPS);
+    }
+    for (int i = 0; i < TC_RING; ++i) {
+      mbar_init(&ring_full[i], 8);
+      mbar_init(&ring_empty[i], 1);
+    }
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&op_full[i], TC_EPI_WARPS);
+      mbar_init(&op_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tm_full[i], 1);
+      mbar_init(&tm_empty[i], TC_GROUP_WARPS);
+    }
+    fence_mbar_init();
+  }
+  fence_proxy_async();  // query operands -> async proxy
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == TC_SELECT) {
+    // ------------------------------------------------ top-k warp
+    WarpList top, hit;
+    list_init(top);
+    list_init(hit);
+    long long nhit = 0;
+    uint32_t rf = 0;
+    for (int ci = 0; ci < count; ++ci) {
+      const int rs = ci % TC_RING;
+      mbar_wait(&ring_full[rs], (rf >> rs) & 1u);
+      rf ^= 1u << rs;
+      const float* rr = red + rs * 16;
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // fixed order: group 0 quarters 0-3, then group 1
+        s0 += rr[2 * k];
+        s1 += rr[2 * k + 1];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring_empty[rs]);
+      const float d = s0 / (float)Qn + s1 / (float)P;
+      const long long pos = first + (long long)ci * stride;
+      const long long id = rec_of(pos);
+      if (id != A.exclude_id) {
+        if (A.all_d && lane == 0) A.all_d[(size_t)qi * A.N + id] = d;
+        const long long rpos = A.pos_map ? A.pos_map[pos] : pos + A.pos_base;
+        consider(top, hit, nhit, c, lane, d, rpos, id + A.id_base);
+      }
+    }
+    flush_lists(c, qi, blockIdx.x, lane, top, hit, nhit);
+  } else if (warp == TC_PRODUCER) {
+    // ------------------------------------------------ producer warp
+    // raw curves are prefetched two ahead into four buffers (a buffer is
+    // refilled once the epilogue released the curve it held, 4 curves back)
+    if (lane == 0) {
+      uint32_t re_ph = 0, of_ph = 0, te_ph = 0;
+      auto tma = [&](int ci) {
+        const int rb = ci & 3;
+        if (ci >= 4) {
+          mbar_wait(&raw_empty[rb], (re_ph >> rb) & 1u);
+          re_ph ^= 1u << rb;
+        }
+        mbar_expect_tx(&raw_full[rb], bytes);
+        tma_load_1d(&raw[rb][0], A.db + (size_t)rec_of(first + (long long)ci * stride) * P * 2, bytes, &raw_full[rb]);
+      };
+      if (count > 0) tma(0);
+      if (count > 1) tma(1);
+      int g = 0;
+      for (int ci = 0; ci < count; ++ci) {
+        if (ci + 2 < count) tma(ci + 2);
+        const int b = ci % 3;
+        TCP_T0();
+        mbar_wait(&op_full[b], (of_ph >> b) & 1u);  // operands of curve ci built
+        of_ph ^= 1u << b;
+        TCP_ADD(0);
+        tc_fence_after();
+        for (int t = 0; t < TPC; ++t, ++g) {
+          const int slot = g & 1;
+          if (g >= 2) {
+            TCP_T0();
+            mbar_wait(&tm_empty[slot], (te_ph >> slot) & 1u);
+            te_ph ^= 1u << slot;
+            tc_fence_after();
+            TCP_ADD(1);
+          }
+          const uint32_t d = tmem + (uint32_t)(slot * 256);
+          if (t < MT1)
+            tc_mma(d, smem_u32(qA) + t * 8192, smem_u32(cBb + b * TC_OP), N1);
+          else
+            tc_mma(d, smem_u32(cAb + b * TC_OP) + (t - MT1) * 8192, smem_u32(qB), N2);
+          tc_commit(&tm_full[slot]);
+        }
+        tc_commit(&op_empty[b]);  // fires when all MMAs of curve ci are complete
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ epilogue warps
+    uint32_t rf_ph = 0, oe_ph = 0, tf_ph = 0, re_ph = 0;
+    const int grp = warp / TC_GROUP_WARPS, gw = warp % TC_GROUP_WARPS;
+    const int quarter = gw & 3, half = gw >> 2;  // half = column part 0..2 (0: combiner warp)
+    auto build = [&](int ci) {
+      const int b = ci % 3, rb = ci & 3;
+      mbar_wait(&raw_full[rb], (rf_ph >> rb) & 1u);
+      rf_ph ^= 1u << rb;
+      if (ci >= 3) {  // MMAs of curve ci - 3 done with operand buffer b
+        mbar_wait(&op_empty[b], (oe_ph >> b) & 1u);
+        oe_ph ^= 1u << b;
+      }
+      const float2* cur = &raw[rb][0];
+      unsigned char* cA = cAb + b * TC_OP;
+      unsigned char* cB = cBb + b * TC_OP;
+      for (int r = tid; r < 256; r += TC_EPI_WARPS * 32) {
+        const bool real = r < P;
+        float2 p = make_float2(0.f, 0.f);
+        if (real) {
+          p = cur[r];
+          p.x -= 0.5f;
+          p.y -= 0.5f;
+        }
+        tc_rows(r < 128 * MT2 ? cA : nullptr, r < N1 ? cB : nullptr, r, real, p.x, p.y);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&op_full[b]);
+        if (half) mbar_arrive(&raw_empty[rb]);  // column-half warps never read raw curve ci again
+      }
+    };
+    if (count > 0) build(0);
+    int g = 0;
+    float sum0 = 0.f, sum1 = 0.f;
+    for (int ci = 0; ci < count; ++ci) {
+      TCP_T0();
+      if (ci + 1 < count) build(ci + 1);  // overlaps this curve's MMAs
+      if (warp == 0 && lane == 0) TCP_ADD(2);
+      const float2* cur = &raw[ci & 3][0];
+      for (int t = 0; t < TPC; ++t, ++g) {
+        if ((g & 1) != grp) continue;  // the other group's tile
+        const int dir = t < MT1 ? 0 : 1, mt = dir == 0 ? t : t - MT1;
+        const int NN = dir == 0 ? N1 : N2, rows = dir == 0 ? Qn : P;
+        const int slot = g & 1;
+#ifdef LA_TC_PROF
+        long long _tp = clock64();
+#endif
+        mbar_wait(&tm_full[slot], (tf_ph >> slot) & 1u);
+        tf_ph ^= 1u << slot;
+        tc_fence_after();
+        if (warp == 0 && lane == 0) TCP_ADD(3);
+        const int ncol8 = NN >> 3, c0 = ((ncol8 * half) / 3) << 3, c1 = ((ncol8 * (half + 1)) / 3) << 3;
+        const uint32_t tbase = tmem + (uint32_t)(slot * 256) + ((uint32_t)(quarter * 32) << 16);
+        const float m = tc_rowmin(tbase, c0, c1);
+        if (warp == 0 && lane == 0) TCP_ADD(4);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tm_empty[slot]);  // TMEM slot may be overwritten
+        float* pp = part + (grp * 2 + ((g >> 1) & 1)) * 2 * 128;  // per group, double-buffered
+        if (half) pp[(half - 1) * 128 + quarter * 32 + lane] = m;
+        named_sync(1 + grp * 4 + quarter, 96);  // the 3 column-part warps of this lane quarter
+        if (warp == 0 && lane == 0) TCP_ADD(5);
+        if (!half) {
+          const int row = mt * 128 + quarter * 32 + lane;
+          const bool real = row < rows;
+          const float mo = fminf(pp[quarter * 32 + lane], pp[128 + quarter * 32 + lane]);
+          float mm = real ? fminf(m, mo) : INFINITY;
+          unsigned need = __ballot_sync(FULL, real && mm < TC_RECHECK);
+#ifdef LA_TC_PROF
+          if (lane == 0) atomicAdd(&g_tc_prof[7], (unsigned long long)__popc(need));
+          if (lane == 0) atomicAdd(&g_tc_prof[8], 1ull);
+#endif
+          while (__builtin_expect(need != 0u, 0)) {  // cancellation zone: direct differences, the warp sweeping the other side
+            const int src = __ffs(need) - 1;
+            need &= need - 1;
+            const int rr = mt * 128 + quarter * 32 + src;
+            const float2 pt = dir == 0 ? qc[rr] : make_float2(cur[rr].x - 0.5f, cur[rr].y - 0.5f);
+            const int no = dir == 0 ? P : Qn;
+            float e = INFINITY;
+            for (int j = lane; j < no; j += 32) {
+              const float2 o = dir == 0 ? make_float2(cur[j].x - 0.5f, cur[j].y - 0.5f) : qc[j];
+              const float dx = pt.x - o.x, dy = pt.y - o.y;
+              e = fminf(e, fmaf(dy, dy, dx * dx));
+            }
+            for (int o = 16; o > 0; o >>= 1) e = fminf(e, __shfl_xor_sync(FULL, e, o));
+            if (lane == src) mm = e;
+          }
+          if (real) {  // MUFU square root (2^-22 relative): far inside the 1e-4 tolerance
+            float r;
+            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(mm, 0.f)));
+            if (dir == 0) sum0 += r;
+            else sum1 += r;
+          }
+          if (warp == 0 && lane == 0) TCP_ADD(6);
+        }
+      }
+      // curve ci complete: the combiner warps (0-3) hand their sums to the top-k warp
+      if (!half) {
+        const float s0 = warp_sum(sum0), s1 = warp_sum(sum1);
+        const int rs = ci % TC_RING;
+        if (ci >= TC_RING) {
+          mbar_wait(&ring_empty[rs], (re_ph >> rs) & 1u);
+          re_ph ^= 1u << rs;
+        }
+        if (lane == 0) {
+          red[rs * 16 + (grp * 4 + quarter) * 2] = s0;
+          red[rs * 16 + (grp * 4 + quarter) * 2 + 1] = s1;
+          mbar_arrive(&ring_full[rs]);
+          mbar_arrive(&raw_empty[ci & 3]);  // rechecks of curve ci are done
+        }
+      }
+      sum0 = sum1 = 0.f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
 // ------------------------------------------------------------ generic path
 // one CTA per (scan position, query): any P, Q; distances to a dense buffer
 __global__ void __launch_bounds__(256) chamfer_generic_kernel(const la_chamfer_args A, float* dense) {
@@ -712,6 +1182,22 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
   w = static_cast<unsigned char*>(a->ws) + align_up(p.ws_lists);
   c.dense = a->all_d ? a->all_d : reinterpret_cast<float*>(w);
   const dim3 grid(p.grid, a->NQ);
+  if (p.fast && (a->flags & LA_CH_TENSOR) && (a->P % 2) == 0) {
+    // one list per CTA: one CTA per SM (512 TMEM columns), grid split over the queries
+    int sms = sm_count();
+    long long want = a->pos_end - a->pos_begin;
+    long long g = (long long)sms;
+    if (a->NQ > 1) g = (g + a->NQ - 1) / a->NQ;
+    if (g > want) g = want;
+    if (g < 1) g = 1;
+    if (g > p.nwarps) g = p.nwarps;  // list workspace is sized for p.nwarps lists per query
+    ScanCtx ct = c;
+    ct.nwarps_total = (int)g;
+    cudaFuncSetAttribute(chamfer_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
+    chamfer_tc_kernel<<<dim3((unsigned)g, a->NQ), TC_CTA, TC_SMEM, s>>>(ct);
+    if (a->k > 0) merge_kernel<<<a->NQ, 1024, 0, s>>>(ct);
+    return cuda_status("la_chamfer_topk (tensor)");
+  }
   if (p.fast) {
     switch (p.qs) {
 #define LA_CASE(QSV)                                                                                   \
@@ -741,3 +1227,15 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
 }
 
 }  // extern "C"
+
+#ifdef LA_TC_PROF
+extern "C" int la_tc_prof_read(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, la::g_tc_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(la::g_tc_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

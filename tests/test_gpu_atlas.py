@@ -203,3 +203,37 @@ def test_chamfer_expansion_mode_bound(torch):
     b = chamfer_scan(db, q, k=4, dense=True, expansion=False)["all_d"].cpu().numpy()
     assert np.max(np.abs(a - b)) <= 5e-5 + 1e-6
     assert a[0, 0] == 0.0 and a[2, 2] == 0.0
+
+
+def test_chamfer_tensor_core_path(torch):
+    """LA_CH_TENSOR (tcgen05 3xTF32 squared distances + direct recheck of
+    small minima) agrees with the direct-difference kernel within the 1e-4
+    tolerance, returns exact zeros for duplicated curves and the same top-k
+    records on a Fourier database with planted duplicates."""
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    db = fourier_db(20_000, 200, seed=4001)
+    q = fourier_db(3, 200, seed=998)
+    db[5] = q[0]
+    db[17] = q[0]
+    for P, Q in ((200, 200), (64, 200), (200, 37), (128, 128)):
+        d_ = db[:, :P].contiguous()
+        q_ = q[:, :Q].contiguous()
+        a = chamfer_scan(d_, q_, k=10, dense=True)
+        b = chamfer_scan(d_, q_, k=10, dense=True, tensor=True)
+        da, dt = a["all_d"].cpu().numpy(), b["all_d"].cpu().numpy()
+        assert np.max(np.abs(da - dt)) <= 1e-4, (P, Q)
+        if P == 200 and Q == 200:
+            assert dt[0, 5] == 0.0 and dt[0, 17] == 0.0
+        # same records up to swaps of entries closer than the tolerance
+        for qi in range(3):
+            ia, ib = a["top_id"][qi].cpu().numpy(), b["top_id"][qi].cpu().numpy()
+            for x, y in zip(ia, ib):
+                if x != y:
+                    assert abs(da[qi, x] - da[qi, y]) <= 2e-4
+    # thresholded hits and an excluded record
+    a = chamfer_scan(db, q, k=5, threshold=0.08, exclude_id=5)
+    b = chamfer_scan(db, q, k=5, threshold=0.08, exclude_id=5, tensor=True)
+    assert torch.equal(a["n_hits"], b["n_hits"])
+    assert torch.equal(a["hit_id"], b["hit_id"])

@@ -1,0 +1,20 @@
+import os, sys, ctypes as C
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2208_14567_b200 import _native as N
+from paper_2208_14567_b200.atlas import chamfer_scan
+from paper_2208_14567_b200.workloads import fourier_db
+lib = N.load()
+db = fourier_db(200_000, 200, seed=4000)
+q = fourier_db(1, 200, seed=999)
+chamfer_scan(db, q, k=10, tensor=True)
+buf = (C.c_ulonglong * 16)()
+lib.la_tc_prof_read(buf, 1)
+chamfer_scan(db, q, k=10, tensor=True)
+lib.la_tc_prof_read(buf, 0)
+names = ["prod wait op_full", "prod wait tm_empty", "epi build", "epi wait tm_full", "epi rowmin", "epi exchange", "epi combine"]
+ncur = 200_000 / 148
+for i, n in enumerate(names):
+    per = buf[i] / 148 / ncur  # per curve per CTA (warp 0 / producer)
+    print(f"{n:22s} {per:10.0f} cycles/curve")
+print("rechecked rows per curve:", buf[7] / 200_000, " combine calls per curve:", buf[8] / 200_000)

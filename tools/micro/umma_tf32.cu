@@ -105,6 +105,59 @@ __global__ void umma_test(const float* A, const float* B, float* D, int swap_lbo
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(256));
 }
 
+__global__ void umma_rate(const float* A, const float* B, long long* cyc, int reps, int n_cols) {
+  __shared__ __align__(1024) unsigned char sa[M * K * 4];
+  __shared__ __align__(1024) unsigned char sb[256 * K * 4];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < M * K; i += blockDim.x) *reinterpret_cast<float*>(sa + kmajor_off(i / K, i % K)) = A[i];
+  for (int i = tid; i < 256 * K; i += blockDim.x)
+    *reinterpret_cast<float*>(sb + kmajor_off(i / K, i % K)) = B[i % (N * K)];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "n"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    const uint32_t idesc = idesc_tf32(M, n_cols);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int ks = 0; ks < K / 8; ++ks) {
+        const uint64_t ad = smem_desc(smem_u32(sa) + ks * 256, 128, (K / 4) * 128);
+        const uint64_t bd = smem_desc(smem_u32(sb) + ks * 256, 128, (K / 4) * 128);
+        const uint32_t acc = (r | ks) > 0;
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+            " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar)));
+    asm volatile(
+        "{\n .reg .pred P1;\n W2:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra W2;\n}\n" ::"r"(smem_u32(&bar)),
+        "r"(0));
+    cyc[0] = clock64() - t0;
+    // single tile latency
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar)));
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(256));
+}
+
 int main() {
   std::vector<float> A(M * K), B(N * K), D(M * N), R(M * N);
   srand(1);
@@ -142,6 +195,18 @@ int main() {
     }
     printf("swap_lbo_sbo=%d: max |D - ref| = %g, %d / %d mismatches; D[0]=%g ref %g, D[last]=%g ref %g\n", swap,
            maxerr, bad, M * N, D[0], R[0], D[M * N - 1], R[M * N - 1]);
+  }
+  long long* dc;
+  cudaMalloc(&dc, 8);
+  for (int n : {208, 256}) {
+    for (int reps : {1, 16, 256}) {
+      umma_rate<<<1, 128>>>(dA, dB, dc, reps, n);
+      cudaDeviceSynchronize();
+      long long cy;
+      cudaMemcpy(&cy, dc, 8, cudaMemcpyDeviceToHost);
+      const double macs = (double)reps * M * n * K;
+      printf("N=%d reps=%d: %lld cycles, %.1f MAC/clk (tile = %d MACs)\n", n, reps, cy, macs / cy, M * n * K);
+    }
   }
   return 0;
 }
