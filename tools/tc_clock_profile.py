@@ -1,3 +1,5 @@
+"""In-kernel clock64 breakdown of chamfer_tc_kernel (needs a build with -DLA_TC_PROF,
+e.g. tools/build_variants.sh PROF \"-DLA_TC_PROF\" and copying the .so over _lib/)."""
 import os, sys, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

@@ -1,3 +1,4 @@
+"""Workload for ncu captures of the tensor-core chamfer kernel (100k Fourier curves)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
