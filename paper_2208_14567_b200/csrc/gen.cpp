@@ -564,6 +564,10 @@ int64_t layout(Engine& E, int32_t lookahead, int64_t cap, la_plan* plans, int32_
       la::set_error("la_gen_window: one window (%lld) exceeds cap %lld", (long long)need, (long long)cap);
       return LA_EWS;
     }
+    if (!plans) {
+      la::set_error("la_gen_window: null plan table");
+      return LA_EINVAL;
+    }
     S.plan_slot = np;
     plans[np++] = to_rec(S.mech, S.plan);
     S.win.swap(w);
@@ -614,10 +618,18 @@ void la_gen_destroy(void* h) { delete static_cast<Engine*>(h); }
 // candidate count, 0 when every slot is done, <0 on error.
 int64_t la_gen_window(void* h, int32_t lookahead, int64_t cap, int32_t threads, double* pos, int32_t* cand_plan,
                       la_plan* plans, int32_t* n_plans) {
+  if (!h || !n_plans) {
+    la::set_error("la_gen_window: null argument");
+    return LA_EINVAL;
+  }
   Engine& E = *static_cast<Engine*>(h);
   std::vector<Slot*> act;
   const int64_t total = layout(E, lookahead, cap, plans, n_plans, act);
   if (total <= 0) return total;
+  if (!pos || !cand_plan) {
+    la::set_error("la_gen_window: null pose buffer");
+    return LA_EINVAL;
+  }
   parallel_for((int64_t)act.size(), threads, [&](int64_t a) {
     Slot& S = *act[a];
     Pcg64 r = S.pos;
@@ -638,10 +650,18 @@ int64_t la_gen_window(void* h, int32_t lookahead, int64_t cap, int32_t threads, 
 // la_gen_poses.  Candidate c of a batch uses stream draws [2nc, 2n(c+1)).
 int64_t la_gen_window_dev(void* h, int32_t lookahead, int64_t cap, la_gen_batch* batches, int64_t max_batches,
                           int64_t* n_batches, la_plan* plans, int32_t* n_plans) {
+  if (!h || !n_batches || !n_plans) {
+    la::set_error("la_gen_window_dev: null argument");
+    return LA_EINVAL;
+  }
   Engine& E = *static_cast<Engine*>(h);
   std::vector<Slot*> act;
   const int64_t total = layout(E, lookahead, cap, plans, n_plans, act);
   if (total <= 0) return total;
+  if (!batches) {
+    la::set_error("la_gen_window_dev: null descriptor buffer");
+    return LA_EINVAL;
+  }
   int64_t nb = 0;
   for (Slot* S : act)
     for (auto& b : S->win) {
@@ -669,6 +689,10 @@ int64_t la_gen_window_dev(void* h, int32_t lookahead, int64_t cap, la_gen_batch*
 // Walk the device flags of the last window in each slot's stream order:
 // first_t[c] == T_high -> valid; low_t[c] >= 0 -> locked at T_low (step).
 int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int32_t* low_t) {
+  if (!h || !first_t || !low_t) {
+    la::set_error("la_gen_consume: null argument");
+    return LA_EINVAL;
+  }
   Engine& E = *static_cast<Engine*>(h);
   const la_gen_cfg& cfg = E.cfg;
   // pose of candidate c of batch b: from the window buffer, or redrawn from
@@ -763,6 +787,10 @@ int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int
 }
 
 int64_t la_gen_count(void* h, int32_t what) {
+  if (!h) {
+    la::set_error("la_gen_count: null engine");
+    return LA_EINVAL;
+  }
   Engine& E = *static_cast<Engine*>(h);
   int64_t n = 0;
   if (what == 0)
@@ -775,6 +803,10 @@ int64_t la_gen_count(void* h, int32_t what) {
 // records in slot order: meta [R][4] (slot, variant, attempts, n), poses
 // [R][20][2], plans [R], adjacency [R][20][20], types [R][20]
 int la_gen_records(void* h, int64_t* meta, double* pos, la_plan* plans, uint8_t* adj, int8_t* types) {
+  if (!h || !meta || !pos || !plans || !adj || !types) {
+    la::set_error("la_gen_records: null argument");
+    return LA_EINVAL;
+  }
   Engine& E = *static_cast<Engine*>(h);
   int64_t r = 0;
   for (auto& v : E.slot_records)
@@ -798,6 +830,10 @@ int la_gen_records(void* h, int64_t* meta, double* pos, la_plan* plans, uint8_t*
 
 // negatives in slot order: meta [R][3] (slot, locking step, n), poses [R][20][2]
 int la_gen_negatives(void* h, int64_t* meta, double* pos, uint8_t* adj, int8_t* types) {
+  if (!h || !meta || !pos || !adj || !types) {
+    la::set_error("la_gen_negatives: null argument");
+    return LA_EINVAL;
+  }
   Engine& E = *static_cast<Engine*>(h);
   int64_t r = 0;
   for (auto& v : E.slot_negs)
@@ -819,6 +855,10 @@ int la_gen_negatives(void* h, int64_t* meta, double* pos, uint8_t* adj, int8_t* 
 
 // stats: out [21][2] simulated / accepted by joint count; *discarded
 int la_gen_stats(void* h, int64_t* out, int64_t* discarded) {
+  if (!h || !out || !discarded) {
+    la::set_error("la_gen_stats: null argument");
+    return LA_EINVAL;
+  }
   Engine& E = *static_cast<Engine*>(h);
   for (int n = 0; n <= LA_MAX_JOINTS; ++n) out[2 * n] = out[2 * n + 1] = 0;
   int64_t disc = 0;
