@@ -148,7 +148,8 @@ __device__ __forceinline__ double rsqrt_f64(double x) {
 // Newton-refined MUFU reciprocal square roots (a few ulp from numpy; the
 // lock decision can differ only for margins within ~1e-15).
 template <bool EXACT, typename Get, typename Put>
-__device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get get, Put put) {
+__device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get get, Put put,
+                                         double* margin = nullptr) {
   const double eps = 1e-9;
 #pragma unroll 1
   for (int s = 0; s < C.ns; ++s) {
@@ -175,6 +176,8 @@ __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get
       const double d2 = fma(dy, dy, dx * dx);
       const double inv = rsqrt_f64(d2);
       const double d = d2 * inv;
+      if (margin)  // distance of every lock test from its threshold (the exact-mode triage)
+        *margin = fmin(*margin, fmin(fabs(d - eps), fmin(fabs(hl.x - d), fabs(d - hl.y))));
       const bool lock = !(d >= eps) | (d > hl.x) | (d < hl.y);
       if (lock) return s;
       const double x = fma(d, d, rr.x - rr.y) * (0.5 * inv);
@@ -196,6 +199,13 @@ __device__ __forceinline__ double2 crank_tip(const WarpHead& H, const SimCtx& C,
 
 // rare path of the fp32 screen: the whole angle again in f64, positions in
 // a lane-private array; rounded results go back to the fp32 column
+// Exact mode triages: a fast f64 pass first; only when one of its lock
+// tests comes within kExactTriage of its threshold (fast and exact f64
+// differ by a few ulp, amplified at most ~1e8-fold below that margin) is
+// the angle redone in the exact arithmetic.  The lock decision is therefore
+// the exact one, at fast-pass cost for almost every replay.
+constexpr double kExactTriage = 1e-7;
+
 template <bool EXACT>
 __device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, double ct, double st) {
   double2 q[NJ];
@@ -207,11 +217,17 @@ __device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, dou
   }
   q[1] = crank_tip(H, C, ct, st);
   W.p32(1) = make_float2((float)q[1].x, (float)q[1].y);
-  return dyads_f64<EXACT>(H, C, [&](int j) { return q[j]; },
-                   [&](int j, double2 v) {
-                     q[j] = v;
-                     W.p32(j) = make_float2((float)v.x, (float)v.y);
-                   });
+  auto get = [&](int j) { return q[j]; };
+  auto put = [&](int j, double2 v) {
+    q[j] = v;
+    W.p32(j) = make_float2((float)v.x, (float)v.y);
+  };
+  if (EXACT) {
+    double margin = INFINITY;
+    const int lk = dyads_f64<false>(H, C, get, put, &margin);
+    if (margin > kExactTriage) return lk;
+  }
+  return dyads_f64<EXACT>(H, C, get, put);
 }
 
 // fp32 angle evaluation with f64 fix-up.  A lane whose dyad margin
