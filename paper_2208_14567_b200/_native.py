@@ -29,6 +29,9 @@ LA_SIM_SCATTER = 64
 LA_SIM_WRITE_ONLY = 128
 LA_SIM_EXACT64 = 256
 LA_PENDING = -3
+LA_EINVAL = -1
+LA_ERANGE = -2
+LA_EWS = -3
 
 LA_CH_EXPANSION = 1
 LA_CH_SCALAR_PIPE = 2

@@ -213,3 +213,21 @@ def test_moving_joint_rows_follow_cli_normalize(golden):
             want.append((row0[i] + j, meta[i, 0] * cfg.variants + meta[i, 1], j, bool((types[i, nbrs] == 0).any())))
     got = list(zip(rows.tolist(), mids.tolist(), jids.tolist(), arc.tolist()))
     assert got == [tuple(int(x) if k < 3 else x for k, x in enumerate(w)) for w in want]
+
+
+def test_engine_infeasible_size_raises():
+    """n = 4 has no valid topology (SURVEY probe P0): the reference raises
+    GenerationError from sample_topology; the engine reports LA_ERANGE with
+    the same message shape on its first window."""
+    lib = N.load()
+    cfg = N.LaGenCfg(0, 4, 4, 0.25, 5, 50, 200, 5000, 50, 256, 0.0, 1, 0)
+    eng = lib.la_gen_create(C.byref(cfg), 0, 2)
+    assert eng
+    n_plans = C.c_int32(0)
+    pos = np.zeros((1024, NMAX, 2))
+    plan = np.zeros(1024, dtype=np.int32)
+    plans = (N.LaPlan * 2)()
+    rc = lib.la_gen_window(eng, 1, 1024, 1, pos.ctypes.data, plan.ctypes.data, plans, C.byref(n_plans))
+    assert rc == N.LA_ERANGE
+    assert "no valid topology with n=4" in N.last_error()
+    lib.la_gen_destroy(eng)

@@ -110,3 +110,11 @@ def test_host_and_device_windows_agree(golden):
     assert [(r.slot, r.variant, r.attempts) for r in ra] == [(r.slot, r.variant, r.attempts) for r in rb]
     assert all(np.array_equal(x.mechanism.positions0, y.mechanism.positions0) for x, y in zip(ra, rb))
     assert [x.locking_step for x in a.negatives] == [x.locking_step for x in b.negatives]
+
+
+def test_generation_error_like_reference():
+    """No valid topology for n = 4 (reference: GenerationError)."""
+    from paper_2208_14567_b200.generator import GenerationError
+
+    with pytest.raises(GenerationError, match="n=4"):
+        list(GenerationRun(GenerationConfig(count=2, n_min=4, n_max=4, topology_retries=20)).records())
