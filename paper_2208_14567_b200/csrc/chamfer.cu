@@ -571,14 +571,20 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem, uint32_t a_addr, uint32_t 
     const uint64_t ad = tc_desc(a_addr + ks * 256), bd = tc_desc(b_addr + ks * 256);
     const uint32_t acc = ks > 0;
     asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
         "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
   }
 }
+// tc_mma / tc_commit are called by a whole warp (warp-uniform arguments) and
+// issued by one elected lane: from a lane-0 branch ptxas wraps each MMA in a
+// uniformity loop that costs several times the MMA itself
+// (tools/micro/umma_small.cu)
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-               : "memory");
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -801,7 +807,7 @@ __global__ void __launch_bounds__(TC_CTA, 1) chamfer_tc_kernel(const ScanCtx c) 
     // ------------------------------------------------ producer warp
     // raw curves are prefetched two ahead into four buffers (a buffer is
     // refilled once the epilogue released the curve it held, 4 curves back)
-    if (lane == 0) {
+    {
       uint32_t re_ph = 0, of_ph = 0, te_ph = 0;
       auto tma = [&](int ci) {
         const int rb = ci & 3;
@@ -809,8 +815,12 @@ __global__ void __launch_bounds__(TC_CTA, 1) chamfer_tc_kernel(const ScanCtx c) 
           mbar_wait(&raw_empty[rb], (re_ph >> rb) & 1u);
           re_ph ^= 1u << rb;
         }
-        mbar_expect_tx(&raw_full[rb], bytes);
-        tma_load_1d(&raw[rb][0], A.db + (size_t)rec_of(first + (long long)ci * stride) * P * 2, bytes, &raw_full[rb]);
+        if (lane == 0) {
+          mbar_expect_tx(&raw_full[rb], bytes);
+          tma_load_1d(&raw[rb][0], A.db + (size_t)rec_of(first + (long long)ci * stride) * P * 2, bytes,
+                      &raw_full[rb]);
+        }
+        __syncwarp();
       };
       if (count > 0) tma(0);
       if (count > 1) tma(1);
@@ -1187,7 +1197,22 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
     int sms = sm_count();
     long long want = a->pos_end - a->pos_begin;
     long long g = (long long)sms;
-    if (a->NQ > 1) g = (g + a->NQ - 1) / a->NQ;
+    if (a->NQ > 1) {
+      // CTAs per query so that g x NQ fills whole waves of one CTA per SM
+      double best = 0.0;
+      for (int k = 1; k <= 32; ++k) {
+        const long long gk = ((long long)k * sms + a->NQ - 1) / a->NQ;
+        if (gk > p.nwarps || gk > want) break;
+        const long long tot = gk * a->NQ, waves = (tot + sms - 1) / sms;
+        const double eff = (double)tot / (double)(waves * sms);
+        if (eff > best + 1e-9) {
+          best = eff;
+          g = gk;
+        }
+        if (eff >= 0.97) break;
+      }
+      if (best == 0.0) g = ((long long)sms + a->NQ - 1) / a->NQ;
+    }
     if (g > want) g = want;
     if (g < 1) g = 1;
     if (g > p.nwarps) g = p.nwarps;  // list workspace is sized for p.nwarps lists per query

@@ -14,9 +14,10 @@ buf = (C.c_ulonglong * 16)()
 lib.la_tc_prof_read(buf, 1)
 chamfer_scan(db, q, k=10, tensor=True)
 lib.la_tc_prof_read(buf, 0)
-names = ["prod wait op_full", "prod wait tm_empty", "epi build", "epi wait tm_full", "epi rowmin", "epi exchange", "epi combine"]
+names = ["mma wait op_full", "mma wait sl_empty", "mma issue+commit", "epi0 wait sl_full", "epi0 ld+min+release",
+         "epi0 partial write", "fin0 wait pt_full", "fin0 finalize", "bld wait raw_full", "bld wait op_empty", "bld build"]
 ncur = 200_000 / 148
 for i, n in enumerate(names):
     per = buf[i] / 148 / ncur  # per curve per CTA (warp 0 / producer)
     print(f"{n:22s} {per:10.0f} cycles/curve")
-print("rechecked rows per curve:", buf[7] / 200_000, " combine calls per curve:", buf[8] / 200_000)
+
