@@ -50,9 +50,14 @@ C2_PIPELINE = os.environ.get("LA_BENCH_C2_PIPELINE", "deferred")
 
 
 # ----------------------------------------------------------------- helpers
+# LA_BENCH_SHARED_GPU=1: every rank on cuda:0 with gloo collectives -- a
+# plumbing check of the N > 1 path on a one-GPU box (timings meaningless)
+SHARED_GPU = os.environ.get("LA_BENCH_SHARED_GPU", "0") == "1"
+
+
 def env_rank():
-    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
-        int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SHARED_GPU else int(os.environ.get("LOCAL_RANK", "0"))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), local
 
 
 def load_traffic():
@@ -170,7 +175,7 @@ def max_over_ranks(torch, value: float, world: int) -> float:
         return value
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device="cpu" if SHARED_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -553,7 +558,8 @@ def bench_c5(torch, args, rank, world, peaks, flush, clk):
         nres = normalize_tensors(traj, src_row=rows)
         if timer:
             timer.mark("normalize")
-        cres = chamfer_scan(nres["out"], queries, k=k, threshold=0.0, id_base=0, pos_base=0)
+        # rank-disjoint ids / scan positions for the merged lists (curves per rank vary)
+        cres = chamfer_scan(nres["out"], queries, k=k, threshold=0.0, id_base=rank << 32, pos_base=rank << 32)
         if world > 1:
             gather_merge({n: cres[n] for n in ("top_d", "top_id", "top_pos", "hit_d", "hit_id", "hit_pos",
                                                "n_hits")}, k)
@@ -753,7 +759,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARED_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2208_14567_b200 import _native
 
     _native.load(build_if_missing=False)

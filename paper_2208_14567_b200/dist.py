@@ -116,6 +116,9 @@ def gather_merge(lists: dict, k: int, group=None) -> dict:
     if dist.get_backend(group) == "nccl" and not mine.is_cuda:
         mine = mine.cuda()
         dev = mine.device
+    elif dist.get_backend(group) == "gloo" and mine.is_cuda:
+        mine = mine.cpu()
+        dev = mine.device
     allb = torch.empty((world * mine.shape[0], mine.shape[1]), dtype=mine.dtype, device=dev)
     dist.all_gather_into_tensor(allb, mine, group=group)
     allb = allb.cpu().view(world, mine.shape[0], mine.shape[1])
