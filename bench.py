@@ -467,9 +467,13 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
         times.append(e0.elapsed_time(e1))
     e2e_ms = max_over_ranks(torch, statistics.mean(times), world)
     pre = prefilter_c4(torch, args, db, q, flush, stream)
+    cpu = None
+    if rank == 0 and world == 1 and "cpu" not in set(filter(None, args.skip.split(","))):
+        cpu = cpu_baseline_c4(db, q)
     del db
     return {"metric": CHAMFER_METRIC, "prefilter": pre, "value": world * C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s",
             "ms_per_step": ms, "roofline": rl, "launches_per_step": 2,
+            "cpu_baseline": cpu,
             "e2e": {"value": world * C4_COUNT / (e2e_ms / 1e3), "unit": "curve-pairs/s",
                     "h2d_bytes_per_step": C4_P * 8, "d2h_bytes_per_step": k * 12},
             "config": {"workload": "C4: 1 query vs 10M normalised Fourier curves/GPU (5 harmonics, "
@@ -715,6 +719,46 @@ def cpu_baseline_c2(mb, budget_s: float = 15.0, max_groups: int | None = None):
                       f"simulate_batch, fork pool x{cores}", "seconds": dt, "one_thread_est": 1.0 / per}
 
 
+def _cpu_chamfer_worker(args):
+    pts, q = args
+    from threadpoolctl import threadpool_limits
+
+    from oracle import links_oracle as O
+
+    with threadpool_limits(1):
+        for c0 in range(0, len(pts), 512):
+            O.chamfer_expansion_block(pts[c0:c0 + 512], q)
+    return len(pts)
+
+
+def cpu_baseline_c4(db, q, budget_s: float = 8.0):
+    """Oracle port of _chamfer_block (atlas.py:45-55, expansion GEMM in f64)
+    over a bounded prefix of the C4 database, fork pool of all host cores,
+    one BLAS thread per worker."""
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    qh = q[0].double().cpu().numpy()
+    probe = db[:512].double().cpu().numpy()
+    t0 = time.perf_counter()
+    _cpu_chamfer_worker((probe, qh))
+    per = (time.perf_counter() - t0) / len(probe)
+    want = int(budget_s * cores / max(per, 1e-12))
+    want = max(cores * 512, min(want // (cores * 512) * (cores * 512), db.shape[0]))
+    sample = db[:want].double().cpu().numpy()
+    chunks = np.array_split(sample, cores)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_chamfer_worker, [(probe[:8], qh)] * cores)
+        t0 = time.perf_counter()
+        done = sum(pool.map(_cpu_chamfer_worker, [(c, qh) for c in chunks]))
+        dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "curve-pairs/s", "cores": cores, "kind": "port",
+            "one_thread": 1.0 / per,
+            "sample": f"first {done} of the C4 curves vs the C4 query, oracle numpy port of _chamfer_block "
+                      f"(f64 expansion GEMM, 512-curve blocks), fork pool x{cores}, 1 BLAS thread each"}
+
+
 # ----------------------------------------------------------------- main
 def run_reference(args):
     rank, world, _ = env_rank()
@@ -809,8 +853,9 @@ def main():
             "roofline_kernels": c2["roofline_kernels"],
             "kernels_ms": c2["kernels_ms"],
             "e2e": e2e,
-            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind",
-                                                                           "sample")},
+            "cpu_baseline": None if cpu is None else {**{k: cpu[k] for k in ("value", "unit", "cores", "kind",
+                                                                              "sample")},
+                                                      "one_thread": cpu["one_thread_est"]},
             "gpu_launches": c2["launches_per_step"] * args.steps,
             "clocks": clk.summary(),
             "secondary": secondary,
