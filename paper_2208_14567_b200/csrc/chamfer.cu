@@ -512,7 +512,6 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
 // CTA's MMA overlaps the other's epilogue); one elected thread issues TMA
 // and MMA.  Operands are K-major in shared memory without swizzle: 8-row x
 // 16-byte core matrices, K-adjacent ones 128 B apart, 8-row groups 512 B.
-constexpr int TC_THREADS = 256;
 constexpr int TC_K = 16;
 constexpr int TC_ROWB = TC_K * 4;           // bytes per operand row
 constexpr int TC_OP = 256 * TC_ROWB;        // bytes per operand buffer (256 rows)
@@ -589,24 +588,6 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-// min over 32 consecutive TMEM columns of this thread's row (one load, one wait)
-__device__ __forceinline__ float tc_min32(uint32_t taddr) {
-  uint32_t v[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-  float m = INFINITY;
-#pragma unroll
-  for (int j = 0; j < 32; j += 2) m = min3f(m, __uint_as_float(v[j]), __uint_as_float(v[j + 1]));
-  return m;
-}
-
 // min over 8 consecutive TMEM columns of this thread's row
 __device__ __forceinline__ float tc_min8(uint32_t taddr) {
   uint32_t v[8];
@@ -652,16 +633,6 @@ __device__ __forceinline__ float tc_rowmin(uint32_t tbase, int c0, int c1) {
   return fminf(fminf(m0, m1), fminf(m2, m3));
 }
 
-
-// exact (direct-difference) minimum of |p - o_j|^2 over n points of o
-__device__ __forceinline__ float tc_direct_min(float2 p, const float2* o, int n) {
-  float m = INFINITY;
-  for (int j = 0; j < n; ++j) {
-    const float dx = p.x - o[j].x, dy = p.y - o[j].y;
-    m = fminf(m, fmaf(dy, dy, dx * dx));
-  }
-  return m;
-}
 
 // Warp-specialised pipeline, one CTA per SM (512 TMEM columns = two
 // 256-column accumulator slots):

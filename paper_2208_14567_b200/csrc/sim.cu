@@ -43,6 +43,9 @@ constexpr int NJ = LA_MAX_JOINTS;
 constexpr int NS = LA_MAX_STEPS;
 constexpr int SIM_WARPS = 8;
 constexpr int SIM_THREADS = SIM_WARPS * 32;
+#ifndef LA_SIM_MINB
+#define LA_SIM_MINB 4  // resident CTAs per SM the register allocation targets
+#endif
 
 // Per-warp shared memory: step records + initial pose, followed by a joint
 // position column block pos[joint][lane] sized for the batch's largest n.
@@ -367,7 +370,7 @@ __host__ __device__ constexpr size_t col_bytes() {
 }
 
 template <bool WRITE, bool SCREEN64, bool WONLY, bool EXACT>
-__global__ void __launch_bounds__(SIM_THREADS, 4) sim_kernel(const la_sim_args p, int njmax) {
+__global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_sim_args p, int njmax) {
   extern __shared__ __align__(16) unsigned char sim_smem_raw[];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
