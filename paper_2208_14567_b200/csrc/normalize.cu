@@ -406,13 +406,18 @@ __global__ void __launch_bounds__(NT) circle_kernel(const void* paths, int64_t M
 // P x P distance matrix with register blocking — each lane holds up to 8
 // rows (points l, l+32, ...) packed in f32x2 pairs and every column point is
 // a shared-memory broadcast, so a column costs one LDS for 8 pair distances.
-//   pass 1: M = max d^2 (FMNMX3 chains, REDUX.MAX on the float bits)
-//   pass 2: pairs i < j with d^2 >= M (1 - rel)^2 -> near-max count (frame
+//   pass 1: M = max d^2 (FMNMX3 chains, REDUX.MAX on the float bits); each
+//           column's warp maximum is kept in shared memory
+//   pass 2: only the columns whose maximum reaches M (1 - rel)^2: pairs
+//           i < j with d^2 >= M (1 - rel)^2 -> near-max count (frame
 //           stability) and the lexicographically smallest pair with d^2 == M
 // then the f64 frame transform / bbox / half-turn rule / variance with warp
 // shuffles only (no CTA barriers).
 constexpr int NW_WARPS = 8;
 constexpr int NW_PMAX = 256;
+#ifndef LA_NW_MINB
+#define LA_NW_MINB 1  // no register cap: 79 registers give 3 CTAs per SM (measured: capping for 3 or 4 is slower)
+#endif
 
 __device__ __forceinline__ double warp_min_d(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
@@ -427,9 +432,11 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_norm_args p) {
+__global__ void __launch_bounds__(NW_WARPS * 32, LA_NW_MINB) normalize_warp_kernel(const la_norm_args p) {
   __shared__ __align__(16) float2 pts[NW_WARPS][NW_PMAX];
-  __shared__ __align__(16) float4 cen[NW_WARPS][NW_PMAX];  // (x', y', |p'|^2, 0), centred at point 0
+  // (-2x', -2y', |p'|^2, m): p' centred at point 0; m = pass-1 maximum of
+  // column j (and of its partner column: one reduction per column pair)
+  __shared__ __align__(16) float4 cen[NW_WARPS][NW_PMAX];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int P = p.P;
   const int R2 = (P + 63) / 64;  // packed row pairs per lane (<= 4)
@@ -442,7 +449,7 @@ __global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_
       const float2 v = src[k];
       pts[w][k] = v;
       const float x = v.x - o.x, y = v.y - o.y;
-      cen[w][k] = make_float4(x, y, fmaf(y, y, x * x), 0.f);
+      cen[w][k] = make_float4(-2.f * x, -2.f * y, fmaf(y, y, x * x), 0.f);  // -2 p' exact
     }
     __syncwarp();
     // rows l + 64q and l + 64q + 32 packed as f32x2; padding rows duplicate
@@ -452,8 +459,8 @@ __global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_
     for (int q = 0; q < 4; ++q) {
       const int i0 = lane + 64 * q, i1 = i0 + 32;
       const float4 a = cen[w][(q < R2 && i0 < P) ? i0 : 0], b = cen[w][(q < R2 && i1 < P) ? i1 : 0];
-      xr[q] = make_float2(a.x, b.x);
-      yr[q] = make_float2(a.y, b.y);
+      xr[q] = make_float2(-0.5f * a.x, -0.5f * b.x);  // exact
+      yr[q] = make_float2(-0.5f * a.y, -0.5f * b.y);
       nr[q] = make_float2(a.z, b.z);
     }
     // d^2(i, j) = (|p_i|^2 - 2 p_i.p_j) + |p_j|^2 in the expansion form: two
@@ -463,19 +470,38 @@ __global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_
     float M = -INFINITY;
     // column j needs row pairs q < ceil(j / 64): walk the columns in segments
     // with a compile-time pair count (predicated-off groups would still issue)
-    auto pass1 = [&](auto NQc, int j0, int j1) {
+    // column top = max over the lane's rows; (max t) + z == max(t + z)
+    // because rounding is monotonic
+    auto col_top = [&](auto NQc, int j) -> float {
       constexpr int NQ = decltype(NQc)::value;
-#pragma unroll 2
-      for (int j = j0; j < j1; ++j) {
-        const float4 c = cen[w][j];
-        const float2 m2x = make_float2(-2.f * c.x, -2.f * c.x), m2y = make_float2(-2.f * c.y, -2.f * c.y);
-        float cm = -INFINITY;
+      const float4 c = cen[w][j];
+      const float2 m2x = make_float2(c.x, c.x), m2y = make_float2(c.y, c.y);
+      float cm = -INFINITY;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const float2 t = __ffma2_rn(yr[q], m2y, __ffma2_rn(xr[q], m2x, nr[q]));
-          cm = fmaxf(fmaxf(cm, t.x), t.y);
+      for (int q = 0; q < NQ; ++q) {
+        const float2 t = __ffma2_rn(yr[q], m2y, __ffma2_rn(xr[q], m2x, nr[q]));
+        cm = fmaxf(fmaxf(cm, t.x), t.y);
+      }
+      return cm + c.z;
+    };
+    auto pass1 = [&](auto NQc, int j0, int j1) {
+      int j = j0;
+#pragma unroll 1
+      for (; j + 1 < j1; j += 2) {
+        const float t0 = col_top(NQc, j), t1 = col_top(NQc, j + 1);
+        const float tt = fmaxf(t0, t1);
+        M = fmaxf(M, tt);
+        const float cw = __int_as_float(__reduce_max_sync(FULL, __float_as_int(tt)));
+        if (lane == 0) {
+          cen[w][j].w = cw;
+          cen[w][j + 1].w = cw;
         }
-        M = fmaxf(M, cm + c.z);
+      }
+      if (j < j1) {
+        const float tt = col_top(NQc, j);
+        M = fmaxf(M, tt);
+        const float cw = __int_as_float(__reduce_max_sync(FULL, __float_as_int(tt)));
+        if (lane == 0) cen[w][j].w = cw;
       }
     };
     pass1(std::integral_constant<int, 1>{}, 1, min(P, 65));
@@ -491,12 +517,12 @@ __global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_
     // column).
     int cnt = 0, key = INT_MAX;
     bool two = false;
-    auto pass2 = [&](auto NQc, int j0, int j1) {
+    // one column of pass 2 (NQ row pairs)
+    auto col2 = [&](auto NQc, int j) {
       constexpr int NQ = decltype(NQc)::value;
-#pragma unroll 2
-      for (int j = j0; j < j1; ++j) {
+      {
         const float4 c = cen[w][j];
-        const float2 m2x = make_float2(-2.f * c.x, -2.f * c.x), m2y = make_float2(-2.f * c.y, -2.f * c.y);
+        const float2 m2x = make_float2(c.x, c.x), m2y = make_float2(c.y, c.y);
         float2 tv[NQ];
         float cm = -INFINITY;
 #pragma unroll
@@ -527,10 +553,21 @@ __global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_
         }
       }
     };
-    pass2(std::integral_constant<int, 1>{}, 1, min(P, 65));
-    if (R2 >= 2) pass2(std::integral_constant<int, 2>{}, 65, min(P, 129));
-    if (R2 >= 3) pass2(std::integral_constant<int, 3>{}, 129, min(P, 193));
-    if (R2 >= 4) pass2(std::integral_constant<int, 4>{}, 193, P);
+    // candidate columns: warp maximum >= thr (every column holding a pair
+    // with d^2 == M or in the near band), visited in ascending order
+    __syncwarp();
+    for (int j0 = 0; j0 < P; j0 += 32) {
+      const int jl = j0 + lane;
+      unsigned cand = __ballot_sync(FULL, jl >= 1 && jl < P && cen[w][jl].w >= thr);
+      while (cand) {
+        const int j = j0 + __ffs(cand) - 1;
+        cand &= cand - 1;
+        if (j < 65) col2(std::integral_constant<int, 1>{}, j);
+        else if (j < 129) col2(std::integral_constant<int, 2>{}, j);
+        else if (j < 193) col2(std::integral_constant<int, 3>{}, j);
+        else col2(std::integral_constant<int, 4>{}, j);
+      }
+    }
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
     key = __reduce_min_sync(FULL, key);
     const int pi_ = key == INT_MAX ? 0 : key / P, pj_ = key == INT_MAX ? 0 : key % P;
@@ -558,8 +595,14 @@ __global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_
     };
     double lox = INFINITY, loy = INFINITY, hix = -INFINITY, hiy = -INFINITY;
     double ilx = INFINITY, ily = INFINITY, ihx = -INFINITY, ihy = -INFINITY;
+    // frame coordinates computed once, cached in the (now free) cen storage;
+    // the radii of the variance pass go to the pts storage afterwards
+    double2* bc = reinterpret_cast<double2*>(&cen[w][0]);
+    double* rk = reinterpret_cast<double*>(&pts[w][0]);
+    __syncwarp();  // every lane is done with cen (pass 2)
     for (int k = lane; k < P; k += 32) {
       const double2 b = base(k);
+      bc[k] = b;
       lox = fmin(lox, b.x); hix = fmax(hix, b.x);
       loy = fmin(loy, b.y); hiy = fmax(hiy, b.y);
       if (p.bbox) {
@@ -571,8 +614,9 @@ __global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_
     hix = warp_max_d(hix); hiy = warp_max_d(hiy);
     const double mx = (lox + hix) * 0.5, my = (loy + hiy) * 0.5;
     bool use_a;
+    __syncwarp();
     {
-      const double2 b0 = base(0);
+      const double2 b0 = bc[0];
       const double ex = b0.x - mx, ey = b0.y - my;
       const double ax = (ex + 0.5) - 0.5, ay = (ey + 0.5) - 0.5;
       const double bx = (-ex + 0.5) - 0.5, by = (-ey + 0.5) - 0.5;
@@ -582,7 +626,7 @@ __global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_
       if (fabs(aa - ab) <= 1e-12) {
         double ma = 0.0, mb = 0.0;
         for (int k = lane; k < P; k += 32) {
-          const double e = base(k).y - my;
+          const double e = bc[k].y - my;
           ma += fmax((e + 0.5) - 0.5, 0.0);
           mb += fmax((-e + 0.5) - 0.5, 0.0);
         }
@@ -594,26 +638,24 @@ __global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_
     double rsum = 0.0;
     double y0 = 0.0;
     for (int k = lane; k < P; k += 32) {
-      const double2 b = base(k);
+      const double2 b = bc[k];
       const double ex = b.x - mx, ey = b.y - my;
       const double ox = use_a ? ex + 0.5 : -ex + 0.5;
       const double oy = use_a ? ey + 0.5 : -ey + 0.5;
       if (k == 0) y0 = oy;
       if (p.out_f64) reinterpret_cast<double2*>(p.out)[(size_t)m * P + k] = make_double2(ox, oy);
       else reinterpret_cast<float2*>(p.out)[(size_t)m * P + k] = make_float2((float)ox, (float)oy);
-      rsum += sqrt((ox - 0.5) * (ox - 0.5) + (oy - 0.5) * (oy - 0.5));
+      const double r = sqrt((ox - 0.5) * (ox - 0.5) + (oy - 0.5) * (oy - 0.5));
+      rk[k] = r;  // pts[w][k] is not read after the first frame pass
+      rsum += r;
     }
     y0 = __shfl_sync(FULL, y0, 0);
     double var = 0.0;
     if (p.is_circle || p.circle_var) {
       const double mean = warp_sum_d(rsum) / (double)P;
       double acc = 0.0;
-      for (int k = lane; k < P; k += 32) {
-        const double2 b = base(k);
-        const double ex = b.x - mx, ey = b.y - my;
-        const double ox = use_a ? ex + 0.5 : -ex + 0.5;
-        const double oy = use_a ? ey + 0.5 : -ey + 0.5;
-        const double dr = sqrt((ox - 0.5) * (ox - 0.5) + (oy - 0.5) * (oy - 0.5)) - mean;
+      for (int k = lane; k < P; k += 32) {  // each lane reads back its own radii
+        const double dr = rk[k] - mean;
         acc += dr * dr;
       }
       var = warp_sum_d(acc) / (double)P;

@@ -13,6 +13,9 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum",
            "smsp__sass_thread_inst_executed_op_fadd_pred_on.sum",
            "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum",
+           "smsp__sass_thread_inst_executed_op_ffma2_pred_on.sum",
+           "smsp__sass_thread_inst_executed_op_fadd2_pred_on.sum",
+           "smsp__sass_thread_inst_executed_op_fmul2_pred_on.sum",
            "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
            "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
            "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"]
@@ -49,9 +52,13 @@ def main(path):
     for name, m in sorted(agg.items(), key=lambda kv: -kv[1]["gpu__time_duration.sum"]):
         t = m["gpu__time_duration.sum"]
         by = m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]
+        # packed f32x2 instructions (FFMA2/FADD2/FMUL2) carry two lanes' worth
         f32 = (2 * m["smsp__sass_thread_inst_executed_op_ffma_pred_on.sum"]
                + m["smsp__sass_thread_inst_executed_op_fadd_pred_on.sum"]
-               + m["smsp__sass_thread_inst_executed_op_fmul_pred_on.sum"])
+               + m["smsp__sass_thread_inst_executed_op_fmul_pred_on.sum"]
+               + 4 * m["smsp__sass_thread_inst_executed_op_ffma2_pred_on.sum"]
+               + 2 * m["smsp__sass_thread_inst_executed_op_fadd2_pred_on.sum"]
+               + 2 * m["smsp__sass_thread_inst_executed_op_fmul2_pred_on.sum"])
         f64 = (2 * m["smsp__sass_thread_inst_executed_op_dfma_pred_on.sum"]
                + m["smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"]
                + m["smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"])
@@ -59,8 +66,8 @@ def main(path):
         tf = f32 / t / 1e12 if t else 0
         print(f"{name[:52]:52s} {cnt[name]:6d} {t * 1e3:9.3f} {by / 1e6:9.1f} {gbs:8.0f} {gbs / hbm * 100:6.1f} "
               f"{tf:9.2f} {tf / fp32 * 100:6.1f} {f64 / t / 1e12 if t else 0:9.2f}")
-    print("# FP32 counts scalar FFMA/FADD/FMUL thread instructions; packed FFMA2/FADD2 (chamfer) are not in these "
-          "counters, so the chamfer FP32 rate is taken from its algorithmic flops in bench.py instead")
+    print("# FP32 = 2 FFMA + FADD + FMUL + 4 FFMA2 + 2 FADD2 + 2 FMUL2 thread instructions executed (all "
+          "executed flops, including the error-model and padding work; bench.py reports algorithmic flops)")
 
 
 if __name__ == "__main__":
