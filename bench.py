@@ -213,9 +213,10 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
         if timer:
             timer.mark("start")
         if C2_PIPELINE == "deferred":
-            # fp32 screen (coarse survivors deferred) -> compaction -> f64
-            # write-only replay of the survivors (dense paths) -> valid list
-            res = simulate_deferred(pos, table, T, topo, traj=traj, timer=timer)
+            # fp32 screen (coarse survivors deferred) -> compaction with dense
+            # row offsets -> f64 write-only replay of the survivors (paths of
+            # the real joints, no padding rows) -> valid list
+            res = simulate_deferred(pos, table, T, topo, traj=traj, timer=timer, dense_rows=True)
             return res, res["valid_idx"], res["valid_count"]
         # one pass: coarse fp32 screen, exact first lock for the locked ones,
         # f64 replay + fp32 path stores for the survivors (rows b*stride..),
@@ -279,14 +280,16 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
                                                                   for k in ("screen", "paths")}
                                                                if C2_PIPELINE == "deferred" else {})},
         "roofline": rl_sim, "roofline_kernels": [rl_sim, rl_fp32],
-        "launches_per_step": 4, "mb": mb, "table": table,
+        # deferred: screen + 3 row-compaction kernels + write pass + 3 valid-compaction kernels
+        "launches_per_step": 8 if C2_PIPELINE == "deferred" else 5, "mb": mb, "table": table,
     }
 
 
 def e2e_c2(torch, args, mb, table, world):
     """Same pipeline through the public API with pinned host buffers: H2D of
     the poses + plan indices + plan table, the kernels, D2H of the flags of
-    all candidates, and the paths (+ ids) of the coarse survivors."""
+    all candidates, and the paths (+ ids and first rows) of the coarse
+    survivors: their real joints only (dense rows, la_compact_rows)."""
     from paper_2208_14567_b200.solver import simulate_deferred
 
     pos_h = torch.from_numpy(mb.pos).pin_memory()
@@ -297,26 +300,30 @@ def e2e_c2(torch, args, mb, table, world):
     out_traj = torch.empty((mb.B * stride, T, 2), dtype=torch.float32).pin_memory()
     ft_h = torch.empty(mb.B, dtype=torch.int32).pin_memory()
     fj_h = torch.empty(mb.B, dtype=torch.int32).pin_memory()
-    cnt_h = torch.empty(1, dtype=torch.int64).pin_memory()
+    cnt_h = torch.empty(2, dtype=torch.int64).pin_memory()
     stream = torch.cuda.current_stream()
     stats = {}
 
     idx_h = torch.empty(mb.B, dtype=torch.int64).pin_memory()
+    row_h = torch.empty(mb.B, dtype=torch.int64).pin_memory()
+    cnt_d = torch.empty(2, dtype=torch.int64, device="cuda")
 
     def step():
         pos = pos_h.cuda(non_blocking=True)
         topo = topo_h.cuda(non_blocking=True)
-        res = simulate_deferred(pos, table, T, topo, traj=traj)
+        res = simulate_deferred(pos, table, T, topo, traj=traj, dense_rows=True)
         ft_h.copy_(res["first_t"], non_blocking=True)
         fj_h.copy_(res["first_joint"], non_blocking=True)
-        cnt_h.copy_(res["pend_count"], non_blocking=True)
+        cnt_d[0:1].copy_(res["pend_count"])
+        cnt_d[1:2].copy_(res["pend_rows"])
+        cnt_h.copy_(cnt_d, non_blocking=True)
         stream.synchronize()
-        npend = int(cnt_h.item())
-        n = npend * stride
-        out_traj[:n].copy_(traj[:n], non_blocking=True)          # paths of the coarse survivors
+        npend, n = int(cnt_h[0]), int(cnt_h[1])
+        out_traj[:n].copy_(traj[:n], non_blocking=True)          # paths of the coarse survivors' joints
         idx_h[:npend].copy_(res["pend_idx"][:npend], non_blocking=True)  # their candidate ids
+        row_h[:npend].copy_(res["pend_row"][:npend], non_blocking=True)  # and first rows
         stats["h2d"] = pos_h.numel() * 8 + topo_h.numel() * 4 + table.G * 64
-        stats["d2h"] = mb.B * 8 + 8 + n * T * 8 + npend * 8
+        stats["d2h"] = mb.B * 8 + 16 + n * T * 8 + npend * 16
         return res
 
     for _ in range(max(1, args.warmup)):

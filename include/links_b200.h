@@ -143,6 +143,16 @@ int la_compact_valid(const int32_t* first_t, int64_t B, int32_t T,
                      int64_t* valid_idx, int64_t* valid_count,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* The same selection with dense path rows: selected item k (candidate
+ * idx[k]) starts at row row_off[k] = sum of plans[topo[idx[j]]].n over
+ * j < k; *row_total (device) = rows of all selected items.  With
+ * la_sim_args.traj_row = row_off a write pass stores (T,2) paths for the
+ * real joints only (no padding rows up to traj_stride).                    */
+size_t la_compact_rows_workspace(int64_t B);
+int la_compact_rows(const int32_t* first_t, int64_t B, int32_t T, const int32_t* topo,
+                    const la_plan* plans, int64_t* idx, int64_t* row_off, int64_t* count,
+                    int64_t* row_total, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- curves
  * Batched farthest-pair normalisation (normalize, curves.py:45-71) fused
  * with is_circle (curves.py:95-101) and the frame-stability predicate.     */

@@ -43,6 +43,8 @@ EXPORTS = (
     "la_dyad_solve",
     "la_compact_workspace",
     "la_compact_valid",
+    "la_compact_rows_workspace",
+    "la_compact_rows",
     "la_normalize",
     "la_circle_stats",
     "la_chamfer_workspace",
@@ -214,6 +216,9 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_compact_workspace.argtypes = [i64]
     lib.la_compact_workspace.restype = sz
     lib.la_compact_valid.argtypes = [vp, i64, i32, vp, vp, vp, sz, vp]
+    lib.la_compact_rows_workspace.argtypes = [i64]
+    lib.la_compact_rows_workspace.restype = sz
+    lib.la_compact_rows.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.la_normalize.argtypes = [C.POINTER(LaNormArgs), vp]
     lib.la_circle_stats.argtypes = [vp, i32, i64, i32, vp, vp, vp]
     lib.la_chamfer_workspace.argtypes = [C.POINTER(LaChamferArgs)]
@@ -249,7 +254,8 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_last_error.restype = C.c_char_p
     lib.la_device_sm_count.argtypes = []
     for name in EXPORTS:
-        if name not in ("la_last_error", "la_compact_workspace", "la_chamfer_workspace", "la_coarse_workspace",
+        if name not in ("la_last_error", "la_compact_workspace", "la_compact_rows_workspace", "la_chamfer_workspace",
+                        "la_coarse_workspace",
                         "la_gen_create",
                         "la_gen_destroy", "la_gen_window", "la_gen_window_dev", "la_gen_count", "la_moving_joints"):
             getattr(lib, name).restype = C.c_int

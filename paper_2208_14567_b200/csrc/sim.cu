@@ -699,7 +699,7 @@ __global__ void compact_count(const int32_t* __restrict__ first_t, int64_t B, in
 }
 
 // single-block exclusive scan over tile counts (tiles <= a few 10^5)
-__global__ void compact_scan(int32_t* tile_count, long long ntiles, int64_t* total) {
+__device__ void scan_tiles(int32_t* tile_count, long long ntiles, int64_t* total) {
   __shared__ long long carry;
   __shared__ long long wsum[32];
   if (threadIdx.x == 0) carry = 0;
@@ -732,6 +732,18 @@ __global__ void compact_scan(int32_t* tile_count, long long ntiles, int64_t* tot
     __syncthreads();
   }
   if (threadIdx.x == 0) *total = carry;
+  __syncthreads();
+}
+
+__global__ void compact_scan(int32_t* tile_count, long long ntiles, int64_t* total) {
+  scan_tiles(tile_count, ntiles, total);
+}
+
+// both tile arrays of la_compact_rows in one launch
+__global__ void compact_scan2(int32_t* tile_count, int32_t* tile_rows, long long ntiles, int64_t* total,
+                              int64_t* total_rows) {
+  scan_tiles(tile_count, ntiles, total);
+  scan_tiles(tile_rows, ntiles, total_rows);
 }
 
 __global__ void compact_scatter(const int32_t* __restrict__ first_t, int64_t B, int32_t T,
@@ -756,6 +768,80 @@ __global__ void compact_scatter(const int32_t* __restrict__ first_t, int64_t B, 
   if (v) {
     const long long pos = (long long)tile_off[blockIdx.x] + wsum[w] + __popc(bal & ((1u << lane) - 1u));
     out[pos] = i;
+  }
+}
+
+// ---- compaction with dense row offsets: selected item i (first_t == T)
+// gets idx = i and row_off = sum of its predecessors' joint counts, so a
+// write pass with traj_row = row_off stores paths without padding rows
+__device__ __forceinline__ int item_rows(const int32_t* topo, const la_plan* plans, long long i) {
+  return plans[topo ? topo[i] : 0].n;
+}
+
+__global__ void rows_count(const int32_t* __restrict__ first_t, int64_t B, int32_t T, const int32_t* __restrict__ topo,
+                           const la_plan* __restrict__ plans, int32_t* tile_count, int32_t* tile_rows) {
+  const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
+  const bool v = i < B && first_t[i] == T;
+  int r = v ? item_rows(topo, plans, i) : 0;
+  const unsigned bal = __ballot_sync(FULL, v);
+  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(FULL, r, o);
+  __shared__ int wc[CP_THREADS / 32], wr[CP_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) {
+    wc[threadIdx.x >> 5] = __popc(bal);
+    wr[threadIdx.x >> 5] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int c = wc[threadIdx.x], s = wr[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) {
+      c += __shfl_xor_sync(FULL, c, o);
+      s += __shfl_xor_sync(FULL, s, o);
+    }
+    if (threadIdx.x == 0) {
+      tile_count[blockIdx.x] = c;
+      tile_rows[blockIdx.x] = s;
+    }
+  }
+}
+
+__global__ void rows_scatter(const int32_t* __restrict__ first_t, int64_t B, int32_t T,
+                             const int32_t* __restrict__ topo, const la_plan* __restrict__ plans,
+                             const int32_t* __restrict__ tile_off, const int32_t* __restrict__ tile_row_off,
+                             int64_t* idx, int64_t* row_off) {
+  const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
+  const bool v = i < B && first_t[i] == T;
+  const int r = v ? item_rows(topo, plans, i) : 0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(FULL, v);
+  int x = r;  // inclusive warp scan of the row counts
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  __shared__ int wc[CP_THREADS / 32], wr[CP_THREADS / 32];
+  if (lane == 31) {
+    wc[w] = __popc(bal);
+    wr[w] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the warp totals
+    const int c = wc[lane], s = wr[lane];
+    int xc = c, xs = s;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int yc = __shfl_up_sync(FULL, xc, o), ys = __shfl_up_sync(FULL, xs, o);
+      if (lane >= o) {
+        xc += yc;
+        xs += ys;
+      }
+    }
+    wc[lane] = xc - c;
+    wr[lane] = xs - s;
+  }
+  __syncthreads();
+  if (v) {
+    const long long pos = (long long)tile_off[blockIdx.x] + wc[w] + __popc(bal & ((1u << lane) - 1u));
+    idx[pos] = i;
+    row_off[pos] = (long long)tile_row_off[blockIdx.x] + wr[w] + (x - r);
   }
 }
 
@@ -842,6 +928,29 @@ int la_dyad_solve(const double* pa, const double* pb, const double* r_a, const d
 size_t la_compact_workspace(int64_t B) {
   const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
   return (size_t)(tiles > 0 ? tiles : 1) * sizeof(int32_t);
+}
+
+size_t la_compact_rows_workspace(int64_t B) { return 2 * la_compact_workspace(B); }
+
+int la_compact_rows(const int32_t* first_t, int64_t B, int32_t T, const int32_t* topo, const la_plan* plans,
+                    int64_t* idx, int64_t* row_off, int64_t* count, int64_t* row_total, void* ws, size_t ws_bytes,
+                    void* stream) {
+  if (B < 0 || B >= (1ll << 31) / LA_MAX_JOINTS || !first_t || !plans || !idx || !row_off || !count || !row_total)
+    return fail(LA_EINVAL, "la_compact_rows: bad args");
+  if (ws_bytes < la_compact_rows_workspace(B) || !ws) return fail(LA_EWS, "la_compact_rows: workspace");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (B == 0) {
+    cudaMemsetAsync(count, 0, sizeof(int64_t), s);
+    cudaMemsetAsync(row_total, 0, sizeof(int64_t), s);
+    return cuda_status("la_compact_rows");
+  }
+  const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
+  int32_t* tc = static_cast<int32_t*>(ws);
+  int32_t* tr = tc + la_compact_workspace(B) / sizeof(int32_t);
+  rows_count<<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr);
+  compact_scan2<<<1, 1024, 0, s>>>(tc, tr, tiles, count, row_total);
+  rows_scatter<<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, idx, row_off);
+  return cuda_status("la_compact_rows");
 }
 
 int la_compact_valid(const int32_t* first_t, int64_t B, int32_t T, int64_t* valid_idx,

@@ -301,7 +301,7 @@ def compact_valid(first_t, T: int, stream=None):
     lib = N.load()
     B = first_t.numel()
     idx = torch.empty(max(B, 1), dtype=torch.int64, device=first_t.device)
-    cnt = torch.zeros(1, dtype=torch.int64, device=first_t.device)
+    cnt = torch.empty(1, dtype=torch.int64, device=first_t.device)  # written by the scan (or zeroed for B == 0)
     wsb = int(lib.la_compact_workspace(B))
     ws = torch.empty(wsb, dtype=torch.uint8, device=first_t.device)
     N.check(lib.la_compact_valid(first_t.data_ptr(), B, T, idx.data_ptr(), cnt.data_ptr(),
@@ -309,8 +309,31 @@ def compact_valid(first_t, T: int, stream=None):
     return idx, cnt
 
 
+def compact_rows(first_t, T: int, table: "PlanTable", topo=None, stream=None):
+    """la_compact_rows: ascending indices of candidates with first_t == T,
+    their dense first path rows (running sum of plan joint counts) and, on
+    the device, the count and the total number of rows."""
+    torch = N.require_cuda()
+    lib = N.load()
+    B = first_t.numel()
+    dev = first_t.device
+    idx = torch.empty(max(B, 1), dtype=torch.int64, device=dev)
+    row = torch.empty(max(B, 1), dtype=torch.int64, device=dev)
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)  # written by the scan (or zeroed for B == 0)
+    tot = torch.empty(1, dtype=torch.int64, device=dev)
+    if topo is not None:
+        topo = topo.to(device=dev, dtype=torch.int32).contiguous()
+    wsb = int(lib.la_compact_rows_workspace(B))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    N.check(lib.la_compact_rows(first_t.data_ptr(), B, T, N.ptr(topo), table.tensor().data_ptr(), idx.data_ptr(),
+                                row.data_ptr(), cnt.data_ptr(), tot.data_ptr(), ws.data_ptr(), wsb,
+                                N.stream_ptr(stream)), "la_compact_rows")
+    return idx, row, cnt, tot
+
+
 def simulate_deferred(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None,
-                      fixup_tau: float = DEFAULT_FIXUP_TAU, stream=None, timer=None) -> dict:
+                      fixup_tau: float = DEFAULT_FIXUP_TAU, stream=None, timer=None,
+                      dense_rows: bool = False) -> dict:
     """Two specialised launches, no host sync:
 
     1. fp32 screen (coarse-first, exact first lock for coarse-locked
@@ -323,7 +346,11 @@ def simulate_deferred(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=N
     4. ordered compaction of the valid candidates.
 
     Returns first_t / first_joint (B,), pend_idx / pend_count (the row map of
-    ``traj``), valid_idx / valid_count and traj.
+    ``traj``), valid_idx / valid_count and traj.  ``dense_rows``: pending
+    item i starts at row ``pend_row[i]`` (running sum of the plans' joint
+    counts, la_compact_rows) instead of ``i * stride``, so the first
+    ``pend_rows`` (device scalar) rows of ``traj`` hold every real joint path
+    and no padding rows.
     """
     torch = N.require_cuda()
     B, S, _ = pos0.shape
@@ -332,10 +359,14 @@ def simulate_deferred(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=N
                            _extra_flags=N.LA_SIM_DEFER)
     if timer:
         timer.mark("screen")
-    pend, pcnt = compact_valid(res["first_t"], N.LA_PENDING, stream=stream)
+    prow = prows = None
+    if dense_rows:
+        pend, prow, pcnt, prows = compact_rows(res["first_t"], N.LA_PENDING, table, topo, stream=stream)
+    else:
+        pend, pcnt = compact_valid(res["first_t"], N.LA_PENDING, stream=stream)
     if traj is None:
         traj = torch.empty((max(B, 1) * stride, T, 2), dtype=torch.float32, device=pos0.device)
-    simulate_tensors(pos0, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, cand=pend,
+    simulate_tensors(pos0, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, traj_row=prow, cand=pend,
                      cand_count=pcnt, fixup_tau=fixup_tau, stream=stream,
                      _extra_flags=N.LA_SIM_WRITE_ONLY | N.LA_SIM_SCATTER,
                      _outputs=(res["first_t"], res["first_joint"]))
@@ -345,6 +376,8 @@ def simulate_deferred(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=N
     if timer:
         timer.mark("compact")
     res.update(pend_idx=pend, pend_count=pcnt, valid_idx=vidx, valid_count=vcnt, traj=traj, stride=stride)
+    if dense_rows:
+        res.update(pend_row=prow, pend_rows=prows)
     return res
 
 

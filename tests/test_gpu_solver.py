@@ -413,6 +413,47 @@ def test_deferred_pipeline_matches_single_pass(torch):
     assert torch.equal(res["valid_idx"][:nv], (ref["first_t"] == 200).nonzero().flatten())
 
 
+def test_deferred_dense_rows(torch):
+    """dense_rows (la_compact_rows): the same pending list, row offsets are
+    the running sum of the pending candidates' joint counts, and each
+    candidate's rows equal its strided rows bit for bit (no padding rows)."""
+    from paper_2208_14567_b200.solver import simulate_deferred
+    from paper_2208_14567_b200.workloads import mixed_batch
+
+    mb = mixed_batch(6000, 5, 20, seed=22, stride=20)
+    pos = torch.from_numpy(mb.pos).cuda()
+    topo = torch.from_numpy(mb.topo).cuda()
+    a = simulate_deferred(pos, mb.table(), 200, topo)
+    d = simulate_deferred(pos, mb.table(), 200, topo, dense_rows=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a["first_t"], d["first_t"]) and torch.equal(a["first_joint"], d["first_joint"])
+    npend = int(a["pend_count"].item())
+    assert int(d["pend_count"].item()) == npend
+    pend = a["pend_idx"][:npend].cpu().numpy()
+    assert np.array_equal(d["pend_idx"][:npend].cpu().numpy(), pend)
+    n = mb.n[pend].astype(np.int64)
+    off = np.concatenate([[0], np.cumsum(n)[:-1]])
+    assert np.array_equal(d["pend_row"][:npend].cpu().numpy(), off)
+    assert int(d["pend_rows"].item()) == int(n.sum())
+    ta = a["traj"].view(-1, 20, 200, 2).cpu()
+    td = d["traj"].cpu()
+    ft = d["first_t"].cpu().numpy()
+    for i in range(npend):
+        if ft[pend[i]] == 200:
+            assert torch.equal(td[off[i]:off[i] + n[i]], ta[i, :n[i]])
+    # nothing selected / everything selected
+    from paper_2208_14567_b200.solver import compact_rows
+
+    ft0 = torch.zeros(3000, dtype=torch.int32, device="cuda")
+    _, _, c0, r0 = compact_rows(ft0, 7, mb.table(), topo[:3000])
+    assert int(c0.item()) == 0 and int(r0.item()) == 0
+    idx, row, c1, r1 = compact_rows(ft0, 0, mb.table(), topo[:3000])
+    nn = mb.n[:3000].astype(np.int64)
+    assert int(c1.item()) == 3000 and int(r1.item()) == int(nn.sum())
+    assert np.array_equal(idx[:3000].cpu().numpy(), np.arange(3000))
+    assert np.array_equal(row[:3000].cpu().numpy(), np.concatenate([[0], np.cumsum(nn)[:-1]]))
+
+
 def test_bit_exact_f64_replay(torch, golden):
     """The f64 rounds follow numpy's operation order with IEEE ops and
     glibc's hypot: f64 paths are bit-identical to the reference, fp32 paths
