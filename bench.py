@@ -77,61 +77,86 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def _clock_worker(conn, device_index, uuid, timed, stop):
+    """Sampler process: NVML SM clock + clock-event reasons every 2 ms (a
+    separate process, so it never contends for the bench's GIL)."""
+    import pynvml
+
+    pynvml.nvmlInit()
+    try:
+        h = pynvml.nvmlDeviceGetHandleByUUID(uuid) if uuid else pynvml.nvmlDeviceGetHandleByIndex(device_index)
+    except Exception:
+        h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+    conn.send(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+    all_, samples = [], []
+    while not stop.is_set():
+        try:
+            rec = (pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                   pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+        except Exception:
+            break
+        all_.append(rec)
+        if timed.value:
+            samples.append(rec)
+        time.sleep(0.002)
+    conn.send((all_, samples))
+
+
 class ClockSampler:
     """SM clock + clock-event (throttle) reasons sampled through NVML every
-    2 ms in a background thread; only samples taken while ``timed`` is set
-    count as "during the timed region"."""
+    2 ms in a separate (spawned) process; only samples taken while ``timed``
+    is set count as "during the timed region"."""
 
     REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
                ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, torch, device_index: int):
-        self.timed = False
-        self.samples = []
-        self.all = []
-        self._stop = threading.Event()
-        self.handle = None
-        try:
-            import pynvml
+        import multiprocessing as mp
 
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            h = None
-            try:
-                uuid = str(torch.cuda.get_device_properties(device_index).uuid)
-                h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
-            except Exception:
-                h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
-            self.handle = h
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        self.samples, self.all, self.max_mhz, self.proc = [], [], None, None
+        try:
+            import pynvml  # noqa: F401
+
+            uuid = str(torch.cuda.get_device_properties(device_index).uuid)
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
         except Exception:
-            self.handle = None
-            self.max_mhz = None
-        self.t = threading.Thread(target=self._run, daemon=True)
+            uuid = None
+        ctx = mp.get_context("spawn")
+        self._timed = ctx.Value("b", 0, lock=False)
+        self._stop = ctx.Event()
+        self._conn, child = ctx.Pipe()
+        self._args = (child, device_index, uuid, self._timed, self._stop)
+        self._ctx = ctx
+
+    @property
+    def timed(self):
+        return bool(self._timed.value)
+
+    @timed.setter
+    def timed(self, v):
+        self._timed.value = 1 if v else 0
 
     def start(self):
-        if self.handle is not None:
-            self.t.start()
+        if os.environ.get("LA_BENCH_NO_CLOCKS") == "1":
+            return self
+        try:
+            self.proc = self._ctx.Process(target=_clock_worker, args=self._args, daemon=True)
+            self.proc.start()
+            if self._conn.poll(60):
+                self.max_mhz = self._conn.recv()
+            else:
+                self.proc = None
+        except Exception:
+            self.proc = None
         return self
 
-    def _run(self):
-        nv = self.nv
-        while not self._stop.is_set():
-            try:
-                mhz = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
-            except Exception:
-                break
-            rec = (mhz, rs)
-            self.all.append(rec)
-            if self.timed:
-                self.samples.append(rec)
-            time.sleep(0.002)
-
     def stop(self):
+        if self.proc is None:
+            return
         self._stop.set()
-        if self.t.is_alive():
-            self.t.join(timeout=2)
+        if self._conn.poll(10):
+            self.all, self.samples = self._conn.recv()
+        self.proc.join(timeout=5)
 
     def summary(self):
         src = self.samples if self.samples else self.all
@@ -145,7 +170,7 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(m for m, _ in src), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(reasons), "samples": len(src),
                 "window": "timed regions" if self.samples else "whole run (timed regions too short)",
-                "source": "NVML (nvmlDeviceGetClockInfo / GetCurrentClocksEventReasons), 2 ms"}
+                "source": "NVML (nvmlDeviceGetClockInfo / GetCurrentClocksEventReasons), 2 ms, sampler process"}
 
 
 class Timer:
@@ -207,16 +232,19 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
     stride = table.max_n
     traj = torch.empty((mb.B * stride, T, 2), dtype=torch.float32, device="cuda")
 
-    from paper_2208_14567_b200.solver import compact_valid, simulate_deferred
+    from paper_2208_14567_b200.solver import DeferredGraph, compact_valid
+
+    # fp32 screen (coarse survivors deferred) -> compaction with dense row
+    # offsets -> f64 write-only replay of the survivors (paths of the real
+    # joints, no padding rows) -> valid list; captured once as CUDA graphs
+    # (one per stage) so no host launch gap can fall inside a timed step
+    graph = DeferredGraph(pos, table, T, topo, traj=traj) if C2_PIPELINE == "deferred" else None
 
     def step(timer=None):
         if timer:
             timer.mark("start")
-        if C2_PIPELINE == "deferred":
-            # fp32 screen (coarse survivors deferred) -> compaction with dense
-            # row offsets -> f64 write-only replay of the survivors (paths of
-            # the real joints, no padding rows) -> valid list
-            res = simulate_deferred(pos, table, T, topo, traj=traj, timer=timer, dense_rows=True)
+        if graph is not None:
+            res = graph.replay(timer)
             return res, res["valid_idx"], res["valid_count"]
         # one pass: coarse fp32 screen, exact first lock for the locked ones,
         # f64 replay + fp32 path stores for the survivors (rows b*stride..),
@@ -287,10 +315,11 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
 
 def e2e_c2(torch, args, mb, table, world):
     """Same pipeline through the public API with pinned host buffers: H2D of
-    the poses + plan indices + plan table, the kernels, D2H of the flags of
-    all candidates, and the paths (+ ids and first rows) of the coarse
-    survivors: their real joints only (dense rows, la_compact_rows)."""
-    from paper_2208_14567_b200.solver import simulate_deferred
+    the poses + plan indices into the DeferredGraph's input buffers, the
+    graph replay, D2H of the flags of all candidates, and the paths (+ ids
+    and first rows) of the coarse survivors: their real joints only (dense
+    rows, la_compact_rows)."""
+    from paper_2208_14567_b200.solver import DeferredGraph
 
     pos_h = torch.from_numpy(mb.pos).pin_memory()
     topo_h = torch.from_numpy(mb.topo).pin_memory()
@@ -307,11 +336,16 @@ def e2e_c2(torch, args, mb, table, world):
     idx_h = torch.empty(mb.B, dtype=torch.int64).pin_memory()
     row_h = torch.empty(mb.B, dtype=torch.int64).pin_memory()
     cnt_d = torch.empty(2, dtype=torch.int64, device="cuda")
+    pos_d = torch.empty(pos_h.shape, dtype=pos_h.dtype, device="cuda")
+    topo_d = torch.empty(topo_h.shape, dtype=topo_h.dtype, device="cuda")
+    pos_d.copy_(pos_h)
+    topo_d.copy_(topo_h)
+    graph = DeferredGraph(pos_d, table, T, topo_d, traj=traj)
 
     def step():
-        pos = pos_h.cuda(non_blocking=True)
-        topo = topo_h.cuda(non_blocking=True)
-        res = simulate_deferred(pos, table, T, topo, traj=traj, dense_rows=True)
+        pos_d.copy_(pos_h, non_blocking=True)
+        topo_d.copy_(topo_h, non_blocking=True)
+        res = graph.replay()
         ft_h.copy_(res["first_t"], non_blocking=True)
         fj_h.copy_(res["first_joint"], non_blocking=True)
         cnt_d[0:1].copy_(res["pend_count"])

@@ -352,33 +352,84 @@ def simulate_deferred(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=N
     ``pend_rows`` (device scalar) rows of ``traj`` hold every real joint path
     and no padding rows.
     """
+    stages, out = _deferred_stages(pos0, table, T, topo, traj, fixup_tau, stream, dense_rows)
+    for name, fn in stages:
+        fn()
+        if timer:
+            timer.mark(name)
+    return out
+
+
+def _deferred_stages(pos0, table: PlanTable, T: int, topo, traj, fixup_tau: float, stream, dense_rows: bool):
+    """simulate_deferred as three stage callables (screen; pending compaction
+    + write pass; valid compaction) filling one result dict."""
     torch = N.require_cuda()
-    B, S, _ = pos0.shape
+    B = pos0.shape[0]
     stride = table.max_n
-    res = simulate_tensors(pos0, table, T, topo, write_traj=False, fixup_tau=fixup_tau, stream=stream,
-                           _extra_flags=N.LA_SIM_DEFER)
-    if timer:
-        timer.mark("screen")
-    prow = prows = None
-    if dense_rows:
-        pend, prow, pcnt, prows = compact_rows(res["first_t"], N.LA_PENDING, table, topo, stream=stream)
-    else:
-        pend, pcnt = compact_valid(res["first_t"], N.LA_PENDING, stream=stream)
     if traj is None:
         traj = torch.empty((max(B, 1) * stride, T, 2), dtype=torch.float32, device=pos0.device)
-    simulate_tensors(pos0, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, traj_row=prow, cand=pend,
-                     cand_count=pcnt, fixup_tau=fixup_tau, stream=stream,
-                     _extra_flags=N.LA_SIM_WRITE_ONLY | N.LA_SIM_SCATTER,
-                     _outputs=(res["first_t"], res["first_joint"]))
-    if timer:
-        timer.mark("paths")
-    vidx, vcnt = compact_valid(res["first_t"], T, stream=stream)
-    if timer:
-        timer.mark("compact")
-    res.update(pend_idx=pend, pend_count=pcnt, valid_idx=vidx, valid_count=vcnt, traj=traj, stride=stride)
-    if dense_rows:
-        res.update(pend_row=prow, pend_rows=prows)
-    return res
+    out = {"traj": traj, "stride": stride}
+
+    def screen():
+        out.update(simulate_tensors(pos0, table, T, topo, write_traj=False, fixup_tau=fixup_tau, stream=stream,
+                                    _extra_flags=N.LA_SIM_DEFER))
+
+    def paths():
+        prow = None
+        if dense_rows:
+            pend, prow, pcnt, prows = compact_rows(out["first_t"], N.LA_PENDING, table, topo, stream=stream)
+            out.update(pend_row=prow, pend_rows=prows)
+        else:
+            pend, pcnt = compact_valid(out["first_t"], N.LA_PENDING, stream=stream)
+        out.update(pend_idx=pend, pend_count=pcnt)
+        simulate_tensors(pos0, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, traj_row=prow,
+                         cand=pend, cand_count=pcnt, fixup_tau=fixup_tau, stream=stream,
+                         _extra_flags=N.LA_SIM_WRITE_ONLY | N.LA_SIM_SCATTER,
+                         _outputs=(out["first_t"], out["first_joint"]))
+
+    def compact():
+        vidx, vcnt = compact_valid(out["first_t"], T, stream=stream)
+        out.update(valid_idx=vidx, valid_count=vcnt)
+
+    return [("screen", screen), ("paths", paths), ("compact", compact)], out
+
+
+class DeferredGraph:
+    """simulate_deferred captured once as CUDA graphs, one per stage, over
+    fixed device buffers (pos0, topo, traj and every intermediate):
+    ``replay()`` reruns the whole pipeline on the current contents of pos0 /
+    topo with no host work between kernels (for repeated batches of one
+    shape; results in ``out``, same keys as simulate_deferred)."""
+
+    def __init__(self, pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None,
+                 fixup_tau: float = DEFAULT_FIXUP_TAU, dense_rows: bool = True):
+        torch = N.require_cuda()
+        if topo is not None:
+            topo = topo.to(device=pos0.device, dtype=torch.int32).contiguous()
+        crank_table(T, pos0.device)  # device constants cached before capture
+        table.tensor()
+        stages, self.out = _deferred_stages(pos0, table, T, topo, traj, fixup_tau, None, dense_rows)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up outside capture
+            for _, fn in stages:
+                fn()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graphs = []
+        for name, fn in stages:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            self.graphs.append((name, g))
+        self._keep = (pos0, topo)
+
+    def replay(self, timer=None) -> dict:
+        for name, g in self.graphs:
+            g.replay()
+            if timer:
+                timer.mark(name)
+        return self.out
 
 
 def simulate_compact(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None, traj_f64: bool = False,

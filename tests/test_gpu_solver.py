@@ -454,6 +454,41 @@ def test_deferred_dense_rows(torch):
     assert np.array_equal(row[:3000].cpu().numpy(), np.concatenate([[0], np.cumsum(nn)[:-1]]))
 
 
+def test_deferred_graph_replay(torch):
+    """DeferredGraph (the deferred pipeline captured as CUDA graphs) equals
+    simulate_deferred, and a replay after new poses are copied into its
+    input buffer recomputes everything."""
+    from paper_2208_14567_b200.solver import DeferredGraph, simulate_deferred
+    from paper_2208_14567_b200.workloads import mixed_batch
+
+    mb = mixed_batch(5000, 6, 8, seed=31, stride=8)
+    p1 = torch.from_numpy(mb.pos).cuda()
+    rng = np.random.default_rng(5)
+    p2 = p1 + torch.from_numpy(rng.normal(0.0, 0.02, size=mb.pos.shape)).cuda()  # other poses, same topologies
+    pos = p1.clone()
+    topo = torch.from_numpy(mb.topo).cuda()
+    table = mb.table()
+    g = DeferredGraph(pos, table, 200, topo)
+    for src in (p1, p2, p1):
+        pos.copy_(src)
+        out = g.replay()
+        torch.cuda.synchronize()
+        ref = simulate_deferred(src.clone(), table, 200, topo, dense_rows=True)
+        for k in ("first_t", "first_joint"):
+            assert torch.equal(out[k], ref[k]), k
+        n = int(ref["pend_rows"].item())
+        assert int(out["pend_rows"].item()) == n
+        nv = int(ref["valid_count"].item())
+        assert torch.equal(out["valid_idx"][:nv], ref["valid_idx"][:nv])
+        np_ = int(ref["pend_count"].item())
+        ok = (ref["first_t"][ref["pend_idx"][:np_]] == 200).cpu().numpy()
+        rows = ref["pend_row"][:np_].cpu().numpy()
+        nn = mb.n[ref["pend_idx"][:np_].cpu().numpy()]
+        for i in np.flatnonzero(ok)[:500]:
+            r0, r1 = int(rows[i]), int(rows[i] + nn[i])
+            assert torch.equal(out["traj"][r0:r1], ref["traj"][r0:r1])
+
+
 def test_bit_exact_f64_replay(torch, golden):
     """The f64 rounds follow numpy's operation order with IEEE ops and
     glibc's hypot: f64 paths are bit-identical to the reference, fp32 paths
