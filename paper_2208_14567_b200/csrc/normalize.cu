@@ -415,9 +415,6 @@ __global__ void __launch_bounds__(NT) circle_kernel(const void* paths, int64_t M
 // shuffles only (no CTA barriers).
 constexpr int NW_WARPS = 8;
 constexpr int NW_PMAX = 256;
-#ifndef LA_NW_MINB
-#define LA_NW_MINB 1  // no register cap: 79 registers give 3 CTAs per SM (measured: capping for 3 or 4 is slower)
-#endif
 
 __device__ __forceinline__ double warp_min_d(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
@@ -432,7 +429,10 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(NW_WARPS * 32, LA_NW_MINB) normalize_warp_kernel(const la_norm_args p) {
+// maxThreads only: ptxas then settles at 79 registers (3 CTAs per SM); an
+// explicit minBlocks of 1 gives 114 (2 CTAs, 10 % slower), 3 or 4 cap it
+// tighter and are slower too (measured, round 1 session 2)
+__global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_norm_args p) {
   __shared__ __align__(16) float2 pts[NW_WARPS][NW_PMAX];
   // (-2x', -2y', |p'|^2, m): p' centred at point 0; m = pass-1 maximum of
   // column j (and of its partner column: one reduction per column pair)

@@ -16,6 +16,7 @@ METRICS = [
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram throughput %"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("sm__inst_executed.avg.per_cycle_active", "IPC (per SM)"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma pipe %"),
     ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "alu pipe %"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe %"),

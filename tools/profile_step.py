@@ -27,7 +27,7 @@ if what == "c2":
     topo = torch.from_numpy(mb.topo).cuda()
     table = mb.table()
     for _ in range(reps):
-        simulate_deferred(pos, table, 200, topo)
+        simulate_deferred(pos, table, 200, topo, dense_rows=True)
 elif what == "c3":
     from paper_2208_14567_b200.solver import PlanTable, simulate_tensors
     from paper_2208_14567_b200.workloads import device_poses, topology_pool
