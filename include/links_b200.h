@@ -36,6 +36,7 @@ extern "C" {
 #define LA_EINVAL (-1)     /* bad argument / shape                              */
 #define LA_ERANGE (-2)     /* size beyond a compiled limit                      */
 #define LA_EWS (-3)        /* workspace too small                               */
+#define LA_EHOST (-4)      /* host-side failure (allocation, thread creation)   */
 
 /* ---------------------------------------------------------------- plans
  * One compiled solve order (solver.py:26-46 SolutionPlan, built by

@@ -32,6 +32,7 @@ LA_PENDING = -3
 LA_EINVAL = -1
 LA_ERANGE = -2
 LA_EWS = -3
+LA_EHOST = -4
 
 LA_CH_EXPANSION = 1
 LA_CH_SCALAR_PIPE = 2

@@ -12,6 +12,8 @@
 // PCG64 (128-bit LCG, XSL-RR output) seeding, Generator.random() /
 // uniform() (53-bit doubles), Generator.integers() (Lemire bounded draw on
 // the buffered 32-bit stream).
+#include <mutex>
+#include <exception>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -316,22 +318,53 @@ void parallel_for(int64_t G, int threads, F f) {
     for (int64_t g = 0; g < G; ++g) f(g);
     return;
   }
+  // exception-safe: a worker's exception is rethrown on the calling thread
+  // (then turned into LA_EHOST at the C ABI), a failed thread creation
+  // joins the workers already started
   std::vector<std::thread> ts;
   const int T = (int)std::min<int64_t>(threads, G);
-  for (int t = 0; t < T; ++t)
-    ts.emplace_back([&, t] {
+  std::exception_ptr err;
+  std::mutex mu;
+  auto work = [&](int t) {
+    try {
       for (int64_t g = t; g < G; g += T) f(g);
-    });
+    } catch (...) {
+      std::lock_guard<std::mutex> lock(mu);
+      if (!err) err = std::current_exception();
+    }
+  };
+  try {
+    for (int t = 0; t < T; ++t) ts.emplace_back(work, t);
+  } catch (...) {
+    for (auto& th : ts) th.join();
+    throw;
+  }
   for (auto& th : ts) th.join();
+  if (err) std::rethrow_exception(err);
 }
 
 }  // namespace
+
+// C-ABI guard: no C++ exception (allocation, thread creation) may cross
+// into the caller; it becomes LA_EHOST (or a null engine) + la_last_error
+#define LA_HOST_TRY try {
+#define LA_HOST_CATCH(err)                                         \
+  }                                                                \
+  catch (const std::exception& e) {                                \
+    la::set_error("%s: %s", __func__, e.what());                   \
+    return err;                                                    \
+  }                                                                \
+  catch (...) {                                                    \
+    la::set_error("%s: unknown host exception", __func__);         \
+    return err;                                                    \
+  }
 
 extern "C" {
 
 int la_sample_topologies(int64_t seed, int64_t g0, int64_t G, int32_t n_lo, int32_t n_hi, double ng_prob,
                          int32_t retries, int32_t threads, la_plan* plans, int8_t* types, uint8_t* adj,
                          int32_t* n_out) {
+  LA_HOST_TRY
   if (G < 0 || n_lo < 4 || n_hi < n_lo || n_hi > LA_MAX_JOINTS || !plans || !n_out || retries < 1 || seed < 0 ||
       g0 < 0) {
     la::set_error("la_sample_topologies: bad arguments");
@@ -373,10 +406,12 @@ int la_sample_topologies(int64_t seed, int64_t g0, int64_t G, int32_t n_lo, int3
       return LA_ERANGE;
     }
   return 0;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 int la_sample_poses(int64_t seed, int64_t g0, int64_t G, int32_t per_group, const int32_t* n_of_group,
                     int32_t stride, int32_t threads, double* pos) {
+  LA_HOST_TRY
   if (G < 0 || per_group < 0 || !n_of_group || !pos || stride < 2 || seed < 0 || g0 < 0) {
     la::set_error("la_sample_poses: bad arguments");
     return LA_EINVAL;
@@ -404,12 +439,14 @@ int la_sample_poses(int64_t seed, int64_t g0, int64_t G, int32_t per_group, cons
     }
   });
   return 0;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 // raw stream access for the parity tests: n doubles / ints of
 // default_rng(entropy) where entropy = [e0, e1, e2][:n_ent]
 int la_rng_draw(const int64_t* entropy, int32_t n_ent, int32_t kind, int64_t bound, int64_t count,
                 double* out_d, int64_t* out_i) {
+  LA_HOST_TRY
   std::vector<uint32_t> e;
   for (int i = 0; i < n_ent; ++i) int_words((uint64_t)entropy[i], e);
   Pcg64 r(e);
@@ -418,6 +455,7 @@ int la_rng_draw(const int64_t* entropy, int32_t n_ent, int32_t kind, int64_t bou
     else out_i[i] = r.integers(0, bound);
   }
   return 0;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 }  // extern "C"
@@ -583,6 +621,7 @@ int64_t layout(Engine& E, int32_t lookahead, int64_t cap, la_plan* plans, int32_
 extern "C" {
 
 void* la_gen_create(const la_gen_cfg* cfg, int64_t slot0, int64_t n_slots) {
+  LA_HOST_TRY
   if (!cfg || n_slots < 0 || cfg->n_min < 4 || cfg->n_max < cfg->n_min || cfg->n_max > LA_MAX_JOINTS ||
       cfg->variants < 1 || cfg->batch < 1 || cfg->max_attempts < 1 || cfg->retries < 1 || cfg->seed < 0) {
     la::set_error("la_gen_create: bad configuration");
@@ -606,6 +645,7 @@ void* la_gen_create(const la_gen_cfg* cfg, int64_t slot0, int64_t n_slots) {
       snprintf(E->err, sizeof(E->err), "slot %lld: no valid topology with n=%d", (long long)S.id, S.n);
     }
   return E;
+  LA_HOST_CATCH(nullptr)
 }
 
 void la_gen_destroy(void* h) { delete static_cast<Engine*>(h); }
@@ -618,6 +658,7 @@ void la_gen_destroy(void* h) { delete static_cast<Engine*>(h); }
 // candidate count, 0 when every slot is done, <0 on error.
 int64_t la_gen_window(void* h, int32_t lookahead, int64_t cap, int32_t threads, double* pos, int32_t* cand_plan,
                       la_plan* plans, int32_t* n_plans) {
+  LA_HOST_TRY
   if (!h || !n_plans) {
     la::set_error("la_gen_window: null argument");
     return LA_EINVAL;
@@ -643,6 +684,7 @@ int64_t la_gen_window(void* h, int32_t lookahead, int64_t cap, int32_t threads, 
     }
   });
   return total;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 // Same window, drawn on the device: one descriptor per batch (its pose
@@ -650,6 +692,7 @@ int64_t la_gen_window(void* h, int32_t lookahead, int64_t cap, int32_t threads, 
 // la_gen_poses.  Candidate c of a batch uses stream draws [2nc, 2n(c+1)).
 int64_t la_gen_window_dev(void* h, int32_t lookahead, int64_t cap, la_gen_batch* batches, int64_t max_batches,
                           int64_t* n_batches, la_plan* plans, int32_t* n_plans) {
+  LA_HOST_TRY
   if (!h || !n_batches || !n_plans) {
     la::set_error("la_gen_window_dev: null argument");
     return LA_EINVAL;
@@ -684,11 +727,13 @@ int64_t la_gen_window_dev(void* h, int32_t lookahead, int64_t cap, la_gen_batch*
     }
   *n_batches = nb;
   return total;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 // Walk the device flags of the last window in each slot's stream order:
 // first_t[c] == T_high -> valid; low_t[c] >= 0 -> locked at T_low (step).
 int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int32_t* low_t) {
+  LA_HOST_TRY
   if (!h || !first_t || !low_t) {
     la::set_error("la_gen_consume: null argument");
     return LA_EINVAL;
@@ -784,9 +829,11 @@ int la_gen_consume(void* h, const double* pos, const int32_t* first_t, const int
     return E.error;
   }
   return 0;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 int64_t la_gen_count(void* h, int32_t what) {
+  LA_HOST_TRY
   if (!h) {
     la::set_error("la_gen_count: null engine");
     return LA_EINVAL;
@@ -798,11 +845,13 @@ int64_t la_gen_count(void* h, int32_t what) {
   else
     for (auto& v : E.slot_negs) n += (int64_t)v.size();
   return n;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 // records in slot order: meta [R][4] (slot, variant, attempts, n), poses
 // [R][20][2], plans [R], adjacency [R][20][20], types [R][20]
 int la_gen_records(void* h, int64_t* meta, double* pos, la_plan* plans, uint8_t* adj, int8_t* types) {
+  LA_HOST_TRY
   if (!h || !meta || !pos || !plans || !adj || !types) {
     la::set_error("la_gen_records: null argument");
     return LA_EINVAL;
@@ -826,10 +875,12 @@ int la_gen_records(void* h, int64_t* meta, double* pos, la_plan* plans, uint8_t*
       ++r;
     }
   return 0;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 // negatives in slot order: meta [R][3] (slot, locking step, n), poses [R][20][2]
 int la_gen_negatives(void* h, int64_t* meta, double* pos, uint8_t* adj, int8_t* types) {
+  LA_HOST_TRY
   if (!h || !meta || !pos || !adj || !types) {
     la::set_error("la_gen_negatives: null argument");
     return LA_EINVAL;
@@ -851,10 +902,12 @@ int la_gen_negatives(void* h, int64_t* meta, double* pos, uint8_t* adj, int8_t* 
       ++r;
     }
   return 0;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 // stats: out [21][2] simulated / accepted by joint count; *discarded
 int la_gen_stats(void* h, int64_t* out, int64_t* discarded) {
+  LA_HOST_TRY
   if (!h || !out || !discarded) {
     la::set_error("la_gen_stats: null argument");
     return LA_EINVAL;
@@ -869,6 +922,7 @@ int la_gen_stats(void* h, int64_t* out, int64_t* discarded) {
   }
   *discarded = disc;
   return 0;
+  LA_HOST_CATCH(LA_EHOST)
 }
 
 }  // extern "C"
