@@ -698,9 +698,9 @@ __global__ void __launch_bounds__(TC_CTA, 1) chamfer_tc_kernel(const ScanCtx c) 
   const int MT1 = (Qn + 127) / 128, MT2 = (P + 127) / 128;
   const int TPC = MT1 + MT2;
   const float2* qsrc = reinterpret_cast<const float2*>(A.queries) + (size_t)qi * Qn;
-  const int first = (int)(A.pos_begin + blockIdx.x);
+  const long long first = A.pos_begin + blockIdx.x;  // scan positions are int64 (N may exceed 2^31)
   const int stride = (int)gridDim.x;
-  const int count = first < A.pos_end ? (int)((A.pos_end - first + stride - 1) / stride) : 0;
+  const int count = first < A.pos_end ? (int)((A.pos_end - first + stride - 1) / stride) : 0;  // per CTA
   const uint32_t bytes = (uint32_t)P * 8u;
   auto rec_of = [&](long long pos) -> long long { return A.order ? A.order[pos] : pos; };
 
