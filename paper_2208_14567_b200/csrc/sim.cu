@@ -101,6 +101,20 @@ struct SimCtx {
   float2 p0f;
 };
 
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+// shared-space accesses by 32-bit address (one IADD per access in the dyad
+// loop instead of generic-pointer arithmetic); "memory" keeps them ordered
+// with the other shared-memory accesses of the warp
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f2(uint32_t a, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
 __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -258,7 +272,7 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
     const float2 c = cs32[t];
     W.p32(1) = make_float2(fmaf(C.r1f, c.x, C.p0f.x), fmaf(C.r1f, c.y, C.p0f.y));
     const float tau = C.tau;
-    unsigned char* col = W.cols + W.lane * 8;
+    const uint32_t col = smem_u32(W.cols) + (uint32_t)W.lane * 8u;
     // running first-order bound on the fp32 position error of any joint
     // placed so far (inputs rounded to fp32, then each dyad amplifies the
     // error of its two parents by kappa and adds its own rounding)
@@ -272,8 +286,8 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
     for (; s < C.ns; ++s) {
       const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
       const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].pmask);
-      const float2 pa = *reinterpret_cast<const float2*>(col + g1.y);
-      const float2 pb = *reinterpret_cast<const float2*>(col + g1.z);
+      const float2 pa = lds_f2(col + g1.y);
+      const float2 pb = lds_f2(col + g1.z);
       const float dx = pb.x - pa.x, dy = pb.y - pa.y;
       const float d2 = fmaf(dy, dy, dx * dx);
       const float inv = rsqrt_approx(d2);
@@ -296,16 +310,16 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
       // every later dependent step of this angle goes to the f64 replay.
       const float ax = fabsf(x);
       const float num = ax * fmaf(ax, inv, 1.0f);
-      if (tp || num > h) {  // amplifying dyad (kappa = num / h > 1) or tainted parent
-        err_t = fmaxf(err_t, fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep));
-        taint |= 1u << (g1.w >> 8);
-      } else {
-        err += kErrStep;
-      }
+      // amplifying dyad (kappa = num / h > 1) or tainted parent: branch-free
+      // (most dyads amplify), the same arithmetic either way
+      const bool amp = tp || num > h;
+      const float et = fmaxf(err_t, fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep));
+      err_t = amp ? et : err_t;
+      taint |= amp ? 1u << (g1.w >> 8) : 0u;
+      err = amp ? err : err + kErrStep;
       const float xi = x * inv;
       const float hb = copysignf(h, g0.w) * inv;
-      *reinterpret_cast<float2*>(col + g1.w) =
-          make_float2(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)));
+      sts_f2(col + g1.w, make_float2(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y))));
     }
     if (COUNT) {
       ++ctr.lane_angles;

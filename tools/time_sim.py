@@ -4,6 +4,7 @@ writes, valid compaction) and a 1M-candidate 5-20 joint screen (C3 shape).
 
     python tools/time_sim.py [label]
 """
+import hashlib
 import os
 import statistics
 import sys
@@ -43,11 +44,17 @@ res = {}
 
 
 def c2():
-    res["r"] = simulate_deferred(pos, table, 200, topo, traj=traj)
+    res["r"] = simulate_deferred(pos, table, 200, topo, traj=traj, dense_rows=True)
 
 
 ms2 = timed(c2)
 nv = int(res["r"]["valid_count"].item())
+traj.zero_()  # digest run: rows never written stay zero
+c2()
+h = hashlib.sha256()
+for k in ("first_t", "first_joint"):
+    h.update(res["r"][k].cpu().numpy().tobytes())
+h.update(traj[: int(res["r"]["pend_rows"].item())].cpu().numpy().tobytes())
 
 mechs, plans = topology_pool(256, 5, 20, seed=3000)
 t3 = PlanTable(plans)
@@ -62,5 +69,8 @@ def c3():
 
 ms3 = timed(c3)
 v3 = int((res["s"]["first_t"] == 200).sum().item())
+for k in ("first_t", "first_joint"):
+    h.update(res["s"][k].cpu().numpy().tobytes())
 print(f"{label}: C2 deferred {ms2:.4f} ms ({1e5 / (ms2 / 1e3):.3e} sims/s, valid {nv}) | "
-      f"C3-1M screen {ms3:.4f} ms ({B / (ms3 / 1e3):.3e} cand/s, valid {v3})", flush=True)
+      f"C3-1M screen {ms3:.4f} ms ({B / (ms3 / 1e3):.3e} cand/s, valid {v3}), digest {h.hexdigest()[:16]}",
+      flush=True)
