@@ -1098,6 +1098,31 @@ struct Plan {
   size_t ws_dense; // bytes of dense scratch (generic path without all_d)
 };
 
+// resident CTAs per SM of chamfer_scan_kernel<qs> (registers and the 58 KB
+// of shared memory allow 3 for Q = 200, not 4)
+int scan_occupancy(int qs) {
+  static int cache[9] = {0};
+  if (qs < 1 || qs > 8) return 3;
+  if (cache[qs]) return cache[qs];
+  const void* k = nullptr;
+  switch (qs) {
+    case 1: k = (const void*)chamfer_scan_kernel<1>; break;
+    case 2: k = (const void*)chamfer_scan_kernel<2>; break;
+    case 3: k = (const void*)chamfer_scan_kernel<3>; break;
+    case 4: k = (const void*)chamfer_scan_kernel<4>; break;
+    case 5: k = (const void*)chamfer_scan_kernel<5>; break;
+    case 6: k = (const void*)chamfer_scan_kernel<6>; break;
+    case 7: k = (const void*)chamfer_scan_kernel<7>; break;
+    default: k = (const void*)chamfer_scan_kernel<8>; break;
+  }
+  int occ = 0;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SCAN_SMEM) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, CT, SCAN_SMEM) != cudaSuccess || occ < 1)
+    occ = 3;
+  cache[qs] = occ;
+  return occ;
+}
+
 Plan make_plan(const la_chamfer_args* a) {
   Plan p{};
   const long long npos = a->pos_end - a->pos_begin;
@@ -1106,8 +1131,25 @@ Plan make_plan(const la_chamfer_args* a) {
   int sms = sm_count();
   if (sms <= 0) sms = 148;
   long long want = (npos + CW - 1) / CW;
-  long long cap = (long long)sms * 4;  // resident CTAs per SM for the fast kernel
-  if (a->NQ > 1) cap = (cap + a->NQ - 1) / a->NQ;
+  // one full wave of resident CTAs (a grid beyond it runs a second, mostly
+  // idle wave); with several queries, CTAs per query so that the whole grid
+  // fills whole waves
+  const long long wave = (long long)sms * (p.fast ? scan_occupancy(p.qs) : 4);
+  long long cap = wave;
+  if (a->NQ > 1) {
+    cap = (wave + a->NQ - 1) / a->NQ;
+    double best = 0.0;
+    for (int k = 1; k <= 32; ++k) {
+      const long long gk = ((long long)k * wave + a->NQ - 1) / a->NQ;
+      const long long tot = gk * a->NQ, waves = (tot + wave - 1) / wave;
+      const double eff = (double)tot / (double)(waves * wave);
+      if (eff > best + 1e-9) {
+        best = eff;
+        cap = gk;
+      }
+      if (eff >= 0.97 || gk >= want) break;
+    }
+  }
   if (cap < 1) cap = 1;
   long long g = want < cap ? want : cap;
   if (g < 1) g = 1;
