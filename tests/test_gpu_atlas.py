@@ -190,6 +190,24 @@ def test_chamfer_multi_query_and_odd_sizes(torch):
             assert res["top_id"][qi].tolist() == top.tolist()
 
 
+def test_chamfer_many_queries_equal_single_scans(torch):
+    """The wave-filling grid for many queries (CTAs per query chosen from
+    the occupancy so the whole grid fills whole waves) returns, per query,
+    exactly the lists and distances of a single-query scan."""
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    db = fourier_db(60_000, 200, seed=4100)
+    for nq in (2, 7, 64):
+        qs = fourier_db(nq, 200, seed=500 + nq)
+        many = chamfer_scan(db, qs, k=10, dense=True)
+        for qi in sorted({0, nq // 2, nq - 1}):
+            one = chamfer_scan(db, qs[qi:qi + 1], k=10, dense=True)
+            assert torch.equal(many["all_d"][qi], one["all_d"][0]), (nq, qi)
+            for n in ("top_id", "top_pos", "top_d", "hit_id", "n_hits"):
+                assert torch.equal(many[n][qi], one[n][0]), (nq, qi, n)
+
+
 def test_chamfer_expansion_mode_bound(torch):
     """Expansion inner loop with the rigorous rounding bound: every distance
     within fix_tol of the direct-difference value, near-duplicates re-checked."""
