@@ -910,7 +910,11 @@ int la_simulate(const la_sim_args* a, void* stream) {
   const int sms = sm_count();
   if (sms <= 0) return fail(LA_EINVAL, "la_simulate: no device");
   long long want = (items + SIM_WARPS - 1) / SIM_WARPS;
-  long long grid = (long long)sms * (occ > 0 ? occ : 1);
+  // four waves of resident CTAs: candidates differ widely in cost (early
+  // lock vs all T angles), and the hardware refills SMs with fresh CTAs as
+  // earlier ones finish (measured 1/2/4/8/16 waves: C2 step 0.310 / 0.298 /
+  // 0.290 / 0.298 / 0.310 ms)
+  long long grid = (long long)sms * (occ > 0 ? occ : 1) * 4;
   if (grid > want) grid = want;
   const la_sim_args p = *a;
   kern<<<(unsigned)grid, SIM_THREADS, smem, s>>>(p, njmax);
