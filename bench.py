@@ -53,6 +53,7 @@ C2_PIPELINE = os.environ.get("LA_BENCH_C2_PIPELINE", "deferred")
 # LA_BENCH_SHARED_GPU=1: every rank on cuda:0 with gloo collectives -- a
 # plumbing check of the N > 1 path on a one-GPU box (timings meaningless)
 SHARED_GPU = os.environ.get("LA_BENCH_SHARED_GPU", "0") == "1"
+E2E_CHUNKS = int(os.environ.get("LA_BENCH_E2E_CHUNKS", "2"))  # HostPipeline chunks of the e2e line
 
 
 def env_rank():
@@ -314,50 +315,21 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
 
 
 def e2e_c2(torch, args, mb, table, world):
-    """Same pipeline through the public API with pinned host buffers: H2D of
-    the poses + plan indices into the DeferredGraph's input buffers, the
-    graph replay, D2H of the flags of all candidates, and the paths (+ ids
-    and first rows) of the coarse survivors: their real joints only (dense
-    rows, la_compact_rows)."""
-    from paper_2208_14567_b200.solver import DeferredGraph
+    """Same pipeline through the public host-to-host API
+    (solver.HostPipeline): from pinned host buffers, H2D of the poses + plan
+    indices, the deferred pipeline per chunk as CUDA graphs, D2H of the flags
+    of all candidates and of the paths (+ ids and first rows) of the coarse
+    survivors' real joints (dense rows, la_compact_rows); chunk c's download
+    overlaps the upload and device work of the later chunks."""
+    from paper_2208_14567_b200.solver import HostPipeline
 
-    pos_h = torch.from_numpy(mb.pos).pin_memory()
-    topo_h = torch.from_numpy(mb.topo).pin_memory()
-    stride = table.max_n
-    table.tensor()
-    traj = torch.empty((mb.B * stride, T, 2), dtype=torch.float32, device="cuda")
-    out_traj = torch.empty((mb.B * stride, T, 2), dtype=torch.float32).pin_memory()
-    ft_h = torch.empty(mb.B, dtype=torch.int32).pin_memory()
-    fj_h = torch.empty(mb.B, dtype=torch.int32).pin_memory()
-    cnt_h = torch.empty(2, dtype=torch.int64).pin_memory()
+    pipe = HostPipeline(torch.from_numpy(mb.pos), table, T, torch.from_numpy(mb.topo), chunks=E2E_CHUNKS)
     stream = torch.cuda.current_stream()
     stats = {}
 
-    idx_h = torch.empty(mb.B, dtype=torch.int64).pin_memory()
-    row_h = torch.empty(mb.B, dtype=torch.int64).pin_memory()
-    cnt_d = torch.empty(2, dtype=torch.int64, device="cuda")
-    pos_d = torch.empty(pos_h.shape, dtype=pos_h.dtype, device="cuda")
-    topo_d = torch.empty(topo_h.shape, dtype=topo_h.dtype, device="cuda")
-    pos_d.copy_(pos_h)
-    topo_d.copy_(topo_h)
-    graph = DeferredGraph(pos_d, table, T, topo_d, traj=traj)
-
     def step():
-        pos_d.copy_(pos_h, non_blocking=True)
-        topo_d.copy_(topo_h, non_blocking=True)
-        res = graph.replay()
-        ft_h.copy_(res["first_t"], non_blocking=True)
-        fj_h.copy_(res["first_joint"], non_blocking=True)
-        cnt_d[0:1].copy_(res["pend_count"])
-        cnt_d[1:2].copy_(res["pend_rows"])
-        cnt_h.copy_(cnt_d, non_blocking=True)
-        stream.synchronize()
-        npend, n = int(cnt_h[0]), int(cnt_h[1])
-        out_traj[:n].copy_(traj[:n], non_blocking=True)          # paths of the coarse survivors' joints
-        idx_h[:npend].copy_(res["pend_idx"][:npend], non_blocking=True)  # their candidate ids
-        row_h[:npend].copy_(res["pend_row"][:npend], non_blocking=True)  # and first rows
-        stats["h2d"] = pos_h.numel() * 8 + topo_h.numel() * 4 + table.G * 64
-        stats["d2h"] = mb.B * 8 + 16 + n * T * 8 + npend * 16
+        res = pipe.run()
+        stats["h2d"], stats["d2h"] = res["h2d_bytes"], res["d2h_bytes"]
         return res
 
     for _ in range(max(1, args.warmup)):
@@ -375,7 +347,7 @@ def e2e_c2(torch, args, mb, table, world):
     barrier(torch, world)
     ms = max_over_ranks(torch, statistics.mean(times), world)
     return {"value": world * mb.B / (ms / 1e3), "unit": "simulations/s", "h2d_bytes_per_step": stats["h2d"],
-            "d2h_bytes_per_step": stats["d2h"], "ms_per_step": ms}
+            "d2h_bytes_per_step": stats["d2h"], "ms_per_step": ms, "chunks": E2E_CHUNKS}
 
 
 # ----------------------------------------------------------------- C3
@@ -469,30 +441,36 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
     for _ in range(args.warmup):
         step()
     spans = []
+    n_full = []
     barrier(torch, world)
     clk.timed = True
     for _ in range(args.steps):
         flush()
         tm = Timer(torch, stream)
-        step(tm)
+        res = step(tm)
         spans.append(tm.spans())
+        n_full.append(res["n_full"])
     clk.timed = False
     barrier(torch, world)
     ms = max_over_ranks(torch, statistics.mean(s["total"] for s in spans), world)
     kscan = statistics.mean(s["scan"] for s in spans)
+    full = statistics.mean(int(t.sum().item()) for t in n_full)
     sm_clock = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12
-    flops = PAIR_FLOPS * C4_COUNT
-    trc = load_traffic().get("chamfer_scan_c4_1M", {})
-    rl = {"kernel": "chamfer_scan_kernel<7>", "bound": "fp32", "achieved": flops / (kscan / 1e3) / 1e12,
-          "peak": fp32_peak, "unit": "TFLOP/s", "frac": flops / (kscan / 1e3) / 1e12 / fp32_peak,
-          "algorithmic_flops": flops, "ms": kscan,
-          "traffic": (trc["per_launch_bytes"] / trc["curves"] * C4_COUNT) if trc else None,
-          "traffic_note": "ncu DRAM bytes per curve (1M-curve capture) x curves per launch" if trc else None,
-          "hbm_bytes_algorithmic": C4_COUNT * C4_P * 8,
-          "measured_mix_ceiling_pairs_per_s": 1.40e8,
-          "measured_mix_ceiling_note": "tools/micro/chamfer_inner.cu: FFMA2+FMNMX3 inner loop alone, no row "
-                                       "reduction, 224 slots"}
+    hbm_bytes = C4_COUNT * C4_P * 8
+    trc = load_traffic().get("chamfer_scan_c4_pruned", {})
+    # exact pruning: every curve is read once (1.6 KB) and bounded; only the
+    # curves whose bound does not rule them out get the 40,000-pair
+    # evaluation, so the scan is bounded by the curve stream from HBM
+    rl = {"kernel": "chamfer_scan_kernel<7> (bound stages + exact evaluation of the unpruned)", "bound": "hbm",
+          "achieved": hbm_bytes / (kscan / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+          "frac": hbm_bytes / (kscan / 1e3) / 1e9 / peaks["hbm_gbs"],
+          "algorithmic_bytes": hbm_bytes, "ms": kscan,
+          "traffic": trc.get("per_launch_bytes"), "traffic_source": "profiles/traffic.json" if trc else None,
+          "curves_evaluated_in_full": full, "pruned_frac": 1.0 - full / C4_COUNT,
+          "exhaustive_equivalent_TFLOPs": PAIR_FLOPS * C4_COUNT / (kscan / 1e3) / 1e12,
+          "executed_pair_TFLOPs": PAIR_FLOPS * full / (kscan / 1e3) / 1e12, "fp32_peak_TFLOPs": fp32_peak,
+          "note": "lists identical to the unpruned scan (tests/test_gpu_atlas.py::test_pruned_scan_equals_full_scan)"}
     # e2e: host query -> scan -> merged top-k back to the host
     qh = q.cpu().pin_memory()
     times = []
@@ -513,7 +491,7 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
         cpu = cpu_baseline_c4(db, q)
     del db
     return {"metric": CHAMFER_METRIC, "prefilter": pre, "value": world * C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s",
-            "ms_per_step": ms, "roofline": rl, "launches_per_step": 2,
+            "ms_per_step": ms, "roofline": rl, "launches_per_step": 4,
             "cpu_baseline": cpu,
             "e2e": {"value": world * C4_COUNT / (e2e_ms / 1e3), "unit": "curve-pairs/s",
                     "h2d_bytes_per_step": C4_P * 8, "d2h_bytes_per_step": k * 12},

@@ -199,6 +199,8 @@ int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P,
                                 f32x2 (FFMA2/FADD2) forms                    */
 #define LA_CH_TENSOR 8u      /* squared distances on tcgen05 (3xTF32 split,
                                 direct-difference recheck of small minima)   */
+#define LA_CH_NO_PRUNE 16u   /* disable the exact lower-bound pruning of the
+                                top-k scan (every curve fully evaluated)     */
 
 typedef struct la_chamfer_args {
   const float* db;            /* (device) [N][P][2] f32 normalised curves     */
@@ -226,6 +228,8 @@ typedef struct la_chamfer_args {
   float fixup_below;          /* expansion mode: max tolerated error bound on a
                                  curve's distance (e.g. 5e-5) before the
                                  direct-difference recomputation             */
+  int64_t* n_full;            /* (device, optional) [NQ] += curves evaluated in
+                                 full (the rest were pruned by their bound)  */
 } la_chamfer_args;
 
 size_t la_chamfer_workspace(const la_chamfer_args* args);

@@ -37,6 +37,7 @@ LA_EHOST = -4
 LA_CH_EXPANSION = 1
 LA_CH_SCALAR_PIPE = 2
 LA_CH_TENSOR = 8
+LA_CH_NO_PRUNE = 16
 
 EXPORTS = (
     "la_simulate",
@@ -198,6 +199,7 @@ class LaChamferArgs(C.Structure):
         ("ws_bytes", C.c_size_t),
         ("flags", C.c_uint32),
         ("fixup_below", C.c_float),
+        ("n_full", C.c_void_p),
     ]
 
 

@@ -24,6 +24,8 @@
 // and the first-k hits (by pos); a merge kernel reduces the per-warp lists.
 #include "common.cuh"
 #include <climits>
+#include <cstdlib>
+#include <cuda_fp16.h>
 
 namespace la {
 namespace {
@@ -73,6 +75,12 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // lane-distributed sorted list of up to k entries; lane i holds entry i
 struct WarpList {
   float d;
@@ -117,6 +125,15 @@ struct ScanCtx {
   long long* ws_hit_id;
   long long* ws_nhit;  // [NQ][nwarps]
   float* dense;        // [NQ][N] (generic path) or NULL
+  // exact pruning (fast path, top-k without all_d): per-query distance grid
+  // of the query (lower bounds of the DB-to-query row minima) and a running
+  // upper bound of the k-th best non-hit distance
+  const __half* lb_dt;  // [NQ][LBV][LBV] vertex distances to the query, rounded down
+  const float* lb_par;  // [NQ][8]: lo.x, lo.y, 1/h.x, 1/h.y, h.x, h.y
+  unsigned* thr;        // [NQ] float bits of a k-th best upper bound
+  unsigned* slots;      // [NQ][32] float bits: min d of the evaluated non-hits with id % 32 == slot
+  int prune;
+  float lb_slack;       // absolute slack subtracted from a curve's bound
 };
 
 __device__ __forceinline__ void consider(WarpList& top, WarpList& hit, long long& nhit, const ScanCtx& c,
@@ -355,6 +372,60 @@ __device__ void load_query(QueryRegs<QS>& Q, const float2* __restrict__ qsrc, in
   Q.r2 = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(qr2)));
 }
 
+// Column-term lower bound (prune stage 3): the database curve's points in
+// runs of LB_RUN, each run's bounding box; min_a |q - a| >= distance from q
+// to the nearest box.  Boxes (centred like the query registers) are built
+// into `boxes` (one lane per run) and scanned by every lane for its query
+// slots.  Returns mean_q of the bound (uniform across the warp).
+constexpr int LB_RUN = 10;
+
+template <int QS>
+__device__ __forceinline__ float curve_col_bound(const QueryRegs<QS>& Q, const float2* __restrict__ cur, int P,
+                                                 int Qn, float4* __restrict__ boxes, int lane) {
+  constexpr int NP = QS / 2;
+  const int nb = (P + LB_RUN - 1) / LB_RUN;
+  if (lane < nb) {
+    float lx = INFINITY, ly = INFINITY, hx = -INFINITY, hy = -INFINITY;
+    const int e = min(P, (lane + 1) * LB_RUN);
+    for (int i = lane * LB_RUN; i < e; ++i) {
+      const float2 a = cur[i];
+      lx = fminf(lx, a.x); ly = fminf(ly, a.y); hx = fmaxf(hx, a.x); hy = fmaxf(hy, a.y);
+    }
+    boxes[lane] = make_float4(lx - 0.5f, ly - 0.5f, hx - 0.5f, hy - 0.5f);
+  }
+  __syncwarp();
+  float2 m[NP > 0 ? NP : 1];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) m[j] = make_float2(INFINITY, INFINITY);
+  float mt = INFINITY;
+  for (int b = 0; b < nb; ++b) {
+    const float4 bx = boxes[b];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const float dx0 = fmaxf(fmaxf(bx.x - Q.qx[j].x, Q.qx[j].x - bx.z), 0.f);
+      const float dx1 = fmaxf(fmaxf(bx.x - Q.qx[j].y, Q.qx[j].y - bx.z), 0.f);
+      const float dy0 = fmaxf(fmaxf(bx.y - Q.qy[j].x, Q.qy[j].x - bx.w), 0.f);
+      const float dy1 = fmaxf(fmaxf(bx.y - Q.qy[j].y, Q.qy[j].y - bx.w), 0.f);
+      m[j].x = fminf(m[j].x, fmaf(dy0, dy0, dx0 * dx0));
+      m[j].y = fminf(m[j].y, fmaf(dy1, dy1, dx1 * dx1));
+    }
+    if (QS & 1) {
+      const float dx = fmaxf(fmaxf(bx.x - Q.tx, Q.tx - bx.z), 0.f);
+      const float dy = fmaxf(fmaxf(bx.y - Q.ty, Q.ty - bx.w), 0.f);
+      mt = fminf(mt, fmaf(dy, dy, dx * dx));
+    }
+  }
+  __syncwarp();
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    if (lane + 32 * (2 * j) < Qn) sum += sqrt_approx(m[j].x);
+    if (lane + 32 * (2 * j + 1) < Qn) sum += sqrt_approx(m[j].y);
+  }
+  if ((QS & 1) && lane + 32 * (QS - 1) < Qn) sum += sqrt_approx(mt);
+  return warp_sum(sum) / (float)Qn;
+}
+
 // rare path: direct differences for a curve whose expansion error bound is
 // too large (near-duplicates); own register file, query reloaded from L2
 template <int QS>
@@ -366,9 +437,160 @@ __device__ __noinline__ float direct_chamfer(const float2* __restrict__ qsrc, in
   return curve_chamfer<QS, true>(Q, ex, en, P, Qn, lane, 0.f, dummy, rowbuf);
 }
 
+// ------------------------------------------------------------ exact pruning
+// Row-term lower bound.  For a vertex v of a grid laid over the query's
+// box, DT(v) = min_q |v - q|; for any database point a and any vertex v,
+// min_q |a - q| >= DT(v) - |a - v| (triangle inequality).  Taking the best
+// of the four corners of a's cell and averaging over the curve's points
+// bounds the first chamfer term from below, and the second term is >= 0, so
+//   chamfer(a, q) >= LB(a) = mean_i max(0, max_corners DT(v) - |a_i - v|).
+// A curve whose bound (less slack for fp32 rounding) exceeds both the
+// threshold (so it is no hit) and an upper bound of the k-th best non-hit
+// distance found so far (thr) cannot enter the result and is skipped before
+// its 40,000 point pairs are evaluated.  Three bounds of increasing cost
+// and strength run in turn: the row term from the nearest grid vertex, from
+// the best of the cell's four corners, and that plus the column term from
+// bounding boxes of 10-point runs of the database curve
+// (curve_col_bound).  thr falls as curves are evaluated: the k-th smallest
+// of 32 per-query slot minima (slot = record id % 32, publish_kth), or
+// optionally starts at the k-th best of a seed scan (LA_CH_SEED_DIV).  The
+// result lists are identical to the unpruned scan: every curve in the
+// final top-k has d <= (final k-th) <= thr at all times, and ties never
+// prune (strict >).
+constexpr int LBG = 64;             // grid cells per axis
+constexpr int LBV = LBG + 1;        // vertices per axis
+constexpr size_t LB_DT_BYTES = ((size_t)LBV * LBV * sizeof(__half) + 15) & ~(size_t)15;
+constexpr long long PRUNE_MIN_POS = 1 << 16;  // smaller scans: no seed launches
+
+// grid over the query's bounding box joined with the unit square (the
+// normalised-curve frame), padded by 1/32; DT rounded toward -inf after a
+// 1e-6 slack for the fp32 distance evaluation.  grid (ceil, NQ), 256 threads.
+__global__ void __launch_bounds__(256) lb_grid_kernel(const float* __restrict__ queries, int Q,
+                                                      __half* __restrict__ dt, float* __restrict__ par) {
+  const int qi = blockIdx.y;
+  const float2* q = reinterpret_cast<const float2*>(queries) + (size_t)qi * Q;
+  __shared__ float2 sq[256];
+  __shared__ float red[4][8];
+  float lx = 0.f, ly = 0.f, hx = 1.f, hy = 1.f;
+  for (int i = threadIdx.x; i < Q; i += 256) {
+    const float2 v = q[i];
+    lx = fminf(lx, v.x); ly = fminf(ly, v.y); hx = fmaxf(hx, v.x); hy = fmaxf(hy, v.y);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lx = fminf(lx, __shfl_xor_sync(FULL, lx, o)); ly = fminf(ly, __shfl_xor_sync(FULL, ly, o));
+    hx = fmaxf(hx, __shfl_xor_sync(FULL, hx, o)); hy = fmaxf(hy, __shfl_xor_sync(FULL, hy, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { red[0][w] = lx; red[1][w] = ly; red[2][w] = hx; red[3][w] = hy; }
+  __syncthreads();
+  lx = red[0][0]; ly = red[1][0]; hx = red[2][0]; hy = red[3][0];
+  for (int j = 1; j < 8; ++j) {
+    lx = fminf(lx, red[0][j]); ly = fminf(ly, red[1][j]); hx = fmaxf(hx, red[2][j]); hy = fmaxf(hy, red[3][j]);
+  }
+  const float padx = (hx - lx) / 32.f, pady = (hy - ly) / 32.f;
+  lx -= padx; ly -= pady; hx += padx; hy += pady;
+  const float cx = (hx - lx) / (float)LBG, cy = (hy - ly) / (float)LBG;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    float* pp = par + (size_t)qi * 8;
+    pp[0] = lx; pp[1] = ly; pp[2] = 1.f / cx; pp[3] = 1.f / cy; pp[4] = cx; pp[5] = cy; pp[6] = 0.f; pp[7] = 0.f;
+  }
+  __half* out = dt + (size_t)qi * (LB_DT_BYTES / sizeof(__half));
+  const int v = blockIdx.x * 256 + threadIdx.x;
+  const bool live = v < LBV * LBV;
+  const int ix = live ? v / LBV : 0, iy = live ? v % LBV : 0;
+  const float vx = __fmaf_rn((float)ix, cx, lx), vy = __fmaf_rn((float)iy, cy, ly);
+  float m = INFINITY;
+  for (int b = 0; b < Q; b += 256) {
+    __syncthreads();
+    if (b + threadIdx.x < Q) sq[threadIdx.x] = q[b + threadIdx.x];
+    __syncthreads();
+    const int e = min(256, Q - b);
+    for (int j = 0; j < e; ++j) {
+      const float dx = vx - sq[j].x, dy = vy - sq[j].y;
+      m = fminf(m, __fmaf_rn(dy, dy, dx * dx));
+    }
+  }
+  if (live) out[v] = __float2half_rd(fmaxf(sqrtf(m) * (1.f - 1e-6f) - 1e-6f, 0.f));
+}
+
+// k-th best of the seed scan's merged list -> thr (inf when fewer than k)
+__global__ void thr_init_kernel(const float* __restrict__ seed_d, int k, int NQ, unsigned* __restrict__ thr,
+                                unsigned* __restrict__ slots) {
+  const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= NQ) return;
+  const float d = seed_d ? seed_d[(size_t)qi * k + k - 1] : INFINITY;
+  thr[qi] = __float_as_uint(d < INFINITY && d >= 0.f ? d : INFINITY);
+  for (int j = 0; j < 32; ++j) slots[(size_t)qi * 32 + j] = __float_as_uint(INFINITY);
+}
+
+// A fully evaluated non-hit with d below thr: lower its slot (id % 32) and,
+// when that changed the slot, publish the k-th smallest slot minimum.  The
+// 32 slot minima are distances of 32 distinct evaluated records, so their
+// k-th smallest bounds the final k-th best from above.  Lock-free; after the
+// first wave of curves it triggers only for new near-best curves.  Whole
+// warp (d, id uniform).
+__device__ __forceinline__ void publish_kth(unsigned* __restrict__ thr, unsigned* __restrict__ slots, int k,
+                                            int lane, float d, long long id) {
+  unsigned old = 0u;
+  if (lane == 0) old = atomicMin(&slots[id & 31], __float_as_uint(d));
+  old = __shfl_sync(FULL, old, 0);
+  if (old <= __float_as_uint(d)) return;
+  const unsigned v = __ldcg(&slots[lane]);
+  int rank = 0;
+#pragma unroll 8
+  for (int j = 0; j < 32; ++j) {
+    const unsigned o = __shfl_sync(FULL, v, j);
+    rank += (o < v) || (o == v && j < lane);
+  }
+  const unsigned kth_lane = __ballot_sync(FULL, rank == k - 1);
+  const unsigned kth = __shfl_sync(FULL, v, __ffs(kth_lane) - 1);
+  if (lane == 0 && kth < __float_as_uint(INFINITY)) atomicMin(thr, kth);
+}
+
+// cheaper first stage: nearest vertex only (one square root per point);
+// same vertex coordinates as lb_grid_kernel (fmaf of an integral float)
+__device__ __forceinline__ float curve_row_bound_near(const float2* __restrict__ cur, int P,
+                                                      const __half* __restrict__ dt, float lx, float ly, float ihx,
+                                                      float ihy, float cx, float cy, int lane) {
+  float s = 0.f;
+  for (int i = lane; i < P; i += 32) {
+    const float2 a = cur[i];
+    const float fx = fminf(fmaxf(rintf((a.x - lx) * ihx), 0.f), (float)LBG);
+    const float fy = fminf(fmaxf(rintf((a.y - ly) * ihy), 0.f), (float)LBG);
+    const float ex = a.x - __fmaf_rn(fx, cx, lx), ey = a.y - __fmaf_rn(fy, cy, ly);
+    const float L = __half2float(dt[(int)fx * LBV + (int)fy]) - sqrt_approx(fmaf(ey, ey, ex * ex));
+    s += fmaxf(L, 0.f);
+  }
+  return warp_sum(s) / (float)P;
+}
+
+// mean over the curve's points of the per-point bound (whole warp; all
+// lanes return the same value)
+__device__ __forceinline__ float curve_row_bound(const float2* __restrict__ cur, int P, const __half* __restrict__ dt,
+                                                 float lx, float ly, float ihx, float ihy, float cx, float cy,
+                                                 int lane) {
+  float s = 0.f;
+  for (int i = lane; i < P; i += 32) {
+    const float2 a = cur[i];
+    const int ix = min(max(__float2int_rd((a.x - lx) * ihx), 0), LBG - 1);
+    const int iy = min(max(__float2int_rd((a.y - ly) * ihy), 0), LBG - 1);
+    const float x0 = __fmaf_rn((float)ix, cx, lx), x1 = __fmaf_rn((float)(ix + 1), cx, lx);
+    const float y0 = __fmaf_rn((float)iy, cy, ly), y1 = __fmaf_rn((float)(iy + 1), cy, ly);
+    const float ex0 = a.x - x0, ex1 = a.x - x1, ey0 = a.y - y0, ey1 = a.y - y1;
+    const float sx0 = ex0 * ex0, sx1 = ex1 * ex1, sy0 = ey0 * ey0, sy1 = ey1 * ey1;
+    const __half* d0 = dt + ix * LBV + iy;
+    float L = __half2float(d0[0]) - sqrt_approx(sx0 + sy0);
+    L = fmaxf(L, __half2float(d0[1]) - sqrt_approx(sx0 + sy1));
+    L = fmaxf(L, __half2float(d0[LBV]) - sqrt_approx(sx1 + sy0));
+    L = fmaxf(L, __half2float(d0[LBV + 1]) - sqrt_approx(sx1 + sy1));
+    s += fmaxf(L, 0.f);
+  }
+  return warp_sum(s) / (float)P;
+}
+
 constexpr size_t SCAN_SMEM_PER_WARP =
     2 * PMAX * sizeof(float2) + (PMAX / 2) * (sizeof(float4) + sizeof(float2)) + 32 * sizeof(float);
-constexpr size_t SCAN_SMEM = CW * SCAN_SMEM_PER_WARP + CW * 2 * sizeof(uint64_t);
+constexpr size_t SCAN_SMEM = CW * SCAN_SMEM_PER_WARP + CW * 2 * sizeof(uint64_t) + LB_DT_BYTES;
 
 template <int QS>
 __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
@@ -381,6 +603,7 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
                                            CW * (PMAX / 2) * (sizeof(float4) + sizeof(float2))) +
                   32 * (threadIdx.x >> 5);
   auto bars = reinterpret_cast<uint64_t(*)[2]>(scan_smem + CW * SCAN_SMEM_PER_WARP);
+  __half* lb_dt = reinterpret_cast<__half*>(scan_smem + CW * SCAN_SMEM_PER_WARP + CW * 2 * sizeof(uint64_t));
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int qi = blockIdx.y;
@@ -400,6 +623,21 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
   list_init(top);
   list_init(hit);
   long long nhit = 0;
+
+  // pruning: the query's distance grid in shared memory
+  const bool prune = c.prune != 0;
+  float lb_lx = 0.f, lb_ly = 0.f, lb_ihx = 0.f, lb_ihy = 0.f, lb_cx = 0.f, lb_cy = 0.f;
+  if (prune) {
+    const uint4* src = reinterpret_cast<const uint4*>(c.lb_dt + (size_t)qi * (LB_DT_BYTES / sizeof(__half)));
+    uint4* dst = reinterpret_cast<uint4*>(lb_dt);
+    for (int i = threadIdx.x; i < (int)(LB_DT_BYTES / 16); i += CT) dst[i] = src[i];
+    const float* pp = c.lb_par + (size_t)qi * 8;
+    lb_lx = pp[0]; lb_ly = pp[1]; lb_ihx = pp[2]; lb_ihy = pp[3]; lb_cx = pp[4]; lb_cy = pp[5];
+    __syncthreads();
+  }
+  const unsigned* thr_q = prune ? c.thr + qi : nullptr;
+  long long nfull = 0;
+  const float lb_slack = c.lb_slack;
 
   const long long first = A.pos_begin + gw;
   const long long count = first < A.pos_end ? (A.pos_end - first + stride - 1) / stride : 0;
@@ -443,6 +681,17 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
       cur = &raw[w][0][0];
     }
     if (id == A.exclude_id) continue;
+    if (prune) {
+      // two bounds of increasing cost; d > lba: neither a hit nor in the top k
+      const float t = fmaxf(__uint_as_float(__shfl_sync(FULL, __ldcg(thr_q), 0)), A.threshold);
+      const float lb1 = curve_row_bound_near(cur, P, lb_dt, lb_lx, lb_ly, lb_ihx, lb_ihy, lb_cx, lb_cy, lane);
+      if (fmaf(lb1, 1.f - 1e-4f, -lb_slack) > t) continue;
+      const float lb4 = curve_row_bound(cur, P, lb_dt, lb_lx, lb_ly, lb_ihx, lb_ihy, lb_cx, lb_cy, lane);
+      if (fmaf(lb4, 1.f - 1e-4f, -lb_slack) > t) continue;
+      const float lbc = curve_col_bound<QS>(Q, cur, P, Qn, exs[w], lane);
+      if (fmaf(lb4 + lbc, 1.f - 1e-4f, -lb_slack) > t) continue;
+    }
+    ++nfull;
     // expand + swizzle (each lane handles pairs lane, lane+32, ...)
     float ar2 = 0.f;
     for (int i = lane; i < Ppad / 2; i += 32) {
@@ -490,8 +739,12 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
     if (A.all_d && lane == 0) A.all_d[(size_t)qi * A.N + id] = d;
     const long long rpos = A.pos_map ? A.pos_map[pos] : pos + A.pos_base;
     consider(top, hit, nhit, c, lane, d, rpos, id + A.id_base);
+    if (prune && d >= A.threshold && d < __uint_as_float(__shfl_sync(FULL, __ldcg(thr_q), 0)))
+      publish_kth(c.thr + qi, c.slots + (size_t)qi * 32, A.k, lane, d, id);
   }
   flush_lists(c, qi, gw, lane, top, hit, nhit);
+  if (A.n_full && lane == 0 && nfull) atomicAdd(reinterpret_cast<unsigned long long*>(A.n_full + qi),
+                                                 (unsigned long long)nfull);
 }
 
 // ------------------------------------------------------------ tensor-core path
@@ -1096,6 +1349,10 @@ struct Plan {
   int nwarps;      // per query
   size_t ws_lists; // bytes of list area
   size_t ws_dense; // bytes of dense scratch (generic path without all_d)
+  bool prune;      // exact row-bound pruning with a seed scan (fast path, top-k only)
+  long long seed_end;
+  int seed_grid;
+  size_t ws_prune; // bytes of the pruning area
 };
 
 // resident CTAs per SM of chamfer_scan_kernel<qs> (registers and the 58 KB
@@ -1158,6 +1415,26 @@ Plan make_plan(const la_chamfer_args* a) {
   const size_t per = (size_t)a->NQ * p.nwarps * (a->k > 0 ? a->k : 1);
   p.ws_lists = per * (2 * sizeof(float) + 4 * sizeof(long long)) + (size_t)a->NQ * p.nwarps * sizeof(long long);
   p.ws_dense = (!p.fast && !a->all_d) ? (size_t)a->NQ * a->N * sizeof(float) : 0;
+  p.prune = p.fast && a->k > 0 && !a->all_d && !(a->flags & (LA_CH_TENSOR | LA_CH_NO_PRUNE)) &&
+            npos >= PRUNE_MIN_POS;
+  if (p.prune) {
+    // seed: ~1/128 of the range (at least 64 k records), >= 8 curves per warp
+    static const long long seed_div = [] {
+      const char* e = getenv("LA_CH_SEED_DIV");  // tuning knob (A/B timing only)
+      const long long v = e ? atoll(e) : 0;
+      return v > 0 ? v : 0LL;  // default: no seed scan (the running list converges within a wave)
+    }();
+    long long sn = seed_div > 0 ? npos / seed_div : 0;
+    if (seed_div > 0 && sn < 64LL * a->k) sn = 64LL * a->k;
+    if (sn > npos) sn = npos;
+    p.seed_end = a->pos_begin + sn;
+    long long sg = (sn + 8LL * CW - 1) / (8LL * CW);
+    if (sg > p.grid) sg = p.grid;
+    if (sg < 1) sg = 1;
+    p.seed_grid = (int)sg;
+    p.ws_prune = (size_t)a->NQ * (LB_DT_BYTES + 8 * sizeof(float) + 33 * sizeof(unsigned)) + 16 +
+                 (size_t)a->NQ * a->k * 2 * (sizeof(float) + 2 * sizeof(long long)) + 256;
+  }
   return p;
 }
 
@@ -1173,7 +1450,7 @@ extern "C" {
 size_t la_chamfer_workspace(const la_chamfer_args* a) {
   if (!a) return 0;
   const Plan p = make_plan(a);
-  return align_up(p.ws_lists) + align_up(p.ws_dense) + 1024;
+  return align_up(p.ws_lists) + align_up(p.ws_dense) + align_up(p.ws_prune) + 1024;
 }
 
 int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
@@ -1237,17 +1514,53 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
     return cuda_status("la_chamfer_topk (tensor)");
   }
   if (p.fast) {
-    switch (p.qs) {
+    auto scan = [&](const ScanCtx& cc, dim3 g) -> int {
+      switch (p.qs) {
 #define LA_CASE(QSV)                                                                                   \
   case QSV:                                                                                            \
     cudaFuncSetAttribute(chamfer_scan_kernel<QSV>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
                          (int)SCAN_SMEM);                                                             \
-    chamfer_scan_kernel<QSV><<<grid, CT, SCAN_SMEM, s>>>(c);                                          \
-    break;
-      LA_CASE(1) LA_CASE(2) LA_CASE(3) LA_CASE(4) LA_CASE(5) LA_CASE(6) LA_CASE(7) LA_CASE(8)
+    chamfer_scan_kernel<QSV><<<g, CT, SCAN_SMEM, s>>>(cc);                                            \
+    return 0;
+        LA_CASE(1) LA_CASE(2) LA_CASE(3) LA_CASE(4) LA_CASE(5) LA_CASE(6) LA_CASE(7) LA_CASE(8)
 #undef LA_CASE
-      default: return fail(LA_ERANGE, "la_chamfer_topk: Q=%d", a->Q);
+        default: return fail(LA_ERANGE, "la_chamfer_topk: Q=%d", a->Q);
+      }
+    };
+    if (p.prune) {
+      unsigned char* pw = static_cast<unsigned char*>(a->ws) + align_up(p.ws_lists) + align_up(p.ws_dense);
+      __half* dt = reinterpret_cast<__half*>(pw); pw += (size_t)a->NQ * LB_DT_BYTES;
+      float* par = reinterpret_cast<float*>(pw); pw += (size_t)a->NQ * 8 * sizeof(float);
+      unsigned* thr = reinterpret_cast<unsigned*>(pw); pw += (size_t)a->NQ * sizeof(unsigned);
+      unsigned* slots = reinterpret_cast<unsigned*>(pw); pw += (size_t)a->NQ * 32 * sizeof(unsigned);
+      pw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(pw) + 15) & ~(uintptr_t)15);
+      const size_t nk = (size_t)a->NQ * a->k;
+      int64_t* sp = reinterpret_cast<int64_t*>(pw);  // top_id, top_pos, hit_id, hit_pos
+      float* sd = reinterpret_cast<float*>(sp + 4 * nk); // top_d, hit_d
+      lb_grid_kernel<<<dim3((LBV * LBV + 255) / 256, a->NQ), 256, 0, s>>>(a->queries, a->Q, dt, par);
+      // optional seed: plain scan of a prefix, merged; its k-th best starts thr
+      float* seed_kth = nullptr;
+      if (p.seed_end > a->pos_begin) {
+        ScanCtx sc = c;
+        sc.a.pos_end = p.seed_end;
+        sc.a.n_hits = nullptr;
+        sc.a.n_full = nullptr;
+        sc.a.top_id = sp; sc.a.top_pos = sp + nk; sc.a.hit_id = sp + 2 * nk; sc.a.hit_pos = sp + 3 * nk;
+        sc.a.top_d = sd; sc.a.hit_d = sd + nk;
+        sc.nwarps_total = p.seed_grid * CW;
+        if (int e = scan(sc, dim3(p.seed_grid, a->NQ))) return e;
+        merge_kernel<<<a->NQ, 1024, 0, s>>>(sc);
+        seed_kth = sd;
+      }
+      thr_init_kernel<<<(a->NQ + 255) / 256, 256, 0, s>>>(seed_kth, a->k, a->NQ, thr, slots);
+      c.slots = slots;
+      c.lb_dt = dt;
+      c.lb_par = par;
+      c.thr = thr;
+      c.prune = 1;
+      c.lb_slack = 4e-6f + ((a->flags & LA_CH_EXPANSION) ? a->fixup_below : 0.f);
     }
+    if (int e = scan(c, grid)) return e;
   } else {
     const size_t smem = sizeof(float2) * ((size_t)a->P + a->Q);
     if (smem > 200 * 1024) return fail(LA_ERANGE, "la_chamfer_topk: P+Q too large for the generic path");

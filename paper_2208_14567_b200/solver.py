@@ -432,6 +432,117 @@ class DeferredGraph:
         return self.out
 
 
+class HostPipeline:
+    """Host-to-host batch simulation: poses and plan indices in pinned host
+    memory in, lock flags of every candidate and the fp32 paths of the real
+    joints of every coarse survivor (dense rows) back in pinned host memory.
+
+    The batch is split into ``chunks`` contiguous candidate ranges, each a
+    DeferredGraph over its own device buffers.  Uploads run on one copy
+    stream, the graphs on the compute stream, downloads on a third stream,
+    so chunk c's path download (the bound: ~11 KB per valid 7-joint
+    candidate over PCIe) overlaps the upload and device work of chunks
+    c + 1, ...  The host waits only for each chunk's two row counts (the
+    download sizes) before queueing its copies.
+
+    ``run()`` returns host tensors (views of buffers reused by the next
+    run): ``first_t`` / ``first_joint`` (B,), ``pend_idx`` (global candidate
+    ids of the survivors, ascending), ``pend_row`` (each survivor's first
+    row in ``traj``), ``traj`` (rows, T, 2) float32, and the byte counts of
+    the step's uploads and downloads.  Survivor i's joint j path is
+    ``traj[pend_row[i] + j]``; it is meaningful where
+    ``first_t[pend_idx[i]] == T`` (the rest locked in the fine pass).
+    """
+
+    def __init__(self, pos_h, table: PlanTable, T: int = 200, topo_h=None, *, chunks: int = 4,
+                 fixup_tau: float = DEFAULT_FIXUP_TAU):
+        torch = N.require_cuda()
+        if pos_h.is_cuda or pos_h.dtype != torch.float64 or pos_h.dim() != 3:
+            raise ValueError("pos_h must be a (B, S, 2) float64 host tensor")
+        if not pos_h.is_pinned():
+            pos_h = pos_h.pin_memory()
+        B = pos_h.shape[0]
+        if topo_h is None:
+            topo_h = torch.zeros(B, dtype=torch.int32)
+        topo_h = topo_h.to(dtype=torch.int32).contiguous()
+        if not topo_h.is_pinned():
+            topo_h = topo_h.pin_memory()
+        self.pos_h, self.topo_h, self.table, self.T = pos_h, topo_h, table, T
+        stride = table.max_n
+        chunks = max(1, min(int(chunks), B))
+        bounds = [B * c // chunks for c in range(chunks + 1)]
+        self.ranges = [(bounds[c], bounds[c + 1]) for c in range(chunks) if bounds[c + 1] > bounds[c]]
+        self.pos_d = torch.empty(pos_h.shape, dtype=pos_h.dtype, device="cuda")
+        self.topo_d = torch.empty(topo_h.shape, dtype=topo_h.dtype, device="cuda")
+        self.pos_d.copy_(pos_h)
+        self.topo_d.copy_(topo_h)
+        self.graphs = []
+        for lo, hi in self.ranges:
+            traj = torch.empty(((hi - lo) * stride, T, 2), dtype=torch.float32, device="cuda")
+            self.graphs.append(DeferredGraph(self.pos_d[lo:hi], table, T, self.topo_d[lo:hi], traj=traj,
+                                             fixup_tau=fixup_tau))
+        nc = len(self.ranges)
+        self.cnt_d = torch.empty((nc, 2), dtype=torch.int64, device="cuda")
+        self.cnt_h = torch.empty((nc, 2), dtype=torch.int64).pin_memory()
+        self.ft_h = torch.empty(B, dtype=torch.int32).pin_memory()
+        self.fj_h = torch.empty(B, dtype=torch.int32).pin_memory()
+        self.idx_h = torch.empty(B, dtype=torch.int64).pin_memory()
+        self.row_h = torch.empty(B, dtype=torch.int64).pin_memory()
+        self.traj_h = torch.empty((B * stride, T, 2), dtype=torch.float32).pin_memory()
+        self.up = torch.cuda.Stream()
+        self.down = torch.cuda.Stream()
+        self.ev_in = [torch.cuda.Event() for _ in self.ranges]
+        self.ev_done = [torch.cuda.Event() for _ in self.ranges]
+        self.ev_cnt = [torch.cuda.Event() for _ in self.ranges]
+
+    def run(self) -> dict:
+        torch = N.require_cuda()
+        comp = torch.cuda.current_stream()
+        self.up.wait_stream(comp)  # previous users of the input buffers
+        self.down.wait_stream(comp)
+        with torch.cuda.stream(self.up):
+            for (lo, hi), ev in zip(self.ranges, self.ev_in):
+                self.pos_d[lo:hi].copy_(self.pos_h[lo:hi], non_blocking=True)
+                self.topo_d[lo:hi].copy_(self.topo_h[lo:hi], non_blocking=True)
+                ev.record(self.up)
+        outs = []
+        for c, g in enumerate(self.graphs):
+            comp.wait_event(self.ev_in[c])
+            out = g.replay()
+            self.cnt_d[c, 0:1].copy_(out["pend_count"])
+            self.cnt_d[c, 1:2].copy_(out["pend_rows"])
+            self.cnt_h[c].copy_(self.cnt_d[c], non_blocking=True)
+            self.ev_cnt[c].record(comp)
+            outs.append(out)
+        nrow = npend = 0
+        down_rows = []
+        for c, ((lo, hi), out) in enumerate(zip(self.ranges, outs)):
+            self.ev_cnt[c].synchronize()
+            p, r = int(self.cnt_h[c, 0]), int(self.cnt_h[c, 1])
+            self.down.wait_event(self.ev_cnt[c])
+            with torch.cuda.stream(self.down):
+                self.traj_h[nrow:nrow + r].copy_(out["traj"][:r], non_blocking=True)
+                self.ft_h[lo:hi].copy_(out["first_t"], non_blocking=True)
+                self.fj_h[lo:hi].copy_(out["first_joint"], non_blocking=True)
+                self.idx_h[npend:npend + p].copy_(out["pend_idx"][:p], non_blocking=True)
+                self.row_h[npend:npend + p].copy_(out["pend_row"][:p], non_blocking=True)
+            down_rows.append((lo, nrow, npend, p))
+            nrow += r
+            npend += p
+        self.down.synchronize()
+        for lo, r0, p0, p in down_rows:  # chunk-local ids and rows -> global
+            if lo:
+                self.idx_h[p0:p0 + p] += lo
+            if r0:
+                self.row_h[p0:p0 + p] += r0
+        comp.wait_stream(self.down)
+        B = self.pos_h.shape[0]
+        return {"first_t": self.ft_h, "first_joint": self.fj_h, "pend_idx": self.idx_h[:npend],
+                "pend_row": self.row_h[:npend], "traj": self.traj_h[:nrow],
+                "h2d_bytes": self.pos_h.numel() * 8 + self.topo_h.numel() * 4,
+                "d2h_bytes": B * 8 + len(self.ranges) * 16 + nrow * self.T * 8 + npend * 16}
+
+
 def simulate_compact(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None, traj_f64: bool = False,
                      fixup_tau: float = DEFAULT_FIXUP_TAU, stream=None) -> dict:
     """Batch simulation with compacted output, all on device, no host sync.

@@ -255,3 +255,49 @@ def test_chamfer_tensor_core_path(torch):
     b = chamfer_scan(db, q, k=5, threshold=0.08, exclude_id=5, tensor=True)
     assert torch.equal(a["n_hits"], b["n_hits"])
     assert torch.equal(a["hit_id"], b["hit_id"])
+
+
+def _lists_equal(torch, a, b, names=("top_d", "top_id", "top_pos", "hit_d", "hit_id", "hit_pos", "n_hits")):
+    for name in names:
+        assert torch.equal(a[name], b[name]), name
+
+
+def test_pruned_scan_equals_full_scan(torch):
+    """Exact pruning (query distance-grid lower bound vs the running k-th
+    best) returns the same lists as evaluating every curve: C4-shaped
+    single query, several queries with a shuffled order, hits, an excluded
+    record and P = Q = 64, a scan order sorted worst-first (useless seed),
+    and exact ties at the k-th place (copies of one curve)."""
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    N, P = 300_000, 200
+    db = fourier_db(N, P, seed=21, chunk=1 << 16)
+    q = fourier_db(4, P, seed=22)
+    full = chamfer_scan(db, q[:1], k=10, prune=False)
+    pr = chamfer_scan(db, q[:1], k=10)
+    _lists_equal(torch, full, pr)
+    dense = chamfer_scan(db, q[:1], k=10, dense=True)["all_d"][0].cpu().numpy()
+    assert np.array_equal(pr["top_id"][0].cpu().numpy(), np.lexsort((np.arange(N), dense))[:10])
+    # several queries, shuffled order, threshold with hits, excluded record
+    order = torch.from_numpy(np.random.default_rng(3).permutation(N)).cuda()
+    thr = float(np.quantile(dense, 2e-5))
+    ex = int(np.argmin(dense))
+    kw = dict(k=7, threshold=thr, order=order, exclude_id=ex)
+    _lists_equal(torch, chamfer_scan(db, q, prune=False, **kw), chamfer_scan(db, q, **kw))
+    # worst-first scan order
+    worst = torch.from_numpy(np.argsort(-dense, kind="stable")).cuda()
+    _lists_equal(torch, chamfer_scan(db, q[:1], k=10, order=worst, prune=False),
+                 chamfer_scan(db, q[:1], k=10, order=worst))
+    # exact ties at the k-th place: 25 copies of the 3rd best curve
+    third = int(np.lexsort((np.arange(N), dense))[2])
+    dbt = db.clone()
+    pos = np.random.default_rng(8).choice(N, 25, replace=False)
+    dbt[torch.from_numpy(pos).cuda()] = db[third]
+    a, b = chamfer_scan(dbt, q[:1], k=10, prune=False), chamfer_scan(dbt, q[:1], k=10)
+    _lists_equal(torch, a, b)
+    assert int((a["top_d"][0] == a["top_d"][0, 9]).sum().item()) >= 2
+    # P = Q = 64 (other query register layout)
+    db64 = fourier_db(100_000, 64, seed=23, chunk=1 << 16)
+    q64 = fourier_db(3, 64, seed=24)
+    _lists_equal(torch, chamfer_scan(db64, q64, k=10, prune=False), chamfer_scan(db64, q64, k=10))

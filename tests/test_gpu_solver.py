@@ -554,3 +554,36 @@ def test_screen_flags_at_scale_vs_exact(torch, seed):
             fixed = [k for k in range(n) if (fm >> k) & 1]
             m = O.simulate(nb.pos[i:i + 1, :n], steps, fixed, 200, with_margin=True)["margin"][0]
             assert m < MARGIN, f"candidate {i}: flag mismatch with margin {m:.3e} ({kw})"
+
+
+def test_host_pipeline_matches_deferred(torch):
+    """HostPipeline (chunked host-to-host pipeline, overlapped copies) returns
+    the same flags, survivor ids and per-survivor paths as one
+    DeferredGraph over the whole batch, for 1 and 3 chunks, and a second
+    run over new host poses recomputes everything."""
+    from paper_2208_14567_b200.solver import HostPipeline, simulate_deferred
+    from paper_2208_14567_b200.workloads import mixed_batch
+
+    mb = mixed_batch(4000, 6, 8, seed=37, stride=8)
+    table = mb.table()
+    pos_h = torch.from_numpy(mb.pos.copy())
+    topo_h = torch.from_numpy(mb.topo)
+    for chunks in (1, 3):
+        pipe = HostPipeline(pos_h, table, 200, topo_h, chunks=chunks)
+        for shift in (0.0, 0.01):
+            pipe.pos_h.copy_(torch.from_numpy(mb.pos + shift))
+            res = pipe.run()
+            ref = simulate_deferred(pipe.pos_h.cuda(), table, 200, topo_h.cuda(), dense_rows=True)
+            assert torch.equal(res["first_t"], ref["first_t"].cpu())
+            assert torch.equal(res["first_joint"], ref["first_joint"].cpu())
+            np_ = int(ref["pend_count"].item())
+            assert torch.equal(res["pend_idx"], ref["pend_idx"][:np_].cpu())
+            rr = ref["pend_row"][:np_].cpu().numpy()
+            hr = res["pend_row"].numpy()
+            nn = mb.n[res["pend_idx"].numpy()]
+            assert res["traj"].shape[0] == int(nn.sum()) == int(ref["pend_rows"].item())
+            assert res["d2h_bytes"] == 4000 * 8 + len(pipe.ranges) * 16 + int(nn.sum()) * 200 * 8 + np_ * 16
+            rt = ref["traj"].cpu()
+            ok = (res["first_t"][res["pend_idx"]] == 200).numpy()  # rows of fine-pass locks are scratch
+            for i in np.flatnonzero(ok)[::max(1, np_ // 300)]:
+                assert torch.equal(res["traj"][hr[i]:hr[i] + nn[i]], rt[rr[i]:rr[i] + nn[i]])
