@@ -592,6 +592,47 @@ constexpr size_t SCAN_SMEM_PER_WARP =
     2 * PMAX * sizeof(float2) + (PMAX / 2) * (sizeof(float4) + sizeof(float2)) + 32 * sizeof(float);
 constexpr size_t SCAN_SMEM = CW * SCAN_SMEM_PER_WARP + CW * 2 * sizeof(uint64_t) + LB_DT_BYTES;
 
+// The CTA's 8 warp lists -> one list (warp 0 inserts the other warps'
+// entries), flushed as list blockIdx.x of gridDim.x: the merge kernel then
+// scans 8x fewer entries (most warp lists are short once pruning starts).
+__device__ __forceinline__ void cta_flush_lists(const ScanCtx& c, int qi, int w, int lane, WarpList& top,
+                                                WarpList& hit, long long nhit, unsigned char* smem) {
+  const int k = c.a.k;
+  if (k <= 0) return;
+  struct Ent { float d; long long pos, id; };
+  Ent* et = reinterpret_cast<Ent*>(smem);                  // [CW][32] top
+  Ent* eh = et + CW * 32;                                   // [CW][32] hits
+  long long* nh = reinterpret_cast<long long*>(eh + CW * 32);  // [CW]
+  __syncthreads();  // every warp is done with the shared buffers
+  et[w * 32 + lane] = Ent{top.d, top.pos, top.id};
+  eh[w * 32 + lane] = Ent{hit.d, hit.pos, hit.id};
+  if (lane == 0) nh[w] = nhit;
+  __syncthreads();
+  if (w != 0) return;
+  long long tot = nhit;
+  for (int v = 1; v < CW; ++v) {
+    tot += nh[v];
+    for (int j = 0; j < k; ++j) {
+      const Ent e = et[v * 32 + j];
+      if (e.pos == LLONG_MAX) break;  // sorted: the rest is empty
+      const float kd = __shfl_sync(FULL, top.d, k - 1);
+      const long long kp = __shfl_sync(FULL, top.pos, k - 1);
+      if (!key_less(e.d, e.pos, kd, kp)) break;
+      list_insert(top, k, lane, e.d, e.pos, e.id, false);
+    }
+    for (int j = 0; j < k; ++j) {
+      const Ent e = eh[v * 32 + j];
+      if (e.pos == LLONG_MAX) break;
+      const long long kp = __shfl_sync(FULL, hit.pos, k - 1);
+      if (!(e.pos < kp)) break;
+      list_insert(hit, k, lane, e.d, e.pos, e.id, true);
+    }
+  }
+  ScanCtx cc = c;
+  cc.nwarps_total = gridDim.x;
+  flush_lists(cc, qi, blockIdx.x, lane, top, hit, tot);
+}
+
 template <int QS>
 __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
   extern __shared__ __align__(128) unsigned char scan_smem[];
@@ -742,7 +783,7 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
     if (prune && d >= A.threshold && d < __uint_as_float(__shfl_sync(FULL, __ldcg(thr_q), 0)))
       publish_kth(c.thr + qi, c.slots + (size_t)qi * 32, A.k, lane, d, id);
   }
-  flush_lists(c, qi, gw, lane, top, hit, nhit);
+  cta_flush_lists(c, qi, w, lane, top, hit, nhit, scan_smem);
   if (A.n_full && lane == 0 && nfull) atomicAdd(reinterpret_cast<unsigned long long*>(A.n_full + qi),
                                                  (unsigned long long)nfull);
 }
@@ -1547,7 +1588,7 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
         sc.a.n_full = nullptr;
         sc.a.top_id = sp; sc.a.top_pos = sp + nk; sc.a.hit_id = sp + 2 * nk; sc.a.hit_pos = sp + 3 * nk;
         sc.a.top_d = sd; sc.a.hit_d = sd + nk;
-        sc.nwarps_total = p.seed_grid * CW;
+        sc.nwarps_total = p.seed_grid;  // one list per CTA (cta_flush_lists)
         if (int e = scan(sc, dim3(p.seed_grid, a->NQ))) return e;
         merge_kernel<<<a->NQ, 1024, 0, s>>>(sc);
         seed_kth = sd;
@@ -1561,6 +1602,7 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
       c.lb_slack = 4e-6f + ((a->flags & LA_CH_EXPANSION) ? a->fixup_below : 0.f);
     }
     if (int e = scan(c, grid)) return e;
+    c.nwarps_total = p.grid;  // one list per CTA (cta_flush_lists)
   } else {
     const size_t smem = sizeof(float2) * ((size_t)a->P + a->Q);
     if (smem > 200 * 1024) return fail(LA_ERANGE, "la_chamfer_topk: P+Q too large for the generic path");
