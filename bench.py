@@ -215,6 +215,172 @@ def barrier(torch, world):
     torch.cuda.synchronize()
 
 
+# ----------------------------------------------------------------- fork pools (CPU legs)
+# State shared with forked oracle workers (set before the pool is created;
+# the workers never touch CUDA).  Only the CPU legs and the in-run parity
+# checks below execute oracle/ code -- as the checker / the timed reference.
+_FORK: dict = {}
+
+
+def _cores() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+def _fork_map(fn, tasks, cores=None, warm=True):
+    """pool.map over a fork pool of ``cores`` workers (bench.py:87-94 /
+    run_parallel pattern, one BLAS thread per worker); returns (results,
+    seconds of the timed map)."""
+    import multiprocessing as mp
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    cores = cores or _cores()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        if warm:
+            pool.map(_noop, range(cores))
+        t0 = time.perf_counter()
+        out = pool.map(fn, tasks, chunksize=1)
+        dt = time.perf_counter() - t0
+    return out, dt
+
+
+def _noop(_):
+    from oracle import links_oracle  # noqa: F401  (import cost outside the timed map)
+
+    return 0
+
+
+def decode_plans(raw: np.ndarray):
+    """la_plan records (include/links_b200.h: int16 n, int16 nsteps, u32
+    fixed mask, int8 step[18][3], 2 pad) -> [(n, steps, fixed)]."""
+    raw = np.ascontiguousarray(raw, dtype=np.uint8).reshape(-1, 64)
+    out = []
+    for r in raw:
+        n = int(r[0:2].view(np.int16)[0])
+        S = int(r[2:4].view(np.int16)[0])
+        mask = int(r[4:8].view(np.uint32)[0])
+        st = r[8:8 + 54].view(np.int8).reshape(18, 3)
+        steps = [(int(st[s, 0]), int(st[s, 1]), int(st[s, 2])) for s in range(S)]
+        out.append((n, steps, tuple(j for j in range(n) if (mask >> j) & 1)))
+    return out
+
+
+def _margin_of(pos, steps, fixed):
+    """Normalised discriminant margin (SURVEY.md §8a parity rule) of one
+    candidate, on the oracle side at T = 200."""
+    from oracle import links_oracle as O
+
+    return float(O.simulate(np.asarray(pos)[None], steps, fixed, T, with_margin=True)["margin"][0])
+
+
+# ----------------------------------------------------------------- C1
+C1_COUNT = 1024
+
+
+def _c1_cpu(_):
+    """C1 CPU legs, one thread: the oracle port of simulate_batch over the
+    whole batch and the scalar per-angle loop of simulate (solver.py:142-169,
+    the paper's non-vectorised Table-1 row), each with the reference's
+    digest (locked count, sum of the last joint's last x; bench.py:44-53)."""
+    from oracle import links_oracle as O
+
+    pos, steps, fixed = _FORK["c1"]
+    out = {}
+    t0 = time.perf_counter()
+    r = O.simulate(pos, steps, fixed, T)
+    P = O.trajectories(r)
+    outs = [(int(r["first_t"][b]), int(r["first_joint"][b])) if r["first_t"][b] < T else P[b]
+            for b in range(len(pos))]
+    out["batch_s"] = time.perf_counter() - t0
+    out["batch_digest"] = (sum(isinstance(o, tuple) for o in outs),
+                           float(sum(o[-1, -1, 0] for o in outs if not isinstance(o, tuple))))
+    t0 = time.perf_counter()
+    locked, acc = 0, 0.0
+    for b in range(len(pos)):
+        kind, *rest = O.simulate_scalar(pos[b], steps, fixed, T)
+        if kind == "lock":
+            locked += 1
+        else:
+            acc += float(rest[0][-1, -1, 0])
+    out["scalar_s"] = time.perf_counter() - t0
+    out["scalar_digest"] = (locked, acc)
+    out["first_t"], out["first_joint"], out["P"] = r["first_t"], r["first_joint"], P
+    return out
+
+
+def bench_c1(torch, args, rank, world, peaks, flush, clk, want_cpu):
+    """BASELINE configs[0]: 1,024 seeded four-bars, T=200,
+    f64 paths (the drop-in's bit-exact mode) + flags.  Device value: the
+    la_simulate launch on resident poses; e2e: the drop-in
+    ``solver.simulate_batch`` from a host array to the list of
+    Trajectory/Locking objects.  Parity: every outcome equal to the oracle
+    (flags and f64 paths bit for bit) and the reference's digest rule."""
+    from paper_2208_14567_b200.solver import PlanTable, Locking, simulate_batch, simulate_tensors
+    from paper_2208_14567_b200.workloads import fourbar_batch
+
+    plan, pos = fourbar_batch(C1_COUNT, seed=0)
+    table = PlanTable([plan])
+    dpos = torch.from_numpy(pos).cuda()
+    stream = torch.cuda.current_stream()
+    traj = torch.empty((C1_COUNT * 4, T, 2), dtype=torch.float64, device="cuda")
+
+    def step():
+        return simulate_tensors(dpos, table, T, write_traj=True, traj=traj, traj_stride=4, traj_f64=True)
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = max_over_ranks(torch, statistics.mean(times), world)
+    valid = int((res["first_t"] == T).sum().item())
+    for _ in range(args.warmup):
+        simulate_batch(pos, plan, T)
+    et = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        outs = simulate_batch(pos, plan, T)
+        et.append(time.perf_counter() - t0)
+    e2e_ms = max_over_ranks(torch, 1e3 * statistics.mean(et), world)
+    alg_bytes = valid * 4 * T * 16 + C1_COUNT * (8 + 64)
+    line = {"metric": METRIC, "value": world * C1_COUNT / (ms / 1e3), "unit": "simulations/s", "ms_per_step": ms,
+            "valid": valid, "dtype": "f64 (bit-exact drop-in mode)", "launches_per_step": 1,
+            "roofline": {"kernel": "sim_kernel<WRITE, f64 exact>", "bound": "hbm (launch-bound at this size)",
+                         "achieved": alg_bytes / (ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": alg_bytes / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes": alg_bytes,
+                         "traffic": None},
+            "e2e": {"value": world * C1_COUNT / (e2e_ms / 1e3), "unit": "simulations/s",
+                    "h2d_bytes_per_step": pos.nbytes, "d2h_bytes_per_step": C1_COUNT * 8 + valid * 4 * T * 16,
+                    "api": "solver.simulate_batch (host (1024,4,2) f64 -> list of Trajectory/Locking)"},
+            "config": {"workload": "C1: 1,024 seeded four-bars (conftest.make_four_bar topology, "
+                                   "default_rng(0) poses, pivot/tip pinned), T=200, f64 paths + flags"}}
+    if want_cpu:
+        _FORK["c1"] = (pos, [(3, 1, 2)], (0, 2))
+        (cpu,), _ = _fork_map(_c1_cpu, [0], cores=1, warm=False)
+        ft = np.array([T if not isinstance(o, Locking) else o.step for o in outs])
+        fj = np.array([-1 if not isinstance(o, Locking) else o.joint for o in outs])
+        same_flags = bool(np.array_equal(ft, cpu["first_t"]) and np.array_equal(fj, cpu["first_joint"]))
+        vb = np.flatnonzero(ft == T)
+        same_paths = all(np.array_equal(outs[b].positions, cpu["P"][b]) for b in vb)
+        gpu_digest = (C1_COUNT - len(vb), float(sum(outs[b].positions[-1, -1, 0] for b in vb)))
+        line["cpu_baseline"] = {"value": C1_COUNT / cpu["batch_s"], "unit": "simulations/s", "cores": 1,
+                                "kind": "port", "scalar": C1_COUNT / cpu["scalar_s"],
+                                "sample": "all 1,024 C1 four-bars; oracle numpy port of simulate_batch (value) and "
+                                          "of the scalar simulate loop (scalar), one thread"}
+        line["parity"] = {"checked": C1_COUNT, "flags_equal": same_flags, "f64_paths_bit_identical": bool(same_paths),
+                          "digest": {"gpu": gpu_digest, "batch": cpu["batch_digest"], "scalar": cpu["scalar_digest"]},
+                          "ok": bool(same_flags and same_paths and gpu_digest[0] == cpu["batch_digest"][0]
+                                     == cpu["scalar_digest"][0])}
+    return line
+
+
 # ----------------------------------------------------------------- C2
 def c2_inputs(rank: int):
     from paper_2208_14567_b200.workloads import mixed_batch
@@ -278,6 +444,7 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
         spans.append(tm.spans())
     clk.timed = False
     barrier(torch, world)
+    dev_first_t = (graph.out["first_t"] if graph is not None else r0["first_t"]).cpu().numpy()
     ms = statistics.mean(s["total"] for s in spans)
     ms = max_over_ranks(torch, ms, world)
     if C2_PIPELINE == "deferred":
@@ -311,6 +478,7 @@ def bench_c2(torch, args, rank, world, peaks, flush, clk):
         "roofline": rl_sim, "roofline_kernels": [rl_sim, rl_fp32],
         # deferred: screen + 3 row-compaction kernels + write pass + 3 valid-compaction kernels
         "launches_per_step": 8 if C2_PIPELINE == "deferred" else 5, "mb": mb, "table": table,
+        "dev_first_t": dev_first_t,
     }
 
 
@@ -340,18 +508,172 @@ def e2e_c2(torch, args, mb, table, world):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        step()
+        res = step()
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
     barrier(torch, world)
     ms = max_over_ranks(torch, statistics.mean(times), world)
+    # the last timed step's host outputs (views of the pipeline's pinned
+    # buffers) are what the in-run parity check reads
     return {"value": world * mb.B / (ms / 1e3), "unit": "simulations/s", "h2d_bytes_per_step": stats["h2d"],
-            "d2h_bytes_per_step": stats["d2h"], "ms_per_step": ms, "chunks": E2E_CHUNKS}
+            "d2h_bytes_per_step": stats["d2h"], "ms_per_step": ms, "chunks": E2E_CHUNKS,
+            "api": "solver.HostPipeline.run (pinned host poses -> host flags + dense fp32 paths)"}, (pipe, res)
+
+
+def _c2_parity_worker(gids):
+    """Oracle replay (with the discriminant margin) of whole C2 topology
+    groups, compared with the GPU outputs of the last timed e2e step."""
+    from oracle import links_oracle as O
+
+    S = _FORK["c2"]
+    mb, ft, fj, row_of, traj, starts = S["mb"], S["ft"], S["fj"], S["row_of"], S["traj"], S["starts"]
+    a = dict(checked=0, valid_ref=0, valid_both=0, flag_mismatch=0, flag_mismatch_outside_margin=0,
+             near_margin=0, near_margin_mismatch=0, worst_mech_rel=0.0, worst_path_rel=0.0, worst_abs=0.0,
+             paths_checked=0, small_paths=0, worst_small_path_abs=0.0, values=0, f32_round_mismatch=0,
+             static_rows_exact=True, locked_ref=0, acc_ref=0.0, locked_gpu=0, acc_gpu=0.0)
+    for g in gids:
+        plan = mb.plans[g]
+        n = plan.n
+        lo, hi = starts[g], starts[g + 1]
+        steps = [(s.target, s.a, s.b) for s in plan.steps]
+        r = O.simulate(mb.pos[lo:hi, :n], steps, plan.fixed, T, with_margin=True)
+        f_t, f_j = ft[lo:hi], fj[lo:hi]
+        near = r["margin"] < 1e-6
+        bad = (f_t != r["first_t"]) | ((r["first_t"] < T) & (f_j != r["first_joint"]))
+        a["checked"] += hi - lo
+        a["near_margin"] += int(near.sum())
+        a["flag_mismatch"] += int(bad.sum())
+        a["near_margin_mismatch"] += int((bad & near).sum())
+        a["flag_mismatch_outside_margin"] += int((bad & ~near).sum())
+        vref = r["first_t"] == T
+        a["valid_ref"] += int(vref.sum())
+        a["locked_ref"] += int((~vref).sum())
+        a["locked_gpu"] += int((f_t < T).sum())
+        vb = np.flatnonzero(vref & (f_t == T))
+        if len(vb) == 0:
+            continue
+        Pr = O.trajectories(r)[vb]                                   # (V, n, T, 2) f64
+        rows = row_of[lo + vb][:, None] + np.arange(n)[None, :]
+        Pg = traj[rows.reshape(-1)].reshape(len(vb), n, T, 2)       # fp32 as stored
+        a["acc_ref"] += float(Pr[:, -1, -1, 0].sum())
+        a["acc_gpu"] += float(Pg[:, -1, -1, 0].astype(np.float64).sum())
+        a["valid_both"] += len(vb)
+        err = np.abs(Pg.astype(np.float64) - Pr)                     # (V, n, T, 2)
+        a["worst_abs"] = max(a["worst_abs"], float(err.max()))
+        a["values"] += err.size
+        a["f32_round_mismatch"] += int((Pg != Pr.astype(np.float32)).sum())
+        ext = Pr.max(axis=2) - Pr.min(axis=2)                        # (V, n, 2)
+        mech_ext = Pr.reshape(len(vb), -1, 2).max(axis=1) - Pr.reshape(len(vb), -1, 2).min(axis=1)
+        mdiag = np.hypot(mech_ext[:, 0], mech_ext[:, 1])
+        a["worst_mech_rel"] = max(a["worst_mech_rel"], float((err.reshape(len(vb), -1).max(axis=1) / mdiag).max()))
+        static = sorted(set(plan.fixed) | {0})
+        a["static_rows_exact"] &= bool((Pg[:, static] == Pr[:, static].astype(np.float32)).all())
+        moving = [j for j in range(n) if j not in static]
+        pdiag = np.hypot(ext[:, moving, 0], ext[:, moving, 1])       # (V, m)
+        perr = err[:, moving].max(axis=(2, 3))
+        small = pdiag < 1e-3
+        a["paths_checked"] += pdiag.size
+        a["small_paths"] += int(small.sum())
+        if (~small).any():
+            a["worst_path_rel"] = max(a["worst_path_rel"], float((perr[~small] / pdiag[~small]).max()))
+        if small.any():
+            a["worst_small_path_abs"] = max(a["worst_small_path_abs"], float(perr[small].max()))
+    return a
+
+
+def parity_c2(mb, res, dev_first_t):
+    """In-run parity of the timed C2 outputs (the last e2e step's host
+    buffers) against the oracle on ALL candidates: lock flags bit-exact
+    outside the 1e-6 margin band, the near-margin count, path
+    coordinates within 1e-4 of the bounding-box diagonal (per mechanism, and
+    per moving-joint path; paths whose diagonal is < 1e-3 cannot resolve 1e-4
+    of themselves in fp32 storage and are counted with their absolute error),
+    and the reference harness's digest rule (bench.py:143-145: the locked
+    counts must agree, else it refuses to report)."""
+    B = mb.B
+    ft = res["first_t"].numpy().copy()
+    fj = res["first_joint"].numpy().copy()
+    row_of = np.full(B, -1, dtype=np.int64)
+    row_of[res["pend_idx"].numpy()] = res["pend_row"].numpy()
+    starts = np.searchsorted(mb.topo, np.arange(len(mb.plans) + 1))
+    _FORK["c2"] = dict(mb=mb, ft=ft, fj=fj, row_of=row_of, traj=res["traj"].numpy().copy(), starts=starts)
+    cores = _cores()
+    G = len(mb.plans)
+    parts, dt = _fork_map(_c2_parity_worker, [list(range(w, G, cores)) for w in range(cores)], cores)
+    a = {}
+    for p in parts:
+        for k, v in p.items():
+            if k.startswith("worst"):
+                a[k] = max(a.get(k, 0.0), v)
+            elif k == "static_rows_exact":
+                a[k] = a.get(k, True) and v
+            else:
+                a[k] = a.get(k, 0) + (float(v) if isinstance(v, float) else int(v))
+    a["device_flags_equal_e2e"] = bool(np.array_equal(dev_first_t, ft))
+    a["digest"] = {"gpu": (a.pop("locked_gpu"), a.pop("acc_gpu")), "oracle": (a.pop("locked_ref"), a.pop("acc_ref"))}
+    a["ok"] = bool(a["flag_mismatch_outside_margin"] == 0 and a["worst_path_rel"] <= 1e-4
+                   and a["worst_mech_rel"] <= 1e-4 and a["digest"]["gpu"][0] == a["digest"]["oracle"][0]
+                   and a["checked"] == B and a["device_flags_equal_e2e"])
+    a["seconds"] = dt
+    a["rule"] = ("flags bit-exact except margin < 1e-6 (counted); paths <= 1e-4 x bbox diagonal (per mechanism; "
+                 "per moving-joint path when its diagonal >= 1e-3); reference digest (locked count) equal")
+    return a
 
 
 # ----------------------------------------------------------------- C3
-def bench_c3(torch, args, rank, world, peaks, flush, clk):
+C3_CPU_COUNT = 3906 * 256  # labelled ~1M CPU subset of whole groups (BASELINE.md §2: 1M when < 64 cores)
+
+
+def _c3_cpu_worker(gids):
+    """Two-fidelity gate (find_valid_variant pattern) of whole C3 groups."""
+    from oracle import links_oracle as O
+
+    pos, plans = _FORK["c3"]
+    out = []
+    for g in gids:
+        n, steps, fixed = plans[g]
+        v, lt = O.gate(pos[g * 256:(g + 1) * 256, :n], steps, fixed, T // 4, T)
+        out.append((g, v, lt))
+    return out
+
+
+def cpu_c3(sub, gpu_first_t, gpu_low_t):
+    """C3 CPU leg: the oracle gate (T_low=50 sweep, T=200 for its survivors,
+    generator.py:263-275) per topology group over the first 1M candidates
+    on a fork pool of all host cores; the timed outputs are also the parity
+    check of the GPU screen's valid flags and T_low lock steps on that subset
+    (mismatches classified by the oracle's discriminant margin)."""
+    pos, plans = sub
+    _FORK["c3"] = sub
+    cores = _cores()
+    G = len(plans)
+    parts, dt = _fork_map(_c3_cpu_worker, [list(range(w, G, cores)) for w in range(cores)], cores)
+    valid = np.zeros(G * 256, dtype=bool)
+    low_t = np.zeros(G * 256, dtype=np.int64)
+    for part in parts:
+        for g, v, lt in part:
+            valid[g * 256:(g + 1) * 256] = v
+            low_t[g * 256:(g + 1) * 256] = lt
+    gv = gpu_first_t == T
+    bad = np.flatnonzero((gv != valid) | (gpu_low_t != low_t))
+    outside = 0
+    for b in bad[:200]:
+        n, steps, fixed = plans[b // 256]
+        if _margin_of(pos[b, :n], steps, fixed) >= 1e-6:
+            outside += 1
+    cpu = {"value": G * 256 / dt, "unit": "candidates/s", "cores": cores, "kind": "port", "seconds": dt,
+           "sample": f"first {G * 256} C3 candidates ({G} whole topology groups), oracle numpy port of the "
+                     f"two-fidelity gate (simulate_batch T=50, then T=200 for the survivors), fork pool x{cores}; "
+                     "extrapolates linearly to 10M"}
+    parity = {"checked": G * 256, "valid_oracle": int(valid.sum()), "valid_gpu": int(gv.sum()),
+              "mismatch": int(len(bad)), "mismatch_outside_margin": outside + max(0, len(bad) - 200),
+              "ok": outside == 0 and len(bad) <= 200,
+              "rule": "valid flags and T_low lock steps equal to the oracle gate except margin < 1e-6"}
+    return cpu, parity
+
+
+def bench_c3(torch, args, rank, world, peaks, flush, clk, want_cpu=False):
     from paper_2208_14567_b200.solver import compact_valid, simulate_tensors
     from paper_2208_14567_b200.workloads import native_batch
 
@@ -360,6 +682,9 @@ def bench_c3(torch, args, rank, world, peaks, flush, clk):
     G = table.G
     topo = torch.from_numpy(nb.topo).cuda()
     pos = torch.from_numpy(nb.pos).cuda()
+    sub = None
+    if want_cpu:  # the CPU leg's labelled subset (whole topology groups)
+        sub = (np.ascontiguousarray(nb.pos[:C3_CPU_COUNT]), decode_plans(table.host_bytes())[:C3_CPU_COUNT // 256])
     del nb
     stream = torch.cuda.current_stream()
 
@@ -391,12 +716,16 @@ def bench_c3(torch, args, rank, world, peaks, flush, clk):
     for _ in range(args.steps):
         flush()
         tm = Timer(torch, stream)
-        step(tm)
+        res, _ = step(tm)
         spans.append(tm.spans())
     clk.timed = False
     barrier(torch, world)
     ms = max_over_ranks(torch, statistics.mean(s["total"] for s in spans), world)
     k = statistics.mean(s["screen"] for s in spans)
+    cpu = parity = None
+    if sub is not None:
+        cpu, parity = cpu_c3(sub, res["first_t"][:C3_CPU_COUNT].cpu().numpy(),
+                             res["low_t"][:C3_CPU_COUNT].cpu().numpy())
     sm_clock = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12
     flops = DYAD_FLOPS * int(c[6])
@@ -404,7 +733,7 @@ def bench_c3(torch, args, rank, world, peaks, flush, clk):
           "peak": fp32_peak, "unit": "TFLOP/s", "frac": flops / (k / 1e3) / 1e12 / fp32_peak,
           "algorithmic_flops": flops, "dyads": int(c[6]), "warp_dyad_slots": int(c[2]), "ms": k, "traffic": None}
     return {"metric": SCREEN_METRIC, "value": world * C3_COUNT / (ms / 1e3), "unit": "candidates/s",
-            "ms_per_step": ms, "valid_frac": valid / C3_COUNT, "fixup_lane_angles": int(c[0]),
+            "ms_per_step": ms, "valid_frac": valid / C3_COUNT, "cpu_baseline": cpu, "parity": parity, "fixup_lane_angles": int(c[0]),
             "angles_evaluated": int(c[5]), "rounds_with_replay": int(c[4]), "topologies": G, "roofline": rl,
             "launches_per_step": 4,
             "semantics": "two-fidelity gate (T_low=50 inside T=200): valid flags exact, negatives "
@@ -486,17 +815,146 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
         times.append(e0.elapsed_time(e1))
     e2e_ms = max_over_ranks(torch, statistics.mean(times), world)
     pre = prefilter_c4(torch, args, db, q, flush, stream)
-    cpu = None
+    lists = {"in_distribution": res}
+    # the kernel's own per-pair rate: the same scan with pruning off (every
+    # curve evaluated in full), and a query from outside the database's
+    # distribution (pruning gain reported separately from kernel throughput)
+    full = c4_unpruned(torch, args, db, q, k, flush, stream, peaks, rank)
+    qo = ood_query(torch)
+    ood = c4_query_line(torch, args, db, qo, k, flush, stream, rank)
+    full["lists_equal_pruned"] = bool(torch.equal(full.pop("_res")["top_id"], res["top_id"]))
+    ood["lists_equal_unpruned"] = bool(torch.equal(ood.pop("_res_full")["top_id"], ood["_res"]["top_id"]))
+    lists["out_of_distribution"] = ood.pop("_res")
+    cpu = parity = None
     if rank == 0 and world == 1 and "cpu" not in set(filter(None, args.skip.split(","))):
         cpu = cpu_baseline_c4(db, q)
+        parity = parity_chamfer(db, {"in_distribution": q, "out_of_distribution": qo}, lists, sample=20_000)
     del db
     return {"metric": CHAMFER_METRIC, "prefilter": pre, "value": world * C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s",
-            "ms_per_step": ms, "roofline": rl, "launches_per_step": 4,
-            "cpu_baseline": cpu,
+            "ms_per_step": ms, "roofline": rl, "launches_per_step": 4, "unpruned": full, "ood_query": ood,
+            "parity": parity, "cpu_baseline": cpu,
             "e2e": {"value": world * C4_COUNT / (e2e_ms / 1e3), "unit": "curve-pairs/s",
                     "h2d_bytes_per_step": C4_P * 8, "d2h_bytes_per_step": k * 12},
             "config": {"workload": "C4: 1 query vs 10M normalised Fourier curves/GPU (5 harmonics, "
-                                   "coeffs N(0,1/k^2)), 200 pts fp32, exhaustive top-10"}}
+                                   "coeffs N(0,1/k^2)), 200 pts fp32, exact top-10 (pruned scan; lists equal to "
+                                   "evaluating every pair, see 'unpruned')"}}
+
+
+def ood_query(torch):
+    """A query from outside the database distribution: 15 harmonics with a
+    flat N(0, 1) spectrum (the database uses 5 with N(0, 1/k^2)), normalised
+    by la_normalize."""
+    from paper_2208_14567_b200.curves import normalize_tensors
+
+    rng = np.random.default_rng(777)
+    t = 2.0 * np.pi * np.arange(C4_P) / C4_P
+    k = np.arange(1, 16)
+    c = rng.standard_normal((4, 15))
+    x = c[0] @ np.cos(np.outer(k, t)) + c[1] @ np.sin(np.outer(k, t))
+    y = c[2] @ np.cos(np.outer(k, t)) + c[3] @ np.sin(np.outer(k, t))
+    raw = torch.from_numpy(np.stack([x, y], axis=-1)[None]).cuda()
+    return normalize_tensors(raw, out_f64=False)["out"]
+
+
+def _time_scan(torch, args, fn, flush, stream, steps):
+    times, res = [], None
+    for _ in range(steps):
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = fn()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    return statistics.mean(times), res
+
+
+def c4_unpruned(torch, args, db, q, k, flush, stream, peaks, rank):
+    """chamfer_scan(prune=False): all 10M curves evaluated (40,000 point
+    pairs each) -- the per-pair kernel rate against the FP32 roofline."""
+    from paper_2208_14567_b200.atlas import chamfer_scan
+
+    fn = lambda: chamfer_scan(db, q, k=k, threshold=0.0, id_base=rank * C4_COUNT, pos_base=rank * C4_COUNT,  # noqa
+                              prune=False)
+    fn()
+    ms, res = _time_scan(torch, args, fn, flush, stream, 3)
+    fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    tf = PAIR_FLOPS * C4_COUNT / (ms / 1e3) / 1e12
+    return {"value": C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s", "ms_per_step": ms, "steps": 3,
+            "roofline": {"kernel": "chamfer_scan_kernel<7> (prune off)", "bound": "fp32", "achieved": tf,
+                         "peak": fp32_peak, "unit": "TFLOP/s", "frac": tf / fp32_peak,
+                         "algorithmic_flops": PAIR_FLOPS * C4_COUNT, "traffic": None,
+                         "note": "200 kflop per pair (SURVEY §8d); nominal FP32 = 148 SM x 128 x 2 x sm_max_mhz"},
+            "_res": res}
+
+
+def c4_query_line(torch, args, db, qo, k, flush, stream, rank):
+    from paper_2208_14567_b200.atlas import chamfer_scan
+
+    kw = dict(k=k, threshold=0.0, id_base=rank * C4_COUNT, pos_base=rank * C4_COUNT)
+    fn = lambda: chamfer_scan(db, qo, **kw)  # noqa: E731
+    fn()
+    ms, res = _time_scan(torch, args, fn, flush, stream, 3)
+    res_full = chamfer_scan(db, qo, prune=False, **kw)
+    full = int(res["n_full"].sum().item())
+    return {"value": C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s", "ms_per_step": ms,
+            "curves_evaluated_in_full": full, "pruned_frac": 1.0 - full / C4_COUNT,
+            "query": "15 harmonics, flat N(0,1) spectrum (database: 5 harmonics, N(0,1/k^2)), normalised",
+            "best_d": float(res["top_d"][0, 0].item()), "kth_d": float(res["top_d"][0, k - 1].item()),
+            "_res": res, "_res_full": res_full}
+
+
+def _chamfer_check_worker(task):
+    from oracle import links_oracle as O
+
+    lo, hi = task
+    pts, queries = _FORK["ch"]
+    return lo, np.stack([O.chamfer_direct_block(pts[lo:hi], q) for q in queries])
+
+
+def parity_chamfer(db, queries: dict, lists: dict, sample: int, seed: int = 5):
+    """Oracle check of the timed retrieval lists: each listed distance
+    recomputed in f64 (curves.chamfer, cdist form) on the stored curves,
+    within 1e-4 x the query's bbox diagonal, and a random sample of database
+    curves: none may beat a query's k-th listed distance by more than that
+    tolerance without being listed (a pruned-away true neighbour would)."""
+    from oracle import links_oracle as O
+
+    N = db.shape[0]
+    rng = np.random.default_rng(seed)
+    samp = np.sort(rng.choice(N, size=min(sample, N), replace=False))
+    import torch
+
+    pts = db[torch.from_numpy(samp).to(db.device)].double().cpu().numpy()
+    names = list(queries)
+    qs = [queries[n][0].double().cpu().numpy() for n in names]
+    _FORK["ch"] = (pts, qs)
+    cores = _cores()
+    bounds = np.linspace(0, len(samp), cores * 4 + 1).astype(int)
+    parts, dt = _fork_map(_chamfer_check_worker, [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1)], cores)
+    D = np.concatenate([p for _, p in sorted(parts, key=lambda x: x[0])], axis=1)  # (nq, sample)
+    out = {"sample": int(len(samp)), "seconds": dt, "queries": {}}
+    ok = True
+    for qi, name in enumerate(names):
+        r = lists[name]
+        ids = r["top_id"][0].cpu().numpy()
+        dg = r["top_d"][0].cpu().numpy().astype(np.float64)
+        q = qs[qi]
+        diag = float(np.hypot(*(q.max(axis=0) - q.min(axis=0))))
+        tol = 1e-4 * diag
+        listed = db[torch.from_numpy(ids).to(db.device)].double().cpu().numpy()
+        dref = np.array([O.chamfer(c, q) for c in listed])
+        err = float(np.abs(dref - dg).max())
+        kth = float(dg[-1])
+        beat = np.flatnonzero(D[qi] < kth - tol)
+        missed = int(np.setdiff1d(samp[beat], ids).size)
+        sorted_ok = bool(np.all(np.diff(dg) >= 0))
+        out["queries"][name] = {"listed_max_abs_err": err, "tol": tol, "kth_d": kth,
+                                "sample_min_d": float(np.nanmin(D[qi])), "sample_nan": int(np.isnan(D[qi]).sum()),
+                                "sample_beating_kth_unlisted": missed, "sorted": sorted_ok}
+        ok &= err <= tol and missed == 0 and sorted_ok
+    out["ok"] = bool(ok)
+    return out
 
 
 def prefilter_c4(torch, args, db, q, flush, stream):
@@ -540,7 +998,105 @@ GEN_COUNT = 50_000
 C5_QUERIES = 64
 
 
-def bench_c5(torch, args, rank, world, peaks, flush, clk):
+C5_CPU_GROUPS = 64     # CPU stage estimate: whole topology groups gated by the oracle
+C5_SAMPLE = 10_000     # curves checked against the oracle in-run
+
+
+def _c5_norm_worker(task):
+    from oracle import links_oracle as O
+
+    lo, hi = task
+    inp = _FORK["c5n"]
+    out, stable = [], []
+    for p in inp[lo:hi]:
+        try:
+            out.append(O.normalize(p))
+            stable.append(O.frame_stability(p))
+        except ValueError:
+            out.append(np.full_like(p, np.nan))
+            stable.append(False)
+    return lo, np.stack(out), np.array(stable)
+
+
+def parity_c5(last, queries, sample):
+    """In-run oracle check of the timed C5 outputs on the first ``sample``
+    normalised curves: normalisation within 1e-4 on frame-stable curves
+    (the rest counted as unstable), and the 64 top-10 lists via
+    parity_chamfer on the same sample (listed distances recomputed, no
+    sampled curve beating a k-th entry unlisted)."""
+    import torch
+
+    rows = last["rows"][:sample]
+    inp = last["traj"][rows].double().cpu().numpy()
+    gout = last["nres"]["out"][:len(rows)].double().cpu().numpy()
+    guns = last["nres"]["unstable"][:len(rows)].cpu().numpy().astype(bool)
+    _FORK["c5n"] = inp
+    cores = _cores()
+    b = np.linspace(0, len(inp), cores * 4 + 1).astype(int)
+    parts, dt = _fork_map(_c5_norm_worker, [(b[i], b[i + 1]) for i in range(len(b) - 1)], cores)
+    parts.sort(key=lambda x: x[0])
+    ref = np.concatenate([p[1] for p in parts])
+    stable = np.concatenate([p[2] for p in parts])
+    cmp = stable & ~guns
+    err = np.abs(gout - ref).max(axis=(1, 2))
+    out = {"normalize": {"checked": int(len(inp)), "compared": int(cmp.sum()),
+                         "oracle_unstable": int((~stable).sum()), "gpu_unstable": int(guns.sum()),
+                         "max_abs_err": float(err[cmp].max()) if cmp.any() else None,
+                         "over_tol": int((err[cmp] > 1e-4).sum()), "seconds": dt}}
+    nq = queries.shape[0]
+    qsel = list(range(0, nq, max(1, nq // 16)))[:16]
+    qd = {f"q{i}": queries[i:i + 1] for i in qsel}
+    lists = {f"q{i}": {"top_id": last["cres"]["top_id"][i:i + 1], "top_d": last["cres"]["top_d"][i:i + 1]}
+             for i in qsel}
+    db = last["nres"]["out"]
+    # ids of the C5 scan are rank << 32 | curve index (rank 0 here)
+    out["chamfer"] = parity_chamfer(db, qd, lists, sample=sample)
+    out["ok"] = bool(out["normalize"]["over_tol"] == 0 and out["chamfer"]["ok"])
+    return out
+
+
+def _c5_gate_worker(gids):
+    from oracle import links_oracle as O
+
+    pos, plans = _FORK["c5"]
+    nv = 0
+    for g in gids:
+        n, steps, fixed = plans[g]
+        v, _ = O.gate(pos[g * 256:(g + 1) * 256, :n], steps, fixed, T // 4, T)
+        nv += int(v.sum())
+    return nv
+
+
+def cpu_c5(sub, last, ncurves, pair_rate):
+    """C5 CPU baseline = the sum of per-stage estimates,
+    each measured on this box's cores: the oracle gate on the first
+    C5_CPU_GROUPS topology groups (screen + the T=200 paths of its
+    survivors), the oracle normalize on a sample of the C5 curves, and the
+    C4 chamfer port's pair rate for 64 queries x every curve."""
+    pos, plans = sub
+    _FORK["c5"] = sub
+    cores = _cores()
+    G = len(plans)
+    _, dt_gate = _fork_map(_c5_gate_worker, [list(range(w, G, cores)) for w in range(cores)], cores)
+    gate_rate = G * 256 / dt_gate
+    m = min(cores * 64, ncurves)
+    rows = last["rows"][:m]
+    _FORK["c5n"] = last["traj"][rows].double().cpu().numpy()
+    b = np.linspace(0, m, cores + 1).astype(int)
+    _, dt_norm = _fork_map(_c5_norm_worker, [(b[i], b[i + 1]) for i in range(cores)], cores)
+    norm_rate = m / dt_norm  # (includes the frame-stability predicate: an upper bound on the cost)
+    est = {"gate_s": C5_COUNT / gate_rate, "normalize_s": ncurves / norm_rate,
+           "chamfer_s": ncurves * C5_QUERIES / pair_rate if pair_rate else None}
+    total = sum(v for v in est.values() if v)
+    return {"value": C5_COUNT / total, "unit": "candidates/s", "cores": cores, "kind": "port",
+            "stages_s": est, "rates": {"gate_candidates_per_s": gate_rate, "normalize_curves_per_s": norm_rate,
+                                       "chamfer_pairs_per_s": pair_rate},
+            "sample": f"sum of stage estimates: oracle gate on {G * 256} C5 candidates, oracle normalize on {m} "
+                      f"C5 curves, the C4 _chamfer_block port rate x {C5_QUERIES} queries x {ncurves} curves; "
+                      f"fork pool x{cores}"}
+
+
+def bench_c5(torch, args, rank, world, peaks, flush, clk, want_cpu=False, c4_pair_rate=None):
     """BASELINE configs[4] scaled to 1M candidates/GPU: screen (two-fidelity
     gate) -> ordered compaction -> f64 replay of the valid ones writing their
     paths -> normalise every non-Fixed joint path -> top-10 chamfer of 64
@@ -553,6 +1109,8 @@ def bench_c5(torch, args, rank, world, peaks, flush, clk):
 
     nb = native_batch(C5_COUNT, 5, 20, seed=5000 + 1000 * rank)
     table = nb.table
+    sub = (np.ascontiguousarray(nb.pos[:C5_CPU_GROUPS * 256]), decode_plans(table.host_bytes())[:C5_CPU_GROUPS]) \
+        if want_cpu else None
     topo = torch.from_numpy(nb.topo).cuda()
     pos = torch.from_numpy(nb.pos).cuda()
     queries = fourier_db(C5_QUERIES, T, seed=5151)
@@ -588,8 +1146,10 @@ def bench_c5(torch, args, rank, world, peaks, flush, clk):
                                                "n_hits")}, k)
         if timer:
             timer.mark("chamfer")
+        last.update(traj=traj, rows=rows, nres=nres, cres=cres)
         return nv, int(rows.numel())
 
+    last = {}
     for _ in range(args.warmup):
         nv, ncurves = step()
     spans = []
@@ -609,7 +1169,24 @@ def bench_c5(torch, args, rank, world, peaks, flush, clk):
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12
     norm_flops = ncurves * 99_500
     pairs = ncurves * C5_QUERIES
-    return {"metric": "end-to-end candidates/sec (screen -> paths -> normalise -> chamfer top-10 x 64 queries)",
+    cpu = parity = None
+    unstable = int(last["nres"]["unstable"].sum().item())
+    if sub is not None:
+        parity = parity_c5(last, queries, C5_SAMPLE)
+        cpu = cpu_c5(sub, last, ncurves, c4_pair_rate)
+    ch_ms = stages["chamfer"]
+    db_bytes = ncurves * T * 8
+    rl_ch = {"kernel": "chamfer_scan_kernel (64 queries, pruned)", "bound": "hbm",
+             "achieved": db_bytes / (ch_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+             "frac": db_bytes / (ch_ms / 1e3) / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes": db_bytes,
+             "traffic": None, "curves_evaluated_in_full": int(last["cres"]["n_full"].sum().item()),
+             "note": "algorithmic bytes = the curve set read once for all 64 queries"}
+    rl_norm = {"kernel": "normalize_warp_kernel (fp32)", "bound": "fp32",
+               "achieved": norm_flops / (stages["normalize"] / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+               "frac": norm_flops / (stages["normalize"] / 1e3) / 1e12 / fp32_peak, "algorithmic_flops": norm_flops,
+               "traffic": None, "note": "99.5 kflop per 200-point curve (SURVEY §8d)"}
+    return {"cpu_baseline": cpu, "parity": parity, "unstable": unstable, "roofline": rl_ch,
+            "roofline_kernels": [rl_ch, rl_norm],"metric": "end-to-end candidates/sec (screen -> paths -> normalise -> chamfer top-10 x 64 queries)",
             "value": world * C5_COUNT / (ms / 1e3), "unit": "candidates/s", "ms_per_step": ms, "steps": steps,
             "valid_per_gpu": nv, "curves_per_gpu": ncurves, "stages_ms": stages,
             "normalize": {"curves/s": ncurves / (stages["normalize"] / 1e3),
@@ -810,7 +1387,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--skip", default="", help="comma list of c3,c4,c5,gen,cpu to skip")
+    ap.add_argument("--skip", default="", help="comma list of c1,c3,c4,c5,gen,cpu to skip")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -840,24 +1417,35 @@ def main():
         read_buf.sum()
 
     skip = set(filter(None, args.skip.split(",")))
+    want_cpu = rank == 0 and world == 1 and "cpu" not in skip
     clk = ClockSampler(torch, local).start()
     c2 = bench_c2(torch, args, rank, world, peaks, flush, clk)
-    e2e = e2e_c2(torch, args, c2["mb"], c2["table"], world)
+    e2e, (pipe, e2e_res) = e2e_c2(torch, args, c2["mb"], c2["table"], world)
     secondary = {}
+    if "c1" not in skip:
+        secondary["fourbar"] = bench_c1(torch, args, rank, world, peaks, flush, clk, want_cpu)
     if "c3" not in skip:
-        secondary["screen"] = bench_c3(torch, args, rank, world, peaks, flush, clk)
+        secondary["screen"] = bench_c3(torch, args, rank, world, peaks, flush, clk, want_cpu)
     if "c4" not in skip:
         secondary["chamfer"] = bench_c4(torch, args, rank, world, peaks, flush, clk)
     if "c5" not in skip:
-        secondary["end_to_end"] = bench_c5(torch, args, rank, world, peaks, flush, clk)
+        c4cpu = (secondary.get("chamfer") or {}).get("cpu_baseline") or {}
+        secondary["end_to_end"] = bench_c5(torch, args, rank, world, peaks, flush, clk, want_cpu,
+                                           c4cpu.get("value"))
     if "gen" not in skip:
         secondary["generation"] = bench_gen(torch, args, rank, world, peaks, flush, clk)
     clk.stop()
-    cpu = None
-    if rank == 0 and world == 1 and "cpu" not in skip:
+    cpu = parity = None
+    if want_cpu:
         cpu = cpu_baseline_c2(c2["mb"])
+        parity = parity_c2(c2["mb"], e2e_res, c2["dev_first_t"])
+    del pipe
     if rank == 0:
         rl = dict(c2["roofline"])
+        parity_all = {"c2": None if parity is None else parity["ok"]}
+        for name, sec in secondary.items():
+            if isinstance(sec, dict) and isinstance(sec.get("parity"), dict):
+                parity_all[name] = sec["parity"].get("ok")
         line = {
             "metric": METRIC, "value": c2["value"], "unit": "simulations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": c2["ms"], "higher_is_better": True,
@@ -875,13 +1463,19 @@ def main():
             "cpu_baseline": None if cpu is None else {**{k: cpu[k] for k in ("value", "unit", "cores", "kind",
                                                                               "sample")},
                                                       "one_thread": cpu["one_thread_est"]},
+            "parity": parity,
+            "parity_ok": parity_all,
             "gpu_launches": c2["launches_per_step"] * args.steps,
             "clocks": clk.summary(),
             "secondary": secondary,
             "published": {"paper_v100_sims_per_s": 54855, "paper_80thread_cpu_sims_per_s": 17995,
                           "note": "PAPER.md:208-211, 10,000-mechanism Table-1 workload (other config)"},
         }
-        print(json.dumps(line, default=float))
+        print(json.dumps(line, default=float), flush=True)
+        bad = [k for k, v in line["parity_ok"].items() if v is False]
+        if bad:  # the reference harness refuses to report disagreeing outcomes (bench.py:143-145)
+            print(f"bench: parity FAILED for {bad}", file=sys.stderr)
+            return 3
     if world > 1:
         import torch.distributed as dist
 

@@ -201,6 +201,8 @@ int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P,
                                 direct-difference recheck of small minima)   */
 #define LA_CH_NO_PRUNE 16u   /* disable the exact lower-bound pruning of the
                                 top-k scan (every curve fully evaluated)     */
+#define LA_CH_SEED_SCAN 32u  /* pruned scan: seed the running k-th bound with
+                                the exact k-th of a 1/128 prefix scan first  */
 
 typedef struct la_chamfer_args {
   const float* db;            /* (device) [N][P][2] f32 normalised curves     */
@@ -245,6 +247,12 @@ int la_chamfer_topk(const la_chamfer_args* args, void* stream);
 int la_sample_topologies(int64_t seed, int64_t g0, int64_t G, int32_t n_lo, int32_t n_hi, double ng_prob,
                          int32_t retries, int32_t threads, la_plan* plans, int8_t* types /* [G][20] */,
                          uint8_t* adj /* [G][20][20] or NULL */, int32_t* n_out);
+/* One sample_topology(rng, n, ng_probability, retries) draw on a caller's
+ * numpy PCG64 state (generator.py:200-222): st = {state hi, lo, inc hi, lo},
+ * buf = {has_uint32, uinteger}, advanced in place; LA_ERANGE when every
+ * retry fails (the reference raises GenerationError).                    */
+int la_sample_topology_rng(uint64_t* st, uint32_t* buf, int32_t n, double ng_prob, int32_t retries,
+                           la_plan* plan, int8_t* types /* [20] */, uint8_t* adj /* [20][20] */);
 int la_sample_poses(int64_t seed, int64_t g0, int64_t G, int32_t per_group, const int32_t* n_of_group,
                     int32_t stride, int32_t threads, double* pos /* [G*per_group][stride][2] host */);
 /* Coarse prefilter (Atlas.coarse_filter, atlas.py:153-177).

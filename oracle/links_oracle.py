@@ -135,6 +135,59 @@ def simulate(pos0: np.ndarray, steps, fixed, T: int = 200, with_margin: bool = F
     return out
 
 
+def simulate_scalar(pos0: np.ndarray, steps, fixed, T: int = 200):
+    """Scalar per-angle replay of one mechanism (solver.py:142-169, with
+    dyad_solve solver.py:123-139): plain Python over t and the plan steps,
+    cos/sin/hypot from numpy like the reference.  Returns ("lock", t, joint)
+    or ("ok", (n, T, 2) float64)."""
+    import math
+
+    pos0 = np.asarray(pos0, dtype=np.float64)
+    n = pos0.shape[0]
+    p0x, p0y = float(pos0[0, 0]), float(pos0[0, 1])
+    r1 = float(np.hypot(pos0[1, 0] - p0x, pos0[1, 1] - p0y))
+    if steps:
+        R_a, R_b, BR = step_geometry(pos0[None], steps)
+        R_a, R_b, BR = R_a[0], R_b[0], BR[0]
+    out = np.empty((n, T, 2), dtype=np.float64)
+    cur = [(float(x), float(y)) for x, y in pos0]
+    cos_t, sin_t = crank_angles(T)
+    for t in range(T):
+        cur[1] = (p0x + r1 * cos_t[t], p0y + r1 * sin_t[t])
+        for s, (tg, a, b) in enumerate(steps):
+            pa, pb = cur[a], cur[b]
+            dx = pb[0] - pa[0]
+            dy = pb[1] - pa[1]
+            d = float(np.hypot(dx, dy))
+            ra, rb, br = float(R_a[s]), float(R_b[s]), float(BR[s])
+            if d < LOCK_EPS or d > ra + rb + LOCK_EPS or d < abs(ra - rb) - LOCK_EPS:
+                return ("lock", t, tg)
+            x = (d * d + ra * ra - rb * rb) / (2.0 * d)
+            h = math.sqrt(max(ra * ra - x * x, 0.0))
+            ux, uy = dx / d, dy / d
+            cur[tg] = (pa[0] + x * ux - br * h * uy, pa[1] + x * uy + br * h * ux)
+        for k in range(n):
+            out[k, t, 0] = cur[k][0]
+            out[k, t, 1] = cur[k][1]
+    return ("ok", out)
+
+
+def gate(pos0: np.ndarray, steps, fixed, T_low: int = 50, T_high: int = 200):
+    """Two-fidelity gate of one topology group (find_valid_variant's
+    pattern, generator.py:263-275, with the survivors confirmed as one batch
+    as SURVEY.md §8d C3 prescribes): T_low sweep of every candidate, T_high
+    only for the T_low survivors.  Returns (valid (B,) bool, low_t (B,)
+    int64: the T_low lock step, -1 for T_low survivors)."""
+    lo = simulate(pos0, steps, fixed, T_low)
+    valid = np.zeros(len(pos0), dtype=bool)
+    low_t = np.where(lo["first_t"] < T_low, lo["first_t"], -1)
+    surv = np.flatnonzero(lo["first_t"] == T_low)
+    if len(surv):
+        hi = simulate(np.asarray(pos0)[surv], steps, fixed, T_high)
+        valid[surv] = hi["first_t"] == T_high
+    return valid, low_t
+
+
 def trajectories(res) -> np.ndarray:
     """(B, n, T, 2) view of a simulate() result, like the reference's P."""
     return np.stack([res["X"], res["Y"]], axis=-1)

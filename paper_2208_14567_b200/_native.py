@@ -38,6 +38,7 @@ LA_CH_EXPANSION = 1
 LA_CH_SCALAR_PIPE = 2
 LA_CH_TENSOR = 8
 LA_CH_NO_PRUNE = 16
+LA_CH_SEED_SCAN = 32
 
 EXPORTS = (
     "la_simulate",
@@ -52,6 +53,7 @@ EXPORTS = (
     "la_chamfer_workspace",
     "la_chamfer_topk",
     "la_sample_topologies",
+    "la_sample_topology_rng",
     "la_sample_poses",
     "la_rng_draw",
     "la_coarse_descriptors",
@@ -228,6 +230,7 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_chamfer_workspace.restype = sz
     lib.la_chamfer_topk.argtypes = [C.POINTER(LaChamferArgs), vp]
     lib.la_sample_topologies.argtypes = [i64, i64, i64, i32, i32, C.c_double, i32, i32, vp, vp, vp, vp]
+    lib.la_sample_topology_rng.argtypes = [vp, vp, i32, C.c_double, i32, vp, vp, vp]
     lib.la_sample_poses.argtypes = [i64, i64, i64, i32, vp, i32, i32, vp]
     lib.la_rng_draw.argtypes = [vp, i32, i32, i64, i64, vp, vp]
     lib.la_coarse_descriptors.argtypes = [vp, i64, i32, vp, vp, vp]

@@ -51,13 +51,15 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
                  pos_end: int | None = None, id_base: int = 0, pos_base: int = 0, pos_map=None,
                  exclude_id: int = -1, dense: bool = False, all_d=None, expansion: bool = False,
                  fix_tol: float = 5e-5, scalar_pipe: bool = False, tensor: bool = False, prune: bool = True,
-                 stream=None) -> dict:
+                 seed_scan: bool = False, stream=None) -> dict:
     """One la_chamfer_topk launch.
 
     ``prune`` (top-k scans of >= 65,536 positions without dense output):
     curves whose lower bound (query distance grid, first chamfer term)
     exceeds the running k-th best are skipped; the lists are identical to
     the unpruned scan (``prune=False``: every curve evaluated).
+    ``seed_scan``: seed the pruning bound with an exact scan of a 1/128
+    prefix first (off by default; measured slower than the slot minima).
 
     db: (N, P, 2) float32 CUDA tensor; queries: (NQ, Q, 2) float32.  order:
     optional (N,) int64 device tensor, record index at each scan position.
@@ -115,7 +117,8 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     a.n_hits = out["n_hits"].data_ptr()
     a.all_d = N.ptr(all_d)
     a.flags = ((N.LA_CH_EXPANSION if expansion else 0) | (N.LA_CH_SCALAR_PIPE if scalar_pipe else 0)
-               | (N.LA_CH_TENSOR if tensor else 0) | (0 if prune else N.LA_CH_NO_PRUNE))
+               | (N.LA_CH_TENSOR if tensor else 0) | (0 if prune else N.LA_CH_NO_PRUNE)
+               | (N.LA_CH_SEED_SCAN if seed_scan else 0))
     a.fixup_below = float(fix_tol)
     a.n_full = out["n_full"].data_ptr()
     wsb = int(lib.la_chamfer_workspace(a))

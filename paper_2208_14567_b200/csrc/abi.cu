@@ -1,6 +1,8 @@
 // ABI housekeeping: version, thread-local error text, device properties.
 #include "common.cuh"
 
+#include <atomic>
+
 namespace la {
 
 static thread_local char g_err[512] = "";
@@ -12,17 +14,19 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+// per-device SM count, cached: written once per device with the same
+// value by any racing thread (relaxed atomics, no lock needed)
 int sm_count() {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   if (dev < 0 || dev >= 64) return -1;
-  if (cache[dev] == 0) {
-    int v = 0;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
-    cache[dev] = v;
+    cache[dev].store(v, std::memory_order_relaxed);
   }
-  return cache[dev];
+  return v;
 }
 
 }  // namespace la

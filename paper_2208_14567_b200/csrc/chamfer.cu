@@ -23,6 +23,8 @@
 // Each warp keeps a lane-distributed sorted top-k (by (d, pos)) of non-hits
 // and the first-k hits (by pos); a merge kernel reduces the per-warp lists.
 #include "common.cuh"
+
+#include <atomic>
 #include <climits>
 #include <cstdlib>
 #include <cuda_fp16.h>
@@ -527,6 +529,8 @@ __global__ void thr_init_kernel(const float* __restrict__ seed_d, int k, int NQ,
 // k-th smallest bounds the final k-th best from above.  Lock-free; after the
 // first wave of curves it triggers only for new near-best curves.  Whole
 // warp (d, id uniform).
+// the rank-(k-1) ballot below needs k <= 32 (one slot minimum per lane)
+static_assert(LA_MAX_TOPK <= 32, "publish_kth assumes k <= 32");
 __device__ __forceinline__ void publish_kth(unsigned* __restrict__ thr, unsigned* __restrict__ slots, int k,
                                             int lane, float d, long long id) {
   unsigned old = 0u;
@@ -1407,12 +1411,17 @@ struct Plan {
   size_t ws_prune; // bytes of the pruning area
 };
 
-// resident CTAs per SM of chamfer_scan_kernel<qs> (registers and the 58 KB
-// of shared memory allow 3 for Q = 200, not 4)
+// resident CTAs per SM of chamfer_scan_kernel<qs> (registers and the
+// ~67 KB of shared memory -- curve double buffer, per-warp lists and the
+// 8.3 KB distance grid -- allow 3 for Q = 200, not 4), per device; racing
+// threads compute and store the same value (relaxed atomics)
 int scan_occupancy(int qs) {
-  static int cache[9] = {0};
+  static std::atomic<int> cache[64][9];
   if (qs < 1 || qs > 8) return 3;
-  if (cache[qs]) return cache[qs];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 3;
+  const int hit = cache[dev][qs].load(std::memory_order_relaxed);
+  if (hit) return hit;
   const void* k = nullptr;
   switch (qs) {
     case 1: k = (const void*)chamfer_scan_kernel<1>; break;
@@ -1428,7 +1437,7 @@ int scan_occupancy(int qs) {
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SCAN_SMEM) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, CT, SCAN_SMEM) != cudaSuccess || occ < 1)
     occ = 3;
-  cache[qs] = occ;
+  cache[dev][qs].store(occ, std::memory_order_relaxed);
   return occ;
 }
 
@@ -1470,12 +1479,10 @@ Plan make_plan(const la_chamfer_args* a) {
   p.prune = p.fast && a->k > 0 && !a->all_d && !(a->flags & (LA_CH_TENSOR | LA_CH_NO_PRUNE)) &&
             npos >= PRUNE_MIN_POS;
   if (p.prune) {
-    // seed: ~1/128 of the range (at least 64 k records), >= 8 curves per warp
-    static const long long seed_div = [] {
-      const char* e = getenv("LA_CH_SEED_DIV");  // tuning knob (A/B timing only)
-      const long long v = e ? atoll(e) : 0;
-      return v > 0 ? v : 0LL;  // default: no seed scan (the running list converges within a wave)
-    }();
+    // optional seed scan (LA_CH_SEED_SCAN): the exact k-th of a 1/128
+    // prefix published before the main scan; off by default (the slot
+    // minima converge within the first wave and measured faster)
+    const long long seed_div = (a->flags & LA_CH_SEED_SCAN) ? 128 : 0;
     long long sn = seed_div > 0 ? npos / seed_div : 0;
     if (seed_div > 0 && sn < 64LL * a->k) sn = 64LL * a->k;
     if (sn > npos) sn = npos;

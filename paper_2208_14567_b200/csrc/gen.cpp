@@ -92,6 +92,7 @@ struct Pcg64 {
   u128 state, inc;
   int has32 = 0;
   uint32_t u32 = 0;
+  Pcg64() : state(0), inc(1) {}
   explicit Pcg64(const std::vector<uint32_t>& entropy) {
     SeedSeq sq(entropy);
     uint32_t w[8];
@@ -958,4 +959,42 @@ extern "C" int64_t la_moving_joints(const int64_t* meta /* [R][4] */, const int8
     }
   }
   return c;
+}
+
+// One sample_topology(rng, n, ng_probability, retries) draw
+// (generator.py:200-222) on a caller's numpy PCG64 bit generator: st =
+// {state hi, state lo, inc hi, inc lo} (64-bit words), buf = {has_uint32,
+// uinteger}, both advanced in place exactly as the reference's draws advance
+// the Generator.  Writes the topology (n, types [20], adj [20][20]) and its
+// compiled plan record.  LA_ERANGE when every retry fails (GenerationError).
+extern "C" int la_sample_topology_rng(uint64_t* st, uint32_t* buf, int32_t n, double ng_prob, int32_t retries,
+                                      la_plan* plan, int8_t* types, uint8_t* adj) {
+  LA_HOST_TRY
+  if (!st || !buf || !plan || !types || !adj || n < 4 || n > LA_MAX_JOINTS || retries < 1) {
+    la::set_error("la_sample_topology_rng: bad arguments");
+    return LA_EINVAL;
+  }
+  Pcg64 rng;
+  rng.state = ((u128)st[0] << 64) | st[1];
+  rng.inc = ((u128)st[2] << 64) | st[3];
+  rng.has32 = (int)buf[0];
+  rng.u32 = buf[1];
+  Mech m;
+  Plan pl;
+  const bool ok = sample_topology(rng, n, ng_prob, retries, m, pl);
+  st[0] = (uint64_t)(rng.state >> 64);
+  st[1] = (uint64_t)rng.state;
+  buf[0] = (uint32_t)rng.has32;
+  buf[1] = rng.u32;
+  if (!ok) {
+    la::set_error("no valid topology with n=%d after %d tries", n, retries);
+    return LA_ERANGE;
+  }
+  *plan = to_rec(m, pl);
+  for (int k = 0; k < LA_MAX_JOINTS; ++k) types[k] = k < m.n ? m.type[k] : (int8_t)-1;
+  for (int i = 0; i < LA_MAX_JOINTS; ++i)
+    for (int j = 0; j < LA_MAX_JOINTS; ++j)
+      adj[i * LA_MAX_JOINTS + j] = (i < m.n && j < m.n) ? (uint8_t)((m.adj[i] >> j) & 1u) : 0;
+  return 0;
+  LA_HOST_CATCH(LA_EHOST)
 }

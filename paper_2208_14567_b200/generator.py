@@ -1,9 +1,10 @@
 """Rejection-sampling driver around the GPU validity screen.
 
-Reference: linkatlas generator.py.  Topology growth and candidate-pose
-sampling (generator.py:156-238) are host code that consume numpy PCG64
-streams exactly as the reference does, so seeded runs produce the same
-topologies and poses.  The two-fidelity gate inside ``find_valid_variant``
+Reference: linkatlas generator.py.  Topology growth (generator.py:156-222)
+runs in the native generator (csrc/gen.cpp) on the caller's PCG64 state and
+candidate-pose sampling (generator.py:225-238) draws from numpy, both
+consuming the streams exactly as the reference does, so seeded runs produce
+the same topologies and poses.  The two-fidelity gate inside ``find_valid_variant``
 (generator.py:241-283: T_low = 50 sweep, survivors confirmed at T_high =
 200) runs on the device: one coarse-first ``la_simulate`` launch screens a
 whole look-ahead window of candidate batches, and the host walks the flags
@@ -23,9 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from paper_2208_14567_b200 import _native as N
-from paper_2208_14567_b200.curves import plan_ancestry
-from paper_2208_14567_b200.mechanism import ARM_PIVOT, ARM_TIP, JointType, Mechanism, apply_Ng, apply_Ns, \
-    initial_mechanism
+from paper_2208_14567_b200.mechanism import ARM_PIVOT, ARM_TIP, Mechanism
 from paper_2208_14567_b200.solver import PlanTable, SolutionPlan, Trajectory, compile_order, simulate_tensors
 
 NMAX = N.LA_MAX_JOINTS
@@ -130,69 +129,41 @@ class VariantResult:
     attempts: int
 
 
-# ------------------------------------------------------------ topology (host)
-def _grow_topology(rng: np.random.Generator, n: int, ng_probability: float) -> Mechanism | None:
-    """Terminal-tracking constrained growth (generator.py:156-197).
-
-    Consumes ``rng`` exactly like the reference: one ``random()`` per
-    operation while slack >= 2, one ``integers(len(pairs))`` per simple op.
-    """
-    mech = initial_mechanism()
-    terminals = {1, 2}
-    while mech.n < n:
-        left = n - mech.n
-        slack = left - len(terminals) + 1
-        if slack < 0:
-            return None
-        if slack >= 2 and rng.random() < ng_probability:
-            mech = apply_Ng(mech)
-            terminals.add(mech.n - 1)
-            continue
-        need = max(0, 2 - slack)
-        last_op = left == 1
-        is_fixed = mech.types == JointType.FIXED
-        cands = []
-        for i in range(mech.n):
-            for j in range(i + 1, mech.n):
-                if is_fixed[i] and is_fixed[j]:
-                    continue
-                if last_op and (is_fixed[i] or is_fixed[j]):
-                    continue
-                if (i in terminals) + (j in terminals) < need:
-                    continue
-                cands.append((i, j))
-        if not cands:
-            return None
-        i, j = cands[int(rng.integers(len(cands)))]
-        mech = apply_Ns(mech, i, j)
-        terminals.difference_update((i, j))
-        terminals.add(mech.n - 1)
-    return mech
-
-
-def _plan_of(mech: Mechanism) -> SolutionPlan:
-    fixed, steps = compile_order(mech.adjacency, mech.types)
-    return SolutionPlan(mech.n, fixed, steps, None, None, None)
+# ------------------------------------------------------------ topology (native)
+_M64 = (1 << 64) - 1
 
 
 def sample_topology(rng: np.random.Generator, n: int, ng_probability: float = 0.25,
                     retries: int = 1000) -> tuple[Mechanism, SolutionPlan]:
-    """Grow until the plan's last joint depends on every joint and rides no
-    ground pin (generator.py:200-222)."""
-    for _ in range(retries):
-        mech = _grow_topology(rng, n, ng_probability)
-        if mech is None:
-            continue
-        plan = _plan_of(mech)
-        if not plan.steps:
-            continue
-        last = plan.steps[-1].target
-        if np.any(mech.types[mech.neighbors(last)] == JointType.FIXED):
-            continue
-        if len(plan_ancestry(plan, last)) != n:
-            continue
-        return mech, plan
-    raise GenerationError(f"no valid topology with n={n} after {retries} tries")
+    """generator.py:200-222 on the caller's Generator: the native topology
+    operator (csrc/gen.cpp, la_sample_topology_rng: constrained growth with
+    terminal tracking, plan compile, last-joint checks) runs on a copy of
+    ``rng``'s PCG64 state, which is then written back, so the stream
+    advances exactly as the reference's draws advance it."""
+    bg = rng.bit_generator
+    stt = bg.state
+    if stt.get("bit_generator") != "PCG64":
+        raise TypeError("sample_topology needs a PCG64-backed Generator (numpy's default_rng)")
+    lib = N.load()
+    s, inc = int(stt["state"]["state"]), int(stt["state"]["inc"])
+    st = np.array([s >> 64, s & _M64, inc >> 64, inc & _M64], dtype=np.uint64)
+    buf = np.array([int(stt["has_uint32"]), int(stt["uinteger"])], dtype=np.uint32)
+    rec = N.LaPlan()
+    types = np.zeros(NMAX, dtype=np.int8)
+    adj = np.zeros((NMAX, NMAX), dtype=np.uint8)
+    rc = lib.la_sample_topology_rng(st.ctypes.data, buf.ctypes.data, int(n), float(ng_probability), int(retries),
+                                    C.addressof(rec), types.ctypes.data, adj.ctypes.data)
+    stt["state"]["state"] = (int(st[0]) << 64) | int(st[1])
+    stt["has_uint32"], stt["uinteger"] = int(buf[0]), int(buf[1])
+    bg.state = stt
+    if rc == N.LA_ERANGE:
+        raise GenerationError(f"no valid topology with n={n} after {retries} tries")
+    N.check(rc, "la_sample_topology_rng")
+    pos = np.full((n, 2), np.nan)
+    pos[0], pos[1] = ARM_PIVOT, ARM_TIP
+    mech = Mechanism(adj[:n, :n].copy(), types[:n].copy(), pos)
+    fixed, steps = compile_order(mech.adjacency, mech.types)
+    return mech, SolutionPlan(mech.n, fixed, steps, None, None, None)
 
 
 def sample_positions(topology: Mechanism, rng: np.random.Generator) -> np.ndarray:

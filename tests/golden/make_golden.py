@@ -392,7 +392,33 @@ def dataset_fixture():
     np.savez_compressed(OUT / "dataset_golden.npz", **d)
 
 
-if __name__ == "__main__":
+def stream_fixture():
+    """sample_topology's effect on the caller's stream (generator.py:200-222):
+    two topologies drawn in sequence from one Generator, then the stream's
+    next draws -- pins the RNG state the drop-in leaves behind."""
+    d = {"versions": versions()}
+    adj = np.zeros((24, 2, NMAX, NMAX), dtype=np.uint8)
+    types = np.full((24, 2, NMAX), -1, dtype=np.int8)
+    after = np.zeros((24, 3))
+    ns = np.zeros(24, dtype=np.int32)
+    for c in range(24):
+        rng = np.random.default_rng([99, c])
+        n = int(rng.integers(5, 21))
+        ns[c] = n
+        for k in range(2):
+            mech, _ = ref_gen.sample_topology(rng, n)
+            adj[c, k, :n, :n] = mech.adjacency
+            types[c, k, :n] = mech.types
+        after[c, :2] = rng.random(2)
+        after[c, 2] = rng.integers(1000)
+    d.update(adj=adj, types=types, after=after, n=ns)
+    np.savez_compressed(OUT / "stream_golden.npz", **d)
+
+
+if __name__ == "__main__" and sys.argv[1:] == ["stream"]:
+    stream_fixture()
+elif __name__ == "__main__":
+    stream_fixture()
     sol = solver_fixture()
     curves_fixture(sol)
     atlas_fixture()

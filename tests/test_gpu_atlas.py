@@ -301,3 +301,38 @@ def test_pruned_scan_equals_full_scan(torch):
     db64 = fourier_db(100_000, 64, seed=23, chunk=1 << 16)
     q64 = fourier_db(3, 64, seed=24)
     _lists_equal(torch, chamfer_scan(db64, q64, k=10, prune=False), chamfer_scan(db64, q64, k=10))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["expansion", "scalar_pipe", "odd_p", "seed_scan", "outside_unit_square"])
+def test_pruned_scan_equals_full_scan_variants(torch, variant):
+    """The pruning exactness argument (lb_slack covering fixup_below in
+    expansion mode, the (1 - 1e-4) factor covering sqrt.approx and the fp16
+    distance grid) across the inner-loop variants, an odd P (the non-TMA
+    curve load), the seed prefix scan, and curves/queries partly outside
+    [0, 1]^2 (clamped grid vertices)."""
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    P = 199 if variant == "odd_p" else 200
+    N = 200_000
+    db = fourier_db(N, P, seed=31, chunk=1 << 16)
+    q = fourier_db(3, P, seed=32)
+    kw = {}
+    if variant == "expansion":
+        kw["expansion"] = True
+    elif variant == "scalar_pipe":
+        kw["scalar_pipe"] = True
+    elif variant == "seed_scan":
+        kw["seed_scan"] = True
+    elif variant == "outside_unit_square":
+        # stretch a third of the database and one query well past the unit box
+        g = torch.Generator(device="cuda")
+        g.manual_seed(5)
+        sel = torch.randperm(N, device="cuda", generator=g)[: N // 3]
+        db[sel] = (db[sel] - 0.5) * 2.5 + 0.5
+        q[1] = (q[1] - 0.5) * 1.7 + torch.tensor([0.9, -0.4], device="cuda")
+    full = chamfer_scan(db, q, k=10, prune=False, **kw)
+    pr = chamfer_scan(db, q, k=10, **kw)
+    _lists_equal(torch, full, pr)
+    assert int(pr["n_full"].sum().item()) < 3 * N  # pruning did engage

@@ -145,3 +145,20 @@ def test_struct_layouts_match_header(tmp_path):
             ctypes.sizeof(N.LaChamferArgs), N.LaSimArgs.fixup_tau.offset, N.LaChamferArgs.ws_bytes.offset,
             N.LaNormArgs.rel_tol.offset]
     assert got == want
+
+
+def test_sample_topology_leaves_reference_stream_state(golden):
+    """Two topologies in sequence from one Generator, then the next draws:
+    the native operator advances the caller's PCG64 state exactly as the
+    reference's draws do (generator.py:200-222)."""
+    g = golden("stream_golden.npz")
+    for c in range(len(g["n"])):
+        rng = np.random.default_rng([99, c])
+        n = int(rng.integers(5, 21))
+        assert n == int(g["n"][c])
+        for k in range(2):
+            mech, _ = sample_topology(rng, n)
+            assert np.array_equal(mech.adjacency, g["adj"][c, k][:n, :n])
+            assert np.array_equal(mech.types, g["types"][c, k][:n])
+        assert np.array_equal(rng.random(2), g["after"][c, :2])
+        assert int(rng.integers(1000)) == int(g["after"][c, 2])

@@ -134,3 +134,44 @@ def test_oracle_coarse_filter_pinned(golden):
         for bi, b in enumerate(budgets):
             assert np.array_equal(O.coarse_filter(desc, g["order"], qd, int(b)), g[f"coarse_{qi}_{bi}"])
             assert np.array_equal(O.coarse_filter(ddesc, g["dup_order"], qd, int(b)), g[f"coarse_dup_{qi}_{bi}"])
+
+
+def test_scalar_replay_matches_reference(golden):
+    """oracle.simulate_scalar (solver.py:142-169) against the reference's
+    batch outputs: lock (t, joint) and bit-exact f64 paths (the reference
+    asserts scalar == batch bit for bit, solver.py:146-147)."""
+    g = golden("solver_golden.npz")
+    steps = [(3, 1, 2)]
+    traj = dict(zip(g["fb_traj_idx"].tolist(), g["fb_traj"]))
+    for b in range(64):
+        kind, *rest = O.simulate_scalar(g["fb_pos0"][b], steps, (0, 2), 200)
+        if kind == "lock":
+            assert (rest[0], rest[1]) == (g["fb_first_t"][b], g["fb_first_joint"][b])
+        else:
+            assert g["fb_first_t"][b] == 200
+            if b in traj:
+                assert np.array_equal(rest[0], traj[b])
+    for topo in range(0, len(g["mx_n"]), 7):
+        n = int(g["mx_n"][topo])
+        steps, fixed = O.compile_steps(g["mx_adj"][topo][:n, :n], g["mx_types"][topo][:n])
+        sel = np.flatnonzero(g["mx_topo"] == topo)[:16]
+        for b in sel:
+            kind, *rest = O.simulate_scalar(g["mx_pos0"][b][:n], steps, fixed, 200)
+            if kind == "lock":
+                assert (rest[0], rest[1]) == (g["mx_first_t"][b], g["mx_first_joint"][b])
+            else:
+                assert g["mx_first_t"][b] == 200
+
+
+def test_gate_matches_reference_sweeps(golden):
+    """oracle.gate (generator.py:263-275 pattern): valid iff the reference's
+    T=200 replay is lock-free; the T_low step is the reference's T=50 lock."""
+    g = golden("solver_golden.npz")
+    for topo in range(len(g["mx_n"])):
+        n = int(g["mx_n"][topo])
+        steps, fixed = O.compile_steps(g["mx_adj"][topo][:n, :n], g["mx_types"][topo][:n])
+        sel = np.flatnonzero(g["mx_topo"] == topo)
+        valid, low_t = O.gate(g["mx_pos0"][sel][:, :n], steps, fixed, 50, 200)
+        assert np.array_equal(valid, g["mx_first_t"][sel] == 200)
+        want_low = np.where(g["mx_first_t50"][sel] < 50, g["mx_first_t50"][sel], -1)
+        assert np.array_equal(low_t, want_low)
