@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define LA_ABI_VERSION 1
+#define LA_ABI_VERSION 2
 #define LA_MAX_JOINTS 20   /* joints per mechanism (generator.py n_max default) */
 #define LA_MAX_STEPS 18    /* dyad steps per plan: n - |fixed| - 1 <= 18       */
 #define LA_MAX_TOPK 32
@@ -69,6 +69,9 @@ typedef struct la_plan {
                                       flags bit-identical to simulate_batch.
                                       Without it the f64 rounds use DFMA and
                                       Newton rsqrt (a few ulp; ~2x faster)   */
+#define LA_SIM_LANE_SCREEN 512u   /* screen with the lane-per-candidate kernel
+                                      (screen.cu) instead of the
+                                      warp-per-candidate one (lanes = angles) */
 #define LA_PENDING (-3)            /* first_t of a deferred coarse survivor    */
 
 /* Batched replay of compiled plans over (candidate x crank angle).
@@ -121,6 +124,11 @@ typedef struct la_sim_args {
                                  dyads); tau is the floor (default 2e-6).
                                  Trajectory rounds always run in f64        */
   uint32_t flags;             /* LA_SIM_*                                     */
+  int32_t screen_refill;      /* lane screen: refill free lanes once at least
+                                 this many are free (0 => 8)                 */
+  int32_t screen_replay;      /* lane screen: replay parked (ambiguous)
+                                 angles in f64 once at least this many lanes
+                                 are parked (0 => 4)                         */
 } la_sim_args;
 
 int la_simulate(const la_sim_args* args, void* stream);

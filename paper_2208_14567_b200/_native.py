@@ -28,7 +28,9 @@ LA_SIM_DEFER = 32
 LA_SIM_SCATTER = 64
 LA_SIM_WRITE_ONLY = 128
 LA_SIM_EXACT64 = 256
+LA_SIM_LANE_SCREEN = 512
 LA_PENDING = -3
+ABI_VERSION = 2
 LA_EINVAL = -1
 LA_ERANGE = -2
 LA_EWS = -3
@@ -148,6 +150,8 @@ class LaSimArgs(C.Structure):
         ("counters", C.c_void_p),
         ("fixup_tau", C.c_float),
         ("flags", C.c_uint32),
+        ("screen_refill", C.c_int32),
+        ("screen_replay", C.c_int32),
     ]
 
 
@@ -284,7 +288,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             raise NativeError(f"CUDA library missing: {LIB_PATH} (run python -m paper_2208_14567_b200.build_lib)")
         lib = C.CDLL(str(LIB_PATH))
         _declare(lib)
-        if lib.la_abi_version() != 1:
+        if lib.la_abi_version() != ABI_VERSION:
             raise NativeError("ABI version mismatch")
         _lib = lib
     return _lib

@@ -13,10 +13,10 @@
 // per-warp shared-memory column pos[joint][lane] (dynamic joint indices
 // without local-memory spills; conflict-free).
 //
-// Precision.  Screen angles are evaluated in fp32 with a running
-// first-order bound on each joint's fp32 position error (input rounding,
-// per-dyad rounding, amplification |x|(1+|x|/d)/h by flat dyads, a taint
-// mask separating amplified from clean joints).  A dyad whose margin
+// Precision.  Screen angles are evaluated in fp32 with a first-order bound
+// on each joint's fp32 position error, kept next to the position (input
+// rounding, per-dyad rounding, amplification |x|(1+|x|/d)/h of the parents'
+// error by flat dyads).  A dyad whose margin
 // min(ra+rb-d, d-|ra-rb|) is within tau + 3 E(parents) of a lock makes the
 // lane's angle ambiguous; ambiguous lanes below the round's first certain
 // lock are replayed in f64.  f64 rounds (replays, path writes, the all-f64
@@ -35,9 +35,11 @@
 // the remaining angles (screen) or all T angles in natural order writing
 // coalesced float2 paths (simulate).
 #include "common.cuh"
+#include "sim_common.cuh"
 #include <type_traits>
 
 namespace la {
+int launch_screen_lane(const la_sim_args& a, cudaStream_t s);  // screen.cu
 namespace {
 
 constexpr int NJ = LA_MAX_JOINTS;
@@ -56,7 +58,7 @@ struct __align__(16) StepRec {
   float df;              // |ra - rb|
   float c2;              // ra^2 - rb^2
   float ra2;             // branch sign * ra^2 (|ra2| = ra^2)
-  uint32_t pmask;        // 1 << a | 1 << b (parents, for error tainting)
+  uint32_t pmask;        // 1 << a | 1 << b (parents; informational)
   uint32_t a_off;        // byte offset of joint a's float2 column
   uint32_t b_off;
   uint32_t t_off;
@@ -85,8 +87,9 @@ struct Warp {
   WarpHead* h;
   unsigned char* cols;   // pos block
   int lane;
+  // fp32 rounds: (x, y) of the 16-byte slot (x, y, e, -); f64 rounds: double2
   __device__ __forceinline__ float2& p32(int j) const {
-    return reinterpret_cast<float2*>(cols)[j * 32 + lane];
+    return *reinterpret_cast<float2*>(reinterpret_cast<float4*>(cols) + j * 32 + lane);
   }
   __device__ __forceinline__ double2& p64(int j) const {
     return reinterpret_cast<double2*>(cols)[j * 32 + lane];
@@ -100,57 +103,6 @@ struct SimCtx {
   float r1f;
   float2 p0f;
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
-}
-// shared-space accesses by 32-bit address (one IADD per access in the dyad
-// loop instead of generic-pointer arithmetic); "memory" keeps them ordered
-// with the other shared-memory accesses of the warp
-__device__ __forceinline__ float2 lds_f2(uint32_t a) {
-  float2 v;
-  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void sts_f2(uint32_t a, float2 v) {
-  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
-}
-__device__ __forceinline__ float rsqrt_approx(float x) {
-  float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// fp32 screen error model (solve32): input rounding of the f64 pose and
-// crank tip, per-dyad rounding of the fp32 evaluation (unit-box magnitudes,
-// rsqrt/sqrt approximations included), and the margin's sensitivity factor
-// with a safety factor of 2 on the first-order bound.
-constexpr float kErr0 = 2e-7f;
-constexpr float kErrStep = 5e-7f;
-constexpr float kMarginK = 3.0f;
-__device__ __forceinline__ float sqrt_approx(float x) {
-  float y;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// f64 reciprocal square root: MUFU.RSQ64H seed + two Newton steps
-// (relative error ~1e-16; not correctly rounded, see dyads_f64)
-__device__ __forceinline__ double rsqrt_f64(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const double e = fma(-h, y * y, 0.5);
-    y = fma(y, e, y);
-  }
-  return y;
-}
 
 // f64 dyad replay of one angle (solver.py:205-231).
 //
@@ -222,7 +174,6 @@ __device__ __forceinline__ double2 crank_tip(const WarpHead& H, const SimCtx& C,
 // differ by a few ulp, amplified at most ~1e8-fold below that margin) is
 // the angle redone in the exact arithmetic.  The lock decision is therefore
 // the exact one, at fast-pass cost for almost every replay.
-constexpr double kExactTriage = 1e-7;
 
 template <bool EXACT>
 __device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, double ct, double st) {
@@ -270,31 +221,27 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
   bool fix = false;
   if (active) {
     const float2 c = cs32[t];
-    W.p32(1) = make_float2(fmaf(C.r1f, c.x, C.p0f.x), fmaf(C.r1f, c.y, C.p0f.y));
+    // each joint's slot holds its fp32 position and a first-order bound e on
+    // that position's error: static joints and the crank tip start at kErr0
+    // (inputs rounded to fp32); a dyad's target gets
+    //   e_t = max(kappa, 1) max(e_a, e_b) + kErrStep
+    // (its parents' error amplified by the dyad, plus its own rounding)
+    const uint32_t col = smem_u32(W.cols) + (uint32_t)W.lane * 16u;
+    sts_f2(col + 512u, make_float2(fmaf(C.r1f, c.x, C.p0f.x), fmaf(C.r1f, c.y, C.p0f.y)));
     const float tau = C.tau;
-    const uint32_t col = smem_u32(W.cols) + (uint32_t)W.lane * 8u;
-    // running first-order bound on the fp32 position error of any joint
-    // placed so far (inputs rounded to fp32, then each dyad amplifies the
-    // error of its two parents by kappa and adds its own rounding)
-    float err = kErr0;  // bound for "clean" joints (no amplifying dyad upstream)
-    // joints downstream of an amplifying dyad carry the separate bound
-    // err_t; the bitmask (parents' bits precomputed per step) tracks them
-    float err_t = 0.0f;
-    unsigned taint = 0u;
     int s = 0;
 #pragma unroll 1
     for (; s < C.ns; ++s) {
       const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
       const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].pmask);
-      const float2 pa = lds_f2(col + g1.y);
-      const float2 pb = lds_f2(col + g1.z);
+      const float4 pa = lds_f4(col + g1.y);
+      const float4 pb = lds_f4(col + g1.z);
       const float dx = pb.x - pa.x, dy = pb.y - pa.y;
       const float d2 = fmaf(dy, dy, dx * dx);
       const float inv = rsqrt_approx(d2);
       const float d = d2 * inv;
       const float m = fminf(g0.x - d, d - g0.y);
-      const bool tp = (taint & g1.x) != 0u;
-      const float ep = tp ? fmaxf(err_t, err) : err;
+      const float ep = fmaxf(pa.z, pb.z);
       // the margin moves by at most 2 ep (d from two parents) + rounding
       fix |= !(fabsf(m) >= fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
       if (m < 0.0f) {
@@ -310,16 +257,10 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
       // every later dependent step of this angle goes to the f64 replay.
       const float ax = fabsf(x);
       const float num = ax * fmaf(ax, inv, 1.0f);
-      // amplifying dyad (kappa = num / h > 1) or tainted parent: branch-free
-      // (most dyads amplify), the same arithmetic either way
-      const bool amp = tp || num > h;
-      const float et = fmaxf(err_t, fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep));
-      err_t = amp ? et : err_t;
-      taint |= amp ? 1u << (g1.w >> 8) : 0u;
-      err = amp ? err : err + kErrStep;
+      const float e = fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep);
       const float xi = x * inv;
       const float hb = copysignf(h, g0.w) * inv;
-      sts_f2(col + g1.w, make_float2(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y))));
+      sts_f4(col + g1.w, make_float4(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)), e, 0.f));
     }
     if (COUNT) {
       ++ctr.lane_angles;
@@ -347,17 +288,22 @@ __device__ __forceinline__ int solve64(const Warp& W, const SimCtx& C, const dou
                                        bool active) {
   if (!active) return -1;
   const WarpHead& H = *W.h;
-  W.p64(1) = crank_tip(H, C, cs[2 * t], cs[2 * t + 1]);
-  return dyads_f64<EXACT>(H, C, [&](int j) { return W.p64(j); }, [&](int j, double2 v) { W.p64(j) = v; });
+  // 32-bit shared addresses: column j of this lane at base + j * 512
+  const uint32_t base = smem_u32(W.cols) + (uint32_t)W.lane * 16u;
+  sts_d2(base + 512u, crank_tip(H, C, cs[2 * t], cs[2 * t + 1]));
+  return dyads_f64<EXACT>(H, C, [&](int j) { return lds_d2(base + ((uint32_t)j << 9)); },
+                          [&](int j, double2 v) { sts_d2(base + ((uint32_t)j << 9), v); });
 }
 
 __device__ __forceinline__ void fill_static32(const Warp& W) {
   const WarpHead& H = *W.h;
+  float4* slot = reinterpret_cast<float4*>(W.cols) + W.lane;
 #pragma unroll 1
   for (int k = 0; k < H.nstatic; ++k) {
     const int j = H.statics[k];
-    W.p32(j) = make_float2((float)H.p0[j].x, (float)H.p0[j].y);
+    slot[j * 32] = make_float4((float)H.p0[j].x, (float)H.p0[j].y, kErr0, 0.f);
   }
+  slot[32] = make_float4(0.f, 0.f, kErr0, 0.f);  // crank tip: error of its inputs
 }
 
 __device__ __forceinline__ void fill_static64(const Warp& W) {
@@ -382,11 +328,10 @@ __device__ __forceinline__ RoundLock round_lock(bool active, int lk) {
   return RoundLock{src, __shfl_sync(FULL, lk, src)};
 }
 
-__device__ __forceinline__ int fine_angle(int i) { return (i / 3) * 4 + 1 + (i % 3); }
 
 template <bool WRITE, bool SCREEN64>
 __host__ __device__ constexpr size_t col_bytes() {
-  return (WRITE || SCREEN64) ? sizeof(double2) : sizeof(float2);
+  return 16;  // one 16-byte slot per (joint, lane): double2, or fp32 (x, y, e, -)
 }
 
 template <bool WRITE, bool SCREEN64, bool WONLY, bool EXACT, bool COUNT>
@@ -489,9 +434,9 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
       r.c2 = (float)(ra * ra - rb * rb);
       r.ra2 = br < 0.0 ? -((float)ra * (float)ra) : (float)ra * (float)ra;
       r.pmask = (1u << ia_) | (1u << ib_);
-      r.a_off = (uint32_t)ia_ * 32u * (uint32_t)sizeof(float2);
-      r.b_off = (uint32_t)ib_ * 32u * (uint32_t)sizeof(float2);
-      r.t_off = (uint32_t)it_ * 32u * (uint32_t)sizeof(float2);
+      r.a_off = (uint32_t)ia_ * 512u;  // slot (joint, lane) at j * 512 + lane * 16
+      r.b_off = (uint32_t)ib_ * 512u;
+      r.t_off = (uint32_t)it_ * 512u;
       H.st[lane] = r;
     }
     {
@@ -583,11 +528,20 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
             break;
           }
           if (act) {
+            // row j of this candidate at out + j * T: one pointer step per
+            // joint, columns read by 32-bit shared address
+            uint32_t a = smem_u32(W.cols) + (uint32_t)lane * 16u;
+            if (out64) {
+              double2* o = out_d + t;
 #pragma unroll 1
-            for (int j = 0; j < C.n; ++j) {
-              const double2 v = W.p64(j);
-              if (out64) __stcs(out_d + (size_t)j * T + t, v);
-              else st_cs(out + (size_t)j * T + t, make_float2((float)v.x, (float)v.y));
+              for (int j = 0; j < C.n; ++j, a += 512u, o += T) __stcs(o, lds_d2(a));
+            } else {
+              float2* o = out + t;
+#pragma unroll 2
+              for (int j = 0; j < C.n; ++j, a += 512u, o += T) {
+                const double2 v = lds_d2(a);
+                st_cs(o, make_float2((float)v.x, (float)v.y));
+              }
             }
           }
         }
@@ -883,13 +837,14 @@ int la_simulate(const la_sim_args* a, void* stream) {
   const bool f64 = (a->flags & LA_SIM_FP64) != 0;
   const int njmax = a->pos_stride < NJ ? a->pos_stride : NJ;
   if (a->T > 2048) return fail(LA_ERANGE, "la_simulate: T=%d beyond 2048", a->T);
-  const size_t colb = (write || f64) ? sizeof(double2) : sizeof(float2);
+  const size_t colb = 16;
   if ((a->flags & LA_SIM_SCATTER) && !a->cand) return fail(LA_EINVAL, "la_simulate: SCATTER needs cand");
   const size_t cs_bytes = ((size_t)a->T * sizeof(float2) + 15) & ~(size_t)15;
   const size_t smem = cs_bytes + (sizeof(WarpHead) + (size_t)njmax * 32 * colb) * SIM_WARPS;
   const bool wonly = (a->flags & LA_SIM_WRITE_ONLY) != 0;
   if (wonly && !write) return fail(LA_EINVAL, "la_simulate: WRITE_ONLY needs WRITE_TRAJ");
   const bool exact = (a->flags & LA_SIM_EXACT64) != 0;
+  if (!write && !f64 && (a->flags & LA_SIM_LANE_SCREEN)) return launch_screen_lane(*a, s);
   using KernT = void (*)(const la_sim_args, int);
   auto pick = [&](auto cnt) -> KernT {
     constexpr bool C = decltype(cnt)::value;

@@ -1,0 +1,84 @@
+// Device helpers shared by the simulation kernels (sim.cu: warp-per-candidate
+// replay and path writes; screen.cu: lane-per-candidate validity screen).
+#pragma once
+#include "common.cuh"
+
+namespace la {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+// shared-space accesses by 32-bit address (one IADD per access in the dyad
+// loop instead of generic-pointer arithmetic); "memory" keeps them ordered
+// with the other shared-memory accesses of the warp
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f2(uint32_t a, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_d2(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// fp32 screen error model (solve32): input rounding of the f64 pose and
+// crank tip, per-dyad rounding of the fp32 evaluation (unit-box magnitudes,
+// rsqrt/sqrt approximations included), and the margin's sensitivity factor
+// with a safety factor of 2 on the first-order bound.
+constexpr float kErr0 = 2e-7f;
+constexpr float kErrStep = 5e-7f;
+constexpr float kMarginK = 3.0f;
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// f64 reciprocal square root: MUFU.RSQ64H seed + two Newton steps
+// (relative error ~1e-16; not correctly rounded, see dyads_f64)
+__device__ __forceinline__ double rsqrt_f64(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double e = fma(-h, y * y, 0.5);
+    y = fma(y, e, y);
+  }
+  return y;
+}
+
+// exact-mode triage of an f64 replay: a fast (DFMA, Newton rsqrt) pass
+// decides unless one of its lock tests is within this distance of its
+// threshold; then the angle is redone in numpy's operation order
+constexpr double kExactTriage = 1e-7;
+
+// i-th fine angle of the coarse-first order (t = 4k + 1, 4k + 2, 4k + 3)
+__device__ __forceinline__ int fine_angle(int i) { return (i / 3) * 4 + 1 + (i % 3); }
+
+}  // namespace la

@@ -208,7 +208,7 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
                      traj_f64: bool = False, cand=None, cand_count=None,
                      fixup_tau: float = DEFAULT_FIXUP_TAU, fp64: bool = False, gate_only: bool = False,
                      coarse: bool = True, counters=None, stream=None, exact: bool | None = None,
-                     _extra_flags: int = 0,
+                     _extra_flags: int = 0, _screen: tuple[int, int] = (0, 0),
                      _outputs=None) -> dict:
     """Launch la_simulate on device tensors.
 
@@ -291,6 +291,7 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
     a.counters = N.ptr(counters)
     a.fixup_tau = float(fixup_tau)
     a.flags = flags
+    a.screen_refill, a.screen_replay = int(_screen[0]), int(_screen[1])
     N.check(lib.la_simulate(a, N.stream_ptr(stream)), "la_simulate")
     return out
 
