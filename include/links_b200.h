@@ -211,6 +211,11 @@ int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P,
                                 top-k scan (every curve fully evaluated)     */
 #define LA_CH_SEED_SCAN 32u  /* pruned scan: seed the running k-th bound with
                                 the exact k-th of a 1/128 prefix scan first  */
+#define LA_CH_NO_MQ 64u      /* pruned scan with NQ >= 2: one CTA set per query
+                                instead of the multi-query kernel (groups of
+                                queries share each streamed curve)           */
+#define LA_CH_MQ_FINE 128u   /* multi-query kernel: 64x64 common grid for the
+                                stage-0 bound instead of 32x32               */
 
 typedef struct la_chamfer_args {
   const float* db;            /* (device) [N][P][2] f32 normalised curves     */
@@ -240,6 +245,11 @@ typedef struct la_chamfer_args {
                                  direct-difference recomputation             */
   int64_t* n_full;            /* (device, optional) [NQ] += curves evaluated in
                                  full (the rest were pruned by their bound)  */
+  int64_t* n_stage;           /* (device, optional) [5] += (query, curve) pairs
+                                 surviving the multi-query kernel's bounds:
+                                 box/gap-table column term, common-grid row
+                                 term, 4-corner row term, 50-point and
+                                 10-point run-box column terms               */
 } la_chamfer_args;
 
 size_t la_chamfer_workspace(const la_chamfer_args* args);

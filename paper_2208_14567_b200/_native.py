@@ -29,6 +29,8 @@ LA_SIM_SCATTER = 64
 LA_SIM_WRITE_ONLY = 128
 LA_SIM_EXACT64 = 256
 LA_SIM_LANE_SCREEN = 512
+LA_CH_NO_MQ = 64
+LA_CH_MQ_FINE = 128
 LA_PENDING = -3
 ABI_VERSION = 2
 LA_EINVAL = -1
@@ -206,6 +208,7 @@ class LaChamferArgs(C.Structure):
         ("flags", C.c_uint32),
         ("fixup_below", C.c_float),
         ("n_full", C.c_void_p),
+        ("n_stage", C.c_void_p),
     ]
 
 

@@ -51,7 +51,8 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
                  pos_end: int | None = None, id_base: int = 0, pos_base: int = 0, pos_map=None,
                  exclude_id: int = -1, dense: bool = False, all_d=None, expansion: bool = False,
                  fix_tol: float = 5e-5, scalar_pipe: bool = False, tensor: bool = False, prune: bool = True,
-                 seed_scan: bool = False, stream=None) -> dict:
+                 seed_scan: bool = False, multi_query: bool = True, mq_fine: bool = False,
+                 stream=None) -> dict:
     """One la_chamfer_topk launch.
 
     ``prune`` (top-k scans of >= 65,536 positions without dense output):
@@ -60,6 +61,10 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     the unpruned scan (``prune=False``: every curve evaluated).
     ``seed_scan``: seed the pruning bound with an exact scan of a 1/128
     prefix first (off by default; measured slower than the slot minima).
+    ``multi_query`` (pruned scans with several queries): groups of queries
+    share each streamed curve and a stage-0 bound on a grid common to the
+    group (``mq_fine``: 64x64 instead of 32x32); ``n_stage`` (5,) counts the
+    (query, curve) pairs surviving its five bound stages.
 
     db: (N, P, 2) float32 CUDA tensor; queries: (NQ, Q, 2) float32.  order:
     optional (N,) int64 device tensor, record index at each scan position.
@@ -94,6 +99,7 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
             out[name] = torch.empty((NQ, kk), dtype=dt, device=dev)
     out["n_hits"] = torch.zeros(NQ, dtype=torch.int64, device=dev)
     out["n_full"] = torch.zeros(NQ, dtype=torch.int64, device=dev)  # curves evaluated in full (fast path)
+    out["n_stage"] = torch.zeros(5, dtype=torch.int64, device=dev)
     if dense and all_d is None:
         all_d = torch.full((NQ, Nn), float("nan"), dtype=torch.float32, device=dev)
     if all_d is not None:
@@ -118,9 +124,11 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     a.all_d = N.ptr(all_d)
     a.flags = ((N.LA_CH_EXPANSION if expansion else 0) | (N.LA_CH_SCALAR_PIPE if scalar_pipe else 0)
                | (N.LA_CH_TENSOR if tensor else 0) | (0 if prune else N.LA_CH_NO_PRUNE)
-               | (N.LA_CH_SEED_SCAN if seed_scan else 0))
+               | (N.LA_CH_SEED_SCAN if seed_scan else 0) | (0 if multi_query else N.LA_CH_NO_MQ)
+               | (N.LA_CH_MQ_FINE if mq_fine else 0))
     a.fixup_below = float(fix_tol)
     a.n_full = out["n_full"].data_ptr()
+    a.n_stage = out["n_stage"].data_ptr()
     wsb = int(lib.la_chamfer_workspace(a))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     a.ws, a.ws_bytes = ws.data_ptr(), wsb

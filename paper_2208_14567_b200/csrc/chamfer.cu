@@ -391,27 +391,34 @@ __device__ __forceinline__ float curve_col_bound(const QueryRegs<QS>& Q, const f
       const float2 a = cur[i];
       lx = fminf(lx, a.x); ly = fminf(ly, a.y); hx = fmaxf(hx, a.x); hy = fmaxf(hy, a.y);
     }
-    boxes[lane] = make_float4(lx - 0.5f, ly - 0.5f, hx - 0.5f, hy - 0.5f);
+    // (lo.x, lo.y, -hi.x, -hi.y), centred like the query registers
+    boxes[lane] = make_float4(lx - 0.5f, ly - 0.5f, 0.5f - hx, 0.5f - hy);
   }
   __syncwarp();
   float2 m[NP > 0 ? NP : 1];
 #pragma unroll
   for (int j = 0; j < NP; ++j) m[j] = make_float2(INFINITY, INFINITY);
   float mt = INFINITY;
+  const float2 neg1 = make_float2(-1.f, -1.f);
   for (int b = 0; b < nb; ++b) {
     const float4 bx = boxes[b];
+    const float2 lox = make_float2(bx.x, bx.x), loy = make_float2(bx.y, bx.y);
+    const float2 nhx = make_float2(bx.z, bx.z), nhy = make_float2(bx.w, bx.w);
+    // two query slots per f32x2 op: lo - q (FFMA2), q - hi (FADD2); the
+    // same roundings as the scalar form
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
-      const float dx0 = fmaxf(fmaxf(bx.x - Q.qx[j].x, Q.qx[j].x - bx.z), 0.f);
-      const float dx1 = fmaxf(fmaxf(bx.x - Q.qx[j].y, Q.qx[j].y - bx.z), 0.f);
-      const float dy0 = fmaxf(fmaxf(bx.y - Q.qy[j].x, Q.qy[j].x - bx.w), 0.f);
-      const float dy1 = fmaxf(fmaxf(bx.y - Q.qy[j].y, Q.qy[j].y - bx.w), 0.f);
-      m[j].x = fminf(m[j].x, fmaf(dy0, dy0, dx0 * dx0));
-      m[j].y = fminf(m[j].y, fmaf(dy1, dy1, dx1 * dx1));
+      const float2 ax = __ffma2_rn(Q.qx[j], neg1, lox), bxv = __fadd2_rn(Q.qx[j], nhx);
+      const float2 ay = __ffma2_rn(Q.qy[j], neg1, loy), byv = __fadd2_rn(Q.qy[j], nhy);
+      const float2 dx = make_float2(fmaxf(fmaxf(ax.x, bxv.x), 0.f), fmaxf(fmaxf(ax.y, bxv.y), 0.f));
+      const float2 dy = make_float2(fmaxf(fmaxf(ay.x, byv.x), 0.f), fmaxf(fmaxf(ay.y, byv.y), 0.f));
+      const float2 d2 = __ffma2_rn(dy, dy, __fmul2_rn(dx, dx));
+      m[j].x = fminf(m[j].x, d2.x);
+      m[j].y = fminf(m[j].y, d2.y);
     }
     if (QS & 1) {
-      const float dx = fmaxf(fmaxf(bx.x - Q.tx, Q.tx - bx.z), 0.f);
-      const float dy = fmaxf(fmaxf(bx.y - Q.ty, Q.ty - bx.w), 0.f);
+      const float dx = fmaxf(fmaxf(bx.x - Q.tx, Q.tx + bx.z), 0.f);
+      const float dy = fmaxf(fmaxf(bx.y - Q.ty, Q.ty + bx.w), 0.f);
       mt = fminf(mt, fmaf(dy, dy, dx * dx));
     }
   }
@@ -801,6 +808,516 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
   cta_flush_lists(c, qi, w, lane, top, hit, nhit, scan_smem);
   if (A.n_full && lane == 0 && nfull) atomicAdd(reinterpret_cast<unsigned long long*>(A.n_full + qi),
                                                  (unsigned long long)nfull);
+}
+
+// ------------------------------------------------------------ multi-query scan
+// (fast path, pruned top-k, NQ >= 2)  chamfer_scan_kernel gives every query
+// its own CTAs, so each query re-streams the whole database and re-derives
+// each curve's grid cells.  Here a CTA holds a GROUP of QG queries: every
+// database curve is fetched once per group (TMA), each of its points is
+// placed once on a grid COMMON to all queries (nearest vertex v, e = |a - v|),
+// and the stage-0 bound of the first chamfer term,
+//   LB0(a, q) = mean_i max(0, DT_q(v_i) - e_i),   DT_q(v) <= min_q |v - q|,
+// costs one shared-memory half load and three FP ops per (point, query).
+// The per-lane partial sums of 8 queries are reduced across the warp by a
+// transposed butterfly (9 shuffles for 8 sums).  A (query, curve) pair whose
+// LB0 exceeds max(threshold, thr_q) is dropped; the survivors go through the
+// single-query stages (4-corner bound on the query's own 64x64 grid, column
+// bound from run boxes) and, if still alive, the exact evaluation.  Lists
+// live per (CTA, query) in shared memory (a per-query lock; insertions are
+// rare), are flushed as list blockIdx.x of the query and merged by
+// merge_kernel.  Lists are identical to the unpruned scan for the same
+// reasons as chamfer_scan_kernel (every bound is a valid lower bound after
+// the (1 - 1e-4) / slack margins; ties never prune).
+constexpr int MQ_W = 8;           // warps per CTA
+constexpr int MQ_T = MQ_W * 32;
+constexpr int MQ_MAXG = 64;       // queries per group (bits of the pass mask)
+constexpr int MQ_TAB_N = 129;     // grid lines of the column-term gap tables
+constexpr int MQ_TAB_BYTES = 2068;  // 8 tables of MQ_TAB_N halves + pad (odd word stride)
+
+template <int G0>
+struct MQGrid {
+  static constexpr int V = G0 + 1;
+  static constexpr int NV = V * V;
+  static constexpr int STRIDE = (NV + 7) & ~7;  // halves per query
+};
+
+// common grid: bounding box of every query point joined with the unit
+// square, padded by 1/32 of its extent; par = lo.x, lo.y, 1/h.x, 1/h.y, h.x, h.y
+__global__ void __launch_bounds__(1024) mq_box_kernel(const float* __restrict__ queries, long long n, int G0,
+                                                      float* __restrict__ par) {
+  const float2* q = reinterpret_cast<const float2*>(queries);
+  float lx = 0.f, ly = 0.f, hx = 1.f, hy = 1.f;
+  for (long long i = threadIdx.x; i < n; i += 1024) {
+    const float2 v = q[i];
+    lx = fminf(lx, v.x); ly = fminf(ly, v.y); hx = fmaxf(hx, v.x); hy = fmaxf(hy, v.y);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lx = fminf(lx, __shfl_xor_sync(FULL, lx, o)); ly = fminf(ly, __shfl_xor_sync(FULL, ly, o));
+    hx = fmaxf(hx, __shfl_xor_sync(FULL, hx, o)); hy = fmaxf(hy, __shfl_xor_sync(FULL, hy, o));
+  }
+  __shared__ float red[4][32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { red[0][w] = lx; red[1][w] = ly; red[2][w] = hx; red[3][w] = hy; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < 32; ++j) {
+      lx = fminf(lx, red[0][j]); ly = fminf(ly, red[1][j]); hx = fmaxf(hx, red[2][j]); hy = fmaxf(hy, red[3][j]);
+    }
+    const float padx = (hx - lx) / 32.f, pady = (hy - ly) / 32.f;
+    lx -= padx; ly -= pady; hx += padx; hy += pady;
+    const float cx = (hx - lx) / (float)G0, cy = (hy - ly) / (float)G0;
+    par[0] = lx; par[1] = ly; par[2] = 1.f / cx; par[3] = 1.f / cy; par[4] = cx; par[5] = cy;
+    const float ccx = (hx - lx) / (float)(MQ_TAB_N - 1), ccy = (hy - ly) / (float)(MQ_TAB_N - 1);
+    par[6] = ccx; par[7] = ccy; par[8] = 1.f / ccx; par[9] = 1.f / ccy;
+    // rotated axes u = x + y, v = x - y (unnormalised) over the box's range
+    const float lu = lx + ly, lv = lx - hy;
+    const float ccu = ((hx + hy) - lu) / (float)(MQ_TAB_N - 1), ccv = ((hx - ly) - lv) / (float)(MQ_TAB_N - 1);
+    par[10] = lu; par[11] = ccu; par[12] = 1.f / ccu; par[13] = lv; par[14] = ccv; par[15] = 1.f / ccv;
+  }
+}
+
+// DT_q on the common grid, rounded toward -inf after a 1e-6 slack (as
+// lb_grid_kernel); grid (ceil(NV / 256), NQ)
+__global__ void __launch_bounds__(256) mq_dt_kernel(const float* __restrict__ queries, int Q, int G0, int stride,
+                                                    const float* __restrict__ par, __half* __restrict__ dt) {
+  const int qi = blockIdx.y;
+  const float2* q = reinterpret_cast<const float2*>(queries) + (size_t)qi * Q;
+  __shared__ float2 sq[256];
+  const int V = G0 + 1;
+  const float lx = par[0], ly = par[1], cx = par[4], cy = par[5];
+  const int v = blockIdx.x * 256 + threadIdx.x;
+  const bool live = v < V * V;
+  const int ix = live ? v / V : 0, iy = live ? v % V : 0;
+  const float vx = __fmaf_rn((float)ix, cx, lx), vy = __fmaf_rn((float)iy, cy, ly);
+  float m = INFINITY;
+  for (int b = 0; b < Q; b += 256) {
+    __syncthreads();
+    if (b + threadIdx.x < Q) sq[threadIdx.x] = q[b + threadIdx.x];
+    __syncthreads();
+    const int e = min(256, Q - b);
+    for (int j = 0; j < e; ++j) {
+      const float dx = vx - sq[j].x, dy = vy - sq[j].y;
+      m = fminf(m, __fmaf_rn(dy, dy, dx * dx));
+    }
+  }
+  if (live) dt[(size_t)qi * stride + v] = __float2half_rd(fmaxf(sqrtf(m) * (1.f - 1e-6f) - 1e-6f, 0.f));
+}
+
+// column-term gap tables per query: for grid lines g_m = lo + m * cc
+// (m = 0..MQ_TAB_N-1, cc = box / (MQ_TAB_N - 1)) along x and y,
+//   A(m) = mean_q max(g_m - q, 0),  B(m) = mean_q max(q - g_m, 0),
+// rounded down; 4 tables of MQ_TAB_N halves, padded so that consecutive
+// queries' tables start in different banks (259 words per query)
+__global__ void __launch_bounds__(160) mq_tab_kernel(const float* __restrict__ queries, int Q,
+                                                     const float* __restrict__ par, __half* __restrict__ tab) {
+  const int qi = blockIdx.x;
+  const float2* q = reinterpret_cast<const float2*>(queries) + (size_t)qi * Q;
+  const int m = threadIdx.x;
+  const float gx = __fmaf_rn((float)m, par[6], par[0]), gy = __fmaf_rn((float)m, par[7], par[1]);
+  const float gu = __fmaf_rn((float)m, par[11], par[10]), gv = __fmaf_rn((float)m, par[14], par[13]);
+  float ax = 0.f, bx = 0.f, ay = 0.f, by = 0.f, au = 0.f, bu = 0.f, av = 0.f, bv = 0.f;
+  for (int i = 0; i < Q; ++i) {
+    const float2 v = q[i];
+    ax += fmaxf(gx - v.x, 0.f); bx += fmaxf(v.x - gx, 0.f);
+    ay += fmaxf(gy - v.y, 0.f); by += fmaxf(v.y - gy, 0.f);
+    const float u = v.x + v.y, w = v.x - v.y;
+    au += fmaxf(gu - u, 0.f); bu += fmaxf(u - gu, 0.f);
+    av += fmaxf(gv - w, 0.f); bv += fmaxf(w - gv, 0.f);
+  }
+  if (m < MQ_TAB_N) {
+    // fp32 sums of <= 256 terms: relative error < 2e-5, covered by 1 - 1e-4
+    const float sc = (1.f - 1e-4f) / (float)Q;
+    __half* t = tab + (size_t)qi * (MQ_TAB_BYTES / 2);
+    t[m] = __float2half_rd(ax * sc);
+    t[MQ_TAB_N + m] = __float2half_rd(bx * sc);
+    t[2 * MQ_TAB_N + m] = __float2half_rd(ay * sc);
+    t[3 * MQ_TAB_N + m] = __float2half_rd(by * sc);
+    // rounding of u, v (<= 2.4e-7 absolute) is covered by the scan's lb_slack
+    t[4 * MQ_TAB_N + m] = __float2half_rd(au * sc);
+    t[5 * MQ_TAB_N + m] = __float2half_rd(bu * sc);
+    t[6 * MQ_TAB_N + m] = __float2half_rd(av * sc);
+    t[7 * MQ_TAB_N + m] = __float2half_rd(bv * sc);
+  }
+  if (m < (MQ_TAB_BYTES / 2 - 8 * MQ_TAB_N)) tab[(size_t)qi * (MQ_TAB_BYTES / 2) + 8 * MQ_TAB_N + m] = __float2half(0.f);
+}
+
+// highest grid line <= v (0 below the box: A vanishes there) / lowest >= v
+__device__ __forceinline__ int mq_line_lo(float v, float lo, float cc, float icc) {
+  int m = (int)floorf((v - lo) * icc);
+  m = max(min(m, MQ_TAB_N - 1), 0);
+  if (m > 0 && __fmaf_rn((float)m, cc, lo) > v) --m;
+  return v >= lo ? m : 0;
+}
+__device__ __forceinline__ int mq_line_hi(float v, float lo, float cc, float icc) {
+  int m = (int)ceilf((v - lo) * icc);
+  m = max(min(m, MQ_TAB_N - 1), 0);
+  if (m < MQ_TAB_N - 1 && __fmaf_rn((float)m, cc, lo) < v) ++m;
+  return __fmaf_rn((float)m, cc, lo) >= v ? m : MQ_TAB_N - 1;
+}
+
+struct MQSmem {
+  // per CTA: dt [QG][STRIDE] halves, lists, counters; per warp: buffers
+  size_t dt, tab, top_d, top_pos, top_id, hit_d, hit_pos, hit_id, nh, lock, cnt, warp0, per_warp, total;
+};
+
+__host__ __device__ inline MQSmem mq_smem(int QG, int k, int stride, int P) {
+  MQSmem m{};
+  auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  const int kk = k > 0 ? k : 1;
+  size_t o = 0;
+  m.dt = o; o = al(o + (size_t)((QG + 7) & ~7) * stride * 2);
+  m.tab = o; o = al(o + (size_t)QG * MQ_TAB_BYTES);
+  m.top_d = o; o = al(o + (size_t)QG * kk * 4);
+  m.hit_d = o; o = al(o + (size_t)QG * kk * 4);
+  m.top_pos = o; o = al(o + (size_t)QG * kk * 8);
+  m.top_id = o; o = al(o + (size_t)QG * kk * 8);
+  m.hit_pos = o; o = al(o + (size_t)QG * kk * 8);
+  m.hit_id = o; o = al(o + (size_t)QG * kk * 8);
+  m.nh = o; o = al(o + (size_t)QG * 8);
+  m.lock = o; o = al(o + (size_t)QG * 4);
+  m.cnt = o; o = al(o + (size_t)(QG + 5) * 4);  // survivors of the 5 bound stages, then n_full per query
+  o = (o + 127) & ~(size_t)127;
+  m.warp0 = o;
+  const int Pe = (P + 1) & ~1, Ppad = (P + 31) & ~31;
+  // curve double buffer, expanded pairs padded to whole 32-point chunks
+  // (float4 + float2, read by curve_chamfer), 32 run boxes, row buffer,
+  // 2 mbarriers
+  m.per_warp = al(2 * (size_t)Pe * 8) + al((size_t)(Ppad / 2) * 16) + al((size_t)(Ppad / 2) * 8) + 32 * 16 + 32 * 4 + 16;
+  m.per_warp = (m.per_warp + 127) & ~(size_t)127;
+  m.total = m.warp0 + MQ_W * m.per_warp;
+  return m;
+}
+
+__device__ __forceinline__ float lds_half(uint32_t a) {
+  unsigned short h;
+  asm("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
+  return __half2float(__ushort_as_half(h));
+}
+
+// insert into the CTA's list of query q under its lock (whole warp)
+__device__ __forceinline__ void mq_insert(float* ld, long long* lp, long long* li, int* lock, int k, int lane,
+                                          float d, long long pos, long long id, bool by_pos) {
+  if (lane == 0) {
+    while (atomicCAS(lock, 0, 1) != 0) __nanosleep(20);
+  }
+  __syncwarp();
+  __threadfence_block();
+  const float cd = lane < k ? ld[lane] : INFINITY;
+  const long long cp = lane < k ? lp[lane] : LLONG_MAX;
+  const long long ci = lane < k ? li[lane] : -1;
+  const bool less = lane < k && (by_pos ? (cp < pos) : key_less(cd, cp, d, pos));
+  const int idx = __popc(__ballot_sync(FULL, less));
+  const float pd = __shfl_up_sync(FULL, cd, 1);
+  const long long pp = __shfl_up_sync(FULL, cp, 1);
+  const long long pi = __shfl_up_sync(FULL, ci, 1);
+  if (idx < k) {
+    if (lane > idx && lane < k) {
+      ld[lane] = pd;
+      lp[lane] = pp;
+      li[lane] = pi;
+    }
+    if (lane == idx) {
+      ld[lane] = d;
+      lp[lane] = pos;
+      li[lane] = id;
+    }
+  }
+  __threadfence_block();
+  __syncwarp();
+  if (lane == 0) atomicExch(lock, 0);
+}
+
+template <int QS, int G0>
+__global__ void __launch_bounds__(MQ_T, 1) chamfer_mq_kernel(const ScanCtx c, int QG, const __half* __restrict__ dt0,
+                                                             const __half* __restrict__ tab0,
+                                                             const float* __restrict__ par0) {
+  using GR = MQGrid<G0>;
+  extern __shared__ __align__(128) unsigned char mq_smem_raw[];
+  const la_chamfer_args& A = c.a;
+  const int P = A.P, Qn = A.Q, k = A.k;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q0 = blockIdx.y * QG;
+  const int nq = min(QG, A.NQ - q0);
+  const MQSmem L = mq_smem(QG, k, GR::STRIDE, P);
+  __half* sdt = reinterpret_cast<__half*>(mq_smem_raw + L.dt);
+  float* s_top_d = reinterpret_cast<float*>(mq_smem_raw + L.top_d);
+  float* s_hit_d = reinterpret_cast<float*>(mq_smem_raw + L.hit_d);
+  long long* s_top_pos = reinterpret_cast<long long*>(mq_smem_raw + L.top_pos);
+  long long* s_top_id = reinterpret_cast<long long*>(mq_smem_raw + L.top_id);
+  long long* s_hit_pos = reinterpret_cast<long long*>(mq_smem_raw + L.hit_pos);
+  long long* s_hit_id = reinterpret_cast<long long*>(mq_smem_raw + L.hit_id);
+  unsigned long long* s_nh = reinterpret_cast<unsigned long long*>(mq_smem_raw + L.nh);
+  int* s_lock = reinterpret_cast<int*>(mq_smem_raw + L.lock);
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(mq_smem_raw + L.cnt);
+  unsigned char* wb = mq_smem_raw + L.warp0 + (size_t)w * L.per_warp;
+  const int Pe = (P + 1) & ~1, Ppad = (P + 31) & ~31;
+  float2* raw0 = reinterpret_cast<float2*>(wb);
+  float2* raw1 = raw0 + Pe;
+  size_t off = ((2 * (size_t)Pe * 8) + 15) & ~(size_t)15;
+  float4* exs = reinterpret_cast<float4*>(wb + off);
+  off += (((size_t)(Ppad / 2) * 16) + 15) & ~(size_t)15;
+  float2* ens = reinterpret_cast<float2*>(wb + off);
+  off += (((size_t)(Ppad / 2) * 8) + 15) & ~(size_t)15;
+  float4* boxes = reinterpret_cast<float4*>(wb + off);
+  off += 32 * 16;
+  float* rowbuf = reinterpret_cast<float*>(wb + off);
+  off += 32 * 4;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wb + off);
+
+  // stage the group's grids, init lists and counters
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(dt0 + (size_t)q0 * GR::STRIDE);
+    uint4* dst = reinterpret_cast<uint4*>(sdt);
+    const int n16 = nq * GR::STRIDE * 2 / 16;
+    for (int i = threadIdx.x; i < n16; i += MQ_T) dst[i] = src[i];
+    const int npad = ((nq + 7) & ~7) * GR::STRIDE * 2 / 16;
+    for (int i = n16 + threadIdx.x; i < npad; i += MQ_T) dst[i] = make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t* tsrc = reinterpret_cast<const uint32_t*>(tab0 + (size_t)q0 * (MQ_TAB_BYTES / 2));
+    uint32_t* tdst = reinterpret_cast<uint32_t*>(mq_smem_raw + L.tab);
+    for (int i = threadIdx.x; i < nq * (MQ_TAB_BYTES / 4); i += MQ_T) tdst[i] = tsrc[i];
+    const int kk = k > 0 ? k : 1;
+    for (int i = threadIdx.x; i < QG * kk; i += MQ_T) {
+      s_top_d[i] = INFINITY; s_hit_d[i] = INFINITY;
+      s_top_pos[i] = LLONG_MAX; s_hit_pos[i] = LLONG_MAX;
+      s_top_id[i] = -1; s_hit_id[i] = -1;
+    }
+    for (int i = threadIdx.x; i < QG; i += MQ_T) { s_nh[i] = 0; s_lock[i] = 0; }
+    for (int i = threadIdx.x; i < QG + 5; i += MQ_T) s_cnt[i] = 0;
+  }
+  __syncthreads();
+  const uint32_t sdt_b = smem_u32(sdt);
+  const uint32_t stab_b = smem_u32(mq_smem_raw + L.tab);
+  const float lx = par0[0], ly = par0[1], ihx = par0[2], ihy = par0[3], cx = par0[4], cy = par0[5];
+  const float ccx = par0[6], ccy = par0[7], iccx = par0[8], iccy = par0[9];
+  const float lu = par0[10], ccu = par0[11], iccu = par0[12], lv = par0[13], ccv = par0[14], iccv = par0[15];
+  const float ox = -lx * ihx, oy = -ly * ihy;
+  const float lb_slack = c.lb_slack;
+  const float invP = 1.f / (float)P;
+  const bool expansion = (A.flags & LA_CH_EXPANSION) != 0;
+
+  const int gw = blockIdx.x * MQ_W + w;
+  const long long stride = (long long)gridDim.x * MQ_W;
+  const long long first = A.pos_begin + gw;
+  const long long count = first < A.pos_end ? (A.pos_end - first + stride - 1) / stride : 0;
+  const bool use_tma = (P % 2) == 0;
+  const uint32_t bytes = (uint32_t)P * 8u;
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto rec_of = [&](long long pos) -> long long { return A.order ? A.order[pos] : pos; };
+  if (use_tma && count > 0 && lane == 0) {
+    mbar_expect_tx(&bars[0], bytes);
+    tma_load_1d(raw0, A.db + (size_t)rec_of(first) * P * 2, bytes, &bars[0]);
+  }
+  uint32_t phase = 0;
+  constexpr int UP = 8;  // points per lane (P <= 256)
+
+  for (long long it = 0; it < count; ++it) {
+    const int bi = (int)(it & 1);
+    const long long pos = first + it * stride;
+    const long long id = rec_of(pos);
+    __syncwarp();
+    const float2* cur;
+    if (use_tma) {
+      if (it + 1 < count && lane == 0) {
+        fence_proxy_async();
+        const long long nid = rec_of(pos + stride);
+        mbar_expect_tx(&bars[bi ^ 1], bytes);
+        tma_load_1d(bi ? raw0 : raw1, A.db + (size_t)nid * P * 2, bytes, &bars[bi ^ 1]);
+      }
+      mbar_wait(&bars[bi], (phase >> bi) & 1u);
+      phase ^= (1u << bi);
+      cur = bi ? raw1 : raw0;
+    } else {
+      const float2* src = reinterpret_cast<const float2*>(A.db) + (size_t)id * P;
+      for (int j = lane; j < P; j += 32) raw0[j] = src[j];
+      __syncwarp();
+      cur = raw0;
+    }
+    if (id == A.exclude_id) continue;
+
+    // ---- stage A, every query of the group: the column term from the
+    // curve's bounding box and the query's gap tables,
+    //   mean_q min_a |q - a| >= mean_q dist(q, box)
+    //                        >= max(X, Y, (X + Y) / sqrt 2),
+    //   X = Ax(lo.x) + Bx(hi.x) = mean_q max(lo.x - q.x, q.x - hi.x, 0), Y alike,
+    // with the box rounded outward to the tables' grid lines
+    float bx0 = INFINITY, by0 = INFINITY, bx1 = -INFINITY, by1 = -INFINITY;
+    float bu0 = INFINITY, bv0 = INFINITY, bu1 = -INFINITY, bv1 = -INFINITY;
+    for (int i = lane; i < P; i += 32) {
+      const float2 a = cur[i];
+      bx0 = fminf(bx0, a.x); by0 = fminf(by0, a.y); bx1 = fmaxf(bx1, a.x); by1 = fmaxf(by1, a.y);
+      const float u = a.x + a.y, v = a.x - a.y;
+      bu0 = fminf(bu0, u); bv0 = fminf(bv0, v); bu1 = fmaxf(bu1, u); bv1 = fmaxf(bv1, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bx0 = fminf(bx0, __shfl_xor_sync(FULL, bx0, o)); by0 = fminf(by0, __shfl_xor_sync(FULL, by0, o));
+      bx1 = fmaxf(bx1, __shfl_xor_sync(FULL, bx1, o)); by1 = fmaxf(by1, __shfl_xor_sync(FULL, by1, o));
+      bu0 = fminf(bu0, __shfl_xor_sync(FULL, bu0, o)); bv0 = fminf(bv0, __shfl_xor_sync(FULL, bv0, o));
+      bu1 = fmaxf(bu1, __shfl_xor_sync(FULL, bu1, o)); bv1 = fmaxf(bv1, __shfl_xor_sync(FULL, bv1, o));
+    }
+    const int ilx = mq_line_lo(bx0, lx, ccx, iccx), ihx_ = mq_line_hi(bx1, lx, ccx, iccx);
+    const int ily = mq_line_lo(by0, ly, ccy, iccy), ihy_ = mq_line_hi(by1, ly, ccy, iccy);
+    // u, v of the curve's points carry fp32 rounding: widen by 1e-6
+    const int ilu = mq_line_lo(bu0 - 1e-6f, lu, ccu, iccu), ihu = mq_line_hi(bu1 + 1e-6f, lu, ccu, iccu);
+    const int ilv = mq_line_lo(bv0 - 1e-6f, lv, ccv, iccv), ihv = mq_line_hi(bv1 + 1e-6f, lv, ccv, iccv);
+    // lane l: queries l and l + 32 of the group.  Projections on the unit
+    // axes x, y and (1, +-1) / sqrt 2 each bound |q - a| from below:
+    //   mean dist >= max(X, Y, (X + Y) / sqrt 2, max(U, V) / sqrt 2, (U + V) / 2)
+    auto col_bound = [&](int qg) -> float {
+      const uint32_t t = stab_b + (uint32_t)qg * MQ_TAB_BYTES;
+      const float X = lds_half(t + 2u * ilx) + lds_half(t + 2u * (MQ_TAB_N + ihx_));
+      const float Y = lds_half(t + 2u * (2 * MQ_TAB_N + ily)) + lds_half(t + 2u * (3 * MQ_TAB_N + ihy_));
+      const float U = lds_half(t + 2u * (4 * MQ_TAB_N + ilu)) + lds_half(t + 2u * (5 * MQ_TAB_N + ihu));
+      const float V = lds_half(t + 2u * (6 * MQ_TAB_N + ilv)) + lds_half(t + 2u * (7 * MQ_TAB_N + ihv));
+      return fmaxf(fmaxf(fmaxf(X, Y), (X + Y) * 0.70710670f), fmaxf(fmaxf(U, V) * 0.70710670f, (U + V) * 0.49999997f));
+    };
+    const float clo = lane < nq ? col_bound(lane) : 0.f;
+    const float chi = lane + 32 < nq ? col_bound(lane + 32) : 0.f;
+    // running bounds: lane l holds thr of queries l, l + 32
+    const float tlo = lane < nq ? __uint_as_float(__ldcg(c.thr + q0 + lane)) : INFINITY;
+    const float thi = lane + 32 < nq ? __uint_as_float(__ldcg(c.thr + q0 + lane + 32)) : INFINITY;
+    unsigned long long pass =
+        (unsigned long long)__ballot_sync(FULL, lane < nq && !(fmaf(clo, 1.f - 1e-4f, -lb_slack) > fmaxf(tlo, A.threshold))) |
+        ((unsigned long long)__ballot_sync(FULL, lane + 32 < nq &&
+                                                     !(fmaf(chi, 1.f - 1e-4f, -lb_slack) > fmaxf(thi, A.threshold)))
+         << 32);
+    if (!pass) continue;
+    if (lane == 0) atomicAdd(&s_cnt[0], (unsigned)__popcll(pass));
+    // ---- stage B (row term on the common grid), computed for the queries
+    // still alive: nearest vertex of each point once per curve
+    int vi[UP];
+    float ve[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int i = lane + 32 * u;
+      vi[u] = 0;
+      ve[u] = INFINITY;  // beyond P: contributes max(dt - inf, 0) = 0
+      if (i < P) {
+        const float2 a = cur[i];
+        const unsigned ix = min(__float2uint_rn(fmaf(a.x, ihx, ox)), (unsigned)G0);
+        const unsigned iy = min(__float2uint_rn(fmaf(a.y, ihy, oy)), (unsigned)G0);
+        const float ex = a.x - __fmaf_rn((float)ix, cx, lx), ey = a.y - __fmaf_rn((float)iy, cy, ly);
+        vi[u] = (int)(ix * GR::V + iy) * 2 + (int)sdt_b;
+        ve[u] = sqrt_approx(fmaf(ey, ey, ex * ex));
+      }
+    }
+    bool expanded = false;
+    float ar2 = 0.f;
+    const long long rpos = A.pos_map ? A.pos_map[pos] : pos + A.pos_base;
+    while (pass) {
+      const int qg = __ffsll((long long)pass) - 1;
+      pass &= pass - 1;
+      const int qi = q0 + qg;
+      // thr as read at the start of this curve: an older (larger) value is
+      // still an upper bound of the final k-th best
+      const float t = fmaxf(__shfl_sync(FULL, qg < 32 ? tlo : thi, qg & 31), A.threshold);
+      const float colb0 = __shfl_sync(FULL, qg < 32 ? clo : chi, qg & 31);
+      float acc = 0.f;
+      const uint32_t qoff = (uint32_t)qg * GR::STRIDE * 2u;
+#pragma unroll
+      for (int u = 0; u < UP; ++u) acc += fmaxf(lds_half((uint32_t)vi[u] + qoff) - ve[u], 0.f);
+      const float row0 = warp_sum(acc) * invP;
+      if (fmaf(row0 + colb0, 1.f - 1e-4f, -lb_slack) > t) continue;
+      if (lane == 0) atomicAdd(&s_cnt[1], 1u);
+      // stage 1: four-corner row bound on the query's own 64x64 grid
+      const float* pp = c.lb_par + (size_t)qi * 8;
+      const float rowb = fmaxf(row0, curve_row_bound(cur, P, c.lb_dt + (size_t)qi * (LB_DT_BYTES / sizeof(__half)),
+                                                     pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], lane));
+      if (fmaf(rowb + colb0, 1.f - 1e-4f, -lb_slack) > t) continue;
+      if (lane == 0) atomicAdd(&s_cnt[2], 1u);
+      // stage 2: plus the column term from 10-point run boxes
+      const float2* qsrc = reinterpret_cast<const float2*>(A.queries) + (size_t)qi * Qn;
+      QueryRegs<QS> Q;
+      load_query<QS>(Q, qsrc, Qn, lane);
+      // column term from 4 boxes of 50-point runs, then 20 of 10-point runs
+      const float colb1 = fmaxf(colb0, curve_col_bound<QS, 50>(Q, cur, P, Qn, boxes, lane));
+      if (fmaf(rowb + colb1, 1.f - 1e-4f, -lb_slack) > t) continue;
+      if (lane == 0) atomicAdd(&s_cnt[3], 1u);
+      __syncwarp();
+      const float colb = fmaxf(colb1, curve_col_bound<QS, 10>(Q, cur, P, Qn, boxes, lane));
+      if (fmaf(rowb + colb, 1.f - 1e-4f, -lb_slack) > t) continue;
+      if (lane == 0) atomicAdd(&s_cnt[4], 1u);
+      if (!expanded) {
+        ar2 = 0.f;
+        for (int i = lane; i < Ppad / 2; i += 32) {
+          float4 e4 = make_float4(-2.f * BIG, -2.f * BIG, -2.f * BIG, -2.f * BIG);
+          float2 n2 = make_float2(FAR_N, FAR_N);
+          if (2 * i < P) {
+            const float2 p0 = cur[2 * i];
+            const float x = p0.x - 0.5f, y = p0.y - 0.5f;
+            e4.x = -2.f * x; e4.z = -2.f * y; n2.x = fmaf(y, y, x * x); ar2 = fmaxf(ar2, n2.x);
+          }
+          if (2 * i + 1 < P) {
+            const float2 p1 = cur[2 * i + 1];
+            const float x = p1.x - 0.5f, y = p1.y - 0.5f;
+            e4.y = -2.f * x; e4.w = -2.f * y; n2.y = fmaf(y, y, x * x); ar2 = fmaxf(ar2, n2.y);
+          }
+          exs[i] = e4;
+          ens[i] = n2;
+        }
+        ar2 = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(ar2)));
+        __syncwarp();
+        expanded = true;
+      }
+      float d;
+      if (expansion) {
+        const float delta = 20.f * U32 * fmaxf(ar2, Q.r2);
+        float err = 0.f;
+        d = curve_chamfer<QS, false>(Q, exs, ens, P, Qn, lane, delta, err, rowbuf);
+        if (!(err <= A.fixup_below)) d = direct_chamfer<QS>(qsrc, Qn, exs, ens, P, lane, rowbuf);
+      } else {
+        float dummy;
+        d = curve_chamfer<QS, true>(Q, exs, ens, P, Qn, lane, 0.f, dummy, rowbuf);
+      }
+      if (lane == 0) atomicAdd(&s_cnt[5 + qg], 1u);  // full evaluations of the query
+      const size_t lb = (size_t)qg * k;
+      if (d < A.threshold) {
+        if (lane == 0) atomicAdd(&s_nh[qg], 1ull);
+        if (rpos < *(volatile long long*)&s_hit_pos[lb + k - 1])
+          mq_insert(s_hit_d + lb, s_hit_pos + lb, s_hit_id + lb, &s_lock[qg], k, lane, d, rpos, id + A.id_base, true);
+      } else {
+        const float kd = *(volatile float*)&s_top_d[lb + k - 1];
+        const long long kp = *(volatile long long*)&s_top_pos[lb + k - 1];
+        if (key_less(d, rpos, kd, kp))
+          mq_insert(s_top_d + lb, s_top_pos + lb, s_top_id + lb, &s_lock[qg], k, lane, d, rpos, id + A.id_base,
+                    false);
+        if (d < __uint_as_float(__ldcg(c.thr + qi)))
+          publish_kth(c.thr + qi, c.slots + (size_t)qi * 32, k, lane, d, id);
+      }
+    }
+  }
+  __syncthreads();
+  // flush: list blockIdx.x of each query of the group
+  for (int qg = w; qg < nq; qg += MQ_W) {
+    const int qi = q0 + qg;
+    const size_t base = ((size_t)qi * c.nwarps_total + blockIdx.x) * k;
+    if (lane < k) {
+      const size_t lb = (size_t)qg * k + lane;
+      c.ws_top_d[base + lane] = s_top_d[lb];
+      c.ws_top_pos[base + lane] = s_top_pos[lb];
+      c.ws_top_id[base + lane] = s_top_id[lb];
+      c.ws_hit_d[base + lane] = s_hit_d[lb];
+      c.ws_hit_pos[base + lane] = s_hit_pos[lb];
+      c.ws_hit_id[base + lane] = s_hit_id[lb];
+    }
+    if (lane == 0) {
+      c.ws_nhit[(size_t)qi * c.nwarps_total + blockIdx.x] = (long long)s_nh[qg];
+      if (A.n_full && s_cnt[5 + qg])
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.n_full + qi), (unsigned long long)s_cnt[5 + qg]);
+    }
+  }
+  // counters: survivors of stages 0/1/2 and full evaluations (whole group)
+  if (threadIdx.x == 0) {
+    if (A.n_stage)
+      for (int j = 0; j < 5; ++j)
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.n_stage + j), (unsigned long long)s_cnt[j]);
+  }
 }
 
 // ------------------------------------------------------------ tensor-core path
@@ -1409,6 +1926,13 @@ struct Plan {
   long long seed_end;
   int seed_grid;
   size_t ws_prune; // bytes of the pruning area
+  // multi-query kernel (pruned, NQ >= 2)
+  bool mq;
+  int mq_g0;       // common grid cells per axis (32 or 64)
+  int mq_qg;       // queries per group
+  int mq_groups;
+  int mq_grid;     // CTAs per group (= lists per query)
+  size_t mq_smem;
 };
 
 // resident CTAs per SM of chamfer_scan_kernel<qs> (registers and the
@@ -1493,6 +2017,30 @@ Plan make_plan(const la_chamfer_args* a) {
     p.seed_grid = (int)sg;
     p.ws_prune = (size_t)a->NQ * (LB_DT_BYTES + 8 * sizeof(float) + 33 * sizeof(unsigned)) + 16 +
                  (size_t)a->NQ * a->k * 2 * (sizeof(float) + 2 * sizeof(long long)) + 256;
+    p.mq = a->NQ >= 2 && !(a->flags & LA_CH_NO_MQ) && (a->P % 2) == 0;
+    if (p.mq) {
+      p.mq_g0 = (a->flags & LA_CH_MQ_FINE) ? 64 : 32;
+      const int stride = p.mq_g0 == 64 ? MQGrid<64>::STRIDE : MQGrid<32>::STRIDE;
+      // largest group whose shared memory fits one CTA per SM, then groups
+      // of equal size
+      const size_t cap = 227 * 1024 - 1024;
+      int qg = MQ_MAXG;
+      while (qg > 1 && mq_smem(qg, a->k, stride, a->P).total > cap) --qg;
+      p.mq_groups = (a->NQ + qg - 1) / qg;
+      p.mq_qg = (a->NQ + p.mq_groups - 1) / p.mq_groups;
+      p.mq_smem = mq_smem(p.mq_qg, a->k, stride, a->P).total;
+      long long gx = ((long long)sms + p.mq_groups - 1) / p.mq_groups;  // one wave of 1 CTA per SM
+      const long long wantx = (npos + MQ_W - 1) / MQ_W;
+      if (gx > wantx) gx = wantx;
+      if (gx < 1) gx = 1;
+      p.mq_grid = (int)gx;
+      if (p.mq_grid > p.nwarps) {  // lists per query: the workspace holds max(nwarps, mq_grid)
+        p.nwarps = p.mq_grid;
+        const size_t per2 = (size_t)a->NQ * p.nwarps * (a->k > 0 ? a->k : 1);
+        p.ws_lists = per2 * (2 * sizeof(float) + 4 * sizeof(long long)) + (size_t)a->NQ * p.nwarps * sizeof(long long);
+      }
+      p.ws_prune += (size_t)a->NQ * (stride * sizeof(__half) + MQ_TAB_BYTES) + 16 * sizeof(float) + 256;
+    }
   }
   return p;
 }
@@ -1618,6 +2166,38 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
       c.thr = thr;
       c.prune = 1;
       c.lb_slack = 4e-6f + ((a->flags & LA_CH_EXPANSION) ? a->fixup_below : 0.f);
+      if (p.mq) {
+        // common-grid distance tables of every query, then one launch over
+        // (CTAs, query groups)
+        pw = reinterpret_cast<unsigned char*>(sd + 2 * nk);
+        pw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(pw) + 255) & ~(uintptr_t)255);
+        const int stride = p.mq_g0 == 64 ? MQGrid<64>::STRIDE : MQGrid<32>::STRIDE;
+        __half* dt0 = reinterpret_cast<__half*>(pw); pw += (size_t)a->NQ * stride * sizeof(__half);
+        __half* tab0 = reinterpret_cast<__half*>(pw); pw += (size_t)a->NQ * MQ_TAB_BYTES;
+        float* par0 = reinterpret_cast<float*>(pw);
+        mq_box_kernel<<<1, 1024, 0, s>>>(a->queries, (long long)a->NQ * a->Q, p.mq_g0, par0);
+        const int nv = (p.mq_g0 + 1) * (p.mq_g0 + 1);
+        mq_dt_kernel<<<dim3((nv + 255) / 256, a->NQ), 256, 0, s>>>(a->queries, a->Q, p.mq_g0, stride, par0, dt0);
+        mq_tab_kernel<<<a->NQ, 160, 0, s>>>(a->queries, a->Q, par0, tab0);
+        c.nwarps_total = p.mq_grid;  // lists per query written by the kernel (and merged)
+        const dim3 g(p.mq_grid, p.mq_groups);
+        cudaError_t ce = cudaSuccess;
+        switch (p.qs * 100 + p.mq_g0) {
+#define LA_MQ(QSV, G)                                                                                  \
+  case QSV * 100 + G:                                                                                  \
+    ce = cudaFuncSetAttribute(chamfer_mq_kernel<QSV, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                              (int)p.mq_smem);                                                         \
+    chamfer_mq_kernel<QSV, G><<<g, MQ_T, p.mq_smem, s>>>(c, p.mq_qg, dt0, tab0, par0);                 \
+    break;
+          LA_MQ(1, 32) LA_MQ(2, 32) LA_MQ(3, 32) LA_MQ(4, 32) LA_MQ(5, 32) LA_MQ(6, 32) LA_MQ(7, 32) LA_MQ(8, 32)
+          LA_MQ(1, 64) LA_MQ(2, 64) LA_MQ(3, 64) LA_MQ(4, 64) LA_MQ(5, 64) LA_MQ(6, 64) LA_MQ(7, 64) LA_MQ(8, 64)
+#undef LA_MQ
+          default: return fail(LA_ERANGE, "la_chamfer_topk: Q=%d", a->Q);
+        }
+        if (ce != cudaSuccess) return fail((int)ce, "la_chamfer_topk: mq smem attr: %s", cudaGetErrorString(ce));
+        if (a->k > 0) merge_kernel<<<a->NQ, 1024, 0, s>>>(c);
+        return cuda_status("la_chamfer_topk (multi-query)");
+      }
     }
     if (int e = scan(c, grid)) return e;
     c.nwarps_total = p.grid;  // one list per CTA (cta_flush_lists)

@@ -85,11 +85,11 @@ struct __align__(16) WarpHead {
 
 struct Warp {
   WarpHead* h;
-  unsigned char* cols;   // pos block
+  unsigned char* cols;   // pos block: slot (joint j, lane) at (j * 32 + lane) * slot bytes
   int lane;
-  // fp32 rounds: (x, y) of the 16-byte slot (x, y, e, -); f64 rounds: double2
+  int slot;              // 8 (fp32 x, y) or 16 (fp32 x, y, e, - / f64 x, y)
   __device__ __forceinline__ float2& p32(int j) const {
-    return *reinterpret_cast<float2*>(reinterpret_cast<float4*>(cols) + j * 32 + lane);
+    return *reinterpret_cast<float2*>(cols + (size_t)(j * 32 + lane) * slot);
   }
   __device__ __forceinline__ double2& p64(int j) const {
     return reinterpret_cast<double2*>(cols)[j * 32 + lane];
@@ -213,7 +213,7 @@ struct Ctr {
 // COUNT: maintain the diagnostic counters (la_sim_args.counters); the
 // uninstrumented instantiation keeps ~10 registers free (fewer spills, 4-5 %
 // faster screen)
-template <bool EXACT, bool COUNT>
+template <bool EXACT, bool COUNT, bool ERR4>
 __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const double* __restrict__ cs,
                                        const float2* __restrict__ cs32, int t, bool active, Ctr& ctr) {
   const WarpHead& H = *W.h;
@@ -221,48 +221,91 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
   bool fix = false;
   if (active) {
     const float2 c = cs32[t];
-    // each joint's slot holds its fp32 position and a first-order bound e on
-    // that position's error: static joints and the crank tip start at kErr0
-    // (inputs rounded to fp32); a dyad's target gets
-    //   e_t = max(kappa, 1) max(e_a, e_b) + kErrStep
-    // (its parents' error amplified by the dyad, plus its own rounding)
-    const uint32_t col = smem_u32(W.cols) + (uint32_t)W.lane * 16u;
-    sts_f2(col + 512u, make_float2(fmaf(C.r1f, c.x, C.p0f.x), fmaf(C.r1f, c.y, C.p0f.y)));
     const float tau = C.tau;
+    const uint32_t col = smem_u32(W.cols) + (uint32_t)W.lane * (uint32_t)W.slot;
+    sts_f2(col + 32u * (uint32_t)W.slot, make_float2(fmaf(C.r1f, c.x, C.p0f.x), fmaf(C.r1f, c.y, C.p0f.y)));
     int s = 0;
+    if (ERR4) {
+      // each joint's 16-byte slot holds its fp32 position and a first-order
+      // bound e on that position's error: static joints and the crank tip
+      // start at kErr0 (inputs rounded to fp32); a dyad's target gets
+      //   e_t = max(kappa, 1) max(e_a, e_b) + kErrStep
+      // (its parents' error amplified by the dyad, plus its own rounding)
 #pragma unroll 1
-    for (; s < C.ns; ++s) {
-      const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
-      const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].pmask);
-      const float4 pa = lds_f4(col + g1.y);
-      const float4 pb = lds_f4(col + g1.z);
-      const float dx = pb.x - pa.x, dy = pb.y - pa.y;
-      const float d2 = fmaf(dy, dy, dx * dx);
-      const float inv = rsqrt_approx(d2);
-      const float d = d2 * inv;
-      const float m = fminf(g0.x - d, d - g0.y);
-      const float ep = fmaxf(pa.z, pb.z);
-      // the margin moves by at most 2 ep (d from two parents) + rounding
-      fix |= !(fabsf(m) >= fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
-      if (m < 0.0f) {
-        lk = s;
-        break;
+      for (; s < C.ns; ++s) {
+        const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
+        const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].pmask);
+        const float4 pa = lds_f4(col + g1.y);
+        const float4 pb = lds_f4(col + g1.z);
+        const float dx = pb.x - pa.x, dy = pb.y - pa.y;
+        const float d2 = fmaf(dy, dy, dx * dx);
+        const float inv = rsqrt_approx(d2);
+        const float d = d2 * inv;
+        const float m = fminf(g0.x - d, d - g0.y);
+        const float ep = fmaxf(pa.z, pb.z);
+        // the margin moves by at most 2 ep (d from two parents) + rounding
+        fix |= !(fabsf(m) >= fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
+        if (m < 0.0f) {
+          lk = s;
+          break;
+        }
+        const float x = (d2 + g0.z) * (0.5f * inv);
+        const float h = sqrt_approx(fmaxf(fmaf(-x, x, fabsf(g0.w)), 0.0f));
+        // amplification of parent errors by an ill-conditioned (flat) dyad:
+        // dh/dd = -(x/h)(1 - x/d), so |dh| <= |x| (1 + |x|/d) / h * |dd|;
+        // well-conditioned dyads move their target about as far as their
+        // parents moved (kappa ~ 1).  h -> 0 makes the bound infinite, so
+        // every later dependent step of this angle goes to the f64 replay.
+        const float ax = fabsf(x);
+        const float num = ax * fmaf(ax, inv, 1.0f);
+        const float e = fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep);
+        const float xi = x * inv;
+        const float hb = copysignf(h, g0.w) * inv;
+        sts_f4(col + g1.w,
+               make_float4(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)), e, 0.f));
       }
-      const float x = (d2 + g0.z) * (0.5f * inv);
-      const float h = sqrt_approx(fmaxf(fmaf(-x, x, fabsf(g0.w)), 0.0f));
-      // amplification of parent errors by an ill-conditioned (flat) dyad:
-      // dh/dd = -(x/h)(1 - x/d), so |dh| <= |x| (1 + |x|/d) / h * |dd|;
-      // well-conditioned dyads move their target about as far as their
-      // parents moved (kappa ~ 1).  h -> 0 makes the bound infinite, so
-      // every later dependent step of this angle goes to the f64 replay.
-      const float ax = fabsf(x);
-      const float num = ax * fmaf(ax, inv, 1.0f);
-      const float e = fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep);
-      const float xi = x * inv;
-      const float hb = copysignf(h, g0.w) * inv;
-      sts_f4(col + g1.w, make_float4(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)), e, 0.f));
+    } else {
+      // 8-byte slots (large mechanisms: keeps occupancy): one running bound
+      // for "clean" joints and one for joints downstream of an amplifying
+      // dyad, a bitmask (parents' bits precomputed per step) separating them
+      float err = kErr0;
+      float err_t = 0.0f;
+      unsigned taint = 0u;
+      const int tsh = W.slot == 16 ? 9 : 8;  // byte offset of a joint's slot -> joint index
+#pragma unroll 1
+      for (; s < C.ns; ++s) {
+        const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
+        const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].pmask);
+        const float2 pa = lds_f2(col + g1.y);
+        const float2 pb = lds_f2(col + g1.z);
+        const float dx = pb.x - pa.x, dy = pb.y - pa.y;
+        const float d2 = fmaf(dy, dy, dx * dx);
+        const float inv = rsqrt_approx(d2);
+        const float d = d2 * inv;
+        const float m = fminf(g0.x - d, d - g0.y);
+        const bool tp = (taint & g1.x) != 0u;
+        const float ep = tp ? fmaxf(err_t, err) : err;
+        fix |= !(fabsf(m) >= fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
+        if (m < 0.0f) {
+          lk = s;
+          break;
+        }
+        const float x = (d2 + g0.z) * (0.5f * inv);
+        const float h = sqrt_approx(fmaxf(fmaf(-x, x, fabsf(g0.w)), 0.0f));
+        const float ax = fabsf(x);
+        const float num = ax * fmaf(ax, inv, 1.0f);
+        // amplifying dyad (kappa = num / h > 1) or tainted parent: branch-free
+        const bool amp = tp || num > h;
+        const float et = fmaxf(err_t, fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep));
+        err_t = amp ? et : err_t;
+        taint |= amp ? 1u << (g1.w >> tsh) : 0u;
+        err = amp ? err : err + kErrStep;
+        const float xi = x * inv;
+        const float hb = copysignf(h, g0.w) * inv;
+        sts_f2(col + g1.w, make_float2(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y))));
+      }
     }
-    if (COUNT) {
+  if (COUNT) {
       ++ctr.lane_angles;
       ctr.lane_dyads += (unsigned)(s < C.ns ? s + 1 : C.ns);
     }
@@ -297,13 +340,21 @@ __device__ __forceinline__ int solve64(const Warp& W, const SimCtx& C, const dou
 
 __device__ __forceinline__ void fill_static32(const Warp& W) {
   const WarpHead& H = *W.h;
-  float4* slot = reinterpret_cast<float4*>(W.cols) + W.lane;
+  if (W.slot == 16) {
+    float4* slot = reinterpret_cast<float4*>(W.cols) + W.lane;
 #pragma unroll 1
-  for (int k = 0; k < H.nstatic; ++k) {
-    const int j = H.statics[k];
-    slot[j * 32] = make_float4((float)H.p0[j].x, (float)H.p0[j].y, kErr0, 0.f);
+    for (int k = 0; k < H.nstatic; ++k) {
+      const int j = H.statics[k];
+      slot[j * 32] = make_float4((float)H.p0[j].x, (float)H.p0[j].y, kErr0, 0.f);
+    }
+    slot[32] = make_float4(0.f, 0.f, kErr0, 0.f);  // crank tip: error of its inputs
+  } else {
+#pragma unroll 1
+    for (int k = 0; k < H.nstatic; ++k) {
+      const int j = H.statics[k];
+      W.p32(j) = make_float2((float)H.p0[j].x, (float)H.p0[j].y);
+    }
   }
-  slot[32] = make_float4(0.f, 0.f, kErr0, 0.f);  // crank tip: error of its inputs
 }
 
 __device__ __forceinline__ void fill_static64(const Warp& W) {
@@ -329,12 +380,15 @@ __device__ __forceinline__ RoundLock round_lock(bool active, int lk) {
 }
 
 
-template <bool WRITE, bool SCREEN64>
+// bytes per (joint, lane) slot: double2 for f64 rounds; fp32 screens use
+// (x, y, e, -) with per-joint error bounds (ERR4) or (x, y) with the taint
+// model (large mechanisms, where 16-byte slots would cost occupancy)
+template <bool WRITE, bool SCREEN64, bool ERR4>
 __host__ __device__ constexpr size_t col_bytes() {
-  return 16;  // one 16-byte slot per (joint, lane): double2, or fp32 (x, y, e, -)
+  return (WRITE || SCREEN64 || ERR4) ? 16 : 8;
 }
 
-template <bool WRITE, bool SCREEN64, bool WONLY, bool EXACT, bool COUNT>
+template <bool WRITE, bool SCREEN64, bool WONLY, bool EXACT, bool COUNT, bool ERR4>
 __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_sim_args p, int njmax) {
   extern __shared__ __align__(16) unsigned char sim_smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -346,11 +400,13 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
   for (int t = threadIdx.x; t < T; t += SIM_THREADS)
     cs32[t] = make_float2((float)p.crank_cs[2 * t], (float)p.crank_cs[2 * t + 1]);
   __syncthreads();
-  const size_t per_warp = sizeof(WarpHead) + (size_t)njmax * 32 * col_bytes<WRITE, SCREEN64>();
+  constexpr uint32_t SLOT = (uint32_t)col_bytes<WRITE, SCREEN64, ERR4>();
+  const size_t per_warp = sizeof(WarpHead) + (size_t)njmax * 32 * SLOT;
   Warp W;
   W.h = reinterpret_cast<WarpHead*>(sim_smem_raw + cs_bytes + per_warp * w);
   W.cols = sim_smem_raw + cs_bytes + per_warp * w + sizeof(WarpHead);
   W.lane = lane;
+  W.slot = (int)SLOT;
   WarpHead& H = *W.h;
   const long long nwarps = (long long)gridDim.x * SIM_WARPS;
   const bool coarse = !WONLY && !(p.flags & LA_SIM_NO_COARSE) && (T % 4 == 0) && T >= 8;
@@ -434,9 +490,9 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
       r.c2 = (float)(ra * ra - rb * rb);
       r.ra2 = br < 0.0 ? -((float)ra * (float)ra) : (float)ra * (float)ra;
       r.pmask = (1u << ia_) | (1u << ib_);
-      r.a_off = (uint32_t)ia_ * 512u;  // slot (joint, lane) at j * 512 + lane * 16
-      r.b_off = (uint32_t)ib_ * 512u;
-      r.t_off = (uint32_t)it_ * 512u;
+      r.a_off = (uint32_t)ia_ * 32u * SLOT;  // slot (joint, lane) at (j * 32 + lane) * SLOT
+      r.b_off = (uint32_t)ib_ * 32u * SLOT;
+      r.t_off = (uint32_t)it_ * 32u * SLOT;
       H.st[lane] = r;
     }
     {
@@ -457,7 +513,7 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
 
     auto screen = [&](int t, bool act) -> int {
       if (SCREEN64 || WONLY) return solve64<EXACT>(W, C, p.crank_cs, t, act);
-      return solve32<EXACT, COUNT>(W, C, p.crank_cs, cs32, t, act, ctr);
+      return solve32<EXACT, COUNT, ERR4>(W, C, p.crank_cs, cs32, t, act, ctr);
     };
 
     int first_t = T, first_j = -1, low_t = -1, low_j = -1;
@@ -837,7 +893,11 @@ int la_simulate(const la_sim_args* a, void* stream) {
   const bool f64 = (a->flags & LA_SIM_FP64) != 0;
   const int njmax = a->pos_stride < NJ ? a->pos_stride : NJ;
   if (a->T > 2048) return fail(LA_ERANGE, "la_simulate: T=%d beyond 2048", a->T);
-  const size_t colb = 16;
+  // fp32 screens of small mechanisms keep a per-joint error bound in
+  // 16-byte slots; from 13 joints on the 8-byte taint-model slots keep three
+  // CTAs per SM resident (measured C3, 20 joints: 19.4 vs 21.8 ms)
+  const bool err4 = njmax <= 12;
+  const size_t colb = (write || f64 || err4) ? 16 : 8;
   if ((a->flags & LA_SIM_SCATTER) && !a->cand) return fail(LA_EINVAL, "la_simulate: SCATTER needs cand");
   const size_t cs_bytes = ((size_t)a->T * sizeof(float2) + 15) & ~(size_t)15;
   const size_t smem = cs_bytes + (sizeof(WarpHead) + (size_t)njmax * 32 * colb) * SIM_WARPS;
@@ -848,13 +908,17 @@ int la_simulate(const la_sim_args* a, void* stream) {
   using KernT = void (*)(const la_sim_args, int);
   auto pick = [&](auto cnt) -> KernT {
     constexpr bool C = decltype(cnt)::value;
-    return exact ? (wonly ? sim_kernel<true, false, true, true, C>
-                          : write ? (f64 ? sim_kernel<true, true, false, true, C> : sim_kernel<true, false, false, true, C>)
-                                  : (f64 ? sim_kernel<false, true, false, true, C> : sim_kernel<false, false, false, true, C>))
-                 : (wonly ? sim_kernel<true, false, true, false, C>
-                          : write ? (f64 ? sim_kernel<true, true, false, false, C> : sim_kernel<true, false, false, false, C>)
-                                  : (f64 ? sim_kernel<false, true, false, false, C>
-                                         : sim_kernel<false, false, false, false, C>));
+    // ERR4 only matters where the fp32 screen runs (not WONLY / FP64)
+    if (exact) {
+      if (wonly) return sim_kernel<true, false, true, true, C, false>;
+      if (f64) return write ? sim_kernel<true, true, false, true, C, false> : sim_kernel<false, true, false, true, C, false>;
+      if (write) return err4 ? sim_kernel<true, false, false, true, C, true> : sim_kernel<true, false, false, true, C, false>;
+      return err4 ? sim_kernel<false, false, false, true, C, true> : sim_kernel<false, false, false, true, C, false>;
+    }
+    if (wonly) return sim_kernel<true, false, true, false, C, false>;
+    if (f64) return write ? sim_kernel<true, true, false, false, C, false> : sim_kernel<false, true, false, false, C, false>;
+    if (write) return err4 ? sim_kernel<true, false, false, false, C, true> : sim_kernel<true, false, false, false, C, false>;
+    return err4 ? sim_kernel<false, false, false, false, C, true> : sim_kernel<false, false, false, false, C, false>;
   };
   const KernT kern = a->counters ? pick(std::true_type{}) : pick(std::false_type{});
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

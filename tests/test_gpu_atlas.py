@@ -336,3 +336,44 @@ def test_pruned_scan_equals_full_scan_variants(torch, variant):
     pr = chamfer_scan(db, q, k=10, **kw)
     _lists_equal(torch, full, pr)
     assert int(pr["n_full"].sum().item()) < 3 * N  # pruning did engage
+
+
+@pytest.mark.parametrize("case", ["many_queries", "groups_hits_order", "expansion", "odd_q", "fine_grid",
+                                  "outside_unit_square"])
+def test_multi_query_scan_equals_unpruned(torch, case):
+    """The multi-query pruned kernel (query groups sharing each streamed
+    curve, box/gap-table column bound, common-grid row bound, then the
+    single-query stages) returns the unpruned scan's lists: 64 queries,
+    more queries than one group holds (hits, shuffled order, excluded
+    record, pos_map), expansion mode, an odd query length (tail register
+    slot), the 64x64 common grid, and data partly outside [0, 1]^2."""
+    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    N, P = 120_000, 200
+    db = fourier_db(N, P, seed=41, chunk=1 << 16)
+    nq = 150 if case == "groups_hits_order" else 64
+    q = fourier_db(nq, P, seed=42)
+    kw = dict(k=10)
+    if case == "groups_hits_order":
+        dense = chamfer_scan(db, q[:1], k=10, dense=True)["all_d"][0].cpu().numpy()
+        kw.update(k=6, threshold=float(np.quantile(dense, 1e-4)), exclude_id=int(np.argmin(dense)),
+                  order=torch.from_numpy(np.random.default_rng(5).permutation(N)).cuda(),
+                  pos_map=torch.arange(N, device="cuda", dtype=torch.int64) * 3 + 7)
+    elif case == "expansion":
+        kw["expansion"] = True
+    elif case == "odd_q":
+        q = q[:, :133].contiguous()
+    elif case == "fine_grid":
+        kw["mq_fine"] = True
+    elif case == "outside_unit_square":
+        g = torch.Generator(device="cuda")
+        g.manual_seed(7)
+        sel = torch.rand(N, generator=g, device="cuda") < 0.3
+        db = db.clone()
+        db[sel] = db[sel] * 1.7 - 0.35
+        q = q.clone()
+        q[:5] = q[:5] * 1.5 - 0.25
+    mq = chamfer_scan(db, q, **kw)
+    assert int(mq["n_stage"][0].item()) > 0  # the multi-query kernel ran
+    _lists_equal(torch, chamfer_scan(db, q, prune=False, **{k: v for k, v in kw.items() if k != "mq_fine"}), mq)
