@@ -255,6 +255,17 @@ typedef struct la_chamfer_args {
 size_t la_chamfer_workspace(const la_chamfer_args* args);
 int la_chamfer_topk(const la_chamfer_args* args, void* stream);
 
+/* Merge of the per-shard (NQ x k) lists every rank all-gathered (multi-GPU
+ * retrieval): gathered = (device) [world][NQ][6k+1] int64
+ * rows (top_d float bits, top_id, top_pos, hit_d float bits, hit_id,
+ * hit_pos, n_hits); outputs (device) [NQ][k] as la_chamfer_topk's, non-hits
+ * by (d, scan position), hits by scan position, n_hits summed.  Replaces the
+ * scan-order bookkeeping of Atlas.retrieve (atlas.py:207-235) across
+ * shards.                                                                 */
+int la_merge_shard_lists(const int64_t* gathered, int32_t world, int32_t NQ, int32_t k, float* top_d,
+                         int64_t* top_id, int64_t* top_pos, float* hit_d, int64_t* hit_id, int64_t* hit_pos,
+                         int64_t* n_hits, void* stream);
+
 /* ---------------------------------------------------------------- generator
  * Host (CPU, multi-threaded) reproduction of the reference's candidate
  * streams: group g draws n = integers(n_lo, n_hi + 1) and its topology from

@@ -385,6 +385,30 @@ def topk_exhaustive(dists: np.ndarray, scan_pos: np.ndarray, k: int):
     return key[:k]
 
 
+def merge_shard_lists(parts: list, k: int) -> dict:
+    """Merge of per-shard retrieval lists (numpy dicts of (NQ, k) arrays with
+    global ids / scan positions; id < 0 = empty): the scan-order rules of
+    atlas.py:207-235 applied to the union of the shards -- non-hits by
+    (d, scan position), hits by scan position, hit counts summed."""
+    NQ = parts[0]["top_d"].shape[0]
+    out = {"top_d": np.full((NQ, k), np.inf, np.float32), "hit_d": np.full((NQ, k), np.inf, np.float32)}
+    for n in ("top_id", "top_pos", "hit_id", "hit_pos"):
+        out[n] = np.full((NQ, k), -1, np.int64)
+    out["n_hits"] = sum(np.asarray(p["n_hits"], np.int64) for p in parts)
+    for q in range(NQ):
+        for kind in ("top", "hit"):
+            d = np.concatenate([np.asarray(p[f"{kind}_d"][q]) for p in parts])
+            ids = np.concatenate([np.asarray(p[f"{kind}_id"][q]) for p in parts])
+            pos = np.concatenate([np.asarray(p[f"{kind}_pos"][q]) for p in parts])
+            keep = ids >= 0
+            d, ids, pos = d[keep], ids[keep], pos[keep]
+            sel = (np.argsort(pos, kind="stable") if kind == "hit" else np.lexsort((pos, d)))[:k]
+            out[f"{kind}_d"][q, :len(sel)] = d[sel]
+            out[f"{kind}_id"][q, :len(sel)] = ids[sel]
+            out[f"{kind}_pos"][q, :len(sel)] = pos[sel]
+    return out
+
+
 # ---------------------------------------------------------------- coarse filter
 def coarse_descriptor(path: np.ndarray) -> np.ndarray:
     """Radial-histogram + extent descriptor (atlas.py:167-172)."""

@@ -56,6 +56,7 @@ EXPORTS = (
     "la_circle_stats",
     "la_chamfer_workspace",
     "la_chamfer_topk",
+    "la_merge_shard_lists",
     "la_sample_topologies",
     "la_sample_topology_rng",
     "la_sample_poses",
@@ -236,6 +237,7 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_chamfer_workspace.argtypes = [C.POINTER(LaChamferArgs)]
     lib.la_chamfer_workspace.restype = sz
     lib.la_chamfer_topk.argtypes = [C.POINTER(LaChamferArgs), vp]
+    lib.la_merge_shard_lists.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.la_sample_topologies.argtypes = [i64, i64, i64, i32, i32, C.c_double, i32, i32, vp, vp, vp, vp]
     lib.la_sample_topology_rng.argtypes = [vp, vp, i32, C.c_double, i32, vp, vp, vp]
     lib.la_sample_poses.argtypes = [i64, i64, i64, i32, vp, i32, i32, vp]

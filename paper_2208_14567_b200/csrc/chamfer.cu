@@ -1915,6 +1915,67 @@ __global__ void __launch_bounds__(1024) merge_kernel(const ScanCtx c) {
   }
 }
 
+
+// ---- merge of per-shard lists gathered from every rank (dist.gather_merge):
+// packed rows [world][NQ][6k + 1] int64 = top_d bits, top_id, top_pos,
+// hit_d bits, hit_id, hit_pos (k each), n_hits.  Non-hits by (d, global scan
+// position), hits by position (atlas.py:207-235 over the union of shards);
+// entries with id < 0 are empty.  One CTA per query, rank selection.
+__global__ void __launch_bounds__(256) shard_merge_kernel(const int64_t* __restrict__ g, int world, int NQ, int k,
+                                                          float* top_d, int64_t* top_id, int64_t* top_pos,
+                                                          float* hit_d, int64_t* hit_id, int64_t* hit_pos,
+                                                          int64_t* n_hits) {
+  const int qi = blockIdx.x;
+  const int row = 6 * k + 1;
+  const int n = world * k;
+  __shared__ int nvalid[2];
+  if (threadIdx.x < 2) nvalid[threadIdx.x] = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {  // 0: non-hits, 1: hits
+    const int c0 = pass * 3 * k;
+    float* od = pass ? hit_d : top_d;
+    int64_t* oi = pass ? hit_id : top_id;
+    int64_t* op = pass ? hit_pos : top_pos;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int64_t* r = g + ((size_t)(i / k) * NQ + qi) * row;
+      const int e = i % k;
+      const long long id = r[c0 + k + e];
+      if (id < 0) continue;
+      const float d = __int_as_float((int)(r[c0 + e] & 0xffffffffll));
+      const long long pos = r[c0 + 2 * k + e];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const int64_t* rj = g + ((size_t)(j / k) * NQ + qi) * row;
+        const int ej = j % k;
+        if (rj[c0 + k + ej] < 0) continue;
+        const float dj = __int_as_float((int)(rj[c0 + ej] & 0xffffffffll));
+        const long long pj = rj[c0 + 2 * k + ej];
+        const bool less = pass ? (pj < pos || (pj == pos && j < i))
+                               : (key_less(dj, pj, d, pos) || (dj == d && pj == pos && j < i));
+        rank += less;
+      }
+      atomicAdd(&nvalid[pass], 1);
+      if (rank < k) {
+        od[(size_t)qi * k + rank] = d;
+        oi[(size_t)qi * k + rank] = id;
+        op[(size_t)qi * k + rank] = pos;
+      }
+    }
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass)
+    for (int r = nvalid[pass] + threadIdx.x; r < k; r += blockDim.x) {
+      (pass ? hit_d : top_d)[(size_t)qi * k + r] = INFINITY;
+      (pass ? hit_id : top_id)[(size_t)qi * k + r] = -1;
+      (pass ? hit_pos : top_pos)[(size_t)qi * k + r] = -1;
+    }
+  if (threadIdx.x == 0 && n_hits) {
+    long long h = 0;
+    for (int w = 0; w < world; ++w) h += g[((size_t)w * NQ + qi) * row + 6 * k];
+    n_hits[qi] = h;
+  }
+}
+
 struct Plan {
   bool fast;
   int qs;
@@ -2053,6 +2114,18 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 using namespace la;
 
 extern "C" {
+
+int la_merge_shard_lists(const int64_t* gathered, int32_t world, int32_t NQ, int32_t k, float* top_d,
+                         int64_t* top_id, int64_t* top_pos, float* hit_d, int64_t* hit_id, int64_t* hit_pos,
+                         int64_t* n_hits, void* stream) {
+  if (!gathered || world < 1 || NQ < 1 || k < 1 || k > LA_MAX_TOPK || !top_d || !top_id || !top_pos || !hit_d ||
+      !hit_id || !hit_pos)
+    return fail(LA_EINVAL, "la_merge_shard_lists: bad args");
+  if (NQ > 2147483647 || (long long)world * k > (1 << 20)) return fail(LA_ERANGE, "la_merge_shard_lists: too large");
+  shard_merge_kernel<<<NQ, 256, 0, static_cast<cudaStream_t>(stream)>>>(gathered, world, NQ, k, top_d, top_id,
+                                                                       top_pos, hit_d, hit_id, hit_pos, n_hits);
+  return cuda_status("la_merge_shard_lists");
+}
 
 size_t la_chamfer_workspace(const la_chamfer_args* a) {
   if (!a) return 0;

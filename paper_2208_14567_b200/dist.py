@@ -6,14 +6,18 @@ record ranges; each rank scans its records in GLOBAL scan order (the
 restriction of the atlas permutation to its shard), so its per-query lists
 carry global ids and global scan positions.  The only exchange is one
 ``all_gather_into_tensor`` of the small (Q x k) lists over NCCL (NVLink /
-NVSwitch on a B200 node; gloo in the CPU tests), after which every rank
-merges deterministically: non-hits by (distance, scan position), hits by
-scan position (the threshold rule of atlas.py:207-235).
+NVSwitch on a B200 node; gloo when the ranks share a GPU or in the CPU
+tests), after which every rank merges the gathered lists on its device with
+``la_merge_shard_lists``: non-hits by (distance, scan position), hits by scan
+position (the threshold rule of atlas.py:207-235).  No host round trip on
+the NCCL path.
 """
 
 from __future__ import annotations
 
 import numpy as np
+
+from . import _native as N
 
 LIST_KEYS = ("top_d", "top_id", "top_pos", "hit_d", "hit_id", "hit_pos")
 
@@ -44,82 +48,68 @@ def local_scan_plan(order: np.ndarray, lo: int, hi: int) -> tuple[np.ndarray, np
     return order[pos] - lo, pos
 
 
-def _empty_like_lists(NQ: int, k: int, torch):
-    return {
-        "top_d": torch.full((NQ, k), float("inf"), dtype=torch.float32),
-        "top_id": torch.full((NQ, k), -1, dtype=torch.int64),
-        "top_pos": torch.full((NQ, k), -1, dtype=torch.int64),
-        "hit_d": torch.full((NQ, k), float("inf"), dtype=torch.float32),
-        "hit_id": torch.full((NQ, k), -1, dtype=torch.int64),
-        "hit_pos": torch.full((NQ, k), -1, dtype=torch.int64),
-        "n_hits": torch.zeros(NQ, dtype=torch.int64),
-    }
-
-
-def merge_lists(parts: list[dict], k: int) -> dict:
-    """Deterministic merge of per-shard lists (host tensors).
-
-    Non-hits: ascending (d, global scan position); hits: ascending position.
-    Missing entries (id < 0) are dropped; the result is padded like the
-    kernel output (d = inf, id = pos = -1).
-    """
-    import torch
-
-    NQ = parts[0]["top_d"].shape[0]
-    out = _empty_like_lists(NQ, k, torch)
-    out["n_hits"] = sum(p["n_hits"].to(torch.int64) for p in parts)
-    for q in range(NQ):
-        for kind in ("top", "hit"):
-            d = torch.cat([p[f"{kind}_d"][q] for p in parts]).numpy()
-            ids = torch.cat([p[f"{kind}_id"][q] for p in parts]).numpy()
-            pos = torch.cat([p[f"{kind}_pos"][q] for p in parts]).numpy()
-            keep = ids >= 0
-            d, ids, pos = d[keep], ids[keep], pos[keep]
-            sel = np.argsort(pos, kind="stable") if kind == "hit" else np.lexsort((pos, d))
-            sel = sel[:k]
-            m = len(sel)
-            out[f"{kind}_d"][q, :m] = torch.from_numpy(d[sel].astype(np.float32))
-            out[f"{kind}_id"][q, :m] = torch.from_numpy(ids[sel])
-            out[f"{kind}_pos"][q, :m] = torch.from_numpy(pos[sel])
-    return out
-
-
 def pack_lists(lists: dict, k: int):
-    """(NQ, 6k + 1) float64 carrier of one rank's lists (ids and positions
-    are < 2^53, exact in f64)."""
+    """(NQ, 6k + 1) int64 rows of one rank's lists, on the lists' device:
+    top_d float bits, top_id, top_pos, hit_d float bits, hit_id, hit_pos,
+    n_hits (the layout la_merge_shard_lists reads)."""
     import torch
 
-    cols = [lists[n].to(torch.float64) for n in LIST_KEYS] + [lists["n_hits"].to(torch.float64)[:, None]]
+    cols = []
+    for n in LIST_KEYS:
+        v = lists[n]
+        cols.append(v.contiguous().view(torch.int32).to(torch.int64) if n.endswith("_d") else v.to(torch.int64))
+    cols.append(lists["n_hits"].to(torch.int64)[:, None])
     return torch.cat(cols, dim=1).contiguous()
 
 
 def unpack_lists(buf, k: int) -> dict:
+    """Inverse of pack_lists (any device)."""
     import torch
 
     out = {}
     for i, n in enumerate(LIST_KEYS):
         col = buf[:, i * k:(i + 1) * k]
-        out[n] = col.to(torch.float32) if n.endswith("_d") else col.to(torch.int64)
-    out["n_hits"] = buf[:, 6 * k].to(torch.int64)
+        out[n] = col.to(torch.int32).view(torch.float32) if n.endswith("_d") else col.contiguous()
+    out["n_hits"] = buf[:, 6 * k].contiguous()
     return out
 
 
-def gather_merge(lists: dict, k: int, group=None) -> dict:
-    """All-gather every rank's (Q x k) lists and merge them identically on
-    each rank.  One collective: all_gather_into_tensor."""
+def gather_lists(lists: dict, k: int, group=None):
+    """All-gather every rank's packed lists: (world, NQ, 6k + 1) int64 on the
+    collective's device (CUDA for NCCL, host for gloo).  One collective."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    mine = pack_lists({n: v for n, v in lists.items() if n in LIST_KEYS or n == "n_hits"}, k)
-    dev = mine.device
-    if dist.get_backend(group) == "nccl" and not mine.is_cuda:
-        mine = mine.cuda()
-        dev = mine.device
-    elif dist.get_backend(group) == "gloo" and mine.is_cuda:
+    mine = pack_lists(lists, k)
+    if dist.get_backend(group) == "gloo":
         mine = mine.cpu()
-        dev = mine.device
-    allb = torch.empty((world * mine.shape[0], mine.shape[1]), dtype=mine.dtype, device=dev)
+    elif not mine.is_cuda:
+        raise ValueError("NCCL gather needs CUDA lists")
+    allb = torch.empty((world * mine.shape[0], mine.shape[1]), dtype=mine.dtype, device=mine.device)
     dist.all_gather_into_tensor(allb, mine, group=group)
-    allb = allb.cpu().view(world, mine.shape[0], mine.shape[1])
-    return merge_lists([unpack_lists(allb[r], k) for r in range(world)], k)
+    return allb.view(world, mine.shape[0], mine.shape[1])
+
+
+def merge_gathered(gathered, k: int, stream=None) -> dict:
+    """la_merge_shard_lists over a (world, NQ, 6k + 1) gathered buffer; the
+    merged (NQ, k) lists stay on the device."""
+    torch = N.require_cuda()
+    lib = N.load()
+    g = gathered.to(device="cuda", dtype=torch.int64).contiguous()
+    world, NQ, row = g.shape
+    if row != 6 * k + 1:
+        raise ValueError("gathered rows do not match k")
+    dev = g.device
+    out = {n: torch.empty((NQ, k), dtype=torch.float32 if n.endswith("_d") else torch.int64, device=dev)
+           for n in LIST_KEYS}
+    out["n_hits"] = torch.empty(NQ, dtype=torch.int64, device=dev)
+    N.check(lib.la_merge_shard_lists(g.data_ptr(), world, NQ, k, *(out[n].data_ptr() for n in LIST_KEYS),
+                                     out["n_hits"].data_ptr(), N.stream_ptr(stream)), "la_merge_shard_lists")
+    return out
+
+
+def gather_merge(lists: dict, k: int, group=None, stream=None) -> dict:
+    """All-gather every rank's (Q x k) lists and merge them identically on
+    each rank's device (one collective + one merge kernel)."""
+    return merge_gathered(gather_lists(lists, k, group), k, stream)

@@ -1,6 +1,9 @@
-"""world_size-2 gloo test of the multi-GPU merge path (CPU): each rank builds
-its shard's (Q x k) lists from oracle distances exactly as the kernel defines
-them, all-gathers them, and must reproduce the single-scan answer."""
+"""world_size-2 gloo test of the multi-GPU exchange path (CPU): each rank
+builds its shard's (Q x k) lists from oracle distances exactly as the kernel
+defines them, packs and all-gathers them (dist.gather_lists, the product's
+one collective); the gathered rows must unpack to every rank's lists, and
+their merge (oracle merge_shard_lists here; la_merge_shard_lists on the GPU,
+tests/test_gpu_dist.py) must reproduce the single-scan answer."""
 
 import os
 import socket
@@ -12,7 +15,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import links_oracle as O
-from paper_2208_14567_b200.dist import balanced_ranges, gather_merge, local_scan_plan, merge_lists, shard_range
+from paper_2208_14567_b200.dist import (balanced_ranges, gather_lists, local_scan_plan, pack_lists, shard_range,
+                                         unpack_lists)
 
 K = 5
 THR = 0.2
@@ -58,8 +62,14 @@ def _worker(rank, world, port, q):
         lorder, pmap = local_scan_plan(order, lo, hi)
         ids = lorder + lo
         mine = lists_for(d[:, ids], ids, pmap, K, THR)
-        merged = gather_merge(mine, K)
-        q.put((rank, {k: v.numpy() for k, v in merged.items()}))
+        g = gather_lists(mine, K)
+        assert tuple(g.shape) == (world, d.shape[0], 6 * K + 1)
+        parts = [{n: v.numpy() for n, v in unpack_lists(g[r], K).items()} for r in range(world)]
+        mine_back = parts[rank]
+        for n, v in mine.items():
+            assert np.array_equal(mine_back[n], v.numpy()), n
+        merged = O.merge_shard_lists(parts, K)
+        q.put((rank, merged))
     finally:
         dist.destroy_process_group()
 
@@ -96,14 +106,17 @@ def test_gather_merge_world2_equals_single_scan():
     assert res["n_hits"][0] == int((d[0] < THR).sum())
 
 
-def test_merge_lists_single_part_identity():
+def test_pack_unpack_roundtrip_and_single_part_merge():
     N, order, d = problem()
     pos_of = np.empty(N, dtype=np.int64)
     pos_of[order] = np.arange(N)
     lists = lists_for(d, np.arange(N), pos_of, K, THR)
-    m = merge_lists([lists], K)
+    back = unpack_lists(pack_lists(lists, K), K)
     for name in lists:
-        assert torch.equal(m[name], lists[name])
+        assert torch.equal(back[name], lists[name]), name
+    m = O.merge_shard_lists([{n: v.numpy() for n, v in lists.items()}], K)
+    for name in lists:
+        assert np.array_equal(m[name], lists[name].numpy()), name
 
 
 def test_balanced_ranges_cover():

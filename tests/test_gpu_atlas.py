@@ -122,7 +122,7 @@ def test_scan_threshold_mode_and_shards(torch):
     shard decomposition used by the multi-GPU merge give the same answer
     as one scan over everything."""
     from paper_2208_14567_b200.atlas import chamfer_scan
-    from paper_2208_14567_b200.dist import local_scan_plan, merge_lists
+    from paper_2208_14567_b200.dist import local_scan_plan, merge_gathered, pack_lists
     from paper_2208_14567_b200.workloads import fourier_db
 
     N, P = 30_000, 64
@@ -150,9 +150,9 @@ def test_scan_threshold_mode_and_shards(torch):
         lorder, pmap = local_scan_plan(order, lo, hi)
         parts.append(chamfer_scan(db[lo:hi], qs, k=7, threshold=0.25, order=torch.from_numpy(lorder).cuda(),
                                   pos_map=torch.from_numpy(pmap).cuda(), id_base=lo))
-    merged = merge_lists([{k: v.cpu() for k, v in p.items() if not k.startswith("_")} for p in parts], 7)
-    for name in ("top_id", "hit_id", "top_pos", "hit_pos", "n_hits"):
-        assert torch.equal(merged[name], res[name].cpu()), name
+    merged = merge_gathered(torch.stack([pack_lists(p, 7) for p in parts]), 7)  # la_merge_shard_lists
+    for name in ("top_d", "top_id", "hit_id", "top_pos", "hit_pos", "n_hits"):
+        assert torch.equal(merged[name], res[name]), name
 
 
 def test_retrieve_large_k_and_budget(torch, atlas_fx):
