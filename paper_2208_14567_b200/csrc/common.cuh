@@ -49,10 +49,13 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
-// glibc's hypot for finite binary64 (Borges' corrected sqrt, non-FMA
-// kernel), the function numpy.hypot calls; explicit round-to-nearest ops so
-// nothing is contracted.  Bit-identical to np.hypot (checked on 2e7 pairs,
-// tests/test_gpu_filter.py, tests/test_gpu_solver.py).
+// hypot for finite binary64 with the algorithm of glibc's __ieee754_hypot
+// (Borges, "An Improved Algorithm for hypot(a,b)", 2019: corrected square
+// root, the non-FMA kernel), the function numpy.hypot calls on Linux; explicit
+// round-to-nearest ops so nothing is contracted.  Provenance: restated from
+// the published algorithm to reproduce np.hypot bit for bit, not copied from
+// glibc's sources (LGPL-2.1); bit-identical to np.hypot (checked on 2e7
+// pairs, tests/test_gpu_filter.py, tests/test_gpu_solver.py).
 __device__ __forceinline__ double np_hypot(double x, double y) {
   x = fabs(x);
   y = fabs(y);
