@@ -518,7 +518,9 @@ def e2e_c2(torch, args, mb, table, world):
     # buffers) are what the in-run parity check reads
     return {"value": world * mb.B / (ms / 1e3), "unit": "simulations/s", "h2d_bytes_per_step": stats["h2d"],
             "d2h_bytes_per_step": stats["d2h"], "ms_per_step": ms, "chunks": E2E_CHUNKS,
-            "api": "solver.HostPipeline.run (pinned host poses -> host flags + dense fp32 paths)"}, (pipe, res)
+            "api": "solver.HostPipeline.run (pinned host poses -> host flags + dense fp32 dyad-target paths; "
+                   "static joints and crank tip closed-form in the poses, rebuilt by HostPipeline.paths)",
+            "rows_shipped": "dyad targets (the device writes every joint's rows)"}, (pipe, res)
 
 
 def _c2_parity_worker(gids):
@@ -526,12 +528,16 @@ def _c2_parity_worker(gids):
     groups, compared with the GPU outputs of the last timed e2e step."""
     from oracle import links_oracle as O
 
+    from paper_2208_14567_b200.solver import assemble_paths
+
     S = _FORK["c2"]
     mb, ft, fj, row_of, traj, starts = S["mb"], S["ft"], S["fj"], S["row_of"], S["traj"], S["starts"]
+    row2_of, traj2 = S["row2_of"], S["traj2"]
     a = dict(checked=0, valid_ref=0, valid_both=0, flag_mismatch=0, flag_mismatch_outside_margin=0,
              near_margin=0, near_margin_mismatch=0, worst_mech_rel=0.0, worst_path_rel=0.0, worst_abs=0.0,
              paths_checked=0, small_paths=0, worst_small_path_abs=0.0, values=0, f32_round_mismatch=0,
-             static_rows_exact=True, locked_ref=0, acc_ref=0.0, locked_gpu=0, acc_gpu=0.0)
+             static_rows_exact=True, rebuilt_rows_equal_device=True, locked_ref=0, acc_ref=0.0, locked_gpu=0,
+             acc_gpu=0.0)
     for g in gids:
         plan = mb.plans[g]
         n = plan.n
@@ -554,8 +560,15 @@ def _c2_parity_worker(gids):
         if len(vb) == 0:
             continue
         Pr = O.trajectories(r)[vb]                                   # (V, n, T, 2) f64
-        rows = row_of[lo + vb][:, None] + np.arange(n)[None, :]
-        Pg = traj[rows.reshape(-1)].reshape(len(vb), n, T, 2)       # fp32 as stored
+        # the e2e result: dyad-target rows shipped, static joints + crank tip
+        # rebuilt on the host from the poses (split rows); the device wrote
+        # those rows too (traj2) and they must equal the rebuild bit for bit
+        targets = sorted(s_[0] for s_ in steps)
+        others = [j for j in range(n) if j not in set(targets)]
+        Pg = np.stack([assemble_paths(traj, int(row_of[lo + b]), mb.pos[lo + b, :n], n, targets, T) for b in vb])
+        dev_o = traj2[(row2_of[lo + vb][:, None] + np.arange(len(others))[None, :]).reshape(-1)]
+        a["rebuilt_rows_equal_device"] &= bool(np.array_equal(dev_o.reshape(len(vb), len(others), T, 2),
+                                                             Pg[:, others]))
         a["acc_ref"] += float(Pr[:, -1, -1, 0].sum())
         a["acc_gpu"] += float(Pg[:, -1, -1, 0].astype(np.float64).sum())
         a["valid_both"] += len(vb)
@@ -582,7 +595,7 @@ def _c2_parity_worker(gids):
     return a
 
 
-def parity_c2(mb, res, dev_first_t):
+def parity_c2(mb, res, dev_first_t, pipe=None):
     """In-run parity of the timed C2 outputs (the last e2e step's host
     buffers) against the oracle on ALL candidates: lock flags bit-exact
     outside the 1e-6 margin band, the near-margin count, path
@@ -596,8 +609,18 @@ def parity_c2(mb, res, dev_first_t):
     fj = res["first_joint"].numpy().copy()
     row_of = np.full(B, -1, dtype=np.int64)
     row_of[res["pend_idx"].numpy()] = res["pend_row"].numpy()
+    # the device's other-joint rows (traj2) of every chunk, by candidate
+    row2_of = np.full(B, -1, dtype=np.int64)
+    parts2, base2 = [], 0
+    for (lo, _), g in zip(pipe.ranges, pipe.graphs):
+        o = g.out
+        npend, nr2 = int(o["pend_count"].item()), int(o["pend_rows2"].item())
+        row2_of[o["pend_idx"][:npend].cpu().numpy() + lo] = o["pend_row2"][:npend].cpu().numpy() + base2
+        parts2.append(o["traj2"][:nr2].cpu().numpy())
+        base2 += nr2
     starts = np.searchsorted(mb.topo, np.arange(len(mb.plans) + 1))
-    _FORK["c2"] = dict(mb=mb, ft=ft, fj=fj, row_of=row_of, traj=res["traj"].numpy().copy(), starts=starts)
+    _FORK["c2"] = dict(mb=mb, ft=ft, fj=fj, row_of=row_of, traj=res["traj"].numpy().copy(), starts=starts,
+                       row2_of=row2_of, traj2=np.concatenate(parts2))
     cores = _cores()
     G = len(mb.plans)
     parts, dt = _fork_map(_c2_parity_worker, [list(range(w, G, cores)) for w in range(cores)], cores)
@@ -606,13 +629,14 @@ def parity_c2(mb, res, dev_first_t):
         for k, v in p.items():
             if k.startswith("worst"):
                 a[k] = max(a.get(k, 0.0), v)
-            elif k == "static_rows_exact":
+            elif k in ("static_rows_exact", "rebuilt_rows_equal_device"):
                 a[k] = a.get(k, True) and v
             else:
                 a[k] = a.get(k, 0) + (float(v) if isinstance(v, float) else int(v))
     a["device_flags_equal_e2e"] = bool(np.array_equal(dev_first_t, ft))
     a["digest"] = {"gpu": (a.pop("locked_gpu"), a.pop("acc_gpu")), "oracle": (a.pop("locked_ref"), a.pop("acc_ref"))}
     a["ok"] = bool(a["flag_mismatch_outside_margin"] == 0 and a["worst_path_rel"] <= 1e-4
+                   and a["rebuilt_rows_equal_device"]
                    and a["worst_mech_rel"] <= 1e-4 and a["digest"]["gpu"][0] == a["digest"]["oracle"][0]
                    and a["checked"] == B and a["device_flags_equal_e2e"])
     a["seconds"] = dt
@@ -1438,7 +1462,7 @@ def main():
     cpu = parity = None
     if want_cpu:
         cpu = cpu_baseline_c2(c2["mb"])
-        parity = parity_c2(c2["mb"], e2e_res, c2["dev_first_t"])
+        parity = parity_c2(c2["mb"], e2e_res, c2["dev_first_t"], pipe)
     del pipe
     if rank == 0:
         rl = dict(c2["roofline"])

@@ -124,6 +124,11 @@ typedef struct la_sim_args {
                                  dyads); tau is the floor (default 2e-6).
                                  Trajectory rounds always run in f64        */
   uint32_t flags;             /* LA_SIM_*                                     */
+  void* traj2;                /* (device, optional) split rows: with it the
+                                 write pass stores dyad-target rows in traj
+                                 and the other joints' rows (static joints,
+                                 crank tip) in traj2, ascending joint order  */
+  const int64_t* traj_row2;   /* (device) [B] first traj2 row of item i      */
   int32_t screen_refill;      /* lane screen: refill free lanes once at least
                                  this many are free (0 => 8)                 */
   int32_t screen_replay;      /* lane screen: replay parked (ambiguous)
@@ -158,6 +163,13 @@ int la_compact_valid(const int32_t* first_t, int64_t B, int32_t T,
  * la_sim_args.traj_row = row_off a write pass stores (T,2) paths for the
  * real joints only (no padding rows up to traj_stride).                    */
 size_t la_compact_rows_workspace(int64_t B);
+/* Split rows: per selected item its dyad-target rows (plan nsteps) and its
+ * other rows (static joints + crank tip, n - nsteps), two running sums; the
+ * write pass stores them to traj / traj2 (la_sim_args.traj2).             */
+size_t la_compact_rows_split_workspace(int64_t B);
+int la_compact_rows_split(const int32_t* first_t, int64_t B, int32_t T, const int32_t* topo, const la_plan* plans,
+                          int64_t* idx, int64_t* target_row, int64_t* other_row, int64_t* count,
+                          int64_t* target_total, int64_t* other_total, void* ws, size_t ws_bytes, void* stream);
 int la_compact_rows(const int32_t* first_t, int64_t B, int32_t T, const int32_t* topo,
                     const la_plan* plans, int64_t* idx, int64_t* row_off, int64_t* count,
                     int64_t* row_total, void* ws, size_t ws_bytes, void* stream);

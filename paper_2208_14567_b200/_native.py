@@ -52,6 +52,8 @@ EXPORTS = (
     "la_compact_valid",
     "la_compact_rows_workspace",
     "la_compact_rows",
+    "la_compact_rows_split_workspace",
+    "la_compact_rows_split",
     "la_normalize",
     "la_circle_stats",
     "la_chamfer_workspace",
@@ -153,6 +155,8 @@ class LaSimArgs(C.Structure):
         ("counters", C.c_void_p),
         ("fixup_tau", C.c_float),
         ("flags", C.c_uint32),
+        ("traj2", C.c_void_p),
+        ("traj_row2", C.c_void_p),
         ("screen_refill", C.c_int32),
         ("screen_replay", C.c_int32),
     ]
@@ -232,6 +236,9 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_compact_rows_workspace.argtypes = [i64]
     lib.la_compact_rows_workspace.restype = sz
     lib.la_compact_rows.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.la_compact_rows_split_workspace.argtypes = [i64]
+    lib.la_compact_rows_split_workspace.restype = sz
+    lib.la_compact_rows_split.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.la_normalize.argtypes = [C.POINTER(LaNormArgs), vp]
     lib.la_circle_stats.argtypes = [vp, i32, i64, i32, vp, vp, vp]
     lib.la_chamfer_workspace.argtypes = [C.POINTER(LaChamferArgs)]
@@ -269,7 +276,8 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_last_error.restype = C.c_char_p
     lib.la_device_sm_count.argtypes = []
     for name in EXPORTS:
-        if name not in ("la_last_error", "la_compact_workspace", "la_compact_rows_workspace", "la_chamfer_workspace",
+        if name not in ("la_last_error", "la_compact_workspace", "la_compact_rows_workspace",
+                        "la_compact_rows_split_workspace", "la_chamfer_workspace",
                         "la_coarse_workspace",
                         "la_gen_create",
                         "la_gen_destroy", "la_gen_window", "la_gen_window_dev", "la_gen_count", "la_moving_joints"):

@@ -496,13 +496,10 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
       H.st[lane] = r;
     }
     {
+      // crank radius as np.hypot in every mode (solver.py:180): with the
+      // host's crank table the crank tip row is then rebuilt bit for bit
       const double dx = dsub(H.p0[1].x, H.p0[0].x), dy = dsub(H.p0[1].y, H.p0[0].y);
-      if (EXACT) {
-        C.r1 = np_hypot(dx, dy);  // solver.py:180
-      } else {
-        const double r2 = dadd(dmul(dx, dx), dmul(dy, dy));
-        C.r1 = r2 > 0.0 ? dmul(r2, rsqrt_f64(r2)) : 0.0;
-      }
+      C.r1 = np_hypot(dx, dy);
       C.r1f = (float)C.r1;
       C.p0f = make_float2((float)H.p0[0].x, (float)H.p0[0].y);
     }
@@ -571,6 +568,17 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
         const bool out64 = (p.flags & LA_SIM_TRAJ_F64) != 0;
         float2* out = reinterpret_cast<float2*>(p.traj) + (size_t)row * T;
         double2* out_d = reinterpret_cast<double2*>(p.traj) + (size_t)row * T;
+        // split rows (traj2): dyad targets to traj, the static joints and the
+        // crank tip (closed-form in the inputs, solver.py:183-187) to traj2,
+        // each in ascending joint order
+        const bool split = p.traj2 != nullptr;
+        uint32_t tmask = 0u;
+        float2* out2 = nullptr;
+        if (split) {
+#pragma unroll 1
+          for (int s = 0; s < C.ns; ++s) tmask |= 1u << H.tg[s];
+          out2 = reinterpret_cast<float2*>(p.traj2) + (size_t)p.traj_row2[item] * T;
+        }
 #pragma unroll 1
         for (int r = 0; r * 32 < T; ++r) {
           const int t = r * 32 + lane;
@@ -591,6 +599,17 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
               double2* o = out_d + t;
 #pragma unroll 1
               for (int j = 0; j < C.n; ++j, a += 512u, o += T) __stcs(o, lds_d2(a));
+            } else if (split) {
+              float2* o = out + t;
+              float2* o2 = out2 + t;
+#pragma unroll 1
+              for (int j = 0; j < C.n; ++j, a += 512u) {
+                const double2 v = lds_d2(a);
+                const bool tj = (tmask >> j) & 1u;
+                st_cs(tj ? o : o2, make_float2((float)v.x, (float)v.y));
+                if (tj) o += T;
+                else o2 += T;
+              }
             } else {
               float2* o = out + t;
 #pragma unroll 2
@@ -801,72 +820,121 @@ __global__ void compact_scatter(const int32_t* __restrict__ first_t, int64_t B, 
 __device__ __forceinline__ int item_rows(const int32_t* topo, const la_plan* plans, long long i) {
   return plans[topo ? topo[i] : 0].n;
 }
+// split rows: dyad targets (nsteps rows) / the other joints (static + crank)
+__device__ __forceinline__ int2 item_rows2(const int32_t* topo, const la_plan* plans, long long i) {
+  const la_plan& p = plans[topo ? topo[i] : 0];
+  return make_int2(p.nsteps, p.n - p.nsteps);
+}
 
+template <bool SPLIT>
 __global__ void rows_count(const int32_t* __restrict__ first_t, int64_t B, int32_t T, const int32_t* __restrict__ topo,
-                           const la_plan* __restrict__ plans, int32_t* tile_count, int32_t* tile_rows) {
+                           const la_plan* __restrict__ plans, int32_t* tile_count, int32_t* tile_rows,
+                           int32_t* tile_rows2) {
   const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
   const bool v = i < B && first_t[i] == T;
-  int r = v ? item_rows(topo, plans, i) : 0;
+  int r = 0, r2 = 0;
+  if (v) {
+    if (SPLIT) {
+      const int2 q = item_rows2(topo, plans, i);
+      r = q.x;
+      r2 = q.y;
+    } else {
+      r = item_rows(topo, plans, i);
+    }
+  }
   const unsigned bal = __ballot_sync(FULL, v);
-  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(FULL, r, o);
-  __shared__ int wc[CP_THREADS / 32], wr[CP_THREADS / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    r += __shfl_xor_sync(FULL, r, o);
+    if (SPLIT) r2 += __shfl_xor_sync(FULL, r2, o);
+  }
+  __shared__ int wc[CP_THREADS / 32], wr[CP_THREADS / 32], wr2[CP_THREADS / 32];
   if ((threadIdx.x & 31) == 0) {
     wc[threadIdx.x >> 5] = __popc(bal);
     wr[threadIdx.x >> 5] = r;
+    wr2[threadIdx.x >> 5] = r2;
   }
   __syncthreads();
   if (threadIdx.x < 32) {
-    int c = wc[threadIdx.x], s = wr[threadIdx.x];
+    int c = wc[threadIdx.x], s = wr[threadIdx.x], s2 = wr2[threadIdx.x];
     for (int o = 16; o > 0; o >>= 1) {
       c += __shfl_xor_sync(FULL, c, o);
       s += __shfl_xor_sync(FULL, s, o);
+      s2 += __shfl_xor_sync(FULL, s2, o);
     }
     if (threadIdx.x == 0) {
       tile_count[blockIdx.x] = c;
       tile_rows[blockIdx.x] = s;
+      if (SPLIT) tile_rows2[blockIdx.x] = s2;
     }
   }
 }
 
+template <bool SPLIT>
 __global__ void rows_scatter(const int32_t* __restrict__ first_t, int64_t B, int32_t T,
                              const int32_t* __restrict__ topo, const la_plan* __restrict__ plans,
                              const int32_t* __restrict__ tile_off, const int32_t* __restrict__ tile_row_off,
-                             int64_t* idx, int64_t* row_off) {
+                             const int32_t* __restrict__ tile_row_off2, int64_t* idx, int64_t* row_off,
+                             int64_t* row_off2) {
   const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
   const bool v = i < B && first_t[i] == T;
-  const int r = v ? item_rows(topo, plans, i) : 0;
+  int r = 0, r2 = 0;
+  if (v) {
+    if (SPLIT) {
+      const int2 q = item_rows2(topo, plans, i);
+      r = q.x;
+      r2 = q.y;
+    } else {
+      r = item_rows(topo, plans, i);
+    }
+  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned bal = __ballot_sync(FULL, v);
-  int x = r;  // inclusive warp scan of the row counts
+  int x = r, x2 = r2;  // inclusive warp scans of the row counts
   for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(FULL, x, o);
-    if (lane >= o) x += y;
+    const int y = __shfl_up_sync(FULL, x, o), y2 = __shfl_up_sync(FULL, x2, o);
+    if (lane >= o) {
+      x += y;
+      x2 += y2;
+    }
   }
-  __shared__ int wc[CP_THREADS / 32], wr[CP_THREADS / 32];
+  __shared__ int wc[CP_THREADS / 32], wr[CP_THREADS / 32], wr2[CP_THREADS / 32];
   if (lane == 31) {
     wc[w] = __popc(bal);
     wr[w] = x;
+    wr2[w] = x2;
   }
   __syncthreads();
   if (threadIdx.x < 32) {  // exclusive scan of the warp totals
-    const int c = wc[lane], s = wr[lane];
-    int xc = c, xs = s;
+    const int c = wc[lane], s = wr[lane], s2 = wr2[lane];
+    int xc = c, xs = s, xs2 = s2;
     for (int o = 1; o < 32; o <<= 1) {
-      const int yc = __shfl_up_sync(FULL, xc, o), ys = __shfl_up_sync(FULL, xs, o);
+      const int yc = __shfl_up_sync(FULL, xc, o), ys = __shfl_up_sync(FULL, xs, o),
+                ys2 = __shfl_up_sync(FULL, xs2, o);
       if (lane >= o) {
         xc += yc;
         xs += ys;
+        xs2 += ys2;
       }
     }
     wc[lane] = xc - c;
     wr[lane] = xs - s;
+    wr2[lane] = xs2 - s2;
   }
   __syncthreads();
   if (v) {
     const long long pos = (long long)tile_off[blockIdx.x] + wc[w] + __popc(bal & ((1u << lane) - 1u));
     idx[pos] = i;
     row_off[pos] = (long long)tile_row_off[blockIdx.x] + wr[w] + (x - r);
+    if (SPLIT) row_off2[pos] = (long long)tile_row_off2[blockIdx.x] + wr2[w] + (x2 - r2);
   }
+}
+
+// the three tile arrays of la_compact_rows_split in one launch
+__global__ void compact_scan3(int32_t* tile_count, int32_t* tile_rows, int32_t* tile_rows2, long long ntiles,
+                              int64_t* total, int64_t* total_rows, int64_t* total_rows2) {
+  scan_tiles(tile_count, ntiles, total);
+  scan_tiles(tile_rows, ntiles, total_rows);
+  scan_tiles(tile_rows2, ntiles, total_rows2);
 }
 
 }  // namespace
@@ -984,10 +1052,39 @@ int la_compact_rows(const int32_t* first_t, int64_t B, int32_t T, const int32_t*
   const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
   int32_t* tc = static_cast<int32_t*>(ws);
   int32_t* tr = tc + la_compact_workspace(B) / sizeof(int32_t);
-  rows_count<<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr);
+  rows_count<false><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, nullptr);
   compact_scan2<<<1, 1024, 0, s>>>(tc, tr, tiles, count, row_total);
-  rows_scatter<<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, idx, row_off);
+  rows_scatter<false><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, nullptr, idx,
+                                                             row_off, nullptr);
   return cuda_status("la_compact_rows");
+}
+
+size_t la_compact_rows_split_workspace(int64_t B) { return 3 * la_compact_workspace(B); }
+
+int la_compact_rows_split(const int32_t* first_t, int64_t B, int32_t T, const int32_t* topo, const la_plan* plans,
+                          int64_t* idx, int64_t* target_row, int64_t* other_row, int64_t* count,
+                          int64_t* target_total, int64_t* other_total, void* ws, size_t ws_bytes, void* stream) {
+  if (B < 0 || B >= (1ll << 31) / LA_MAX_JOINTS || !first_t || !plans || !idx || !target_row || !other_row ||
+      !count || !target_total || !other_total)
+    return fail(LA_EINVAL, "la_compact_rows_split: bad args");
+  if (ws_bytes < la_compact_rows_split_workspace(B) || !ws) return fail(LA_EWS, "la_compact_rows_split: workspace");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (B == 0) {
+    cudaMemsetAsync(count, 0, sizeof(int64_t), s);
+    cudaMemsetAsync(target_total, 0, sizeof(int64_t), s);
+    cudaMemsetAsync(other_total, 0, sizeof(int64_t), s);
+    return cuda_status("la_compact_rows_split");
+  }
+  const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
+  const size_t per = la_compact_workspace(B) / sizeof(int32_t);
+  int32_t* tc = static_cast<int32_t*>(ws);
+  int32_t* tr = tc + per;
+  int32_t* tr2 = tr + per;
+  rows_count<true><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, tr2);
+  compact_scan3<<<1, 1024, 0, s>>>(tc, tr, tr2, tiles, count, target_total, other_total);
+  rows_scatter<true><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, tr2, idx,
+                                                            target_row, other_row);
+  return cuda_status("la_compact_rows_split");
 }
 
 int la_compact_valid(const int32_t* first_t, int64_t B, int32_t T, int64_t* valid_idx,

@@ -209,7 +209,7 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
                      fixup_tau: float = DEFAULT_FIXUP_TAU, fp64: bool = False, gate_only: bool = False,
                      coarse: bool = True, counters=None, stream=None, exact: bool | None = None,
                      _extra_flags: int = 0, _screen: tuple[int, int] = (0, 0),
-                     _outputs=None) -> dict:
+                     traj2=None, traj_row2=None, _outputs=None) -> dict:
     """Launch la_simulate on device tensors.
 
     pos0: (B, S, 2) float64 CUDA tensor (S >= every plan's n); topo: (B,)
@@ -292,6 +292,9 @@ def simulate_tensors(pos0, table: PlanTable, T: int = 200, topo=None, *, write_t
     a.fixup_tau = float(fixup_tau)
     a.flags = flags
     a.screen_refill, a.screen_replay = int(_screen[0]), int(_screen[1])
+    if (traj2 is None) != (traj_row2 is None):
+        raise ValueError("traj2 and traj_row2 go together")
+    a.traj2, a.traj_row2 = N.ptr(traj2), N.ptr(traj_row2)
     N.check(lib.la_simulate(a, N.stream_ptr(stream)), "la_simulate")
     return out
 
@@ -332,9 +335,72 @@ def compact_rows(first_t, T: int, table: "PlanTable", topo=None, stream=None):
     return idx, row, cnt, tot
 
 
+def compact_rows_split(first_t, T: int, table: "PlanTable", topo=None, stream=None):
+    """la_compact_rows_split: ascending indices of candidates with
+    first_t == T, and for each its first dyad-target row and first other row
+    (static joints + crank tip) in two dense row sets; device counts: items,
+    target rows, other rows."""
+    torch = N.require_cuda()
+    lib = N.load()
+    B = first_t.numel()
+    dev = first_t.device
+    idx, row, row2 = (torch.empty(max(B, 1), dtype=torch.int64, device=dev) for _ in range(3))
+    cnt, tot, tot2 = (torch.empty(1, dtype=torch.int64, device=dev) for _ in range(3))
+    if topo is not None:
+        topo = topo.to(device=dev, dtype=torch.int32).contiguous()
+    wsb = int(lib.la_compact_rows_split_workspace(B))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    N.check(lib.la_compact_rows_split(first_t.data_ptr(), B, T, N.ptr(topo), table.tensor().data_ptr(), idx.data_ptr(),
+                                      row.data_ptr(), row2.data_ptr(), cnt.data_ptr(), tot.data_ptr(), tot2.data_ptr(),
+                                      ws.data_ptr(), wsb, N.stream_ptr(stream)), "la_compact_rows_split")
+    return idx, row, row2, cnt, tot, tot2
+
+
+def plan_row_split(plan) -> tuple[list[int], list[int]]:
+    """Joint order of the split row layout: (dyad targets ascending, other
+    joints ascending) -- the static joints and the crank tip are the others."""
+    targets = sorted(st.target for st in plan.steps)
+    tset = set(targets)
+    return targets, [j for j in range(plan.n) if j not in tset]
+
+
+def plan_targets(table: "PlanTable") -> list[tuple[int, list[int]]]:
+    """(n, ascending dyad targets) of every plan of a table, decoded from its
+    64-byte la_plan records."""
+    raw = table.host_bytes().reshape(-1, 64)
+    n = raw[:, 0:2].copy().view(np.int16)[:, 0]
+    ns = raw[:, 2:4].copy().view(np.int16)[:, 0]
+    return [(int(n[g]), sorted(int(raw[g, 8 + 3 * s]) for s in range(int(ns[g])))) for g in range(len(raw))]
+
+
+def assemble_paths(target_rows, first_row: int, pos0: np.ndarray, n: int, targets: list[int],
+                   T: int = 200) -> np.ndarray:
+    """Full (n, T, 2) fp32 paths of one candidate from its dyad-target rows
+    (split layout: ``targets`` ascending from ``first_row``) and its f64
+    pose: static joints stay at the pose (solver.py:183-184), the crank tip
+    is p0 + r1 (cos, sin) with r1 = np.hypot (solver.py:180, 185-187) -- the
+    f64 operations the device performs, rounded to fp32, so the rebuilt rows
+    equal the device's (tests/test_gpu_solver.py)."""
+    out = np.empty((n, T, 2), dtype=np.float32)
+    out[targets] = np.asarray(target_rows[first_row:first_row + len(targets)])
+    tset = set(targets)
+    th = 2.0 * np.pi * np.arange(T) / T
+    for j in range(n):
+        if j in tset:
+            continue
+        if j == 1:
+            p0 = pos0[0]
+            r1 = np.hypot(pos0[1, 0] - p0[0], pos0[1, 1] - p0[1])
+            out[1, :, 0] = (p0[0] + r1 * np.cos(th)).astype(np.float32)
+            out[1, :, 1] = (p0[1] + r1 * np.sin(th)).astype(np.float32)
+        else:
+            out[j] = pos0[j].astype(np.float32)
+    return out
+
+
 def simulate_deferred(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None,
                       fixup_tau: float = DEFAULT_FIXUP_TAU, stream=None, timer=None,
-                      dense_rows: bool = False) -> dict:
+                      dense_rows: bool = False, split_rows: bool = False, traj2=None) -> dict:
     """Two specialised launches, no host sync:
 
     1. fp32 screen (coarse-first, exact first lock for coarse-locked
@@ -351,9 +417,13 @@ def simulate_deferred(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=N
     item i starts at row ``pend_row[i]`` (running sum of the plans' joint
     counts, la_compact_rows) instead of ``i * stride``, so the first
     ``pend_rows`` (device scalar) rows of ``traj`` hold every real joint path
-    and no padding rows.
+    and no padding rows.  ``split_rows``: dense rows in two sets -- ``traj``
+    holds the dyad targets' rows (pending item i from ``pend_row[i]``, its
+    plan's nsteps rows in ascending joint order, ``pend_rows`` in all) and
+    ``traj2`` the static joints' and crank tip's rows (``pend_row2``,
+    ``pend_rows2``); see ``plan_row_split`` / ``assemble_paths``.
     """
-    stages, out = _deferred_stages(pos0, table, T, topo, traj, fixup_tau, stream, dense_rows)
+    stages, out = _deferred_stages(pos0, table, T, topo, traj, fixup_tau, stream, dense_rows, split_rows, traj2)
     for name, fn in stages:
         fn()
         if timer:
@@ -361,7 +431,8 @@ def simulate_deferred(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=N
     return out
 
 
-def _deferred_stages(pos0, table: PlanTable, T: int, topo, traj, fixup_tau: float, stream, dense_rows: bool):
+def _deferred_stages(pos0, table: PlanTable, T: int, topo, traj, fixup_tau: float, stream, dense_rows: bool,
+                     split_rows: bool = False, traj2=None):
     """simulate_deferred as three stage callables (screen; pending compaction
     + write pass; valid compaction) filling one result dict."""
     torch = N.require_cuda()
@@ -369,15 +440,23 @@ def _deferred_stages(pos0, table: PlanTable, T: int, topo, traj, fixup_tau: floa
     stride = table.max_n
     if traj is None:
         traj = torch.empty((max(B, 1) * stride, T, 2), dtype=torch.float32, device=pos0.device)
+    if split_rows and traj2 is None:
+        traj2 = torch.empty((max(B, 1) * stride, T, 2), dtype=torch.float32, device=pos0.device)
     out = {"traj": traj, "stride": stride}
+    if split_rows:
+        out["traj2"] = traj2
 
     def screen():
         out.update(simulate_tensors(pos0, table, T, topo, write_traj=False, fixup_tau=fixup_tau, stream=stream,
                                     _extra_flags=N.LA_SIM_DEFER))
 
     def paths():
-        prow = None
-        if dense_rows:
+        prow = prow2 = None
+        if split_rows:
+            pend, prow, prow2, pcnt, prows, prows2 = compact_rows_split(out["first_t"], N.LA_PENDING, table, topo,
+                                                                        stream=stream)
+            out.update(pend_row=prow, pend_rows=prows, pend_row2=prow2, pend_rows2=prows2)
+        elif dense_rows:
             pend, prow, pcnt, prows = compact_rows(out["first_t"], N.LA_PENDING, table, topo, stream=stream)
             out.update(pend_row=prow, pend_rows=prows)
         else:
@@ -386,7 +465,7 @@ def _deferred_stages(pos0, table: PlanTable, T: int, topo, traj, fixup_tau: floa
         simulate_tensors(pos0, table, T, topo, write_traj=True, traj=traj, traj_stride=stride, traj_row=prow,
                          cand=pend, cand_count=pcnt, fixup_tau=fixup_tau, stream=stream,
                          _extra_flags=N.LA_SIM_WRITE_ONLY | N.LA_SIM_SCATTER,
-                         _outputs=(out["first_t"], out["first_joint"]))
+                         _outputs=(out["first_t"], out["first_joint"]), traj2=traj2, traj_row2=prow2)
 
     def compact():
         vidx, vcnt = compact_valid(out["first_t"], T, stream=stream)
@@ -403,13 +482,15 @@ class DeferredGraph:
     shape; results in ``out``, same keys as simulate_deferred)."""
 
     def __init__(self, pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None,
-                 fixup_tau: float = DEFAULT_FIXUP_TAU, dense_rows: bool = True):
+                 fixup_tau: float = DEFAULT_FIXUP_TAU, dense_rows: bool = True, split_rows: bool = False,
+                 traj2=None):
         torch = N.require_cuda()
         if topo is not None:
             topo = topo.to(device=pos0.device, dtype=torch.int32).contiguous()
         crank_table(T, pos0.device)  # device constants cached before capture
         table.tensor()
-        stages, self.out = _deferred_stages(pos0, table, T, topo, traj, fixup_tau, None, dense_rows)
+        stages, self.out = _deferred_stages(pos0, table, T, topo, traj, fixup_tau, None, dense_rows, split_rows,
+                                            traj2)
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # warm-up outside capture
@@ -450,13 +531,20 @@ class HostPipeline:
     run): ``first_t`` / ``first_joint`` (B,), ``pend_idx`` (global candidate
     ids of the survivors, ascending), ``pend_row`` (each survivor's first
     row in ``traj``), ``traj`` (rows, T, 2) float32, and the byte counts of
-    the step's uploads and downloads.  Survivor i's joint j path is
-    ``traj[pend_row[i] + j]``; it is meaningful where
+    the step's uploads and downloads.  Rows are meaningful where
     ``first_t[pend_idx[i]] == T`` (the rest locked in the fine pass).
+
+    ``split_rows`` (default): the device writes every joint's path, but only
+    the dyad targets' rows cross PCIe -- survivor i's plan targets (ascending)
+    are ``traj[pend_row[i]:]``; its static joints and crank tip are
+    closed-form in the pose the host already holds (solver.py:180-187) and
+    ``paths(res, i)`` rebuilds its full (n, T, 2) array bit-identical to the
+    device rows.  Without it survivor i's joint j path is
+    ``traj[pend_row[i] + j]``.
     """
 
     def __init__(self, pos_h, table: PlanTable, T: int = 200, topo_h=None, *, chunks: int = 4,
-                 fixup_tau: float = DEFAULT_FIXUP_TAU):
+                 fixup_tau: float = DEFAULT_FIXUP_TAU, split_rows: bool = True):
         torch = N.require_cuda()
         if pos_h.is_cuda or pos_h.dtype != torch.float64 or pos_h.dim() != 3:
             raise ValueError("pos_h must be a (B, S, 2) float64 host tensor")
@@ -478,10 +566,13 @@ class HostPipeline:
         self.pos_d.copy_(pos_h)
         self.topo_d.copy_(topo_h)
         self.graphs = []
+        self.split = bool(split_rows)
         for lo, hi in self.ranges:
             traj = torch.empty(((hi - lo) * stride, T, 2), dtype=torch.float32, device="cuda")
+            traj2 = torch.empty(((hi - lo) * stride, T, 2), dtype=torch.float32, device="cuda") if self.split else None
             self.graphs.append(DeferredGraph(self.pos_d[lo:hi], table, T, self.topo_d[lo:hi], traj=traj,
-                                             fixup_tau=fixup_tau))
+                                             fixup_tau=fixup_tau, split_rows=self.split, traj2=traj2))
+        self._targets = plan_targets(table) if self.split else None
         nc = len(self.ranges)
         self.cnt_d = torch.empty((nc, 2), dtype=torch.int64, device="cuda")
         self.cnt_h = torch.empty((nc, 2), dtype=torch.int64).pin_memory()
@@ -539,9 +630,23 @@ class HostPipeline:
         comp.wait_stream(self.down)
         B = self.pos_h.shape[0]
         return {"first_t": self.ft_h, "first_joint": self.fj_h, "pend_idx": self.idx_h[:npend],
-                "pend_row": self.row_h[:npend], "traj": self.traj_h[:nrow],
+                "pend_row": self.row_h[:npend], "traj": self.traj_h[:nrow], "split_rows": self.split,
                 "h2d_bytes": self.pos_h.numel() * 8 + self.topo_h.numel() * 4,
                 "d2h_bytes": B * 8 + len(self.ranges) * 16 + nrow * self.T * 8 + npend * 16}
+
+    def paths(self, res: dict, i: int) -> np.ndarray:
+        """Full (n, T, 2) fp32 paths of survivor i of a ``run()`` result."""
+        b = int(res["pend_idx"][i])
+        g = int(self.topo_h[b])
+        row = int(res["pend_row"][i])
+        if not self.split:
+            n = self._n_of(g)
+            return res["traj"][row:row + n].numpy()
+        n, targets = self._targets[g]
+        return assemble_paths(res["traj"], row, self.pos_h[b].numpy(), n, targets, self.T)
+
+    def _n_of(self, g: int) -> int:
+        return int(self.table.host_bytes().reshape(-1, 64)[g, 0:2].copy().view(np.int16)[0])
 
 
 def simulate_compact(pos0, table: PlanTable, T: int = 200, topo=None, *, traj=None, traj_f64: bool = False,

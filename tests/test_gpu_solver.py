@@ -559,8 +559,11 @@ def test_screen_flags_at_scale_vs_exact(torch, seed):
 def test_host_pipeline_matches_deferred(torch):
     """HostPipeline (chunked host-to-host pipeline, overlapped copies) returns
     the same flags, survivor ids and per-survivor paths as one
-    DeferredGraph over the whole batch, for 1 and 3 chunks, and a second
-    run over new host poses recomputes everything."""
+    DeferredGraph over the whole batch, for 1 and 3 chunks, with and without
+    split rows (only dyad-target rows cross PCIe; HostPipeline.paths
+    rebuilds the static joints and the crank tip bit-identical to the
+    device's rows), and a second run over new host poses recomputes
+    everything."""
     from paper_2208_14567_b200.solver import HostPipeline, simulate_deferred
     from paper_2208_14567_b200.workloads import mixed_batch
 
@@ -568,8 +571,9 @@ def test_host_pipeline_matches_deferred(torch):
     table = mb.table()
     pos_h = torch.from_numpy(mb.pos.copy())
     topo_h = torch.from_numpy(mb.topo)
-    for chunks in (1, 3):
-        pipe = HostPipeline(pos_h, table, 200, topo_h, chunks=chunks)
+    nsteps = np.array([len(p.steps) for p in mb.plans])[mb.topo]
+    for chunks, split in ((1, True), (3, True), (3, False)):
+        pipe = HostPipeline(pos_h, table, 200, topo_h, chunks=chunks, split_rows=split)
         for shift in (0.0, 0.01):
             pipe.pos_h.copy_(torch.from_numpy(mb.pos + shift))
             res = pipe.run()
@@ -579,11 +583,46 @@ def test_host_pipeline_matches_deferred(torch):
             np_ = int(ref["pend_count"].item())
             assert torch.equal(res["pend_idx"], ref["pend_idx"][:np_].cpu())
             rr = ref["pend_row"][:np_].cpu().numpy()
-            hr = res["pend_row"].numpy()
             nn = mb.n[res["pend_idx"].numpy()]
-            assert res["traj"].shape[0] == int(nn.sum()) == int(ref["pend_rows"].item())
-            assert res["d2h_bytes"] == 4000 * 8 + len(pipe.ranges) * 16 + int(nn.sum()) * 200 * 8 + np_ * 16
-            rt = ref["traj"].cpu()
+            shipped = nsteps[res["pend_idx"].numpy()] if split else nn
+            assert res["traj"].shape[0] == int(shipped.sum())
+            assert res["d2h_bytes"] == 4000 * 8 + len(pipe.ranges) * 16 + int(shipped.sum()) * 200 * 8 + np_ * 16
+            rt = ref["traj"].cpu().numpy()
             ok = (res["first_t"][res["pend_idx"]] == 200).numpy()  # rows of fine-pass locks are scratch
             for i in np.flatnonzero(ok)[::max(1, np_ // 300)]:
-                assert torch.equal(res["traj"][hr[i]:hr[i] + nn[i]], rt[rr[i]:rr[i] + nn[i]])
+                assert np.array_equal(pipe.paths(res, int(i)), rt[rr[i]:rr[i] + nn[i]]), (chunks, split, i)
+
+
+def test_split_rows_layout(torch):
+    """simulate_deferred(split_rows=True): the dyad-target rows (traj) and the
+    static + crank rows (traj2) of every valid survivor are the dense
+    layout's rows, and assemble_paths' host rebuild of the static + crank
+    rows is bit-identical to traj2 (numpy's crank arithmetic, np.hypot)."""
+    from paper_2208_14567_b200.solver import assemble_paths, plan_row_split, simulate_deferred
+    from paper_2208_14567_b200.workloads import mixed_batch
+
+    mb = mixed_batch(6000, 5, 9, seed=41, stride=9)
+    table = mb.table()
+    pos, topo = torch.from_numpy(mb.pos).cuda(), torch.from_numpy(mb.topo).cuda()
+    dense = simulate_deferred(pos, table, 200, topo, dense_rows=True)
+    split = simulate_deferred(pos, table, 200, topo, split_rows=True)
+    assert torch.equal(dense["first_t"], split["first_t"])
+    np_ = int(dense["pend_count"].item())
+    assert torch.equal(dense["pend_idx"][:np_], split["pend_idx"][:np_])
+    idx = dense["pend_idx"][:np_].cpu().numpy()
+    ft = dense["first_t"].cpu().numpy()
+    dr, tr, orow = (dense["pend_row"][:np_].cpu().numpy(), split["pend_row"][:np_].cpu().numpy(),
+                    split["pend_row2"][:np_].cpu().numpy())
+    D, A, O2 = dense["traj"].cpu().numpy(), split["traj"].cpu().numpy(), split["traj2"].cpu().numpy()
+    checked = 0
+    for i, b in enumerate(idx):
+        if ft[b] != 200:
+            continue
+        plan = mb.plans[mb.topo[b]]
+        targets, others = plan_row_split(plan)
+        full = D[dr[i]:dr[i] + plan.n]
+        assert np.array_equal(A[tr[i]:tr[i] + len(targets)], full[targets])
+        assert np.array_equal(O2[orow[i]:orow[i] + len(others)], full[others])
+        assert np.array_equal(assemble_paths(A, int(tr[i]), mb.pos[b, :plan.n], plan.n, targets, 200), full)
+        checked += 1
+    assert checked > 500
