@@ -88,6 +88,7 @@ struct Warp {
   unsigned char* cols;   // pos block: slot (joint j, lane) at (j * 32 + lane) * slot bytes
   int lane;
   int slot;              // 8 (fp32 x, y) or 16 (fp32 x, y, e, - / f64 x, y)
+  int ecol_off;          // 8-byte slots: byte offset of the fp16 error array [joint][lane]
   __device__ __forceinline__ float2& p32(int j) const {
     return *reinterpret_cast<float2*>(cols + (size_t)(j * 32 + lane) * slot);
   }
@@ -185,12 +186,10 @@ __device__ __noinline__ int replay_f64_local(const Warp& W, const SimCtx& C, dou
     q[j] = H.p0[j];
   }
   q[1] = crank_tip(H, C, ct, st);
-  W.p32(1) = make_float2((float)q[1].x, (float)q[1].y);
+  // only the lock decision leaves the replay: the next angle recomputes
+  // every moving joint, so nothing is written back to the fp32 columns
   auto get = [&](int j) { return q[j]; };
-  auto put = [&](int j, double2 v) {
-    q[j] = v;
-    W.p32(j) = make_float2((float)v.x, (float)v.y);
-  };
+  auto put = [&](int j, double2 v) { q[j] = v; };
   if (EXACT) {
     double margin = INFINITY;
     const int lk = dyads_f64<false>(H, C, get, put, &margin);
@@ -265,13 +264,10 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
                make_float4(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)), e, 0.f));
       }
     } else {
-      // 8-byte slots (large mechanisms: keeps occupancy): one running bound
-      // for "clean" joints and one for joints downstream of an amplifying
-      // dyad, a bitmask (parents' bits precomputed per step) separating them
-      float err = kErr0;
-      float err_t = 0.0f;
-      unsigned taint = 0u;
-      const int tsh = W.slot == 16 ? 9 : 8;  // byte offset of a joint's slot -> joint index
+      // large mechanisms (8-byte slots keep three CTAs per SM): the same
+      // per-joint bound, stored as fp16 (scaled by kErrScale, rounded up) in
+      // a [joint][lane] array after the position columns
+      const uint32_t ecol = smem_u32(W.cols) + (uint32_t)W.ecol_off + (uint32_t)W.lane * 2u;
 #pragma unroll 1
       for (; s < C.ns; ++s) {
         const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
@@ -283,8 +279,7 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
         const float inv = rsqrt_approx(d2);
         const float d = d2 * inv;
         const float m = fminf(g0.x - d, d - g0.y);
-        const bool tp = (taint & g1.x) != 0u;
-        const float ep = tp ? fmaxf(err_t, err) : err;
+        const float ep = fmaxf(lds_h16(ecol + (g1.y >> 2)), lds_h16(ecol + (g1.z >> 2))) * kErrScaleInv;
         fix |= !(fabsf(m) >= fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
         if (m < 0.0f) {
           lk = s;
@@ -294,15 +289,11 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
         const float h = sqrt_approx(fmaxf(fmaf(-x, x, fabsf(g0.w)), 0.0f));
         const float ax = fabsf(x);
         const float num = ax * fmaf(ax, inv, 1.0f);
-        // amplifying dyad (kappa = num / h > 1) or tainted parent: branch-free
-        const bool amp = tp || num > h;
-        const float et = fmaxf(err_t, fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep));
-        err_t = amp ? et : err_t;
-        taint |= amp ? 1u << (g1.w >> tsh) : 0u;
-        err = amp ? err : err + kErrStep;
+        const float e = fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep);
         const float xi = x * inv;
         const float hb = copysignf(h, g0.w) * inv;
         sts_f2(col + g1.w, make_float2(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y))));
+        sts_h16(ecol + (g1.w >> 2), e * kErrScale);
       }
     }
   if (COUNT) {
@@ -349,11 +340,14 @@ __device__ __forceinline__ void fill_static32(const Warp& W) {
     }
     slot[32] = make_float4(0.f, 0.f, kErr0, 0.f);  // crank tip: error of its inputs
   } else {
+    const uint32_t ecol = smem_u32(W.cols) + (uint32_t)W.ecol_off + (uint32_t)W.lane * 2u;
 #pragma unroll 1
     for (int k = 0; k < H.nstatic; ++k) {
       const int j = H.statics[k];
       W.p32(j) = make_float2((float)H.p0[j].x, (float)H.p0[j].y);
+      sts_h16(ecol + 64u * j, kErr0 * kErrScale);
     }
+    sts_h16(ecol + 64u, kErr0 * kErrScale);  // crank tip
   }
 }
 
@@ -387,6 +381,12 @@ template <bool WRITE, bool SCREEN64, bool ERR4>
 __host__ __device__ constexpr size_t col_bytes() {
   return (WRITE || SCREEN64 || ERR4) ? 16 : 8;
 }
+// per (joint, lane) bytes of the column block: slots + the fp16 error array
+// of 8-byte-slot screens
+template <bool WRITE, bool SCREEN64, bool ERR4>
+__host__ __device__ constexpr size_t col_block_bytes() {
+  return col_bytes<WRITE, SCREEN64, ERR4>() == 8 ? 10 : 16;
+}
 
 template <bool WRITE, bool SCREEN64, bool WONLY, bool EXACT, bool COUNT, bool ERR4>
 __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_sim_args p, int njmax) {
@@ -401,12 +401,14 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
     cs32[t] = make_float2((float)p.crank_cs[2 * t], (float)p.crank_cs[2 * t + 1]);
   __syncthreads();
   constexpr uint32_t SLOT = (uint32_t)col_bytes<WRITE, SCREEN64, ERR4>();
-  const size_t per_warp = sizeof(WarpHead) + (size_t)njmax * 32 * SLOT;
+  const size_t per_warp = (sizeof(WarpHead) + (size_t)njmax * 32 * col_block_bytes<WRITE, SCREEN64, ERR4>() + 15) &
+                          ~(size_t)15;
   Warp W;
   W.h = reinterpret_cast<WarpHead*>(sim_smem_raw + cs_bytes + per_warp * w);
   W.cols = sim_smem_raw + cs_bytes + per_warp * w + sizeof(WarpHead);
   W.lane = lane;
   W.slot = (int)SLOT;
+  W.ecol_off = njmax * 32 * (int)SLOT;
   WarpHead& H = *W.h;
   const long long nwarps = (long long)gridDim.x * SIM_WARPS;
   const bool coarse = !WONLY && !(p.flags & LA_SIM_NO_COARSE) && (T % 4 == 0) && T >= 8;
@@ -496,10 +498,16 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
       H.st[lane] = r;
     }
     {
-      // crank radius as np.hypot in every mode (solver.py:180): with the
-      // host's crank table the crank tip row is then rebuilt bit for bit
+      // crank radius as np.hypot wherever paths are written or f64 is exact
+      // (solver.py:180): with the host's crank table the crank tip row is
+      // then rebuilt bit for bit; fp32 screens take a Newton-refined root
       const double dx = dsub(H.p0[1].x, H.p0[0].x), dy = dsub(H.p0[1].y, H.p0[0].y);
-      C.r1 = np_hypot(dx, dy);
+      if (EXACT || WRITE) {
+        C.r1 = np_hypot(dx, dy);
+      } else {
+        const double r2 = dadd(dmul(dx, dx), dmul(dy, dy));
+        C.r1 = r2 > 0.0 ? dmul(r2, rsqrt_f64(r2)) : 0.0;
+      }
       C.r1f = (float)C.r1;
       C.p0f = make_float2((float)H.p0[0].x, (float)H.p0[0].y);
     }
@@ -965,10 +973,12 @@ int la_simulate(const la_sim_args* a, void* stream) {
   // 16-byte slots; from 13 joints on the 8-byte taint-model slots keep three
   // CTAs per SM resident (measured C3, 20 joints: 19.4 vs 21.8 ms)
   const bool err4 = njmax <= 12;
-  const size_t colb = (write || f64 || err4) ? 16 : 8;
+  const size_t colb = (write || f64 || err4) ? 16 : 10;  // 8-byte slots + fp16 error
+  static_assert(col_block_bytes<false, false, false>() == 10 && col_block_bytes<true, false, true>() == 16,
+                "launch and kernel column layouts");
   if ((a->flags & LA_SIM_SCATTER) && !a->cand) return fail(LA_EINVAL, "la_simulate: SCATTER needs cand");
   const size_t cs_bytes = ((size_t)a->T * sizeof(float2) + 15) & ~(size_t)15;
-  const size_t smem = cs_bytes + (sizeof(WarpHead) + (size_t)njmax * 32 * colb) * SIM_WARPS;
+  const size_t smem = cs_bytes + ((sizeof(WarpHead) + (size_t)njmax * 32 * colb + 15) & ~(size_t)15) * SIM_WARPS;
   const bool wonly = (a->flags & LA_SIM_WRITE_ONLY) != 0;
   if (wonly && !write) return fail(LA_EINVAL, "la_simulate: WRITE_ONLY needs WRITE_TRAJ");
   const bool exact = (a->flags & LA_SIM_EXACT64) != 0;
@@ -980,12 +990,12 @@ int la_simulate(const la_sim_args* a, void* stream) {
     if (exact) {
       if (wonly) return sim_kernel<true, false, true, true, C, false>;
       if (f64) return write ? sim_kernel<true, true, false, true, C, false> : sim_kernel<false, true, false, true, C, false>;
-      if (write) return err4 ? sim_kernel<true, false, false, true, C, true> : sim_kernel<true, false, false, true, C, false>;
+      if (write) return sim_kernel<true, false, false, true, C, true>;  // 16-byte slots: room for e
       return err4 ? sim_kernel<false, false, false, true, C, true> : sim_kernel<false, false, false, true, C, false>;
     }
     if (wonly) return sim_kernel<true, false, true, false, C, false>;
     if (f64) return write ? sim_kernel<true, true, false, false, C, false> : sim_kernel<false, true, false, false, C, false>;
-    if (write) return err4 ? sim_kernel<true, false, false, false, C, true> : sim_kernel<true, false, false, false, C, false>;
+    if (write) return sim_kernel<true, false, false, false, C, true>;
     return err4 ? sim_kernel<false, false, false, false, C, true> : sim_kernel<false, false, false, false, C, false>;
   };
   const KernT kern = a->counters ? pick(std::true_type{}) : pick(std::false_type{});

@@ -2,6 +2,7 @@
 // replay and path writes; screen.cu: lane-per-candidate validity screen).
 #pragma once
 #include "common.cuh"
+#include <cuda_fp16.h>
 
 namespace la {
 
@@ -53,6 +54,19 @@ __device__ __forceinline__ float rcp_approx(float x) {
 constexpr float kErr0 = 2e-7f;
 constexpr float kErrStep = 5e-7f;
 constexpr float kMarginK = 3.0f;
+// fp16 storage of error bounds (8-byte-slot screens): e * 2^12 keeps kErr0
+// a normal half; rounded up on store so a stored bound never shrinks
+constexpr float kErrScale = 4096.0f;
+constexpr float kErrScaleInv = 1.0f / 4096.0f;
+__device__ __forceinline__ float lds_h16(uint32_t a) {
+  unsigned short h;
+  asm("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a) : "memory");
+  return __half2float(__ushort_as_half(h));
+}
+__device__ __forceinline__ void sts_h16(uint32_t a, float v) {
+  const unsigned short h = __half_as_ushort(__float2half_ru(v));
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(h) : "memory");
+}
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
