@@ -466,7 +466,9 @@ __device__ __noinline__ float direct_chamfer(const float2* __restrict__ qsrc, in
 // prune (strict >).
 constexpr int LBG = 64;             // grid cells per axis
 constexpr int LBV = LBG + 1;        // vertices per axis
-constexpr size_t LB_DT_BYTES = ((size_t)LBV * LBV * sizeof(__half) + 15) & ~(size_t)15;
+constexpr size_t LB_VTX_BYTES = ((size_t)LBV * LBV * sizeof(__half) + 15) & ~(size_t)15;
+// per query: the vertex table (LBV x LBV) then the cell table (LBG x LBG)
+constexpr size_t LB_DT_BYTES = LB_VTX_BYTES + (size_t)LBG * LBG * sizeof(__half);
 constexpr long long PRUNE_MIN_POS = 1 << 16;  // smaller scans: no seed launches
 
 // grid over the query's bounding box joined with the unit square (the
@@ -506,7 +508,16 @@ __global__ void __launch_bounds__(256) lb_grid_kernel(const float* __restrict__ 
   const bool live = v < LBV * LBV;
   const int ix = live ? v / LBV : 0, iy = live ? v % LBV : 0;
   const float vx = __fmaf_rn((float)ix, cx, lx), vy = __fmaf_rn((float)iy, cy, ly);
-  float m = INFINITY;
+  // cell table: distance from the query to cell c's box, the border cells
+  // open toward infinity (points outside the grid clamp into them) and
+  // interior edges widened by 1e-6 (rounding of the scan's cell index)
+  const bool lc = v < LBG * LBG;
+  const int cxi = lc ? v / LBG : 0, cyi = lc ? v % LBG : 0;
+  const float bx0 = cxi == 0 ? -INFINITY : __fmaf_rn((float)cxi, cx, lx) - 1e-6f;
+  const float bx1 = cxi == LBG - 1 ? INFINITY : __fmaf_rn((float)(cxi + 1), cx, lx) + 1e-6f;
+  const float by0 = cyi == 0 ? -INFINITY : __fmaf_rn((float)cyi, cy, ly) - 1e-6f;
+  const float by1 = cyi == LBG - 1 ? INFINITY : __fmaf_rn((float)(cyi + 1), cy, ly) + 1e-6f;
+  float m = INFINITY, mc = INFINITY;
   for (int b = 0; b < Q; b += 256) {
     __syncthreads();
     if (b + threadIdx.x < Q) sq[threadIdx.x] = q[b + threadIdx.x];
@@ -515,9 +526,13 @@ __global__ void __launch_bounds__(256) lb_grid_kernel(const float* __restrict__ 
     for (int j = 0; j < e; ++j) {
       const float dx = vx - sq[j].x, dy = vy - sq[j].y;
       m = fminf(m, __fmaf_rn(dy, dy, dx * dx));
+      const float ex = fmaxf(fmaxf(bx0 - sq[j].x, sq[j].x - bx1), 0.f);
+      const float ey = fmaxf(fmaxf(by0 - sq[j].y, sq[j].y - by1), 0.f);
+      mc = fminf(mc, __fmaf_rn(ey, ey, ex * ex));
     }
   }
   if (live) out[v] = __float2half_rd(fmaxf(sqrtf(m) * (1.f - 1e-6f) - 1e-6f, 0.f));
+  if (lc) out[LB_VTX_BYTES / sizeof(__half) + v] = __float2half_rd(fmaxf(sqrtf(mc) * (1.f - 1e-6f) - 1e-6f, 0.f));
 }
 
 // k-th best of the seed scan's merged list -> thr (inf when fewer than k)
@@ -577,6 +592,48 @@ __device__ __forceinline__ float curve_row_bound_near(const float2* __restrict__
   const int P1 = min(P, 128);
   float s = 0.f;
   for (int i = lane; i < P1; i += 32) s += point(i);
+  const float s1 = warp_sum(s) / (float)P;
+  if (s1 > early || P1 == P) return s1;
+  s = 0.f;
+  for (int i = P1 + lane; i < P; i += 32) s += point(i);
+  return s1 + warp_sum(s) / (float)P;
+}
+
+// cheapest first stage: every point a lies in (or clamps into) grid cell
+// c(a), and min_q |a - q| >= CT(c) = distance from the query to c's box
+// (lb_grid_kernel's cell table): one table load per point, no square root.
+// cur_s / ct_s: shared-space addresses of the curve and the cell table.
+__device__ __forceinline__ float lds_halfp(uint32_t a) {
+  unsigned short h;
+  asm("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
+  return __half2float(__ushort_as_half(h));
+}
+__device__ __forceinline__ float2 lds_f2p(uint32_t a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float curve_row_bound_cell(uint32_t cur_s, int P, uint32_t ct_s, float lx, float ly,
+                                                      float ihx, float ihy, int lane, float early) {
+  const float ox = -lx * ihx, oy = -ly * ihy;
+  auto point = [&](int i) {
+    const float2 a = lds_f2p(cur_s + 8u * (uint32_t)i);
+    const unsigned ix = min(__float2uint_rd(fmaf(a.x, ihx, ox)), (unsigned)(LBG - 1));
+    const unsigned iy = min(__float2uint_rd(fmaf(a.y, ihy, oy)), (unsigned)(LBG - 1));
+    return lds_halfp(ct_s + 2u * (ix * LBG + iy));
+  };
+  float s = 0.f;
+  int P1;
+  if (P >= 128) {
+    // the first 128 points, four per lane, independent loads
+    P1 = 128;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s += point(lane + 32 * u);
+  } else {
+    P1 = P;
+    for (int i = lane; i < P; i += 32) s += point(i);
+  }
+  // the terms are >= 0: a partial sum is already a (weaker) bound
   const float s1 = warp_sum(s) / (float)P;
   if (s1 > early || P1 == P) return s1;
   s = 0.f;
@@ -718,6 +775,8 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
     tma_load_1d(&raw[w][0][0], A.db + (size_t)id * P * 2, bytes, &bars[w][0]);
   }
   uint32_t phase = 0;
+  float thr_c = prune ? __uint_as_float(__ldcg(thr_q)) : INFINITY;
+  const uint32_t lbc_s = smem_u32(lb_dt) + (uint32_t)LB_VTX_BYTES;  // cell table
 
   for (long long it = 0; it < count; ++it) {
     const int bi = (int)(it & 1);
@@ -743,9 +802,13 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
     }
     if (id == A.exclude_id) continue;
     if (prune) {
-      // two bounds of increasing cost; d > lba: neither a hit nor in the top k
-      const float t = fmaxf(__uint_as_float(__shfl_sync(FULL, __ldcg(thr_q), 0)), A.threshold);
-      const float lb1 = curve_row_bound_near(cur, P, lb_dt, lb_lx, lb_ly, lb_ihx, lb_ihy, lb_cx, lb_cy, lane,
+      // bounds of increasing cost; d > lb: neither a hit nor in the top k.
+      // thr as loaded one curve earlier (the load's latency hides behind
+      // this curve; an older, larger value still bounds the final k-th best
+      // from above)
+      const float t = fmaxf(thr_c, A.threshold);
+      thr_c = __uint_as_float(__ldcg(thr_q));
+      const float lb1 = curve_row_bound_cell(smem_u32(cur), P, lbc_s, lb_lx, lb_ly, lb_ihx, lb_ihy, lane,
                                              (t + lb_slack) * (1.f + 2e-4f));
       if (fmaf(lb1, 1.f - 1e-4f, -lb_slack) > t) continue;
       const float lb4 = curve_row_bound(cur, P, lb_dt, lb_lx, lb_ly, lb_ihx, lb_ihy, lb_cx, lb_cy, lane);
