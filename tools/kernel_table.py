@@ -23,6 +23,12 @@ pos = torch.from_numpy(mb.pos).cuda()
 topo = torch.from_numpy(mb.topo).cuda()
 table = mb.table()
 res = simulate_deferred(pos, table, 200, topo)                         # screen, compaction x2, write-only
+simulate_deferred(pos, table, 200, topo, split_rows=True)              # split-row compaction + split write
+simulate_tensors(pos, table, 200, topo, write_traj=False, _extra_flags=N.LA_SIM_LANE_SCREEN)  # lane screen
+from paper_2208_14567_b200.workloads import native_batch  # noqa: E402
+nb = native_batch(200_000, 5, 20, seed=3000)
+simulate_tensors(torch.from_numpy(nb.pos).cuda(), nb.table, 200, torch.from_numpy(nb.topo).cuda(),
+                 write_traj=False, gate_only=True, low=True)           # 20-joint screen (fp16 error slots)
 simulate_tensors(pos, table, 200, topo, write_traj=True, traj_f64=True, traj_stride=8)  # exact f64 writes
 mech = four_bar()
 plan = bare_plan(mech)
@@ -36,7 +42,12 @@ circle_stats(n64["out"])                                               # circle_
 db = fourier_db(1_000_000, 200, seed=4000)
 q = fourier_db(64, 200, seed=999)
 chamfer_scan(db, q[:1], k=10)                                          # chamfer scan + select/merge
-chamfer_scan(db[:200_000], q, k=10)                                    # 64 queries
+chamfer_scan(db[:200_000], q, k=10)                                    # 64 queries: multi-query kernel
+chamfer_scan(db[:200_000], q, k=10, multi_query=False)                 # 64 queries, one CTA set each
+from paper_2208_14567_b200.dist import merge_gathered, pack_lists  # noqa: E402
+parts = [chamfer_scan(db[i * 100_000:(i + 1) * 100_000], q[:8], k=10, id_base=i * 100_000,
+                      pos_base=i * 100_000) for i in range(2)]
+merge_gathered(torch.stack([pack_lists(p_, 10) for p_ in parts]), 10)  # shard_merge_kernel
 desc = coarse_descriptors(raw64)                                       # descriptor_kernel
 big = desc.repeat(50, 1)
 coarse_select(big, desc[3], big.shape[0] // 100, torch.randperm(big.shape[0], device="cuda"))
