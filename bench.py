@@ -1200,11 +1200,17 @@ def bench_c5(torch, args, rank, world, peaks, flush, clk, want_cpu=False, c4_pai
         cpu = cpu_c5(sub, last, ncurves, c4_pair_rate)
     ch_ms = stages["chamfer"]
     db_bytes = ncurves * T * 8
-    rl_ch = {"kernel": "chamfer_scan_kernel (64 queries, pruned)", "bound": "hbm",
+    trm = load_traffic().get("chamfer_mq_c5", {})
+    nst = last["cres"]["n_stage"].tolist()
+    rl_ch = {"kernel": "chamfer_mq_kernel (64 queries, multi-query pruned scan)", "bound": "hbm",
              "achieved": db_bytes / (ch_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
              "frac": db_bytes / (ch_ms / 1e3) / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes": db_bytes,
-             "traffic": None, "curves_evaluated_in_full": int(last["cres"]["n_full"].sum().item()),
-             "note": "algorithmic bytes = the curve set read once for all 64 queries"}
+             "traffic": trm.get("per_launch_bytes"), "traffic_source": "profiles/traffic.json" if trm else None,
+             "curves_evaluated_in_full": int(last["cres"]["n_full"].sum().item()),
+             "pairs_surviving_bound_stages": nst,
+             "note": "algorithmic bytes = the curve set read once for all 64 queries; the kernel is bound by the "
+                     "issue of its lower-bound stages, not by HBM (profiles/r02_ncu_c5.txt: 41 % issue slots busy, "
+                     "IPC 1.65, one 8-warp CTA per SM at 254 registers)"}
     rl_norm = {"kernel": "normalize_warp_kernel (fp32)", "bound": "fp32",
                "achieved": norm_flops / (stages["normalize"] / 1e3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
                "frac": norm_flops / (stages["normalize"] / 1e3) / 1e12 / fp32_peak, "algorithmic_flops": norm_flops,
