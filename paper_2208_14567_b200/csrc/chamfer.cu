@@ -70,6 +70,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// the same on precomputed shared-space addresses (hot loops)
+__device__ __forceinline__ void mbar_expect_tx_s(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d_s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
 __device__ __forceinline__ float min3f(float a, float b, float c) { return fminf(fminf(a, b), c); }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -469,6 +488,7 @@ constexpr int LBV = LBG + 1;        // vertices per axis
 constexpr size_t LB_VTX_BYTES = ((size_t)LBV * LBV * sizeof(__half) + 15) & ~(size_t)15;
 // per query: the vertex table (LBV x LBV) then the cell table (LBG x LBG)
 constexpr size_t LB_DT_BYTES = LB_VTX_BYTES + (size_t)LBG * LBG * sizeof(__half);
+constexpr float LB_CELL_ONE = 16384.f;  // cell table fixed point: units of 2^-14
 constexpr long long PRUNE_MIN_POS = 1 << 16;  // smaller scans: no seed launches
 
 // grid over the query's bounding box joined with the unit square (the
@@ -532,7 +552,13 @@ __global__ void __launch_bounds__(256) lb_grid_kernel(const float* __restrict__ 
     }
   }
   if (live) out[v] = __float2half_rd(fmaxf(sqrtf(m) * (1.f - 1e-6f) - 1e-6f, 0.f));
-  if (lc) out[LB_VTX_BYTES / sizeof(__half) + v] = __float2half_rd(fmaxf(sqrtf(mc) * (1.f - 1e-6f) - 1e-6f, 0.f));
+  // cell table in fixed point, floor(d * 2^14) (6.1e-5 resolution, finer
+  // than fp16 above 0.125; integer sums of <= 256 terms fit 32 bits)
+  if (lc) {
+    const float dc = fmaxf(sqrtf(mc) * (1.f - 1e-6f) - 1e-6f, 0.f);
+    reinterpret_cast<unsigned short*>(out + LB_VTX_BYTES / sizeof(__half))[v] =
+        (unsigned short)min(__float2uint_rd(dc * (float)LB_CELL_ONE), 65535u);
+  }
 }
 
 // k-th best of the seed scan's merged list -> thr (inf when fewer than k)
@@ -571,58 +597,33 @@ __device__ __forceinline__ void publish_kth(unsigned* __restrict__ thr, unsigned
   if (lane == 0 && kth < __float_as_uint(INFINITY)) atomicMin(thr, kth);
 }
 
-// cheaper first stage: nearest vertex only (one square root per point);
-// same vertex coordinates as lb_grid_kernel (fmaf of an integral float)
-__device__ __forceinline__ float curve_row_bound_near(const float2* __restrict__ cur, int P,
-                                                      const __half* __restrict__ dt, float lx, float ly, float ihx,
-                                                      float ihy, float cx, float cy, int lane, float early) {
-  // any vertex gives a valid bound, so the cell choice may round freely:
-  // saturating conversions (negative / NaN -> 0) and one clamp per axis
-  const float ox = -lx * ihx, oy = -ly * ihy;
-  auto point = [&](int i) {
-    const float2 a = cur[i];
-    const unsigned ix = min(__float2uint_rn(fmaf(a.x, ihx, ox)), (unsigned)LBG);
-    const unsigned iy = min(__float2uint_rn(fmaf(a.y, ihy, oy)), (unsigned)LBG);
-    const float ex = a.x - __fmaf_rn((float)ix, cx, lx), ey = a.y - __fmaf_rn((float)iy, cy, ly);
-    const float L = __half2float(dt[ix * LBV + iy]) - sqrt_approx(fmaf(ey, ey, ex * ex));
-    return fmaxf(L, 0.f);
-  };
-  // the terms are >= 0: a partial sum over the first 128 points is already
-  // a (weaker) bound, enough to prune most curves at ~60 % of the cost
-  const int P1 = min(P, 128);
-  float s = 0.f;
-  for (int i = lane; i < P1; i += 32) s += point(i);
-  const float s1 = warp_sum(s) / (float)P;
-  if (s1 > early || P1 == P) return s1;
-  s = 0.f;
-  for (int i = P1 + lane; i < P; i += 32) s += point(i);
-  return s1 + warp_sum(s) / (float)P;
-}
-
 // cheapest first stage: every point a lies in (or clamps into) grid cell
 // c(a), and min_q |a - q| >= CT(c) = distance from the query to c's box
 // (lb_grid_kernel's cell table): one table load per point, no square root.
 // cur_s / ct_s: shared-space addresses of the curve and the cell table.
-__device__ __forceinline__ float lds_halfp(uint32_t a) {
-  unsigned short h;
-  asm("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
-  return __half2float(__ushort_as_half(h));
-}
 __device__ __forceinline__ float2 lds_f2p(uint32_t a) {
   float2 v;
   asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
   return v;
 }
+__device__ __forceinline__ unsigned lds_u16p(uint32_t a) {
+  unsigned short h;
+  asm("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
+  return h;
+}
 __device__ __forceinline__ float curve_row_bound_cell(uint32_t cur_s, int P, uint32_t ct_s, float lx, float ly,
                                                       float ihx, float ihy, int lane, float early) {
   const float ox = -lx * ihx, oy = -ly * ihy;
-  auto point = [&](int i) {
+  // fixed-point table entries (floors) summed as integers: the sum is itself
+  // a floor, and the warp total is one REDUX
+  auto point = [&](int i) -> unsigned {
     const float2 a = lds_f2p(cur_s + 8u * (uint32_t)i);
     const unsigned ix = min(__float2uint_rd(fmaf(a.x, ihx, ox)), (unsigned)(LBG - 1));
     const unsigned iy = min(__float2uint_rd(fmaf(a.y, ihy, oy)), (unsigned)(LBG - 1));
-    return lds_halfp(ct_s + 2u * (ix * LBG + iy));
+    return lds_u16p(ct_s + 2u * (ix * LBG + iy));
   };
-  float s = 0.f;
+  const float scale = 1.f / (LB_CELL_ONE * (float)P);
+  unsigned s = 0u;
   int P1;
   if (P >= 128) {
     // the first 128 points, four per lane, independent loads
@@ -634,11 +635,12 @@ __device__ __forceinline__ float curve_row_bound_cell(uint32_t cur_s, int P, uin
     for (int i = lane; i < P; i += 32) s += point(i);
   }
   // the terms are >= 0: a partial sum is already a (weaker) bound
-  const float s1 = warp_sum(s) / (float)P;
+  const unsigned t1 = __reduce_add_sync(FULL, s);
+  const float s1 = (float)t1 * scale;
   if (s1 > early || P1 == P) return s1;
-  s = 0.f;
+  s = 0u;
   for (int i = P1 + lane; i < P; i += 32) s += point(i);
-  return s1 + warp_sum(s) / (float)P;
+  return (float)(t1 + __reduce_add_sync(FULL, s)) * scale;
 }
 
 // mean over the curve's points of the per-point bound (whole warp; all
@@ -775,8 +777,12 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
     tma_load_1d(&raw[w][0][0], A.db + (size_t)id * P * 2, bytes, &bars[w][0]);
   }
   uint32_t phase = 0;
+  // running bound read one curve ahead (an older value is larger, still an
+  // upper bound of the final k-th best)
   float thr_c = prune ? __uint_as_float(__ldcg(thr_q)) : INFINITY;
   const uint32_t lbc_s = smem_u32(lb_dt) + (uint32_t)LB_VTX_BYTES;  // cell table
+  const uint32_t bar_s = smem_u32(&bars[w][0]);                     // + 8 * buffer
+  const uint32_t raw_s = smem_u32(&raw[w][0][0]);                   // + PMAX * 8 * buffer
 
   for (long long it = 0; it < count; ++it) {
     const int bi = (int)(it & 1);
@@ -788,10 +794,11 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
       if (it + 1 < count && lane == 0) {
         fence_proxy_async();
         const long long nid = rec_of(pos + stride);
-        mbar_expect_tx(&bars[w][bi ^ 1], bytes);
-        tma_load_1d(&raw[w][bi ^ 1][0], A.db + (size_t)nid * P * 2, bytes, &bars[w][bi ^ 1]);
+        const uint32_t nb = (uint32_t)(bi ^ 1);
+        mbar_expect_tx_s(bar_s + 8u * nb, bytes);
+        tma_load_1d_s(raw_s + (uint32_t)(PMAX * 8) * nb, A.db + (size_t)nid * P * 2, bytes, bar_s + 8u * nb);
       }
-      mbar_wait(&bars[w][bi], (phase >> bi) & 1u);
+      mbar_wait_s(bar_s + 8u * (uint32_t)bi, (phase >> bi) & 1u);
       phase ^= (1u << bi);
       cur = &raw[w][bi][0];
     } else {
@@ -807,8 +814,9 @@ __global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
       // this curve; an older, larger value still bounds the final k-th best
       // from above)
       const float t = fmaxf(thr_c, A.threshold);
-      thr_c = __uint_as_float(__ldcg(thr_q));
-      const float lb1 = curve_row_bound_cell(smem_u32(cur), P, lbc_s, lb_lx, lb_ly, lb_ihx, lb_ihy, lane,
+      thr_c = __uint_as_float(__ldcg(thr_q));  // for the next curve (measured: two in flight was slower)
+      const uint32_t cur_s = use_tma ? raw_s + (uint32_t)(PMAX * 8 * bi) : raw_s;  // = cur
+      const float lb1 = curve_row_bound_cell(cur_s, P, lbc_s, lb_lx, lb_ly, lb_ihx, lb_ihy, lane,
                                              (t + lb_slack) * (1.f + 2e-4f));
       if (fmaf(lb1, 1.f - 1e-4f, -lb_slack) > t) continue;
       const float lb4 = curve_row_bound(cur, P, lb_dt, lb_lx, lb_ly, lb_ihx, lb_ihy, lb_cx, lb_cy, lane);
