@@ -58,7 +58,7 @@ struct __align__(16) StepRec {
   float df;              // |ra - rb|
   float c2;              // ra^2 - rb^2
   float ra2;             // branch sign * ra^2 (|ra2| = ra^2)
-  uint32_t pmask;        // 1 << a | 1 << b (parents; informational)
+  uint32_t pmask;        // 8-byte slots: fp16 error offsets of the parents (a | b << 16)
   uint32_t a_off;        // byte offset of joint a's float2 column
   uint32_t b_off;
   uint32_t t_off;
@@ -265,7 +265,8 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
       }
     } else {
       // large mechanisms (8-byte slots keep three CTAs per SM): the same
-      // per-joint bound, stored as fp16 (scaled by kErrScale, rounded up) in
+      // per-joint bound, stored as fp16 (rounded up; kErr0 and small bounds
+      // are subnormal halves, resolution 6e-8) in
       // a [joint][lane] array after the position columns
       const uint32_t ecol = smem_u32(W.cols) + (uint32_t)W.ecol_off + (uint32_t)W.lane * 2u;
 #pragma unroll 1
@@ -279,7 +280,8 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
         const float inv = rsqrt_approx(d2);
         const float d = d2 * inv;
         const float m = fminf(g0.x - d, d - g0.y);
-        const float ep = fmaxf(lds_h16(ecol + (g1.y >> 2)), lds_h16(ecol + (g1.z >> 2))) * kErrScaleInv;
+        // pmask holds the parents' error offsets (a | b << 16)
+        const float ep = fmaxf(lds_h16(ecol + (g1.x & 0xffffu)), lds_h16(ecol + (g1.x >> 16)));
         fix |= !(fabsf(m) >= fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
         if (m < 0.0f) {
           lk = s;
@@ -293,7 +295,7 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
         const float xi = x * inv;
         const float hb = copysignf(h, g0.w) * inv;
         sts_f2(col + g1.w, make_float2(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y))));
-        sts_h16(ecol + (g1.w >> 2), e * kErrScale);
+        sts_h16(ecol + (g1.w >> 2), e);
       }
     }
   if (COUNT) {
@@ -345,9 +347,9 @@ __device__ __forceinline__ void fill_static32(const Warp& W) {
     for (int k = 0; k < H.nstatic; ++k) {
       const int j = H.statics[k];
       W.p32(j) = make_float2((float)H.p0[j].x, (float)H.p0[j].y);
-      sts_h16(ecol + 64u * j, kErr0 * kErrScale);
+      sts_h16(ecol + 64u * j, kErr0);
     }
-    sts_h16(ecol + 64u, kErr0 * kErrScale);  // crank tip
+    sts_h16(ecol + 64u, kErr0);  // crank tip
   }
 }
 
@@ -491,7 +493,9 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
       r.df = (float)fabs(ra - rb);
       r.c2 = (float)(ra * ra - rb * rb);
       r.ra2 = br < 0.0 ? -((float)ra * (float)ra) : (float)ra * (float)ra;
-      r.pmask = (1u << ia_) | (1u << ib_);
+      // 8-byte slots: the parents' fp16 error offsets (a | b << 16); the
+      // 16-byte-slot screens keep their bound inside the slot
+      r.pmask = SLOT == 8 ? ((uint32_t)ia_ * 64u) | ((uint32_t)ib_ * 64u << 16) : 0u;
       r.a_off = (uint32_t)ia_ * 32u * SLOT;  // slot (joint, lane) at (j * 32 + lane) * SLOT
       r.b_off = (uint32_t)ib_ * 32u * SLOT;
       r.t_off = (uint32_t)it_ * 32u * SLOT;

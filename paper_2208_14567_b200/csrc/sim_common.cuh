@@ -54,10 +54,9 @@ __device__ __forceinline__ float rcp_approx(float x) {
 constexpr float kErr0 = 2e-7f;
 constexpr float kErrStep = 5e-7f;
 constexpr float kMarginK = 3.0f;
-// fp16 storage of error bounds (8-byte-slot screens): e * 2^12 keeps kErr0
-// a normal half; rounded up on store so a stored bound never shrinks
-constexpr float kErrScale = 4096.0f;
-constexpr float kErrScaleInv = 1.0f / 4096.0f;
+// fp16 storage of error bounds (8-byte-slot screens): rounded up on store
+// so a stored bound never shrinks (bounds below 6.1e-5 are subnormal halves,
+// absolute resolution 6e-8 -- far below the 2e-6 ambiguity floor)
 __device__ __forceinline__ float lds_h16(uint32_t a) {
   unsigned short h;
   asm("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a) : "memory");
