@@ -712,8 +712,11 @@ __device__ __forceinline__ void cta_flush_lists(const ScanCtx& c, int qi, int w,
   flush_lists(cc, qi, blockIdx.x, lane, top, hit, tot);
 }
 
+#ifndef LA_CH_MINB
+#define LA_CH_MINB 2  // resident CTAs per SM the register budget targets (3: 80 registers with spills, 12 % slower on C4)
+#endif
 template <int QS>
-__global__ void __launch_bounds__(CT, 3) chamfer_scan_kernel(const ScanCtx c) {
+__global__ void __launch_bounds__(CT, LA_CH_MINB) chamfer_scan_kernel(const ScanCtx c) {
   extern __shared__ __align__(128) unsigned char scan_smem[];
   auto raw = reinterpret_cast<float2(*)[2][PMAX]>(scan_smem);                                  // [CW][2][PMAX]
   auto exs = reinterpret_cast<float4(*)[PMAX / 2]>(scan_smem + CW * 2 * PMAX * sizeof(float2));  // [CW][PMAX/2]
