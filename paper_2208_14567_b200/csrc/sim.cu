@@ -738,94 +738,6 @@ __global__ void dyad_kernel(const double* __restrict__ pa, const double* __restr
 // ---------------------------------------------------------------- compaction
 constexpr int CP_THREADS = 1024;  // one tile = 1024 candidates
 
-__global__ void compact_count(const int32_t* __restrict__ first_t, int64_t B, int32_t T,
-                              int32_t* tile_count) {
-  const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
-  const bool v = i < B && first_t[i] == T;
-  const unsigned bal = __ballot_sync(FULL, v);
-  __shared__ int wsum[CP_THREADS / 32];
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(bal);
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int s = wsum[threadIdx.x];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if (threadIdx.x == 0) tile_count[blockIdx.x] = s;
-  }
-}
-
-// single-block exclusive scan over tile counts (tiles <= a few 10^5)
-__device__ void scan_tiles(int32_t* tile_count, long long ntiles, int64_t* total) {
-  __shared__ long long carry;
-  __shared__ long long wsum[32];
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (long long base = 0; base < ntiles; base += 1024) {
-    const long long i = base + threadIdx.x;
-    long long v = i < ntiles ? tile_count[i] : 0;
-    // inclusive warp scan
-    long long x = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      long long y = __shfl_up_sync(FULL, x, o);
-      if ((threadIdx.x & 31) >= o) x += y;
-    }
-    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      long long s = wsum[threadIdx.x];
-      for (int o = 1; o < 32; o <<= 1) {
-        long long y = __shfl_up_sync(FULL, s, o);
-        if (threadIdx.x >= o) s += y;
-      }
-      wsum[threadIdx.x] = s;
-    }
-    __syncthreads();
-    const long long wbase = (threadIdx.x >= 32) ? wsum[(threadIdx.x >> 5) - 1] : 0;
-    const long long excl = carry + wbase + x - v;
-    __syncthreads();
-    if (i < ntiles) tile_count[i] = (int32_t)excl;  // offsets fit: B < 2^31 per launch
-    if (threadIdx.x == 1023) carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *total = carry;
-  __syncthreads();
-}
-
-__global__ void compact_scan(int32_t* tile_count, long long ntiles, int64_t* total) {
-  scan_tiles(tile_count, ntiles, total);
-}
-
-// both tile arrays of la_compact_rows in one launch
-__global__ void compact_scan2(int32_t* tile_count, int32_t* tile_rows, long long ntiles, int64_t* total,
-                              int64_t* total_rows) {
-  scan_tiles(tile_count, ntiles, total);
-  scan_tiles(tile_rows, ntiles, total_rows);
-}
-
-__global__ void compact_scatter(const int32_t* __restrict__ first_t, int64_t B, int32_t T,
-                                const int32_t* __restrict__ tile_off, int64_t* out) {
-  const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
-  const bool v = i < B && first_t[i] == T;
-  const unsigned bal = __ballot_sync(FULL, v);
-  __shared__ int wsum[CP_THREADS / 32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) wsum[w] = __popc(bal);
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int s = wsum[lane];
-    int x = s;
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(FULL, x, o);
-      if (lane >= o) x += y;
-    }
-    wsum[lane] = x - s;
-  }
-  __syncthreads();
-  if (v) {
-    const long long pos = (long long)tile_off[blockIdx.x] + wsum[w] + __popc(bal & ((1u << lane) - 1u));
-    out[pos] = i;
-  }
-}
-
 // ---- compaction with dense row offsets: selected item i (first_t == T)
 // gets idx = i and row_off = sum of its predecessors' joint counts, so a
 // write pass with traj_row = row_off stores paths without padding rows
@@ -838,87 +750,64 @@ __device__ __forceinline__ int2 item_rows2(const int32_t* topo, const la_plan* p
   return make_int2(p.nsteps, p.n - p.nsteps);
 }
 
-template <bool SPLIT>
-__global__ void rows_count(const int32_t* __restrict__ first_t, int64_t B, int32_t T, const int32_t* __restrict__ topo,
-                           const la_plan* __restrict__ plans, int32_t* tile_count, int32_t* tile_rows,
-                           int32_t* tile_rows2) {
-  const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
-  const bool v = i < B && first_t[i] == T;
-  int r = 0, r2 = 0;
-  if (v) {
-    if (SPLIT) {
-      const int2 q = item_rows2(topo, plans, i);
-      r = q.x;
-      r2 = q.y;
-    } else {
-      r = item_rows(topo, plans, i);
-    }
-  }
-  const unsigned bal = __ballot_sync(FULL, v);
-  for (int o = 16; o > 0; o >>= 1) {
-    r += __shfl_xor_sync(FULL, r, o);
-    if (SPLIT) r2 += __shfl_xor_sync(FULL, r2, o);
-  }
-  __shared__ int wc[CP_THREADS / 32], wr[CP_THREADS / 32], wr2[CP_THREADS / 32];
-  if ((threadIdx.x & 31) == 0) {
-    wc[threadIdx.x >> 5] = __popc(bal);
-    wr[threadIdx.x >> 5] = r;
-    wr2[threadIdx.x >> 5] = r2;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int c = wc[threadIdx.x], s = wr[threadIdx.x], s2 = wr2[threadIdx.x];
-    for (int o = 16; o > 0; o >>= 1) {
-      c += __shfl_xor_sync(FULL, c, o);
-      s += __shfl_xor_sync(FULL, s, o);
-      s2 += __shfl_xor_sync(FULL, s2, o);
-    }
-    if (threadIdx.x == 0) {
-      tile_count[blockIdx.x] = c;
-      tile_rows[blockIdx.x] = s;
-      if (SPLIT) tile_rows2[blockIdx.x] = s2;
-    }
-  }
-}
+// ---- single-pass ordered selection (decoupled look-back).  Tile t of
+// CP_THREADS consecutive items is taken in ticket order (so every
+// predecessor tile is held by a running CTA); its selected count and row
+// sums are block-scanned, published as an aggregate, and the tile's
+// exclusive prefix is gathered from its predecessors' published values --
+// aggregates, back to the nearest inclusive prefix -- by one warp, 32 tiles
+// per step.  One launch replaces count + single-CTA scan + scatter.
+//   MODE 0: ids only; 1: rows = plan n; 2: rows = plan nsteps (dyad
+//   targets), rows2 = n - nsteps (static joints + crank tip)
+// Tile word: flag (2 bits: 0 empty, 1 aggregate, 2 inclusive) | count (31)
+// | rows (31); rows2 lives in agg2 / inc2, written before the word.
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_INC = 2ull << 62;
 
-template <bool SPLIT>
-__global__ void rows_scatter(const int32_t* __restrict__ first_t, int64_t B, int32_t T,
-                             const int32_t* __restrict__ topo, const la_plan* __restrict__ plans,
-                             const int32_t* __restrict__ tile_off, const int32_t* __restrict__ tile_row_off,
-                             const int32_t* __restrict__ tile_row_off2, int64_t* idx, int64_t* row_off,
-                             int64_t* row_off2) {
-  const long long i = (long long)blockIdx.x * CP_THREADS + threadIdx.x;
-  const bool v = i < B && first_t[i] == T;
-  int r = 0, r2 = 0;
-  if (v) {
-    if (SPLIT) {
-      const int2 q = item_rows2(topo, plans, i);
-      r = q.x;
-      r2 = q.y;
-    } else {
-      r = item_rows(topo, plans, i);
-    }
-  }
+template <int MODE>
+__global__ void __launch_bounds__(CP_THREADS) select_kernel(const int32_t* __restrict__ first_t, int64_t B,
+                                                            int32_t value, const int32_t* __restrict__ topo,
+                                                            const la_plan* __restrict__ plans,
+                                                            unsigned long long* st, long long* agg2, long long* inc2,
+                                                            unsigned* ticket, long long ntiles, int64_t* idx,
+                                                            int64_t* row, int64_t* row2, int64_t* count,
+                                                            int64_t* total, int64_t* total2) {
+  __shared__ unsigned s_tile;
+  __shared__ int wc[CP_THREADS / 32], wr[CP_THREADS / 32], wr2[CP_THREADS / 32];
+  __shared__ long long s_ex[3];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const long long tile = s_tile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long i = tile * CP_THREADS + threadIdx.x;
+  const bool v = i < B && first_t[i] == value;
+  int r = 0, r2 = 0;
+  if (v && MODE == 1) r = item_rows(topo, plans, i);
+  if (v && MODE == 2) {
+    const int2 q = item_rows2(topo, plans, i);
+    r = q.x;
+    r2 = q.y;
+  }
   const unsigned bal = __ballot_sync(FULL, v);
   int x = r, x2 = r2;  // inclusive warp scans of the row counts
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(FULL, x, o), y2 = __shfl_up_sync(FULL, x2, o);
-    if (lane >= o) {
-      x += y;
-      x2 += y2;
+  if (MODE > 0) {
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, x, o), y2 = __shfl_up_sync(FULL, x2, o);
+      if (lane >= o) {
+        x += y;
+        x2 += y2;
+      }
     }
   }
-  __shared__ int wc[CP_THREADS / 32], wr[CP_THREADS / 32], wr2[CP_THREADS / 32];
   if (lane == 31) {
     wc[w] = __popc(bal);
     wr[w] = x;
     wr2[w] = x2;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {  // exclusive scan of the warp totals
-    const int c = wc[lane], s = wr[lane], s2 = wr2[lane];
-    int xc = c, xs = s, xs2 = s2;
+  if (w == 0) {
+    // exclusive scan of the warp totals, tile totals in lane 31
+    const int c = wc[lane], sr = wr[lane], sr2 = wr2[lane];
+    int xc = c, xs = sr, xs2 = sr2;
     for (int o = 1; o < 32; o <<= 1) {
       const int yc = __shfl_up_sync(FULL, xc, o), ys = __shfl_up_sync(FULL, xs, o),
                 ys2 = __shfl_up_sync(FULL, xs2, o);
@@ -929,24 +818,65 @@ __global__ void rows_scatter(const int32_t* __restrict__ first_t, int64_t B, int
       }
     }
     wc[lane] = xc - c;
-    wr[lane] = xs - s;
-    wr2[lane] = xs2 - s2;
+    wr[lane] = xs - sr;
+    wr2[lane] = xs2 - sr2;
+    const long long tc = __shfl_sync(FULL, xc, 31), tr = __shfl_sync(FULL, xs, 31), tr2 = __shfl_sync(FULL, xs2, 31);
+    if (lane == 0) {
+      agg2[tile] = tr2;
+      __threadfence();
+      atomicExch(st + tile, LB_AGG | ((unsigned long long)tc << 31) | (unsigned long long)tr);
+    }
+    // look-back
+    long long ec = 0, er = 0, er2 = 0;
+    for (long long j = tile - 1; j >= 0;) {
+      const long long k = j - lane;
+      unsigned long long wv = LB_INC;  // k < 0: an inclusive zero
+      if (k >= 0) wv = *reinterpret_cast<volatile unsigned long long*>(st + k);
+      const unsigned long long flag = wv & (3ull << 62);
+      const unsigned inc = __ballot_sync(FULL, flag == LB_INC);
+      const int lim = inc ? __ffs(inc) - 1 : 31;  // lanes 0..lim are needed
+      const unsigned need = lim == 31 ? FULL : ((2u << lim) - 1u);
+      if (__ballot_sync(FULL, flag == 0ull) & need) continue;  // a predecessor has not published yet
+      long long c = 0, rr = 0, rr2 = 0;
+      if (lane <= lim && k >= 0) {
+        c = (long long)((wv >> 31) & 0x7fffffffull);
+        rr = (long long)(wv & 0x7fffffffull);
+        __threadfence();
+        rr2 = flag == LB_INC ? *reinterpret_cast<volatile long long*>(inc2 + k)
+                             : *reinterpret_cast<volatile long long*>(agg2 + k);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        c += __shfl_xor_sync(FULL, c, o);
+        rr += __shfl_xor_sync(FULL, rr, o);
+        rr2 += __shfl_xor_sync(FULL, rr2, o);
+      }
+      ec += c;
+      er += rr;
+      er2 += rr2;
+      if (inc) break;
+      j -= 32;
+    }
+    if (lane == 0) {
+      inc2[tile] = er2 + tr2;
+      __threadfence();
+      atomicExch(st + tile, LB_INC | ((unsigned long long)(ec + tc) << 31) | (unsigned long long)(er + tr));
+      s_ex[0] = ec;
+      s_ex[1] = er;
+      s_ex[2] = er2;
+      if (tile == ntiles - 1) {
+        *count = ec + tc;
+        if (total) *total = er + tr;
+        if (total2) *total2 = er2 + tr2;
+      }
+    }
   }
   __syncthreads();
   if (v) {
-    const long long pos = (long long)tile_off[blockIdx.x] + wc[w] + __popc(bal & ((1u << lane) - 1u));
+    const long long pos = s_ex[0] + wc[w] + __popc(bal & ((1u << lane) - 1u));
     idx[pos] = i;
-    row_off[pos] = (long long)tile_row_off[blockIdx.x] + wr[w] + (x - r);
-    if (SPLIT) row_off2[pos] = (long long)tile_row_off2[blockIdx.x] + wr2[w] + (x2 - r2);
+    if (MODE > 0) row[pos] = s_ex[1] + wr[w] + (x - r);
+    if (MODE == 2) row2[pos] = s_ex[2] + wr2[w] + (x2 - r2);
   }
-}
-
-// the three tile arrays of la_compact_rows_split in one launch
-__global__ void compact_scan3(int32_t* tile_count, int32_t* tile_rows, int32_t* tile_rows2, long long ntiles,
-                              int64_t* total, int64_t* total_rows, int64_t* total_rows2) {
-  scan_tiles(tile_count, ntiles, total);
-  scan_tiles(tile_rows, ntiles, total_rows);
-  scan_tiles(tile_rows2, ntiles, total_rows2);
 }
 
 }  // namespace
@@ -1044,12 +974,42 @@ int la_dyad_solve(const double* pa, const double* pb, const double* r_a, const d
   return cuda_status("la_dyad_solve");
 }
 
-size_t la_compact_workspace(int64_t B) {
+// look-back selection workspace: a ticket, then per tile the published
+// word and the aggregate / inclusive rows2 (zeroed by a memset per call)
+static size_t select_ws(int64_t B) {
   const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
-  return (size_t)(tiles > 0 ? tiles : 1) * sizeof(int32_t);
+  return 16 + (size_t)(tiles > 0 ? tiles : 1) * 3 * sizeof(long long);
 }
 
-size_t la_compact_rows_workspace(int64_t B) { return 2 * la_compact_workspace(B); }
+static int select_launch(int mode, const int32_t* first_t, int64_t B, int32_t value, const int32_t* topo,
+                         const la_plan* plans, int64_t* idx, int64_t* row, int64_t* row2, int64_t* count,
+                         int64_t* total, int64_t* total2, void* ws, cudaStream_t s) {
+  const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  unsigned* ticket = reinterpret_cast<unsigned*>(w);
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(w + 16);
+  long long* agg2 = reinterpret_cast<long long*>(st + tiles);
+  long long* inc2 = agg2 + tiles;
+  cudaMemsetAsync(ws, 0, 16 + (size_t)tiles * sizeof(unsigned long long), s);
+  switch (mode) {
+    case 0:
+      select_kernel<0><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, value, topo, plans, st, agg2, inc2, ticket,
+                                                              tiles, idx, row, row2, count, total, total2);
+      break;
+    case 1:
+      select_kernel<1><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, value, topo, plans, st, agg2, inc2, ticket,
+                                                              tiles, idx, row, row2, count, total, total2);
+      break;
+    default:
+      select_kernel<2><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, value, topo, plans, st, agg2, inc2, ticket,
+                                                              tiles, idx, row, row2, count, total, total2);
+  }
+  return 0;
+}
+
+size_t la_compact_workspace(int64_t B) { return select_ws(B); }
+
+size_t la_compact_rows_workspace(int64_t B) { return select_ws(B); }
 
 int la_compact_rows(const int32_t* first_t, int64_t B, int32_t T, const int32_t* topo, const la_plan* plans,
                     int64_t* idx, int64_t* row_off, int64_t* count, int64_t* row_total, void* ws, size_t ws_bytes,
@@ -1063,17 +1023,11 @@ int la_compact_rows(const int32_t* first_t, int64_t B, int32_t T, const int32_t*
     cudaMemsetAsync(row_total, 0, sizeof(int64_t), s);
     return cuda_status("la_compact_rows");
   }
-  const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
-  int32_t* tc = static_cast<int32_t*>(ws);
-  int32_t* tr = tc + la_compact_workspace(B) / sizeof(int32_t);
-  rows_count<false><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, nullptr);
-  compact_scan2<<<1, 1024, 0, s>>>(tc, tr, tiles, count, row_total);
-  rows_scatter<false><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, nullptr, idx,
-                                                             row_off, nullptr);
+  select_launch(1, first_t, B, T, topo, plans, idx, row_off, nullptr, count, row_total, nullptr, ws, s);
   return cuda_status("la_compact_rows");
 }
 
-size_t la_compact_rows_split_workspace(int64_t B) { return 3 * la_compact_workspace(B); }
+size_t la_compact_rows_split_workspace(int64_t B) { return select_ws(B); }
 
 int la_compact_rows_split(const int32_t* first_t, int64_t B, int32_t T, const int32_t* topo, const la_plan* plans,
                           int64_t* idx, int64_t* target_row, int64_t* other_row, int64_t* count,
@@ -1089,15 +1043,7 @@ int la_compact_rows_split(const int32_t* first_t, int64_t B, int32_t T, const in
     cudaMemsetAsync(other_total, 0, sizeof(int64_t), s);
     return cuda_status("la_compact_rows_split");
   }
-  const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
-  const size_t per = la_compact_workspace(B) / sizeof(int32_t);
-  int32_t* tc = static_cast<int32_t*>(ws);
-  int32_t* tr = tc + per;
-  int32_t* tr2 = tr + per;
-  rows_count<true><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, tr2);
-  compact_scan3<<<1, 1024, 0, s>>>(tc, tr, tr2, tiles, count, target_total, other_total);
-  rows_scatter<true><<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, topo, plans, tc, tr, tr2, idx,
-                                                            target_row, other_row);
+  select_launch(2, first_t, B, T, topo, plans, idx, target_row, other_row, count, target_total, other_total, ws, s);
   return cuda_status("la_compact_rows_split");
 }
 
@@ -1111,11 +1057,7 @@ int la_compact_valid(const int32_t* first_t, int64_t B, int32_t T, int64_t* vali
     cudaMemsetAsync(valid_count, 0, sizeof(int64_t), s);
     return cuda_status("la_compact_valid");
   }
-  const long long tiles = (B + CP_THREADS - 1) / CP_THREADS;
-  int32_t* tc = static_cast<int32_t*>(ws);
-  compact_count<<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, tc);
-  compact_scan<<<1, 1024, 0, s>>>(tc, tiles, valid_count);
-  compact_scatter<<<(unsigned)tiles, CP_THREADS, 0, s>>>(first_t, B, T, tc, valid_idx);
+  select_launch(0, first_t, B, T, nullptr, nullptr, valid_idx, nullptr, nullptr, valid_count, nullptr, nullptr, ws, s);
   return cuda_status("la_compact_valid");
 }
 
