@@ -903,7 +903,10 @@ __global__ void __launch_bounds__(CT, LA_CH_MINB) chamfer_scan_kernel(const Scan
 // merge_kernel.  Lists are identical to the unpruned scan for the same
 // reasons as chamfer_scan_kernel (every bound is a valid lower bound after
 // the (1 - 1e-4) / slack margins; ties never prune).
-constexpr int MQ_W = 8;           // warps per CTA
+#ifndef LA_MQ_WARPS
+#define LA_MQ_WARPS 12  // 8 / 10 / 12 warps: C5 25.7 / 23.4 / 20.6 ms (12 still fits 32-query groups)
+#endif
+constexpr int MQ_W = LA_MQ_WARPS;  // warps per CTA
 constexpr int MQ_T = MQ_W * 32;
 constexpr int MQ_MAXG = 64;       // queries per group (bits of the pass mask)
 constexpr int MQ_TAB_N = 129;     // grid lines of the column-term gap tables
