@@ -1312,9 +1312,17 @@ __global__ void __launch_bounds__(MQ_T, 1) chamfer_mq_kernel(const ScanCtx c, in
       const float2* qsrc = reinterpret_cast<const float2*>(A.queries) + (size_t)qi * Qn;
       QueryRegs<QS> Q;
       load_query<QS>(Q, qsrc, Qn, lane);
-      // column term from 4 boxes of 50-point runs, then 20 of 10-point runs
-      const float colb1 = fmaxf(colb0, curve_col_bound<QS, 50>(Q, cur, P, Qn, boxes, lane));
+      // column term from coarse boxes (10 of 20-point runs), then 20 of
+      // 10-point runs
+#ifndef LA_MQ_RUN1
+#define LA_MQ_RUN1 20  // C5: 50 / 25 / 20 / 16 / none: 20.6 / 19.2 / 18.9 / 19.1 / 19.4 ms
+#endif
+#if LA_MQ_RUN1 > 0
+      const float colb1 = fmaxf(colb0, curve_col_bound<QS, LA_MQ_RUN1>(Q, cur, P, Qn, boxes, lane));
       if (fmaf(rowb + colb1, 1.f - 1e-4f, -lb_slack) > t) continue;
+#else
+      const float colb1 = colb0;
+#endif
       if (lane == 0) atomicAdd(&s_cnt[3], 1u);
       __syncwarp();
       const float colb = fmaxf(colb1, curve_col_bound<QS, 10>(Q, cur, P, Qn, boxes, lane));
