@@ -32,7 +32,10 @@
 namespace la {
 namespace {
 
-constexpr int CW = 8;           // warps per CTA
+#ifndef LA_CH_WARPS
+#define LA_CH_WARPS 10  // x 2 CTAs at 96 registers: C4 8 / 10 / 12 warps 3.58 / 3.39 / 4.03 ms
+#endif
+constexpr int CW = LA_CH_WARPS;  // warps per CTA
 constexpr int CT = CW * 32;
 constexpr int PMAX = 256;       // database points per curve (fast path)
 constexpr float BIG = 1.0e18f;  // padding coordinate: never a minimum
