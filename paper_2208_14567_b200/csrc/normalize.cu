@@ -413,7 +413,10 @@ __global__ void __launch_bounds__(NT) circle_kernel(const void* paths, int64_t M
 //           stability) and the lexicographically smallest pair with d^2 == M
 // then the f64 frame transform / bbox / half-turn rule / variance with warp
 // shuffles only (no CTA barriers).
-constexpr int NW_WARPS = 8;
+#ifndef LA_NW_WARPS
+#define LA_NW_WARPS 8
+#endif
+constexpr int NW_WARPS = LA_NW_WARPS;
 constexpr int NW_PMAX = 256;
 
 __device__ __forceinline__ double warp_min_d(double v) {
@@ -432,7 +435,10 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // maxThreads only: ptxas then settles at 79 registers (3 CTAs per SM); an
 // explicit minBlocks of 1 gives 114 (2 CTAs, 10 % slower), 3 or 4 cap it
 // tighter and are slower too (measured, round 1 session 2)
-__global__ void __launch_bounds__(NW_WARPS * 32) normalize_warp_kernel(const la_norm_args p) {
+#ifndef LA_NW_MINB
+#define LA_NW_MINB 3  // 3 CTAs per SM: 200k curves 1.63 (no bound) / 1.53 / 1.73 (4) ms
+#endif
+__global__ void __launch_bounds__(NW_WARPS * 32, LA_NW_MINB) normalize_warp_kernel(const la_norm_args p) {
   __shared__ __align__(16) float2 pts[NW_WARPS][NW_PMAX];
   // (-2x', -2y', |p'|^2, m): p' centred at point 0; m = pass-1 maximum of
   // column j (and of its partner column: one reduction per column pair)
