@@ -2084,10 +2084,11 @@ struct Plan {
   size_t mq_smem;
 };
 
-// resident CTAs per SM of chamfer_scan_kernel<qs> (registers and the
-// ~67 KB of shared memory -- curve double buffer, per-warp lists and the
-// 8.3 KB distance grid -- allow 3 for Q = 200, not 4), per device; racing
-// threads compute and store the same value (relaxed atomics)
+// resident CTAs per SM of chamfer_scan_kernel<qs> (the register budget of
+// LA_CH_MINB and ~90 KB of shared memory -- ten warps' curve double buffers,
+// expanded curves and row buffers plus the 16.3 KB vertex + cell tables --
+// allow 2), per device; racing threads compute and store the same value
+// (relaxed atomics).  Unpruned scans reserve the tables too (unused).
 int scan_occupancy(int qs) {
   static std::atomic<int> cache[64][9];
   if (qs < 1 || qs > 8) return 3;

@@ -44,7 +44,10 @@ namespace {
 
 constexpr int NJ = LA_MAX_JOINTS;
 constexpr int NS = LA_MAX_STEPS;
-constexpr int SIM_WARPS = 8;
+#ifndef LA_SIM_WARPS
+#define LA_SIM_WARPS 8
+#endif
+constexpr int SIM_WARPS = LA_SIM_WARPS;
 constexpr int SIM_THREADS = SIM_WARPS * 32;
 #ifndef LA_SIM_MINB
 #define LA_SIM_MINB 4  // resident CTAs per SM the register allocation targets
