@@ -907,13 +907,17 @@ __global__ void __launch_bounds__(CT, LA_CH_MINB) chamfer_scan_kernel(const Scan
 // reasons as chamfer_scan_kernel (every bound is a valid lower bound after
 // the (1 - 1e-4) / slack margins; ties never prune).
 #ifndef LA_MQ_WARPS
-#define LA_MQ_WARPS 12  // 8 / 10 / 12 warps: C5 25.7 / 23.4 / 20.6 ms (12 still fits 32-query groups)
+#define LA_MQ_WARPS 16  // C5: 8 / 12 / 16 warps 25.7 / 18.4 / 17.0 ms (16 still fits 32-query groups)
 #endif
 constexpr int MQ_W = LA_MQ_WARPS;  // warps per CTA
 constexpr int MQ_T = MQ_W * 32;
 constexpr int MQ_MAXG = 64;       // queries per group (bits of the pass mask)
 constexpr int MQ_TAB_N = 129;     // grid lines of the column-term gap tables
-constexpr int MQ_TAB_BYTES = 2068;  // 8 tables of MQ_TAB_N halves + pad (odd word stride)
+#ifndef LA_MQ_DIAG
+#define LA_MQ_DIAG 0  // gap tables along the diagonals too (measured: no extra pruning on C5)
+#endif
+constexpr int MQ_NTAB = LA_MQ_DIAG ? 8 : 4;
+constexpr int MQ_TAB_BYTES = LA_MQ_DIAG ? 2068 : 1036;  // MQ_NTAB tables of MQ_TAB_N halves + pad (odd word stride)
 
 template <int G0>
 struct MQGrid {
@@ -1014,12 +1018,15 @@ __global__ void __launch_bounds__(160) mq_tab_kernel(const float* __restrict__ q
     t[2 * MQ_TAB_N + m] = __float2half_rd(ay * sc);
     t[3 * MQ_TAB_N + m] = __float2half_rd(by * sc);
     // rounding of u, v (<= 2.4e-7 absolute) is covered by the scan's lb_slack
-    t[4 * MQ_TAB_N + m] = __float2half_rd(au * sc);
-    t[5 * MQ_TAB_N + m] = __float2half_rd(bu * sc);
-    t[6 * MQ_TAB_N + m] = __float2half_rd(av * sc);
-    t[7 * MQ_TAB_N + m] = __float2half_rd(bv * sc);
+    if (LA_MQ_DIAG) {
+      t[4 * MQ_TAB_N + m] = __float2half_rd(au * sc);
+      t[5 * MQ_TAB_N + m] = __float2half_rd(bu * sc);
+      t[6 * MQ_TAB_N + m] = __float2half_rd(av * sc);
+      t[7 * MQ_TAB_N + m] = __float2half_rd(bv * sc);
+    }
   }
-  if (m < (MQ_TAB_BYTES / 2 - 8 * MQ_TAB_N)) tab[(size_t)qi * (MQ_TAB_BYTES / 2) + 8 * MQ_TAB_N + m] = __float2half(0.f);
+  if (m < (MQ_TAB_BYTES / 2 - MQ_NTAB * MQ_TAB_N))
+    tab[(size_t)qi * (MQ_TAB_BYTES / 2) + MQ_NTAB * MQ_TAB_N + m] = __float2half(0.f);
 }
 
 // highest grid line <= v (0 below the box: A vanishes there) / lowest >= v
@@ -1231,15 +1238,19 @@ __global__ void __launch_bounds__(MQ_T, 1) chamfer_mq_kernel(const ScanCtx c, in
     for (int i = lane; i < P; i += 32) {
       const float2 a = cur[i];
       bx0 = fminf(bx0, a.x); by0 = fminf(by0, a.y); bx1 = fmaxf(bx1, a.x); by1 = fmaxf(by1, a.y);
-      const float u = a.x + a.y, v = a.x - a.y;
-      bu0 = fminf(bu0, u); bv0 = fminf(bv0, v); bu1 = fmaxf(bu1, u); bv1 = fmaxf(bv1, v);
+      if (LA_MQ_DIAG) {
+        const float u = a.x + a.y, v = a.x - a.y;
+        bu0 = fminf(bu0, u); bv0 = fminf(bv0, v); bu1 = fmaxf(bu1, u); bv1 = fmaxf(bv1, v);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       bx0 = fminf(bx0, __shfl_xor_sync(FULL, bx0, o)); by0 = fminf(by0, __shfl_xor_sync(FULL, by0, o));
       bx1 = fmaxf(bx1, __shfl_xor_sync(FULL, bx1, o)); by1 = fmaxf(by1, __shfl_xor_sync(FULL, by1, o));
-      bu0 = fminf(bu0, __shfl_xor_sync(FULL, bu0, o)); bv0 = fminf(bv0, __shfl_xor_sync(FULL, bv0, o));
-      bu1 = fmaxf(bu1, __shfl_xor_sync(FULL, bu1, o)); bv1 = fmaxf(bv1, __shfl_xor_sync(FULL, bv1, o));
+      if (LA_MQ_DIAG) {
+        bu0 = fminf(bu0, __shfl_xor_sync(FULL, bu0, o)); bv0 = fminf(bv0, __shfl_xor_sync(FULL, bv0, o));
+        bu1 = fmaxf(bu1, __shfl_xor_sync(FULL, bu1, o)); bv1 = fmaxf(bv1, __shfl_xor_sync(FULL, bv1, o));
+      }
     }
     const int ilx = mq_line_lo(bx0, lx, ccx, iccx), ihx_ = mq_line_hi(bx1, lx, ccx, iccx);
     const int ily = mq_line_lo(by0, ly, ccy, iccy), ihy_ = mq_line_hi(by1, ly, ccy, iccy);
@@ -1253,6 +1264,7 @@ __global__ void __launch_bounds__(MQ_T, 1) chamfer_mq_kernel(const ScanCtx c, in
       const uint32_t t = stab_b + (uint32_t)qg * MQ_TAB_BYTES;
       const float X = lds_half(t + 2u * ilx) + lds_half(t + 2u * (MQ_TAB_N + ihx_));
       const float Y = lds_half(t + 2u * (2 * MQ_TAB_N + ily)) + lds_half(t + 2u * (3 * MQ_TAB_N + ihy_));
+      if (!LA_MQ_DIAG) return fmaxf(fmaxf(X, Y), (X + Y) * 0.70710670f);
       const float U = lds_half(t + 2u * (4 * MQ_TAB_N + ilu)) + lds_half(t + 2u * (5 * MQ_TAB_N + ihu));
       const float V = lds_half(t + 2u * (6 * MQ_TAB_N + ilv)) + lds_half(t + 2u * (7 * MQ_TAB_N + ihv));
       return fmaxf(fmaxf(fmaxf(X, Y), (X + Y) * 0.70710670f), fmaxf(fmaxf(U, V) * 0.70710670f, (U + V) * 0.49999997f));
