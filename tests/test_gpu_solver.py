@@ -291,6 +291,35 @@ def test_compaction_ordered(torch):
         assert torch.equal(idx[: want.numel()], want)
 
 
+def test_compaction_lookback_edges(torch):
+    """The single-pass look-back selection: none / all selected, sizes around
+    a tile, a few thousand tiles (look-back over many published aggregates),
+    and the split row sums of la_compact_rows_split against numpy."""
+    from paper_2208_14567_b200.solver import compact_rows_split, compact_valid
+    from paper_2208_14567_b200.workloads import mixed_batch
+
+    for B, fill in ((5000, 0), (5000, 200), (2_500_003, None)):
+        ft = (torch.full((B,), fill, dtype=torch.int32, device="cuda") if fill is not None else
+              torch.randint(190, 201, (B,), device="cuda", dtype=torch.int32))
+        idx, cnt = compact_valid(ft, 200)
+        want = torch.nonzero(ft == 200).flatten()
+        assert int(cnt.item()) == want.numel()
+        assert torch.equal(idx[: want.numel()], want)
+    mb = mixed_batch(70_000, 5, 12, seed=29, stride=12)
+    table = mb.table()
+    topo = torch.from_numpy(mb.topo).cuda()
+    ft = torch.randint(198, 201, (mb.B,), device="cuda", dtype=torch.int32)
+    idx, row, row2, cnt, tot, tot2 = compact_rows_split(ft, 200, table, topo)
+    sel = np.flatnonzero(ft.cpu().numpy() == 200)
+    ns = np.array([len(p.steps) for p in mb.plans])[mb.topo[sel]]
+    n = mb.n[sel]
+    k = int(cnt.item())
+    assert k == len(sel) and np.array_equal(idx[:k].cpu().numpy(), sel)
+    assert np.array_equal(row[:k].cpu().numpy(), np.concatenate([[0], np.cumsum(ns)[:-1]]))
+    assert np.array_equal(row2[:k].cpu().numpy(), np.concatenate([[0], np.cumsum(n - ns)[:-1]]))
+    assert int(tot.item()) == int(ns.sum()) and int(tot2.item()) == int((n - ns).sum())
+
+
 def test_gate_only_flag(torch, golden):
     """LA_SIM_GATE_ONLY: negatives carry the coarse lock, positives exact."""
     from paper_2208_14567_b200.workloads import bare_plan, four_bar
