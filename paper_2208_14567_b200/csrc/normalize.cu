@@ -626,9 +626,23 @@ __global__ void __launch_bounds__(NW_WARPS * 32, LA_NW_MINB) normalize_warp_kern
       const double ex = b0.x - mx, ey = b0.y - my;
       const double ax = (ex + 0.5) - 0.5, ay = (ey + 0.5) - 0.5;
       const double bx = (-ex + 0.5) - 0.5, by = (-ey + 0.5) - 0.5;
-      double aa = atan2(ay, ax), ab = atan2(by, bx);
-      if (aa < 0.0) aa += 6.283185307179586;
-      if (ab < 0.0) ab += 6.283185307179586;
+      // clear half-planes decide without atan2: ay >= 1e-6 puts aa strictly
+      // inside (0, pi) and by <= -1e-6 puts ab inside (pi, 2 pi), so
+      // aa < ab and |aa - ab| > 1e-12 (and symmetrically); the first point
+      // within 1e-6 of the flip line takes the reference's atan2 path
+      double aa = 0.0, ab = 0.0;
+      if (ay >= 1e-6 && by <= -1e-6) {
+        aa = 0.0;
+        ab = 4.0;
+      } else if (ay <= -1e-6 && by >= 1e-6) {
+        aa = 4.0;
+        ab = 0.0;
+      } else {
+        aa = atan2(ay, ax);
+        ab = atan2(by, bx);
+        if (aa < 0.0) aa += 6.283185307179586;
+        if (ab < 0.0) ab += 6.283185307179586;
+      }
       if (fabs(aa - ab) <= 1e-12) {
         double ma = 0.0, mb = 0.0;
         for (int k = lane; k < P; k += 32) {
