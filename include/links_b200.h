@@ -72,6 +72,9 @@ typedef struct la_plan {
 #define LA_SIM_LANE_SCREEN 512u   /* screen with the lane-per-candidate kernel
                                       (screen.cu) instead of the
                                       warp-per-candidate one (lanes = angles) */
+#define LA_SIM_STATIC_GRID 1024u  /* deal the candidates to the warps round-robin
+                                      (four waves of CTAs) instead of through
+                                      the persistent grid's work queue        */
 #define LA_PENDING (-3)            /* first_t of a deferred coarse survivor    */
 
 /* Batched replay of compiled plans over (candidate x crank angle).

@@ -29,6 +29,7 @@ LA_SIM_SCATTER = 64
 LA_SIM_WRITE_ONLY = 128
 LA_SIM_EXACT64 = 256
 LA_SIM_LANE_SCREEN = 512
+LA_SIM_STATIC_GRID = 1024
 LA_CH_NO_MQ = 64
 LA_CH_MQ_FINE = 128
 LA_PENDING = -3

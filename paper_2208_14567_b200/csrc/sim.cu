@@ -36,6 +36,8 @@
 // coalesced float2 paths (simulate).
 #include "common.cuh"
 #include "sim_common.cuh"
+#include <atomic>
+#include <mutex>
 #include <type_traits>
 
 namespace la {
@@ -49,6 +51,12 @@ constexpr int NS = LA_MAX_STEPS;
 #endif
 constexpr int SIM_WARPS = LA_SIM_WARPS;
 constexpr int SIM_THREADS = SIM_WARPS * 32;
+#ifndef LA_SIM_CHUNK
+#define LA_SIM_CHUNK 32  // most candidates per work chunk
+#endif
+#ifndef LA_SIM_TICKETS
+#define LA_SIM_TICKETS 8  // chunks per warp a launch aims for
+#endif
 #ifndef LA_SIM_MINB
 #define LA_SIM_MINB 4  // resident CTAs per SM the register allocation targets
 #endif
@@ -71,6 +79,8 @@ struct __align__(16) StepRec64 {
   uint32_t idx;          // target | a << 8 | b << 16
   uint32_t _u;
   double br;             // branch sign
+  // exact mode: hi, lo, ra^2, rb^2; fast mode: hi^2, lo^2 (-1 if lo <= 0),
+  // ra^2, (ra^2 - rb^2) / 2
   double hi;             // (ra + rb) + LOCK_EPS   (solver.py:213, same rounding)
   double lo;             // |ra - rb| - LOCK_EPS
   double ra2;            // ra * ra
@@ -118,9 +128,10 @@ struct SimCtx {
 //   ux = dx/d, uy = dy/d
 //   p = ((pa.x + x*ux) - (br*h)*uy,  (pa.y + x*uy) + (br*h)*ux)
 // so positions and lock decisions are bit-identical to simulate_batch.
-// Fast mode: the same formulas contracted to DFMA with d, 1/d and h from
-// Newton-refined MUFU reciprocal square roots (a few ulp from numpy; the
-// lock decision can differ only for margins within ~1e-15).
+// Fast mode: DFMA throughout, u = x / d and (h / d)^2 from one refined MUFU
+// reciprocal of d^2, h / d from one refined reciprocal square root (a few
+// ulp from numpy; the lock decision, taken on d^2 against the squared
+// thresholds, can differ only for margins within ~1e-15).
 template <bool EXACT, typename Get, typename Put>
 __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get get, Put put,
                                          double* margin = nullptr) {
@@ -146,12 +157,13 @@ __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get
       const double bh = dmul(br, h);
       put(t, make_double2(dsub(dadd(pa.x, dmul(x, ux)), dmul(bh, uy)),
                           dadd(dadd(pa.y, dmul(x, uy)), dmul(bh, ux))));
-    } else {
+    } else if (margin) {
+      // triage pass of the exact mode (records as in exact mode): the
+      // distance of every lock test from its threshold
       const double d2 = fma(dy, dy, dx * dx);
       const double inv = rsqrt_f64(d2);
       const double d = d2 * inv;
-      if (margin)  // distance of every lock test from its threshold (the exact-mode triage)
-        *margin = fmin(*margin, fmin(fabs(d - eps), fmin(fabs(hl.x - d), fabs(d - hl.y))));
+      *margin = fmin(*margin, fmin(fabs(d - eps), fmin(fabs(hl.x - d), fabs(d - hl.y))));
       const bool lock = !(d >= eps) | (d > hl.x) | (d < hl.y);
       if (lock) return s;
       const double x = fma(d, d, rr.x - rr.y) * (0.5 * inv);
@@ -162,6 +174,23 @@ __device__ __forceinline__ int dyads_f64(const WarpHead& H, const SimCtx& C, Get
       const double xi = x * inv;
       const double hb = br * h * inv;
       put(t, make_double2(fma(-hb, dy, fma(xi, dx, pa.x)), fma(hb, dx, fma(xi, dy, pa.y))));
+    } else {
+      // fast records: hl = (hi^2, lo^2 or -1 when lo <= 0), rr = (ra^2,
+      // (ra^2 - rb^2) / 2).  With r = 1 / d^2:
+      //   x / d = 1/2 + (ra^2 - rb^2) r / 2 = u,   (h / d)^2 = ra^2 r - u^2
+      // so one reciprocal and one square root per dyad, and the lock tests
+      // compare d^2 with the squared thresholds (same decisions up to the
+      // rounding of a square, ~1e-16 relative)
+      const double d2 = fma(dy, dy, dx * dx);
+      const bool lock = !(d2 >= eps * eps) | (d2 > hl.x) | (d2 < hl.y);
+      if (lock) return s;
+      const double r = rcp_f64(d2);
+      const double u = fma(rr.y, r, 0.5);
+      const double w = fma(-u, u, rr.x * r);
+      const double wc = fmax(w, 1e-300);
+      const double vv = wc * rsqrt_f64(wc);
+      const double hb = br * (w > 0.0 ? vv : 0.0);
+      put(t, make_double2(fma(-hb, dy, fma(u, dx, pa.x)), fma(hb, dx, fma(u, dy, pa.y))));
     }
   }
   return -1;
@@ -394,7 +423,8 @@ __host__ __device__ constexpr size_t col_block_bytes() {
 }
 
 template <bool WRITE, bool SCREEN64, bool WONLY, bool EXACT, bool COUNT, bool ERR4>
-__global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_sim_args p, int njmax) {
+__global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_sim_args p, int njmax, int chunk_items,
+                                                                    unsigned* queue) {
   extern __shared__ __align__(16) unsigned char sim_smem_raw[];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
@@ -428,44 +458,84 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
     const long long c = *p.cand_count;
     nitems = c < nitems ? c : nitems;
   }
-  for (long long item = (long long)blockIdx.x * SIM_WARPS + w; item < nitems; item += nwarps) {
+  // Work assignment: chunks of CH consecutive candidates.  The first chunk
+  // of every warp is static (chunk = global warp index); with a work queue
+  // (queue != nullptr: a zeroed counter, one-wave persistent grid) every
+  // further chunk is the next ticket, so warps stay busy until the batch is
+  // drained whatever their candidates cost; the last warp to leave zeroes
+  // the counters again.  Without a queue the chunks are dealt round-robin.
+  // What depends only on the plan (step indices, column offsets, static
+  // joints) is decoded once per run of candidates sharing a plan (generator
+  // batches hold each topology's candidates together).
+  const int CH = chunk_items;
+  const unsigned nchunks = (unsigned)((nitems + CH - 1) / CH);  // la_simulate bounds the item count
+  int g_cur = -1;
+  bool bad_plan = false;
+  uint32_t tab = 0u;  // this lane's step: target | a << 8 | b << 16
+  SimCtx C;
+  C.n = 0;
+  C.ns = 0;
+  C.tau = p.fixup_tau;
+  unsigned chunk = blockIdx.x * SIM_WARPS + w;
+  while (chunk < nchunks) {
+  unsigned next = chunk + (unsigned)nwarps;
+  if (queue) {
+    // the ticket is taken now and first needed after this chunk
+    if (lane == 0) next = (unsigned)nwarps + atomicAdd(queue, 1u);
+    next = __shfl_sync(FULL, next, 0);
+  }
+  const long long base = (long long)chunk * CH;
+  const int cnt = nitems - base < CH ? (int)(nitems - base) : CH;
+  chunk = next;
+#pragma unroll 1
+  for (int k = 0; k < cnt; ++k) {
+    const long long item = base + k;
     const long long b = p.cand ? p.cand[item] : item;
     const int g = p.topo ? p.topo[b] : 0;
-    const la_plan* pl = p.plans + g;
-    SimCtx C;
-    C.n = pl->n;
-    C.ns = pl->nsteps;
-    C.tau = p.fixup_tau;
-    const uint32_t fixed = pl->fixed_mask | 1u;  // joint 0 is static (solver.py:183)
-    if (C.n > njmax || C.n < 2 || C.ns > NS || C.ns < 0) {
-      // plan does not fit the launch (n > pos_stride): flag, do not touch smem
+    const double* P0 = p.pos0 + (size_t)b * p.pos_stride * 2;
+    __syncwarp();  // every lane is past the previous candidate
+    if (lane < njmax) H.p0[lane] = make_double2(P0[2 * lane], P0[2 * lane + 1]);
+    if (g != g_cur) {
+      // plan-dependent state, kept across candidates of the same plan
+      g_cur = g;
+      const la_plan* pl = p.plans + g;
+      C.n = pl->n;
+      C.ns = pl->nsteps;
+      const uint32_t fixed = pl->fixed_mask | 1u;  // joint 0 is static (solver.py:183)
+      bad_plan = C.n > njmax || C.n < 2 || C.ns > NS || C.ns < 0;
+      if (!bad_plan) {
+        if (lane < C.ns) {
+          const uint32_t it_ = (uint8_t)pl->step[lane][0], ia_ = (uint8_t)pl->step[lane][1],
+                         ib_ = (uint8_t)pl->step[lane][2];
+          tab = it_ | (ia_ << 8) | (ib_ << 16);
+          H.tg[lane] = (int8_t)it_;
+          H.st64[lane].idx = tab;
+          // 8-byte slots: the parents' fp16 error offsets (a | b << 16); the
+          // 16-byte-slot screens keep their bound inside the slot; then the
+          // column offsets: slot (joint, lane) at (j * 32 + lane) * SLOT
+          *reinterpret_cast<uint4*>(&H.st[lane].pmask) =
+              make_uint4(SLOT == 8 ? ((uint32_t)ia_ * 64u) | ((uint32_t)ib_ * 64u << 16) : 0u,
+                         (uint32_t)ia_ * 32u * SLOT, (uint32_t)ib_ * 32u * SLOT, (uint32_t)it_ * 32u * SLOT);
+        }
+        // static joints (1 is the crank tip even if typed Fixed)
+        const bool is_static = lane < C.n && lane != 1 && ((fixed >> lane) & 1u);
+        const unsigned bal = __ballot_sync(FULL, is_static);
+        if (is_static) H.statics[__popc(bal & ((1u << lane) - 1u))] = (int8_t)lane;
+        if (lane == 0) H.nstatic = (int8_t)__popc(bal);
+      }
+    }
+    __syncwarp();
+    if (bad_plan) {
+      // plan does not fit the launch (n > pos_stride): flag only
       if (lane == 0) {
         if (p.first_t) p.first_t[item] = -1;
         if (p.first_joint) p.first_joint[item] = -2;
       }
       continue;
     }
-    const double* P0 = p.pos0 + (size_t)b * p.pos_stride * 2;
-    __syncwarp();
-    if (lane < C.n) H.p0[lane] = make_double2(P0[2 * lane], P0[2 * lane + 1]);
-    int it_ = 0, ia_ = 0, ib_ = 0;
-    if (lane < C.ns) {
-      it_ = (uint8_t)pl->step[lane][0];
-      ia_ = (uint8_t)pl->step[lane][1];
-      ib_ = (uint8_t)pl->step[lane][2];
-      H.tg[lane] = (int8_t)it_;
-    }
-    {
-      // static joints (1 is the crank tip even if typed Fixed)
-      const bool is_static = lane < C.n && lane != 1 && ((fixed >> lane) & 1u);
-      const unsigned bal = __ballot_sync(FULL, is_static);
-      if (is_static) H.statics[__popc(bal & ((1u << lane) - 1u))] = (int8_t)lane;
-      if (lane == 0) H.nstatic = (int8_t)__popc(bal);
-    }
-    __syncwarp();
     if (lane < C.ns) {
       // plan_geometry (solver.py:105-120), f64
-      const double2 pa = H.p0[ia_], pb = H.p0[ib_], pt = H.p0[it_];
+      const double2 pa = H.p0[(tab >> 8) & 0xffu], pb = H.p0[tab >> 16], pt = H.p0[tab & 0xffu];
       const double ax = dsub(pt.x, pa.x), ay = dsub(pt.y, pa.y);
       const double bx = dsub(pt.x, pb.x), by = dsub(pt.y, pb.y);
       // np.hypot bit for bit (glibc algorithm, common.cuh) in exact mode;
@@ -482,27 +552,20 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
       const double cross = dsub(dmul(dsub(pb.x, pa.x), dsub(pt.y, pa.y)),
                                 dmul(dsub(pb.y, pa.y), dsub(pt.x, pa.x)));
       const double br = cross >= 0.0 ? 1.0 : -1.0;
-      StepRec64 r64;
-      r64.idx = (uint32_t)it_ | ((uint32_t)ia_ << 8) | ((uint32_t)ib_ << 16);
-      r64._u = 0;
-      r64.hi = dadd(dadd(ra, rb), 1e-9);
-      r64.lo = dsub(fabs(dsub(ra, rb)), 1e-9);
-      r64.ra2 = dmul(ra, ra);
-      r64.rb2 = dmul(rb, rb);
+      StepRec64& r64 = H.st64[lane];  // idx stays (plan-dependent)
       r64.br = br;
-      H.st64[lane] = r64;
-      StepRec r;
-      r.sp = (float)(ra + rb);
-      r.df = (float)fabs(ra - rb);
-      r.c2 = (float)(ra * ra - rb * rb);
-      r.ra2 = br < 0.0 ? -((float)ra * (float)ra) : (float)ra * (float)ra;
-      // 8-byte slots: the parents' fp16 error offsets (a | b << 16); the
-      // 16-byte-slot screens keep their bound inside the slot
-      r.pmask = SLOT == 8 ? ((uint32_t)ia_ * 64u) | ((uint32_t)ib_ * 64u << 16) : 0u;
-      r.a_off = (uint32_t)ia_ * 32u * SLOT;  // slot (joint, lane) at (j * 32 + lane) * SLOT
-      r.b_off = (uint32_t)ib_ * 32u * SLOT;
-      r.t_off = (uint32_t)it_ * 32u * SLOT;
-      H.st[lane] = r;
+      const double hi = dadd(dadd(ra, rb), 1e-9), lo = dsub(fabs(dsub(ra, rb)), 1e-9);
+      if (EXACT) {
+        *reinterpret_cast<double2*>(&r64.hi) = make_double2(hi, lo);
+        *reinterpret_cast<double2*>(&r64.ra2) = make_double2(dmul(ra, ra), dmul(rb, rb));
+      } else {
+        // fast records (dyads_f64): squared thresholds, ra^2 and (ra^2 - rb^2) / 2
+        *reinterpret_cast<double2*>(&r64.hi) = make_double2(hi * hi, lo > 0.0 ? lo * lo : -1.0);
+        *reinterpret_cast<double2*>(&r64.ra2) = make_double2(ra * ra, 0.5 * (ra * ra - rb * rb));
+      }
+      *reinterpret_cast<float4*>(&H.st[lane].sp) =
+          make_float4((float)(ra + rb), (float)fabs(ra - rb), (float)(ra * ra - rb * rb),
+                      br < 0.0 ? -((float)ra * (float)ra) : (float)ra * (float)ra);
     }
     {
       // crank radius as np.hypot wherever paths are written or f64 is exact
@@ -665,6 +728,15 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
       n_angles += 32ull * rounds;
       n_dyads += 32ull * rounds * (unsigned long long)C.ns;
       ++n_cand;
+    }
+  }
+  }
+  if (queue && lane == 0) {
+    // leave the counters zeroed for the next launch that gets this slot
+    __threadfence();
+    if (atomicAdd(queue + 1, 1u) == (unsigned)nwarps - 1u) {
+      queue[0] = 0u;
+      queue[1] = 0u;
     }
   }
   if (COUNT && p.counters) {
@@ -887,6 +959,52 @@ __global__ void __launch_bounds__(CP_THREADS) select_kernel(const int32_t* __res
 
 using namespace la;
 
+// Work-queue counters of la_simulate's persistent launches: per device one
+// zeroed array of (ticket, done) pairs.  A launch takes the next pair of a
+// ring (its kernel leaves the pair zeroed, and the ring is far longer than
+// any number of launches in flight); a launch recorded into a CUDA graph
+// takes a pair of its own that is never handed out again (a graph may be
+// replayed at any time); when those run out, or the array cannot be
+// allocated, the launch falls back to the static round-robin schedule.
+namespace {
+constexpr unsigned Q_RING = 1u << 15, Q_CAPTURED = 1u << 15;
+struct QueuePool {
+  std::atomic<unsigned*> base{nullptr};
+  std::atomic<unsigned> ring{0}, captured{0};
+};
+unsigned* take_queue(cudaStream_t s) {
+  static QueuePool pools[64];
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  QueuePool& P = pools[dev];
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  unsigned* base = P.base.load(std::memory_order_acquire);
+  if (!base) {
+    if (cap != cudaStreamCaptureStatusNone) return nullptr;  // no allocation while a graph is being recorded
+    std::lock_guard<std::mutex> lock(mu);
+    base = P.base.load(std::memory_order_acquire);
+    if (!base) {
+      const size_t bytes = (size_t)(Q_RING + Q_CAPTURED) * 2 * sizeof(unsigned);
+      if (cudaMalloc(&base, bytes) != cudaSuccess || cudaMemset(base, 0, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      P.base.store(base, std::memory_order_release);
+    }
+  }
+  if (cap != cudaStreamCaptureStatusNone) {
+    const unsigned c = P.captured.fetch_add(1, std::memory_order_relaxed);
+    return c < Q_CAPTURED ? base + 2 * (size_t)(Q_RING + c) : nullptr;
+  }
+  return base + 2 * (size_t)(P.ring.fetch_add(1, std::memory_order_relaxed) % Q_RING);
+}
+}  // namespace
+
 extern "C" {
 
 int la_simulate(const la_sim_args* a, void* stream) {
@@ -902,6 +1020,7 @@ int la_simulate(const la_sim_args* a, void* stream) {
   if (write && !a->traj) return fail(LA_EINVAL, "la_simulate: WRITE_TRAJ without traj");
   const long long items = a->cand ? a->n_cand : a->B;
   if (a->B == 0 || items == 0) return 0;
+  if (items >= (1ll << 36)) return fail(LA_ERANGE, "la_simulate: more than 2^36 candidates in one launch");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool f64 = (a->flags & LA_SIM_FP64) != 0;
   const int njmax = a->pos_stride < NJ ? a->pos_stride : NJ;
@@ -920,7 +1039,7 @@ int la_simulate(const la_sim_args* a, void* stream) {
   if (wonly && !write) return fail(LA_EINVAL, "la_simulate: WRITE_ONLY needs WRITE_TRAJ");
   const bool exact = (a->flags & LA_SIM_EXACT64) != 0;
   if (!write && !f64 && (a->flags & LA_SIM_LANE_SCREEN)) return launch_screen_lane(*a, s);
-  using KernT = void (*)(const la_sim_args, int);
+  using KernT = void (*)(const la_sim_args, int, int, unsigned*);
   auto pick = [&](auto cnt) -> KernT {
     constexpr bool C = decltype(cnt)::value;
     // ERR4 only matters where the fp32 screen runs (not WONLY / FP64)
@@ -943,15 +1062,29 @@ int la_simulate(const la_sim_args* a, void* stream) {
   if (e != cudaSuccess) return fail((int)e, "la_simulate: occupancy: %s", cudaGetErrorString(e));
   const int sms = sm_count();
   if (sms <= 0) return fail(LA_EINVAL, "la_simulate: no device");
-  long long want = (items + SIM_WARPS - 1) / SIM_WARPS;
-  // four waves of resident CTAs: candidates differ widely in cost (early
-  // lock vs all T angles), and the hardware refills SMs with fresh CTAs as
-  // earlier ones finish (measured 1/2/4/8/16 waves: C2 step 0.310 / 0.298 /
-  // 0.290 / 0.298 / 0.310 ms)
-  long long grid = (long long)sms * (occ > 0 ? occ : 1) * 4;
+  // Persistent one-wave grid fed by a work queue (tickets of CH candidates:
+  // candidates differ widely in cost -- early lock vs all T angles -- and
+  // the queue keeps every warp busy until the batch is drained).  A ticket
+  // covers more candidates in larger batches (about LA_SIM_TICKETS tickets
+  // per resident warp), so consecutive candidates share their plan's decode
+  // and the ticket counter stays cold.  Without a queue: four waves of resident CTAs, chunks dealt
+  // round-robin (measured 1/2/4/8/16 waves: C2 step 0.310 / 0.298 / 0.290 /
+  // 0.298 / 0.310 ms).
+#ifdef LA_SIM_FORCE_STATIC
+  unsigned* queue = nullptr;
+#else
+  // (the write-only pass keeps the round-robin deal: its candidates cost
+  // about the same, measured 0.123 ms static vs 0.127 ms queued on C2)
+  unsigned* queue = ((a->flags & LA_SIM_STATIC_GRID) || wonly) ? nullptr : take_queue(s);
+#endif
+  const long long resident = (long long)sms * (occ > 0 ? occ : 1);
+  long long per = items / (resident * SIM_WARPS * LA_SIM_TICKETS);
+  const int chunk = (per < 1 || wonly) ? 1 : per > LA_SIM_CHUNK ? LA_SIM_CHUNK : (int)per;
+  const long long want = ((items + chunk - 1) / chunk + SIM_WARPS - 1) / SIM_WARPS;
+  long long grid = queue ? resident : resident * 4;
   if (grid > want) grid = want;
   const la_sim_args p = *a;
-  kern<<<(unsigned)grid, SIM_THREADS, smem, s>>>(p, njmax);
+  kern<<<(unsigned)grid, SIM_THREADS, smem, s>>>(p, njmax, chunk, queue);
   return cuda_status("la_simulate");
 }
 

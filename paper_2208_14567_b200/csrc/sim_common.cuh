@@ -37,6 +37,11 @@ __device__ __forceinline__ double2 lds_d2(uint32_t a) {
 __device__ __forceinline__ void sts_d2(uint32_t a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+// 8-byte asynchronous global -> shared copy (LDGSTS) and its completion
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -72,18 +77,23 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return y;
 }
 
-// f64 reciprocal square root: MUFU.RSQ64H seed + two Newton steps
-// (relative error ~1e-16; not correctly rounded, see dyads_f64)
+// f64 reciprocal square root and reciprocal: the MUFU seeds (RSQ64H / RCP64H,
+// relative error 1e-6 measured, tools/micro/f64_seeds.cu) refined by one
+// third-order step each -- Halley's y (1 + e/2 + 3 e^2/8), e = 1 - x y^2, and
+// y (1 + e + e^2), e = 1 - x y -- to 1 ulp (2.2e-16 measured; two Newton
+// steps give 2.6e-16 with two more DFMA).  Not correctly rounded, see
+// dyads_f64.
 __device__ __forceinline__ double rsqrt_f64(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const double e = fma(-h, y * y, 0.5);
-    y = fma(y, e, y);
-  }
-  return y;
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
+}
+__device__ __forceinline__ double rcp_f64(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y, 1.0);
+  return fma(y, fma(e, e, e), y);
 }
 
 // exact-mode triage of an f64 replay: a fast (DFMA, Newton rsqrt) pass
