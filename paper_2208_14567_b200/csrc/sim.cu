@@ -255,7 +255,11 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
     const float tau = C.tau;
     const uint32_t col = smem_u32(W.cols) + (uint32_t)W.lane * (uint32_t)W.slot;
     sts_f2(col + 32u * (uint32_t)W.slot, make_float2(fmaf(C.r1f, c.x, C.p0f.x), fmaf(C.r1f, c.y, C.p0f.y)));
-    int s = 0;
+    // step records walked by shared address; the lock step is recovered
+    // from the address when a lane leaves the loop
+    const uint32_t rec0 = smem_u32(&H.st[0]), rec_end = rec0 + (uint32_t)C.ns * (uint32_t)sizeof(StepRec);
+    uint32_t rec = rec0;
+    unsigned fixw = 0u;
     if (ERR4) {
       // each joint's 16-byte slot holds its fp32 position and a first-order
       // bound e on that position's error: static joints and the crank tip
@@ -263,9 +267,9 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
       //   e_t = max(kappa, 1) max(e_a, e_b) + kErrStep
       // (its parents' error amplified by the dyad, plus its own rounding)
 #pragma unroll 1
-      for (; s < C.ns; ++s) {
-        const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
-        const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].pmask);
+      for (; rec != rec_end; rec += (uint32_t)sizeof(StepRec)) {
+        const float4 g0 = lds_f4(rec);
+        const uint4 g1 = lds_u4(rec + 16u);
         const float4 pa = lds_f4(col + g1.y);
         const float4 pb = lds_f4(col + g1.z);
         const float dx = pb.x - pa.x, dy = pb.y - pa.y;
@@ -275,9 +279,9 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
         const float m = fminf(g0.x - d, d - g0.y);
         const float ep = fmaxf(pa.z, pb.z);
         // the margin moves by at most 2 ep (d from two parents) + rounding
-        fix |= !(fabsf(m) >= fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
+        flag_below(fixw, fabsf(m), fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
         if (m < 0.0f) {
-          lk = s;
+          lk = (int)((rec - rec0) / (uint32_t)sizeof(StepRec));
           break;
         }
         const float x = (d2 + g0.z) * (0.5f * inv);
@@ -292,8 +296,9 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
         const float e = fmaf(fmaxf(num * rcp_approx(h), 1.0f), ep, kErrStep);
         const float xi = x * inv;
         const float hb = copysignf(h, g0.w) * inv;
+        // (the slot's fourth word is never read)
         sts_f4(col + g1.w,
-               make_float4(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)), e, 0.f));
+               make_float4(fmaf(-hb, dy, fmaf(xi, dx, pa.x)), fmaf(hb, dx, fmaf(xi, dy, pa.y)), e, e));
       }
     } else {
       // large mechanisms (8-byte slots keep three CTAs per SM): the same
@@ -302,9 +307,9 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
       // a [joint][lane] array after the position columns
       const uint32_t ecol = smem_u32(W.cols) + (uint32_t)W.ecol_off + (uint32_t)W.lane * 2u;
 #pragma unroll 1
-      for (; s < C.ns; ++s) {
-        const float4 g0 = *reinterpret_cast<const float4*>(&H.st[s].sp);
-        const uint4 g1 = *reinterpret_cast<const uint4*>(&H.st[s].pmask);
+      for (; rec != rec_end; rec += (uint32_t)sizeof(StepRec)) {
+        const float4 g0 = lds_f4(rec);
+        const uint4 g1 = lds_u4(rec + 16u);
         const float2 pa = lds_f2(col + g1.y);
         const float2 pb = lds_f2(col + g1.z);
         const float dx = pb.x - pa.x, dy = pb.y - pa.y;
@@ -314,9 +319,9 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
         const float m = fminf(g0.x - d, d - g0.y);
         // pmask holds the parents' error offsets (a | b << 16)
         const float ep = fmaxf(lds_h16(ecol + (g1.x & 0xffffu)), lds_h16(ecol + (g1.x >> 16)));
-        fix |= !(fabsf(m) >= fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
+        flag_below(fixw, fabsf(m), fmaf(kMarginK, ep, tau));  // NaN -> f64 decides
         if (m < 0.0f) {
-          lk = s;
+          lk = (int)((rec - rec0) / (uint32_t)sizeof(StepRec));
           break;
         }
         const float x = (d2 + g0.z) * (0.5f * inv);
@@ -330,6 +335,8 @@ __device__ __forceinline__ int solve32(const Warp& W, const SimCtx& C, const dou
         sts_h16(ecol + (g1.w >> 2), e);
       }
     }
+    fix = fixw != 0u;
+    const int s = (int)((rec - rec0) / (uint32_t)sizeof(StepRec));
   if (COUNT) {
       ++ctr.lane_angles;
       ctr.lane_dyads += (unsigned)(s < C.ns ? s + 1 : C.ns);
@@ -478,18 +485,14 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
   C.tau = p.fixup_tau;
   unsigned chunk = blockIdx.x * SIM_WARPS + w;
   while (chunk < nchunks) {
+  // the next ticket is taken now by lane 0 and broadcast after this chunk,
+  // so the atomic's round trip runs under the chunk's work
   unsigned next = chunk + (unsigned)nwarps;
-  if (queue) {
-    // the ticket is taken now and first needed after this chunk
-    if (lane == 0) next = (unsigned)nwarps + atomicAdd(queue, 1u);
-    next = __shfl_sync(FULL, next, 0);
-  }
-  const long long base = (long long)chunk * CH;
-  const int cnt = nitems - base < CH ? (int)(nitems - base) : CH;
-  chunk = next;
+  if (queue && lane == 0) next = (unsigned)nwarps + atomicAdd(queue, 1u);
+  // (la_simulate bounds the item count by 2^31)
+  const unsigned item_end = min(chunk * (unsigned)CH + (unsigned)CH, (unsigned)nitems);
 #pragma unroll 1
-  for (int k = 0; k < cnt; ++k) {
-    const long long item = base + k;
+  for (unsigned item = chunk * (unsigned)CH; item < item_end; ++item) {
     const long long b = p.cand ? p.cand[item] : item;
     const int g = p.topo ? p.topo[b] : 0;
     const double* P0 = p.pos0 + (size_t)b * p.pos_stride * 2;
@@ -730,6 +733,7 @@ __global__ void __launch_bounds__(SIM_THREADS, LA_SIM_MINB) sim_kernel(const la_
       ++n_cand;
     }
   }
+  chunk = queue ? __shfl_sync(FULL, next, 0) : next;
   }
   if (queue && lane == 0) {
     // leave the counters zeroed for the next launch that gets this slot
@@ -1020,7 +1024,7 @@ int la_simulate(const la_sim_args* a, void* stream) {
   if (write && !a->traj) return fail(LA_EINVAL, "la_simulate: WRITE_TRAJ without traj");
   const long long items = a->cand ? a->n_cand : a->B;
   if (a->B == 0 || items == 0) return 0;
-  if (items >= (1ll << 36)) return fail(LA_ERANGE, "la_simulate: more than 2^36 candidates in one launch");
+  if (items >= (1ll << 31)) return fail(LA_ERANGE, "la_simulate: more than 2^31 candidates in one launch");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool f64 = (a->flags & LA_SIM_FP64) != 0;
   const int njmax = a->pos_stride < NJ ? a->pos_stride : NJ;

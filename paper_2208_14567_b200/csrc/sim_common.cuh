@@ -29,6 +29,15 @@ __device__ __forceinline__ void sts_f4(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+// flag = 1 unless v >= bound (so a NaN sets it): one FSETP and a predicated move
+__device__ __forceinline__ void flag_below(unsigned& flag, float v, float bound) {
+  asm("{\n\t.reg .pred p;\n\tsetp.ltu.f32 p, %1, %2;\n\t@p mov.u32 %0, 1;\n\t}" : "+r"(flag) : "f"(v), "f"(bound));
+}
 __device__ __forceinline__ double2 lds_d2(uint32_t a) {
   double2 v;
   asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");

@@ -655,3 +655,44 @@ def test_split_rows_layout(torch):
         assert np.array_equal(assemble_paths(A, int(tr[i]), mb.pos[b, :plan.n], plan.n, targets, 200), full)
         checked += 1
     assert checked > 500
+
+
+def test_work_queue_schedule(torch):
+    """The persistent grid's work queue (tickets of consecutive candidates)
+    only changes which warp replays which candidate: flags, low-fidelity
+    flags and paths equal the round-robin schedule (LA_SIM_STATIC_GRID) bit
+    for bit, at sizes below one ticket per warp, around the chunking
+    thresholds and with many tickets per warp; repeated launches on two
+    streams (each takes its own counter pair, left zeroed by its kernel) keep
+    returning the same answer."""
+    from paper_2208_14567_b200 import _native as N
+    from paper_2208_14567_b200.solver import simulate_tensors
+    from paper_2208_14567_b200.workloads import native_batch
+
+    nb = native_batch(400_000, 5, 20, seed=77)
+    pos_all = torch.from_numpy(nb.pos).cuda()
+    topo_all = torch.from_numpy(nb.topo).cuda()
+    for count in (1, 33, 4_736, 40_001, 400_000):
+        pos, topo = pos_all[:count], topo_all[:count]
+        for kw in ({"write_traj": False}, {"write_traj": False, "gate_only": True, "low": True},
+                   {"write_traj": True} if count <= 40_001 else None):
+            if kw is None:
+                continue
+            # (zeroed path buffers: padding rows and the rows of locked
+            # candidates past their first lock are not written)
+            bufs = [dict(traj=torch.zeros((count * nb.table.max_n, 200, 2), dtype=torch.float32, device="cuda"))
+                    if kw["write_traj"] else {} for _ in range(2)]
+            ref = simulate_tensors(pos, nb.table, 200, topo, _extra_flags=N.LA_SIM_STATIC_GRID, **kw, **bufs[0])
+            res = simulate_tensors(pos, nb.table, 200, topo, **kw, **bufs[1])
+            for key in ref:
+                assert torch.equal(ref[key], res[key]), (count, kw, key)
+    pos, topo = pos_all[:100_000], topo_all[:100_000]
+    ref = simulate_tensors(pos, nb.table, 200, topo, write_traj=False, _extra_flags=N.LA_SIM_STATIC_GRID)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for i in range(40):
+        with torch.cuda.stream(streams[i % 2]):
+            outs.append(simulate_tensors(pos, nb.table, 200, topo, write_traj=False, stream=streams[i % 2]))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o["first_t"], ref["first_t"]) and torch.equal(o["first_joint"], ref["first_joint"])
