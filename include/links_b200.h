@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define LA_ABI_VERSION 2
+#define LA_ABI_VERSION 3
 #define LA_MAX_JOINTS 20   /* joints per mechanism (generator.py n_max default) */
 #define LA_MAX_STEPS 18    /* dyad steps per plan: n - |fixed| - 1 <= 18       */
 #define LA_MAX_TOPK 32
@@ -229,6 +229,7 @@ int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P,
 #define LA_CH_NO_MQ 64u      /* pruned scan with NQ >= 2: one CTA set per query
                                 instead of the multi-query kernel (groups of
                                 queries share each streamed curve)           */
+#define LA_CH_NO_INDEX 256u  /* ignore la_chamfer_args.cells                  */
 #define LA_CH_MQ_FINE 128u   /* multi-query kernel: 64x64 common grid for the
                                 stage-0 bound instead of 32x32               */
 
@@ -265,7 +266,22 @@ typedef struct la_chamfer_args {
                                  box/gap-table column term, common-grid row
                                  term, 4-corner row term, 50-point and
                                  10-point run-box column terms               */
+  const uint16_t* cells;      /* (device, optional) [N][LA_INDEX_ROW(P)] cell index of db from
+                                 la_chamfer_index: single-query pruned scans
+                                 first bound every curve from its 2-byte
+                                 cells against the k-th best of a seed scan
+                                 and scan only the survivors (same lists);
+                                 n_stage[0] += survivors                     */
 } la_chamfer_args;
+
+#define LA_INDEX_ROW(P) (((P) + 15) & ~15) /* cells per index row (32-byte sectors) */
+/* Cell index of a curve database for la_chamfer_args.cells: cells[i][j] =
+ * cell of point j of curve i on the fixed 64 x 64 grid over the unit square
+ * padded by 1/32 (outside points clamp into the border cells), numbered
+ * ix * 66 + iy (table rows padded against bank conflicts); entries j >= P
+ * of a row hold the null cell 64.  cells: [N][LA_INDEX_ROW(P)].  Built once
+ * per database (Atlas build / load); 2 bytes per point.                      */
+int la_chamfer_index(const float* db, int64_t N, int32_t P, uint16_t* cells, void* stream);
 
 size_t la_chamfer_workspace(const la_chamfer_args* args);
 int la_chamfer_topk(const la_chamfer_args* args, void* stream);

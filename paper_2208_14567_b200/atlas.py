@@ -52,8 +52,14 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
                  exclude_id: int = -1, dense: bool = False, all_d=None, expansion: bool = False,
                  fix_tol: float = 5e-5, scalar_pipe: bool = False, tensor: bool = False, prune: bool = True,
                  seed_scan: bool = False, multi_query: bool = True, mq_fine: bool = False,
-                 stream=None) -> dict:
+                 cells=None, stream=None) -> dict:
     """One la_chamfer_topk launch.
+
+    ``cells`` (uint16 rows from ``chamfer_index(db)``; single-query pruned
+    scans): every curve is first bounded from its 2-byte cell row against the
+    k-th best of a seed scan over a 1/64 prefix, and only the survivors'
+    points are streamed; the lists are identical to the scan without it
+    (``n_stage[0]`` counts the survivors).
 
     ``prune`` (top-k scans of >= 65,536 positions without dense output):
     curves whose lower bound (query distance grid, first chamfer term)
@@ -129,12 +135,32 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     a.fixup_below = float(fix_tol)
     a.n_full = out["n_full"].data_ptr()
     a.n_stage = out["n_stage"].data_ptr()
+    if cells is not None:
+        if cells.dtype != torch.uint16 or tuple(cells.shape) != (Nn, (P + 15) & ~15) or not cells.is_cuda:
+            raise ValueError("cells must be the (N, P rounded up to 16) uint16 CUDA tensor of chamfer_index(db)")
+        cells = cells.contiguous()
+    a.cells = N.ptr(cells)
     wsb = int(lib.la_chamfer_workspace(a))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     a.ws, a.ws_bytes = ws.data_ptr(), wsb
     N.check(lib.la_chamfer_topk(a, N.stream_ptr(stream)), "la_chamfer_topk")
     out["_ws"] = ws  # keep alive until the stream consumes it
     return out
+
+
+def chamfer_index(db, stream=None):
+    """Cell index of a curve database (la_chamfer_index): (N, P rounded up to
+    16) uint16, the 64 x 64 grid cell of every point (row padding: the null
+    cell); pass it to ``chamfer_scan(cells=...)``."""
+    torch = N.require_cuda()
+    lib = N.load()
+    if db.dtype != torch.float32 or db.dim() != 3 or db.shape[2] != 2 or not db.is_cuda:
+        raise ValueError("db must be a (N, P, 2) float32 CUDA tensor")
+    db = db.contiguous()
+    cells = torch.empty((db.shape[0], (db.shape[1] + 15) & ~15), dtype=torch.uint16, device=db.device)
+    N.check(lib.la_chamfer_index(db.data_ptr(), db.shape[0], db.shape[1], cells.data_ptr(), N.stream_ptr(stream)),
+            "la_chamfer_index")
+    return cells
 
 
 _EDGES = np.linspace(0.0, 0.75, 17)  # np.histogram(bins=16, range=(0, .75)) edges (atlas.py:169)
@@ -305,6 +331,12 @@ class Atlas:
             self._dev = torch.from_numpy(self.points.astype(np.float32)).cuda()
         return self._dev
 
+    def device_cells(self):
+        """Cell index of the device curves (built once, chamfer_index)."""
+        if getattr(self, "_cells_dev", None) is None:
+            self._cells_dev = chamfer_index(self.device_points())
+        return self._cells_dev
+
     def exact_index(self, query: np.ndarray) -> int | None:
         """Index of the LAST stored curve byte-identical to ``query``
         (the dict comprehension of atlas.py:78-80 keeps the last)."""
@@ -372,7 +404,8 @@ class Atlas:
         db = self.device_points()
         res = chamfer_scan(db, torch.from_numpy(query.astype(np.float32)).cuda()[None],
                            k=int(k), threshold=threshold, order=scan,
-                           pos_end=int(scan.numel()), exclude_id=-1 if self_idx is None else int(self_idx))
+                           pos_end=int(scan.numel()), exclude_id=-1 if self_idx is None else int(self_idx),
+                           cells=self.device_cells() if scan.numel() >= (1 << 16) else None)
         host = {n: res[n][0].cpu().numpy() for n in ("hit_d", "hit_id", "top_d", "top_id")}
         rows = assemble_hits(host["hit_d"], host["hit_id"], host["top_d"], host["top_id"], int(k), threshold,
                              self_idx)

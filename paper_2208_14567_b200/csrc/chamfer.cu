@@ -158,6 +158,9 @@ struct ScanCtx {
   unsigned* slots;      // [NQ][32] float bits: min d of the evaluated non-hits with id % 32 == slot
   int prune;
   float lb_slack;       // absolute slack subtracted from a curve's bound
+  // indexed scans: number of scan positions actually present (the survivor
+  // list's device-side count), or NULL: [pos_begin, pos_end)
+  const long long* pos_count;
 };
 
 __device__ __forceinline__ void consider(WarpList& top, WarpList& hit, long long& nhit, const ScanCtx& c,
@@ -574,6 +577,168 @@ __global__ void thr_init_kernel(const float* __restrict__ seed_d, int k, int NQ,
   for (int j = 0; j < 32; ++j) slots[(size_t)qi * 32 + j] = __float_as_uint(INFINITY);
 }
 
+// ------------------------------------------------------------ cell index
+// The cheapest bound of the scan (curve_row_bound_cell: every database point
+// a lies in grid cell c(a), and min_q |a - q| >= CT(c) = distance from the
+// query to c's box) only needs each point's CELL.  la_chamfer_index stores
+// the cells of every database point once, on a fixed 64 x 64 grid over the
+// unit square padded by 1/32 (the frame of normalised curves; points outside
+// clamp into the border cells, whose boxes are open toward infinity): 2 bytes
+// per point instead of 8.  An indexed scan then runs in three steps:
+//   seed   the pruned scan over a 1/64 prefix; its k-th best distance t0
+//          bounds the final k-th best from above;
+//   bound  every curve's cell row against the query's cell table (one u16
+//          table load and an integer add per point, 400 bytes per curve
+//          streamed): curves whose bound exceeds max(t0, threshold) can be
+//          neither hits nor in the top k;
+//   scan   the pruned scan over the ordered list of the others (running
+//          bound, later stages, full evaluation as before), which reports
+//          their original scan positions.
+// Lists identical to the scan without an index: the bound is the first
+// stage's (same slack rule), only taken against t0 instead of the running
+// bound.
+__device__ __forceinline__ unsigned lds_u16i(uint32_t a) {
+  unsigned short h;
+  asm("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
+  return h;
+}
+// table rows padded to 66 entries: cell (ix, iy) at ix * 66 + iy, so that
+// neighbouring cells in x fall into neighbouring shared-memory banks (with a
+// stride of 64 two-byte entries a horizontal run of a curve -- the same iy
+// in every lane -- would hit one bank 32 ways)
+constexpr int IDX_STRIDE = LBG + 2;
+constexpr int IDX_TAB = LBG * IDX_STRIDE;  // table entries (8,448 bytes)
+constexpr unsigned IDX_NULL = LBG;         // a padding slot of row 0: table value 0 (row padding cells)
+// cells per index row: P rounded up to 16 (whole 32-byte sectors per curve)
+__host__ __device__ constexpr int idx_row(int P) { return (P + 15) & ~15; }
+constexpr float IDX_LO = -1.f / 32.f;
+constexpr float IDX_CELL = (1.f + 2.f / 32.f) / (float)LBG;  // 17 / 1024, exact
+constexpr float IDX_INV = 1.f / IDX_CELL;
+
+__device__ __forceinline__ unsigned idx_cell(float2 a) {
+  const unsigned ix = min(__float2uint_rd(fmaf(a.x, IDX_INV, -IDX_LO * IDX_INV)), (unsigned)(LBG - 1));
+  const unsigned iy = min(__float2uint_rd(fmaf(a.y, IDX_INV, -IDX_LO * IDX_INV)), (unsigned)(LBG - 1));
+  return ix * IDX_STRIDE + iy;
+}
+
+__global__ void __launch_bounds__(256) index_kernel(const float2* __restrict__ db, long long N, int P,
+                                                    unsigned short* __restrict__ cells) {
+  const int Pp = idx_row(P);
+  const long long n = N * Pp;
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const long long r = i / Pp;
+    const int j = (int)(i - r * Pp);
+    cells[i] = j < P ? (unsigned short)idx_cell(db[r * P + j]) : (unsigned short)IDX_NULL;
+  }
+}
+
+// the query's cell table on the index grid: floor(2^14 x distance from the
+// query to the cell's box), boxes widened by 1e-6 (rounding of idx_cell),
+// border cells open, the distance rounded down as in lb_grid_kernel.
+// grid ceil(IDX_TAB / 256), 256 threads.
+__global__ void __launch_bounds__(256) index_table_kernel(const float* __restrict__ query, int Q,
+                                                          unsigned short* __restrict__ table) {
+  __shared__ float2 sq[256];
+  const float2* q = reinterpret_cast<const float2*>(query);
+  const int v = blockIdx.x * 256 + threadIdx.x;  // table slot
+  const int cxi = min(v / IDX_STRIDE, LBG - 1), cyi = min(v % IDX_STRIDE, LBG - 1);
+  const float bx0 = cxi == 0 ? -INFINITY : __fmaf_rn((float)cxi, IDX_CELL, IDX_LO) - 1e-6f;
+  const float bx1 = cxi == LBG - 1 ? INFINITY : __fmaf_rn((float)(cxi + 1), IDX_CELL, IDX_LO) + 1e-6f;
+  const float by0 = cyi == 0 ? -INFINITY : __fmaf_rn((float)cyi, IDX_CELL, IDX_LO) - 1e-6f;
+  const float by1 = cyi == LBG - 1 ? INFINITY : __fmaf_rn((float)(cyi + 1), IDX_CELL, IDX_LO) + 1e-6f;
+  float mc = INFINITY;
+  for (int b = 0; b < Q; b += 256) {
+    __syncthreads();
+    if (b + threadIdx.x < Q) sq[threadIdx.x] = q[b + threadIdx.x];
+    __syncthreads();
+    const int e = min(256, Q - b);
+    for (int j = 0; j < e; ++j) {
+      const float ex = fmaxf(fmaxf(bx0 - sq[j].x, sq[j].x - bx1), 0.f);
+      const float ey = fmaxf(fmaxf(by0 - sq[j].y, sq[j].y - by1), 0.f);
+      mc = fminf(mc, __fmaf_rn(ey, ey, ex * ex));
+    }
+  }
+  const float dc = fmaxf(sqrtf(mc) * (1.f - 1e-6f) - 1e-6f, 0.f);
+  // padding slots (iy >= LBG) hold 0: IDX_NULL, the cell of row padding, adds nothing
+  if (v < IDX_TAB)
+    table[v] = v % IDX_STRIDE >= LBG ? (unsigned short)0
+                                     : (unsigned short)min(__float2uint_rd(dc * (float)LB_CELL_ONE), 65535u);
+}
+
+// bound step: one THREAD per curve (no warp reduction, ~4 instructions per
+// point; a warp per curve measured 3.2 ms per 10M curves against 1.45 ms).
+// A curve that is not pruned is
+// appended (one atomic per warp) to the survivor list as (record, reported
+// scan position); the list's order does not matter: the scan's lists are
+// keyed by (distance, position) and its hit lists by position.
+constexpr int IB_T = 256;
+__global__ void __launch_bounds__(IB_T) index_bound_kernel(const unsigned short* __restrict__ cells, int P,
+                                                           const int64_t* __restrict__ order,
+                                                           const int64_t* __restrict__ pos_map, long long pos_begin,
+                                                           long long pos_base, long long npos,
+                                                           const unsigned short* __restrict__ table,
+                                                           const unsigned* __restrict__ thr, float threshold,
+                                                           float lb_slack, int64_t* __restrict__ order2,
+                                                           int64_t* __restrict__ pos_map2,
+                                                           unsigned long long* __restrict__ count) {
+  __shared__ unsigned short tab[IDX_TAB];
+  for (int i = threadIdx.x; i < IDX_TAB / 2; i += IB_T)
+    reinterpret_cast<unsigned*>(tab)[i] = reinterpret_cast<const unsigned*>(table)[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const float t = fmaxf(__uint_as_float(*thr), threshold);
+  const float scale = 1.f / (LB_CELL_ONE * (float)P);
+  const uint32_t tab_s = smem_u32(tab);
+  auto look = [&](unsigned c) -> unsigned { return lds_u16i(tab_s + 2u * c); };
+  auto rec_of = [&](long long i) -> long long { return order ? order[pos_begin + i] : pos_begin + i; };
+  // the warp's kept curves (lane l: relative position i, record rec) are appended together
+  auto append = [&](bool keep, long long i, long long rec) {
+    const unsigned mask = __ballot_sync(FULL, keep);
+    if (!mask) return;
+    unsigned long long base = 0ull;
+    if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(mask));
+    base = __shfl_sync(FULL, base, 0);
+    if (keep) {
+      const long long at = (long long)base + __popc(mask & ((1u << lane) - 1u));
+      const long long pos = pos_begin + i;
+      order2[at] = rec;
+      pos_map2[at] = pos_map ? pos_map[pos] : pos + pos_base;
+    }
+  };
+  // one THREAD per curve: its row as whole 32-byte sectors (padding cells
+  // are IDX_NULL, table value 0)
+  const int Pp = idx_row(P);
+  const int W = Pp / 16;  // sectors per curve
+  const long long nth = (long long)gridDim.x * IB_T;
+  for (long long i0 = (long long)blockIdx.x * IB_T + (threadIdx.x & ~31); i0 < npos; i0 += nth) {
+    const long long i = i0 + lane;
+    const bool live = i < npos;
+    const long long rec = live ? rec_of(i) : 0;
+    const uint4* row = reinterpret_cast<const uint4*>(cells + (size_t)rec * Pp);
+    unsigned s0 = 0u, s1 = 0u;
+    if (live) {
+#pragma unroll 2
+      for (int k = 0; k < W; ++k) {
+        uint4 v, u;  // one 32-byte sector (LDG.256; two 16-byte loads fetched every sector twice)
+        asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w), "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                     : "l"(row + 2 * k));
+        s0 += look(v.x & 0xffffu) + look(v.y & 0xffffu) + look(v.z & 0xffffu) + look(v.w & 0xffffu);
+        s1 += look(v.x >> 16) + look(v.y >> 16) + look(v.z >> 16) + look(v.w >> 16);
+        s0 += look(u.x & 0xffffu) + look(u.y & 0xffffu) + look(u.z & 0xffffu) + look(u.w & 0xffffu);
+        s1 += look(u.x >> 16) + look(u.y >> 16) + look(u.z >> 16) + look(u.w >> 16);
+        // the terms are >= 0: once a partial sum prunes, so does the total
+        if (fmaf((float)(s0 + s1) * scale, 1.f - 1e-4f, -lb_slack) > t) break;
+      }
+    }
+    append(live && !(fmaf((float)(s0 + s1) * scale, 1.f - 1e-4f, -lb_slack) > t), i, rec);
+  }
+}
+
+__global__ void index_count_kernel(const long long* __restrict__ count, int64_t* __restrict__ n_stage) {
+  n_stage[0] += *count;  // curves surviving the bound step
+}
+
 // A fully evaluated non-hit with d below thr: lower its slot (id % 32) and,
 // when that changed the slot, publish the k-th smallest slot minimum.  The
 // 32 slot minima are distances of 32 distinct evaluated records, so their
@@ -766,7 +931,9 @@ __global__ void __launch_bounds__(CT, LA_CH_MINB) chamfer_scan_kernel(const Scan
   const float lb_slack = c.lb_slack;
 
   const long long first = A.pos_begin + gw;
-  const long long count = first < A.pos_end ? (A.pos_end - first + stride - 1) / stride : 0;
+  long long pos_end = A.pos_end;
+  if (c.pos_count) pos_end = min(pos_end, A.pos_begin + *c.pos_count);
+  const long long count = first < pos_end ? (pos_end - first + stride - 1) / stride : 0;
   const bool use_tma = (P % 2) == 0;
   const uint32_t bytes = (uint32_t)P * 8u;
   const int Ppad = (P + 31) & ~31;
@@ -2087,6 +2254,8 @@ struct Plan {
   long long seed_end;
   int seed_grid;
   size_t ws_prune; // bytes of the pruning area
+  bool index;      // indexed scan (cells given, one query): seed, bound step, scan of the survivors
+  size_t ws_index;
   // multi-query kernel (pruned, NQ >= 2)
   bool mq;
   int mq_g0;       // common grid cells per axis (32 or 64)
@@ -2126,6 +2295,8 @@ int scan_occupancy(int qs) {
   cache[dev][qs].store(occ, std::memory_order_relaxed);
   return occ;
 }
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 Plan make_plan(const la_chamfer_args* a) {
   Plan p{};
@@ -2168,7 +2339,8 @@ Plan make_plan(const la_chamfer_args* a) {
     // optional seed scan (LA_CH_SEED_SCAN): the exact k-th of a 1/128
     // prefix published before the main scan; off by default (the slot
     // minima converge within the first wave and measured faster)
-    const long long seed_div = (a->flags & LA_CH_SEED_SCAN) ? 128 : 0;
+    p.index = a->cells != nullptr && a->NQ == 1 && !(a->flags & LA_CH_NO_INDEX);
+    const long long seed_div = p.index ? 64 : (a->flags & LA_CH_SEED_SCAN) ? 128 : 0;
     long long sn = seed_div > 0 ? npos / seed_div : 0;
     if (seed_div > 0 && sn < 64LL * a->k) sn = 64LL * a->k;
     if (sn > npos) sn = npos;
@@ -2179,6 +2351,11 @@ Plan make_plan(const la_chamfer_args* a) {
     p.seed_grid = (int)sg;
     p.ws_prune = (size_t)a->NQ * (LB_DT_BYTES + 8 * sizeof(float) + 33 * sizeof(unsigned)) + 16 +
                  (size_t)a->NQ * a->k * 2 * (sizeof(float) + 2 * sizeof(long long)) + 256;
+    if (p.index) {
+      // cell table, the survivors' records and reported positions, their count
+      p.ws_index = align_up((size_t)IDX_TAB * sizeof(unsigned short)) +
+                   2 * align_up((size_t)npos * sizeof(long long)) + 256;
+    }
     p.mq = a->NQ >= 2 && !(a->flags & LA_CH_NO_MQ) && (a->P % 2) == 0;
     if (p.mq) {
       p.mq_g0 = (a->flags & LA_CH_MQ_FINE) ? 64 : 32;
@@ -2207,8 +2384,6 @@ Plan make_plan(const la_chamfer_args* a) {
   return p;
 }
 
-size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
-
 }  // namespace
 }  // namespace la
 
@@ -2231,7 +2406,20 @@ int la_merge_shard_lists(const int64_t* gathered, int32_t world, int32_t NQ, int
 size_t la_chamfer_workspace(const la_chamfer_args* a) {
   if (!a) return 0;
   const Plan p = make_plan(a);
-  return align_up(p.ws_lists) + align_up(p.ws_dense) + align_up(p.ws_prune) + 1024;
+  return align_up(p.ws_lists) + align_up(p.ws_dense) + align_up(p.ws_prune) + align_up(p.ws_index) + 1024;
+}
+
+int la_chamfer_index(const float* db, int64_t N, int32_t P, uint16_t* cells, void* stream) {
+  if (N < 0 || P < 1 || !db || !cells) return fail(LA_EINVAL, "la_chamfer_index: bad args");
+  if (N == 0) return 0;
+  const long long n = (long long)N * idx_row(P);
+  int sms = sm_count();
+  if (sms <= 0) sms = 148;
+  long long g = (n + 255) / 256;
+  if (g > (long long)sms * 16) g = (long long)sms * 16;
+  index_kernel<<<(unsigned)g, 256, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const float2*>(db), N, P,
+                                                                           cells);
+  return cuda_status("la_chamfer_index");
 }
 
 int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
@@ -2319,27 +2507,67 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
       int64_t* sp = reinterpret_cast<int64_t*>(pw);  // top_id, top_pos, hit_id, hit_pos
       float* sd = reinterpret_cast<float*>(sp + 4 * nk); // top_d, hit_d
       lb_grid_kernel<<<dim3((LBV * LBV + 255) / 256, a->NQ), 256, 0, s>>>(a->queries, a->Q, dt, par);
-      // optional seed: plain scan of a prefix, merged; its k-th best starts thr
-      float* seed_kth = nullptr;
-      if (p.seed_end > a->pos_begin) {
-        ScanCtx sc = c;
-        sc.a.pos_end = p.seed_end;
-        sc.a.n_hits = nullptr;
-        sc.a.n_full = nullptr;
-        sc.a.top_id = sp; sc.a.top_pos = sp + nk; sc.a.hit_id = sp + 2 * nk; sc.a.hit_pos = sp + 3 * nk;
-        sc.a.top_d = sd; sc.a.hit_d = sd + nk;
-        sc.nwarps_total = p.seed_grid;  // one list per CTA (cta_flush_lists)
-        if (int e = scan(sc, dim3(p.seed_grid, a->NQ))) return e;
-        merge_kernel<<<a->NQ, 1024, 0, s>>>(sc);
-        seed_kth = sd;
-      }
-      thr_init_kernel<<<(a->NQ + 255) / 256, 256, 0, s>>>(seed_kth, a->k, a->NQ, thr, slots);
       c.slots = slots;
       c.lb_dt = dt;
       c.lb_par = par;
       c.thr = thr;
-      c.prune = 1;
       c.lb_slack = 4e-6f + ((a->flags & LA_CH_EXPANSION) ? a->fixup_below : 0.f);
+      if (p.index) {
+        // seed: the pruned scan over the prefix, only for its running bound
+        // (k-th smallest of the slot minima: an upper bound of the final
+        // k-th best; its lists are not needed -- the bound step looks at
+        // every position again)
+        const long long npos = a->pos_end - a->pos_begin;
+        thr_init_kernel<<<1, 32, 0, s>>>(nullptr, a->k, a->NQ, thr, slots);
+        ScanCtx sc = c;
+        sc.prune = 1;
+        sc.a.pos_end = p.seed_end;
+        sc.a.n_hits = nullptr;
+        sc.a.n_full = nullptr;
+        sc.nwarps_total = p.seed_grid;
+        if (int e = scan(sc, dim3(p.seed_grid, 1))) return e;
+        // bound step against that bound; survivors appended to (order2,
+        // pos_map2), counted on the device; then the pruned scan over them
+        unsigned char* iw = static_cast<unsigned char*>(a->ws) + align_up(p.ws_lists) + align_up(p.ws_dense) +
+                            align_up(p.ws_prune);
+        unsigned short* table = reinterpret_cast<unsigned short*>(iw); iw += align_up((size_t)IDX_TAB * 2);
+        int64_t* order2 = reinterpret_cast<int64_t*>(iw); iw += align_up((size_t)npos * sizeof(long long));
+        int64_t* pmap2 = reinterpret_cast<int64_t*>(iw); iw += align_up((size_t)npos * sizeof(long long));
+        long long* cnt = reinterpret_cast<long long*>(iw); iw += 256;
+        int sms = sm_count();
+        if (sms <= 0) sms = 148;
+        cudaMemsetAsync(cnt, 0, sizeof(long long), s);
+        index_table_kernel<<<(IDX_TAB + 255) / 256, 256, 0, s>>>(a->queries, a->Q, table);
+        long long bg = (npos + IB_T - 1) / IB_T;
+        if (bg > (long long)sms * 8) bg = (long long)sms * 8;
+        index_bound_kernel<<<(unsigned)bg, IB_T, 0, s>>>(a->cells, a->P, a->order, a->pos_map, a->pos_begin,
+                                                         a->pos_base, npos, table, thr, a->threshold, c.lb_slack,
+                                                         order2, pmap2, reinterpret_cast<unsigned long long*>(cnt));
+        c.a.order = order2;
+        c.a.pos_map = pmap2;
+        c.a.pos_begin = 0;
+        c.a.pos_end = npos;
+        c.pos_count = cnt;
+        c.prune = 1;
+        if (a->n_stage) index_count_kernel<<<1, 1, 0, s>>>(cnt, a->n_stage);
+      } else {
+        // optional seed: plain scan of a prefix, merged; its k-th best starts thr
+        float* seed_kth = nullptr;
+        if (p.seed_end > a->pos_begin) {
+          ScanCtx sc = c;
+          sc.a.pos_end = p.seed_end;
+          sc.a.n_hits = nullptr;
+          sc.a.n_full = nullptr;
+          sc.a.top_id = sp; sc.a.top_pos = sp + nk; sc.a.hit_id = sp + 2 * nk; sc.a.hit_pos = sp + 3 * nk;
+          sc.a.top_d = sd; sc.a.hit_d = sd + nk;
+          sc.nwarps_total = p.seed_grid;  // one list per CTA (cta_flush_lists)
+          if (int e = scan(sc, dim3(p.seed_grid, a->NQ))) return e;
+          merge_kernel<<<a->NQ, 1024, 0, s>>>(sc);
+          seed_kth = sd;
+        }
+        thr_init_kernel<<<(a->NQ + 255) / 256, 256, 0, s>>>(seed_kth, a->k, a->NQ, thr, slots);
+        c.prune = 1;
+      }
       if (p.mq) {
         // common-grid distance tables of every query, then one launch over
         // (CTAs, query groups)

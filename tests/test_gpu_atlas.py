@@ -377,3 +377,61 @@ def test_multi_query_scan_equals_unpruned(torch, case):
     mq = chamfer_scan(db, q, **kw)
     assert int(mq["n_stage"][0].item()) > 0  # the multi-query kernel ran
     _lists_equal(torch, chamfer_scan(db, q, prune=False, **{k: v for k, v in kw.items() if k != "mq_fine"}), mq)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["c4", "order_hits_exclude", "odd_p", "outside_unit_square", "ties", "sharded",
+                                  "expansion"])
+def test_indexed_scan_equals_full_scan(torch, case):
+    """Indexed single-query scans (la_chamfer_index cells: seed scan, bound
+    step on the 2-byte cell rows, pruned scan of the survivors) return the
+    lists of the scan that evaluates every curve: C4 shape; shuffled order
+    with hits and an excluded record; odd P (16-bit cell loads); curves and
+    query partly outside the unit square (border cells); exact ties at the
+    k-th place; a shard with global positions (pos_map, id_base); the
+    expansion inner loop (its slack enters the bound)."""
+    from paper_2208_14567_b200.atlas import chamfer_index, chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    P = 199 if case == "odd_p" else 200
+    N = 300_000
+    db = fourier_db(N, P, seed=41, chunk=1 << 16)
+    q = fourier_db(2, P, seed=42)
+    kw = dict(k=10)
+    if case == "outside_unit_square":
+        g = torch.Generator(device="cuda")
+        g.manual_seed(5)
+        sel = torch.randperm(N, device="cuda", generator=g)[: N // 3]
+        db[sel] = (db[sel] - 0.5) * 2.5 + 0.5
+        q[0] = (q[0] - 0.5) * 1.7 + torch.tensor([0.9, -0.4], device="cuda")
+    dense = chamfer_scan(db, q[:1], k=10, dense=True)["all_d"][0].cpu().numpy()
+    if case == "order_hits_exclude":
+        kw = dict(k=7, threshold=float(np.quantile(dense, 2e-5)), exclude_id=int(np.argmin(dense)),
+                  order=torch.from_numpy(np.random.default_rng(3).permutation(N)).cuda())
+    elif case == "ties":
+        third = int(np.lexsort((np.arange(N), dense))[2])
+        pos = np.random.default_rng(8).choice(N, 25, replace=False)
+        db[torch.from_numpy(pos).cuda()] = db[third].clone()
+    elif case == "sharded":
+        rng = np.random.default_rng(9)
+        kw = dict(k=10, id_base=1_000_000, pos_map=torch.from_numpy(np.sort(rng.choice(10 * N, N, replace=False))).cuda(),
+                  order=torch.from_numpy(rng.permutation(N)).cuda())
+    elif case == "expansion":
+        kw = dict(k=10, expansion=True)
+    cells = chamfer_index(db)
+    for qq in (q[:1], q[1:2]):
+        full = chamfer_scan(db, qq, prune=False, **kw)
+        idx = chamfer_scan(db, qq, cells=cells, **kw)
+        _lists_equal(torch, full, idx)
+        surv = int(idx["n_stage"][0].item())
+        assert 0 < surv < N, surv  # the bound step ran and pruned
+    if case == "c4":
+        assert np.array_equal(chamfer_scan(db, q[:1], cells=cells, k=10)["top_id"][0].cpu().numpy(),
+                              np.lexsort((np.arange(N), dense))[:10])
+        # cells of points: floor((x + 1/32) * 1024 / 17) clamped, x major, rows of 66
+        pts = db[:1000].cpu().numpy().astype(np.float64)
+        cx = np.clip(np.floor((pts[..., 0] + 1 / 32) * 1024 / 17), 0, 63)
+        cy = np.clip(np.floor((pts[..., 1] + 1 / 32) * 1024 / 17), 0, 63)
+        got = cells[:1000, :P].cpu().numpy().astype(np.int64)
+        assert cells.shape[1] == 208 and bool((cells[:, P:] == 64).all())  # row padding: the null cell
+        assert (got == (cx * 66 + cy).astype(np.int64)).mean() > 0.999  # fp32 rounding at cell edges aside
