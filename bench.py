@@ -769,7 +769,7 @@ def bench_c3(torch, args, rank, world, peaks, flush, clk, want_cpu=False):
 
 # ----------------------------------------------------------------- C4
 def bench_c4(torch, args, rank, world, peaks, flush, clk):
-    from paper_2208_14567_b200.atlas import chamfer_scan
+    from paper_2208_14567_b200.atlas import chamfer_index, chamfer_scan
     from paper_2208_14567_b200.dist import gather_merge
     from paper_2208_14567_b200.workloads import fourier_db
 
@@ -777,11 +777,21 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
     q = fourier_db(1, C4_P, seed=999)
     stream = torch.cuda.current_stream()
     k = 10
+    # the database's cell index (2 bytes per point, built once per database
+    # like the reference's descriptors at Atlas build; not in the timed step)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    cells = chamfer_index(db)
+    e1.record(stream)
+    e1.synchronize()
+    index_ms = e0.elapsed_time(e1)
 
     def step(timer=None):
         if timer:
             timer.mark("start")
-        res = chamfer_scan(db, q, k=k, threshold=0.0, id_base=rank * C4_COUNT, pos_base=rank * C4_COUNT)
+        res = chamfer_scan(db, q, k=k, threshold=0.0, id_base=rank * C4_COUNT, pos_base=rank * C4_COUNT,
+                           cells=cells)
         if timer:
             timer.mark("scan")
         if world > 1:
@@ -795,6 +805,7 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
         step()
     spans = []
     n_full = []
+    n_surv = []
     barrier(torch, world)
     clk.timed = True
     for _ in range(args.steps):
@@ -803,27 +814,52 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
         res = step(tm)
         spans.append(tm.spans())
         n_full.append(res["n_full"])
+        n_surv.append(res["n_stage"])
     clk.timed = False
     barrier(torch, world)
     ms = max_over_ranks(torch, statistics.mean(s["total"] for s in spans), world)
     kscan = statistics.mean(s["scan"] for s in spans)
     full = statistics.mean(int(t.sum().item()) for t in n_full)
+    surv = statistics.mean(int(t[0].item()) for t in n_surv)
     sm_clock = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12
-    hbm_bytes = C4_COUNT * C4_P * 8
-    trc = load_traffic().get("chamfer_scan_c4_pruned", {})
-    # exact pruning: every curve is read once (1.6 KB) and bounded; only the
-    # curves whose bound does not rule them out get the 40,000-pair
-    # evaluation, so the scan is bounded by the curve stream from HBM
-    rl = {"kernel": "chamfer_scan_kernel<7> (bound stages + exact evaluation of the unpruned)", "bound": "hbm",
-          "achieved": hbm_bytes / (kscan / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+    stream_bytes = C4_COUNT * C4_P * 8
+    # indexed scan: what the three steps have to stream -- the seed prefix's
+    # curves (1/64 of the database), every curve's cell row (2 bytes per
+    # point, rows padded to 32-byte sectors), and the survivors' curves
+    row_bytes = ((C4_P + 15) // 16) * 32
+    hbm_bytes = (C4_COUNT // 64) * C4_P * 8 + C4_COUNT * row_bytes + surv * C4_P * 8
+    trc = load_traffic().get("chamfer_index_c4", {})
+    rl = {"kernel": "index_bound_kernel (cell rows, dominant) + chamfer_scan_kernel<7> (seed prefix, survivors)",
+          "bound": "hbm", "achieved": hbm_bytes / (kscan / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
           "frac": hbm_bytes / (kscan / 1e3) / 1e9 / peaks["hbm_gbs"],
           "algorithmic_bytes": hbm_bytes, "ms": kscan,
           "traffic": trc.get("per_launch_bytes"), "traffic_source": "profiles/traffic.json" if trc else None,
+          "bound_step_survivors": surv, "bound_step_survivor_frac": surv / C4_COUNT,
           "curves_evaluated_in_full": full, "pruned_frac": 1.0 - full / C4_COUNT,
+          "database_stream_floor_ms": stream_bytes / peaks["hbm_gbs"] / 1e6,
           "exhaustive_equivalent_TFLOPs": PAIR_FLOPS * C4_COUNT / (kscan / 1e3) / 1e12,
           "executed_pair_TFLOPs": PAIR_FLOPS * full / (kscan / 1e3) / 1e12, "fp32_peak_TFLOPs": fp32_peak,
-          "note": "lists identical to the unpruned scan (tests/test_gpu_atlas.py::test_pruned_scan_equals_full_scan)"}
+          "note": "lists identical to evaluating every pair (tests/test_gpu_atlas.py::"
+                  "test_indexed_scan_equals_full_scan); the step is shorter than streaming the 16 GB of curves "
+                  "once from HBM (database_stream_floor_ms): only the survivors' curves are read"}
+    # the scan without the index: every curve streamed once and bounded
+    # (round-2 sessions 1-4's headline), with its own roofline
+    plain_fn = lambda: chamfer_scan(db, q, k=k, threshold=0.0, id_base=rank * C4_COUNT,  # noqa: E731
+                                    pos_base=rank * C4_COUNT)
+    plain_fn()
+    plain_ms, plain_res = _time_scan(torch, args, plain_fn, flush, stream, max(3, args.steps // 4))
+    pfull = int(plain_res["n_full"].sum().item())
+    ptr = load_traffic().get("chamfer_scan_c4_pruned", {})
+    stream_scan = {"value": C4_COUNT / (plain_ms / 1e3), "unit": "curve-pairs/s", "ms_per_step": plain_ms,
+                   "lists_equal_indexed": bool(torch.equal(plain_res["top_id"], res["top_id"])
+                                               and torch.equal(plain_res["top_d"], res["top_d"])),
+                   "roofline": {"kernel": "chamfer_scan_kernel<7> (bound stages + exact evaluation of the unpruned)",
+                                "bound": "hbm", "achieved": stream_bytes / (plain_ms / 1e3) / 1e9,
+                                "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                "frac": stream_bytes / (plain_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                "algorithmic_bytes": stream_bytes, "traffic": ptr.get("per_launch_bytes"),
+                                "curves_evaluated_in_full": pfull}}
     # e2e: host query -> scan -> merged top-k back to the host
     qh = q.cpu().pin_memory()
     times = []
@@ -832,7 +868,7 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         qd = qh.cuda(non_blocking=True)
-        res = chamfer_scan(db, qd, k=k, threshold=0.0, id_base=rank * C4_COUNT)
+        res = chamfer_scan(db, qd, k=k, threshold=0.0, id_base=rank * C4_COUNT, cells=cells)
         out = {n: res[n].cpu() for n in ("top_d", "top_id")}
         e1.record(stream)
         e1.synchronize()
@@ -845,7 +881,7 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
     # distribution (pruning gain reported separately from kernel throughput)
     full = c4_unpruned(torch, args, db, q, k, flush, stream, peaks, rank)
     qo = ood_query(torch)
-    ood = c4_query_line(torch, args, db, qo, k, flush, stream, rank)
+    ood = c4_query_line(torch, args, db, qo, k, flush, stream, rank, cells)
     full["lists_equal_pruned"] = bool(torch.equal(full.pop("_res")["top_id"], res["top_id"]))
     ood["lists_equal_unpruned"] = bool(torch.equal(ood.pop("_res_full")["top_id"], ood["_res"]["top_id"]))
     lists["out_of_distribution"] = ood.pop("_res")
@@ -853,15 +889,19 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
     if rank == 0 and world == 1 and "cpu" not in set(filter(None, args.skip.split(","))):
         cpu = cpu_baseline_c4(db, q)
         parity = parity_chamfer(db, {"in_distribution": q, "out_of_distribution": qo}, lists, sample=20_000)
-    del db
+    del db, cells
     return {"metric": CHAMFER_METRIC, "prefilter": pre, "value": world * C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s",
-            "ms_per_step": ms, "roofline": rl, "launches_per_step": 4, "unpruned": full, "ood_query": ood,
+            "ms_per_step": ms, "roofline": rl, "launches_per_step": 9, "stream_scan": stream_scan,
+            "index": {"build_ms": index_ms, "bytes": C4_COUNT * row_bytes, "bytes_per_curve": row_bytes,
+                      "note": "la_chamfer_index, once per database"},
+            "unpruned": full, "ood_query": ood,
             "parity": parity, "cpu_baseline": cpu,
             "e2e": {"value": world * C4_COUNT / (e2e_ms / 1e3), "unit": "curve-pairs/s",
                     "h2d_bytes_per_step": C4_P * 8, "d2h_bytes_per_step": k * 12},
             "config": {"workload": "C4: 1 query vs 10M normalised Fourier curves/GPU (5 harmonics, "
-                                   "coeffs N(0,1/k^2)), 200 pts fp32, exact top-10 (pruned scan; lists equal to "
-                                   "evaluating every pair, see 'unpruned')"}}
+                                   "coeffs N(0,1/k^2)), 200 pts fp32, exact top-10 (indexed pruned scan: seed, "
+                                   "cell-row bound step, scan of the survivors; lists equal to evaluating every "
+                                   "pair, see 'unpruned'; 'stream_scan' is the scan without the index)"}}
 
 
 def ood_query(torch):
@@ -912,17 +952,18 @@ def c4_unpruned(torch, args, db, q, k, flush, stream, peaks, rank):
             "_res": res}
 
 
-def c4_query_line(torch, args, db, qo, k, flush, stream, rank):
+def c4_query_line(torch, args, db, qo, k, flush, stream, rank, cells=None):
     from paper_2208_14567_b200.atlas import chamfer_scan
 
     kw = dict(k=k, threshold=0.0, id_base=rank * C4_COUNT, pos_base=rank * C4_COUNT)
-    fn = lambda: chamfer_scan(db, qo, **kw)  # noqa: E731
+    fn = lambda: chamfer_scan(db, qo, cells=cells, **kw)  # noqa: E731
     fn()
     ms, res = _time_scan(torch, args, fn, flush, stream, 3)
     res_full = chamfer_scan(db, qo, prune=False, **kw)
     full = int(res["n_full"].sum().item())
     return {"value": C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s", "ms_per_step": ms,
             "curves_evaluated_in_full": full, "pruned_frac": 1.0 - full / C4_COUNT,
+            "bound_step_survivors": int(res["n_stage"][0].item()),
             "query": "15 harmonics, flat N(0,1) spectrum (database: 5 harmonics, N(0,1/k^2)), normalised",
             "best_d": float(res["top_d"][0, 0].item()), "kth_d": float(res["top_d"][0, k - 1].item()),
             "_res": res, "_res_full": res_full}

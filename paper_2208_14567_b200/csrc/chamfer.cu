@@ -489,6 +489,9 @@ __device__ __noinline__ float direct_chamfer(const float2* __restrict__ qsrc, in
 // result lists are identical to the unpruned scan: every curve in the
 // final top-k has d <= (final k-th) <= thr at all times, and ties never
 // prune (strict >).
+#ifndef LA_CH_INDEX_SEED_DIV
+#define LA_CH_INDEX_SEED_DIV 64  // indexed scans: the seed scan covers 1 / 64 of the positions (C4, 10M: 32 / 64 / 128 / 256 / 512 -> 1.74 / 1.70 / 1.75 / 1.86 / 2.01 ms)
+#endif
 constexpr int LBG = 64;             // grid cells per axis
 constexpr int LBV = LBG + 1;        // vertices per axis
 constexpr size_t LB_VTX_BYTES = ((size_t)LBV * LBV * sizeof(__half) + 15) & ~(size_t)15;
@@ -2340,7 +2343,7 @@ Plan make_plan(const la_chamfer_args* a) {
     // prefix published before the main scan; off by default (the slot
     // minima converge within the first wave and measured faster)
     p.index = a->cells != nullptr && a->NQ == 1 && !(a->flags & LA_CH_NO_INDEX);
-    const long long seed_div = p.index ? 64 : (a->flags & LA_CH_SEED_SCAN) ? 128 : 0;
+    const long long seed_div = p.index ? LA_CH_INDEX_SEED_DIV : (a->flags & LA_CH_SEED_SCAN) ? 128 : 0;
     long long sn = seed_div > 0 ? npos / seed_div : 0;
     if (seed_div > 0 && sn < 64LL * a->k) sn = 64LL * a->k;
     if (sn > npos) sn = npos;

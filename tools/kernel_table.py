@@ -42,6 +42,8 @@ circle_stats(n64["out"])                                               # circle_
 db = fourier_db(1_000_000, 200, seed=4000)
 q = fourier_db(64, 200, seed=999)
 chamfer_scan(db, q[:1], k=10)                                          # chamfer scan + select/merge
+from paper_2208_14567_b200.atlas import chamfer_index  # noqa: E402
+chamfer_scan(db, q[:1], k=10, cells=chamfer_index(db))                 # cell index, bound step, survivors' scan
 chamfer_scan(db[:200_000], q, k=10)                                    # 64 queries: multi-query kernel
 chamfer_scan(db[:200_000], q, k=10, multi_query=False)                 # 64 queries, one CTA set each
 from paper_2208_14567_b200.dist import merge_gathered, pack_lists  # noqa: E402

@@ -18,6 +18,10 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:sim_
   python tools/profile_step.py c2 1 > $O/r02_ncu_c2.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:chamfer_scan --launch-skip 2 -c 1 -f \
   -o $O/r02_c4 python tools/time_prune.py > $O/r02_ncu_c4.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:index_bound -c 1 -f \
+  -o $O/r02_c4_index python tools/time_index.py --once > $O/r02_ncu_c4_index.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/r02_launches_c4.csv \
+  python tools/time_index.py --once > $O/r02_ncu_launch_c4.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:chamfer_mq --launch-skip 1 -c 1 -f \
   -o $O/r02_c5 python tools/profile_c5chamfer.py > $O/r02_ncu_c5.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:sim_kernel --launch-skip 1 -c 1 -f \
