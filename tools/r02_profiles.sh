@@ -26,4 +26,15 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:cham
   -o $O/r02_c5 python tools/profile_c5chamfer.py > $O/r02_ncu_c5.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:sim_kernel --launch-skip 1 -c 1 -f \
   -o $O/r02_c3 python tools/time_c3.py 2000000 > $O/r02_ncu_c3.log 2>&1
+# summaries on the box; the reports themselves (tens of MB each with sources)
+# stay behind unless KEEP_REPS is set (gpurun returns at most 64 MiB)
+for n in c2 c3 c4 c4_index c5; do
+  python tools/ncu_summary.py $O/r02_$n.ncu-rep > $O/r02_ncu_$n.txt 2>&1
+  python tools/ncu_lines.py $O/r02_$n.ncu-rep 0 40 > $O/r02_lines_$n.txt 2>&1
+  [ -n "$KEEP_REPS" ] || rm -f $O/r02_$n.ncu-rep
+done
+python tools/launch_list.py $O/r02_launches.csv > $O/r02_launch_list_c2.txt 2>&1
+python tools/launch_list.py $O/r02_launches_c4.csv > $O/r02_launch_list_c4.txt 2>&1
+python tools/ncu_table.py $O/r02_table.csv > $O/r02_kernel_table.txt 2>&1
+du -sh $O
 echo done
