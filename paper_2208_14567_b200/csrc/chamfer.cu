@@ -496,7 +496,15 @@ constexpr int LBG = 64;             // grid cells per axis
 constexpr int LBV = LBG + 1;        // vertices per axis
 constexpr size_t LB_VTX_BYTES = ((size_t)LBV * LBV * sizeof(__half) + 15) & ~(size_t)15;
 // per query: the vertex table (LBV x LBV) then the cell table (LBG x LBG)
-constexpr size_t LB_DT_BYTES = LB_VTX_BYTES + (size_t)LBG * LBG * sizeof(__half);
+#ifndef LA_CH_CELL_STRIDE
+#define LA_CH_CELL_STRIDE (LBG + 2)
+#endif
+// cell table rows padded to LBS entries: neighbouring cells in x then fall
+// into neighbouring shared-memory banks (with 64 two-byte entries per row a
+// horizontal run of a curve -- the same iy in consecutive lanes -- would hit
+// one bank)
+constexpr int LBS = LA_CH_CELL_STRIDE;
+constexpr size_t LB_DT_BYTES = (LB_VTX_BYTES + (size_t)LBG * LBS * sizeof(__half) + 15) & ~(size_t)15;
 constexpr float LB_CELL_ONE = 16384.f;  // cell table fixed point: units of 2^-14
 constexpr long long PRUNE_MIN_POS = 1 << 16;  // smaller scans: no seed launches
 
@@ -565,7 +573,7 @@ __global__ void __launch_bounds__(256) lb_grid_kernel(const float* __restrict__ 
   // than fp16 above 0.125; integer sums of <= 256 terms fit 32 bits)
   if (lc) {
     const float dc = fmaxf(sqrtf(mc) * (1.f - 1e-6f) - 1e-6f, 0.f);
-    reinterpret_cast<unsigned short*>(out + LB_VTX_BYTES / sizeof(__half))[v] =
+    reinterpret_cast<unsigned short*>(out + LB_VTX_BYTES / sizeof(__half))[cxi * LBS + cyi] =
         (unsigned short)min(__float2uint_rd(dc * (float)LB_CELL_ONE), 65535u);
   }
 }
@@ -674,8 +682,18 @@ __global__ void __launch_bounds__(256) index_table_kernel(const float* __restric
 // appended (one atomic per warp) to the survivor list as (record, reported
 // scan position); the list's order does not matter: the scan's lists are
 // keyed by (distance, position) and its hit lists by position.
-constexpr int IB_T = 256;
-__global__ void __launch_bounds__(IB_T) index_bound_kernel(const unsigned short* __restrict__ cells, int P,
+#ifndef LA_IB_T
+#define LA_IB_T 512  // 128x16 / 256x8 / 512x4 threads x CTAs per SM measured 1.71 / 1.69 / 1.66 ms per C4 scan
+#endif
+#ifndef LA_IB_MINB
+#define LA_IB_MINB 4
+#endif
+#ifndef LA_IB_UNROLL
+#define LA_IB_UNROLL 2
+#endif
+constexpr int IB_T = LA_IB_T;
+constexpr int IB_UNROLL = LA_IB_UNROLL;
+__global__ void __launch_bounds__(IB_T, LA_IB_MINB) index_bound_kernel(const unsigned short* __restrict__ cells, int P,
                                                            const int64_t* __restrict__ order,
                                                            const int64_t* __restrict__ pos_map, long long pos_begin,
                                                            long long pos_base, long long npos,
@@ -720,7 +738,7 @@ __global__ void __launch_bounds__(IB_T) index_bound_kernel(const unsigned short*
     const uint4* row = reinterpret_cast<const uint4*>(cells + (size_t)rec * Pp);
     unsigned s0 = 0u, s1 = 0u;
     if (live) {
-#pragma unroll 2
+#pragma unroll IB_UNROLL
       for (int k = 0; k < W; ++k) {
         uint4 v, u;  // one 32-byte sector (LDG.256; two 16-byte loads fetched every sector twice)
         asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -791,7 +809,7 @@ __device__ __forceinline__ float curve_row_bound_cell(uint32_t cur_s, int P, uin
     const float2 a = lds_f2p(cur_s + 8u * (uint32_t)i);
     const unsigned ix = min(__float2uint_rd(fmaf(a.x, ihx, ox)), (unsigned)(LBG - 1));
     const unsigned iy = min(__float2uint_rd(fmaf(a.y, ihy, oy)), (unsigned)(LBG - 1));
-    return lds_u16p(ct_s + 2u * (ix * LBG + iy));
+    return lds_u16p(ct_s + 2u * (ix * LBS + iy));
   };
   const float scale = 1.f / (LB_CELL_ONE * (float)P);
   unsigned s = 0u;
@@ -2542,7 +2560,7 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
         cudaMemsetAsync(cnt, 0, sizeof(long long), s);
         index_table_kernel<<<(IDX_TAB + 255) / 256, 256, 0, s>>>(a->queries, a->Q, table);
         long long bg = (npos + IB_T - 1) / IB_T;
-        if (bg > (long long)sms * 8) bg = (long long)sms * 8;
+        if (bg > (long long)sms * (2048 / IB_T)) bg = (long long)sms * (2048 / IB_T);
         index_bound_kernel<<<(unsigned)bg, IB_T, 0, s>>>(a->cells, a->P, a->order, a->pos_map, a->pos_begin,
                                                          a->pos_base, npos, table, thr, a->threshold, c.lb_slack,
                                                          order2, pmap2, reinterpret_cast<unsigned long long*>(cnt));

@@ -435,3 +435,43 @@ def test_indexed_scan_equals_full_scan(torch, case):
         got = cells[:1000, :P].cpu().numpy().astype(np.int64)
         assert cells.shape[1] == 208 and bool((cells[:, P:] == 64).all())  # row padding: the null cell
         assert (got == (cx * 66 + cy).astype(np.int64)).mean() > 0.999  # fp32 rounding at cell edges aside
+
+
+@pytest.mark.gpu
+def test_atlas_retrieve_with_cell_index(torch):
+    """Atlas.retrieve on 80k stored curves (large enough for the pruned scan,
+    so the atlas' cell index is used): the hits equal those of the same
+    retrieval with the index disabled, for a stored curve (self hit), a
+    fresh query, thresholds with and without hits, and the oracle's
+    distances on the returned records."""
+    import paper_2208_14567_b200.atlas as A
+    from paper_2208_14567_b200 import Atlas
+    from paper_2208_14567_b200.workloads import four_bar, fourier_db
+
+    N = 80_000
+    pts = fourier_db(N + 1, 200, seed=51, chunk=1 << 16).cpu().numpy().astype(np.float64)
+    mech = four_bar()
+    atlas = Atlas(pts[:N], np.arange(N), np.full(N, 3), {i: mech for i in range(N)}, seed=5)
+    qs = [pts[123], pts[N]]
+    dense = O.chamfer_direct_block(pts[:N], pts[N])
+    for q in qs:
+        for k, thr in ((10, 0.0), (5, float(np.quantile(dense, 1e-4)))):
+            got = atlas.retrieve(q, k=k, threshold=thr)
+            cells = atlas._cells_dev
+            assert cells is not None and tuple(cells.shape) == (N, 208)
+            real = A.chamfer_scan
+
+            def no_index(*a, **kw):
+                kw["cells"] = None
+                return real(*a, **kw)
+
+            A.chamfer_scan = no_index
+            try:
+                want = atlas.retrieve(q, k=k, threshold=thr)
+            finally:
+                A.chamfer_scan = real
+            assert [(h.mech_id, h.joint_id, h.distance, h.above_threshold) for h in got] == \
+                   [(h.mech_id, h.joint_id, h.distance, h.above_threshold) for h in want]
+            assert len(got) == k
+    got = atlas.retrieve(pts[N], k=10, threshold=0.0)
+    assert np.allclose(sorted(h.distance for h in got), np.sort(dense)[:10], atol=1e-4)
