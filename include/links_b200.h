@@ -230,6 +230,12 @@ int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P,
                                 instead of the multi-query kernel (groups of
                                 queries share each streamed curve)           */
 #define LA_CH_NO_INDEX 256u  /* ignore la_chamfer_args.cells                  */
+#define LA_CH_INDEX_MQ 512u  /* use la_chamfer_args.cells for NQ >= 2 too:
+                                multi-query seed, bound step for every
+                                (query, curve), per-query survivor scans.
+                                Off by default: measured slower than the
+                                multi-query kernel (the cell-row bound alone
+                                keeps 40-90 % of the curves for most queries) */
 #define LA_CH_MQ_FINE 128u   /* multi-query kernel: 64x64 common grid for the
                                 stage-0 bound instead of 32x32               */
 
@@ -272,6 +278,11 @@ typedef struct la_chamfer_args {
                                  cells against the k-th best of a seed scan
                                  and scan only the survivors (same lists);
                                  n_stage[0] += survivors                     */
+  const uint8_t* coarse;      /* (device, optional, with cells) [N][256] coarse
+                                 distance tables of db from la_chamfer_index:
+                                 adds the column term to the bound step (the
+                                 query's 16 x 16 cell histogram against each
+                                 curve's bytes)                              */
 } la_chamfer_args;
 
 #define LA_INDEX_ROW(P) (((P) + 15) & ~15) /* cells per index row (32-byte sectors) */
@@ -280,8 +291,11 @@ typedef struct la_chamfer_args {
  * padded by 1/32 (outside points clamp into the border cells), numbered
  * ix * 66 + iy (table rows padded against bank conflicts); entries j >= P
  * of a row hold the null cell 64.  cells: [N][LA_INDEX_ROW(P)].  Built once
- * per database (Atlas build / load); 2 bytes per point.                      */
-int la_chamfer_index(const float* db, int64_t N, int32_t P, uint16_t* cells, void* stream);
+ * per database (Atlas build / load); 2 bytes per point.
+ * coarse (optional): [N][256] bytes, coarse[i][cx * 16 + cy] = floor(160 x
+ * distance from cell (cx, cy) of the 16 x 16 grid over the same square to
+ * curve i's nearest point), saturated at 255.                              */
+int la_chamfer_index(const float* db, int64_t N, int32_t P, uint16_t* cells, uint8_t* coarse, void* stream);
 
 size_t la_chamfer_workspace(const la_chamfer_args* args);
 int la_chamfer_topk(const la_chamfer_args* args, void* stream);

@@ -33,6 +33,7 @@ LA_SIM_STATIC_GRID = 1024
 LA_CH_NO_MQ = 64
 LA_CH_MQ_FINE = 128
 LA_CH_NO_INDEX = 256
+LA_CH_INDEX_MQ = 512
 LA_PENDING = -3
 ABI_VERSION = 3
 LA_EINVAL = -1
@@ -218,6 +219,7 @@ class LaChamferArgs(C.Structure):
         ("n_full", C.c_void_p),
         ("n_stage", C.c_void_p),
         ("cells", C.c_void_p),
+        ("coarse", C.c_void_p),
     ]
 
 
@@ -248,7 +250,7 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_chamfer_workspace.argtypes = [C.POINTER(LaChamferArgs)]
     lib.la_chamfer_workspace.restype = sz
     lib.la_chamfer_topk.argtypes = [C.POINTER(LaChamferArgs), vp]
-    lib.la_chamfer_index.argtypes = [vp, i64, i32, vp, vp]
+    lib.la_chamfer_index.argtypes = [vp, i64, i32, vp, vp, vp]
     lib.la_merge_shard_lists.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.la_sample_topologies.argtypes = [i64, i64, i64, i32, i32, C.c_double, i32, i32, vp, vp, vp, vp]
     lib.la_sample_topology_rng.argtypes = [vp, vp, i32, C.c_double, i32, vp, vp, vp]

@@ -21,6 +21,7 @@ import logging
 from dataclasses import dataclass
 
 import numpy as np
+from typing import NamedTuple
 
 from paper_2208_14567_b200 import _native as N
 from paper_2208_14567_b200.curves import is_normalized, normalize, normalize_tensors, reduce_mechanism, resample
@@ -52,14 +53,17 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
                  exclude_id: int = -1, dense: bool = False, all_d=None, expansion: bool = False,
                  fix_tol: float = 5e-5, scalar_pipe: bool = False, tensor: bool = False, prune: bool = True,
                  seed_scan: bool = False, multi_query: bool = True, mq_fine: bool = False,
-                 cells=None, stream=None) -> dict:
+                 cells=None, index_mq: bool = False, stream=None) -> dict:
     """One la_chamfer_topk launch.
 
-    ``cells`` (uint16 rows from ``chamfer_index(db)``; single-query pruned
-    scans): every curve is first bounded from its 2-byte cell row against the
-    k-th best of a seed scan over a 1/64 prefix, and only the survivors'
-    points are streamed; the lists are identical to the scan without it
-    (``n_stage[0]`` counts the survivors).
+    ``cells`` (``chamfer_index(db)``; single-query pruned scans): every curve
+    is first bounded from its index rows -- the row term from its 2-byte
+    cells, the column term from its coarse distance bytes -- against the k-th
+    best of a seed scan over a 1/64 prefix, and only the survivors' points
+    are streamed; the lists are identical to the scan without it
+    (``n_stage[0]`` counts the survivors).  ``index_mq`` uses the cells (row
+    term only) for several queries too (measured slower than the multi-query
+    kernel; off).
 
     ``prune`` (top-k scans of >= 65,536 positions without dense output):
     curves whose lower bound (query distance grid, first chamfer term)
@@ -131,15 +135,21 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     a.flags = ((N.LA_CH_EXPANSION if expansion else 0) | (N.LA_CH_SCALAR_PIPE if scalar_pipe else 0)
                | (N.LA_CH_TENSOR if tensor else 0) | (0 if prune else N.LA_CH_NO_PRUNE)
                | (N.LA_CH_SEED_SCAN if seed_scan else 0) | (0 if multi_query else N.LA_CH_NO_MQ)
-               | (N.LA_CH_MQ_FINE if mq_fine else 0))
+               | (N.LA_CH_MQ_FINE if mq_fine else 0) | (N.LA_CH_INDEX_MQ if index_mq else 0))
     a.fixup_below = float(fix_tol)
     a.n_full = out["n_full"].data_ptr()
     a.n_stage = out["n_stage"].data_ptr()
+    coarse = None
+    if isinstance(cells, ChamferIndex):
+        cells, coarse = cells.cells, cells.coarse
     if cells is not None:
         if cells.dtype != torch.uint16 or tuple(cells.shape) != (Nn, (P + 15) & ~15) or not cells.is_cuda:
-            raise ValueError("cells must be the (N, P rounded up to 16) uint16 CUDA tensor of chamfer_index(db)")
+            raise ValueError("cells must be chamfer_index(db) (or its (N, P rounded up to 16) uint16 cells)")
         cells = cells.contiguous()
+        if coarse is not None and (coarse.dtype != torch.uint8 or tuple(coarse.shape) != (Nn, 256)):
+            raise ValueError("coarse must be the (N, 256) uint8 tensor of chamfer_index(db)")
     a.cells = N.ptr(cells)
+    a.coarse = N.ptr(coarse.contiguous() if coarse is not None else None)
     wsb = int(lib.la_chamfer_workspace(a))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     a.ws, a.ws_bytes = ws.data_ptr(), wsb
@@ -148,19 +158,28 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     return out
 
 
-def chamfer_index(db, stream=None):
-    """Cell index of a curve database (la_chamfer_index): (N, P rounded up to
-    16) uint16, the 64 x 64 grid cell of every point (row padding: the null
-    cell); pass it to ``chamfer_scan(cells=...)``."""
+class ChamferIndex(NamedTuple):
+    """la_chamfer_index outputs for one database: ``cells`` (N, P rounded up
+    to 16) uint16 and ``coarse`` (N, 256) uint8 (or None)."""
+    cells: object
+    coarse: object
+
+
+def chamfer_index(db, coarse: bool = True, stream=None) -> ChamferIndex:
+    """Index of a curve database (la_chamfer_index): the 64 x 64 grid cell of
+    every point (2 bytes; row padding: the null cell) and, with ``coarse``,
+    each curve's 16 x 16 coarse distance table (256 bytes); pass it to
+    ``chamfer_scan(cells=...)``."""
     torch = N.require_cuda()
     lib = N.load()
     if db.dtype != torch.float32 or db.dim() != 3 or db.shape[2] != 2 or not db.is_cuda:
         raise ValueError("db must be a (N, P, 2) float32 CUDA tensor")
     db = db.contiguous()
     cells = torch.empty((db.shape[0], (db.shape[1] + 15) & ~15), dtype=torch.uint16, device=db.device)
-    N.check(lib.la_chamfer_index(db.data_ptr(), db.shape[0], db.shape[1], cells.data_ptr(), N.stream_ptr(stream)),
-            "la_chamfer_index")
-    return cells
+    cd = torch.empty((db.shape[0], 256), dtype=torch.uint8, device=db.device) if coarse else None
+    N.check(lib.la_chamfer_index(db.data_ptr(), db.shape[0], db.shape[1], cells.data_ptr(), N.ptr(cd),
+                                 N.stream_ptr(stream)), "la_chamfer_index")
+    return ChamferIndex(cells, cd)
 
 
 _EDGES = np.linspace(0.0, 0.75, 17)  # np.histogram(bins=16, range=(0, .75)) edges (atlas.py:169)

@@ -432,8 +432,21 @@ def test_indexed_scan_equals_full_scan(torch, case):
         pts = db[:1000].cpu().numpy().astype(np.float64)
         cx = np.clip(np.floor((pts[..., 0] + 1 / 32) * 1024 / 17), 0, 63)
         cy = np.clip(np.floor((pts[..., 1] + 1 / 32) * 1024 / 17), 0, 63)
-        got = cells[:1000, :P].cpu().numpy().astype(np.int64)
-        assert cells.shape[1] == 208 and bool((cells[:, P:] == 64).all())  # row padding: the null cell
+        got = cells.cells[:1000, :P].cpu().numpy().astype(np.int64)
+        assert cells.cells.shape[1] == 208 and bool((cells.cells[:, P:] == 64).all())  # row padding: the null cell
+        # coarse distance tables: floor(160 x distance from the 16 x 16 cell's box to the curve), saturated
+        g0 = -1 / 32 + np.arange(16) * (17 / 256)
+        a = pts[:50]
+        ex = np.maximum(np.maximum(g0[:, None, None] - a[None, :, :, 0], a[None, :, :, 0] - (g0 + 17 / 256)[:, None, None]), 0)
+        ey = np.maximum(np.maximum(g0[:, None, None] - a[None, :, :, 1], a[None, :, :, 1] - (g0 + 17 / 256)[:, None, None]), 0)
+        ex[0] = np.maximum(a[..., 0] - (g0[0] + 17 / 256), 0)
+        ex[15] = np.maximum(g0[15] - a[..., 0], 0)
+        ey[0] = np.maximum(a[..., 1] - (g0[0] + 17 / 256), 0)
+        ey[15] = np.maximum(g0[15] - a[..., 1], 0)
+        dd = np.sqrt(ex[:, None] ** 2 + ey[None, :] ** 2).min(-1)  # (16, 16, 50)
+        want = np.minimum(np.floor(dd * 160), 255).transpose(2, 0, 1).reshape(50, 256)
+        gotc = cells.coarse[:50].cpu().numpy().astype(np.int64)
+        assert (np.abs(gotc - want) <= 1).all() and (gotc <= want).mean() > 0.99
         assert (got == (cx * 66 + cy).astype(np.int64)).mean() > 0.999  # fp32 rounding at cell edges aside
 
 
@@ -458,7 +471,7 @@ def test_atlas_retrieve_with_cell_index(torch):
         for k, thr in ((10, 0.0), (5, float(np.quantile(dense, 1e-4)))):
             got = atlas.retrieve(q, k=k, threshold=thr)
             cells = atlas._cells_dev
-            assert cells is not None and tuple(cells.shape) == (N, 208)
+            assert cells is not None and tuple(cells.cells.shape) == (N, 208) and tuple(cells.coarse.shape) == (N, 256)
             real = A.chamfer_scan
 
             def no_index(*a, **kw):
@@ -475,3 +488,34 @@ def test_atlas_retrieve_with_cell_index(torch):
             assert len(got) == k
     got = atlas.retrieve(pts[N], k=10, threshold=0.0)
     assert np.allclose(sorted(h.distance for h in got), np.sort(dense)[:10], atol=1e-4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["many_queries", "order_hits_exclude", "sharded", "odd_groups"])
+def test_indexed_multi_query_scan_equals_full_scan(torch, case):
+    """Indexed scans with several queries (multi-query seed, bound step with
+    interleaved tables, per-query survivor lists): lists equal to evaluating
+    every curve, with 40 queries (three groups of 16, the last partial), a
+    shuffled order + hits + an excluded record, shard positions, and 17
+    queries (a group of one)."""
+    from paper_2208_14567_b200.atlas import chamfer_index, chamfer_scan
+    from paper_2208_14567_b200.workloads import fourier_db
+
+    N, P = 200_000, 200
+    db = fourier_db(N, P, seed=61, chunk=1 << 16)
+    nq = {"many_queries": 40, "odd_groups": 17}.get(case, 5)
+    q = fourier_db(nq, P, seed=62)
+    kw = dict(k=10)
+    if case == "order_hits_exclude":
+        dense = chamfer_scan(db, q[:1], k=10, dense=True)["all_d"][0].cpu().numpy()
+        kw = dict(k=7, threshold=float(np.quantile(dense, 2e-5)), exclude_id=int(np.argmin(dense)),
+                  order=torch.from_numpy(np.random.default_rng(3).permutation(N)).cuda())
+    elif case == "sharded":
+        rng = np.random.default_rng(9)
+        kw = dict(k=10, id_base=1_000_000, pos_map=torch.from_numpy(np.sort(rng.choice(10 * N, N, replace=False))).cuda(),
+                  order=torch.from_numpy(rng.permutation(N)).cuda())
+    full = chamfer_scan(db, q, prune=False, **kw)
+    idx = chamfer_scan(db, q, cells=chamfer_index(db), index_mq=True, **kw)
+    _lists_equal(torch, full, idx)
+    surv = int(idx["n_stage"][0].item())
+    assert 0 < surv < nq * N, surv

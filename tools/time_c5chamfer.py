@@ -12,7 +12,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2208_14567_b200.atlas import chamfer_scan  # noqa: E402
+from paper_2208_14567_b200.atlas import chamfer_index, chamfer_scan  # noqa: E402
 from paper_2208_14567_b200.curves import normalize_tensors  # noqa: E402
 from paper_2208_14567_b200.solver import compact_valid, simulate_tensors  # noqa: E402
 from paper_2208_14567_b200.workloads import fourier_db, native_batch  # noqa: E402
@@ -49,7 +49,11 @@ def timed(fn, reps=3):
 
 
 out = {}
-variants = [("per-query", dict(multi_query=False)), ("mq32", dict()), ("mq64", dict(mq_fine=True))]
+cells = chamfer_index(db)
+variants = [("per-query", dict(multi_query=False)), ("mq32", dict()), ("mq64", dict(mq_fine=True)),
+            ("indexed", dict(cells=cells, index_mq=True))]
+if "--quick" in sys.argv:
+    variants = [("per-query", dict(multi_query=False)), ("mq32", dict()), ("indexed", dict(cells=cells, index_mq=True))]
 if "--unpruned" in sys.argv:
     variants.append(("unpruned", dict(prune=False)))
 for name, kw in variants:

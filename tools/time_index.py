@@ -14,9 +14,10 @@ from paper_2208_14567_b200.workloads import fourier_db  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=10_000_000)
 ap.add_argument("--once", action="store_true")
+ap.add_argument("--query", type=int, default=0)
 args = ap.parse_args()
 db = fourier_db(args.n, 200, seed=4000)
-q = fourier_db(1, 200, seed=999)
+q = fourier_db(args.query + 1, 200, seed=999)[args.query:args.query + 1]
 cells = chamfer_index(db)
 torch.cuda.synchronize()
 for name, kw in (("plain", {}), ("indexed", {"cells": cells})):
