@@ -777,9 +777,9 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
     q = fourier_db(1, C4_P, seed=999)
     stream = torch.cuda.current_stream()
     k = 10
-    # the database's index (2 bytes per point + 256 coarse distance bytes per
-    # curve, built once per database like the reference's descriptors at
-    # Atlas build; not in the timed step)
+    # the database's index (2 bytes per point + 256 + 1,024 distance bytes
+    # per curve, built once per database like the reference's descriptors
+    # at Atlas build; not in the timed step)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -821,16 +821,20 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
     ms = max_over_ranks(torch, statistics.mean(s["total"] for s in spans), world)
     kscan = statistics.mean(s["scan"] for s in spans)
     full = statistics.mean(int(t.sum().item()) for t in n_full)
-    surv = statistics.mean(int(t[0].item()) for t in n_surv)
+    surv1 = statistics.mean(int(t[0].item()) for t in n_surv)  # after the bound step's first level
+    surv = statistics.mean(int(t[1].item()) for t in n_surv)   # after its second level: the curves scanned
     sm_clock = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_clock * 1e6 / 1e12
     stream_bytes = C4_COUNT * C4_P * 8
-    # indexed scan: what the three steps have to stream -- the seed prefix's
-    # curves (1/64 of the database), every curve's index rows (256 coarse
-    # distance bytes + 2 bytes per point, rows padded to 32-byte sectors),
-    # and the survivors' curves
-    row_bytes = ((C4_P + 15) // 16) * 32 + 256
-    hbm_bytes = (C4_COUNT // 64) * C4_P * 8 + C4_COUNT * row_bytes + surv * C4_P * 8
+    # indexed scan: what its steps have to stream -- the seed prefix's curves
+    # (1/64 of the database), every curve's first-level index rows (256
+    # coarse distance bytes + 2 bytes per point, rows padded to 32-byte
+    # sectors), the first level's survivors' 1 KB tables and cell rows again,
+    # and the second level's survivors' curves
+    cell_bytes = ((C4_P + 15) // 16) * 32
+    row_bytes = cell_bytes + 256
+    hbm_bytes = ((C4_COUNT // 64) * C4_P * 8 + C4_COUNT * row_bytes + surv1 * (1024 + cell_bytes)
+                 + surv * C4_P * 8)
     trc = load_traffic().get("chamfer_index_c4", {})
     rl = {"kernel": "index_bound_kernel (index rows, dominant) + chamfer_scan_kernel<7> (seed prefix, survivors)",
           "bound": "hbm", "achieved": hbm_bytes / (kscan / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -838,6 +842,7 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
           "algorithmic_bytes": hbm_bytes, "ms": kscan,
           "traffic": trc.get("per_launch_bytes"), "traffic_source": "profiles/traffic.json" if trc else None,
           "bound_step_survivors": surv, "bound_step_survivor_frac": surv / C4_COUNT,
+          "bound_step_first_level_survivors": surv1,
           "curves_evaluated_in_full": full, "pruned_frac": 1.0 - full / C4_COUNT,
           "database_stream_floor_ms": stream_bytes / peaks["hbm_gbs"] / 1e6,
           "exhaustive_equivalent_TFLOPs": PAIR_FLOPS * C4_COUNT / (kscan / 1e3) / 1e12,
@@ -899,7 +904,7 @@ def bench_c4(torch, args, rank, world, peaks, flush, clk):
     return {"metric": CHAMFER_METRIC, "prefilter": pre, "value": world * C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s",
             "ms_per_step": ms, "roofline": rl, "launches_per_step": 9, "stream_scan": stream_scan,
             "query_sweep": sweep,
-            "index": {"build_ms": index_ms, "bytes": C4_COUNT * row_bytes, "bytes_per_curve": row_bytes,
+            "index": {"build_ms": index_ms, "bytes": C4_COUNT * (row_bytes + 1024), "bytes_per_curve": row_bytes + 1024,
                       "note": "la_chamfer_index, once per database"},
             "unpruned": full, "ood_query": ood,
             "parity": parity, "cpu_baseline": cpu,
@@ -928,7 +933,8 @@ def c4_query_sweep(torch, db, cells, k, flush, stream, rank, count: int = 8):
         ms_p, rp = _time_scan(torch, None, lambda: chamfer_scan(db, qi, **kw), flush, stream, 2)
         ms_i, ri = _time_scan(torch, None, lambda: chamfer_scan(db, qi, cells=cells, **kw), flush, stream, 2)
         rows.append({"query": i, "plain_ms": ms_p, "indexed_ms": ms_i,
-                     "bound_step_survivor_frac": float(ri["n_stage"][0].item()) / C4_COUNT,
+                     "bound_step_survivor_frac": float(ri["n_stage"][1].item()) / C4_COUNT,
+                     "first_level_survivor_frac": float(ri["n_stage"][0].item()) / C4_COUNT,
                      "curves_evaluated_in_full": int(ri["n_full"].sum().item()),
                      "kth_d": float(ri["top_d"][0, k - 1].item()),
                      "lists_equal": bool(torch.equal(rp["top_id"], ri["top_id"]) and torch.equal(rp["top_d"], ri["top_d"]))})
@@ -1002,7 +1008,7 @@ def c4_query_line(torch, args, db, qo, k, flush, stream, rank, cells=None):
     full = int(res["n_full"].sum().item())
     return {"value": C4_COUNT / (ms / 1e3), "unit": "curve-pairs/s", "ms_per_step": ms,
             "curves_evaluated_in_full": full, "pruned_frac": 1.0 - full / C4_COUNT,
-            "bound_step_survivors": int(res["n_stage"][0].item()),
+            "bound_step_survivors": int(res["n_stage"][1].item()),
             "query": "15 harmonics, flat N(0,1) spectrum (database: 5 harmonics, N(0,1/k^2)), normalised",
             "best_d": float(res["top_d"][0, 0].item()), "kth_d": float(res["top_d"][0, k - 1].item()),
             "_res": res, "_res_full": res_full}

@@ -283,6 +283,10 @@ typedef struct la_chamfer_args {
                                  adds the column term to the bound step (the
                                  query's 16 x 16 cell histogram against each
                                  curve's bytes)                              */
+  const uint8_t* fine;        /* (device, optional, with coarse) [N][1024]: the
+                                 32 x 32 tables, read for the bound step's
+                                 survivors only (second level; n_stage[1] +=
+                                 its survivors)                              */
 } la_chamfer_args;
 
 #define LA_INDEX_ROW(P) (((P) + 15) & ~15) /* cells per index row (32-byte sectors) */
@@ -294,8 +298,10 @@ typedef struct la_chamfer_args {
  * per database (Atlas build / load); 2 bytes per point.
  * coarse (optional): [N][256] bytes, coarse[i][cx * 16 + cy] = floor(160 x
  * distance from cell (cx, cy) of the 16 x 16 grid over the same square to
- * curve i's nearest point), saturated at 255.                              */
-int la_chamfer_index(const float* db, int64_t N, int32_t P, uint16_t* cells, uint8_t* coarse, void* stream);
+ * curve i's nearest point), saturated at 255.  fine (optional): [N][1024],
+ * the same on the 32 x 32 grid.                                            */
+int la_chamfer_index(const float* db, int64_t N, int32_t P, uint16_t* cells, uint8_t* coarse, uint8_t* fine,
+                     void* stream);
 
 size_t la_chamfer_workspace(const la_chamfer_args* args);
 int la_chamfer_topk(const la_chamfer_args* args, void* stream);

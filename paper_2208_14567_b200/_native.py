@@ -220,6 +220,7 @@ class LaChamferArgs(C.Structure):
         ("n_stage", C.c_void_p),
         ("cells", C.c_void_p),
         ("coarse", C.c_void_p),
+        ("fine", C.c_void_p),
     ]
 
 
@@ -250,7 +251,7 @@ def _declare(lib: C.CDLL) -> None:
     lib.la_chamfer_workspace.argtypes = [C.POINTER(LaChamferArgs)]
     lib.la_chamfer_workspace.restype = sz
     lib.la_chamfer_topk.argtypes = [C.POINTER(LaChamferArgs), vp]
-    lib.la_chamfer_index.argtypes = [vp, i64, i32, vp, vp, vp]
+    lib.la_chamfer_index.argtypes = [vp, i64, i32, vp, vp, vp, vp]
     lib.la_merge_shard_lists.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.la_sample_topologies.argtypes = [i64, i64, i64, i32, i32, C.c_double, i32, i32, vp, vp, vp, vp]
     lib.la_sample_topology_rng.argtypes = [vp, vp, i32, C.c_double, i32, vp, vp, vp]

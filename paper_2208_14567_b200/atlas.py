@@ -139,17 +139,20 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     a.fixup_below = float(fix_tol)
     a.n_full = out["n_full"].data_ptr()
     a.n_stage = out["n_stage"].data_ptr()
-    coarse = None
+    coarse = fine = None
     if isinstance(cells, ChamferIndex):
-        cells, coarse = cells.cells, cells.coarse
+        cells, coarse, fine = cells.cells, cells.coarse, cells.fine
     if cells is not None:
         if cells.dtype != torch.uint16 or tuple(cells.shape) != (Nn, (P + 15) & ~15) or not cells.is_cuda:
             raise ValueError("cells must be chamfer_index(db) (or its (N, P rounded up to 16) uint16 cells)")
         cells = cells.contiguous()
         if coarse is not None and (coarse.dtype != torch.uint8 or tuple(coarse.shape) != (Nn, 256)):
             raise ValueError("coarse must be the (N, 256) uint8 tensor of chamfer_index(db)")
+        if fine is not None and (fine.dtype != torch.uint8 or tuple(fine.shape) != (Nn, 1024)):
+            raise ValueError("fine must be the (N, 1024) uint8 tensor of chamfer_index(db)")
     a.cells = N.ptr(cells)
     a.coarse = N.ptr(coarse.contiguous() if coarse is not None else None)
+    a.fine = N.ptr(fine.contiguous() if (fine is not None and coarse is not None) else None)
     wsb = int(lib.la_chamfer_workspace(a))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     a.ws, a.ws_bytes = ws.data_ptr(), wsb
@@ -160,16 +163,19 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
 
 class ChamferIndex(NamedTuple):
     """la_chamfer_index outputs for one database: ``cells`` (N, P rounded up
-    to 16) uint16 and ``coarse`` (N, 256) uint8 (or None)."""
+    to 16) uint16, ``coarse`` (N, 256) uint8 (or None) and ``fine`` (N, 1024)
+    uint8 (or None)."""
     cells: object
     coarse: object
+    fine: object = None
 
 
-def chamfer_index(db, coarse: bool = True, stream=None) -> ChamferIndex:
+def chamfer_index(db, coarse: bool = True, fine: bool = True, stream=None) -> ChamferIndex:
     """Index of a curve database (la_chamfer_index): the 64 x 64 grid cell of
-    every point (2 bytes; row padding: the null cell) and, with ``coarse``,
-    each curve's 16 x 16 coarse distance table (256 bytes); pass it to
-    ``chamfer_scan(cells=...)``."""
+    every point (2 bytes; row padding: the null cell); with ``coarse``, each
+    curve's 16 x 16 distance table (256 bytes, the bound step's column term);
+    with ``fine``, its 32 x 32 table (1 KB, read for the bound step's
+    survivors only).  Pass it to ``chamfer_scan(cells=...)``."""
     torch = N.require_cuda()
     lib = N.load()
     if db.dtype != torch.float32 or db.dim() != 3 or db.shape[2] != 2 or not db.is_cuda:
@@ -177,9 +183,10 @@ def chamfer_index(db, coarse: bool = True, stream=None) -> ChamferIndex:
     db = db.contiguous()
     cells = torch.empty((db.shape[0], (db.shape[1] + 15) & ~15), dtype=torch.uint16, device=db.device)
     cd = torch.empty((db.shape[0], 256), dtype=torch.uint8, device=db.device) if coarse else None
-    N.check(lib.la_chamfer_index(db.data_ptr(), db.shape[0], db.shape[1], cells.data_ptr(), N.ptr(cd),
+    fd = torch.empty((db.shape[0], 1024), dtype=torch.uint8, device=db.device) if (coarse and fine) else None
+    N.check(lib.la_chamfer_index(db.data_ptr(), db.shape[0], db.shape[1], cells.data_ptr(), N.ptr(cd), N.ptr(fd),
                                  N.stream_ptr(stream)), "la_chamfer_index")
-    return ChamferIndex(cells, cd)
+    return ChamferIndex(cells, cd, fd)
 
 
 _EDGES = np.linspace(0.0, 0.75, 17)  # np.histogram(bins=16, range=(0, .75)) edges (atlas.py:169)

@@ -664,70 +664,78 @@ __global__ void __launch_bounds__(256) index_kernel(const float2* __restrict__ d
 constexpr int CDG = 16;                  // coarse cells per axis
 constexpr int CD_CELLS = CDG * CDG;      // bytes per curve
 constexpr float CD_ONE = 160.f;          // fixed point: units of 1 / 160 (255 = 1.59)
-constexpr float CD_CELL = (1.f + 2.f / 32.f) / (float)CDG;
-constexpr float CD_INV = 1.f / CD_CELL;
+constexpr int CD2G = 32;                 // second level: 32 x 32 cells, 1 KB per curve
+constexpr int CD2_CELLS = CD2G * CD2G;
 
+template <int G>
 __device__ __forceinline__ unsigned cd_cell(float2 a) {
-  const unsigned ix = min(__float2uint_rd(fmaf(a.x, CD_INV, -IDX_LO * CD_INV)), (unsigned)(CDG - 1));
-  const unsigned iy = min(__float2uint_rd(fmaf(a.y, CD_INV, -IDX_LO * CD_INV)), (unsigned)(CDG - 1));
-  return ix * CDG + iy;
+  constexpr float inv = (float)G / (1.f + 2.f / 32.f);
+  const unsigned ix = min(__float2uint_rd(fmaf(a.x, inv, -IDX_LO * inv)), (unsigned)(G - 1));
+  const unsigned iy = min(__float2uint_rd(fmaf(a.y, inv, -IDX_LO * inv)), (unsigned)(G - 1));
+  return ix * G + iy;
 }
 
-// one warp per curve; lane l owns cells l, l + 32, ... (8 cells), the curve's
-// points are read by every lane (L1 broadcast).  grid-stride over curves.
+// one warp per curve; lane l owns cells l, l + 32, ...; the curve's points
+// are read by every lane (L1 broadcast).  grid-stride over curves.  G = 16:
+// the bound step's table (256 bytes); G = 32: the second level's (1 KB).
+template <int G>
 __global__ void __launch_bounds__(256) index_coarse_kernel(const float2* __restrict__ db, long long N, int P,
                                                            unsigned char* __restrict__ coarse) {
+  constexpr float cell = (1.f + 2.f / 32.f) / (float)G;
+  constexpr int CPL = G * G / 32;  // cells per lane
   const int lane = threadIdx.x & 31;
-  float bx0[8], bx1[8], by0[8], by1[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int c = lane + 32 * u, cx = c / CDG, cy = c % CDG;
-    bx0[u] = cx == 0 ? -INFINITY : __fmaf_rn((float)cx, CD_CELL, IDX_LO) - 1e-6f;
-    bx1[u] = cx == CDG - 1 ? INFINITY : __fmaf_rn((float)(cx + 1), CD_CELL, IDX_LO) + 1e-6f;
-    by0[u] = cy == 0 ? -INFINITY : __fmaf_rn((float)cy, CD_CELL, IDX_LO) - 1e-6f;
-    by1[u] = cy == CDG - 1 ? INFINITY : __fmaf_rn((float)(cy + 1), CD_CELL, IDX_LO) + 1e-6f;
-  }
   const long long nw = (long long)gridDim.x * 8;
   for (long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); r < N; r += nw) {
     const float2* pts = db + r * P;
-    float m[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) m[u] = INFINITY;
-    for (int i = 0; i < P; ++i) {
-      const float2 a = __ldg(pts + i);
+#pragma unroll 1
+    for (int u0 = 0; u0 < CPL; u0 += 8) {
+      float bx0[8], bx1[8], by0[8], by1[8], m[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float ex = fmaxf(fmaxf(bx0[u] - a.x, a.x - bx1[u]), 0.f);
-        const float ey = fmaxf(fmaxf(by0[u] - a.y, a.y - by1[u]), 0.f);
-        m[u] = fminf(m[u], __fmaf_rn(ey, ey, ex * ex));
+        const int c = lane + 32 * (u0 + u), cx = c / G, cy = c % G;
+        bx0[u] = cx == 0 ? -INFINITY : __fmaf_rn((float)cx, cell, IDX_LO) - 1e-6f;
+        bx1[u] = cx == G - 1 ? INFINITY : __fmaf_rn((float)(cx + 1), cell, IDX_LO) + 1e-6f;
+        by0[u] = cy == 0 ? -INFINITY : __fmaf_rn((float)cy, cell, IDX_LO) - 1e-6f;
+        by1[u] = cy == G - 1 ? INFINITY : __fmaf_rn((float)(cy + 1), cell, IDX_LO) + 1e-6f;
+        m[u] = INFINITY;
       }
-    }
+      for (int i = 0; i < P; ++i) {
+        const float2 a = __ldg(pts + i);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      // rounded down, after the slack of the fp32 distance evaluation
-      const float d = fmaxf(sqrtf(m[u]) * (1.f - 1e-6f) - 1e-6f, 0.f);
-      coarse[r * CD_CELLS + lane + 32 * u] = (unsigned char)min(__float2uint_rd(d * CD_ONE), 255u);
+        for (int u = 0; u < 8; ++u) {
+          const float ex = fmaxf(fmaxf(bx0[u] - a.x, a.x - bx1[u]), 0.f);
+          const float ey = fmaxf(fmaxf(by0[u] - a.y, a.y - by1[u]), 0.f);
+          m[u] = fminf(m[u], __fmaf_rn(ey, ey, ex * ex));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        // rounded down, after the slack of the fp32 distance evaluation
+        const float d = fmaxf(sqrtf(m[u]) * (1.f - 1e-6f) - 1e-6f, 0.f);
+        coarse[r * (G * G) + lane + 32 * (u0 + u)] = (unsigned char)min(__float2uint_rd(d * CD_ONE), 255u);
+      }
     }
   }
 }
 
-// the query's coarse-cell histogram as 256 weight bytes (64 words after
-// qw[0], the number of words to use: 64, or 0 when Q > 255 and a weight
-// could overflow its byte -- the column term is then left out).  One CTA of
-// 256 threads.
+// the query's cell histogram on the G x G grid as G * G weight bytes
+// (G * G / 4 words after qw[0], the number of words to use: G * G / 4, or 0
+// when Q > 255 and a weight could overflow its byte -- the column term is
+// then left out).  One CTA of 256 threads.
+template <int G>
 __global__ void __launch_bounds__(256) index_qlist_kernel(const float* __restrict__ query, int Q,
                                                           unsigned* __restrict__ qw) {
-  __shared__ unsigned hist[CD_CELLS];
-  hist[threadIdx.x] = 0u;
+  __shared__ unsigned hist[G * G];
+  for (int c = threadIdx.x; c < G * G; c += 256) hist[c] = 0u;
   __syncthreads();
   const float2* q = reinterpret_cast<const float2*>(query);
-  for (int j = threadIdx.x; j < Q; j += 256) atomicAdd(&hist[cd_cell(q[j])], 1u);
+  for (int j = threadIdx.x; j < Q; j += 256) atomicAdd(&hist[cd_cell<G>(q[j])], 1u);
   __syncthreads();
-  if (threadIdx.x < CD_CELLS / 4) {
-    const int c = 4 * threadIdx.x;
-    qw[1 + threadIdx.x] = hist[c] | (hist[c + 1] << 8) | (hist[c + 2] << 16) | (hist[c + 3] << 24);
+  for (int w = threadIdx.x; w < G * G / 4; w += 256) {
+    const int c = 4 * w;
+    qw[1 + w] = hist[c] | (hist[c + 1] << 8) | (hist[c + 2] << 16) | (hist[c + 3] << 24);
   }
-  if (threadIdx.x == 0) qw[0] = Q <= 255 ? CD_CELLS / 4 : 0;
+  if (threadIdx.x == 0) qw[0] = Q <= 255 ? G * G / 4 : 0;
 }
 
 // the query's cell table on the index grid: floor(2^14 x distance from the
@@ -959,6 +967,84 @@ __global__ void index_count_mq_kernel(const long long* __restrict__ count, int N
   long long sum = 0;
   for (int q = 0; q < NQ; ++q) sum += count[q];
   n_stage[0] += sum;  // (query, curve) pairs surviving the bound step
+}
+
+// second level of the bound step, over the first level's survivors only:
+// the column term from the curve's 32 x 32 table (1 KB, thirty-two 32-byte
+// loads against the query's 1,024 weight bytes), then the whole cell row on
+// top of it with the early exit.  Survivor i of (order_in, pos_in) that still
+// is not pruned goes to (order_out, pos_out).  One thread per survivor.
+__global__ void __launch_bounds__(IB_T, LA_IB_MINB) index_bound2_kernel(
+    const unsigned short* __restrict__ cells, int P, const unsigned char* __restrict__ fine,
+    const long long* __restrict__ count_in, const int64_t* __restrict__ order_in, const int64_t* __restrict__ pos_in,
+    const unsigned short* __restrict__ table, const unsigned* __restrict__ qw2, int Q,
+    const unsigned* __restrict__ thr, float threshold, float lb_slack, int64_t* __restrict__ order_out,
+    int64_t* __restrict__ pos_out, unsigned long long* __restrict__ count_out) {
+  __shared__ unsigned short tab[IDX_TAB];
+  __shared__ __align__(16) unsigned qwt[CD2_CELLS / 4];
+  for (int i = threadIdx.x; i < IDX_TAB / 2; i += IB_T)
+    reinterpret_cast<unsigned*>(tab)[i] = reinterpret_cast<const unsigned*>(table)[i];
+  const int nql = (int)qw2[0];
+  for (int i = threadIdx.x; i < CD2_CELLS / 4; i += IB_T) qwt[i] = i < nql ? qw2[1 + i] : 0u;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const float t = fmaxf(__uint_as_float(*thr), threshold);
+  const float scale = 1.f / (LB_CELL_ONE * (float)P);
+  const float cscale = 1.f / (CD_ONE * (float)Q);
+  const uint32_t tab_s = smem_u32(tab);
+  auto look = [&](unsigned c) -> unsigned { return lds_u16i(tab_s + 2u * c); };
+  const int Pp = idx_row(P);
+  const int W = Pp / 16;
+  const long long n = *count_in;
+  const long long nth = (long long)gridDim.x * IB_T;
+  for (long long i0 = (long long)blockIdx.x * IB_T + (threadIdx.x & ~31); i0 < n; i0 += nth) {
+    const long long i = i0 + lane;
+    const bool live = i < n;
+    const long long rec = live ? order_in[i] : 0;
+    unsigned cs = 0u;
+    if (live) {
+      const unsigned char* drow = fine + (size_t)rec * CD2_CELLS;
+#pragma unroll 4
+      for (int k = 0; k < CD2_CELLS / 32; ++k) {
+        uint4 v, u;
+        asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w), "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                     : "l"(drow + 32 * k));
+        const uint4 wa = reinterpret_cast<const uint4*>(qwt)[2 * k], wb = reinterpret_cast<const uint4*>(qwt)[2 * k + 1];
+        cs = __dp4a(v.x, wa.x, cs); cs = __dp4a(v.y, wa.y, cs); cs = __dp4a(v.z, wa.z, cs); cs = __dp4a(v.w, wa.w, cs);
+        cs = __dp4a(u.x, wb.x, cs); cs = __dp4a(u.y, wb.y, cs); cs = __dp4a(u.z, wb.z, cs); cs = __dp4a(u.w, wb.w, cs);
+      }
+    }
+    const float col = (float)cs * cscale;
+    unsigned s0 = 0u, s1 = 0u;
+    if (live && !(fmaf(col, 1.f - 1e-4f, -lb_slack) > t)) {
+      const uint4* row = reinterpret_cast<const uint4*>(cells + (size_t)rec * Pp);
+#pragma unroll 2
+      for (int k = 0; k < W; ++k) {
+        uint4 v, u;
+        asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w), "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                     : "l"(row + 2 * k));
+        s0 += look(v.x & 0xffffu) + look(v.y & 0xffffu) + look(v.z & 0xffffu) + look(v.w & 0xffffu);
+        s1 += look(v.x >> 16) + look(v.y >> 16) + look(v.z >> 16) + look(v.w >> 16);
+        s0 += look(u.x & 0xffffu) + look(u.y & 0xffffu) + look(u.z & 0xffffu) + look(u.w & 0xffffu);
+        s1 += look(u.x >> 16) + look(u.y >> 16) + look(u.z >> 16) + look(u.w >> 16);
+        if (fmaf(fmaf((float)(s0 + s1), scale, col), 1.f - 1e-4f, -lb_slack) > t) break;
+      }
+    }
+    const bool keep = live && !(fmaf(fmaf((float)(s0 + s1), scale, col), 1.f - 1e-4f, -lb_slack) > t);
+    const unsigned mask = __ballot_sync(FULL, keep);
+    if (mask) {
+      unsigned long long base = 0ull;
+      if (lane == 0) base = atomicAdd(count_out, (unsigned long long)__popc(mask));
+      base = __shfl_sync(FULL, base, 0);
+      if (keep) {
+        const long long at = (long long)base + __popc(mask & ((1u << lane) - 1u));
+        order_out[at] = rec;
+        pos_out[at] = pos_in[i];
+      }
+    }
+  }
 }
 
 __global__ void index_count_kernel(const long long* __restrict__ count, int64_t* __restrict__ n_stage) {
@@ -2586,6 +2672,8 @@ Plan make_plan(const la_chamfer_args* a) {
       // cell table, the survivors' records and reported positions, their count
       p.ws_index = align_up((size_t)IDX_TAB * sizeof(unsigned short)) +
                    2 * align_up((size_t)npos * sizeof(long long)) + 256 + align_up((CD_CELLS + 1) * sizeof(unsigned));
+      if (a->coarse && a->fine)
+        p.ws_index += 2 * align_up((size_t)npos * sizeof(long long)) + align_up((CD2_CELLS / 4 + 1) * sizeof(unsigned));
     }
     p.mq = a->NQ >= 2 && !(a->flags & LA_CH_NO_MQ) && (a->P % 2) == 0;
     if (p.mq) {
@@ -2657,16 +2745,21 @@ size_t la_chamfer_workspace(const la_chamfer_args* a) {
   return align_up(p.ws_lists) + align_up(p.ws_dense) + align_up(p.ws_prune) + align_up(p.ws_index) + 1024;
 }
 
-int la_chamfer_index(const float* db, int64_t N, int32_t P, uint16_t* cells, uint8_t* coarse, void* stream) {
+int la_chamfer_index(const float* db, int64_t N, int32_t P, uint16_t* cells, uint8_t* coarse, uint8_t* fine,
+                     void* stream) {
   if (N < 0 || P < 1 || !db || !cells) return fail(LA_EINVAL, "la_chamfer_index: bad args");
   if (N == 0) return 0;
-  if (coarse) {
+  if (coarse || fine) {
     int sm = sm_count();
     if (sm <= 0) sm = 148;
     long long gc = (N + 7) / 8;
     if (gc > (long long)sm * 8) gc = (long long)sm * 8;
-    index_coarse_kernel<<<(unsigned)gc, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const float2*>(db), N, P, coarse);
+    if (coarse)
+      index_coarse_kernel<CDG><<<(unsigned)gc, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+          reinterpret_cast<const float2*>(db), N, P, coarse);
+    if (fine)
+      index_coarse_kernel<CD2G><<<(unsigned)gc, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+          reinterpret_cast<const float2*>(db), N, P, fine);
   }
   const long long n = (long long)N * idx_row(P);
   int sms = sm_count();
@@ -2793,22 +2886,37 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
         unsigned* qlist = reinterpret_cast<unsigned*>(iw); iw += align_up((CD_CELLS + 1) * sizeof(unsigned));
         int sms = sm_count();
         if (sms <= 0) sms = 148;
-        cudaMemsetAsync(cnt, 0, sizeof(long long), s);
+        cudaMemsetAsync(cnt, 0, 2 * sizeof(long long), s);
         index_table_kernel<<<dim3((IDX_TAB + 255) / 256, 1), 256, 0, s>>>(a->queries, a->Q, table);
-        if (a->coarse) index_qlist_kernel<<<1, 256, 0, s>>>(a->queries, a->Q, qlist);
+        if (a->coarse) index_qlist_kernel<CDG><<<1, 256, 0, s>>>(a->queries, a->Q, qlist);
         long long bg = (npos + IB_T - 1) / IB_T;
         if (bg > (long long)sms * (2048 / IB_T)) bg = (long long)sms * (2048 / IB_T);
         index_bound_kernel<<<(unsigned)bg, IB_T, 0, s>>>(a->cells, a->P, a->order, a->pos_map, a->pos_begin,
                                                          a->pos_base, npos, table, thr, a->threshold, c.lb_slack,
                                                          order2, pmap2, reinterpret_cast<unsigned long long*>(cnt),
                                                          a->coarse, qlist, a->Q);
+        if (a->n_stage) index_count_kernel<<<1, 1, 0, s>>>(cnt, a->n_stage);
+        if (a->coarse && a->fine) {
+          // second level over the survivors: the 32 x 32 tables
+          int64_t* order3 = reinterpret_cast<int64_t*>(iw); iw += align_up((size_t)npos * sizeof(long long));
+          int64_t* pmap3 = reinterpret_cast<int64_t*>(iw); iw += align_up((size_t)npos * sizeof(long long));
+          unsigned* qw2 = reinterpret_cast<unsigned*>(iw); iw += align_up((CD2_CELLS / 4 + 1) * sizeof(unsigned));
+          long long* cnt2 = cnt + 1;
+          index_qlist_kernel<CD2G><<<1, 256, 0, s>>>(a->queries, a->Q, qw2);
+          index_bound2_kernel<<<(unsigned)((long long)sms * (2048 / IB_T)), IB_T, 0, s>>>(
+              a->cells, a->P, a->fine, cnt, order2, pmap2, table, qw2, a->Q, thr, a->threshold, c.lb_slack, order3,
+              pmap3, reinterpret_cast<unsigned long long*>(cnt2));
+          if (a->n_stage) index_count_kernel<<<1, 1, 0, s>>>(cnt2, a->n_stage + 1);
+          order2 = order3;
+          pmap2 = pmap3;
+          cnt = cnt2;
+        }
         c.a.order = order2;
         c.a.pos_map = pmap2;
         c.a.pos_begin = 0;
         c.a.pos_end = npos;
         c.pos_count = cnt;
         c.prune = 1;
-        if (a->n_stage) index_count_kernel<<<1, 1, 0, s>>>(cnt, a->n_stage);
       } else {
         // optional seed: plain scan of a prefix, merged; its k-th best starts thr
         float* seed_kth = nullptr;

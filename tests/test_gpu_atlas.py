@@ -423,8 +423,11 @@ def test_indexed_scan_equals_full_scan(torch, case):
         full = chamfer_scan(db, qq, prune=False, **kw)
         idx = chamfer_scan(db, qq, cells=cells, **kw)
         _lists_equal(torch, full, idx)
-        surv = int(idx["n_stage"][0].item())
-        assert 0 < surv < N, surv  # the bound step ran and pruned
+        surv, surv2 = int(idx["n_stage"][0].item()), int(idx["n_stage"][1].item())
+        assert 0 < surv2 <= surv < N, (surv, surv2)  # both levels of the bound step ran and pruned
+        # the index's parts on their own: cells only, cells + 16 x 16 tables
+        for part in (cells.cells, cells._replace(fine=None)):
+            _lists_equal(torch, full, chamfer_scan(db, qq, cells=part, **kw))
     if case == "c4":
         assert np.array_equal(chamfer_scan(db, q[:1], cells=cells, k=10)["top_id"][0].cpu().numpy(),
                               np.lexsort((np.arange(N), dense))[:10])
