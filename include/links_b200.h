@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define LA_ABI_VERSION 3
+#define LA_ABI_VERSION 4
 #define LA_MAX_JOINTS 20   /* joints per mechanism (generator.py n_max default) */
 #define LA_MAX_STEPS 18    /* dyad steps per plan: n - |fixed| - 1 <= 18       */
 #define LA_MAX_TOPK 32

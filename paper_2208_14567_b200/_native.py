@@ -35,7 +35,7 @@ LA_CH_MQ_FINE = 128
 LA_CH_NO_INDEX = 256
 LA_CH_INDEX_MQ = 512
 LA_PENDING = -3
-ABI_VERSION = 3
+ABI_VERSION = 4
 LA_EINVAL = -1
 LA_ERANGE = -2
 LA_EWS = -3
@@ -303,8 +303,16 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         if build_if_missing:
             from paper_2208_14567_b200 import build_lib
 
-            if not LIB_PATH.exists():
-                build_lib.build()
+            # missing, or older than its sources (a stale library with another
+            # struct layout must not be called): rebuild; if nvcc is not there
+            # an existing library is still tried -- the ABI version check
+            # below refuses one of another interface version
+            if build_lib.needs_build():
+                try:
+                    build_lib.build()
+                except Exception:
+                    if not LIB_PATH.exists():
+                        raise
         if not LIB_PATH.exists():
             raise NativeError(f"CUDA library missing: {LIB_PATH} (run python -m paper_2208_14567_b200.build_lib)")
         lib = C.CDLL(str(LIB_PATH))

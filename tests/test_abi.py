@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_text_without_gpu():
     lib = N.load()
-    assert lib.la_abi_version() == 3
+    assert lib.la_abi_version() == 4
     assert isinstance(lib.la_last_error(), bytes)
     # argument validation happens before any CUDA call
     rc = lib.la_simulate(None, None)
