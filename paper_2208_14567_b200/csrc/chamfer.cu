@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(256) index_kernel(const float2* __restrict__ d
 constexpr int CDG = 16;                  // coarse cells per axis
 constexpr int CD_CELLS = CDG * CDG;      // bytes per curve
 constexpr float CD_ONE = 160.f;          // fixed point: units of 1 / 160 (255 = 1.59)
+constexpr float kFrontFrac = 0.85f;      // second level: survivors with bound <= 0.85 t are scanned first
 constexpr int CD2G = 32;                 // second level: 32 x 32 cells, 1 KB per curve
 constexpr int CD2_CELLS = CD2G * CD2G;
 
@@ -979,7 +980,7 @@ __global__ void __launch_bounds__(IB_T, LA_IB_MINB) index_bound2_kernel(
     const long long* __restrict__ count_in, const int64_t* __restrict__ order_in, const int64_t* __restrict__ pos_in,
     const unsigned short* __restrict__ table, const unsigned* __restrict__ qw2, int Q,
     const unsigned* __restrict__ thr, float threshold, float lb_slack, int64_t* __restrict__ order_out,
-    int64_t* __restrict__ pos_out, unsigned long long* __restrict__ count_out) {
+    int64_t* __restrict__ pos_out, unsigned long long* __restrict__ count_out, long long cap) {
   __shared__ unsigned short tab[IDX_TAB];
   __shared__ __align__(16) unsigned qwt[CD2_CELLS / 4];
   for (int i = threadIdx.x; i < IDX_TAB / 2; i += IB_T)
@@ -1032,20 +1033,55 @@ __global__ void __launch_bounds__(IB_T, LA_IB_MINB) index_bound2_kernel(
         if (fmaf(fmaf((float)(s0 + s1), scale, col), 1.f - 1e-4f, -lb_slack) > t) break;
       }
     }
-    const bool keep = live && !(fmaf(fmaf((float)(s0 + s1), scale, col), 1.f - 1e-4f, -lb_slack) > t);
-    const unsigned mask = __ballot_sync(FULL, keep);
-    if (mask) {
-      unsigned long long base = 0ull;
-      if (lane == 0) base = atomicAdd(count_out, (unsigned long long)__popc(mask));
-      base = __shfl_sync(FULL, base, 0);
+    const float bnd = fmaf(fmaf((float)(s0 + s1), scale, col), 1.f - 1e-4f, -lb_slack);
+    const bool keep = live && !(bnd > t);
+    // survivors whose bound is well below the threshold (the final top k is
+    // among them unless the seed's bound was far off) fill the list from the
+    // front, the others from the back (count_out[1]); index_close_kernel then
+    // joins the two parts, so the scan meets the promising curves first and
+    // its running k-th best falls early.  Order only: every survivor is kept.
+    const bool front = keep && bnd <= kFrontFrac * t;
+    const unsigned mf = __ballot_sync(FULL, front), mb = __ballot_sync(FULL, keep && !front);
+    if (mf | mb) {
+      unsigned long long bf = 0ull, bb = 0ull;
+      if (lane == 0) {
+        if (mf) bf = atomicAdd(count_out, (unsigned long long)__popc(mf));
+        if (mb) bb = atomicAdd(count_out + 1, (unsigned long long)__popc(mb));
+      }
+      bf = __shfl_sync(FULL, bf, 0);
+      bb = __shfl_sync(FULL, bb, 0);
       if (keep) {
-        const long long at = (long long)base + __popc(mask & ((1u << lane) - 1u));
+        const unsigned below = (1u << lane) - 1u;
+        const long long at = front ? (long long)bf + __popc(mf & below) : cap - 1 - ((long long)bb + __popc(mb & below));
         order_out[at] = rec;
         pos_out[at] = pos_in[i];
       }
     }
   }
 }
+
+// joins the back part of index_bound2_kernel's list to its front part:
+// entries cap-1-j (j < count[1]) move to count[0] + j; count[0] becomes the
+// total.  A grid-wide pass reading the old counts, then one thread updating
+// them, are two launches (index_close_kernel, index_close_count_kernel).
+__global__ void index_close_kernel(int64_t* __restrict__ order, int64_t* __restrict__ pos,
+                                   const unsigned long long* __restrict__ count, long long cap) {
+  const long long c0 = (long long)count[0], c1 = (long long)count[1];
+  // back entries already inside the joined range [c0, c0 + c1) stay where
+  // they are; the others (sources >= c0 + c1, never a target) fill the
+  // slots [c0, cap - c1) the stayers leave free
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < c1; j += (long long)gridDim.x * blockDim.x) {
+    const long long src = cap - 1 - j, dst = c0 + j;
+    if (src >= c0 + c1) {  // sources inside [c0, c0 + c1) are already in the joined range
+      order[dst] = order[src];
+      pos[dst] = pos[src];
+    }
+  }
+}
+__global__ void index_close_count_kernel(unsigned long long* __restrict__ count) {
+  count[0] += count[1];
+}
+
 
 __global__ void index_count_kernel(const long long* __restrict__ count, int64_t* __restrict__ n_stage) {
   n_stage[0] += *count;  // curves surviving the bound step
@@ -1303,9 +1339,13 @@ __global__ void __launch_bounds__(CT, LA_CH_MINB) chamfer_scan_kernel(const Scan
       const float t = fmaxf(thr_c, A.threshold);
       thr_c = __uint_as_float(__ldcg(thr_q));  // for the next curve (measured: two in flight was slower)
       const uint32_t cur_s = use_tma ? raw_s + (uint32_t)(PMAX * 8 * bi) : raw_s;  // = cur
-      const float lb1 = curve_row_bound_cell(cur_s, P, lbc_s, lb_lx, lb_ly, lb_ihx, lb_ihy, lane,
-                                             (t + lb_slack) * (1.f + 2e-4f));
-      if (fmaf(lb1, 1.f - 1e-4f, -lb_slack) > t) continue;
+      // (a survivor list of the index's bound step already passed this
+      // stage's bound, against a looser threshold; it rarely prunes there)
+      if (!c.pos_count) {
+        const float lb1 = curve_row_bound_cell(cur_s, P, lbc_s, lb_lx, lb_ly, lb_ihx, lb_ihy, lane,
+                                               (t + lb_slack) * (1.f + 2e-4f));
+        if (fmaf(lb1, 1.f - 1e-4f, -lb_slack) > t) continue;
+      }
       const float lb4 = curve_row_bound(cur, P, lb_dt, lb_lx, lb_ly, lb_ihx, lb_ihy, lb_cx, lb_cy, lane);
       if (fmaf(lb4, 1.f - 1e-4f, -lb_slack) > t) continue;
       // column term from 10-point runs (a 40-point pre-stage measured slower)
@@ -2886,7 +2926,7 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
         unsigned* qlist = reinterpret_cast<unsigned*>(iw); iw += align_up((CD_CELLS + 1) * sizeof(unsigned));
         int sms = sm_count();
         if (sms <= 0) sms = 148;
-        cudaMemsetAsync(cnt, 0, 2 * sizeof(long long), s);
+        cudaMemsetAsync(cnt, 0, 3 * sizeof(long long), s);
         index_table_kernel<<<dim3((IDX_TAB + 255) / 256, 1), 256, 0, s>>>(a->queries, a->Q, table);
         if (a->coarse) index_qlist_kernel<CDG><<<1, 256, 0, s>>>(a->queries, a->Q, qlist);
         long long bg = (npos + IB_T - 1) / IB_T;
@@ -2905,7 +2945,9 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
           index_qlist_kernel<CD2G><<<1, 256, 0, s>>>(a->queries, a->Q, qw2);
           index_bound2_kernel<<<(unsigned)((long long)sms * (2048 / IB_T)), IB_T, 0, s>>>(
               a->cells, a->P, a->fine, cnt, order2, pmap2, table, qw2, a->Q, thr, a->threshold, c.lb_slack, order3,
-              pmap3, reinterpret_cast<unsigned long long*>(cnt2));
+              pmap3, reinterpret_cast<unsigned long long*>(cnt2), npos);
+          index_close_kernel<<<sms * 2, 256, 0, s>>>(order3, pmap3, reinterpret_cast<unsigned long long*>(cnt2), npos);
+          index_close_count_kernel<<<1, 1, 0, s>>>(reinterpret_cast<unsigned long long*>(cnt2));
           if (a->n_stage) index_count_kernel<<<1, 1, 0, s>>>(cnt2, a->n_stage + 1);
           order2 = order3;
           pmap2 = pmap3;
