@@ -233,9 +233,11 @@ int la_circle_stats(const void* paths, int32_t in_f64, int64_t M, int32_t P,
 #define LA_CH_INDEX_MQ 512u  /* use la_chamfer_args.cells for NQ >= 2 too:
                                 multi-query seed, bound step for every
                                 (query, curve), per-query survivor scans.
-                                Off by default: measured slower than the
-                                multi-query kernel (the cell-row bound alone
-                                keeps 40-90 % of the curves for most queries) */
+                                Off by default: against the multi-query
+                                kernel it wins for few queries on a large
+                                database (10M x 4: 16.6 vs 23.3 ms) and
+                                loses for many on a small one (616k x 64:
+                                40.6 vs 17.0 ms)                             */
 #define LA_CH_MQ_FINE 128u   /* multi-query kernel: 64x64 common grid for the
                                 stage-0 bound instead of 32x32               */
 

@@ -61,9 +61,10 @@ def chamfer_scan(db, queries, *, k: int = 10, threshold: float = 0.0, order=None
     cells, the column term from its coarse distance bytes -- against the k-th
     best of a seed scan over a 1/64 prefix, and only the survivors' points
     are streamed; the lists are identical to the scan without it
-    (``n_stage[0]`` counts the survivors).  ``index_mq`` uses the cells (row
-    term only) for several queries too (measured slower than the multi-query
-    kernel; off).
+    (``n_stage[0]`` / ``[1]`` count the survivors of its two levels).
+    ``index_mq`` uses the index for several queries too (a multi-query bound
+    step, per-query survivor scans: faster than the multi-query kernel for
+    few queries on a large database, slower for many on a small one; off).
 
     ``prune`` (top-k scans of >= 65,536 positions without dense output):
     curves whose lower bound (query distance grid, first chamfer term)

@@ -729,7 +729,8 @@ __global__ void __launch_bounds__(256) index_qlist_kernel(const float* __restric
   __shared__ unsigned hist[G * G];
   for (int c = threadIdx.x; c < G * G; c += 256) hist[c] = 0u;
   __syncthreads();
-  const float2* q = reinterpret_cast<const float2*>(query);
+  const float2* q = reinterpret_cast<const float2*>(query) + (size_t)blockIdx.x * Q;  // one CTA per query
+  qw += (size_t)blockIdx.x * (G * G / 4 + 1);
   for (int j = threadIdx.x; j < Q; j += 256) atomicAdd(&hist[cd_cell<G>(q[j])], 1u);
   __syncthreads();
   for (int w = threadIdx.x; w < G * G / 4; w += 256) {
@@ -888,8 +889,9 @@ __global__ void __launch_bounds__(IB_T, LA_IB_MINB) index_bound_kernel(const uns
 // its own survivor list (order2 / pos_map2 + q * cap, count[q]).
 constexpr int IBM_QG = 16;
 constexpr int IBM_T = 512;
-constexpr int IBM_ROW = 512;  // staging bytes per curve (P <= 256)
-constexpr size_t IBM_SMEM = (size_t)IDX_TAB * IBM_QG * 2 + (size_t)(IBM_T / 32) * 2 * IBM_ROW;
+constexpr int IBM_ROW = 512 + CD_CELLS;  // staging bytes per curve: cells (P <= 256), coarse distance bytes
+constexpr int IBM_WQ = (CD_CELLS / 4) * IBM_QG * 4;  // the group's weight words, interleaved like the tables
+constexpr size_t IBM_SMEM = (size_t)IDX_TAB * IBM_QG * 2 + IBM_WQ + (size_t)(IBM_T / 32) * 2 * IBM_ROW;
 __global__ void __launch_bounds__(IBM_T, 1) index_bound_mq_kernel(const unsigned short* __restrict__ cells, int P,
                                                                   const int64_t* __restrict__ order,
                                                                   const int64_t* __restrict__ pos_map,
@@ -900,15 +902,25 @@ __global__ void __launch_bounds__(IBM_T, 1) index_bound_mq_kernel(const unsigned
                                                                   float lb_slack, long long cap,
                                                                   int64_t* __restrict__ order2,
                                                                   int64_t* __restrict__ pos_map2,
-                                                                  unsigned long long* __restrict__ count) {
+                                                                  unsigned long long* __restrict__ count,
+                                                                  const unsigned char* __restrict__ coarse,
+                                                                  const unsigned* __restrict__ qw, int Q) {
   extern __shared__ __align__(16) unsigned char ibm_smem[];
   unsigned short* tab = reinterpret_cast<unsigned short*>(ibm_smem);
+  unsigned* wq = reinterpret_cast<unsigned*>(ibm_smem + (size_t)IDX_TAB * IBM_QG * 2);
   const int q0 = blockIdx.y * IBM_QG;
   for (int i = threadIdx.x; i < IDX_TAB * IBM_QG; i += IBM_T) {
     const int cell = i / IBM_QG, ql = i % IBM_QG;
     tab[i] = q0 + ql < NQ ? tables[(size_t)(q0 + ql) * IDX_TAB + cell] : (unsigned short)0;
   }
+  // weight word w of query ql at wq[w * IBM_QG + ql] (zero: no column term)
+  for (int i = threadIdx.x; i < (CD_CELLS / 4) * IBM_QG; i += IBM_T) {
+    const int w = i / IBM_QG, ql = i % IBM_QG;
+    const unsigned* src = qw + (size_t)(q0 + ql) * (CD_CELLS / 4 + 1);
+    wq[i] = (coarse && q0 + ql < NQ && src[0]) ? src[1 + w] : 0u;
+  }
   __syncthreads();
+  const float cscale = 1.f / (CD_ONE * (float)Q);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int h = lane >> 4, ql = lane & 15;
   const int q = q0 + ql;
@@ -917,7 +929,7 @@ __global__ void __launch_bounds__(IBM_T, 1) index_bound_mq_kernel(const unsigned
   const float scale = 1.f / (LB_CELL_ONE * (float)P);
   const int Pp = idx_row(P);
   const int W = Pp / 16;  // sectors per curve (<= 16)
-  unsigned char* stage = ibm_smem + (size_t)IDX_TAB * IBM_QG * 2 + ((size_t)w * 2 + h) * IBM_ROW;
+  unsigned char* stage = ibm_smem + (size_t)IDX_TAB * IBM_QG * 2 + IBM_WQ + ((size_t)w * 2 + h) * IBM_ROW;
   const uint32_t stage_s = smem_u32(stage);
   const uint32_t lane_tab = smem_u32(tab) + 2u * (uint32_t)ql;
   auto look = [&](unsigned c) -> unsigned { return lds_u16i(lane_tab + c * (2u * IBM_QG)); };
@@ -935,9 +947,35 @@ __global__ void __launch_bounds__(IBM_T, 1) index_bound_mq_kernel(const unsigned
       reinterpret_cast<uint4*>(stage)[2 * ql] = v;
       reinterpret_cast<uint4*>(stage)[2 * ql + 1] = u;
     }
+    if (live && coarse && ql < CD_CELLS / 32) {  // the curve's 256 coarse distance bytes
+      uint4 v, u;
+      asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w), "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                   : "l"(coarse + (size_t)rec * CD_CELLS + 32 * ql));
+      reinterpret_cast<uint4*>(stage + 512)[2 * ql] = v;
+      reinterpret_cast<uint4*>(stage + 512)[2 * ql + 1] = u;
+    }
     __syncwarp();
     unsigned s0 = 0u, s1 = 0u;
-    bool alive = live && qlive;
+    // column term: the curve's bytes (a broadcast) against this lane's query's weights
+    float col = 0.f;
+    if (live && qlive && coarse) {
+      unsigned cs = 0u;
+#pragma unroll 4
+      for (int k = 0; k < CD_CELLS / 16; ++k) {
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(stage_s + 512u + 16u * (uint32_t)k));
+        const unsigned* wk = wq + (4 * k) * IBM_QG + ql;
+        cs = __dp4a(v.x, wk[0], cs);
+        cs = __dp4a(v.y, wk[IBM_QG], cs);
+        cs = __dp4a(v.z, wk[2 * IBM_QG], cs);
+        cs = __dp4a(v.w, wk[3 * IBM_QG], cs);
+      }
+      col = (float)cs * cscale;
+    }
+    bool alive = live && qlive && !(fmaf(col, 1.f - 1e-4f, -lb_slack) > t);
 #pragma unroll 1
     for (int k = 0; k < W; ++k) {
       if (alive) {
@@ -951,7 +989,7 @@ __global__ void __launch_bounds__(IBM_T, 1) index_bound_mq_kernel(const unsigned
           s1 += look(v.x >> 16) + look(v.y >> 16) + look(v.z >> 16) + look(v.w >> 16);
         }
         // the terms are >= 0: once a partial sum prunes, so does the total
-        if (fmaf((float)(s0 + s1) * scale, 1.f - 1e-4f, -lb_slack) > t) alive = false;
+        if (fmaf(fmaf((float)(s0 + s1), scale, col), 1.f - 1e-4f, -lb_slack) > t) alive = false;
       }
       if (!__any_sync(FULL, alive)) break;
     }
@@ -2753,7 +2791,8 @@ Plan make_plan(const la_chamfer_args* a) {
         if (gq > p.nwarps) gq = p.nwarps;
         p.iq_grid = (int)gq;
         p.ws_index = align_up((size_t)a->NQ * IDX_TAB * sizeof(unsigned short)) +
-                     2 * align_up((size_t)a->NQ * npos * sizeof(long long)) + align_up((size_t)a->NQ * 8) + 256;
+                     2 * align_up((size_t)a->NQ * npos * sizeof(long long)) + align_up((size_t)a->NQ * 8) + 256 +
+                     align_up((size_t)a->NQ * (CD_CELLS / 4 + 1) * sizeof(unsigned));
       }
     }
   }
@@ -3037,9 +3076,11 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
           const int ngroups = (a->NQ + IBM_QG - 1) / IBM_QG;
           long long bx = ((npos + 1) / 2 + IBM_T / 32 - 1) / (IBM_T / 32);
           if (bx > sms) bx = sms;
+          unsigned* qwm = reinterpret_cast<unsigned*>(reinterpret_cast<unsigned char*>(cnt) + align_up((size_t)a->NQ * 8));
+          if (a->coarse) index_qlist_kernel<CDG><<<a->NQ, 256, 0, s>>>(a->queries, a->Q, qwm);
           index_bound_mq_kernel<<<dim3((unsigned)bx, ngroups), IBM_T, IBM_SMEM, s>>>(
               a->cells, a->P, a->order, a->pos_map, a->pos_begin, a->pos_base, npos, a->NQ, tables, thr, a->threshold,
-              c.lb_slack, npos, order2, pmap2, reinterpret_cast<unsigned long long*>(cnt));
+              c.lb_slack, npos, order2, pmap2, reinterpret_cast<unsigned long long*>(cnt), a->coarse, qwm, a->Q);
           if (a->n_stage) index_count_mq_kernel<<<1, 1, 0, s>>>(cnt, a->NQ, a->n_stage);
           ScanCtx c2 = c;
           c2.a.order = order2;
