@@ -2947,15 +2947,6 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
         // every position again)
         const long long npos = a->pos_end - a->pos_begin;
         thr_init_kernel<<<1, 32, 0, s>>>(nullptr, a->k, a->NQ, thr, slots);
-        ScanCtx sc = c;
-        sc.prune = 1;
-        sc.a.pos_end = p.seed_end;
-        sc.a.n_hits = nullptr;
-        sc.a.n_full = nullptr;
-        sc.nwarps_total = p.seed_grid;
-        if (int e = scan(sc, dim3(p.seed_grid, 1))) return e;
-        // bound step against that bound; survivors appended to (order2,
-        // pos_map2), counted on the device; then the pruned scan over them
         unsigned char* iw = static_cast<unsigned char*>(a->ws) + align_up(p.ws_lists) + align_up(p.ws_dense) +
                             align_up(p.ws_prune);
         unsigned short* table = reinterpret_cast<unsigned short*>(iw); iw += align_up((size_t)IDX_TAB * 2);
@@ -2965,9 +2956,43 @@ int la_chamfer_topk(const la_chamfer_args* a, void* stream) {
         unsigned* qlist = reinterpret_cast<unsigned*>(iw); iw += align_up((CD_CELLS + 1) * sizeof(unsigned));
         int sms = sm_count();
         if (sms <= 0) sms = 148;
-        cudaMemsetAsync(cnt, 0, 3 * sizeof(long long), s);
         index_table_kernel<<<dim3((IDX_TAB + 255) / 256, 1), 256, 0, s>>>(a->queries, a->Q, table);
         if (a->coarse) index_qlist_kernel<CDG><<<1, 256, 0, s>>>(a->queries, a->Q, qlist);
+        // The seed prefix (1/64 of the positions) is itself scanned through
+        // the bound step when it is long enough: a plain pruned scan of its
+        // first 1/16 gives a first bound, the bound step over the prefix
+        // lists the curves that bound leaves, and their scan leaves the
+        // seed's running bound -- the same bound the plain scan of the whole
+        // prefix would reach (its k-th best comes from the same curves), for
+        // a fraction of the point streaming.
+        const long long sn = p.seed_end - a->pos_begin;
+        const long long sn0 = sn >= 65536 ? sn / 16 : sn;
+        ScanCtx sc = c;
+        sc.prune = 1;
+        sc.a.pos_end = a->pos_begin + sn0;
+        sc.a.n_hits = nullptr;
+        sc.a.n_full = nullptr;
+        sc.nwarps_total = p.seed_grid;
+        if (int e = scan(sc, dim3(p.seed_grid, 1))) return e;
+        if (sn0 < sn) {
+          cudaMemsetAsync(cnt, 0, sizeof(long long), s);
+          long long bs = (sn + IB_T - 1) / IB_T;
+          if (bs > (long long)sms * (2048 / IB_T)) bs = (long long)sms * (2048 / IB_T);
+          index_bound_kernel<<<(unsigned)bs, IB_T, 0, s>>>(a->cells, a->P, a->order, a->pos_map, a->pos_begin,
+                                                           a->pos_base, sn, table, thr, a->threshold, c.lb_slack,
+                                                           order2, pmap2, reinterpret_cast<unsigned long long*>(cnt),
+                                                           a->coarse, qlist, a->Q);
+          ScanCtx sb = sc;
+          sb.a.order = order2;
+          sb.a.pos_map = pmap2;
+          sb.a.pos_begin = 0;
+          sb.a.pos_end = sn;
+          sb.pos_count = cnt;
+          if (int e = scan(sb, dim3(p.seed_grid, 1))) return e;
+        }
+        // bound step against the seed's bound; survivors appended to (order2,
+        // pos_map2), counted on the device; then the pruned scan over them
+        cudaMemsetAsync(cnt, 0, 3 * sizeof(long long), s);
         long long bg = (npos + IB_T - 1) / IB_T;
         if (bg > (long long)sms * (2048 / IB_T)) bg = (long long)sms * (2048 / IB_T);
         index_bound_kernel<<<(unsigned)bg, IB_T, 0, s>>>(a->cells, a->P, a->order, a->pos_map, a->pos_begin,
