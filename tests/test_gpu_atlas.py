@@ -450,6 +450,18 @@ def test_indexed_scan_equals_full_scan(torch, case):
         want = np.minimum(np.floor(dd * 160), 255).transpose(2, 0, 1).reshape(50, 256)
         gotc = cells.coarse[:50].cpu().numpy().astype(np.int64)
         assert (np.abs(gotc - want) <= 1).all() and (gotc <= want).mean() > 0.99
+        # the 32 x 32 tables the same way
+        g0 = -1 / 32 + np.arange(32) * (17 / 512)
+        ex = np.maximum(np.maximum(g0[:, None, None] - a[None, :, :, 0], a[None, :, :, 0] - (g0 + 17 / 512)[:, None, None]), 0)
+        ey = np.maximum(np.maximum(g0[:, None, None] - a[None, :, :, 1], a[None, :, :, 1] - (g0 + 17 / 512)[:, None, None]), 0)
+        ex[0] = np.maximum(a[..., 0] - (g0[0] + 17 / 512), 0)
+        ex[31] = np.maximum(g0[31] - a[..., 0], 0)
+        ey[0] = np.maximum(a[..., 1] - (g0[0] + 17 / 512), 0)
+        ey[31] = np.maximum(g0[31] - a[..., 1], 0)
+        dd = np.sqrt(ex[:, None] ** 2 + ey[None, :] ** 2).min(-1)
+        want = np.minimum(np.floor(dd * 160), 255).transpose(2, 0, 1).reshape(50, 1024)
+        gotf = cells.fine[:50].cpu().numpy().astype(np.int64)
+        assert (np.abs(gotf - want) <= 1).all() and (gotf <= want).mean() > 0.99
         assert (got == (cx * 66 + cy).astype(np.int64)).mean() > 0.999  # fp32 rounding at cell edges aside
 
 

@@ -18,8 +18,13 @@ ap.add_argument("--query", type=int, default=0)
 args = ap.parse_args()
 db = fourier_db(args.n, 200, seed=4000)
 q = fourier_db(args.query + 1, 200, seed=999)[args.query:args.query + 1]
-cells = chamfer_index(db)
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+cells = chamfer_index(db)
+e1.record()
+torch.cuda.synchronize()
+print(f"index build: {e0.elapsed_time(e1):.1f} ms for {args.n} curves", flush=True)
 for name, kw in (("plain", {}), ("indexed", {"cells": cells})):
     res = None
     for _ in range(0 if args.once else 2):
